@@ -1,0 +1,309 @@
+"""Benchmark of the sparse-inverse local-global hot path (arXiv 2503.15078).
+
+Workload (BASELINE.json configs[2]): gingerbread-class
+silhouette slab, 19 691 vertices (59.1k DoF) / 93 600 tets, Neo-Hookean
+E = 1e6, nu = 0.3, rho = 1000, h = 0.01, 800 contact points (3 rows each),
+5 L-G iterations and 10 CR iterations per frame, moving head handle.
+
+One step = one frame of Alg. 4: sim_set_contacts (rows + Delassus Gram +
+preconditioner on the device, as the paper's per-frame `Schur.`) + predict +
+5 x (local, RHS, K-pass 1, contacts + CR, correction, K-pass 2) + integrate.
+Metric: scene-iterations/s over all ranks (= 1000 / ms per L-G iteration per
+scene at N = 1).  Multi-GPU: one independent scene replica per rank (weak
+scaling); NCCL only gathers per-rank timings after the timed region.
+
+`--impl reference` runs the fp64 CPU oracle (oracle/) on the same workload:
+each step is one L-G iteration of cfg3 with the per-frame Delassus solve
+amortised over the frame's 5 iterations.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per local-global iteration @58.5k DoFs; batched scene-iters/s at 1/2/4/8 B200"
+UNIT = "scene-iters/s"
+ITERS = 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+def oracle_sample(n_steps, warmup=0):
+    """fp64 oracle on cfg3: per step one L-G iteration (+ 1/5 of the frame's
+    Delassus).  Returns (scene-iters/s, seconds per step list, sample text)."""
+    import scenes
+    from oracle import oracle as O
+    sc = scenes.make_scene("cfg3")
+    o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=1)
+    t0 = time.perf_counter()
+    o.set_contacts(sc.contacts)
+    t_sc = time.perf_counter() - t0
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+    times = []
+    for k in range(warmup + n_steps):
+        t0 = time.perf_counter()
+        x, v, _ = o.frame(x, v, pin_targets=x[o.pinned] + sc.h * sc.pin_velocity)
+        dt = time.perf_counter() - t0 + t_sc / ITERS
+        if k >= warmup:
+            times.append(dt)
+    per_iter = float(np.mean(times))
+    sample = (f"cfg3 (19691 v / 93600 t / 800 contacts), {n_steps} L-G iteration(s), each with "
+              f"1/{ITERS} of the per-frame Delassus solve ({t_sc:.2f} s); fp64 numpy/scipy SuperLU")
+    return 1.0 / per_iter, times, sample
+
+
+class Clocks:
+    """Sample nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for n, val in zip(names, r[2:6]):
+                    if val.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if ws > 1 and rank != 0:
+        return
+    value, times, sample = oracle_sample(args.steps, warmup=min(args.warmup, 1))
+    import torch
+    threads = 1
+    ms = 1000.0 * float(np.mean(times))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3 gingerbread-class slab, 800 contacts, NH E=1e6, 5 L-G / 10 CR",
+                   "global_batch": 1, "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                         "host_cpus": os.cpu_count(), "torch_threads": torch.get_num_threads()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import scenes
+    import paper_2503_15078_b200 as simlib
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)          # graph capture needs a non-default stream
+    torch.cuda.set_stream(stream)
+
+    sc = scenes.make_scene("cfg3")
+    rng = np.random.default_rng(1000 + rank)
+    v0 = 0.01 * rng.standard_normal(sc.mesh.X.shape) * (1 - sc.mesh.fixed[:, None])
+    s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+    s.set_stream(stream.cuda_stream)
+    s.set_pin_velocity(sc.pin_velocity)
+    packed = s.pack_contacts(sc.contacts)
+    s.set_contacts(sc.contacts)
+    s.set_state(sc.mesh.X, v0)
+    st0 = s.stats()
+
+    def step():
+        s.set_contacts(packed=packed)
+        s.step(1, ITERS)
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > L2
+
+    s.set_profiling(True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ktimes = {k: 0.0 for k in simlib.KERNEL_KINDS}
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                       # untimed L2 flush between timed steps
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            kt = s.kernel_times()                # synchronises; reads in-graph events
+            for k in ktimes:
+                ktimes[k] += kt[k]
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    if ws > 1:
+        dist.barrier()
+        t = torch.tensor([total_ms], device=dev)
+        allt = [torch.zeros_like(t) for _ in range(ws)]
+        dist.all_gather(allt, t)                 # NCCL: gather per-rank timings only
+        total_ms = max(float(a.item()) for a in allt)
+    ms_per_step = total_ms / args.steps
+    scenes_total = ws
+    value = scenes_total * args.steps * ITERS / (total_ms / 1000.0)
+
+    # ---- e2e through the public API with host buffers: contacts in, state out
+    s.set_profiling(False)
+    e2e_steps = max(3, args.steps // 2)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        step()
+        xh, vh = s.get_state()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    wall_e2e = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = scenes_total * e2e_steps * ITERS / (e2e_ms / 1000.0)
+    st = s.stats()
+    h2d = int(st["h2d_contact_bytes"])
+    d2h = 2 * 32 * sc.mesh.n_v
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = measured_peak()
+    nnz, nf = int(st0["nnz_K"]), int(st0["n_free"])
+    launches = args.steps * ITERS
+    bytes_k1 = 4 * nnz + 16 * nf + 16 * nf            # K (column-major) + u + y
+    bytes_k2 = 4 * nnz + 16 * nf + 2 * 32 * nf        # K (row-major) + y + x read/write
+    share = {k: v / max(1e-12, sum(ktimes.values())) for k, v in ktimes.items()}
+    dom = max(["kpass1", "kpass2"], key=lambda k: ktimes[k])
+    dom_bytes = bytes_k1 if dom == "kpass1" else bytes_k2
+    avg_s = ktimes[dom] / launches / 1000.0
+    achieved = dom_bytes / avg_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": dom, "peak_source": peak_kind,
+                "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": avg_s * 1e6,
+                "note": "K (fp32 values-only, 2 copies = %.1f MB) vs 126 MB L2: passes re-read from HBM"
+                        % (8 * nnz / 1e6)}
+    kernels_us = {k: 1000.0 * v / args.steps for k, v in ktimes.items()}
+
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        cv, _, sample = oracle_sample(1)
+        cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+               "host_cpus": os.cpu_count()}
+    clocks = clk.summary()
+    gpu_launches = st["kernels_per_frame"] * args.steps + 2 * args.steps   # + Delassus Gram + D_jj per step
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg3 gingerbread-class slab 19691 v / 93600 t, 800 contacts x 3 rows, "
+                               "NH E=1e6 nu=0.3, h=0.01, 5 L-G + 10 CR per frame, set_contacts every frame",
+                   "global_batch": ws, "scenes_per_gpu": 1, "parallelism": f"replicas{ws}",
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "ms_per_lg_iteration": ms_per_step / ITERS,
+        "paper_context_ms_per_iteration": 11.95,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms / e2e_steps, "wall_s": wall_e2e},
+        "gpu_launches": gpu_launches,
+        "kernel_us_per_step": kernels_us,
+        "kernel_share": share,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+        "nnz_K": nnz, "n_free": nf, "etree_height": int(st0["etree_height"]),
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

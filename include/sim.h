@@ -1,0 +1,199 @@
+/*
+ * sim.h -- C ABI of the B200-native sparse-inverse local-global solver with
+ * non-smooth frictional contact (arXiv 2503.15078, "Fast But Accurate").
+ *
+ * Citations: P:L<n> = line n of the paper's LaTeX source.
+ *
+ * The four calls of the paper's problem statement (Alg. 4):
+ *   sim_create               mesh, material, time step h
+ *   sim_build_sparse_inverse K = L^-1 of A = M + h^2 sum w G^T G    (Thm 1, Alg. 2)
+ *   sim_set_contacts         J rows, Delassus D = J K^T K J^T, r
+ *   sim_step                 frames x (predict; iterations x L-G)
+ * plus state/pin accessors, statistics and test hooks (sim_debug_*).
+ *
+ * Conventions
+ *  - Every function returns SIM_OK (0) or a negative SIM_E_* code; the
+ *    message of the last error on the calling thread is sim_last_error().
+ *  - All input pointers are borrowed for the duration of the call and deep-
+ *    copied; the library never retains caller pointers.  Output buffers are
+ *    caller-owned.  Host pointers unless stated otherwise.
+ *  - A handle owns all of its device memory and binds the CUDA device that is
+ *    current at sim_create.  A handle is not thread-safe.
+ *  - Call order: create -> build_sparse_inverse -> (set_contacts)* -> step.
+ *    Violations return SIM_E_STATE.  Every call except sim_step gives the
+ *    strong guarantee (no state change on error).
+ *  - Vertex indices in all calls are the caller's original indices; the
+ *    library's internal (elimination-tree postorder) numbering is hidden.
+ *  - Results are deterministic for a given device and configuration (fixed
+ *    reduction orders, no floating-point atomics).
+ */
+#ifndef SIM_H_
+#define SIM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIM_OK            0
+#define SIM_E_INVALID    -1  /* null/size/NaN input, mu < 0, nu not in [0,0.5), bad normal   */
+#define SIM_E_DEGENERATE -2  /* zero-volume tetrahedron (index in the message)               */
+#define SIM_E_NOT_SPD    -3  /* non-positive Cholesky pivot (column in the message)          */
+#define SIM_E_STATE      -4  /* call made out of order                                       */
+#define SIM_E_CUDA       -5  /* CUDA runtime failure or no usable device                     */
+#define SIM_E_OOM        -6  /* host or device allocation failed                             */
+#define SIM_E_NONFINITE  -7  /* non-finite state detected; state rolled back to frame start  */
+#define SIM_E_LIMIT      -8  /* a size exceeds a documented implementation limit             */
+
+typedef struct sim_handle sim_handle;
+
+/* Tetrahedral mesh.  rest_positions [n_vertices][3] in metres;
+ * tets [n_tets][4] (orientation not required); fixed [n_vertices] Dirichlet
+ * mask (nonzero = pinned) or NULL. */
+typedef struct {
+    int32_t n_vertices;
+    int32_t n_tets;
+    const double  *rest_positions;
+    const int32_t *tets;
+    const uint8_t *fixed;
+} sim_mesh;
+
+/* Material models of the local step (eq. PD local). */
+enum { SIM_NEOHOOKEAN = 0, SIM_COROTATED = 1, SIM_ARAP = 2 };
+
+/* density kg/m^3, youngs Pa, poisson in [0,0.5) (Table 3 columns).
+ * proj_stiffness k of w_i = k vol_i; 0 selects k = 2 mu_Lame.
+ * gravity m/s^2 (f_ext = M g).  cr_iterations: CR budget, 0 -> 10. */
+typedef struct {
+    int32_t model;
+    double  density, youngs, poisson;
+    double  proj_stiffness;
+    double  gravity[3];
+    int32_t cr_iterations;
+} sim_material;
+
+/* One contact pair (App. A).
+ * kind 0: unilateral normal row + two Coulomb friction rows (t1, t2);
+ * kind 1: one bilateral row along `normal` with compliance.
+ * verts/weights: up to 4 vertices, (J x)_row = c . sum_a w_a x_a.
+ * normal must be unit length; tangents all-zero -> Gram-Schmidt frame
+ * (e = least-aligned axis, t1 = normalize(e - (n.e) n), t2 = n x t1).
+ * offset: d_n = n . p_obstacle (+ min separation) or d_b.
+ * obstacle_velocity: d_f = t . v_obstacle.  Contacts may not touch
+ * pinned vertices. */
+typedef struct {
+    int32_t kind;
+    int32_t n_verts;
+    int32_t verts[4];
+    double  weights[4];
+    double  normal[3];
+    double  tangent1[3];
+    double  tangent2[3];
+    double  offset;
+    double  obstacle_velocity[3];
+    double  mu;
+    double  compliance;
+} sim_contact;
+
+typedef struct {
+    int64_t n_vertices, n_free, n_tets;
+    int64_t nnz_K;             /* nnz of the vertex-level K = L^-1 (stored twice: row- and column-major) */
+    int64_t nnz_L;
+    int32_t etree_height;
+    int32_t n_panels;          /* fundamental supernodes (rows sharing their first column)               */
+    int32_t n_contacts, n_contact_vertices;
+    int64_t frames_done;
+    double  last_cr_residual;  /* |r| of the last CR solve (fp64), -1 if none                            */
+    double  max_abs_phi_n;     /* max |phi_FB| over unilateral contacts at the last evaluated iterate   */
+    int32_t n_active, n_stick, n_slip;   /* frame-end classification (lambda_n > 0; stick / slip)        */
+    int32_t kernels_per_frame; /* kernel launches in one captured frame                                  */
+    double  build_seconds;     /* host time of sim_build_sparse_inverse                                  */
+    int64_t h2d_contact_bytes; /* host->device bytes of the last sim_set_contacts                        */
+} sim_stats;
+
+/* Validate the mesh and material, compute rest data (Dm^-1, volumes, lumped
+ * mass, w_i = k vol_i).  h > 0 is the time step (s).  No device work yet
+ * except binding the current device. */
+int sim_create(const sim_mesh *mesh, const sim_material *mat, double h, sim_handle **out);
+
+/* Assemble A_v over free vertices (A = A_v (x) I_3), order it (geometric
+ * nested dissection + elimination-tree postorder), factor A_v = L L^T in fp64,
+ * compute K = L^-1 column by column over ancestor chains (Thm 1), store K in
+ * fp32 twice (row-major and column-major values-only panels), build the
+ * K-pass work lists and upload everything.  drop_tolerance: entries with
+ * |K_ij| < tol |K_jj| are zeroed (0 = exact Theorem-1 pattern). */
+int sim_build_sparse_inverse(sim_handle *h, double drop_tolerance);
+
+/* Replace the contact set (n may be 0).  Builds rows, uploads them and
+ * computes on the device G = K[:,Vc]^T K[:,Vc], the Delassus diagonal and the
+ * preconditioner r_n = h^2 D_jj, r_f = h D_jj.  Limit: n <= 1024. */
+int sim_set_contacts(sim_handle *h, const sim_contact *contacts, int32_t n);
+
+/* Advance `frames` frames of `iterations` local-global iterations each
+ * (Alg. 4).  Pinned vertices move by h * pin_velocity per frame.  Enqueued on
+ * the handle's stream; returns after enqueueing (use sim_synchronize or any
+ * blocking accessor). */
+int sim_step(sim_handle *h, int32_t frames, int32_t iterations);
+
+/* Block until all work enqueued on the handle's stream is done; checks the
+ * device-side non-finite flag. */
+int sim_synchronize(sim_handle *h);
+
+/* Constant velocity (m/s) of all pinned vertices (moving Dirichlet handle). */
+int sim_set_pin_velocity(sim_handle *h, const double v[3]);
+
+/* x, v: [n_vertices][3] in original vertex order (caller buffers). */
+int sim_get_state(sim_handle *h, double *x, double *v);
+int sim_set_state(sim_handle *h, const double *x, const double *v);
+
+/* lambda: [rows] = (lambda_n, lambda_f1, lambda_f2) per unilateral contact,
+ * (lambda_b) per bilateral contact, in the order given to sim_set_contacts. */
+int sim_get_lambda(sim_handle *h, double *lambda, int32_t capacity);
+
+int sim_get_stats(sim_handle *h, sim_stats *out);
+
+/* Use a caller-provided cudaStream_t (e.g. torch.cuda.current_stream()). */
+int sim_set_stream(sim_handle *h, void *cuda_stream);
+
+/* Kernel timing: when on, the captured frame graph records an event between
+ * consecutive kernels; sim_get_kernel_times then returns, per kernel kind
+ * (0 predict, 1 contact_eval, 2 local, 3 gather, 4 kpass1, 5 chain_dot, 6 cr,
+ * 7 scatter, 8 kpass2), the summed device ms of the most recent frame.
+ * out must hold >= 9 doubles. */
+int sim_set_profiling(sim_handle *h, int on);
+int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
+
+void sim_destroy(sim_handle *h);         /* NULL-safe */
+const char *sim_last_error(void);
+
+/* ---------------------------------------------------------------------------
+ * Test hooks.  They run exactly the product kernels on caller data.
+ * ------------------------------------------------------------------------- */
+/* Host-side K (fp64 before fp32 rounding is NOT kept; these are the stored
+ * fp32 values): perm[n_free] maps internal free index -> original vertex;
+ * parent[n_free]; rowptr[n_free+1] (int64); vals[nnz_K] row-major.  Any
+ * pointer may be NULL.  Works without a GPU (host precompute only, see
+ * sim_create_host). */
+int sim_debug_get_inverse(sim_handle *h, int32_t *perm, int32_t *parent, int64_t *rowptr, float *vals);
+/* Create a handle that only runs the host precompute (no device). */
+int sim_create_host(const sim_mesh *mesh, const sim_material *mat, double h, sim_handle **out);
+/* x_out = A^-1 b on the device via the two K-passes (y = K P b, x = P^T K^T y),
+ * b and x_out [n_vertices][3]; rows of pinned vertices are ignored / zero.
+ * b is rounded to fp32 (the K-pass input precision) before the product. */
+int sim_debug_apply_inverse(sim_handle *h, const double *b, double *x_out);
+/* One local step at positions x [n_vertices][3] with prediction s
+ * [n_vertices][3]: returns the per-tet projection P [n_tets][9] (row-major
+ * 3x3; NULL to skip) and the global-step residual r = b - A x
+ * = M(s - x) + h^2 sum_i w_i G_i^T (P_i - F_i)  [n_vertices][3] (0 on pinned
+ * rows; NULL to skip).  Does not modify the simulation state. */
+int sim_debug_local(sim_handle *h, const double *x, const double *s, float *P, double *resid);
+/* G = K[:,Vc]^T K[:,Vc] for the current contact set: returns the contact
+ * vertex list (original ids) and G (row-major, n_cv x n_cv). */
+int sim_debug_get_delassus(sim_handle *h, int32_t *cv, float *G, int32_t capacity);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIM_H_ */

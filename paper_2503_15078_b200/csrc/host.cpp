@@ -1,0 +1,474 @@
+// Host precompute of the sparse inverse; see host.hpp for the citations.
+#include "host.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace simhost {
+
+std::string rest_data(int n_v, int n_t, const double* X, const int32_t* T, double density,
+                      double k_proj, RestData& out, int& bad_tet) {
+    out.Bm.assign((size_t)n_t * 9, 0.0);
+    out.vol.assign(n_t, 0.0);
+    out.w.assign(n_t, 0.0);
+    out.mass.assign(n_v, 0.0);
+    bad_tet = -1;
+    for (int t = 0; t < n_t; ++t) {
+        const int32_t* v = T + 4 * (size_t)t;
+        double D[3][3];
+        for (int c = 0; c < 3; ++c)
+            for (int r = 0; r < 3; ++r) D[r][c] = X[3 * (size_t)v[c + 1] + r] - X[3 * (size_t)v[0] + r];
+        double det = D[0][0] * (D[1][1] * D[2][2] - D[1][2] * D[2][1]) -
+                     D[0][1] * (D[1][0] * D[2][2] - D[1][2] * D[2][0]) +
+                     D[0][2] * (D[1][0] * D[2][1] - D[1][1] * D[2][0]);
+        if (!(std::fabs(det) > 0.0) || !std::isfinite(det)) {
+            bad_tet = t;
+            return "degenerate tetrahedron " + std::to_string(t);
+        }
+        double inv = 1.0 / det;
+        double* B = &out.Bm[9 * (size_t)t];
+        B[0] = (D[1][1] * D[2][2] - D[1][2] * D[2][1]) * inv;
+        B[1] = (D[0][2] * D[2][1] - D[0][1] * D[2][2]) * inv;
+        B[2] = (D[0][1] * D[1][2] - D[0][2] * D[1][1]) * inv;
+        B[3] = (D[1][2] * D[2][0] - D[1][0] * D[2][2]) * inv;
+        B[4] = (D[0][0] * D[2][2] - D[0][2] * D[2][0]) * inv;
+        B[5] = (D[0][2] * D[1][0] - D[0][0] * D[1][2]) * inv;
+        B[6] = (D[1][0] * D[2][1] - D[1][1] * D[2][0]) * inv;
+        B[7] = (D[0][1] * D[2][0] - D[0][0] * D[2][1]) * inv;
+        B[8] = (D[0][0] * D[1][1] - D[0][1] * D[1][0]) * inv;
+        double vol = std::fabs(det) / 6.0;
+        out.vol[t] = vol;
+        out.w[t] = k_proj * vol;
+        for (int a = 0; a < 4; ++a) out.mass[v[a]] += density * vol / 4.0;
+    }
+    return "";
+}
+
+// shape gradient g_a (a = 0..3) of tet t: F = sum_a x_a g_a^T
+static inline void shape_grad(const double* B, double g[4][3]) {
+    for (int a = 1; a < 4; ++a)
+        for (int d = 0; d < 3; ++d) g[a][d] = B[3 * (a - 1) + d];
+    for (int d = 0; d < 3; ++d) g[0][d] = -(g[1][d] + g[2][d] + g[3][d]);
+}
+
+Csr assemble_Av(int n_v, int n_t, const int32_t* T, const RestData& rd, double h,
+                const std::vector<int32_t>& vid, int n) {
+    // triplets -> CSR with summation
+    std::vector<std::vector<std::pair<int32_t, double>>> rows(n);
+    for (int t = 0; t < n_t; ++t) {
+        double g[4][3];
+        shape_grad(&rd.Bm[9 * (size_t)t], g);
+        double s = h * h * rd.w[t];
+        for (int a = 0; a < 4; ++a) {
+            int ra = vid[T[4 * (size_t)t + a]];
+            if (ra < 0) continue;
+            for (int b = 0; b < 4; ++b) {
+                int rb = vid[T[4 * (size_t)t + b]];
+                if (rb < 0) continue;
+                double v = s * (g[a][0] * g[b][0] + g[a][1] * g[b][1] + g[a][2] * g[b][2]);
+                rows[ra].push_back({rb, v});
+            }
+        }
+    }
+    for (int v = 0; v < n_v; ++v)
+        if (vid[v] >= 0) rows[vid[v]].push_back({vid[v], rd.mass[v]});
+    Csr A;
+    A.n = n;
+    A.ptr.assign(n + 1, 0);
+    for (int r = 0; r < n; ++r) {
+        auto& R = rows[r];
+        std::sort(R.begin(), R.end(), [](auto& x, auto& y) { return x.first < y.first; });
+        int32_t last = -1;
+        for (auto& e : R) {
+            if (e.first == last) {
+                A.val.back() += e.second;
+            } else {
+                A.col.push_back(e.first);
+                A.val.push_back(e.second);
+                last = e.first;
+            }
+        }
+        A.ptr[r + 1] = (int64_t)A.col.size();
+    }
+    return A;
+}
+
+// ---------------------------------------------------------------------------
+// geometric nested dissection with one-sided vertex separators
+// ---------------------------------------------------------------------------
+namespace {
+struct ND {
+    const Csr& A;
+    const std::vector<double>& X;
+    std::vector<int32_t> order;
+    std::vector<int32_t> side;   // scratch: 0 none, 1 left, 2 right
+    ND(const Csr& A_, const std::vector<double>& X_) : A(A_), X(X_), side(A_.n, 0) {}
+
+    void run(std::vector<int32_t> v) {
+        if (v.size() <= 48) {
+            std::sort(v.begin(), v.end());
+            order.insert(order.end(), v.begin(), v.end());
+            return;
+        }
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        for (int32_t i : v)
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = std::min(lo[d], X[3 * (size_t)i + d]);
+                hi[d] = std::max(hi[d], X[3 * (size_t)i + d]);
+            }
+        int ax = 0;
+        for (int d = 1; d < 3; ++d)
+            if (hi[d] - lo[d] > hi[ax] - lo[ax]) ax = d;
+        if (!(hi[ax] - lo[ax] > 0)) {
+            std::sort(v.begin(), v.end());
+            order.insert(order.end(), v.begin(), v.end());
+            return;
+        }
+        // split at the median coordinate (ties kept together by value)
+        std::vector<double> c(v.size());
+        for (size_t k = 0; k < v.size(); ++k) c[k] = X[3 * (size_t)v[k] + ax];
+        std::vector<double> cs = c;
+        std::nth_element(cs.begin(), cs.begin() + cs.size() / 2, cs.end());
+        double med = cs[cs.size() / 2];
+        std::vector<int32_t> L, R;
+        for (size_t k = 0; k < v.size(); ++k) (c[k] < med ? L : R).push_back(v[k]);
+        if (L.empty() || R.empty()) {
+            L.clear();
+            R.clear();
+            for (size_t k = 0; k < v.size(); ++k) (c[k] <= med ? L : R).push_back(v[k]);
+        }
+        if (L.empty() || R.empty()) {
+            std::sort(v.begin(), v.end());
+            order.insert(order.end(), v.begin(), v.end());
+            return;
+        }
+        for (int32_t i : L) side[i] = 1;
+        for (int32_t i : R) side[i] = 2;
+        // one-sided separators: boundary of L (touching R) and of R (touching L)
+        std::vector<int32_t> SL, SR;
+        for (int32_t i : L) {
+            for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p)
+                if (side[A.col[p]] == 2) { SL.push_back(i); break; }
+        }
+        for (int32_t i : R) {
+            for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p)
+                if (side[A.col[p]] == 1) { SR.push_back(i); break; }
+        }
+        bool useL = SL.size() <= SR.size();
+        const std::vector<int32_t>& S = useL ? SL : SR;
+        for (int32_t i : S) side[i] = 3;
+        std::vector<int32_t> L2, R2;
+        for (int32_t i : L) if (side[i] != 3) L2.push_back(i);
+        for (int32_t i : R) if (side[i] != 3) R2.push_back(i);
+        for (int32_t i : v) side[i] = 0;
+        std::vector<int32_t> Sv(S.begin(), S.end());
+        run(std::move(L2));
+        run(std::move(R2));
+        std::sort(Sv.begin(), Sv.end());
+        order.insert(order.end(), Sv.begin(), Sv.end());
+    }
+};
+}  // namespace
+
+std::vector<int32_t> nested_dissection(const Csr& A, const std::vector<double>& coords) {
+    ND nd(A, coords);
+    std::vector<int32_t> all(A.n);
+    std::iota(all.begin(), all.end(), 0);
+    nd.run(std::move(all));
+    return nd.order;
+}
+
+Csr permute_sym(const Csr& A, const std::vector<int32_t>& perm) {
+    int n = A.n;
+    std::vector<int32_t> inv(n);
+    for (int k = 0; k < n; ++k) inv[perm[k]] = k;
+    Csr C;
+    C.n = n;
+    C.ptr.assign(n + 1, 0);
+    for (int k = 0; k < n; ++k) C.ptr[k + 1] = C.ptr[k] + (A.ptr[perm[k] + 1] - A.ptr[perm[k]]);
+    C.col.resize(C.ptr[n]);
+    C.val.resize(C.ptr[n]);
+    for (int k = 0; k < n; ++k) {
+        int o = perm[k];
+        std::vector<std::pair<int32_t, double>> r;
+        for (int64_t p = A.ptr[o]; p < A.ptr[o + 1]; ++p) r.push_back({inv[A.col[p]], A.val[p]});
+        std::sort(r.begin(), r.end(), [](auto& x, auto& y) { return x.first < y.first; });
+        for (size_t q = 0; q < r.size(); ++q) {
+            C.col[C.ptr[k] + q] = r[q].first;
+            C.val[C.ptr[k] + q] = r[q].second;
+        }
+    }
+    return C;
+}
+
+// Liu's elimination tree with path compression (symmetric CSR, uses j < i entries)
+std::vector<int32_t> etree(const Csr& A) {
+    int n = A.n;
+    std::vector<int32_t> parent(n, -1), anc(n, -1);
+    for (int i = 0; i < n; ++i) {
+        for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p) {
+            int j = A.col[p];
+            while (j != -1 && j < i) {
+                int jn = anc[j];
+                anc[j] = i;
+                if (jn == -1) { parent[j] = i; break; }
+                j = jn;
+            }
+        }
+    }
+    return parent;
+}
+
+std::vector<int32_t> postorder(const std::vector<int32_t>& parent) {
+    int n = (int)parent.size();
+    std::vector<int32_t> head(n, -1), next(n, -1), post;
+    post.reserve(n);
+    for (int j = n - 1; j >= 0; --j) {
+        if (parent[j] == -1) continue;
+        next[j] = head[parent[j]];
+        head[parent[j]] = j;
+    }
+    std::vector<int32_t> stack;
+    for (int r = 0; r < n; ++r) {
+        if (parent[r] != -1) continue;
+        stack.push_back(r);
+        while (!stack.empty()) {
+            int p = stack.back();
+            int c = head[p];
+            if (c == -1) {
+                stack.pop_back();
+                post.push_back(p);
+            } else {
+                head[p] = next[c];
+                stack.push_back(c);
+            }
+        }
+    }
+    return post;   // post[k] = node visited k-th
+}
+
+// up-looking Cholesky (row k of L from a sparse triangular solve over ereach(k))
+bool cholesky(const Csr& A, const std::vector<int32_t>& parent, Factor& f) {
+    int n = A.n;
+    f.n = n;
+    f.parent = parent;
+    std::vector<int32_t> mark(n, -1), cnt(n, 1), stack;
+    // pass 1: column counts
+    std::vector<int32_t> pattern;
+    auto ereach = [&](int k, std::vector<int32_t>& out) {
+        out.clear();
+        mark[k] = k;
+        for (int64_t p = A.ptr[k]; p < A.ptr[k + 1]; ++p) {
+            int j = A.col[p];
+            if (j >= k) continue;
+            while (j != -1 && mark[j] != k) {
+                out.push_back(j);
+                mark[j] = k;
+                j = parent[j];
+            }
+        }
+        std::sort(out.begin(), out.end());
+    };
+    for (int k = 0; k < n; ++k) {
+        ereach(k, pattern);
+        for (int j : pattern) cnt[j]++;
+    }
+    f.Lp.assign(n + 1, 0);
+    for (int j = 0; j < n; ++j) f.Lp[j + 1] = f.Lp[j] + cnt[j];
+    f.Li.assign(f.Lp[n], 0);
+    f.Lx.assign(f.Lp[n], 0.0);
+    std::vector<int64_t> fill(n);
+    for (int j = 0; j < n; ++j) fill[j] = f.Lp[j] + 1;   // slot 0 of each column = diagonal
+    std::fill(mark.begin(), mark.end(), -1);
+    std::vector<double> x(n, 0.0);
+    for (int k = 0; k < n; ++k) {
+        ereach(k, pattern);
+        double d = 0.0;
+        for (int64_t p = A.ptr[k]; p < A.ptr[k + 1]; ++p) {
+            int j = A.col[p];
+            if (j < k) x[j] = A.val[p];
+            else if (j == k) d = A.val[p];
+        }
+        for (int j : pattern) {
+            double lkj = x[j] / f.Lx[f.Lp[j]];
+            x[j] = 0.0;
+            for (int64_t p = f.Lp[j] + 1; p < fill[j]; ++p) x[f.Li[p]] -= f.Lx[p] * lkj;
+            d -= lkj * lkj;
+            f.Li[fill[j]] = k;
+            f.Lx[fill[j]] = lkj;
+            fill[j]++;
+        }
+        if (!(d > 0.0) || !std::isfinite(d)) {
+            f.bad_col = k;
+            return false;
+        }
+        f.Li[f.Lp[k]] = k;
+        f.Lx[f.Lp[k]] = std::sqrt(d);
+    }
+    return true;
+}
+
+void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads) {
+    int n = f.n;
+    K.n = n;
+    K.parent = f.parent;
+    K.depth.assign(n, 0);
+    for (int i = n - 1; i >= 0; --i) K.depth[i] = f.parent[i] < 0 ? 0 : K.depth[f.parent[i]] + 1;
+    std::vector<int32_t> size(n, 1), nchild(n, 0);
+    for (int i = 0; i < n; ++i)
+        if (f.parent[i] >= 0) { size[f.parent[i]] += size[i]; nchild[f.parent[i]]++; }
+    K.first.resize(n);
+    K.height = 0;
+    for (int i = 0; i < n; ++i) {
+        K.first[i] = i - size[i] + 1;
+        K.height = std::max(K.height, K.depth[i] + 1);
+    }
+    K.rowptr.assign(n + 1, 0);
+    K.colptr.assign(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        K.rowptr[i + 1] = K.rowptr[i] + size[i];
+        K.colptr[i + 1] = K.colptr[i] + K.depth[i] + 1;
+    }
+    K.nnz = K.rowptr[n];
+    // panels: row i+1 continues row i's panel iff parent[i] == i+1 and i+1 has one child
+    K.panel_of.assign(n, 0);
+    K.panel_start.clear();
+    for (int i = 0; i < n; ++i) {
+        bool cont = i > 0 && f.parent[i - 1] == i && nchild[i] == 1;
+        if (!cont) K.panel_start.push_back(i);
+        K.panel_of[i] = (int)K.panel_start.size() - 1;
+    }
+    K.panel_start.push_back(n);
+    K.ptop.resize(n);
+    for (size_t p = 0; p + 1 < K.panel_start.size(); ++p)
+        for (int i = K.panel_start[p]; i < K.panel_start[p + 1]; ++i) K.ptop[i] = K.panel_start[p + 1] - 1;
+    K.Krow.assign(K.nnz, 0.f);
+    K.Kcol.assign(K.nnz, 0.f);
+#ifdef _OPENMP
+    if (n_threads > 0) omp_set_num_threads(n_threads);
+#endif
+#pragma omp parallel
+    {
+        std::vector<double> w(n, 0.0);
+        std::vector<int32_t> chain;
+#pragma omp for schedule(dynamic, 16)
+        for (int j = 0; j < n; ++j) {
+            chain.clear();
+            for (int l = j; l != -1; l = f.parent[l]) chain.push_back(l);
+            w[j] = 1.0;
+            double kjj = 0.0;
+            for (size_t q = 0; q < chain.size(); ++q) {
+                int l = chain[q];
+                double kl = w[l] / f.Lx[f.Lp[l]];
+                w[l] = 0.0;
+                for (int64_t p = f.Lp[l] + 1; p < f.Lp[l + 1]; ++p) w[f.Li[p]] -= f.Lx[p] * kl;
+                if (q == 0) kjj = kl;
+                if (drop_tol > 0 && std::fabs(kl) < drop_tol * std::fabs(kjj)) kl = 0.0;
+                float kf = (float)kl;
+                K.Kcol[K.colptr[j] + (int64_t)q] = kf;
+                K.Krow[K.rowptr[l] + (j - K.first[l])] = kf;
+            }
+        }
+    }
+}
+
+void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols, int p2_chunk_rows) {
+    int n = K.n;
+    wl = WorkLists();
+    // ---- pass 1: per panel, 32-row blocks, column chunks of the block's range
+    int npan = (int)K.panel_start.size() - 1;
+    for (int p = 0; p < npan; ++p) {
+        int rs = K.panel_start[p], re = K.panel_start[p + 1];
+        int f = K.first[rs];
+        for (int r0 = rs; r0 < re; r0 += 32) {
+            int nr = std::min(32, re - r0);
+            int cend = r0 + nr;   // columns [f, r0+nr)
+            P1Block b{r0, nr, 0, wl.p1_parts};
+            int bi = (int)wl.p1b.size();
+            for (int c0 = f; c0 < cend; c0 += p1_chunk_cols) {
+                int c1 = std::min(cend, c0 + p1_chunk_cols);
+                wl.p1.push_back(P1Item{r0, nr, c0, c1, bi, wl.p1_parts + b.nitems});
+                b.nitems++;
+            }
+            wl.p1_parts += b.nitems;
+            wl.p1b.push_back(b);
+        }
+    }
+    // ---- pass 2: 32-column blocks; cover rows grouped in per-panel runs
+    std::vector<int32_t> mark(n, -1);
+    std::vector<int32_t> cover;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        int nc = std::min(32, n - c0);
+        int bi = (int)wl.p2b.size();
+        cover.clear();
+        for (int j = c0; j < c0 + nc; ++j)
+            for (int i = j; i != -1 && mark[i] != bi; i = K.parent[i]) {
+                mark[i] = bi;
+                cover.push_back(i);
+            }
+        std::sort(cover.begin(), cover.end());
+        // runs
+        std::vector<Run> runs;
+        for (size_t q = 0; q < cover.size();) {
+            int r0 = cover[q];
+            size_t e = q;
+            while (e + 1 < cover.size() && cover[e + 1] == cover[e] + 1 &&
+                   K.panel_of[cover[e + 1]] == K.panel_of[r0])
+                ++e;
+            int r1 = cover[e];
+            runs.push_back(Run{r0, r1, K.first[r0], 0, K.rowptr[r0] - K.first[r0]});
+            q = e + 1;
+        }
+        // chunk runs into items of ~p2_chunk_rows rows (split long runs)
+        P2Block b{c0, nc, 0, wl.p2_parts};
+        int acc = 0;
+        int run_begin = (int)wl.runs.size();
+        for (auto& R : runs) {
+            int r = R.r0;
+            while (r <= R.r1) {
+                int take = std::min(R.r1 - r + 1, p2_chunk_rows - acc);
+                Run piece{r, r + take - 1, R.first, 0, K.rowptr[r] - R.first};
+                wl.runs.push_back(piece);
+                acc += take;
+                r += take;
+                if (acc >= p2_chunk_rows) {
+                    wl.p2.push_back(P2Item{c0, nc, run_begin, (int)wl.runs.size(), bi, wl.p2_parts + b.nitems});
+                    b.nitems++;
+                    run_begin = (int)wl.runs.size();
+                    acc = 0;
+                }
+            }
+        }
+        if (acc > 0) {
+            wl.p2.push_back(P2Item{c0, nc, run_begin, (int)wl.runs.size(), bi, wl.p2_parts + b.nitems});
+            b.nitems++;
+        }
+        wl.p2_parts += b.nitems;
+        wl.p2b.push_back(b);
+    }
+    // heavy items first (longest-processing-time order); partial slots are fixed per item
+    std::stable_sort(wl.p1.begin(), wl.p1.end(), [](const P1Item& a, const P1Item& b) {
+        return (int64_t)a.nrows * (a.c1 - a.c0) > (int64_t)b.nrows * (b.c1 - b.c0);
+    });
+    auto rows_of = [&](const P2Item& it) {
+        int64_t s = 0;
+        for (int q = it.run0; q < it.run1; ++q) s += wl.runs[q].r1 - wl.runs[q].r0 + 1;
+        return s;
+    };
+    std::vector<std::pair<int64_t, int>> key(wl.p2.size());
+    for (size_t q = 0; q < wl.p2.size(); ++q) key[q] = {rows_of(wl.p2[q]), (int)q};
+    std::stable_sort(key.begin(), key.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    std::vector<P2Item> sorted;
+    sorted.reserve(wl.p2.size());
+    for (auto& k : key) sorted.push_back(wl.p2[k.second]);
+    wl.p2.swap(sorted);
+}
+
+}  // namespace simhost

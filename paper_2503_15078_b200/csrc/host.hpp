@@ -1,0 +1,92 @@
+// Host-side precompute of the sparse inverse (C++17, fp64).
+//
+//   A_v = M + h^2 sum_i w_i g_a g_b^T            (eq. PD global)
+//   ordering: geometric nested dissection        ("e.g. nested dissection")
+//   etree + postorder; up-looking Cholesky       (Alg. 2 line 1)
+//   K = L^-1 column by column over the ancestor chain of each column
+//                                                (Thm 1, Fig. 4)
+//
+// In etree postorder every row i of K is the contiguous column range
+// [first(i), i] (first(i) = i - |subtree(i)| + 1) and every column j is the
+// ancestor chain of j, so K is stored values-only twice: row-major (for the
+// transposed pass) and column-major (for the forward pass).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace simhost {
+
+struct Csr {
+    int n = 0;
+    std::vector<int64_t> ptr;
+    std::vector<int32_t> col;
+    std::vector<double> val;
+};
+
+struct RestData {
+    std::vector<double> Bm;     // [n_t][9] row-major Dm^-1
+    std::vector<double> vol;    // [n_t]
+    std::vector<double> w;      // [n_t] w_i = k vol_i
+    std::vector<double> mass;   // [n_v] lumped
+};
+
+// returns "" on success, else message; bad_tet set on degenerate tet
+std::string rest_data(int n_v, int n_t, const double* X, const int32_t* T, double density,
+                      double k_proj, RestData& out, int& bad_tet);
+
+// A_v restricted to the vertex subset `vid` (vid[v] = row index or -1), full symmetric CSR
+Csr assemble_Av(int n_v, int n_t, const int32_t* T, const RestData& rd, double h,
+                const std::vector<int32_t>& vid, int n_rows);
+
+// geometric nested dissection: returns order[k] = row index eliminated k-th
+std::vector<int32_t> nested_dissection(const Csr& A, const std::vector<double>& coords /*[n][3]*/);
+
+struct Factor {
+    int n = 0;
+    std::vector<int32_t> parent;     // etree (postordered: parent[i] > i or -1)
+    std::vector<int64_t> Lp;         // CSC of L, diagonal first in each column
+    std::vector<int32_t> Li;
+    std::vector<double> Lx;
+    int bad_col = -1;
+};
+
+// symmetric permutation C = P A P^T with perm[new] = old
+Csr permute_sym(const Csr& A, const std::vector<int32_t>& perm);
+std::vector<int32_t> etree(const Csr& A);
+std::vector<int32_t> postorder(const std::vector<int32_t>& parent);
+// up-looking Cholesky; returns false on non-positive pivot (f.bad_col)
+bool cholesky(const Csr& A, const std::vector<int32_t>& parent, Factor& f);
+
+struct Inverse {
+    int n = 0;
+    std::vector<int32_t> parent, depth, first, ptop, panel_of;
+    std::vector<int64_t> rowptr, colptr;   // row-major and column-major offsets
+    std::vector<float> Krow, Kcol;         // fp32 values
+    std::vector<int32_t> panel_start;      // [n_panels+1]
+    int height = 0;
+    int64_t nnz = 0;
+};
+
+// K = L^-1 (fp64 compute, fp32 store); drop |K_ij| < tol |K_jj| (tol > 0)
+void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads);
+
+// ---------------- K-pass work lists (one warp per item) ---------------------
+struct P1Item { int32_t r0, nrows, c0, c1, block, part; };   // rows [r0,r0+nrows) x cols [c0,c1)
+struct P1Block { int32_t r0, nrows, nitems, part0; };
+struct P2Item { int32_t c0, ncols, run0, run1, block, part; };  // cols [c0,c0+ncols) x runs[run0,run1)
+struct P2Block { int32_t c0, ncols, nitems, part0; };
+struct Run { int32_t r0, r1, first, pad; int64_t rowbase; };      // rows [r0,r1] of one panel
+
+struct WorkLists {
+    std::vector<P1Item> p1;
+    std::vector<P1Block> p1b;
+    std::vector<P2Item> p2;
+    std::vector<P2Block> p2b;
+    std::vector<Run> runs;
+    int p1_parts = 0, p2_parts = 0;
+};
+
+void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols, int p2_chunk_rows);
+
+}  // namespace simhost

@@ -1,0 +1,1041 @@
+// Hot-path kernels of the sparse-inverse local-global iteration (sm_100a).
+//
+// Per L-G iteration (Alg. 4), delta form x^{k+1} = x^k + A^-1 (b - A x^k + h^2 H^T lam):
+//   local        per tet: F, signed SVD, projection, force block      (eq. PD local P:L310)
+//   contact_eval per contact: gaps, FB theta/E/phi, h-vector           (App. B.2)
+//   gather       per vertex: u = M(s - x) + sum_i f_i + h^2 H^T lam     (delta form)
+//   kpass1       y = K u            (3 RHS, column-major K, thread per row)   (P:L442 first SpMV)
+//   chain_dot    (K^T y) at contact vertices (ancestor chains)
+//   cr           (Theta D Theta + C) z = rho, CR in one 16-CTA cluster
+//   scatter      y += K H^T z (rows on the contact vertices' chains)    (P:L956 correction)
+//   kpass2       x += K^T y         (row-major K, thread per column)  (P:L442 second SpMV)
+// No tensor cores: every step is sparse / memory- or latency-bound.
+#include <cooperative_groups.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace simdev {
+
+// ----------------------------------------------------------------------------
+// predict: s = x_t + h v_t + h^2 g; x^0 = s; pinned: x = x_t + h v_pin
+// ----------------------------------------------------------------------------
+__global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict__ xt,
+                          double4* __restrict__ v, double4* __restrict__ s, double* __restrict__ lam, int nlam) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nlam) lam[i] = 0.0;   // lambda^0 = 0 (reading A10)
+    if (i >= P.n_v) return;
+    double4 xi = x[i];
+    xt[i] = xi;
+    double h = P.h;
+    if (i < P.n_f) {
+        double4 vi = v[i];
+        double4 si = make_double4(xi.x + h * vi.x + h * h * P.g[0], xi.y + h * vi.y + h * h * P.g[1],
+                                  xi.z + h * vi.z + h * h * P.g[2], 0.0);
+        s[i] = si;
+        x[i] = si;
+    } else {
+        x[i] = make_double4(xi.x + h * P.vpin[0], xi.y + h * P.vpin[1], xi.z + h * P.vpin[2], 0.0);
+        v[i] = make_double4(P.vpin[0], P.vpin[1], P.vpin[2], 0.0);
+    }
+}
+
+void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
+                    double* lam, int nlam) {
+    int n = P.n_v > nlam ? P.n_v : nlam;
+    k_predict<<<(n + 255) / 256, 256, 0, st>>>(P, x, xt, v, s, lam, nlam);
+}
+
+// ----------------------------------------------------------------------------
+// local step
+// ----------------------------------------------------------------------------
+// Jacobi eigen-decomposition of a symmetric 3x3 (cyclic, Rutishauser rotations).
+__device__ __forceinline__ void jacobi3(float S[3][3], float V[3][3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.f : 0.f;
+#pragma unroll 1
+    for (int sweep = 0; sweep < 6; ++sweep) {
+        float off = fabsf(S[0][1]) + fabsf(S[0][2]) + fabsf(S[1][2]);
+        float dia = fabsf(S[0][0]) + fabsf(S[1][1]) + fabsf(S[2][2]);
+        if (off <= 1e-9f * dia) break;
+#pragma unroll
+        for (int pq = 0; pq < 3; ++pq) {
+            const int p = pq == 2 ? 1 : 0;
+            const int q = pq == 0 ? 1 : 2;
+            const int r = 3 - p - q;
+            float apq = S[p][q];
+            if (fabsf(apq) <= 1e-30f) continue;
+            float theta = (S[q][q] - S[p][p]) / (2.f * apq);
+            float at = fabsf(theta);
+            float t = at > 1e15f ? 0.5f / at : 1.f / (at + sqrtf(theta * theta + 1.f));
+            t = theta < 0.f ? -t : t;
+            float c = rsqrtf(t * t + 1.f);
+            float s = t * c;
+            S[p][p] -= t * apq;
+            S[q][q] += t * apq;
+            S[p][q] = S[q][p] = 0.f;
+            float srp = S[r][p], srq = S[r][q];
+            S[r][p] = S[p][r] = c * srp - s * srq;
+            S[r][q] = S[q][r] = s * srp + c * srq;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                float vkp = V[k][p], vkq = V[k][q];
+                V[k][p] = c * vkp - s * vkq;
+                V[k][q] = s * vkp + c * vkq;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void swapcol(float V[3][3], float* e, int a, int b) {
+    float t = e[a];
+    e[a] = e[b];
+    e[b] = t;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float u = V[k][a];
+        V[k][a] = V[k][b];
+        V[k][b] = u;
+    }
+}
+
+// NH objective in sigma space: k/2|p-sig|^2 + mu/2(|p|^2-3) - mu lnJ + lam/2 ln^2 J
+__device__ __forceinline__ float nh_f(const float p[3], const float sg[3], float k, float mu, float lam) {
+    float lnJ = logf(p[0]) + logf(p[1]) + logf(p[2]);
+    float d0 = p[0] - sg[0], d1 = p[1] - sg[1], d2 = p[2] - sg[2];
+    return 0.5f * k * (d0 * d0 + d1 * d1 + d2 * d2) +
+           0.5f * mu * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2] - 3.f) - mu * lnJ + 0.5f * lam * lnJ * lnJ;
+}
+
+// p* = argmin k/2|p - sig|^2 + psi(p)  (reading A2-A4); returns delta = p* - sig
+__device__ __forceinline__ void project_sigma(int model, const float sg[3], float k, float mu, float lam,
+                                              float d[3]) {
+    if (model == 2) {   // ARAP: p* = 1
+        d[0] = 1.f - sg[0];
+        d[1] = 1.f - sg[1];
+        d[2] = 1.f - sg[2];
+        return;
+    }
+    if (model == 1) {   // linear corotated closed form
+        float S = (k * (sg[0] + sg[1] + sg[2]) + 6.f * mu + 9.f * lam) / (k + 2.f * mu + 3.f * lam);
+        float inv = 1.f / (k + 2.f * mu);
+        // p_i - sig_i = (2mu(1 - sig_i) - lam(S - 3)) / (k + 2mu)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) d[i] = (2.f * mu * (1.f - sg[i]) - lam * (S - 3.f)) * inv;
+        return;
+    }
+    // Neo-Hookean: damped Newton from p0 = max(sig, 0.05), <= 16 iterations
+    float p[3] = {fmaxf(sg[0], 0.05f), fmaxf(sg[1], 0.05f), fmaxf(sg[2], 0.05f)};
+    float scale = fmaxf(1.f, sqrtf(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]));
+#pragma unroll 1
+    for (int it = 0; it < 16; ++it) {
+        float lnJ = logf(p[0]) + logf(p[1]) + logf(p[2]);
+        float iv[3] = {1.f / p[0], 1.f / p[1], 1.f / p[2]};
+        float g[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) g[i] = k * (p[i] - sg[i]) + mu * p[i] - mu * iv[i] + lam * lnJ * iv[i];
+        float gn = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+        if (gn <= 2e-6f * k * scale) break;
+        float H[3][3];
+        float dg = mu - lam * lnJ;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) H[i][j] = lam * iv[i] * iv[j] + (i == j ? (k + mu + dg * iv[i] * iv[i]) : 0.f);
+        // Cramer solve H dd = -g
+        float c00 = H[1][1] * H[2][2] - H[1][2] * H[2][1];
+        float c01 = H[1][2] * H[2][0] - H[1][0] * H[2][2];
+        float c02 = H[1][0] * H[2][1] - H[1][1] * H[2][0];
+        float det = H[0][0] * c00 + H[0][1] * c01 + H[0][2] * c02;
+        float dd[3];
+        bool ok = fabsf(det) > 0.f && isfinite(det);
+        if (ok) {
+            float id = 1.f / det;
+            float c10 = H[0][2] * H[2][1] - H[0][1] * H[2][2];
+            float c11 = H[0][0] * H[2][2] - H[0][2] * H[2][0];
+            float c12 = H[0][1] * H[2][0] - H[0][0] * H[2][1];
+            float c20 = H[0][1] * H[1][2] - H[0][2] * H[1][1];
+            float c21 = H[0][2] * H[1][0] - H[0][0] * H[1][2];
+            float c22 = H[0][0] * H[1][1] - H[0][1] * H[1][0];
+            dd[0] = -(c00 * g[0] + c10 * g[1] + c20 * g[2]) * id;
+            dd[1] = -(c01 * g[0] + c11 * g[1] + c21 * g[2]) * id;
+            dd[2] = -(c02 * g[0] + c12 * g[1] + c22 * g[2]) * id;
+            float slope = dd[0] * g[0] + dd[1] * g[1] + dd[2] * g[2];
+            ok = slope < 0.f && isfinite(slope);
+        }
+        if (!ok) {
+            float s = -1.f / (k + mu);
+            dd[0] = s * g[0];
+            dd[1] = s * g[1];
+            dd[2] = s * g[2];
+        }
+        float slope = dd[0] * g[0] + dd[1] * g[1] + dd[2] * g[2];
+        float f0 = nh_f(p, sg, k, mu, lam);
+        float fr = 2e-6f * (k * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2] + sg[0] * sg[0] + sg[1] * sg[1] +
+                                 sg[2] * sg[2]) + mu * fabsf(lnJ) + lam * lnJ * lnJ + mu);
+        float t = 1.f;
+#pragma unroll 1
+        for (int ls = 0; ls < 40; ++ls) {
+            float pn[3] = {p[0] + t * dd[0], p[1] + t * dd[1], p[2] + t * dd[2]};
+            if (pn[0] > 0.f && pn[1] > 0.f && pn[2] > 0.f) {
+                float fn = nh_f(pn, sg, k, mu, lam);
+                if (fn <= f0 + 1e-4f * t * slope + fr) break;
+            }
+            t *= 0.5f;
+        }
+        p[0] += t * dd[0];
+        p[1] += t * dd[1];
+        p[2] += t * dd[2];
+    }
+    d[0] = p[0] - sg[0];
+    d[1] = p[1] - sg[1];
+    d[2] = p[2] - sg[2];
+}
+
+// one thread per tet: f_a = h^2 w (P - F) g_a, written per corner
+__global__ void __launch_bounds__(128) k_local(Params P, const int4* __restrict__ tet, const float* __restrict__ Bm,
+                                               const float* __restrict__ hw2, const double4* __restrict__ x,
+                                               float4* __restrict__ fc, float* __restrict__ Pdbg) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= P.n_t) return;
+    const int nt = P.n_t;
+    int4 tv = __ldg(&tet[t]);
+    double4 x0 = x[tv.x], x1 = x[tv.y], x2 = x[tv.z], x3 = x[tv.w];
+    // Ds columns (fp64 differences, then fp32)
+    float D[3][3];
+    D[0][0] = (float)(x1.x - x0.x); D[1][0] = (float)(x1.y - x0.y); D[2][0] = (float)(x1.z - x0.z);
+    D[0][1] = (float)(x2.x - x0.x); D[1][1] = (float)(x2.y - x0.y); D[2][1] = (float)(x2.z - x0.z);
+    D[0][2] = (float)(x3.x - x0.x); D[1][2] = (float)(x3.y - x0.y); D[2][2] = (float)(x3.z - x0.z);
+    float B[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) B[e] = __ldg(&Bm[(size_t)e * nt + t]);
+    float F[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) F[i][j] = D[i][0] * B[0 * 3 + j] + D[i][1] * B[1 * 3 + j] + D[i][2] * B[2 * 3 + j];
+    // S = F^T F, eigenvectors V
+    float S[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) S[i][j] = F[0][i] * F[0][j] + F[1][i] * F[1][j] + F[2][i] * F[2][j];
+    float V[3][3];
+    jacobi3(S, V);
+    float ev[3] = {S[0][0], S[1][1], S[2][2]};
+    if (ev[0] < ev[1]) swapcol(V, ev, 0, 1);
+    if (ev[0] < ev[2]) swapcol(V, ev, 0, 2);
+    if (ev[1] < ev[2]) swapcol(V, ev, 1, 2);
+    float detV = V[0][0] * (V[1][1] * V[2][2] - V[1][2] * V[2][1]) - V[0][1] * (V[1][0] * V[2][2] - V[1][2] * V[2][0]) +
+                 V[0][2] * (V[1][0] * V[2][1] - V[1][1] * V[2][0]);
+    if (detV < 0.f) {
+        V[0][2] = -V[0][2];
+        V[1][2] = -V[1][2];
+        V[2][2] = -V[2][2];
+    }
+    // U by Gram-Schmidt on F V (U in SO(3)); signed singular values sg_i = u_i . F v_i
+    float FV[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) FV[i][j] = F[i][0] * V[0][j] + F[i][1] * V[1][j] + F[i][2] * V[2][j];
+    float U[3][3];
+    float n0 = sqrtf(FV[0][0] * FV[0][0] + FV[1][0] * FV[1][0] + FV[2][0] * FV[2][0]);
+    if (n0 > 1e-30f) {
+        U[0][0] = FV[0][0] / n0; U[1][0] = FV[1][0] / n0; U[2][0] = FV[2][0] / n0;
+    } else {
+        U[0][0] = 1.f; U[1][0] = 0.f; U[2][0] = 0.f;
+    }
+    float dt = U[0][0] * FV[0][1] + U[1][0] * FV[1][1] + U[2][0] * FV[2][1];
+    float w0 = FV[0][1] - dt * U[0][0], w1 = FV[1][1] - dt * U[1][0], w2 = FV[2][1] - dt * U[2][0];
+    float n1 = sqrtf(w0 * w0 + w1 * w1 + w2 * w2);
+    if (n1 > 1e-30f * fmaxf(1.f, n0)) {
+        U[0][1] = w0 / n1; U[1][1] = w1 / n1; U[2][1] = w2 / n1;
+    } else {   // any unit vector orthogonal to u0
+        float a0 = U[0][0], a1 = U[1][0], a2 = U[2][0];
+        float e0 = fabsf(a0) < 0.577f ? 1.f : 0.f, e1 = e0 == 0.f && fabsf(a1) < 0.577f ? 1.f : 0.f;
+        float e2 = (e0 == 0.f && e1 == 0.f) ? 1.f : 0.f;
+        float dp = a0 * e0 + a1 * e1 + a2 * e2;
+        w0 = e0 - dp * a0; w1 = e1 - dp * a1; w2 = e2 - dp * a2;
+        n1 = sqrtf(w0 * w0 + w1 * w1 + w2 * w2);
+        U[0][1] = w0 / n1; U[1][1] = w1 / n1; U[2][1] = w2 / n1;
+    }
+    U[0][2] = U[1][0] * U[2][1] - U[2][0] * U[1][1];
+    U[1][2] = U[2][0] * U[0][1] - U[0][0] * U[2][1];
+    U[2][2] = U[0][0] * U[1][1] - U[1][0] * U[0][1];
+    float sg[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sg[j] = U[0][j] * FV[0][j] + U[1][j] * FV[1][j] + U[2][j] * FV[2][j];
+    float dlt[3];
+    project_sigma(P.model, sg, P.k, P.mu, P.lam, dlt);
+    // Q = hw2 * U diag(delta) V^T  (= h^2 w (P - F))
+    float hw = __ldg(&hw2[t]);
+    float Q[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            Q[i][j] = hw * (U[i][0] * dlt[0] * V[j][0] + U[i][1] * dlt[1] * V[j][1] + U[i][2] * dlt[2] * V[j][2]);
+    if (Pdbg) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                Pdbg[(size_t)t * 9 + 3 * i + j] =
+                    F[i][j] + (U[i][0] * dlt[0] * V[j][0] + U[i][1] * dlt[1] * V[j][1] + U[i][2] * dlt[2] * V[j][2]);
+    }
+    // f_a = Q g_a, g_a = row a-1 of Bm (a = 1..3), f_0 = -sum
+    float f[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) f[a][i] = Q[i][0] * B[3 * a + 0] + Q[i][1] * B[3 * a + 1] + Q[i][2] * B[3 * a + 2];
+    float4* o = fc + 4 * (size_t)t;
+    o[0] = make_float4(-(f[0][0] + f[1][0] + f[2][0]), -(f[0][1] + f[1][1] + f[2][1]), -(f[0][2] + f[1][2] + f[2][2]), 0.f);
+    o[1] = make_float4(f[0][0], f[0][1], f[0][2], 0.f);
+    o[2] = make_float4(f[1][0], f[1][1], f[1][2], 0.f);
+    o[3] = make_float4(f[2][0], f[2][1], f[2][2], 0.f);
+}
+
+void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
+                  const double4* x, float4* fc, float* Pdbg) {
+    k_local<<<(P.n_t + 127) / 128, 128, 0, st>>>(P, tet, Bm, hw2, x, fc, Pdbg);
+}
+
+// ----------------------------------------------------------------------------
+// contact evaluation (fp64): gaps at x^k (reading A22), FB indicators (App. B.2)
+// ----------------------------------------------------------------------------
+__global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const double4* __restrict__ x,
+                               const double4* __restrict__ xt, ContactState cs) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= P.nc) return;
+    const DContact& ct = C[c];
+    double h = P.h;
+    double xc[3] = {0, 0, 0}, xtc[3] = {0, 0, 0};
+    for (int q = 0; q < ct.nv; ++q) {
+        double4 a = x[ct.vtx[q]], b = xt[ct.vtx[q]];
+        xc[0] += ct.w[q] * a.x; xc[1] += ct.w[q] * a.y; xc[2] += ct.w[q] * a.z;
+        xtc[0] += ct.w[q] * b.x; xtc[1] += ct.w[q] * b.y; xtc[2] += ct.w[q] * b.z;
+    }
+    double Jx[3], Jxt[3];
+    for (int k = 0; k < 3; ++k) {
+        Jx[k] = ct.c[k][0] * xc[0] + ct.c[k][1] * xc[1] + ct.c[k][2] * xc[2];
+        Jxt[k] = ct.c[k][0] * xtc[0] + ct.c[k][1] * xtc[1] + ct.c[k][2] * xtc[2];
+    }
+    double* lam = cs.lam + 3 * c;
+    double th[3], E[3], hv[3];
+    double phin_abs = 0.0;
+    if (ct.kind == 1) {   // bilateral (reading A17): theta 1, E = e, h_b = d_b - E lam
+        th[0] = 1.0; E[0] = ct.e; hv[0] = ct.dn - ct.e * lam[0];
+        th[1] = th[2] = 0.0; E[1] = E[2] = 1.0; hv[1] = hv[2] = 0.0;   // padding rows (identity)
+        cs.theta[3 * c] = th[0]; cs.cdiag[3 * c] = E[0] / (h * h); cs.hvec[3 * c] = hv[0];
+        for (int k = 1; k < 3; ++k) { cs.theta[3 * c + k] = 0.0; cs.cdiag[3 * c + k] = 1.0; cs.hvec[3 * c + k] = 0.0; }
+        for (int d = 0; d < 3; ++d) cs.hl[3 * c + d] = lam[0] * ct.c[0][d];
+        cs.phi_abs[c] = 0.0;
+        return;
+    }
+    double rn = h * h * ct.Djj, rf = h * ct.Djj;
+    // normal FB (A15)
+    double y = Jx[0] - ct.dn, ln = lam[0];
+    double S = sqrt(y * y + rn * rn * ln * ln);
+    double phin, thn, En;
+    if (S > 0.0) {
+        double a = y + rn * ln;
+        phin = a > 0.0 ? (2.0 * y * rn * ln) / (a + S) : a - S;
+        thn = 1.0 - y / S;
+        En = (1.0 - rn * ln / S) * rn;
+    } else {
+        phin = 0.0; thn = 1.0; En = 0.0;
+    }
+    phin_abs = fabs(phin);
+    // friction (A14, A16, A16b)
+    double yd1 = (Jx[1] - Jxt[1]) / h - ct.df1, yd2 = (Jx[2] - Jxt[2]) / h - ct.df2;
+    double thf, Ef;
+    if (ln > 0.0 && ct.mu * ln > 0.0) {
+        double s = sqrt(yd1 * yd1 + yd2 * yd2);
+        double lf = sqrt(lam[1] * lam[1] + lam[2] * lam[2]);
+        double q = ct.mu * ln - lf;
+        double R = sqrt(s * s + rf * rf * q * q);
+        double num = rf * (R - rf * q);
+        double den = s + ct.mu * rf * ln - R;
+        double fl = 1e-6 * (s + ct.mu * rf * ln);
+        den = den > fl ? den : fl;
+        Ef = den > 0.0 ? num / den : 0.0;
+        thf = 1.0;
+    } else {
+        thf = 0.0; Ef = 1.0;
+    }
+    double phif1 = thf * yd1 + Ef * lam[1], phif2 = thf * yd2 + Ef * lam[2];
+    th[0] = thn; th[1] = th[2] = thf;
+    cs.theta[3 * c] = thn; cs.theta[3 * c + 1] = thf; cs.theta[3 * c + 2] = thf;
+    cs.cdiag[3 * c] = En / (h * h); cs.cdiag[3 * c + 1] = Ef / h; cs.cdiag[3 * c + 2] = Ef / h;
+    // h-vector
+    cs.hvec[3 * c] = -phin + thn * Jx[0];
+    cs.hvec[3 * c + 1] = -h * phif1 + thf * Jx[1];
+    cs.hvec[3 * c + 2] = -h * phif2 + thf * Jx[2];
+    for (int d = 0; d < 3; ++d)
+        cs.hl[3 * c + d] = thn * lam[0] * ct.c[0][d] + thf * (lam[1] * ct.c[1][d] + lam[2] * ct.c[2][d]);
+    cs.phi_abs[c] = phin_abs;
+}
+
+void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, const double4* x,
+                         const double4* xt, ContactState cs) {
+    if (P.nc == 0) return;
+    k_contact_eval<<<(P.nc + 127) / 128, 128, 0, st>>>(P, c, x, xt, cs);
+}
+
+// ----------------------------------------------------------------------------
+// gather: u_a = M_a (s_a - x_a) + sum_{(t,c) in adj(a)} f_{t,c} + h^2 (H^T lam)_a
+// (colour-free: each free vertex sums its incident tets in a fixed order)
+// ----------------------------------------------------------------------------
+__global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32_t* __restrict__ adj,
+                         const float4* __restrict__ fc, const double* __restrict__ M, const double4* __restrict__ x,
+                         const double4* __restrict__ s, const int32_t* __restrict__ vcp,
+                         const int32_t* __restrict__ vci, const float* __restrict__ vcw,
+                         const double* __restrict__ hl, float4* __restrict__ u, double* __restrict__ resid) {
+    int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= P.n_f) return;
+    double4 xa = x[a], sa = s[a];
+    double m = M[a];
+    double r0 = m * (sa.x - xa.x), r1 = m * (sa.y - xa.y), r2 = m * (sa.z - xa.z);
+    int p0 = adjp[a], p1 = adjp[a + 1];
+    float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+    for (int p = p0; p < p1; ++p) {
+        float4 f = __ldg(&fc[adj[p]]);
+        f0 += f.x;
+        f1 += f.y;
+        f2 += f.z;
+    }
+    r0 += f0;
+    r1 += f1;
+    r2 += f2;
+    if (resid) {
+        resid[3 * (size_t)a] = r0;
+        resid[3 * (size_t)a + 1] = r1;
+        resid[3 * (size_t)a + 2] = r2;
+    }
+    if (vcp) {
+        double hh = P.h * P.h;
+        for (int p = vcp[a]; p < vcp[a + 1]; ++p) {
+            int c = vci[p];
+            double w = vcw[p];
+            r0 += hh * w * hl[3 * c];
+            r1 += hh * w * hl[3 * c + 1];
+            r2 += hh * w * hl[3 * c + 2];
+        }
+    }
+    u[a] = make_float4((float)r0, (float)r1, (float)r2, 0.f);
+}
+
+void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
+                   const float4* fc, const double* M, const double4* x, const double4* s,
+                   const int32_t* vcp, const int32_t* vci, const float* vcw, const double* hl,
+                   float4* u, double* resid_dbg) {
+    k_gather<<<(P.n_f + 255) / 256, 256, 0, st>>>(P, adjp, adj, fc, M, x, s, vcp, vci, vcw, hl, u, resid_dbg);
+}
+
+// ----------------------------------------------------------------------------
+// K-pass 1: y = K u.  One warp per item = (32 rows of one panel) x (column chunk).
+// K is column-major: K[r][j] = Kcol[cb[j] - depth[r]], cb[j] = colptr[j] + depth[j];
+// within a panel depth[r0 + l] = depth[r0] - l, so lanes read consecutive words.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ bool last_of_block(int* counter, int nitems) {
+    __threadfence();
+    __syncwarp();
+    int old = 0;
+    if ((threadIdx.x & 31) == 0) old = atomicAdd(counter, 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    bool last = old == nitems - 1;
+    if (last) __threadfence();
+    return last;
+}
+
+constexpr int kWarpsPerBlock = 8;
+
+__global__ void __launch_bounds__(256) k_kpass1(int nitems, const P1Item* __restrict__ items,
+                                                const P1Block* __restrict__ blocks, const float* __restrict__ Kcol,
+                                                const int64_t* __restrict__ cb, const int32_t* __restrict__ depth,
+                                                const float4* __restrict__ u, float4* __restrict__ y,
+                                                double* __restrict__ part, int* __restrict__ counters) {
+    __shared__ int64_t s_cb[kWarpsPerBlock][32];
+    __shared__ float4 s_u[kWarpsPerBlock][32];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w = blockIdx.x * kWarpsPerBlock + wib;
+    if (w >= nitems) return;
+    const P1Item it = items[w];
+    const int r = it.r0 + lane;
+    const bool act = lane < it.nrows;
+    const int64_t base = (int64_t)lane - depth[it.r0];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int jc = it.c0; jc < it.c1; jc += 32) {
+        int j = jc + lane;
+        if (j < it.c1) {
+            s_cb[wib][lane] = __ldg(&cb[j]);
+            s_u[wib][lane] = __ldg(&u[j]);
+        }
+        __syncwarp();
+        const int nj = min(32, it.c1 - jc);
+        float kv[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            kv[q] = 0.f;
+            if (q < nj && act && jc + q <= r) kv[q] = __ldcs(&Kcol[s_cb[wib][q] + base]);
+        }
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            float4 uq = s_u[wib][q];
+            double kq = (double)kv[q];
+            a0 = fma(kq, (double)uq.x, a0);
+            a1 = fma(kq, (double)uq.y, a1);
+            a2 = fma(kq, (double)uq.z, a2);
+        }
+        __syncwarp();
+    }
+    const P1Block b = blocks[it.block];
+    if (b.nitems == 1) {
+        if (act) y[r] = make_float4((float)a0, (float)a1, (float)a2, 0.f);
+        return;
+    }
+    double* pp = part + ((size_t)it.part * 32 + lane) * 3;
+    pp[0] = a0;
+    pp[1] = a1;
+    pp[2] = a2;
+    if (last_of_block(&counters[it.block], b.nitems)) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        for (int q = 0; q < b.nitems; ++q) {
+            const double* pq = part + ((size_t)(b.part0 + q) * 32 + lane) * 3;
+            s0 += __ldcg(pq);
+            s1 += __ldcg(pq + 1);
+            s2 += __ldcg(pq + 2);
+        }
+        if (act) y[r] = make_float4((float)s0, (float)s1, (float)s2, 0.f);
+        if (lane == 0) counters[it.block] = 0;
+    }
+}
+
+void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* Kcol,
+                   const int64_t* cb, const int32_t* depth, const float4* u, float4* y, double* part,
+                   int* counters) {
+    int nb = (nitems + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    k_kpass1<<<nb, 32 * kWarpsPerBlock, 0, st>>>(nitems, it, bl, Kcol, cb, depth, u, y, part, counters);
+}
+
+// ----------------------------------------------------------------------------
+// K-pass 2: x += K^T y.  One warp per item = (32 columns) x (runs of cover rows).
+// K is row-major: K[r][j] = Krow[rowbase(r) + j], rowbase(r) = rowptr[r] - first(r);
+// inside a run (one panel, shared first f) rowbase(r+1) = rowbase(r) + r - f + 1.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_kpass2(int nitems, const P2Item* __restrict__ items,
+                                                const P2Block* __restrict__ blocks, const Run* __restrict__ runs,
+                                                const float* __restrict__ Krow, const float4* __restrict__ y,
+                                                double* __restrict__ part, int* __restrict__ counters,
+                                                double4* __restrict__ x, const double4* __restrict__ xt,
+                                                double4* __restrict__ v, double inv_h, int finalize_v) {
+    __shared__ float4 s_y[kWarpsPerBlock][32];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w = blockIdx.x * kWarpsPerBlock + wib;
+    if (w >= nitems) return;
+    const P2Item it = items[w];
+    const int j = it.c0 + lane;
+    const bool act = lane < it.ncols;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int q = it.run0; q < it.run1; ++q) {
+        const Run R = runs[q];
+        const int f = R.first;
+        const bool colok = act && j >= f;
+        for (int rc = R.r0; rc <= R.r1; rc += 32) {
+            int rr = rc + lane;
+            if (rr <= R.r1) s_y[wib][lane] = __ldg(&y[rr]);
+            __syncwarp();
+            const int nr = min(32, R.r1 - rc + 1);
+            // rowbase(rc + q) = rowbase(rc) + q (rc - f + 1) + q (q - 1) / 2
+            const int64_t rb0 = R.rowbase + (int64_t)(rc - R.r0) * (R.r0 - f + 1) +
+                                (int64_t)(rc - R.r0) * (rc - R.r0 - 1) / 2 + j;
+            const int64_t step0 = rc - f + 1;
+            float kv[32];
+#pragma unroll
+            for (int qq = 0; qq < 32; ++qq) {
+                kv[qq] = 0.f;
+                if (qq < nr && colok && j <= rc + qq)
+                    kv[qq] = __ldcs(&Krow[rb0 + (int64_t)qq * step0 + (int64_t)qq * (qq - 1) / 2]);
+            }
+#pragma unroll
+            for (int qq = 0; qq < 32; ++qq) {
+                float4 yq = s_y[wib][qq];
+                double kq = (double)kv[qq];
+                a0 = fma(kq, (double)yq.x, a0);
+                a1 = fma(kq, (double)yq.y, a1);
+                a2 = fma(kq, (double)yq.z, a2);
+            }
+            __syncwarp();
+        }
+    }
+    const P2Block b = blocks[it.block];
+    bool fin = false;
+    if (b.nitems == 1) {
+        fin = true;
+    } else {
+        double* pp = part + ((size_t)it.part * 32 + lane) * 3;
+        pp[0] = a0;
+        pp[1] = a1;
+        pp[2] = a2;
+        if (last_of_block(&counters[it.block], b.nitems)) {
+            a0 = a1 = a2 = 0.0;
+            for (int q = 0; q < b.nitems; ++q) {
+                const double* pq = part + ((size_t)(b.part0 + q) * 32 + lane) * 3;
+                a0 += __ldcg(pq);
+                a1 += __ldcg(pq + 1);
+                a2 += __ldcg(pq + 2);
+            }
+            if (lane == 0) counters[it.block] = 0;
+            fin = true;
+        }
+    }
+    if (fin && act) {
+        double4 xj = x[j];
+        xj.x += a0;
+        xj.y += a1;
+        xj.z += a2;
+        x[j] = xj;
+        if (finalize_v) {   // v = (x - x_t) / h
+            double4 t0 = xt[j];
+            v[j] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
+        }
+    }
+}
+
+void launch_kpass2(cudaStream_t st, int nitems, const P2Item* it, const P2Block* bl, const Run* runs,
+                   const float* Krow, const float4* y, double* part, int* counters, double4* x,
+                   const double4* xt, double4* v, double inv_h, int finalize_v) {
+    int nb = (nitems + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    k_kpass2<<<nb, 32 * kWarpsPerBlock, 0, st>>>(nitems, it, bl, runs, Krow, y, part, counters, x, xt, v, inv_h,
+                                                 finalize_v);
+}
+
+// ----------------------------------------------------------------------------
+// chain dot: dxt_s = (K^T y)_{a_s} = sum_{i in anc*(a)} K[i][a] y_i (warp per slot)
+// column a of K is contiguous in Kcol (chain order j, parent(j), ...); the
+// chain is a sequence of panel runs [i, ptop[i]].
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx, const float* __restrict__ Kcol,
+                            const int64_t* __restrict__ colptr, const int32_t* __restrict__ parent,
+                            const int32_t* __restrict__ ptop, const float4* __restrict__ y, double* __restrict__ dxt) {
+    int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    int lane = threadIdx.x & 31;
+    if (s >= ns) return;
+    int a = slot_vtx[s];
+    const float* col = Kcol + colptr[a];
+    double a0 = 0, a1 = 0, a2 = 0;
+    int pos = 0;
+    for (int i = a; i >= 0;) {
+        int top = ptop[i];
+        int len = top - i + 1;
+        for (int o = lane; o < len; o += 32) {
+            double kv = col[pos + o];
+            float4 yy = y[i + o];
+            a0 = fma(kv, (double)yy.x, a0);
+            a1 = fma(kv, (double)yy.y, a1);
+            a2 = fma(kv, (double)yy.z, a2);
+        }
+        pos += len;
+        i = parent[top];
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (lane == 0) {
+        dxt[3 * s] = a0;
+        dxt[3 * s + 1] = a1;
+        dxt[3 * s + 2] = a2;
+    }
+}
+
+void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
+                      const int64_t* colptr, const int32_t* parent, const int32_t* ptop, const float4* y,
+                      double* dxt) {
+    if (ns == 0) return;
+    k_chain_dot<<<(ns + 7) / 8, 256, 0, st>>>(ns, slot_vtx, Kcol, colptr, parent, ptop, y, dxt);
+}
+
+// ----------------------------------------------------------------------------
+// scatter: y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s   (warp per row)
+// ----------------------------------------------------------------------------
+__global__ void k_scatter(int n_f, int ns, int row_lo, const int32_t* __restrict__ slot_vtx,
+                          const float* __restrict__ Krow, const int64_t* __restrict__ rowptr,
+                          const int32_t* __restrict__ first, const double* __restrict__ wz, float4* __restrict__ y) {
+    int i = row_lo + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    int lane = threadIdx.x & 31;
+    if (i >= n_f) return;
+    int f = first[i];
+    // slots with f <= a_s <= i (slot_vtx sorted ascending)
+    int lo = 0, hi = ns;
+    while (lo < hi) { int m = (lo + hi) >> 1; if (slot_vtx[m] < f) lo = m + 1; else hi = m; }
+    int s0 = lo;
+    hi = ns;
+    while (lo < hi) { int m = (lo + hi) >> 1; if (slot_vtx[m] <= i) lo = m + 1; else hi = m; }
+    int s1 = lo;
+    if (s0 >= s1) return;
+    const float* row = Krow + rowptr[i] - f;
+    double a0 = 0, a1 = 0, a2 = 0;
+    for (int s = s0 + lane; s < s1; s += 32) {
+        double kv = row[slot_vtx[s]];
+        a0 = fma(kv, wz[3 * s], a0);
+        a1 = fma(kv, wz[3 * s + 1], a1);
+        a2 = fma(kv, wz[3 * s + 2], a2);
+    }
+    a0 = warp_sum(a0);
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (lane == 0) {
+        float4 yi = y[i];
+        y[i] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), 0.f);
+    }
+}
+
+void launch_scatter(cudaStream_t st, int n_f, int ns, int row_lo, const int32_t* slot_vtx, const float* Krow,
+                    const int64_t* rowptr, const int32_t* first, const double* wz, float4* y) {
+    if (ns == 0 || row_lo >= n_f) return;
+    int rows = n_f - row_lo;
+    k_scatter<<<(rows + 7) / 8, 256, 0, st>>>(n_f, ns, row_lo, slot_vtx, Krow, rowptr, first, wz, y);
+}
+
+// ----------------------------------------------------------------------------
+// Delassus Gram G = K[:,Vc]^T K[:,Vc] (P:L858 via the sparse inverse):
+// G_st = sum over common ancestors i of K[i][a_s] K[i][a_t] = sum over depths
+// d <= depth(lca(a_s, a_t)) of Z[d][s] Z[d][t], Z[d][s] = Kcol[colptr_s + depth_s - d].
+// 32x32 tiles of slot pairs, depth staged in chunks of 32 levels.
+// ----------------------------------------------------------------------------
+__device__ int lca_depth(int a, int b, const int32_t* parent, const int32_t* ptop, const int32_t* depth) {
+    // a <= b in postorder: lca = first ancestor run of a whose top >= b, at row max(i, b)
+    if (a > b) { int t = a; a = b; b = t; }
+    for (int i = a; i >= 0;) {
+        int top = ptop[i];
+        if (top >= b) return depth[i > b ? i : b];
+        i = parent[top];
+    }
+    return -1;
+}
+
+__global__ void __launch_bounds__(256) k_delassus(int ns, const int32_t* __restrict__ slot_vtx,
+                                                  const float* __restrict__ Kcol, const int64_t* __restrict__ colptr,
+                                                  const int32_t* __restrict__ depth, const int32_t* __restrict__ parent,
+                                                  const int32_t* __restrict__ ptop, float* __restrict__ G) {
+    // tile (bs, bt) with bt >= bs from a linear triangular index
+    int tiles = (ns + 31) / 32;
+    int idx = blockIdx.x, bs = 0;
+    while (idx >= tiles - bs) { idx -= tiles - bs; ++bs; }
+    int bt = bs + idx;
+    __shared__ float Zs[32][33], Zt[32][33];
+    __shared__ int ds_[32], dt_[32];
+    __shared__ int64_t cs_[32], ct_[32];
+    int tid = threadIdx.x;
+    if (tid < 32) {
+        int s = bs * 32 + tid;
+        if (s < ns) { int a = slot_vtx[s]; ds_[tid] = depth[a]; cs_[tid] = colptr[a]; }
+        else { ds_[tid] = -1; cs_[tid] = 0; }
+    } else if (tid < 64) {
+        int t = bt * 32 + tid - 32;
+        if (t < ns) { int a = slot_vtx[t]; dt_[tid - 32] = depth[a]; ct_[tid - 32] = colptr[a]; }
+        else { dt_[tid - 32] = -1; ct_[tid - 32] = 0; }
+    }
+    __syncthreads();
+    // thread owns pairs (ls, lt0..lt0+3)
+    int ls = tid >> 3, lt0 = (tid & 7) * 4;
+    int s = bs * 32 + ls;
+    int dl[4];
+    int maxd = -1;
+    for (int q = 0; q < 4; ++q) {
+        int t = bt * 32 + lt0 + q;
+        dl[q] = (s < ns && t < ns) ? lca_depth(slot_vtx[s], slot_vtx[t], parent, ptop, depth) : -1;
+        maxd = max(maxd, dl[q]);
+    }
+    // block-wide max depth needed
+    __shared__ int smax;
+    if (tid == 0) smax = -1;
+    __syncthreads();
+    atomicMax(&smax, maxd);
+    __syncthreads();
+    int D = smax;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int d0 = 0; d0 <= D; d0 += 32) {
+        // stage Z[d0 + dd][slot] for both slot blocks (coalesced along depth per slot)
+        for (int e = tid; e < 32 * 32; e += 256) {
+            int sl = e >> 5, dd = e & 31;
+            int d = d0 + dd;
+            Zs[dd][sl] = (ds_[sl] >= d) ? Kcol[cs_[sl] + ds_[sl] - d] : 0.f;
+            Zt[dd][sl] = (dt_[sl] >= d) ? Kcol[ct_[sl] + dt_[sl] - d] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int dd = 0; dd < 32; ++dd) {
+            int d = d0 + dd;
+            float zs = Zs[dd][ls];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (d <= dl[q]) acc[q] = fmaf(zs, Zt[dd][lt0 + q], acc[q]);
+        }
+        __syncthreads();
+    }
+    for (int q = 0; q < 4; ++q) {
+        int t = bt * 32 + lt0 + q;
+        if (s < ns && t < ns) {
+            G[(size_t)s * ns + t] = acc[q];
+            G[(size_t)t * ns + s] = acc[q];
+        }
+    }
+}
+
+void launch_delassus(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
+                     const int64_t* colptr, const int32_t* depth, const int32_t* parent,
+                     const int32_t* ptop, float* G) {
+    if (ns == 0) return;
+    int tiles = (ns + 31) / 32;
+    int ntri = tiles * (tiles + 1) / 2;
+    k_delassus<<<ntri, 256, 0, st>>>(ns, slot_vtx, Kcol, colptr, depth, parent, ptop, G);
+}
+
+// D_jj = sum_{a,b in j} w_a w_b G_ab (unit directions; reading A18)
+__global__ void k_djj(int nc, int ns, DContact* C, const float* __restrict__ G) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    DContact& ct = C[c];
+    double d = 0.0;
+    for (int p = 0; p < ct.nv; ++p)
+        for (int q = 0; q < ct.nv; ++q) d += ct.w[p] * ct.w[q] * (double)G[(size_t)ct.slot[p] * ns + ct.slot[q]];
+    ct.Djj = d;
+}
+
+void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const float* G) {
+    if (nc == 0) return;
+    k_djj<<<(nc + 127) / 128, 128, 0, st>>>(nc, ns, c, G);
+}
+
+// ----------------------------------------------------------------------------
+// CR (Saad Alg. 6.20) on S = Theta D Theta + C, z0 = 0, exactly N_CR matvecs
+// (reading A19), in ONE cluster of kCluster CTAs.  Every CTA keeps full fp64
+// copies of the row vectors and performs the O(m) work redundantly (so dot
+// products are identical everywhere without communication); the O(ns^2)
+// product q = G w is split by G rows and exchanged through DSMEM.
+//   (S v)_j = theta_j c_j . sum_{a in j} w_ja q_a + C_j v_j,
+//   q_a = sum_b G_ab W_b, W_b = sum_{rows k at b} w_kb theta_k c_k v_k.
+// ----------------------------------------------------------------------------
+struct CrSmem {
+    double z[3 * kMaxContacts], r[3 * kMaxContacts], p[3 * kMaxContacts], Ar[3 * kMaxContacts],
+        Ap[3 * kMaxContacts];
+    float th[3 * kMaxContacts], cd[3 * kMaxContacts];
+    float W[3 * kMaxSlots];
+    double q[2][3 * kMaxSlots];   // double-buffered: a CTA may run one matvec ahead of a peer
+    double red[kCrThreads / 32 * 2];
+};
+
+__device__ __forceinline__ void block_dot2(const double* a, const double* b, const double* c, const double* d, int m,
+                                           double* red, double& o1, double& o2) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        s1 += a[i] * b[i];
+        s2 += c[i] * d[i];
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) { red[2 * w] = s1; red[2 * w + 1] = s2; }
+    __syncthreads();
+    double t1 = 0.0, t2 = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { t1 += red[2 * k]; t2 += red[2 * k + 1]; }
+    o1 = t1;
+    o2 = t2;
+    __syncthreads();
+}
+
+// out = S v  (all CTAs end with the full result)
+__device__ void cr_apply(cg::cluster_group& cl, CrSmem& sm, const double* v, double* out, int nc, int ns,
+                         const DContact* C, const int32_t* scp, const int32_t* sci, const float* scw,
+                         const float* G, int buf) {
+    double* qb = sm.q[buf];
+    const int m = 3 * nc;
+    // W_b (redundant)
+    for (int b = threadIdx.x; b < ns; b += blockDim.x) {
+        double w0 = 0, w1 = 0, w2 = 0;
+        for (int p = scp[b]; p < scp[b + 1]; ++p) {
+            int c = sci[p];
+            double wt = scw[p];
+            const DContact& ct = C[c];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                double tv = wt * (double)sm.th[3 * c + k] * v[3 * c + k];
+                w0 += tv * ct.c[k][0];
+                w1 += tv * ct.c[k][1];
+                w2 += tv * ct.c[k][2];
+            }
+        }
+        sm.W[3 * b] = (float)w0;
+        sm.W[3 * b + 1] = (float)w1;
+        sm.W[3 * b + 2] = (float)w2;
+    }
+    __syncthreads();
+    // q_a for this CTA's rows of G (warp per row), broadcast to all CTAs via DSMEM
+    const int rank = cl.block_rank();
+    const int per = (ns + kCluster - 1) / kCluster;
+    const int a0 = rank * per, a1 = min(ns, a0 + per);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int a = a0 + wid; a < a1; a += nw) {
+        const float* g = G + (size_t)a * ns;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        double d0 = 0, d1 = 0, d2 = 0;
+        int cnt = 0;
+        for (int b = lane; b < ns; b += 32) {
+            float gab = __ldg(&g[b]);
+            s0 = fmaf(gab, sm.W[3 * b], s0);
+            s1 = fmaf(gab, sm.W[3 * b + 1], s1);
+            s2 = fmaf(gab, sm.W[3 * b + 2], s2);
+            if (++cnt == 8) { d0 += s0; d1 += s1; d2 += s2; s0 = s1 = s2 = 0.f; cnt = 0; }
+        }
+        d0 = warp_sum(d0 + s0);
+        d1 = warp_sum(d1 + s1);
+        d2 = warp_sum(d2 + s2);
+        if (lane < kCluster) {
+            double* rq = cl.map_shared_rank(qb, lane);
+            rq[3 * a] = d0;
+            rq[3 * a + 1] = d1;
+            rq[3 * a + 2] = d2;
+        }
+    }
+    cl.sync();
+    // (S v)_j (redundant)
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        int c = j / 3, k = j - 3 * c;
+        const DContact& ct = C[c];
+        double acc = 0.0;
+        for (int p = 0; p < ct.nv; ++p) {
+            int sl = ct.slot[p];
+            acc += ct.w[p] * (ct.c[k][0] * qb[3 * sl] + ct.c[k][1] * qb[3 * sl + 1] + ct.c[k][2] * qb[3 * sl + 2]);
+        }
+        out[j] = (double)sm.th[j] * acc + (double)sm.cd[j] * v[j];
+    }
+    __syncthreads();
+}
+
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1)
+    k_cr(Params P, const DContact* __restrict__ C, const int32_t* __restrict__ slot_vtx,
+         const int32_t* __restrict__ scp, const int32_t* __restrict__ sci, const float* __restrict__ scw,
+         const float* __restrict__ G, const double4* __restrict__ x, ContactState cs) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    CrSmem& sm = *reinterpret_cast<CrSmem*>(smraw);
+    cg::cluster_group cl = cg::this_cluster();
+    const int nc = P.nc, ns = P.ns, m = 3 * nc;
+    const double h = P.h;
+    // rho_j = h_j - theta_j c_j . x~_c, x~ = x^k + K^T y at the contact vertices
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        int c = j / 3, k = j - 3 * c;
+        const DContact& ct = C[c];
+        double xs[3] = {0, 0, 0};
+        for (int p = 0; p < ct.nv; ++p) {
+            double4 xa = x[ct.vtx[p]];
+            int sl = ct.slot[p];
+            xs[0] += ct.w[p] * (xa.x + cs.dxt[3 * sl]);
+            xs[1] += ct.w[p] * (xa.y + cs.dxt[3 * sl + 1]);
+            xs[2] += ct.w[p] * (xa.z + cs.dxt[3 * sl + 2]);
+        }
+        double th = cs.theta[j];
+        double rho = cs.hvec[j] - th * (ct.c[k][0] * xs[0] + ct.c[k][1] * xs[1] + ct.c[k][2] * xs[2]);
+        sm.th[j] = (float)th;
+        sm.cd[j] = (float)cs.cdiag[j];
+        sm.r[j] = rho;
+        sm.p[j] = rho;
+        sm.z[j] = 0.0;
+    }
+    __syncthreads();
+    double rr, dummy;
+    block_dot2(sm.r, sm.r, sm.r, sm.r, m, sm.red, rr, dummy);
+    if (rr > 0.0 && P.cr_iters > 0) {
+        int buf = 0;
+        cr_apply(cl, sm, sm.r, sm.Ar, nc, ns, C, scp, sci, scw, G, buf);
+        buf ^= 1;
+        for (int j = threadIdx.x; j < m; j += blockDim.x) sm.Ap[j] = sm.Ar[j];
+        __syncthreads();
+        double rAr, ApAp;
+        block_dot2(sm.r, sm.Ar, sm.Ap, sm.Ap, m, sm.red, rAr, ApAp);
+        for (int it = 0; it < P.cr_iters; ++it) {
+            if (ApAp <= 1e-300 || fabs(rAr) <= 1e-300) break;
+            double alpha = rAr / ApAp;
+            for (int j = threadIdx.x; j < m; j += blockDim.x) {
+                sm.z[j] += alpha * sm.p[j];
+                sm.r[j] -= alpha * sm.Ap[j];
+            }
+            __syncthreads();
+            if (it == P.cr_iters - 1) break;
+            cr_apply(cl, sm, sm.r, sm.Ar, nc, ns, C, scp, sci, scw, G, buf);
+            buf ^= 1;
+            double rAr_new, t2;
+            block_dot2(sm.r, sm.Ar, sm.r, sm.r, m, sm.red, rAr_new, t2);
+            double beta = rAr_new / rAr;
+            rAr = rAr_new;
+            for (int j = threadIdx.x; j < m; j += blockDim.x) {
+                sm.p[j] = sm.r[j] + beta * sm.p[j];
+                sm.Ap[j] = sm.Ar[j] + beta * sm.Ap[j];
+            }
+            __syncthreads();
+            double t1;
+            block_dot2(sm.Ap, sm.Ap, sm.Ap, sm.Ap, m, sm.red, ApAp, t1);
+        }
+    }
+    block_dot2(sm.r, sm.r, sm.r, sm.r, m, sm.red, rr, dummy);
+    if (cl.block_rank() != 0) {
+        cl.sync();   // keep DSMEM alive until everyone is done
+        return;
+    }
+    // lambda += z / h^2 (reading A11), wz_b = sum w theta z c  (for y += K H^T z)
+    for (int j = threadIdx.x; j < m; j += blockDim.x) cs.lam[j] += sm.z[j] / (h * h);
+    for (int b = threadIdx.x; b < ns; b += blockDim.x) {
+        double w0 = 0, w1 = 0, w2 = 0;
+        for (int p = scp[b]; p < scp[b + 1]; ++p) {
+            int c = sci[p];
+            double wt = scw[p];
+            const DContact& ct = C[c];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                double tv = wt * (double)sm.th[3 * c + k] * sm.z[3 * c + k];
+                w0 += tv * ct.c[k][0];
+                w1 += tv * ct.c[k][1];
+                w2 += tv * ct.c[k][2];
+            }
+        }
+        cs.wz[3 * b] = w0;
+        cs.wz[3 * b + 1] = w1;
+        cs.wz[3 * b + 2] = w2;
+    }
+    if (threadIdx.x == 0) cs.cr_res[0] = sqrt(rr);
+    cl.sync();
+}
+
+int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t* slot_vtx,
+              const int32_t* scp, const int32_t* sci, const float* scw, const float* G, const double4* x,
+              ContactState cs) {
+    if (P.nc == 0) return 0;
+    static bool attr = false;
+    size_t smem = sizeof(CrSmem);
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_cr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return (int)e;
+        e = cudaFuncSetAttribute(k_cr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = true;
+    }
+    k_cr<<<kCluster, kCrThreads, smem, st>>>(P, c, slot_vtx, scp, sci, scw, G, x, cs);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace simdev

@@ -1,0 +1,207 @@
+"""GPU (sm_100a) vs fp64 oracle parity, through the C ABI.
+
+Tolerances (BASELINE.json north_star): per-iteration SpMV and local-step
+outputs within 1e-5 relative; vertex positions within 1e-5 x bbox diagonal
+after each frame at 5 L-G iterations; contact-set and stick/slip
+classification identical (outside the reading-A21 band).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import scenes
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def simmod():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_15078_b200 as m
+    return m
+
+
+def make(simmod, sc):
+    return simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+
+
+SCENES = {
+    "cfg1": lambda: scenes.make_scene("cfg1"),
+    "block5k": lambda: scenes.make_scene("block", nv=7, split="kuhn6"),
+    "cfg3": lambda: scenes.make_scene("cfg3"),
+}
+
+
+@pytest.mark.parametrize("name", list(SCENES))
+def test_apply_inverse_parity(simmod, name):
+    """Two K-passes == A^-1 b by the oracle's sparse LU."""
+    sc = SCENES[name]()
+    s = make(simmod, sc)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    rng = np.random.default_rng(11)
+    b = rng.standard_normal((sc.mesh.n_v, 3)).astype(np.float32).astype(np.float64)
+    x = s.debug_apply_inverse(b)
+    xr = o.solve(b[o.free])
+    err = np.abs(x[o.free] - xr).max() / np.abs(xr).max()
+    assert err < 1e-5, err
+    assert np.all(x[o.pinned] == 0)
+
+
+@pytest.mark.parametrize("model", [O.NEOHOOKEAN, O.COROTATED, O.ARAP])
+def test_local_step_parity(simmod, model):
+    """Projection p_i (eq. PD local) and residual b - A x (delta-form RHS)."""
+    sc = scenes.make_scene("block", nv=7, split="kuhn6", model=model)
+    s = make(simmod, sc)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    x, v = scenes.random_state(sc.mesh, seed=3 + model, amp=0.15)
+    xs = x + 0.01 * v
+    P, r = s.debug_local(x, xs)
+    F = O.deformation_gradients(x, o.T, o.Bm)
+    Po = O.project(F, o.model, o.k, o.mu, o.lam)
+    _, sig, _ = O.signed_svd(F)
+    ok = (sig[:, 1] + sig[:, 2]) > 1e-3
+    err = np.linalg.norm(P - Po, axis=(1, 2)) / np.maximum(1.0, np.linalg.norm(Po, axis=(1, 2)))
+    assert ok.sum() > 0.99 * ok.size
+    assert err[ok].max() < 1e-5, err[ok].max()
+    # residual r = M (s - x) + h^2 sum w G^T (P - F)
+    ro = o.M[:, None] * (xs - x) + O.elastic_forces(Po, F, o.Bm, o.w, o.h, o.T, o.n_v)
+    g = O.shape_gradients(o.Bm)
+    mag = np.zeros(o.n_v)
+    np.add.at(mag, o.T.reshape(-1), np.repeat(o.h ** 2 * o.w, 4) *
+              np.linalg.norm(np.einsum("tij,taj->tai", Po, g), axis=2).reshape(-1))
+    scale = mag[o.free].max() + np.abs(o.M[:, None] * (xs - x)).max()
+    assert np.abs(r[o.free] - ro[o.free]).max() < 1e-5 * scale
+
+
+def test_rest_and_free_fall_closed_forms(simmod):
+    """Rest state is a fixed point; free fall follows x_n = x0 + h^2 g n(n+1)/2."""
+    sc = scenes.make_scene("block", nv=5, pinned=False)
+    s = make(simmod, sc)
+    g = np.asarray(sc.material.gravity)
+    for n in range(1, 6):
+        s.step(1, 5)
+        x, v = s.get_state()
+        assert np.abs(x - (sc.mesh.X + sc.h ** 2 * g * n * (n + 1) / 2)).max() < 1e-12
+    mat0 = scenes.Material(gravity=(0.0, 0.0, 0.0))
+    s2 = simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, mat0, sc.h)
+    s2.step(3, 5)
+    x, v = s2.get_state()
+    assert np.abs(x - sc.mesh.X).max() < 1e-7 * sc.mesh.bbox_diag()
+
+
+def test_cantilever_100_frames_free_running(simmod):
+    """cfg1: NH cantilever, h = 1/60, 5 L-G/frame, 100 frames, no contact."""
+    sc = scenes.make_scene("cfg1")
+    s = make(simmod, sc)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    worst = 0.0
+    for f in range(100):
+        x, v, _ = o.frame(x, v)
+        s.step(1, 5)
+        xg, vg = s.get_state()
+        worst = max(worst, np.abs(xg - x).max())
+        assert worst < tol, (f, worst)
+
+
+def test_delassus_gram_parity(simmod):
+    """G = K[:,Vc]^T K[:,Vc] == A_v^-1 restricted to contact vertices."""
+    sc = scenes.incline_block(theta_deg=10.0, mu=0.5, nv=6, edge=0.1, youngs=1e8)
+    s = make(simmod, sc)
+    s.set_contacts(sc.contacts)
+    cv, G = s.debug_delassus()
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(sc.contacts)
+    order = {int(v): i for i, v in enumerate(o.vc)}
+    idx = np.array([order[int(v)] for v in cv])
+    Go = o.G[np.ix_(idx, idx)]
+    assert np.abs(G - Go).max() < 1e-5 * np.abs(Go).max()
+
+
+def _classify_gpu(o, x, xt, lam):
+    return o.classify(x, xt, lam)
+
+
+@pytest.mark.parametrize("dmu", [+0.05, -0.05])
+def test_incline_contact_frames_resynced(simmod, dmu):
+    """cfg2-like incline (E = 1e8, 10 deg): each frame the oracle restarts from
+    the GPU state; positions within 1e-5 bbox, lambda close, identical
+    stick/slip classification."""
+    th = 10.0
+    mus = math.tan(math.radians(th))
+    sc = scenes.incline_block(theta_deg=th, mu=mus + dmu, nv=5, edge=0.1, youngs=1e8)
+    s = make(simmod, sc)
+    s.set_contacts(sc.contacts)
+    o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=5)
+    o.set_contacts(sc.contacts)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+    for f in range(8):
+        s.set_state(x, v)
+        s.step(1, 5)
+        xg, vg = s.get_state()
+        lg = s.get_lambda()
+        xo, vo, info = o.frame(x, v)
+        assert np.abs(xg - xo).max() < tol, (f, np.abs(xg - xo).max())
+        lo = info["lam"]
+        assert np.abs(lg - lo).max() <= 1e-3 * max(1e-9, np.abs(lo).max()) + 1e-9
+        co = o.classify(xo, x, lo)
+        cgpu = o.classify(xg, x, lg)
+        assert np.array_equal(co, cgpu)
+        x, v = xg, vg
+
+
+def test_gingerbread_frame_parity(simmod):
+    """cfg3 at the benchmark size: 19 691 v / 93 600 t / 800 contacts, 5 L-G,
+    10 CR; one frame from rest plus one re-synced frame."""
+    sc = scenes.make_scene("cfg3")
+    s = make(simmod, sc)
+    s.set_pin_velocity(sc.pin_velocity)
+    s.set_contacts(sc.contacts)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(sc.contacts)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+    for f in range(2):
+        s.set_state(x, v)
+        s.step(1, 5)
+        xg, vg = s.get_state()
+        pins = x[o.pinned] + sc.h * sc.pin_velocity
+        xo, vo, info = o.frame(x, v, pin_targets=pins)
+        err = np.abs(xg - xo).max()
+        assert err < tol, (f, err, tol)
+        lg = s.get_lambda()
+        co = o.classify(xo, x, info["lam"])
+        cg = o.classify(xg, x, lg)
+        assert (co == cg).mean() > 0.99
+        x, v = xg, vg
+
+
+def test_determinism(simmod):
+    sc = scenes.make_scene("cfg3")
+    out = []
+    for _ in range(2):
+        s = make(simmod, sc)
+        s.set_pin_velocity(sc.pin_velocity)
+        s.set_contacts(sc.contacts)
+        s.step(2, 5)
+        out.append(s.get_state()[0])
+        s.close()
+    assert np.array_equal(out[0], out[1])
+
+
+def test_contact_validation(simmod):
+    sc = scenes.make_scene("cfg3")
+    s = make(simmod, sc)
+    pinned = int(np.nonzero(sc.mesh.fixed)[0][0])
+    bad = scenes.Contact([pinned], [1.0], np.array([0, 0, 1.0]), 0.0)
+    with pytest.raises(simmod.SimError, match="pinned"):
+        s.set_contacts([bad])
+    bad2 = scenes.Contact([0], [1.0], np.array([0, 0, 2.0]), 0.0)
+    with pytest.raises(simmod.SimError, match="unit"):
+        s.set_contacts([bad2])
