@@ -128,7 +128,10 @@ int sim_build_sparse_inverse(sim_handle *h, double drop_tolerance);
 
 /* Replace the contact set (n may be 0).  Builds rows, uploads them and
  * computes on the device G = K[:,Vc]^T K[:,Vc], the Delassus diagonal and the
- * preconditioner r_n = h^2 D_jj, r_f = h D_jj.  Limit: n <= 1024. */
+ * preconditioner r_n = h^2 D_jj, r_f = h D_jj.  Limits: n <= 1024 contacts on
+ * <= 1024 distinct vertices, and the CR cluster's fp64 working set
+ * 184 n + 72 n_vertices bytes must fit 227 KB (about 900 single-vertex
+ * contacts); SIM_E_LIMIT otherwise. */
 int sim_set_contacts(sim_handle *h, const sim_contact *contacts, int32_t n);
 
 /* Advance `frames` frames of `iterations` local-global iterations each
@@ -192,6 +195,14 @@ int sim_debug_local(sim_handle *h, const double *x, const double *s, float *P, d
 /* G = K[:,Vc]^T K[:,Vc] for the current contact set: returns the contact
  * vertex list (original ids) and G (row-major, n_cv x n_cv). */
 int sim_debug_get_delassus(sim_handle *h, int32_t *cv, float *G, int32_t capacity);
+
+/* Contact scratch of the most recent L-G iteration (after sim_step):
+ * theta, C diagonal and h-vector per row ([3 * n_contacts], rows n, t1, t2;
+ * bilateral contacts pad rows 1-2 with theta 0, C 1), dxt = (A^-1 r) at each
+ * contact vertex ([n_cv][3]), the contact vertices (original ids, [n_cv]) and
+ * D_jj per contact ([n_contacts]).  Any pointer may be NULL. */
+int sim_debug_contact_state(sim_handle *h, double *theta, double *cdiag, double *hvec, double *dxt,
+                            int32_t *slot_vertex, double *djj);
 
 #ifdef __cplusplus
 }

@@ -546,6 +546,7 @@ class Oracle:
                 # x^{k+1} = A^-1 (b + h^2 H^T lambda^{k+1})
                 xn = x.copy()
                 xn[F_] = self.solve(b_f + h * h * self.JT(theta * lam)[F_])
+                info["theta_last"] = theta
                 if capture:
                     rec.update(theta=theta, E=E, phi=phi, rho=rho, z=z, cr_res=res,
                                x_tilde=xt)

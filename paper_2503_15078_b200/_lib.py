@@ -16,7 +16,7 @@ EXPORTED_SYMBOLS = [
     "sim_synchronize", "sim_set_pin_velocity", "sim_get_state", "sim_set_state", "sim_get_lambda",
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
-    "sim_get_kernel_times",
+    "sim_get_kernel_times", "sim_debug_contact_state",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2"]
 
@@ -79,6 +79,7 @@ def _load():
         "sim_debug_get_delassus": [H, ip, fp, C.c_int32],
         "sim_set_profiling": [H, C.c_int],
         "sim_get_kernel_times": [H, dp, C.c_int32],
+        "sim_debug_contact_state": [H, dp, dp, dp, dp, ip, dp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -254,3 +255,16 @@ class Sim:
         _check(lib.sim_debug_get_delassus(self._h, cv.ctypes.data_as(C.POINTER(C.c_int32)),
                                           G.ctypes.data_as(C.POINTER(C.c_float)), max(1, ns)))
         return cv[:ns], G[:ns, :ns]
+
+
+def debug_contact_state(sim):
+    """Contact scratch of the last L-G iteration (see sim_debug_contact_state)."""
+    st = sim.stats()
+    nc, ns = int(st["n_contacts"]), int(st["n_contact_vertices"])
+    th, cd, hv = np.empty(3 * nc), np.empty(3 * nc), np.empty(3 * nc)
+    dxt = np.empty((max(1, ns), 3))
+    sv = np.empty(max(1, ns), np.int32)
+    djj = np.empty(max(1, nc))
+    _check(lib.sim_debug_contact_state(sim._h, _dptr(th), _dptr(cd), _dptr(hv), _dptr(dxt),
+                                       sv.ctypes.data_as(C.POINTER(C.c_int32)), _dptr(djj)))
+    return {"theta": th, "cdiag": cd, "hvec": hv, "dxt": dxt[:ns], "slot_vertex": sv[:ns], "djj": djj[:nc]}

@@ -90,14 +90,13 @@ struct sim_handle {
     DBuf<int32_t> adjp, adj;
     // device: K
     DBuf<float> Krow, Kcol;
-    DBuf<int64_t> rowptr, colptr, cb;
-    DBuf<int32_t> first, depth, parent, ptop;
+    DBuf<int64_t> colptr;
+    DBuf<int32_t> cb, depth, parent, ptop, cover;
+    DBuf<int2> meta;                 // {rowptr[i] - first[i], first[i]}
     DBuf<P1Item> p1;
     DBuf<P1Block> p1b;
-    DBuf<P2Item> p2;
     DBuf<P2Block> p2b;
-    DBuf<Run> runs;
-    DBuf<double> part1, part2;
+    DBuf<double> part1;
     DBuf<int> counters;
     // contacts
     int nc = 0, ns = 0, row_lo = 0;
@@ -107,9 +106,15 @@ struct sim_handle {
     DBuf<int32_t> slot_vtx, scp, sci, vcp, vci;
     DBuf<float> scw, vcw, G;
     DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res;
+    DBuf<int32_t> chain_off, chain_rows;
+    DBuf<uint8_t> flag;
+    DBuf<int> ucount;
+    DBuf<int4> ulist;
+    DBuf<float> Zc;
+    int contact_gen = 0;
     // graph
     cudaGraphExec_t gexec = nullptr;
-    int g_iters = -1, g_nc = -1, g_ns = -1, g_prof = -1;
+    int g_iters = -1, g_nc = -1, g_ns = -1, g_prof = -1, g_gen = -1;
     // in-graph kernel timing (event record nodes between kernels)
     int profiling = 0;
     std::vector<cudaEvent_t> pev;
@@ -206,10 +211,11 @@ extern "C" void sim_destroy(sim_handle* H) {
         if (H->gexec) cudaGraphExecDestroy(H->gexec);
         H->x.release(); H->xt.release(); H->v.release(); H->s.release(); H->M.release();
         H->tet.release(); H->Bm.release(); H->hw2.release(); H->fc.release(); H->u.release(); H->y.release();
-        H->adjp.release(); H->adj.release(); H->Krow.release(); H->Kcol.release(); H->rowptr.release();
-        H->colptr.release(); H->cb.release(); H->first.release(); H->depth.release(); H->parent.release();
-        H->ptop.release(); H->p1.release(); H->p1b.release(); H->p2.release(); H->p2b.release();
-        H->runs.release(); H->part1.release(); H->part2.release(); H->counters.release();
+        H->adjp.release(); H->adj.release(); H->Krow.release(); H->Kcol.release(); H->meta.release();
+        H->colptr.release(); H->cb.release(); H->cover.release(); H->depth.release(); H->parent.release();
+        H->ptop.release(); H->p1.release(); H->p1b.release(); H->p2b.release();
+        H->part1.release(); H->counters.release();
+        H->chain_off.release(); H->chain_rows.release(); H->flag.release(); H->ucount.release(); H->ulist.release(); H->Zc.release();
         H->dc.release(); H->slot_vtx.release(); H->scp.release(); H->sci.release(); H->vcp.release();
         H->vci.release(); H->scw.release(); H->vcw.release(); H->G.release(); H->lam.release();
         H->theta.release(); H->cdiag.release(); H->hvec.release(); H->hl.release(); H->dxt.release();
@@ -293,24 +299,25 @@ static int upload_all(sim_handle* H) {
     const simhost::Inverse& K = H->K;
     CK(H->Krow.alloc(K.nnz)); CK(H->Krow.upload(K.Krow.data(), K.nnz, st));
     CK(H->Kcol.alloc(K.nnz)); CK(H->Kcol.upload(K.Kcol.data(), K.nnz, st));
-    CK(H->rowptr.alloc(nf + 1)); CK(H->rowptr.upload(K.rowptr.data(), nf + 1, st));
+    std::vector<int32_t> cb(nf);
+    std::vector<int2> meta(nf);
+    for (int j = 0; j < nf; ++j) {
+        cb[j] = (int32_t)(K.colptr[j] + K.depth[j]);
+        meta[j] = make_int2((int32_t)(K.rowptr[j] - K.first[j]), K.first[j]);
+    }
     CK(H->colptr.alloc(nf + 1)); CK(H->colptr.upload(K.colptr.data(), nf + 1, st));
-    std::vector<int64_t> cb(nf);
-    for (int j = 0; j < nf; ++j) cb[j] = K.colptr[j] + K.depth[j];
     CK(H->cb.alloc(nf)); CK(H->cb.upload(cb.data(), nf, st));
-    CK(H->first.alloc(nf)); CK(H->first.upload(K.first.data(), nf, st));
+    CK(H->meta.alloc(nf)); CK(H->meta.upload(meta.data(), nf, st));
     CK(H->depth.alloc(nf)); CK(H->depth.upload(K.depth.data(), nf, st));
     CK(H->parent.alloc(nf)); CK(H->parent.upload(K.parent.data(), nf, st));
     CK(H->ptop.alloc(nf)); CK(H->ptop.upload(K.ptop.data(), nf, st));
     const simhost::WorkLists& W = H->wl;
     CK(H->p1.alloc(W.p1.size())); CK(H->p1.upload(W.p1.data(), W.p1.size(), st));
     CK(H->p1b.alloc(W.p1b.size())); CK(H->p1b.upload(W.p1b.data(), W.p1b.size(), st));
-    CK(H->p2.alloc(W.p2.size())); CK(H->p2.upload(W.p2.data(), W.p2.size(), st));
     CK(H->p2b.alloc(W.p2b.size())); CK(H->p2b.upload(W.p2b.data(), W.p2b.size(), st));
-    CK(H->runs.alloc(W.runs.size())); CK(H->runs.upload(W.runs.data(), W.runs.size(), st));
+    CK(H->cover.alloc(W.cover.size())); CK(H->cover.upload(W.cover.data(), W.cover.size(), st));
     CK(H->part1.alloc((size_t)std::max(1, W.p1_parts) * 32 * 3));
-    CK(H->part2.alloc((size_t)std::max(1, W.p2_parts) * 32 * 3));
-    size_t ncnt = W.p1b.size() + W.p2b.size();
+    size_t ncnt = W.p1b.size();
     CK(H->counters.alloc(ncnt));
     CK(cudaMemsetAsync(H->counters.p, 0, ncnt * sizeof(int), st));
     // contact buffers at capacity (pointers stay fixed for graph reuse)
@@ -326,6 +333,8 @@ static int upload_all(sim_handle* H) {
     CK(H->lam.alloc(3 * kMaxContacts)); CK(H->theta.alloc(3 * kMaxContacts)); CK(H->cdiag.alloc(3 * kMaxContacts));
     CK(H->hvec.alloc(3 * kMaxContacts)); CK(H->hl.alloc(3 * kMaxContacts)); CK(H->dxt.alloc(3 * kMaxSlots));
     CK(H->wz.alloc(3 * kMaxSlots)); CK(H->phi_abs.alloc(kMaxContacts)); CK(H->cr_res.alloc(1));
+    CK(H->chain_off.alloc(kMaxSlots + 1)); CK(H->flag.alloc(nf)); CK(H->ucount.alloc(2)); CK(H->ulist.alloc(nf));
+    CK(cudaMemsetAsync(H->ucount.p, 0, 2 * sizeof(int), st));
     CK(cudaMemsetAsync(H->lam.p, 0, 3 * kMaxContacts * sizeof(double), st));
     CK(cudaMemsetAsync(H->vcp.p, 0, (nf + 1) * sizeof(int32_t), st));
     CK(cudaMemsetAsync(H->cr_res.p, 0, sizeof(double), st));
@@ -364,7 +373,9 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     H->nnzL = (int64_t)F.Lp[nf];
     int nthr = (int)std::max(1u, std::thread::hardware_concurrency());
     simhost::sparse_inverse(F, drop_tol, H->K, nthr);
-    simhost::build_worklists(H->K, H->wl, 256, 256);
+    if (H->K.nnz >= (int64_t)INT32_MAX)
+        return fail(SIM_E_LIMIT, "nnz(K) = %lld exceeds the int32 offset limit", (long long)H->K.nnz);
+    simhost::build_worklists(H->K, H->wl, 1024);
     H->n_f = nf;
     H->int2orig.assign(nv, -1);
     H->orig2int.assign(nv, -1);
@@ -451,6 +462,9 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
     std::sort(verts.begin(), verts.end());
     verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
     if ((int)verts.size() > kMaxSlots) return fail(SIM_E_LIMIT, "at most %d contact vertices", kMaxSlots);
+    if (cr_smem_bytes(n, (int)verts.size()) > kCrMaxSmem)
+        return fail(SIM_E_LIMIT, "%d contacts on %d vertices exceed the CR cluster's shared memory (%zu > %zu B)", n,
+                    (int)verts.size(), cr_smem_bytes(n, (int)verts.size()), kCrMaxSmem);
     const int ns = (int)verts.size();
     std::vector<int32_t> slot_of(H->n_f, -1);
     for (int s = 0; s < ns; ++s) slot_of[verts[s]] = s;
@@ -482,6 +496,21 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
     H->h2d_contact_bytes = (int64_t)(n * sizeof(DContact) + ns * sizeof(int32_t) + (ns + 1) * sizeof(int32_t) +
                                      2 * sci.size() * (sizeof(int32_t) + sizeof(float)) +
                                      (H->n_f + 1) * sizeof(int32_t));
+    // ancestor chains of the contact vertices (for chain_dot / scatter)
+    std::vector<int32_t> coff(ns + 1, 0);
+    for (int s = 0; s < ns; ++s) coff[s + 1] = coff[s] + H->K.depth[verts[s]] + 1;
+    if ((size_t)coff[ns] > H->chain_rows.n) {
+        CK(cudaStreamSynchronize(st));
+        CK(H->chain_rows.alloc(std::max<size_t>(coff[ns], 2 * H->chain_rows.n)));
+        CK(H->Zc.alloc(H->chain_rows.n));
+        H->contact_gen++;
+    }
+    CK(H->chain_off.upload(coff.data(), ns + 1, st));
+    CK(cudaMemsetAsync(H->flag.p, 0, H->n_f, st));
+    CK(cudaMemsetAsync(H->ucount.p, 0, 2 * sizeof(int), st));
+    launch_chain_rows(st, ns, H->slot_vtx.p, H->chain_off.p, H->parent.p, H->ptop.p, H->chain_rows.p, H->flag.p);
+    launch_ulist(st, H->n_f, ns, H->flag.p, H->slot_vtx.p, H->meta.p, H->ucount.p, H->ulist.p, H->Krow.p, H->Zc.p);
+    H->h2d_contact_bytes += (ns + 1) * sizeof(int32_t);
     // Delassus Gram and D_jj on the device
     launch_delassus(st, ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
     launch_djj(st, n, ns, H->dc.p, H->G.p);
@@ -551,22 +580,23 @@ static int enqueue_frame(sim_handle* H, int iters) {
         launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, H->x.p, H->fc.p, nullptr); nk++;
         MARK(KK_GATHER);
         launch_gather(st, P, H->adjp.p, H->adj.p, H->fc.p, H->M.p, H->x.p, H->s.p, con ? H->vcp.p : nullptr,
-                      H->vci.p, H->vcw.p, H->hl.p, H->u.p, nullptr); nk++;
+                      H->vci.p, H->vcw.p, H->hl.p, H->cb.p, H->u.p, nullptr); nk++;
         MARK(KK_KPASS1);
-        launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->Kcol.p, H->cb.p, H->depth.p, H->u.p, H->y.p,
+        launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->Kcol.p, H->depth.p, H->u.p, H->y.p,
                       H->part1.p, H->counters.p); nk++;
         if (con) {
             MARK(KK_CHAIN);
-            launch_chain_dot(st, H->ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->parent.p, H->ptop.p, H->y.p, H->dxt.p); nk++;
+            launch_chain_dot(st, H->ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
+                             H->y.p, H->dxt.p); nk++;
             MARK(KK_CR);
             int e = launch_cr(st, P, H->dc.p, H->slot_vtx.p, H->scp.p, H->sci.p, H->scw.p, H->G.p, H->x.p, cs); nk++;
             if (e) return -e;
             MARK(KK_SCATTER);
-            launch_scatter(st, H->n_f, H->ns, H->row_lo, H->slot_vtx.p, H->Krow.p, H->rowptr.p, H->first.p, H->wz.p, H->y.p); nk++;
+            launch_scatter(st, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
         }
         MARK(KK_KPASS2);
-        launch_kpass2(st, (int)H->wl.p2.size(), H->p2.p, H->p2b.p, H->runs.p, H->Krow.p, H->y.p, H->part2.p,
-                      H->counters.p + H->wl.p1b.size(), H->x.p, H->xt.p, H->v.p, 1.0 / H->h, k == iters - 1); nk++;
+        launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->meta.p, H->Krow.p, H->y.p, H->x.p, H->xt.p,
+                      H->v.p, 1.0 / H->h, k == iters - 1); nk++;
     }
     MARK(KK_N);
 #undef MARK
@@ -600,7 +630,8 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     if (H->state != 1) return fail(SIM_E_STATE, "build the sparse inverse first");
     if (frames < 0 || iters < 1) return fail(SIM_E_INVALID, "frames >= 0 and iterations >= 1");
     if (frames == 0) return SIM_OK;
-    if (!H->gexec || H->g_iters != iters || H->g_nc != H->nc || H->g_ns != H->ns || H->g_prof != H->profiling) {
+    if (!H->gexec || H->g_iters != iters || H->g_nc != H->nc || H->g_ns != H->ns || H->g_prof != H->profiling ||
+        H->g_gen != H->contact_gen) {
         if (H->gexec) {
             cudaGraphExecDestroy(H->gexec);
             H->gexec = nullptr;
@@ -618,6 +649,7 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
         H->g_nc = H->nc;
         H->g_ns = H->ns;
         H->g_prof = H->profiling;
+        H->g_gen = H->contact_gen;
         H->kernels_per_frame = nk;
     }
     for (int f = 0; f < frames; ++f) CK(cudaGraphLaunch(H->gexec, H->stream));
@@ -762,7 +794,10 @@ extern "C" int sim_debug_apply_inverse(sim_handle* H, const double* b, double* x
     std::vector<float4> hu(nf);
     for (int k = 0; k < nf; ++k) {
         int o = H->int2orig[k];
-        hu[k] = make_float4((float)b[3 * o], (float)b[3 * o + 1], (float)b[3 * o + 2], 0.f);
+        int32_t cbk = (int32_t)(H->K.colptr[k] + H->K.depth[k]);
+        float cbf;
+        memcpy(&cbf, &cbk, sizeof cbf);
+        hu[k] = make_float4((float)b[3 * o], (float)b[3 * o + 1], (float)b[3 * o + 2], cbf);
     }
     DBuf<double4> dx;
     CK(dx.alloc(nf));
@@ -770,10 +805,10 @@ extern "C" int sim_debug_apply_inverse(sim_handle* H, const double* b, double* x
     CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(H->u.p, hu.data(), nf * sizeof(float4), cudaMemcpyHostToDevice));
     CK(cudaMemset(dx.p, 0, nf * sizeof(double4)));
-    launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->Kcol.p, H->cb.p, H->depth.p, H->u.p, H->y.p,
+    launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->Kcol.p, H->depth.p, H->u.p, H->y.p,
                   H->part1.p, H->counters.p);
-    launch_kpass2(st, (int)H->wl.p2.size(), H->p2.p, H->p2b.p, H->runs.p, H->Krow.p, H->y.p, H->part2.p,
-                  H->counters.p + H->wl.p1b.size(), dx.p, nullptr, nullptr, 1.0, 0);
+    launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->meta.p, H->Krow.p, H->y.p, dx.p, nullptr,
+                  nullptr, 1.0, 0);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     std::vector<double4> hx(nf);
@@ -810,7 +845,7 @@ extern "C" int sim_debug_local(sim_handle* H, const double* x, const double* s, 
     Params P = make_params(H);
     launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, dx.p, H->fc.p, dP.p);
     launch_gather(st, P, H->adjp.p, H->adj.p, H->fc.p, H->M.p, dx.p, ds.p, nullptr, nullptr, nullptr, nullptr,
-                  H->u.p, dr.p);
+                  H->cb.p, H->u.p, dr.p);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     if (Pout) CK(cudaMemcpy(Pout, dP.p, (size_t)9 * nt * sizeof(float), cudaMemcpyDeviceToHost));
@@ -834,5 +869,26 @@ extern "C" int sim_debug_get_delassus(sim_handle* H, int32_t* cv, float* G, int3
     CK(cudaStreamSynchronize(H->stream));
     if (cv) for (int s = 0; s < H->ns; ++s) cv[s] = H->int2orig[H->slot_vtx_h[s]];
     if (G && H->ns) CK(cudaMemcpy(G, H->G.p, (size_t)H->ns * H->ns * sizeof(float), cudaMemcpyDeviceToHost));
+    return SIM_OK;
+}
+
+// contact scratch of the last evaluated L-G iteration: per row (3 per contact)
+// theta, C diagonal, h-vector; per slot dxt = (K^T y) at the slot vertex; slot vertices
+extern "C" int sim_debug_contact_state(sim_handle* H, double* theta, double* cdiag, double* hvec, double* dxt,
+                                       int32_t* slot_vertex, double* djj) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
+    CK(cudaStreamSynchronize(H->stream));
+    size_t m = 3 * (size_t)H->nc;
+    if (theta && m) CK(cudaMemcpy(theta, H->theta.p, m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (cdiag && m) CK(cudaMemcpy(cdiag, H->cdiag.p, m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (hvec && m) CK(cudaMemcpy(hvec, H->hvec.p, m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (dxt && H->ns) CK(cudaMemcpy(dxt, H->dxt.p, 3 * (size_t)H->ns * sizeof(double), cudaMemcpyDeviceToHost));
+    if (slot_vertex) for (int s = 0; s < H->ns; ++s) slot_vertex[s] = H->int2orig[H->slot_vtx_h[s]];
+    if (djj && H->nc) {
+        std::vector<DContact> hc(H->nc);
+        CK(cudaMemcpy(hc.data(), H->dc.p, H->nc * sizeof(DContact), cudaMemcpyDeviceToHost));
+        for (int c = 0; c < H->nc; ++c) djj[c] = hc[c].Djj;
+    }
     return SIM_OK;
 }

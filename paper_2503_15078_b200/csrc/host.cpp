@@ -379,17 +379,17 @@ void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads)
     }
 }
 
-void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols, int p2_chunk_rows) {
+void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols) {
     int n = K.n;
     wl = WorkLists();
-    // ---- pass 1: per panel, 32-row blocks, column chunks of the block's range
+    // ---- pass 1: per panel, 32-row blocks, column chunks of the block's range [f, r0 + nr)
     int npan = (int)K.panel_start.size() - 1;
     for (int p = 0; p < npan; ++p) {
         int rs = K.panel_start[p], re = K.panel_start[p + 1];
         int f = K.first[rs];
         for (int r0 = rs; r0 < re; r0 += 32) {
             int nr = std::min(32, re - r0);
-            int cend = r0 + nr;   // columns [f, r0+nr)
+            int cend = r0 + nr;
             P1Block b{r0, nr, 0, wl.p1_parts};
             int bi = (int)wl.p1b.size();
             for (int c0 = f; c0 < cend; c0 += p1_chunk_cols) {
@@ -401,74 +401,30 @@ void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols, int p2_
             wl.p1b.push_back(b);
         }
     }
-    // ---- pass 2: 32-column blocks; cover rows grouped in per-panel runs
-    std::vector<int32_t> mark(n, -1);
-    std::vector<int32_t> cover;
-    for (int c0 = 0; c0 < n; c0 += 32) {
-        int nc = std::min(32, n - c0);
-        int bi = (int)wl.p2b.size();
-        cover.clear();
-        for (int j = c0; j < c0 + nc; ++j)
-            for (int i = j; i != -1 && mark[i] != bi; i = K.parent[i]) {
-                mark[i] = bi;
-                cover.push_back(i);
-            }
-        std::sort(cover.begin(), cover.end());
-        // runs
-        std::vector<Run> runs;
-        for (size_t q = 0; q < cover.size();) {
-            int r0 = cover[q];
-            size_t e = q;
-            while (e + 1 < cover.size() && cover[e + 1] == cover[e] + 1 &&
-                   K.panel_of[cover[e + 1]] == K.panel_of[r0])
-                ++e;
-            int r1 = cover[e];
-            runs.push_back(Run{r0, r1, K.first[r0], 0, K.rowptr[r0] - K.first[r0]});
-            q = e + 1;
-        }
-        // chunk runs into items of ~p2_chunk_rows rows (split long runs)
-        P2Block b{c0, nc, 0, wl.p2_parts};
-        int acc = 0;
-        int run_begin = (int)wl.runs.size();
-        for (auto& R : runs) {
-            int r = R.r0;
-            while (r <= R.r1) {
-                int take = std::min(R.r1 - r + 1, p2_chunk_rows - acc);
-                Run piece{r, r + take - 1, R.first, 0, K.rowptr[r] - R.first};
-                wl.runs.push_back(piece);
-                acc += take;
-                r += take;
-                if (acc >= p2_chunk_rows) {
-                    wl.p2.push_back(P2Item{c0, nc, run_begin, (int)wl.runs.size(), bi, wl.p2_parts + b.nitems});
-                    b.nitems++;
-                    run_begin = (int)wl.runs.size();
-                    acc = 0;
-                }
-            }
-        }
-        if (acc > 0) {
-            wl.p2.push_back(P2Item{c0, nc, run_begin, (int)wl.runs.size(), bi, wl.p2_parts + b.nitems});
-            b.nitems++;
-        }
-        wl.p2_parts += b.nitems;
-        wl.p2b.push_back(b);
-    }
     // heavy items first (longest-processing-time order); partial slots are fixed per item
     std::stable_sort(wl.p1.begin(), wl.p1.end(), [](const P1Item& a, const P1Item& b) {
         return (int64_t)a.nrows * (a.c1 - a.c0) > (int64_t)b.nrows * (b.c1 - b.c0);
     });
-    auto rows_of = [&](const P2Item& it) {
-        int64_t s = 0;
-        for (int q = it.run0; q < it.run1; ++q) s += wl.runs[q].r1 - wl.runs[q].r0 + 1;
-        return s;
-    };
-    std::vector<std::pair<int64_t, int>> key(wl.p2.size());
-    for (size_t q = 0; q < wl.p2.size(); ++q) key[q] = {rows_of(wl.p2[q]), (int)q};
-    std::stable_sort(key.begin(), key.end(), [](auto& a, auto& b) { return a.first > b.first; });
-    std::vector<P2Item> sorted;
-    sorted.reserve(wl.p2.size());
-    for (auto& k : key) sorted.push_back(wl.p2[k.second]);
-    wl.p2.swap(sorted);
+    // ---- pass 2: 32-column blocks with their sorted cover rows
+    std::vector<int32_t> mark(n, -1);
+    std::vector<int32_t> cov;
+    std::vector<std::pair<int64_t, P2Block>> blocks;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        int nc = std::min(32, n - c0);
+        int bi = c0 / 32;
+        cov.clear();
+        for (int j = c0; j < c0 + nc; ++j)
+            for (int i = j; i != -1 && mark[i] != bi; i = K.parent[i]) {
+                mark[i] = bi;
+                cov.push_back(i);
+            }
+        std::sort(cov.begin(), cov.end());
+        P2Block b{c0, nc, (int)wl.cover.size(), (int)(wl.cover.size() + cov.size())};
+        wl.cover.insert(wl.cover.end(), cov.begin(), cov.end());
+        blocks.push_back({(int64_t)cov.size(), b});
+    }
+    std::stable_sort(blocks.begin(), blocks.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    for (auto& b : blocks) wl.p2b.push_back(b.second);
 }
 
 }  // namespace simhost

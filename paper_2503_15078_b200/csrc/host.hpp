@@ -71,22 +71,22 @@ struct Inverse {
 // K = L^-1 (fp64 compute, fp32 store); drop |K_ij| < tol |K_jj| (tol > 0)
 void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads);
 
-// ---------------- K-pass work lists (one warp per item) ---------------------
-struct P1Item { int32_t r0, nrows, c0, c1, block, part; };   // rows [r0,r0+nrows) x cols [c0,c1)
+// ---------------- K-pass work lists (one CTA per item) ----------------------
+// pass 1 (y = K u, column-major K): item = (<= 32 rows of one panel) x (<= 1024 columns)
+struct P1Item { int32_t r0, nrows, c0, c1, block, part; };
 struct P1Block { int32_t r0, nrows, nitems, part0; };
-struct P2Item { int32_t c0, ncols, run0, run1, block, part; };  // cols [c0,c0+ncols) x runs[run0,run1)
-struct P2Block { int32_t c0, ncols, nitems, part0; };
-struct Run { int32_t r0, r1, first, pad; int64_t rowbase; };      // rows [r0,r1] of one panel
+// pass 2 (x += K^T y, row-major K): one item per 32-column block, its cover rows
+// (rows i >= c0 with first(i) <= c0 + 31) in cover[list0, list1)
+struct P2Block { int32_t c0, ncols, list0, list1; };
 
 struct WorkLists {
     std::vector<P1Item> p1;
     std::vector<P1Block> p1b;
-    std::vector<P2Item> p2;
     std::vector<P2Block> p2b;
-    std::vector<Run> runs;
-    int p1_parts = 0, p2_parts = 0;
+    std::vector<int32_t> cover;
+    int p1_parts = 0;
 };
 
-void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols, int p2_chunk_rows);
+void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols);
 
 }  // namespace simhost

@@ -398,7 +398,8 @@ __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32
                          const float4* __restrict__ fc, const double* __restrict__ M, const double4* __restrict__ x,
                          const double4* __restrict__ s, const int32_t* __restrict__ vcp,
                          const int32_t* __restrict__ vci, const float* __restrict__ vcw,
-                         const double* __restrict__ hl, float4* __restrict__ u, double* __restrict__ resid) {
+                         const double* __restrict__ hl, const int32_t* __restrict__ cb, float4* __restrict__ u,
+                         double* __restrict__ resid) {
     int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= P.n_f) return;
     double4 xa = x[a], sa = s[a];
@@ -430,227 +431,206 @@ __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32
             r2 += hh * w * hl[3 * c + 2];
         }
     }
-    u[a] = make_float4((float)r0, (float)r1, (float)r2, 0.f);
+    u[a] = make_float4((float)r0, (float)r1, (float)r2, __int_as_float(cb[a]));
 }
 
 void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
                    const float4* fc, const double* M, const double4* x, const double4* s,
                    const int32_t* vcp, const int32_t* vci, const float* vcw, const double* hl,
-                   float4* u, double* resid_dbg) {
-    k_gather<<<(P.n_f + 255) / 256, 256, 0, st>>>(P, adjp, adj, fc, M, x, s, vcp, vci, vcw, hl, u, resid_dbg);
+                   const int32_t* cb, float4* u, double* resid_dbg) {
+    k_gather<<<(P.n_f + 255) / 256, 256, 0, st>>>(P, adjp, adj, fc, M, x, s, vcp, vci, vcw, hl, cb, u, resid_dbg);
 }
 
 // ----------------------------------------------------------------------------
-// K-pass 1: y = K u.  One warp per item = (32 rows of one panel) x (column chunk).
-// K is column-major: K[r][j] = Kcol[cb[j] - depth[r]], cb[j] = colptr[j] + depth[j];
-// within a panel depth[r0 + l] = depth[r0] - l, so lanes read consecutive words.
+// K-pass 1: y = K u.  One CTA (8 warps) per item = (<= 32 rows of one panel) x
+// (<= 1024 columns); warps take interleaved 32-column chunks, lane = row.
+// K is column-major: K[r][j] = Kcol[cb[j] - depth[r]], cb[j] = colptr[j] + depth[j]
+// (carried in u[j].w); inside a panel depth[r0 + l] = depth[r0] - l, so the 32
+// lanes read 32 consecutive words of column j.
 // ----------------------------------------------------------------------------
-__device__ __forceinline__ bool last_of_block(int* counter, int nitems) {
-    __threadfence();
-    __syncwarp();
-    int old = 0;
-    if ((threadIdx.x & 31) == 0) old = atomicAdd(counter, 1);
-    old = __shfl_sync(0xffffffffu, old, 0);
-    bool last = old == nitems - 1;
-    if (last) __threadfence();
-    return last;
-}
+constexpr int kWarps = 8;
 
-constexpr int kWarpsPerBlock = 8;
-
-__global__ void __launch_bounds__(256) k_kpass1(int nitems, const P1Item* __restrict__ items,
-                                                const P1Block* __restrict__ blocks, const float* __restrict__ Kcol,
-                                                const int64_t* __restrict__ cb, const int32_t* __restrict__ depth,
-                                                const float4* __restrict__ u, float4* __restrict__ y,
-                                                double* __restrict__ part, int* __restrict__ counters) {
-    __shared__ int64_t s_cb[kWarpsPerBlock][32];
-    __shared__ float4 s_u[kWarpsPerBlock][32];
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int w = blockIdx.x * kWarpsPerBlock + wib;
-    if (w >= nitems) return;
-    const P1Item it = items[w];
-    const int r = it.r0 + lane;
-    const bool act = lane < it.nrows;
-    const int64_t base = (int64_t)lane - depth[it.r0];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int jc = it.c0; jc < it.c1; jc += 32) {
-        int j = jc + lane;
-        if (j < it.c1) {
-            s_cb[wib][lane] = __ldg(&cb[j]);
-            s_u[wib][lane] = __ldg(&u[j]);
-        }
-        __syncwarp();
-        const int nj = min(32, it.c1 - jc);
-        float kv[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            kv[q] = 0.f;
-            if (q < nj && act && jc + q <= r) kv[q] = __ldcs(&Kcol[s_cb[wib][q] + base]);
-        }
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            float4 uq = s_u[wib][q];
-            double kq = (double)kv[q];
-            a0 = fma(kq, (double)uq.x, a0);
-            a1 = fma(kq, (double)uq.y, a1);
-            a2 = fma(kq, (double)uq.z, a2);
-        }
-        __syncwarp();
-    }
-    const P1Block b = blocks[it.block];
-    if (b.nitems == 1) {
-        if (act) y[r] = make_float4((float)a0, (float)a1, (float)a2, 0.f);
-        return;
-    }
-    double* pp = part + ((size_t)it.part * 32 + lane) * 3;
-    pp[0] = a0;
-    pp[1] = a1;
-    pp[2] = a2;
-    if (last_of_block(&counters[it.block], b.nitems)) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-        for (int q = 0; q < b.nitems; ++q) {
-            const double* pq = part + ((size_t)(b.part0 + q) * 32 + lane) * 3;
-            s0 += __ldcg(pq);
-            s1 += __ldcg(pq + 1);
-            s2 += __ldcg(pq + 2);
-        }
-        if (act) y[r] = make_float4((float)s0, (float)s1, (float)s2, 0.f);
-        if (lane == 0) counters[it.block] = 0;
-    }
-}
-
-void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* Kcol,
-                   const int64_t* cb, const int32_t* depth, const float4* u, float4* y, double* part,
-                   int* counters) {
-    int nb = (nitems + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    k_kpass1<<<nb, 32 * kWarpsPerBlock, 0, st>>>(nitems, it, bl, Kcol, cb, depth, u, y, part, counters);
-}
-
-// ----------------------------------------------------------------------------
-// K-pass 2: x += K^T y.  One warp per item = (32 columns) x (runs of cover rows).
-// K is row-major: K[r][j] = Krow[rowbase(r) + j], rowbase(r) = rowptr[r] - first(r);
-// inside a run (one panel, shared first f) rowbase(r+1) = rowbase(r) + r - f + 1.
-// ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_kpass2(int nitems, const P2Item* __restrict__ items,
-                                                const P2Block* __restrict__ blocks, const Run* __restrict__ runs,
-                                                const float* __restrict__ Krow, const float4* __restrict__ y,
-                                                double* __restrict__ part, int* __restrict__ counters,
-                                                double4* __restrict__ x, const double4* __restrict__ xt,
-                                                double4* __restrict__ v, double inv_h, int finalize_v) {
-    __shared__ float4 s_y[kWarpsPerBlock][32];
-    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int w = blockIdx.x * kWarpsPerBlock + wib;
-    if (w >= nitems) return;
-    const P2Item it = items[w];
-    const int j = it.c0 + lane;
-    const bool act = lane < it.ncols;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int q = it.run0; q < it.run1; ++q) {
-        const Run R = runs[q];
-        const int f = R.first;
-        const bool colok = act && j >= f;
-        for (int rc = R.r0; rc <= R.r1; rc += 32) {
-            int rr = rc + lane;
-            if (rr <= R.r1) s_y[wib][lane] = __ldg(&y[rr]);
-            __syncwarp();
-            const int nr = min(32, R.r1 - rc + 1);
-            // rowbase(rc + q) = rowbase(rc) + q (rc - f + 1) + q (q - 1) / 2
-            const int64_t rb0 = R.rowbase + (int64_t)(rc - R.r0) * (R.r0 - f + 1) +
-                                (int64_t)(rc - R.r0) * (rc - R.r0 - 1) / 2 + j;
-            const int64_t step0 = rc - f + 1;
-            float kv[32];
-#pragma unroll
-            for (int qq = 0; qq < 32; ++qq) {
-                kv[qq] = 0.f;
-                if (qq < nr && colok && j <= rc + qq)
-                    kv[qq] = __ldcs(&Krow[rb0 + (int64_t)qq * step0 + (int64_t)qq * (qq - 1) / 2]);
-            }
-#pragma unroll
-            for (int qq = 0; qq < 32; ++qq) {
-                float4 yq = s_y[wib][qq];
-                double kq = (double)kv[qq];
-                a0 = fma(kq, (double)yq.x, a0);
-                a1 = fma(kq, (double)yq.y, a1);
-                a2 = fma(kq, (double)yq.z, a2);
-            }
-            __syncwarp();
-        }
-    }
-    const P2Block b = blocks[it.block];
-    bool fin = false;
-    if (b.nitems == 1) {
-        fin = true;
-    } else {
-        double* pp = part + ((size_t)it.part * 32 + lane) * 3;
-        pp[0] = a0;
-        pp[1] = a1;
-        pp[2] = a2;
-        if (last_of_block(&counters[it.block], b.nitems)) {
-            a0 = a1 = a2 = 0.0;
-            for (int q = 0; q < b.nitems; ++q) {
-                const double* pq = part + ((size_t)(b.part0 + q) * 32 + lane) * 3;
-                a0 += __ldcg(pq);
-                a1 += __ldcg(pq + 1);
-                a2 += __ldcg(pq + 2);
-            }
-            if (lane == 0) counters[it.block] = 0;
-            fin = true;
-        }
-    }
-    if (fin && act) {
-        double4 xj = x[j];
-        xj.x += a0;
-        xj.y += a1;
-        xj.z += a2;
-        x[j] = xj;
-        if (finalize_v) {   // v = (x - x_t) / h
-            double4 t0 = xt[j];
-            v[j] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
-        }
-    }
-}
-
-void launch_kpass2(cudaStream_t st, int nitems, const P2Item* it, const P2Block* bl, const Run* runs,
-                   const float* Krow, const float4* y, double* part, int* counters, double4* x,
-                   const double4* xt, double4* v, double inv_h, int finalize_v) {
-    int nb = (nitems + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    k_kpass2<<<nb, 32 * kWarpsPerBlock, 0, st>>>(nitems, it, bl, runs, Krow, y, part, counters, x, xt, v, inv_h,
-                                                 finalize_v);
-}
-
-// ----------------------------------------------------------------------------
-// chain dot: dxt_s = (K^T y)_{a_s} = sum_{i in anc*(a)} K[i][a] y_i (warp per slot)
-// column a of K is contiguous in Kcol (chain order j, parent(j), ...); the
-// chain is a sequence of panel runs [i, ptop[i]].
-// ----------------------------------------------------------------------------
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
-__global__ void k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx, const float* __restrict__ Kcol,
-                            const int64_t* __restrict__ colptr, const int32_t* __restrict__ parent,
-                            const int32_t* __restrict__ ptop, const float4* __restrict__ y, double* __restrict__ dxt) {
-    int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    int lane = threadIdx.x & 31;
-    if (s >= ns) return;
-    int a = slot_vtx[s];
-    const float* col = Kcol + colptr[a];
-    double a0 = 0, a1 = 0, a2 = 0;
-    int pos = 0;
-    for (int i = a; i >= 0;) {
-        int top = ptop[i];
-        int len = top - i + 1;
-        for (int o = lane; o < len; o += 32) {
-            double kv = col[pos + o];
-            float4 yy = y[i + o];
-            a0 = fma(kv, (double)yy.x, a0);
-            a1 = fma(kv, (double)yy.y, a1);
-            a2 = fma(kv, (double)yy.z, a2);
+__global__ void __launch_bounds__(256) k_kpass1(const P1Item* __restrict__ items, const P1Block* __restrict__ blocks,
+                                                const float* __restrict__ Kcol, const int32_t* __restrict__ depth,
+                                                const float4* __restrict__ u, float4* __restrict__ y,
+                                                double* __restrict__ part, int* __restrict__ counters) {
+    __shared__ float4 s_u[kWarps][32];
+    __shared__ double s_red[kWarps][3][32];
+    __shared__ int s_last;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const P1Item it = items[blockIdx.x];
+    const int r = it.r0 + lane;
+    const bool act = lane < it.nrows;
+    const int base = lane - depth[it.r0];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int jc = it.c0 + 32 * w; jc < it.c1; jc += 32 * kWarps) {
+        const int j = jc + lane;
+        s_u[w][lane] = j < it.c1 ? __ldg(&u[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncwarp();
+        const int nj = min(32, it.c1 - jc);
+        float kv[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const float4 uq = s_u[w][q];
+            kv[q] = (q < nj && act && jc + q <= r) ? __ldg(&Kcol[__float_as_int(uq.w) + base]) : 0.f;
         }
-        pos += len;
-        i = parent[top];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const float4 uq = s_u[w][q];
+            const double kq = (double)kv[q];
+            a0 = fma(kq, (double)uq.x, a0);
+            a1 = fma(kq, (double)uq.y, a1);
+            a2 = fma(kq, (double)uq.z, a2);
+        }
+        __syncwarp();
+    }
+    s_red[w][0][lane] = a0;
+    s_red[w][1][lane] = a1;
+    s_red[w][2][lane] = a2;
+    __syncthreads();
+    if (w != 0) return;
+    a0 = a1 = a2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) {
+        a0 += s_red[q][0][lane];
+        a1 += s_red[q][1][lane];
+        a2 += s_red[q][2][lane];
+    }
+    const P1Block b = blocks[it.block];
+    if (b.nitems == 1) {
+        if (act) y[r] = make_float4((float)a0, (float)a1, (float)a2, 0.f);
+        return;
+    }
+    double* pp = part + ((size_t)it.part * 3) * 32 + lane;
+    pp[0] = a0;
+    pp[32] = a1;
+    pp[64] = a2;
+    __threadfence();
+    __syncwarp();
+    int old = 0;
+    if (lane == 0) old = atomicAdd(&counters[it.block], 1);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != b.nitems - 1) return;
+    __threadfence();
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int q = 0; q < b.nitems; ++q) {
+        const double* pq = part + ((size_t)(b.part0 + q) * 3) * 32 + lane;
+        s0 += __ldcg(pq);
+        s1 += __ldcg(pq + 32);
+        s2 += __ldcg(pq + 64);
+    }
+    if (act) y[r] = make_float4((float)s0, (float)s1, (float)s2, 0.f);
+    if (lane == 0) counters[it.block] = 0;
+}
+
+void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* Kcol,
+                   const int32_t* depth, const float4* u, float4* y, double* part, int* counters) {
+    k_kpass1<<<nitems, 32 * kWarps, 0, st>>>(it, bl, Kcol, depth, u, y, part, counters);
+}
+
+// ----------------------------------------------------------------------------
+// K-pass 2: x += K^T y.  One CTA per 32-column block (lane = column), warps
+// take interleaved 32-row chunks of the block's cover rows.  K is row-major:
+// K[r][j] = Krow[rb(r) + j], rb(r) = rowptr[r] - first(r) (meta[r] = {rb, first}).
+// No partial sums, no atomics: the CTA owns its 32 columns.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_kpass2(const P2Block* __restrict__ blocks, const int32_t* __restrict__ cover,
+                                                const int2* __restrict__ meta, const float* __restrict__ Krow,
+                                                const float4* __restrict__ y, double4* __restrict__ x,
+                                                const double4* __restrict__ xt, double4* __restrict__ v, double inv_h,
+                                                int finalize_v) {
+    __shared__ int s_rb[kWarps][32], s_f[kWarps][32], s_r[kWarps][32];
+    __shared__ float4 s_y[kWarps][32];
+    __shared__ double s_red[kWarps][3][32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const P2Block b = blocks[blockIdx.x];
+    const int j = b.c0 + lane;
+    const bool act = lane < b.ncols;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int k0 = b.list0 + 32 * w; k0 < b.list1; k0 += 32 * kWarps) {
+        const int k = k0 + lane;
+        if (k < b.list1) {
+            const int r = __ldg(&cover[k]);
+            const int2 m = __ldg(&meta[r]);
+            s_r[w][lane] = r;
+            s_rb[w][lane] = m.x;
+            s_f[w][lane] = m.y;
+            s_y[w][lane] = __ldg(&y[r]);
+        } else {
+            s_y[w][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncwarp();
+        const int n = min(32, b.list1 - k0);
+        float kv[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+            kv[q] = (q < n && act && j >= s_f[w][q] && j <= s_r[w][q]) ? __ldg(&Krow[s_rb[w][q] + j]) : 0.f;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const float4 yq = s_y[w][q];
+            const double kq = (double)kv[q];
+            a0 = fma(kq, (double)yq.x, a0);
+            a1 = fma(kq, (double)yq.y, a1);
+            a2 = fma(kq, (double)yq.z, a2);
+        }
+        __syncwarp();
+    }
+    s_red[w][0][lane] = a0;
+    s_red[w][1][lane] = a1;
+    s_red[w][2][lane] = a2;
+    __syncthreads();
+    if (w != 0 || !act) return;
+    a0 = a1 = a2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) {
+        a0 += s_red[q][0][lane];
+        a1 += s_red[q][1][lane];
+        a2 += s_red[q][2][lane];
+    }
+    double4 xj = x[j];
+    xj.x += a0;
+    xj.y += a1;
+    xj.z += a2;
+    x[j] = xj;
+    if (finalize_v) {   // v = (x - x_t) / h
+        const double4 t0 = xt[j];
+        v[j] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
+    }
+}
+
+void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const int2* meta,
+                   const float* Krow, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
+                   int finalize_v) {
+    k_kpass2<<<nblocks, 32 * kWarps, 0, st>>>(bl, cover, meta, Krow, y, x, xt, v, inv_h, finalize_v);
+}
+
+// ----------------------------------------------------------------------------
+// chain dot: dxt_s = (K^T y)_{a_s} = sum_{k} Kcol[colptr_a + k] y[chain_rows[off_s + k]]
+// (column a of K is contiguous in Kcol; its rows are a's ancestor chain)
+// ----------------------------------------------------------------------------
+__global__ void k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx, const float* __restrict__ Kcol,
+                            const int64_t* __restrict__ colptr, const int32_t* __restrict__ chain_off,
+                            const int32_t* __restrict__ chain_rows, const float4* __restrict__ y,
+                            double* __restrict__ dxt) {
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s >= ns) return;
+    const int a = slot_vtx[s];
+    const float* col = Kcol + colptr[a];
+    const int o0 = chain_off[s], len = chain_off[s + 1] - o0;
+    double a0 = 0, a1 = 0, a2 = 0;
+    for (int k = lane; k < len; k += 32) {
+        const double kv = __ldg(&col[k]);
+        const float4 yy = __ldg(&y[__ldg(&chain_rows[o0 + k])]);
+        a0 = fma(kv, (double)yy.x, a0);
+        a1 = fma(kv, (double)yy.y, a1);
+        a2 = fma(kv, (double)yy.z, a2);
     }
     a0 = warp_sum(a0);
     a1 = warp_sum(a1);
@@ -663,52 +643,109 @@ __global__ void k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx, const 
 }
 
 void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
-                      const int64_t* colptr, const int32_t* parent, const int32_t* ptop, const float4* y,
-                      double* dxt) {
+                      const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
+                      const float4* y, double* dxt) {
     if (ns == 0) return;
-    k_chain_dot<<<(ns + 7) / 8, 256, 0, st>>>(ns, slot_vtx, Kcol, colptr, parent, ptop, y, dxt);
+    k_chain_dot<<<(ns + 7) / 8, 256, 0, st>>>(ns, slot_vtx, Kcol, colptr, chain_off, chain_rows, y, dxt);
 }
 
-// ----------------------------------------------------------------------------
-// scatter: y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s   (warp per row)
-// ----------------------------------------------------------------------------
-__global__ void k_scatter(int n_f, int ns, int row_lo, const int32_t* __restrict__ slot_vtx,
-                          const float* __restrict__ Krow, const int64_t* __restrict__ rowptr,
-                          const int32_t* __restrict__ first, const double* __restrict__ wz, float4* __restrict__ y) {
-    int i = row_lo + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    int lane = threadIdx.x & 31;
-    if (i >= n_f) return;
-    int f = first[i];
-    // slots with f <= a_s <= i (slot_vtx sorted ascending)
+// per-contact-set: chain rows of every slot (walk panel runs) + row flags
+__global__ void k_chain_rows(int ns, const int32_t* __restrict__ slot_vtx, const int32_t* __restrict__ chain_off,
+                             const int32_t* __restrict__ parent, const int32_t* __restrict__ ptop,
+                             int32_t* __restrict__ chain_rows, uint8_t* __restrict__ flag) {
+    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s >= ns) return;
+    int pos = chain_off[s];
+    for (int i = slot_vtx[s]; i >= 0;) {
+        const int top = ptop[i];
+        const int len = top - i + 1;
+        for (int o = lane; o < len; o += 32) {
+            chain_rows[pos + o] = i + o;
+            flag[i + o] = 1;
+        }
+        pos += len;
+        i = parent[top];
+    }
+}
+
+void launch_chain_rows(cudaStream_t st, int ns, const int32_t* slot_vtx, const int32_t* chain_off,
+                       const int32_t* parent, const int32_t* ptop, int32_t* chain_rows, uint8_t* flag) {
+    if (ns == 0) return;
+    k_chain_rows<<<(ns + 7) / 8, 256, 0, st>>>(ns, slot_vtx, chain_off, parent, ptop, chain_rows, flag);
+}
+
+// rows on any chain, with the slot range in their subtree [first(i), i] and an
+// offset into the compact copy Zc of K[i][a_s], s in [s0, s1)
+__global__ void k_ulist(int n_f, int ns, const uint8_t* __restrict__ flag, const int32_t* __restrict__ slot_vtx,
+                        const int2* __restrict__ meta, int* __restrict__ ucount, int4* __restrict__ ulist) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_f || !flag[i]) return;
+    const int f = meta[i].y;
     int lo = 0, hi = ns;
     while (lo < hi) { int m = (lo + hi) >> 1; if (slot_vtx[m] < f) lo = m + 1; else hi = m; }
-    int s0 = lo;
+    const int s0 = lo;
     hi = ns;
     while (lo < hi) { int m = (lo + hi) >> 1; if (slot_vtx[m] <= i) lo = m + 1; else hi = m; }
-    int s1 = lo;
-    if (s0 >= s1) return;
-    const float* row = Krow + rowptr[i] - f;
-    double a0 = 0, a1 = 0, a2 = 0;
-    for (int s = s0 + lane; s < s1; s += 32) {
-        double kv = row[slot_vtx[s]];
-        a0 = fma(kv, wz[3 * s], a0);
-        a1 = fma(kv, wz[3 * s + 1], a1);
-        a2 = fma(kv, wz[3 * s + 2], a2);
-    }
-    a0 = warp_sum(a0);
-    a1 = warp_sum(a1);
-    a2 = warp_sum(a2);
-    if (lane == 0) {
-        float4 yi = y[i];
-        y[i] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), 0.f);
+    // list order and offsets are arbitrary but each row's values stay contiguous
+    const int idx = atomicAdd(&ucount[0], 1);
+    const int off = atomicAdd(&ucount[1], lo - s0);
+    ulist[idx] = make_int4(i, s0, lo, off);
+}
+
+// Zc[off + s - s0] = K[i][a_s]  (one warp per listed row)
+__global__ void k_zfill(const int* __restrict__ ucount, const int4* __restrict__ ulist,
+                        const int32_t* __restrict__ slot_vtx, const float* __restrict__ Krow,
+                        const int2* __restrict__ meta, float* __restrict__ Zc) {
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    const int cnt = ucount[0];
+    for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
+        const int4 u = ulist[e];
+        const float* row = Krow + meta[u.x].x;
+        for (int s = u.y + lane; s < u.z; s += 32) Zc[u.w + s - u.y] = row[slot_vtx[s]];
     }
 }
 
-void launch_scatter(cudaStream_t st, int n_f, int ns, int row_lo, const int32_t* slot_vtx, const float* Krow,
-                    const int64_t* rowptr, const int32_t* first, const double* wz, float4* y) {
-    if (ns == 0 || row_lo >= n_f) return;
-    int rows = n_f - row_lo;
-    k_scatter<<<(rows + 7) / 8, 256, 0, st>>>(n_f, ns, row_lo, slot_vtx, Krow, rowptr, first, wz, y);
+void launch_ulist(cudaStream_t st, int n_f, int ns, const uint8_t* flag, const int32_t* slot_vtx,
+                  const int2* meta, int* ucount, int4* ulist, const float* Krow, float* Zc) {
+    if (ns == 0) return;
+    k_ulist<<<(n_f + 255) / 256, 256, 0, st>>>(n_f, ns, flag, slot_vtx, meta, ucount, ulist);
+    k_zfill<<<148 * 4, 256, 0, st>>>(ucount, ulist, slot_vtx, Krow, meta, Zc);
+}
+
+// ----------------------------------------------------------------------------
+// scatter (P:L956 correction, delta form): y_i += sum_{s0 <= s < s1} K[i][a_s] wz_s
+// for the rows i on the contact vertices' chains (warp per row, grid-stride)
+// ----------------------------------------------------------------------------
+__global__ void k_scatter(const int* __restrict__ ucount, const int4* __restrict__ ulist,
+                          const float* __restrict__ Zc, const double* __restrict__ wz, float4* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    const int cnt = ucount[0];
+    for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
+        const int4 u = ulist[e];
+        const float* zr = Zc + u.w - u.y;   // zr[s] = K[i][a_s]
+        double a0 = 0, a1 = 0, a2 = 0;
+        for (int s = u.y + lane; s < u.z; s += 32) {
+            const double kv = __ldg(&zr[s]);
+            a0 = fma(kv, wz[3 * s], a0);
+            a1 = fma(kv, wz[3 * s + 1], a1);
+            a2 = fma(kv, wz[3 * s + 2], a2);
+        }
+        a0 = warp_sum(a0);
+        a1 = warp_sum(a1);
+        a2 = warp_sum(a2);
+        if (lane == 0) {
+            const float4 yi = y[u.x];
+            y[u.x] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), yi.w);
+        }
+    }
+}
+
+void launch_scatter(cudaStream_t st, const int* ucount, const int4* ulist, const float* Zc, const double* wz,
+                    float4* y) {
+    k_scatter<<<148 * 4, 256, 0, st>>>(ucount, ulist, Zc, wz, y);
 }
 
 // ----------------------------------------------------------------------------
@@ -825,31 +862,55 @@ void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const float* G) {
 // ----------------------------------------------------------------------------
 // CR (Saad Alg. 6.20) on S = Theta D Theta + C, z0 = 0, exactly N_CR matvecs
 // (reading A19), in ONE cluster of kCluster CTAs.  Every CTA keeps full fp64
-// copies of the row vectors and performs the O(m) work redundantly (so dot
-// products are identical everywhere without communication); the O(ns^2)
-// product q = G w is split by G rows and exchanged through DSMEM.
+// copies of the row vectors and the compact contact geometry in shared
+// memory and performs the O(m) work redundantly (so dot products are identical
+// everywhere without communication); the O(ns^2) product q = G W is split by
+// G rows and exchanged through DSMEM.
 //   (S v)_j = theta_j c_j . sum_{a in j} w_ja q_a + C_j v_j,
-//   q_a = sum_b G_ab W_b, W_b = sum_{rows k at b} w_kb theta_k c_k v_k.
+//   q_a = sum_b G_ab W_b,   W_b = sum_{rows k at b} w_kb theta_k c_k v_k.
+// Shared memory is carved dynamically for the actual (nc, ns).
 // ----------------------------------------------------------------------------
-struct CrSmem {
-    double z[3 * kMaxContacts], r[3 * kMaxContacts], p[3 * kMaxContacts], Ar[3 * kMaxContacts],
-        Ap[3 * kMaxContacts];
-    float th[3 * kMaxContacts], cd[3 * kMaxContacts];
-    float W[3 * kMaxSlots];
-    double q[2][3 * kMaxSlots];   // double-buffered: a CTA may run one matvec ahead of a peer
-    double red[kCrThreads / 32 * 2];
+struct CrLayout {
+    int m, nc, ns;
+    size_t z, r, p, Ar, Ap, th, cd, c9, s0, W, q, red, total;
+    __host__ __device__ CrLayout(int nc_, int ns_) : m(3 * nc_), nc(nc_), ns(ns_) {
+        size_t o = 0;
+        auto take = [&](size_t bytes) { size_t at = o; o += (bytes + 15) & ~size_t(15); return at; };
+        z = take(8 * (size_t)m); r = take(8 * (size_t)m); p = take(8 * (size_t)m);
+        Ar = take(8 * (size_t)m); Ap = take(8 * (size_t)m);
+        th = take(4 * (size_t)m); cd = take(4 * (size_t)m);
+        c9 = take(4 * 9 * (size_t)nc); s0 = take(4 * (size_t)nc);
+        W = take(8 * 3 * (size_t)ns); q = take(8 * 2 * 3 * (size_t)ns);
+        red = take(8 * 2 * (kCrThreads / 32));
+        total = o;
+    }
 };
+
+struct CrView {
+    double *z, *r, *p, *Ar, *Ap, *red, *W, *q;
+    float *th, *cd, *c9;
+    int* s0;
+};
+
+__device__ __forceinline__ CrView cr_view(unsigned char* base, const CrLayout& L) {
+    CrView v;
+    v.z = (double*)(base + L.z); v.r = (double*)(base + L.r); v.p = (double*)(base + L.p);
+    v.Ar = (double*)(base + L.Ar); v.Ap = (double*)(base + L.Ap); v.red = (double*)(base + L.red);
+    v.th = (float*)(base + L.th); v.cd = (float*)(base + L.cd); v.c9 = (float*)(base + L.c9);
+    v.W = (double*)(base + L.W); v.q = (double*)(base + L.q); v.s0 = (int*)(base + L.s0);
+    return v;
+}
 
 __device__ __forceinline__ void block_dot2(const double* a, const double* b, const double* c, const double* d, int m,
                                            double* red, double& o1, double& o2) {
     double s1 = 0.0, s2 = 0.0;
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        s1 += a[i] * b[i];
-        s2 += c[i] * d[i];
+        s1 = fma(a[i], b[i], s1);
+        s2 = fma(c[i], d[i], s2);
     }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
-    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     __syncthreads();
     if (l == 0) { red[2 * w] = s1; red[2 * w + 1] = s2; }
     __syncthreads();
@@ -857,33 +918,35 @@ __device__ __forceinline__ void block_dot2(const double* a, const double* b, con
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { t1 += red[2 * k]; t2 += red[2 * k + 1]; }
     o1 = t1;
     o2 = t2;
-    __syncthreads();
 }
 
 // out = S v  (all CTAs end with the full result)
-__device__ void cr_apply(cg::cluster_group& cl, CrSmem& sm, const double* v, double* out, int nc, int ns,
-                         const DContact* C, const int32_t* scp, const int32_t* sci, const float* scw,
-                         const float* G, int buf) {
-    double* qb = sm.q[buf];
-    const int m = 3 * nc;
-    // W_b (redundant)
+__device__ void cr_apply(cg::cluster_group& cl, const CrView& sv, const CrLayout& L, const double* v, double* out,
+                         const DContact* __restrict__ C, const int32_t* __restrict__ scp,
+                         const int32_t* __restrict__ sci, const float* __restrict__ scw,
+                         const float* __restrict__ G, int buf) {
+    const int nc = L.nc, ns = L.ns, m = L.m;
+    double* qb = sv.q + (size_t)buf * 3 * ns;
+    // W_b (redundant in every CTA).  fp64 throughout the D product: G = A_v^-1
+    // restricted to contact vertices is dominated by the rigid-translation
+    // component, so q = G W cancels heavily (fp32 W or fp32 sums cost ~3e-3).
     for (int b = threadIdx.x; b < ns; b += blockDim.x) {
-        double w0 = 0, w1 = 0, w2 = 0;
-        for (int p = scp[b]; p < scp[b + 1]; ++p) {
-            int c = sci[p];
-            double wt = scw[p];
-            const DContact& ct = C[c];
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+        for (int p = __ldg(&scp[b]); p < __ldg(&scp[b + 1]); ++p) {
+            const int c = __ldg(&sci[p]);
+            const double wt = __ldg(&scw[p]);
+            const float* cc = sv.c9 + 9 * c;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                double tv = wt * (double)sm.th[3 * c + k] * v[3 * c + k];
-                w0 += tv * ct.c[k][0];
-                w1 += tv * ct.c[k][1];
-                w2 += tv * ct.c[k][2];
+                const double tv = wt * (double)sv.th[3 * c + k] * v[3 * c + k];
+                w0 = fma(tv, (double)cc[3 * k], w0);
+                w1 = fma(tv, (double)cc[3 * k + 1], w1);
+                w2 = fma(tv, (double)cc[3 * k + 2], w2);
             }
         }
-        sm.W[3 * b] = (float)w0;
-        sm.W[3 * b + 1] = (float)w1;
-        sm.W[3 * b + 2] = (float)w2;
+        sv.W[3 * b] = w0;
+        sv.W[3 * b + 1] = w1;
+        sv.W[3 * b + 2] = w2;
     }
     __syncthreads();
     // q_a for this CTA's rows of G (warp per row), broadcast to all CTAs via DSMEM
@@ -893,19 +956,16 @@ __device__ void cr_apply(cg::cluster_group& cl, CrSmem& sm, const double* v, dou
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int a = a0 + wid; a < a1; a += nw) {
         const float* g = G + (size_t)a * ns;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
         double d0 = 0, d1 = 0, d2 = 0;
-        int cnt = 0;
         for (int b = lane; b < ns; b += 32) {
-            float gab = __ldg(&g[b]);
-            s0 = fmaf(gab, sm.W[3 * b], s0);
-            s1 = fmaf(gab, sm.W[3 * b + 1], s1);
-            s2 = fmaf(gab, sm.W[3 * b + 2], s2);
-            if (++cnt == 8) { d0 += s0; d1 += s1; d2 += s2; s0 = s1 = s2 = 0.f; cnt = 0; }
+            const double gab = (double)__ldg(&g[b]);
+            d0 = fma(gab, sv.W[3 * b], d0);
+            d1 = fma(gab, sv.W[3 * b + 1], d1);
+            d2 = fma(gab, sv.W[3 * b + 2], d2);
         }
-        d0 = warp_sum(d0 + s0);
-        d1 = warp_sum(d1 + s1);
-        d2 = warp_sum(d2 + s2);
+        d0 = warp_sum(d0);
+        d1 = warp_sum(d1);
+        d2 = warp_sum(d2);
         if (lane < kCluster) {
             double* rq = cl.map_shared_rank(qb, lane);
             rq[3 * a] = d0;
@@ -916,14 +976,21 @@ __device__ void cr_apply(cg::cluster_group& cl, CrSmem& sm, const double* v, dou
     cl.sync();
     // (S v)_j (redundant)
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        int c = j / 3, k = j - 3 * c;
-        const DContact& ct = C[c];
-        double acc = 0.0;
-        for (int p = 0; p < ct.nv; ++p) {
-            int sl = ct.slot[p];
-            acc += ct.w[p] * (ct.c[k][0] * qb[3 * sl] + ct.c[k][1] * qb[3 * sl + 1] + ct.c[k][2] * qb[3 * sl + 2]);
+        const int c = j / 3, k = j - 3 * c;
+        const float* cc = sv.c9 + 9 * c + 3 * k;
+        const int sl0 = sv.s0[c];
+        double acc;
+        if (sl0 >= 0) {   // single-vertex contact, weight 1
+            acc = (double)cc[0] * qb[3 * sl0] + (double)cc[1] * qb[3 * sl0 + 1] + (double)cc[2] * qb[3 * sl0 + 2];
+        } else {
+            const DContact& ct = C[c];
+            acc = 0.0;
+            for (int p = 0; p < ct.nv; ++p) {
+                const int sl = ct.slot[p];
+                acc += ct.w[p] * ((double)cc[0] * qb[3 * sl] + (double)cc[1] * qb[3 * sl + 1] + (double)cc[2] * qb[3 * sl + 2]);
+            }
         }
-        out[j] = (double)sm.th[j] * acc + (double)sm.cd[j] * v[j];
+        out[j] = (double)sv.th[j] * acc + (double)sv.cd[j] * v[j];
     }
     __syncthreads();
 }
@@ -933,81 +1000,92 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
          const int32_t* __restrict__ scp, const int32_t* __restrict__ sci, const float* __restrict__ scw,
          const float* __restrict__ G, const double4* __restrict__ x, ContactState cs) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    CrSmem& sm = *reinterpret_cast<CrSmem*>(smraw);
+    const CrLayout L(P.nc, P.ns);
+    const CrView sv = cr_view(smraw, L);
     cg::cluster_group cl = cg::this_cluster();
     const int nc = P.nc, ns = P.ns, m = 3 * nc;
     const double h = P.h;
+    // contact geometry -> shared memory
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+        const DContact& ct = C[c];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) sv.c9[9 * c + 3 * k + d] = (float)ct.c[k][d];
+        sv.s0[c] = (ct.nv == 1 && ct.w[0] == 1.0) ? ct.slot[0] : -1;
+    }
     // rho_j = h_j - theta_j c_j . x~_c, x~ = x^k + K^T y at the contact vertices
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        int c = j / 3, k = j - 3 * c;
+        const int c = j / 3, k = j - 3 * c;
         const DContact& ct = C[c];
         double xs[3] = {0, 0, 0};
         for (int p = 0; p < ct.nv; ++p) {
-            double4 xa = x[ct.vtx[p]];
-            int sl = ct.slot[p];
+            const double4 xa = x[ct.vtx[p]];
+            const int sl = ct.slot[p];
             xs[0] += ct.w[p] * (xa.x + cs.dxt[3 * sl]);
             xs[1] += ct.w[p] * (xa.y + cs.dxt[3 * sl + 1]);
             xs[2] += ct.w[p] * (xa.z + cs.dxt[3 * sl + 2]);
         }
-        double th = cs.theta[j];
-        double rho = cs.hvec[j] - th * (ct.c[k][0] * xs[0] + ct.c[k][1] * xs[1] + ct.c[k][2] * xs[2]);
-        sm.th[j] = (float)th;
-        sm.cd[j] = (float)cs.cdiag[j];
-        sm.r[j] = rho;
-        sm.p[j] = rho;
-        sm.z[j] = 0.0;
+        const double th = cs.theta[j];
+        const double rho = cs.hvec[j] - th * (ct.c[k][0] * xs[0] + ct.c[k][1] * xs[1] + ct.c[k][2] * xs[2]);
+        sv.th[j] = (float)th;
+        sv.cd[j] = (float)cs.cdiag[j];
+        sv.r[j] = rho;
+        sv.p[j] = rho;
+        sv.z[j] = 0.0;
     }
     __syncthreads();
     double rr, dummy;
-    block_dot2(sm.r, sm.r, sm.r, sm.r, m, sm.red, rr, dummy);
+    block_dot2(sv.r, sv.r, sv.r, sv.r, m, sv.red, rr, dummy);
     if (rr > 0.0 && P.cr_iters > 0) {
         int buf = 0;
-        cr_apply(cl, sm, sm.r, sm.Ar, nc, ns, C, scp, sci, scw, G, buf);
+        cr_apply(cl, sv, L, sv.r, sv.Ar, C, scp, sci, scw, G, buf);
         buf ^= 1;
-        for (int j = threadIdx.x; j < m; j += blockDim.x) sm.Ap[j] = sm.Ar[j];
+        for (int j = threadIdx.x; j < m; j += blockDim.x) sv.Ap[j] = sv.Ar[j];
         __syncthreads();
         double rAr, ApAp;
-        block_dot2(sm.r, sm.Ar, sm.Ap, sm.Ap, m, sm.red, rAr, ApAp);
+        block_dot2(sv.r, sv.Ar, sv.Ap, sv.Ap, m, sv.red, rAr, ApAp);
         for (int it = 0; it < P.cr_iters; ++it) {
             if (ApAp <= 1e-300 || fabs(rAr) <= 1e-300) break;
-            double alpha = rAr / ApAp;
+            const double alpha = rAr / ApAp;
             for (int j = threadIdx.x; j < m; j += blockDim.x) {
-                sm.z[j] += alpha * sm.p[j];
-                sm.r[j] -= alpha * sm.Ap[j];
+                sv.z[j] += alpha * sv.p[j];
+                sv.r[j] -= alpha * sv.Ap[j];
             }
             __syncthreads();
             if (it == P.cr_iters - 1) break;
-            cr_apply(cl, sm, sm.r, sm.Ar, nc, ns, C, scp, sci, scw, G, buf);
+            cr_apply(cl, sv, L, sv.r, sv.Ar, C, scp, sci, scw, G, buf);
             buf ^= 1;
             double rAr_new, t2;
-            block_dot2(sm.r, sm.Ar, sm.r, sm.r, m, sm.red, rAr_new, t2);
-            double beta = rAr_new / rAr;
+            block_dot2(sv.r, sv.Ar, sv.r, sv.r, m, sv.red, rAr_new, t2);
+            const double beta = rAr_new / rAr;
             rAr = rAr_new;
             for (int j = threadIdx.x; j < m; j += blockDim.x) {
-                sm.p[j] = sm.r[j] + beta * sm.p[j];
-                sm.Ap[j] = sm.Ar[j] + beta * sm.Ap[j];
+                sv.p[j] = sv.r[j] + beta * sv.p[j];
+                sv.Ap[j] = sv.Ar[j] + beta * sv.Ap[j];
             }
             __syncthreads();
             double t1;
-            block_dot2(sm.Ap, sm.Ap, sm.Ap, sm.Ap, m, sm.red, ApAp, t1);
+            block_dot2(sv.Ap, sv.Ap, sv.Ap, sv.Ap, m, sv.red, ApAp, t1);
         }
     }
-    block_dot2(sm.r, sm.r, sm.r, sm.r, m, sm.red, rr, dummy);
+    __syncthreads();
+    block_dot2(sv.r, sv.r, sv.r, sv.r, m, sv.red, rr, dummy);
     if (cl.block_rank() != 0) {
         cl.sync();   // keep DSMEM alive until everyone is done
         return;
     }
     // lambda += z / h^2 (reading A11), wz_b = sum w theta z c  (for y += K H^T z)
-    for (int j = threadIdx.x; j < m; j += blockDim.x) cs.lam[j] += sm.z[j] / (h * h);
+    for (int j = threadIdx.x; j < m; j += blockDim.x) cs.lam[j] += sv.z[j] / (h * h);
     for (int b = threadIdx.x; b < ns; b += blockDim.x) {
         double w0 = 0, w1 = 0, w2 = 0;
         for (int p = scp[b]; p < scp[b + 1]; ++p) {
-            int c = sci[p];
-            double wt = scw[p];
+            const int c = sci[p];
+            const double wt = scw[p];
             const DContact& ct = C[c];
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                double tv = wt * (double)sm.th[3 * c + k] * sm.z[3 * c + k];
+                const double tv = wt * (double)sv.th[3 * c + k] * sv.z[3 * c + k];
                 w0 += tv * ct.c[k][0];
                 w1 += tv * ct.c[k][1];
                 w2 += tv * ct.c[k][2];
@@ -1021,16 +1099,18 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
     cl.sync();
 }
 
+size_t cr_smem_bytes(int nc, int ns) { return CrLayout(nc, ns).total; }
+
 int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t* slot_vtx,
               const int32_t* scp, const int32_t* sci, const float* scw, const float* G, const double4* x,
               ContactState cs) {
     if (P.nc == 0) return 0;
     static bool attr = false;
-    size_t smem = sizeof(CrSmem);
+    const size_t smem = cr_smem_bytes(P.nc, P.ns);
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_cr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return (int)e;
-        e = cudaFuncSetAttribute(k_cr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(k_cr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrMaxSmem);
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }

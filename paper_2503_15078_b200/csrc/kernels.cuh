@@ -10,13 +10,13 @@ namespace simdev {
 using simhost::P1Block;
 using simhost::P1Item;
 using simhost::P2Block;
-using simhost::P2Item;
-using simhost::Run;
 
 constexpr int kMaxContacts = 1024;   // CR cluster keeps fp64 vectors of 3*kMaxContacts rows in SMEM
 constexpr int kMaxSlots = 1024;      // distinct contact vertices
 constexpr int kCluster = 16;         // CTAs in the CR cluster (non-portable size)
 constexpr int kCrThreads = 512;
+constexpr size_t kCrMaxSmem = 232448;  // 227 KB opt-in shared memory per CTA (sm_100)
+size_t cr_smem_bytes(int nc, int ns);  // the CR cluster's shared-memory footprint for (nc, ns)
 
 // one contact on the device (internal vertex ids, slot ids into the sorted contact-vertex list)
 struct DContact {
@@ -63,26 +63,34 @@ void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, co
 void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
                    const float4* fc, const double* M, const double4* x, const double4* s,
                    const int32_t* vcp, const int32_t* vci, const float* vcw, const double* hl,
-                   float4* u, double* resid_dbg);
+                   const int32_t* cb, float4* u, double* resid_dbg);
+// u[j].w carries cb[j] = colptr[j] + depth[j] as int bits (column base for pass 1)
 void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* Kcol,
-                   const int64_t* cb, const int32_t* depth, const float4* u, float4* y, double* part,
-                   int* counters);
-void launch_kpass2(cudaStream_t st, int nitems, const P2Item* it, const P2Block* bl, const Run* runs,
-                   const float* Krow, const float4* y, double* part, int* counters, double4* x,
-                   const double4* xt, double4* v, double inv_h, int finalize_v);
+                   const int32_t* depth, const float4* u, float4* y, double* part, int* counters);
+void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const int2* meta,
+                   const float* Krow, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
+                   int finalize_v);
 void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
-                      const int64_t* colptr, const int32_t* parent, const int32_t* ptop, const float4* y,
-                      double* dxt);
+                      const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
+                      const float4* y, double* dxt);
 int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t* slot_vtx,
               const int32_t* scp, const int32_t* sci, const float* scw, const float* G, const double4* x,
               ContactState cs);
-void launch_scatter(cudaStream_t st, int n_f, int ns, int row_lo, const int32_t* slot_vtx, const float* Krow,
-                    const int64_t* rowptr, const int32_t* first, const double* wz, float4* y);
+// y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s over the rows of ulist (int4 {row, s0, s1, -})
+void launch_scatter(cudaStream_t st, const int* ucount, const int4* ulist, const float* Zc, const double* wz,
+                    float4* y);
 
 // --- per-contact-set kernels ----------------------------------------------------
 void launch_delassus(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
                      const int64_t* colptr, const int32_t* depth, const int32_t* parent,
                      const int32_t* ptop, float* G);
 void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const float* G);
+// ancestor-chain rows of every slot (chain order = Kcol order) and the rows on
+// any chain with their slot ranges [s0, s1) = slots in [first(i), i]
+void launch_chain_rows(cudaStream_t st, int ns, const int32_t* slot_vtx, const int32_t* chain_off,
+                       const int32_t* parent, const int32_t* ptop, int32_t* chain_rows, uint8_t* flag);
+// ucount[0] = rows listed, ucount[1] = values in the compact copy Zc (both zeroed by the caller)
+void launch_ulist(cudaStream_t st, int n_f, int ns, const uint8_t* flag, const int32_t* slot_vtx,
+                  const int2* meta, int* ucount, int4* ulist, const float* Krow, float* Zc);
 
 }  // namespace simdev

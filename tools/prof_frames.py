@@ -1,0 +1,22 @@
+"""Run a few cfg3 frames (no bench extras) for ncu captures."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import scenes
+import paper_2503_15078_b200 as simlib
+
+frames = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+name = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
+torch.cuda.set_device(0)
+sc = scenes.make_scene(name)
+s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+s.set_pin_velocity(sc.pin_velocity)
+packed = s.pack_contacts(sc.contacts)
+for f in range(frames):
+    s.set_contacts(packed=packed)
+    s.step(1, 5)
+s.synchronize()
+print("done", s.stats()["kernels_per_frame"])
+x, v = s.get_state()
+print("max|x-X|", float(np.abs(x - sc.mesh.X).max()), "finite", bool(np.isfinite(x).all()), "max|v|", float(np.abs(v).max()))
