@@ -104,7 +104,8 @@ struct sim_handle {
     std::vector<int32_t> slot_vtx_h;
     DBuf<DContact> dc;
     DBuf<int32_t> slot_vtx, scp, sci, vcp, vci;
-    DBuf<float> scw, vcw, G;
+    DBuf<float> scw, vcw;
+    DBuf<double> G, GA;   // Delassus Gram and the CR's active-block scratch
     DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res;
     DBuf<int32_t> chain_off, chain_rows;
     DBuf<uint8_t> flag;
@@ -217,7 +218,7 @@ extern "C" void sim_destroy(sim_handle* H) {
         H->part1.release(); H->counters.release();
         H->chain_off.release(); H->chain_rows.release(); H->flag.release(); H->ucount.release(); H->ulist.release(); H->Zc.release();
         H->dc.release(); H->slot_vtx.release(); H->scp.release(); H->sci.release(); H->vcp.release();
-        H->vci.release(); H->scw.release(); H->vcw.release(); H->G.release(); H->lam.release();
+        H->vci.release(); H->scw.release(); H->vcw.release(); H->G.release(); H->GA.release(); H->lam.release();
         H->theta.release(); H->cdiag.release(); H->hvec.release(); H->hl.release(); H->dxt.release();
         H->wz.release(); H->phi_abs.release(); H->cr_res.release();
         for (auto e : H->pev) cudaEventDestroy(e);
@@ -330,6 +331,7 @@ static int upload_all(sim_handle* H) {
     CK(H->vci.alloc(4 * kMaxContacts));
     CK(H->vcw.alloc(4 * kMaxContacts));
     CK(H->G.alloc((size_t)kMaxSlots * kMaxSlots));
+    CK(H->GA.alloc((size_t)kMaxSlots * kMaxSlots));
     CK(H->lam.alloc(3 * kMaxContacts)); CK(H->theta.alloc(3 * kMaxContacts)); CK(H->cdiag.alloc(3 * kMaxContacts));
     CK(H->hvec.alloc(3 * kMaxContacts)); CK(H->hl.alloc(3 * kMaxContacts)); CK(H->dxt.alloc(3 * kMaxSlots));
     CK(H->wz.alloc(3 * kMaxSlots)); CK(H->phi_abs.alloc(kMaxContacts)); CK(H->cr_res.alloc(1));
@@ -589,7 +591,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
             launch_chain_dot(st, H->ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
                              H->y.p, H->dxt.p); nk++;
             MARK(KK_CR);
-            int e = launch_cr(st, P, H->dc.p, H->slot_vtx.p, H->scp.p, H->sci.p, H->scw.p, H->G.p, H->x.p, cs); nk++;
+            int e = launch_cr(st, P, H->dc.p, H->slot_vtx.p, H->scp.p, H->sci.p, H->scw.p, H->G.p, H->GA.p, H->x.p, cs); nk++;
             if (e) return -e;
             MARK(KK_SCATTER);
             launch_scatter(st, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
@@ -868,7 +870,11 @@ extern "C" int sim_debug_get_delassus(sim_handle* H, int32_t* cv, float* G, int3
     if (cap < H->ns) return fail(SIM_E_INVALID, "capacity %d < %d contact vertices", cap, H->ns);
     CK(cudaStreamSynchronize(H->stream));
     if (cv) for (int s = 0; s < H->ns; ++s) cv[s] = H->int2orig[H->slot_vtx_h[s]];
-    if (G && H->ns) CK(cudaMemcpy(G, H->G.p, (size_t)H->ns * H->ns * sizeof(float), cudaMemcpyDeviceToHost));
+    if (G && H->ns) {
+        std::vector<double> g((size_t)H->ns * H->ns);
+        CK(cudaMemcpy(g.data(), H->G.p, g.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        for (size_t q = 0; q < g.size(); ++q) G[q] = (float)g[q];
+    }
     return SIM_OK;
 }
 

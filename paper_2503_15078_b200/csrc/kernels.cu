@@ -456,82 +456,138 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) k_kpass1(const P1Item* __restrict__ items, const P1Block* __restrict__ blocks,
-                                                const float* __restrict__ Kcol, const int32_t* __restrict__ depth,
-                                                const float4* __restrict__ u, float4* __restrict__ y,
-                                                double* __restrict__ part, int* __restrict__ counters) {
-    __shared__ float4 s_u[kWarps][32];
-    __shared__ double s_red[kWarps][3][32];
+// Accumulation: fp32 FMAs over one 32-entry chunk, folded into fp64 once per
+// chunk (fp32->fp64 conversion runs at 1/4 of the FP64 rate on sm_100, so a
+// per-element DFMA would be conversion-bound).
+//
+// Memory pipeline: each warp streams its 32x32 tiles of K (and the matching
+// 32 vector entries) into shared memory with cp.async (4-byte, zero-fill for
+// entries outside the skyline), kStages tiles in flight per warp.
+constexpr int kStages = 2;
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct __align__(16) KTile {
+    float k[32][32];    // [entry q][lane]
+    float4 v[32];       // vector entry q (u_j for pass 1, y_r for pass 2); .w of u carries cb[j]
+};
+
+// ---- pass 1 ----------------------------------------------------------------
+__global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ items,
+                                                   const P1Block* __restrict__ blocks,
+                                                   const float* __restrict__ Kcol, const int32_t* __restrict__ depth,
+                                                   const float4* __restrict__ u, float4* __restrict__ y,
+                                                   double* __restrict__ part, int* __restrict__ counters) {
+    extern __shared__ __align__(16) unsigned char k1smem[];
+    KTile* tiles = reinterpret_cast<KTile*>(k1smem) + (threadIdx.x >> 5) * kStages;
+    double (*s_red)[kWarps][32] = reinterpret_cast<double (*)[kWarps][32]>(k1smem + sizeof(KTile) * kStages * kWarps);
     __shared__ int s_last;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const P1Item it = items[blockIdx.x];
     const int r = it.r0 + lane;
     const bool act = lane < it.nrows;
     const int base = lane - depth[it.r0];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int jc = it.c0 + 32 * w; jc < it.c1; jc += 32 * kWarps) {
+    const int nchunk = (it.c1 - it.c0 + 31) >> 5;
+    // this warp owns chunks w, w + 8, ...; issue = u entries (16 B each), then the 32x32 K tile
+    auto issue = [&](int ci, KTile& T) {
+        const int jc = it.c0 + 32 * ci;
         const int j = jc + lane;
-        s_u[w][lane] = j < it.c1 ? __ldg(&u[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        cp_async16(&T.v[lane], &u[min(j, it.c1 - 1)], j < it.c1);
+        // K addresses need cb[j] = u[j].w: read it from global (L1/L2) for the issuing lane's column
+        const int cbj = j < it.c1 ? __float_as_int(__ldg(&u[j]).w) : 0;
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {
+            const int cq = __shfl_sync(0xffffffffu, cbj, q);
+            const bool ok = act && (jc + q < it.c1) && (jc + q <= r);
+            cp_async4(&T.k[q][lane], &Kcol[ok ? cq + base : 0], ok);
+        }
+    };
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const int mine = (nchunk - w + kWarps - 1) / kWarps;   // chunks of this warp
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < mine) issue(w + kWarps * s, tiles[s]);
+        cp_async_commit();
+    }
+    for (int t = 0; t < mine; ++t) {
+        const int nx = t + kStages - 1;
+        if (nx < mine) issue(w + kWarps * nx, tiles[nx % kStages]);
+        cp_async_commit();
+        cp_async_wait<kStages - 1>();
         __syncwarp();
-        const int nj = min(32, it.c1 - jc);
-        float kv[32];
+        const KTile& T = tiles[t % kStages];
+        float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
-            const float4 uq = s_u[w][q];
-            kv[q] = (q < nj && act && jc + q <= r) ? __ldg(&Kcol[__float_as_int(uq.w) + base]) : 0.f;
+            const float kq = T.k[q][lane];
+            const float4 uq = T.v[q];
+            f0 = fmaf(kq, uq.x, f0);
+            f1 = fmaf(kq, uq.y, f1);
+            f2 = fmaf(kq, uq.z, f2);
         }
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const float4 uq = s_u[w][q];
-            const double kq = (double)kv[q];
-            a0 = fma(kq, (double)uq.x, a0);
-            a1 = fma(kq, (double)uq.y, a1);
-            a2 = fma(kq, (double)uq.z, a2);
-        }
+        a0 += (double)f0;
+        a1 += (double)f1;
+        a2 += (double)f2;
         __syncwarp();
     }
-    s_red[w][0][lane] = a0;
-    s_red[w][1][lane] = a1;
-    s_red[w][2][lane] = a2;
+    cp_async_wait<0>();
+    s_red[0][w][lane] = a0;
+    s_red[1][w][lane] = a1;
+    s_red[2][w][lane] = a2;
     __syncthreads();
-    if (w != 0) return;
-    a0 = a1 = a2 = 0.0;
-#pragma unroll
-    for (int q = 0; q < kWarps; ++q) {
-        a0 += s_red[q][0][lane];
-        a1 += s_red[q][1][lane];
-        a2 += s_red[q][2][lane];
-    }
     const P1Block b = blocks[it.block];
+    const int t = threadIdx.x;
+    double tot = 0.0;
+    if (t < 96) {
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q) tot += s_red[t >> 5][q][t & 31];
+    }
     if (b.nitems == 1) {
-        if (act) y[r] = make_float4((float)a0, (float)a1, (float)a2, 0.f);
+        __syncthreads();
+        if (t < 96) s_red[t >> 5][0][t & 31] = tot;
+        __syncthreads();
+        if (t < it.nrows) y[it.r0 + t] = make_float4((float)s_red[0][0][t], (float)s_red[1][0][t], (float)s_red[2][0][t], 0.f);
         return;
     }
-    double* pp = part + ((size_t)it.part * 3) * 32 + lane;
-    pp[0] = a0;
-    pp[32] = a1;
-    pp[64] = a2;
+    if (t < 96) part[(size_t)it.part * 96 + t] = tot;
     __threadfence();
-    __syncwarp();
-    int old = 0;
-    if (lane == 0) old = atomicAdd(&counters[it.block], 1);
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old != b.nitems - 1) return;
+    __syncthreads();
+    if (t == 0) s_last = atomicAdd(&counters[it.block], 1) == b.nitems - 1;
+    __syncthreads();
+    if (!s_last) return;
     __threadfence();
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int q = 0; q < b.nitems; ++q) {
-        const double* pq = part + ((size_t)(b.part0 + q) * 3) * 32 + lane;
-        s0 += __ldcg(pq);
-        s1 += __ldcg(pq + 32);
-        s2 += __ldcg(pq + 64);
+    if (t < 96) {
+        double s = 0.0;
+        for (int q = 0; q < b.nitems; ++q) s += __ldcg(&part[(size_t)(b.part0 + q) * 96 + t]);
+        s_red[t >> 5][0][t & 31] = s;
     }
-    if (act) y[r] = make_float4((float)s0, (float)s1, (float)s2, 0.f);
-    if (lane == 0) counters[it.block] = 0;
+    __syncthreads();
+    if (t < it.nrows) y[it.r0 + t] = make_float4((float)s_red[0][0][t], (float)s_red[1][0][t], (float)s_red[2][0][t], 0.f);
+    if (t == 0) counters[it.block] = 0;
 }
+
+constexpr size_t kKpassSmem = sizeof(KTile) * kStages * kWarps + sizeof(double) * 3 * kWarps * 32;
 
 void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* Kcol,
                    const int32_t* depth, const float4* u, float4* y, double* part, int* counters) {
-    k_kpass1<<<nitems, 32 * kWarps, 0, st>>>(it, bl, Kcol, depth, u, y, part, counters);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_kpass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpassSmem);
+        attr = true;
+    }
+    k_kpass1<<<nitems, 32 * kWarps, kKpassSmem, st>>>(it, bl, Kcol, depth, u, y, part, counters);
 }
 
 // ----------------------------------------------------------------------------
@@ -540,74 +596,98 @@ void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block*
 // K[r][j] = Krow[rb(r) + j], rb(r) = rowptr[r] - first(r) (meta[r] = {rb, first}).
 // No partial sums, no atomics: the CTA owns its 32 columns.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_kpass2(const P2Block* __restrict__ blocks, const int32_t* __restrict__ cover,
-                                                const int2* __restrict__ meta, const float* __restrict__ Krow,
-                                                const float4* __restrict__ y, double4* __restrict__ x,
-                                                const double4* __restrict__ xt, double4* __restrict__ v, double inv_h,
-                                                int finalize_v) {
-    __shared__ int s_rb[kWarps][32], s_f[kWarps][32], s_r[kWarps][32];
-    __shared__ float4 s_y[kWarps][32];
-    __shared__ double s_red[kWarps][3][32];
+__global__ void __launch_bounds__(256, 2) k_kpass2(const P2Block* __restrict__ blocks,
+                                                   const int32_t* __restrict__ cover, const int2* __restrict__ meta,
+                                                   const float* __restrict__ Krow, const float4* __restrict__ y,
+                                                   double4* __restrict__ x, const double4* __restrict__ xt,
+                                                   double4* __restrict__ v, double inv_h, int finalize_v) {
+    extern __shared__ __align__(16) unsigned char k2smem[];
+    KTile* tiles = reinterpret_cast<KTile*>(k2smem) + (threadIdx.x >> 5) * kStages;
+    double (*s_red)[kWarps][32] = reinterpret_cast<double (*)[kWarps][32]>(k2smem + sizeof(KTile) * kStages * kWarps);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const P2Block b = blocks[blockIdx.x];
     const int j = b.c0 + lane;
     const bool act = lane < b.ncols;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int k0 = b.list0 + 32 * w; k0 < b.list1; k0 += 32 * kWarps) {
-        const int k = k0 + lane;
-        if (k < b.list1) {
-            const int r = __ldg(&cover[k]);
-            const int2 m = __ldg(&meta[r]);
-            s_r[w][lane] = r;
-            s_rb[w][lane] = m.x;
-            s_f[w][lane] = m.y;
-            s_y[w][lane] = __ldg(&y[r]);
-        } else {
-            s_y[w][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int nrow = b.list1 - b.list0;
+    const int nchunk = (nrow + 31) >> 5;
+    auto issue = [&](int ci, KTile& T) {
+        const int k = b.list0 + 32 * ci + lane;
+        const bool okr = k < b.list1;
+        const int r = okr ? __ldg(&cover[k]) : 0;
+        const int2 m = okr ? __ldg(&meta[r]) : make_int2(0, 1 << 30);
+        cp_async16(&T.v[lane], &y[r], okr);
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {
+            const int rq = __shfl_sync(0xffffffffu, r, q);
+            const int rbq = __shfl_sync(0xffffffffu, m.x, q);
+            const int fq = __shfl_sync(0xffffffffu, m.y, q);
+            const bool ok = act && (32 * ci + q < nrow) && j >= fq && j <= rq;
+            cp_async4(&T.k[q][lane], &Krow[ok ? rbq + j : 0], ok);
         }
-        __syncwarp();
-        const int n = min(32, b.list1 - k0);
-        float kv[32];
+    };
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const int mine = (nchunk - w + kWarps - 1) / kWarps;
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-            kv[q] = (q < n && act && j >= s_f[w][q] && j <= s_r[w][q]) ? __ldg(&Krow[s_rb[w][q] + j]) : 0.f;
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < mine) issue(w + kWarps * s, tiles[s]);
+        cp_async_commit();
+    }
+    for (int t = 0; t < mine; ++t) {
+        const int nx = t + kStages - 1;
+        if (nx < mine) issue(w + kWarps * nx, tiles[nx % kStages]);
+        cp_async_commit();
+        cp_async_wait<kStages - 1>();
+        __syncwarp();
+        const KTile& T = tiles[t % kStages];
+        float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
-            const float4 yq = s_y[w][q];
-            const double kq = (double)kv[q];
-            a0 = fma(kq, (double)yq.x, a0);
-            a1 = fma(kq, (double)yq.y, a1);
-            a2 = fma(kq, (double)yq.z, a2);
+            const float kq = T.k[q][lane];
+            const float4 yq = T.v[q];
+            f0 = fmaf(kq, yq.x, f0);
+            f1 = fmaf(kq, yq.y, f1);
+            f2 = fmaf(kq, yq.z, f2);
         }
+        a0 += (double)f0;
+        a1 += (double)f1;
+        a2 += (double)f2;
         __syncwarp();
     }
-    s_red[w][0][lane] = a0;
-    s_red[w][1][lane] = a1;
-    s_red[w][2][lane] = a2;
+    cp_async_wait<0>();
+    s_red[0][w][lane] = a0;
+    s_red[1][w][lane] = a1;
+    s_red[2][w][lane] = a2;
     __syncthreads();
-    if (w != 0 || !act) return;
-    a0 = a1 = a2 = 0.0;
+    const int t = threadIdx.x;
+    if (t < 96) {
+        double tot = 0.0;
 #pragma unroll
-    for (int q = 0; q < kWarps; ++q) {
-        a0 += s_red[q][0][lane];
-        a1 += s_red[q][1][lane];
-        a2 += s_red[q][2][lane];
+        for (int q = 0; q < kWarps; ++q) tot += s_red[t >> 5][q][t & 31];
+        s_red[t >> 5][0][t & 31] = tot;   // each thread owns its (comp, lane) slot: no race
     }
-    double4 xj = x[j];
-    xj.x += a0;
-    xj.y += a1;
-    xj.z += a2;
-    x[j] = xj;
+    __syncthreads();
+    if (t >= b.ncols) return;
+    const int jj = b.c0 + t;
+    double4 xj = x[jj];
+    xj.x += s_red[0][0][t];
+    xj.y += s_red[1][0][t];
+    xj.z += s_red[2][0][t];
+    x[jj] = xj;
     if (finalize_v) {   // v = (x - x_t) / h
-        const double4 t0 = xt[j];
-        v[j] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
+        const double4 t0 = xt[jj];
+        v[jj] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
     }
 }
 
 void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const int2* meta,
                    const float* Krow, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
                    int finalize_v) {
-    k_kpass2<<<nblocks, 32 * kWarps, 0, st>>>(bl, cover, meta, Krow, y, x, xt, v, inv_h, finalize_v);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_kpass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpassSmem);
+        attr = true;
+    }
+    k_kpass2<<<nblocks, 32 * kWarps, kKpassSmem, st>>>(bl, cover, meta, Krow, y, x, xt, v, inv_h, finalize_v);
 }
 
 // ----------------------------------------------------------------------------
@@ -768,7 +848,7 @@ __device__ int lca_depth(int a, int b, const int32_t* parent, const int32_t* pto
 __global__ void __launch_bounds__(256) k_delassus(int ns, const int32_t* __restrict__ slot_vtx,
                                                   const float* __restrict__ Kcol, const int64_t* __restrict__ colptr,
                                                   const int32_t* __restrict__ depth, const int32_t* __restrict__ parent,
-                                                  const int32_t* __restrict__ ptop, float* __restrict__ G) {
+                                                  const int32_t* __restrict__ ptop, double* __restrict__ G) {
     // tile (bs, bt) with bt >= bs from a linear triangular index
     int tiles = (ns + 31) / 32;
     int idx = blockIdx.x, bs = 0;
@@ -828,15 +908,15 @@ __global__ void __launch_bounds__(256) k_delassus(int ns, const int32_t* __restr
     for (int q = 0; q < 4; ++q) {
         int t = bt * 32 + lt0 + q;
         if (s < ns && t < ns) {
-            G[(size_t)s * ns + t] = acc[q];
-            G[(size_t)t * ns + s] = acc[q];
+            G[(size_t)s * ns + t] = (double)acc[q];
+            G[(size_t)t * ns + s] = (double)acc[q];
         }
     }
 }
 
 void launch_delassus(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
                      const int64_t* colptr, const int32_t* depth, const int32_t* parent,
-                     const int32_t* ptop, float* G) {
+                     const int32_t* ptop, double* G) {
     if (ns == 0) return;
     int tiles = (ns + 31) / 32;
     int ntri = tiles * (tiles + 1) / 2;
@@ -844,35 +924,41 @@ void launch_delassus(cudaStream_t st, int ns, const int32_t* slot_vtx, const flo
 }
 
 // D_jj = sum_{a,b in j} w_a w_b G_ab (unit directions; reading A18)
-__global__ void k_djj(int nc, int ns, DContact* C, const float* __restrict__ G) {
+__global__ void k_djj(int nc, int ns, DContact* C, const double* __restrict__ G) {
     int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nc) return;
     DContact& ct = C[c];
     double d = 0.0;
     for (int p = 0; p < ct.nv; ++p)
-        for (int q = 0; q < ct.nv; ++q) d += ct.w[p] * ct.w[q] * (double)G[(size_t)ct.slot[p] * ns + ct.slot[q]];
+        for (int q = 0; q < ct.nv; ++q) d += ct.w[p] * ct.w[q] * G[(size_t)ct.slot[p] * ns + ct.slot[q]];
     ct.Djj = d;
 }
 
-void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const float* G) {
+void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const double* G) {
     if (nc == 0) return;
     k_djj<<<(nc + 127) / 128, 128, 0, st>>>(nc, ns, c, G);
 }
 
 // ----------------------------------------------------------------------------
 // CR (Saad Alg. 6.20) on S = Theta D Theta + C, z0 = 0, exactly N_CR matvecs
-// (reading A19), in ONE cluster of kCluster CTAs.  Every CTA keeps full fp64
-// copies of the row vectors and the compact contact geometry in shared
-// memory and performs the O(m) work redundantly (so dot products are identical
-// everywhere without communication); the O(ns^2) product q = G W is split by
-// G rows and exchanged through DSMEM.
+// (reading A19), in ONE cluster of kCluster CTAs.
+//
+// * Theta-sparsity: rows with theta = 0 (separated contacts, inactive
+//   friction) contribute nothing to Theta D Theta, so the D product only runs
+//   over the "active" contact vertices (any row with theta != 0).  The active
+//   block G_A of G is gathered once per CR call (exact, not an approximation).
+// * Every CTA keeps full fp64 copies of the row vectors and the compact
+//   contact geometry in shared memory and performs the O(m) work redundantly
+//   (dot products are identical everywhere without communication); the
+//   product q = G_A W is split by rows and exchanged through DSMEM.
+// * fp64 in the D product: G = A_v^-1 is a smoothing kernel, so G W cancels
+//   heavily for the oscillatory Krylov vectors (fp32 W or fp32 sums cost ~3e-3).
 //   (S v)_j = theta_j c_j . sum_{a in j} w_ja q_a + C_j v_j,
 //   q_a = sum_b G_ab W_b,   W_b = sum_{rows k at b} w_kb theta_k c_k v_k.
-// Shared memory is carved dynamically for the actual (nc, ns).
 // ----------------------------------------------------------------------------
 struct CrLayout {
     int m, nc, ns;
-    size_t z, r, p, Ar, Ap, th, cd, c9, s0, W, q, red, total;
+    size_t z, r, p, Ar, Ap, th, cd, c9, s0, W, q, aidx, apos, red, total;
     __host__ __device__ CrLayout(int nc_, int ns_) : m(3 * nc_), nc(nc_), ns(ns_) {
         size_t o = 0;
         auto take = [&](size_t bytes) { size_t at = o; o += (bytes + 15) & ~size_t(15); return at; };
@@ -881,7 +967,8 @@ struct CrLayout {
         th = take(4 * (size_t)m); cd = take(4 * (size_t)m);
         c9 = take(4 * 9 * (size_t)nc); s0 = take(4 * (size_t)nc);
         W = take(8 * 3 * (size_t)ns); q = take(8 * 2 * 3 * (size_t)ns);
-        red = take(8 * 2 * (kCrThreads / 32));
+        aidx = take(4 * (size_t)ns); apos = take(4 * (size_t)ns);
+        red = take(8 * 2 * (kCrThreads / 32) + 4 * (kCrThreads / 32 + 1));
         total = o;
     }
 };
@@ -889,7 +976,7 @@ struct CrLayout {
 struct CrView {
     double *z, *r, *p, *Ar, *Ap, *red, *W, *q;
     float *th, *cd, *c9;
-    int* s0;
+    int *s0, *aidx, *apos;
 };
 
 __device__ __forceinline__ CrView cr_view(unsigned char* base, const CrLayout& L) {
@@ -898,6 +985,7 @@ __device__ __forceinline__ CrView cr_view(unsigned char* base, const CrLayout& L
     v.Ar = (double*)(base + L.Ar); v.Ap = (double*)(base + L.Ap); v.red = (double*)(base + L.red);
     v.th = (float*)(base + L.th); v.cd = (float*)(base + L.cd); v.c9 = (float*)(base + L.c9);
     v.W = (double*)(base + L.W); v.q = (double*)(base + L.q); v.s0 = (int*)(base + L.s0);
+    v.aidx = (int*)(base + L.aidx); v.apos = (int*)(base + L.apos);
     return v;
 }
 
@@ -920,17 +1008,16 @@ __device__ __forceinline__ void block_dot2(const double* a, const double* b, con
     o2 = t2;
 }
 
-// out = S v  (all CTAs end with the full result)
-__device__ void cr_apply(cg::cluster_group& cl, const CrView& sv, const CrLayout& L, const double* v, double* out,
-                         const DContact* __restrict__ C, const int32_t* __restrict__ scp,
+// out = S v  (all CTAs end with the full result).  GA: na x na active block of G.
+__device__ void cr_apply(cg::cluster_group& cl, const CrView& sv, const CrLayout& L, int na, const double* v,
+                         double* out, const DContact* __restrict__ C, const int32_t* __restrict__ scp,
                          const int32_t* __restrict__ sci, const float* __restrict__ scw,
-                         const float* __restrict__ G, int buf) {
-    const int nc = L.nc, ns = L.ns, m = L.m;
-    double* qb = sv.q + (size_t)buf * 3 * ns;
-    // W_b (redundant in every CTA).  fp64 throughout the D product: G = A_v^-1
-    // restricted to contact vertices is dominated by the rigid-translation
-    // component, so q = G W cancels heavily (fp32 W or fp32 sums cost ~3e-3).
-    for (int b = threadIdx.x; b < ns; b += blockDim.x) {
+                         const double* __restrict__ GA, int buf) {
+    const int m = L.m;
+    double* qb = sv.q + (size_t)buf * 3 * L.ns;   // indexed by active position
+    // W over the active slots (redundant in every CTA), SoA W0 | W1 | W2
+    for (int i = threadIdx.x; i < na; i += blockDim.x) {
+        const int b = sv.aidx[i];
         double w0 = 0.0, w1 = 0.0, w2 = 0.0;
         for (int p = __ldg(&scp[b]); p < __ldg(&scp[b + 1]); ++p) {
             const int c = __ldg(&sci[p]);
@@ -944,53 +1031,68 @@ __device__ void cr_apply(cg::cluster_group& cl, const CrView& sv, const CrLayout
                 w2 = fma(tv, (double)cc[3 * k + 2], w2);
             }
         }
-        sv.W[3 * b] = w0;
-        sv.W[3 * b + 1] = w1;
-        sv.W[3 * b + 2] = w2;
+        sv.W[i] = w0;
+        sv.W[na + i] = w1;
+        sv.W[2 * na + i] = w2;
     }
     __syncthreads();
-    // q_a for this CTA's rows of G (warp per row), broadcast to all CTAs via DSMEM
     const int rank = cl.block_rank();
-    const int per = (ns + kCluster - 1) / kCluster;
-    const int a0 = rank * per, a1 = min(ns, a0 + per);
+    const int per = (na + kCluster - 1) / kCluster;
+    const int i0 = rank * per, i1 = min(na, i0 + per);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int a = a0 + wid; a < a1; a += nw) {
-        const float* g = G + (size_t)a * ns;
+    const double* W0 = sv.W;
+    const double* W1 = sv.W + na;
+    const double* W2 = sv.W + 2 * na;
+    for (int i = i0 + wid; i < i1; i += nw) {
+        const double* g = GA + (size_t)i * na;
         double d0 = 0, d1 = 0, d2 = 0;
-        for (int b = lane; b < ns; b += 32) {
-            const double gab = (double)__ldg(&g[b]);
-            d0 = fma(gab, sv.W[3 * b], d0);
-            d1 = fma(gab, sv.W[3 * b + 1], d1);
-            d2 = fma(gab, sv.W[3 * b + 2], d2);
+        for (int b0 = 0; b0 < na; b0 += 128) {
+            double gv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int bb = b0 + 32 * u + lane;
+                gv[u] = bb < na ? __ldcg(&g[bb]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int bb = min(b0 + 32 * u + lane, na - 1);
+                d0 = fma(gv[u], W0[bb], d0);
+                d1 = fma(gv[u], W1[bb], d1);
+                d2 = fma(gv[u], W2[bb], d2);
+            }
         }
         d0 = warp_sum(d0);
         d1 = warp_sum(d1);
         d2 = warp_sum(d2);
         if (lane < kCluster) {
             double* rq = cl.map_shared_rank(qb, lane);
-            rq[3 * a] = d0;
-            rq[3 * a + 1] = d1;
-            rq[3 * a + 2] = d2;
+            rq[3 * i] = d0;
+            rq[3 * i + 1] = d1;
+            rq[3 * i + 2] = d2;
         }
     }
     cl.sync();
     // (S v)_j (redundant)
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
         const int c = j / 3, k = j - 3 * c;
-        const float* cc = sv.c9 + 9 * c + 3 * k;
-        const int sl0 = sv.s0[c];
-        double acc;
-        if (sl0 >= 0) {   // single-vertex contact, weight 1
-            acc = (double)cc[0] * qb[3 * sl0] + (double)cc[1] * qb[3 * sl0 + 1] + (double)cc[2] * qb[3 * sl0 + 2];
-        } else {
-            const DContact& ct = C[c];
-            acc = 0.0;
-            for (int p = 0; p < ct.nv; ++p) {
-                const int sl = ct.slot[p];
-                acc += ct.w[p] * ((double)cc[0] * qb[3 * sl] + (double)cc[1] * qb[3 * sl + 1] + (double)cc[2] * qb[3 * sl + 2]);
+        const double th = (double)sv.th[j];
+        double acc = 0.0;
+        if (th != 0.0) {
+            const float* cc = sv.c9 + 9 * c + 3 * k;
+            const int sl0 = sv.s0[c];
+            if (sl0 >= 0) {   // single-vertex contact, weight 1
+                const int ip = sv.apos[sl0];
+                acc = (double)cc[0] * qb[3 * ip] + (double)cc[1] * qb[3 * ip + 1] + (double)cc[2] * qb[3 * ip + 2];
+            } else {
+                const DContact& ct = C[c];
+                for (int p = 0; p < ct.nv; ++p) {
+                    const int ip = sv.apos[ct.slot[p]];
+                    acc += ct.w[p] * ((double)cc[0] * qb[3 * ip] + (double)cc[1] * qb[3 * ip + 1] +
+                                      (double)cc[2] * qb[3 * ip + 2]);
+                }
             }
         }
-        out[j] = (double)sv.th[j] * acc + (double)sv.cd[j] * v[j];
+        out[j] = th * acc + (double)sv.cd[j] * v[j];
     }
     __syncthreads();
 }
@@ -998,7 +1100,7 @@ __device__ void cr_apply(cg::cluster_group& cl, const CrView& sv, const CrLayout
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1)
     k_cr(Params P, const DContact* __restrict__ C, const int32_t* __restrict__ slot_vtx,
          const int32_t* __restrict__ scp, const int32_t* __restrict__ sci, const float* __restrict__ scw,
-         const float* __restrict__ G, const double4* __restrict__ x, ContactState cs) {
+         const double* __restrict__ G, double* __restrict__ GA, const double4* __restrict__ x, ContactState cs) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const CrLayout L(P.nc, P.ns);
     const CrView sv = cr_view(smraw, L);
@@ -1035,11 +1137,53 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
         sv.z[j] = 0.0;
     }
     __syncthreads();
+    // active slots: any incident row with theta != 0; ascending slot order (block scan)
+    int* cnt = reinterpret_cast<int*>(sv.red + 2 * (kCrThreads / 32));   // [0] running count, [1..16] warp sums
+    if (threadIdx.x == 0) cnt[0] = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < ns; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        bool act = false;
+        if (b < ns)
+            for (int p = scp[b]; p < scp[b + 1] && !act; ++p) {
+                const int c = sci[p];
+                act = sv.th[3 * c] != 0.f || sv.th[3 * c + 1] != 0.f || sv.th[3 * c + 2] != 0.f;
+            }
+        const unsigned bal = __ballot_sync(0xffffffffu, act);
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (lane == 0) cnt[1 + wid] = __popc(bal);
+        __syncthreads();
+        int off = cnt[0];
+        for (int q = 0; q < wid; ++q) off += cnt[1 + q];
+        off += __popc(bal & ((1u << lane) - 1u));
+        if (b < ns) {
+            sv.apos[b] = act ? off : -1;
+            if (act) sv.aidx[off] = b;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = cnt[0];
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += cnt[1 + q];
+            cnt[0] = tot;
+        }
+        __syncthreads();
+    }
+    const int na = cnt[0];
+    // gather this CTA's rows of the active block G_A (only this CTA reads them)
+    {
+        const int per = (na + kCluster - 1) / kCluster;
+        const int i0 = cl.block_rank() * per, i1 = min(na, i0 + per);
+        for (int e = threadIdx.x; e < (i1 - i0) * na; e += blockDim.x) {
+            const int i = i0 + e / na, jj = e % na;
+            GA[(size_t)i * na + jj] = G[(size_t)sv.aidx[i] * ns + sv.aidx[jj]];
+        }
+    }
+    __syncthreads();
     double rr, dummy;
     block_dot2(sv.r, sv.r, sv.r, sv.r, m, sv.red, rr, dummy);
     if (rr > 0.0 && P.cr_iters > 0) {
         int buf = 0;
-        cr_apply(cl, sv, L, sv.r, sv.Ar, C, scp, sci, scw, G, buf);
+        cr_apply(cl, sv, L, na, sv.r, sv.Ar, C, scp, sci, scw, GA, buf);
         buf ^= 1;
         for (int j = threadIdx.x; j < m; j += blockDim.x) sv.Ap[j] = sv.Ar[j];
         __syncthreads();
@@ -1054,7 +1198,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
             }
             __syncthreads();
             if (it == P.cr_iters - 1) break;
-            cr_apply(cl, sv, L, sv.r, sv.Ar, C, scp, sci, scw, G, buf);
+            cr_apply(cl, sv, L, na, sv.r, sv.Ar, C, scp, sci, scw, GA, buf);
             buf ^= 1;
             double rAr_new, t2;
             block_dot2(sv.r, sv.Ar, sv.r, sv.r, m, sv.red, rAr_new, t2);
@@ -1102,8 +1246,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
 size_t cr_smem_bytes(int nc, int ns) { return CrLayout(nc, ns).total; }
 
 int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t* slot_vtx,
-              const int32_t* scp, const int32_t* sci, const float* scw, const float* G, const double4* x,
-              ContactState cs) {
+              const int32_t* scp, const int32_t* sci, const float* scw, const double* G, double* GA,
+              const double4* x, ContactState cs) {
     if (P.nc == 0) return 0;
     static bool attr = false;
     const size_t smem = cr_smem_bytes(P.nc, P.ns);
@@ -1114,7 +1258,7 @@ int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
-    k_cr<<<kCluster, kCrThreads, smem, st>>>(P, c, slot_vtx, scp, sci, scw, G, x, cs);
+    k_cr<<<kCluster, kCrThreads, smem, st>>>(P, c, slot_vtx, scp, sci, scw, G, GA, x, cs);
     return (int)cudaGetLastError();
 }
 

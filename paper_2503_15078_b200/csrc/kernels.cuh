@@ -74,8 +74,8 @@ void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const fl
                       const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
                       const float4* y, double* dxt);
 int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t* slot_vtx,
-              const int32_t* scp, const int32_t* sci, const float* scw, const float* G, const double4* x,
-              ContactState cs);
+              const int32_t* scp, const int32_t* sci, const float* scw, const double* G, double* GA,
+              const double4* x, ContactState cs);
 // y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s over the rows of ulist (int4 {row, s0, s1, -})
 void launch_scatter(cudaStream_t st, const int* ucount, const int4* ulist, const float* Zc, const double* wz,
                     float4* y);
@@ -83,8 +83,8 @@ void launch_scatter(cudaStream_t st, const int* ucount, const int4* ulist, const
 // --- per-contact-set kernels ----------------------------------------------------
 void launch_delassus(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
                      const int64_t* colptr, const int32_t* depth, const int32_t* parent,
-                     const int32_t* ptop, float* G);
-void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const float* G);
+                     const int32_t* ptop, double* G);
+void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const double* G);
 // ancestor-chain rows of every slot (chain order = Kcol order) and the rows on
 // any chain with their slot ranges [s0, s1) = slots in [first(i), i]
 void launch_chain_rows(cudaStream_t st, int ns, const int32_t* slot_vtx, const int32_t* chain_off,
