@@ -203,6 +203,10 @@ int sim_debug_get_delassus(sim_handle *h, int32_t *cv, float *G, int32_t capacit
  * D_jj per contact ([n_contacts]).  Any pointer may be NULL. */
 int sim_debug_contact_state(sim_handle *h, double *theta, double *cdiag, double *hvec, double *dxt,
                             int32_t *slot_vertex, double *djj);
+/* Phase timestamps (us since the CR kernel started) of the most recent CR
+ * solve: [1] rho built, [2] active set + G_A gathered, [3 + it] after CR
+ * iteration it, [20] loop end, [21] epilogue end.  out must hold 32 doubles. */
+int sim_debug_cr_timeline(sim_handle *h, double *out);
 
 #ifdef __cplusplus
 }

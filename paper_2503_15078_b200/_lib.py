@@ -16,7 +16,7 @@ EXPORTED_SYMBOLS = [
     "sim_synchronize", "sim_set_pin_velocity", "sim_get_state", "sim_set_state", "sim_get_lambda",
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
-    "sim_get_kernel_times", "sim_debug_contact_state",
+    "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2"]
 
@@ -80,6 +80,7 @@ def _load():
         "sim_set_profiling": [H, C.c_int],
         "sim_get_kernel_times": [H, dp, C.c_int32],
         "sim_debug_contact_state": [H, dp, dp, dp, dp, ip, dp],
+        "sim_debug_cr_timeline": [H, dp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -268,3 +269,9 @@ def debug_contact_state(sim):
     _check(lib.sim_debug_contact_state(sim._h, _dptr(th), _dptr(cd), _dptr(hv), _dptr(dxt),
                                        sv.ctypes.data_as(C.POINTER(C.c_int32)), _dptr(djj)))
     return {"theta": th, "cdiag": cd, "hvec": hv, "dxt": dxt[:ns], "slot_vertex": sv[:ns], "djj": djj[:nc]}
+
+
+def debug_cr_timeline(sim):
+    out = np.zeros(32)
+    _check(lib.sim_debug_cr_timeline(sim._h, _dptr(out)))
+    return out

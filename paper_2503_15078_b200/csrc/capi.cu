@@ -103,6 +103,8 @@ struct sim_handle {
     std::vector<DContact> hc;
     std::vector<int32_t> slot_vtx_h;
     DBuf<DContact> dc;
+    DBuf<float> cc9;
+    DBuf<int32_t> cs0, cv0, cc1;
     DBuf<int32_t> slot_vtx, scp, sci, vcp, vci;
     DBuf<float> scw, vcw;
     DBuf<double> G, GA;   // Delassus Gram and the CR's active-block scratch
@@ -217,7 +219,7 @@ extern "C" void sim_destroy(sim_handle* H) {
         H->ptop.release(); H->p1.release(); H->p1b.release(); H->p2b.release();
         H->part1.release(); H->counters.release();
         H->chain_off.release(); H->chain_rows.release(); H->flag.release(); H->ucount.release(); H->ulist.release(); H->Zc.release();
-        H->dc.release(); H->slot_vtx.release(); H->scp.release(); H->sci.release(); H->vcp.release();
+        H->dc.release(); H->cc9.release(); H->cs0.release(); H->cv0.release(); H->cc1.release(); H->slot_vtx.release(); H->scp.release(); H->sci.release(); H->vcp.release();
         H->vci.release(); H->scw.release(); H->vcw.release(); H->G.release(); H->GA.release(); H->lam.release();
         H->theta.release(); H->cdiag.release(); H->hvec.release(); H->hl.release(); H->dxt.release();
         H->wz.release(); H->phi_abs.release(); H->cr_res.release();
@@ -323,6 +325,8 @@ static int upload_all(sim_handle* H) {
     CK(cudaMemsetAsync(H->counters.p, 0, ncnt * sizeof(int), st));
     // contact buffers at capacity (pointers stay fixed for graph reuse)
     CK(H->dc.alloc(kMaxContacts));
+    CK(H->cc9.alloc(9 * kMaxContacts)); CK(H->cs0.alloc(kMaxContacts)); CK(H->cv0.alloc(kMaxContacts));
+    CK(H->cc1.alloc(kMaxSlots));
     CK(H->slot_vtx.alloc(kMaxSlots));
     CK(H->scp.alloc(kMaxSlots + 1));
     CK(H->sci.alloc(4 * kMaxContacts));
@@ -488,6 +492,25 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
     for (int i = 0; i < H->n_f; ++i) vcp[i + 1] += vcp[i];
     cudaStream_t st = H->stream;
     CK(H->dc.upload(hc.data(), n, st));
+    {
+        std::vector<float> c9(9 * (size_t)n);
+        std::vector<int32_t> s0(n), v0(n);
+        for (int q = 0; q < n; ++q) {
+            for (int a = 0; a < 3; ++a)
+                for (int d = 0; d < 3; ++d) c9[9 * q + 3 * a + d] = (float)hc[q].c[a][d];
+            const bool single = hc[q].nv == 1 && hc[q].w[0] == 1.0;
+            s0[q] = single ? hc[q].slot[0] : -1;
+            v0[q] = single ? hc[q].vtx[0] : -1;
+        }
+        CK(H->cc9.upload(c9.data(), c9.size(), st));
+        CK(H->cs0.upload(s0.data(), n, st));
+        CK(H->cv0.upload(v0.data(), n, st));
+        std::vector<int32_t> c1(ns, -1);
+        for (int s = 0; s < ns; ++s)
+            if (scp[s + 1] - scp[s] == 1 && s0[sci[scp[s]]] == s) c1[s] = sci[scp[s]];
+        CK(H->cc1.upload(c1.data(), ns, st));
+        CK(cudaStreamSynchronize(st));   // host staging vectors go out of scope
+    }
     CK(H->slot_vtx.upload(verts.data(), ns, st));
     CK(H->scp.upload(scp.data(), ns + 1, st));
     CK(H->sci.upload(sci.data(), sci.size(), st));
@@ -591,7 +614,8 @@ static int enqueue_frame(sim_handle* H, int iters) {
             launch_chain_dot(st, H->ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
                              H->y.p, H->dxt.p); nk++;
             MARK(KK_CR);
-            int e = launch_cr(st, P, H->dc.p, H->slot_vtx.p, H->scp.p, H->sci.p, H->scw.p, H->G.p, H->GA.p, H->x.p, cs); nk++;
+            int e = launch_cr(st, P, H->dc.p, CrContacts{H->cc9.p, H->cs0.p, H->cv0.p, H->cc1.p}, H->slot_vtx.p, H->scp.p,
+                              H->sci.p, H->scw.p, H->G.p, H->GA.p, H->x.p, cs); nk++;
             if (e) return -e;
             MARK(KK_SCATTER);
             launch_scatter(st, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
@@ -896,5 +920,18 @@ extern "C" int sim_debug_contact_state(sim_handle* H, double* theta, double* cdi
         CK(cudaMemcpy(hc.data(), H->dc.p, H->nc * sizeof(DContact), cudaMemcpyDeviceToHost));
         for (int c = 0; c < H->nc; ++c) djj[c] = hc[c].Djj;
     }
+    return SIM_OK;
+}
+
+// phase timestamps (ns, %globaltimer) of the most recent CR call: [0] start,
+// [1] after rho, [2] after active set + G_A gather, [3 + it] after CR iteration it,
+// [20] loop end, [21] epilogue end.  out must hold 32 values.
+extern "C" int sim_debug_cr_timeline(sim_handle* H, double* out) {
+    if (!H || !out) return fail(SIM_E_INVALID, "null argument");
+    if (H->host_only) return fail(SIM_E_STATE, "no device");
+    CK(cudaStreamSynchronize(H->stream));
+    unsigned long long t[32];
+    CK((cudaError_t)read_cr_clock(t));
+    for (int i = 0; i < 32; ++i) out[i] = (double)(t[i] - t[0]) * 1e-3;   // us since start
     return SIM_OK;
 }

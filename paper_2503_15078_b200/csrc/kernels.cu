@@ -705,12 +705,28 @@ __global__ void k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx, const 
     const float* col = Kcol + colptr[a];
     const int o0 = chain_off[s], len = chain_off[s + 1] - o0;
     double a0 = 0, a1 = 0, a2 = 0;
-    for (int k = lane; k < len; k += 32) {
-        const double kv = __ldg(&col[k]);
-        const float4 yy = __ldg(&y[__ldg(&chain_rows[o0 + k])]);
-        a0 = fma(kv, (double)yy.x, a0);
-        a1 = fma(kv, (double)yy.y, a1);
-        a2 = fma(kv, (double)yy.z, a2);
+    for (int k0 = 0; k0 < len; k0 += 128) {   // 4 independent gathers in flight per lane
+        int rw[4];
+        float kv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = k0 + 32 * u + lane;
+            rw[u] = k < len ? __ldg(&chain_rows[o0 + k]) : -1;
+            kv[u] = k < len ? __ldg(&col[k]) : 0.f;
+        }
+        float4 yy[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) yy[u] = rw[u] >= 0 ? __ldg(&y[rw[u]]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            f0 = fmaf(kv[u], yy[u].x, f0);
+            f1 = fmaf(kv[u], yy[u].y, f1);
+            f2 = fmaf(kv[u], yy[u].z, f2);
+        }
+        a0 += (double)f0;
+        a1 += (double)f1;
+        a2 += (double)f2;
     }
     a0 = warp_sum(a0);
     a1 = warp_sum(a1);
@@ -807,11 +823,17 @@ __global__ void k_scatter(const int* __restrict__ ucount, const int4* __restrict
         const int4 u = ulist[e];
         const float* zr = Zc + u.w - u.y;   // zr[s] = K[i][a_s]
         double a0 = 0, a1 = 0, a2 = 0;
-        for (int s = u.y + lane; s < u.z; s += 32) {
-            const double kv = __ldg(&zr[s]);
-            a0 = fma(kv, wz[3 * s], a0);
-            a1 = fma(kv, wz[3 * s + 1], a1);
-            a2 = fma(kv, wz[3 * s + 2], a2);
+        for (int s0 = u.y; s0 < u.z; s0 += 64) {   // 2 independent iterations in flight
+            const int sa = s0 + lane, sb = s0 + 32 + lane;
+            const double ka = sa < u.z ? (double)__ldg(&zr[sa]) : 0.0;
+            const double kb = sb < u.z ? (double)__ldg(&zr[sb]) : 0.0;
+            const int ia = min(sa, u.z - 1), ib = min(sb, u.z - 1);
+            a0 = fma(ka, wz[3 * ia], a0);
+            a1 = fma(ka, wz[3 * ia + 1], a1);
+            a2 = fma(ka, wz[3 * ia + 2], a2);
+            a0 = fma(kb, wz[3 * ib], a0);
+            a1 = fma(kb, wz[3 * ib + 1], a1);
+            a2 = fma(kb, wz[3 * ib + 2], a2);
         }
         a0 = warp_sum(a0);
         a1 = warp_sum(a1);
@@ -850,63 +872,77 @@ __global__ void __launch_bounds__(256) k_delassus(int ns, const int32_t* __restr
                                                   const int32_t* __restrict__ depth, const int32_t* __restrict__ parent,
                                                   const int32_t* __restrict__ ptop, double* __restrict__ G) {
     // tile (bs, bt) with bt >= bs from a linear triangular index
-    int tiles = (ns + 31) / 32;
+    const int tiles = (ns + 31) / 32;
     int idx = blockIdx.x, bs = 0;
     while (idx >= tiles - bs) { idx -= tiles - bs; ++bs; }
-    int bt = bs + idx;
-    __shared__ float Zs[32][33], Zt[32][33];
+    const int bt = bs + idx;
+    __shared__ float Zs[2][32][33], Zt[2][32][33];
     __shared__ int ds_[32], dt_[32];
     __shared__ int64_t cs_[32], ct_[32];
-    int tid = threadIdx.x;
+    __shared__ int smax;
+    const int tid = threadIdx.x;
     if (tid < 32) {
-        int s = bs * 32 + tid;
-        if (s < ns) { int a = slot_vtx[s]; ds_[tid] = depth[a]; cs_[tid] = colptr[a]; }
+        const int s = bs * 32 + tid;
+        if (s < ns) { const int a = slot_vtx[s]; ds_[tid] = depth[a]; cs_[tid] = colptr[a]; }
         else { ds_[tid] = -1; cs_[tid] = 0; }
     } else if (tid < 64) {
-        int t = bt * 32 + tid - 32;
-        if (t < ns) { int a = slot_vtx[t]; dt_[tid - 32] = depth[a]; ct_[tid - 32] = colptr[a]; }
+        const int t = bt * 32 + tid - 32;
+        if (t < ns) { const int a = slot_vtx[t]; dt_[tid - 32] = depth[a]; ct_[tid - 32] = colptr[a]; }
         else { dt_[tid - 32] = -1; ct_[tid - 32] = 0; }
     }
+    if (tid == 0) smax = -1;
     __syncthreads();
     // thread owns pairs (ls, lt0..lt0+3)
-    int ls = tid >> 3, lt0 = (tid & 7) * 4;
-    int s = bs * 32 + ls;
+    const int ls = tid >> 3, lt0 = (tid & 7) * 4;
+    const int s = bs * 32 + ls;
     int dl[4];
     int maxd = -1;
     for (int q = 0; q < 4; ++q) {
-        int t = bt * 32 + lt0 + q;
+        const int t = bt * 32 + lt0 + q;
         dl[q] = (s < ns && t < ns) ? lca_depth(slot_vtx[s], slot_vtx[t], parent, ptop, depth) : -1;
         maxd = max(maxd, dl[q]);
     }
-    // block-wide max depth needed
-    __shared__ int smax;
-    if (tid == 0) smax = -1;
-    __syncthreads();
     atomicMax(&smax, maxd);
     __syncthreads();
-    int D = smax;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int d0 = 0; d0 <= D; d0 += 32) {
-        // stage Z[d0 + dd][slot] for both slot blocks (coalesced along depth per slot)
-        for (int e = tid; e < 32 * 32; e += 256) {
-            int sl = e >> 5, dd = e & 31;
-            int d = d0 + dd;
-            Zs[dd][sl] = (ds_[sl] >= d) ? Kcol[cs_[sl] + ds_[sl] - d] : 0.f;
-            Zt[dd][sl] = (dt_[sl] >= d) ? Kcol[ct_[sl] + dt_[sl] - d] : 0.f;
+    const int D = smax;
+    // staging: each thread loads 4 (slot, depth) entries of each block per 32-level chunk
+    float rs[4], rt[4];
+    auto fetch = [&](int d0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + 256 * u;
+            const int sl = e >> 5, dd = e & 31, d = d0 + dd;
+            rs[u] = (ds_[sl] >= d) ? __ldg(&Kcol[cs_[sl] + ds_[sl] - d]) : 0.f;
+            rt[u] = (dt_[sl] >= d) ? __ldg(&Kcol[ct_[sl] + dt_[sl] - d]) : 0.f;
         }
+    };
+    auto stash = [&](int buf) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + 256 * u;
+            Zs[buf][e & 31][e >> 5] = rs[u];
+            Zt[buf][e & 31][e >> 5] = rt[u];
+        }
+    };
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (D >= 0) fetch(0);
+    int buf = 0;
+    for (int d0 = 0; d0 <= D; d0 += 32) {
+        stash(buf);
         __syncthreads();
-#pragma unroll 4
+        if (d0 + 32 <= D) fetch(d0 + 32);   // next chunk in flight while this one is consumed
+#pragma unroll 8
         for (int dd = 0; dd < 32; ++dd) {
-            int d = d0 + dd;
-            float zs = Zs[dd][ls];
+            const int d = d0 + dd;
+            const float zs = Zs[buf][dd][ls];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (d <= dl[q]) acc[q] = fmaf(zs, Zt[dd][lt0 + q], acc[q]);
+                if (d <= dl[q]) acc[q] = fmaf(zs, Zt[buf][dd][lt0 + q], acc[q]);
         }
-        __syncthreads();
+        buf ^= 1;
     }
     for (int q = 0; q < 4; ++q) {
-        int t = bt * 32 + lt0 + q;
+        const int t = bt * 32 + lt0 + q;
         if (s < ns && t < ns) {
             G[(size_t)s * ns + t] = (double)acc[q];
             G[(size_t)t * ns + s] = (double)acc[q];
@@ -946,56 +982,49 @@ void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const double* G) {
 // * Theta-sparsity: rows with theta = 0 (separated contacts, inactive
 //   friction) contribute nothing to Theta D Theta, so the D product only runs
 //   over the "active" contact vertices (any row with theta != 0).  The active
-//   block G_A of G is gathered once per CR call (exact, not an approximation).
-// * Every CTA keeps full fp64 copies of the row vectors and the compact
-//   contact geometry in shared memory and performs the O(m) work redundantly
-//   (dot products are identical everywhere without communication); the
-//   product q = G_A W is split by rows and exchanged through DSMEM.
+//   block G_A of G is gathered once per CR call (exact, not an approximation),
+//   into shared memory when this CTA's rows fit.
+// * Every CTA runs the O(m) recurrences redundantly (dot products come out
+//   identical everywhere without communication).  Each thread owns rows
+//   j = tid + 512 k: z, p, Ap, Ar live in its registers; only r (read by the
+//   W gather) is in shared memory.  q = G_A W is split by rows of G_A and
+//   exchanged through DSMEM (one cluster barrier per matvec).
 // * fp64 in the D product: G = A_v^-1 is a smoothing kernel, so G W cancels
 //   heavily for the oscillatory Krylov vectors (fp32 W or fp32 sums cost ~3e-3).
 //   (S v)_j = theta_j c_j . sum_{a in j} w_ja q_a + C_j v_j,
 //   q_a = sum_b G_ab W_b,   W_b = sum_{rows k at b} w_kb theta_k c_k v_k.
 // ----------------------------------------------------------------------------
+constexpr int kRpt = 6;   // rows per thread: m = 3 nc <= kRpt * kCrThreads
+
 struct CrLayout {
     int m, nc, ns;
-    size_t z, r, p, Ar, Ap, th, cd, c9, s0, W, q, aidx, apos, red, total;
+    size_t r, th, cd, c9, s0, W, q, aidx, apos, acon, red, mbar, gA, total;
     __host__ __device__ CrLayout(int nc_, int ns_) : m(3 * nc_), nc(nc_), ns(ns_) {
         size_t o = 0;
         auto take = [&](size_t bytes) { size_t at = o; o += (bytes + 15) & ~size_t(15); return at; };
-        z = take(8 * (size_t)m); r = take(8 * (size_t)m); p = take(8 * (size_t)m);
-        Ar = take(8 * (size_t)m); Ap = take(8 * (size_t)m);
+        r = take(8 * (size_t)m);
         th = take(4 * (size_t)m); cd = take(4 * (size_t)m);
         c9 = take(4 * 9 * (size_t)nc); s0 = take(4 * (size_t)nc);
         W = take(8 * 3 * (size_t)ns); q = take(8 * 2 * 3 * (size_t)ns);
-        aidx = take(4 * (size_t)ns); apos = take(4 * (size_t)ns);
-        red = take(8 * 2 * (kCrThreads / 32) + 4 * (kCrThreads / 32 + 1));
+        aidx = take(4 * (size_t)ns); apos = take(4 * (size_t)ns); acon = take(4 * (size_t)ns);
+        red = take(8 * 3 * (kCrThreads / 32) + 4 * (kCrThreads / 32 + 1));   // 3 doubles/warp + scan ints
+        mbar = take(16);
+        gA = o;
         total = o;
     }
 };
 
-struct CrView {
-    double *z, *r, *p, *Ar, *Ap, *red, *W, *q;
-    float *th, *cd, *c9;
-    int *s0, *aidx, *apos;
-};
-
-__device__ __forceinline__ CrView cr_view(unsigned char* base, const CrLayout& L) {
-    CrView v;
-    v.z = (double*)(base + L.z); v.r = (double*)(base + L.r); v.p = (double*)(base + L.p);
-    v.Ar = (double*)(base + L.Ar); v.Ap = (double*)(base + L.Ap); v.red = (double*)(base + L.red);
-    v.th = (float*)(base + L.th); v.cd = (float*)(base + L.cd); v.c9 = (float*)(base + L.c9);
-    v.W = (double*)(base + L.W); v.q = (double*)(base + L.q); v.s0 = (int*)(base + L.s0);
-    v.aidx = (int*)(base + L.aidx); v.apos = (int*)(base + L.apos);
-    return v;
+__device__ __forceinline__ double block_sum(double s, double* red) {
+    s = warp_sum(s);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = s;
+    __syncthreads();
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+    return t;
 }
-
-__device__ __forceinline__ void block_dot2(const double* a, const double* b, const double* c, const double* d, int m,
-                                           double* red, double& o1, double& o2) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        s1 = fma(a[i], b[i], s1);
-        s2 = fma(c[i], d[i], s2);
-    }
+__device__ __forceinline__ void block_sum2(double s1, double s2, double* red, double& o1, double& o2) {
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -1008,147 +1037,246 @@ __device__ __forceinline__ void block_dot2(const double* a, const double* b, con
     o2 = t2;
 }
 
-// out = S v  (all CTAs end with the full result).  GA: na x na active block of G.
-__device__ void cr_apply(cg::cluster_group& cl, const CrView& sv, const CrLayout& L, int na, const double* v,
-                         double* out, const DContact* __restrict__ C, const int32_t* __restrict__ scp,
-                         const int32_t* __restrict__ sci, const float* __restrict__ scw,
-                         const double* __restrict__ GA, int buf) {
-    const int m = L.m;
-    double* qb = sv.q + (size_t)buf * 3 * L.ns;   // indexed by active position
-    // W over the active slots (redundant in every CTA), SoA W0 | W1 | W2
+struct CrCtx {
+    double *r, *W, *q, *red, *gA;
+    float *th, *cd, *c9;
+    int *s0, *aidx, *apos, *acon;
+    int na, i0, i1, gA_smem;
+    unsigned mbar;   // shared-window address of this CTA's exchange mbarrier
+    unsigned phase;  // parity of the exchange phase being waited for
+    const double* GAg;   // global fallback for this CTA's G_A rows
+};
+
+// Ar = S r for this thread's rows (registers); r is read from shared memory
+__device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m, const DContact* __restrict__ C,
+                                         const int32_t* __restrict__ scp, const int32_t* __restrict__ sci,
+                                         const float* __restrict__ scw, int buf, double (&Ar)[kRpt]) {
+    const int na = X.na;
+    double* qb = X.q + (size_t)buf * 3 * na;
     for (int i = threadIdx.x; i < na; i += blockDim.x) {
-        const int b = sv.aidx[i];
         double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-        for (int p = __ldg(&scp[b]); p < __ldg(&scp[b + 1]); ++p) {
-            const int c = __ldg(&sci[p]);
-            const double wt = __ldg(&scw[p]);
-            const float* cc = sv.c9 + 9 * c;
+        const int c1 = X.acon[i];
+        if (c1 >= 0) {   // a single single-vertex contact on this slot (weight 1)
+            const float* cc = X.c9 + 9 * c1;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const double tv = wt * (double)sv.th[3 * c + k] * v[3 * c + k];
+                const double tv = (double)X.th[3 * c1 + k] * X.r[3 * c1 + k];
                 w0 = fma(tv, (double)cc[3 * k], w0);
                 w1 = fma(tv, (double)cc[3 * k + 1], w1);
                 w2 = fma(tv, (double)cc[3 * k + 2], w2);
             }
+        } else {
+            const int b = X.aidx[i];
+            for (int p = __ldg(&scp[b]); p < __ldg(&scp[b + 1]); ++p) {
+                const int c = __ldg(&sci[p]);
+                const double wt = __ldg(&scw[p]);
+                const float* cc = X.c9 + 9 * c;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double tv = wt * (double)X.th[3 * c + k] * X.r[3 * c + k];
+                    w0 = fma(tv, (double)cc[3 * k], w0);
+                    w1 = fma(tv, (double)cc[3 * k + 1], w1);
+                    w2 = fma(tv, (double)cc[3 * k + 2], w2);
+                }
+            }
         }
-        sv.W[i] = w0;
-        sv.W[na + i] = w1;
-        sv.W[2 * na + i] = w2;
+        X.W[i] = w0;
+        X.W[na + i] = w1;
+        X.W[2 * na + i] = w2;
     }
     __syncthreads();
-    const int rank = cl.block_rank();
-    const int per = (na + kCluster - 1) / kCluster;
-    const int i0 = rank * per, i1 = min(na, i0 + per);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const double* W0 = sv.W;
-    const double* W1 = sv.W + na;
-    const double* W2 = sv.W + 2 * na;
-    for (int i = i0 + wid; i < i1; i += nw) {
-        const double* g = GA + (size_t)i * na;
+    for (int i = X.i0 + wid; i < X.i1; i += nw) {
+        const double* g = X.gA_smem ? X.gA + (size_t)(i - X.i0) * na : X.GAg + (size_t)i * na;
         double d0 = 0, d1 = 0, d2 = 0;
         for (int b0 = 0; b0 < na; b0 += 128) {
             double gv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int bb = b0 + 32 * u + lane;
-                gv[u] = bb < na ? __ldcg(&g[bb]) : 0.0;
+                gv[u] = bb < na ? (X.gA_smem ? g[bb] : __ldcg(&g[bb])) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int bb = min(b0 + 32 * u + lane, na - 1);
-                d0 = fma(gv[u], W0[bb], d0);
-                d1 = fma(gv[u], W1[bb], d1);
-                d2 = fma(gv[u], W2[bb], d2);
+                d0 = fma(gv[u], X.W[bb], d0);
+                d1 = fma(gv[u], X.W[na + bb], d1);
+                d2 = fma(gv[u], X.W[2 * na + bb], d2);
             }
         }
         d0 = warp_sum(d0);
         d1 = warp_sum(d1);
         d2 = warp_sum(d2);
         if (lane < kCluster) {
+            // write q_i into CTA `lane`, then arrive (release) on that CTA's mbarrier:
+            // each peer expects exactly na arrivals per exchange (one per row of G_A)
             double* rq = cl.map_shared_rank(qb, lane);
             rq[3 * i] = d0;
             rq[3 * i + 1] = d1;
             rq[3 * i + 2] = d2;
+            unsigned remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(X.mbar), "r"(lane));
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
         }
     }
-    cl.sync();
-    // (S v)_j (redundant)
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        const int c = j / 3, k = j - 3 * c;
-        const double th = (double)sv.th[j];
+    if (threadIdx.x == 0 && na > 0) {   // wait for all na rows of q (acquire), then release the CTA
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+                " selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(X.mbar), "r"(X.phase)
+                : "memory");
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRpt; ++k) {
+        const int j = min(threadIdx.x + kCrThreads * k, m - 1);   // rows >= m are padding (never used)
+        const int c = j / 3, kk = j - 3 * c;
+        const double th = (double)X.th[j];
         double acc = 0.0;
         if (th != 0.0) {
-            const float* cc = sv.c9 + 9 * c + 3 * k;
-            const int sl0 = sv.s0[c];
-            if (sl0 >= 0) {   // single-vertex contact, weight 1
-                const int ip = sv.apos[sl0];
+            const float* cc = X.c9 + 9 * c + 3 * kk;
+            const int sl0 = X.s0[c];
+            if (sl0 >= 0) {
+                const int ip = X.apos[sl0];
                 acc = (double)cc[0] * qb[3 * ip] + (double)cc[1] * qb[3 * ip + 1] + (double)cc[2] * qb[3 * ip + 2];
             } else {
                 const DContact& ct = C[c];
                 for (int p = 0; p < ct.nv; ++p) {
-                    const int ip = sv.apos[ct.slot[p]];
+                    const int ip = X.apos[ct.slot[p]];
                     acc += ct.w[p] * ((double)cc[0] * qb[3 * ip] + (double)cc[1] * qb[3 * ip + 1] +
                                       (double)cc[2] * qb[3 * ip + 2]);
                 }
             }
         }
-        out[j] = th * acc + (double)sv.cd[j] * v[j];
+        Ar[k] = th * acc + (double)X.cd[j] * X.r[j];
     }
-    __syncthreads();
+    X.phase ^= 1u;
+}
+
+__device__ unsigned long long g_cr_clock[32];   // phase timestamps (ns) of the last CR call, rank 0
+__device__ __forceinline__ void cr_stamp(int i) {
+    if (threadIdx.x == 0 && cg::this_cluster().block_rank() == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_cr_clock[i] = t;
+    }
 }
 
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1)
-    k_cr(Params P, const DContact* __restrict__ C, const int32_t* __restrict__ slot_vtx,
+    k_cr(Params P, const DContact* __restrict__ C, CrContacts cc, const int32_t* __restrict__ slot_vtx,
          const int32_t* __restrict__ scp, const int32_t* __restrict__ sci, const float* __restrict__ scw,
-         const double* __restrict__ G, double* __restrict__ GA, const double4* __restrict__ x, ContactState cs) {
+         const double* __restrict__ G, double* __restrict__ GA, const double4* __restrict__ x, ContactState cs,
+         int gA_cap) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const CrLayout L(P.nc, P.ns);
-    const CrView sv = cr_view(smraw, L);
     cg::cluster_group cl = cg::this_cluster();
     const int nc = P.nc, ns = P.ns, m = 3 * nc;
     const double h = P.h;
-    // contact geometry -> shared memory
-    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-        const DContact& ct = C[c];
+    cr_stamp(0);
+    CrCtx X;
+    X.r = (double*)(smraw + L.r);
+    X.th = (float*)(smraw + L.th);
+    X.cd = (float*)(smraw + L.cd);
+    X.c9 = (float*)(smraw + L.c9);
+    X.s0 = (int*)(smraw + L.s0);
+    X.W = (double*)(smraw + L.W);
+    X.q = (double*)(smraw + L.q);
+    X.aidx = (int*)(smraw + L.aidx);
+    X.apos = (int*)(smraw + L.apos);
+    X.acon = (int*)(smraw + L.acon);
+    X.red = (double*)(smraw + L.red);
+    X.gA = (double*)(smraw + L.gA);
+    for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[e], true);
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) cp_async4(&X.s0[c], &cc.s0[c], true);
+    cp_async_commit();
+    X.mbar = (unsigned)__cvta_generic_to_shared(smraw + L.mbar);
+    X.phase = 0u;
+    cr_stamp(22);
+    // rho_j = h_j - theta_j c_j . x~_c, x~ = x^k + K^T y at the contact vertices (owner rows)
+    double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
+    // independent loads first (no early exit, so they overlap), then the x/dxt gathers
+    int v0r[kRpt], s0r[kRpt];
+    double thr[kRpt], hvr[kRpt], cdr[kRpt], lamr[kRpt];
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-#pragma unroll
-            for (int d = 0; d < 3; ++d) sv.c9[9 * c + 3 * k + d] = (float)ct.c[k][d];
-        sv.s0[c] = (ct.nv == 1 && ct.w[0] == 1.0) ? ct.slot[0] : -1;
+    for (int k = 0; k < kRpt; ++k) {
+        z[k] = p[k] = Ap[k] = Ar[k] = 0.0;
+        const int j = threadIdx.x + kCrThreads * k;
+        const bool ok = j < m;
+        const int c = ok ? j / 3 : 0;
+        v0r[k] = ok ? __ldg(&cc.v0[c]) : -1;
+        s0r[k] = ok ? __ldg(&cc.s0[c]) : -1;
+        thr[k] = ok ? cs.theta[j] : 0.0;
+        hvr[k] = ok ? cs.hvec[j] : 0.0;
+        cdr[k] = ok ? cs.cdiag[j] : 0.0;
+        lamr[k] = ok ? cs.lam[j] : 0.0;
     }
-    // rho_j = h_j - theta_j c_j . x~_c, x~ = x^k + K^T y at the contact vertices
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
-        const int c = j / 3, k = j - 3 * c;
-        const DContact& ct = C[c];
-        double xs[3] = {0, 0, 0};
-        for (int p = 0; p < ct.nv; ++p) {
-            const double4 xa = x[ct.vtx[p]];
-            const int sl = ct.slot[p];
-            xs[0] += ct.w[p] * (xa.x + cs.dxt[3 * sl]);
-            xs[1] += ct.w[p] * (xa.y + cs.dxt[3 * sl + 1]);
-            xs[2] += ct.w[p] * (xa.z + cs.dxt[3 * sl + 2]);
+    cr_stamp(23);
+    double4 xar[kRpt];
+    double d0r[kRpt], d1r[kRpt], d2r[kRpt];
+#pragma unroll
+    for (int k = 0; k < kRpt; ++k) {
+        const bool single = v0r[k] >= 0;
+        xar[k] = single ? x[v0r[k]] : make_double4(0, 0, 0, 0);
+        d0r[k] = single ? cs.dxt[3 * s0r[k]] : 0.0;
+        d1r[k] = single ? cs.dxt[3 * s0r[k] + 1] : 0.0;
+        d2r[k] = single ? cs.dxt[3 * s0r[k] + 2] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kRpt; ++k) {
+        const int j = threadIdx.x + kCrThreads * k;
+        if (j < m) {
+            const int c = j / 3, kk = j - 3 * c;
+            double xs0, xs1, xs2;
+            if (v0r[k] >= 0) {
+                xs0 = xar[k].x + d0r[k];
+                xs1 = xar[k].y + d1r[k];
+                xs2 = xar[k].z + d2r[k];
+            } else {   // general multi-vertex contact
+                const DContact& ct = C[c];
+                xs0 = xs1 = xs2 = 0.0;
+                for (int q = 0; q < ct.nv; ++q) {
+                    const double4 xa = x[ct.vtx[q]];
+                    const int sl = ct.slot[q];
+                    xs0 += ct.w[q] * (xa.x + cs.dxt[3 * sl]);
+                    xs1 += ct.w[q] * (xa.y + cs.dxt[3 * sl + 1]);
+                    xs2 += ct.w[q] * (xa.z + cs.dxt[3 * sl + 2]);
+                }
+            }
+            const float* c3 = cc.c9 + 9 * c + 3 * kk;
+            const double rho = hvr[k] - thr[k] * ((double)__ldg(&c3[0]) * xs0 + (double)__ldg(&c3[1]) * xs1 +
+                                                  (double)__ldg(&c3[2]) * xs2);
+            X.th[j] = (float)thr[k];
+            X.cd[j] = (float)cdr[k];
+            X.r[j] = rho;
+            p[k] = rho;
         }
-        const double th = cs.theta[j];
-        const double rho = cs.hvec[j] - th * (ct.c[k][0] * xs[0] + ct.c[k][1] * xs[1] + ct.c[k][2] * xs[2]);
-        sv.th[j] = (float)th;
-        sv.cd[j] = (float)cs.cdiag[j];
-        sv.r[j] = rho;
-        sv.p[j] = rho;
-        sv.z[j] = 0.0;
     }
+    cp_async_wait<0>();
     __syncthreads();
-    // active slots: any incident row with theta != 0; ascending slot order (block scan)
-    int* cnt = reinterpret_cast<int*>(sv.red + 2 * (kCrThreads / 32));   // [0] running count, [1..16] warp sums
+    cr_stamp(1);
+    // active slots: any incident row with theta != 0, ascending slot order (block scan)
+    int* cnt = reinterpret_cast<int*>(X.red + 3 * (kCrThreads / 32));
     if (threadIdx.x == 0) cnt[0] = 0;
     __syncthreads();
     for (int b0 = 0; b0 < ns; b0 += blockDim.x) {
         const int b = b0 + threadIdx.x;
         bool act = false;
-        if (b < ns)
-            for (int p = scp[b]; p < scp[b + 1] && !act; ++p) {
-                const int c = sci[p];
-                act = sv.th[3 * c] != 0.f || sv.th[3 * c + 1] != 0.f || sv.th[3 * c + 2] != 0.f;
+        int only = -1;
+        if (b < ns) {
+            only = __ldg(&cc.c1[b]);
+            if (only >= 0) {
+                act = X.th[3 * only] != 0.f || X.th[3 * only + 1] != 0.f || X.th[3 * only + 2] != 0.f;
+            } else {
+                for (int q = scp[b]; q < scp[b + 1] && !act; ++q) {
+                    const int c = sci[q];
+                    act = X.th[3 * c] != 0.f || X.th[3 * c + 1] != 0.f || X.th[3 * c + 2] != 0.f;
+                }
             }
+        }
         const unsigned bal = __ballot_sync(0xffffffffu, act);
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         if (lane == 0) cnt[1 + wid] = __popc(bal);
@@ -1157,8 +1285,11 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
         for (int q = 0; q < wid; ++q) off += cnt[1 + q];
         off += __popc(bal & ((1u << lane) - 1u));
         if (b < ns) {
-            sv.apos[b] = act ? off : -1;
-            if (act) sv.aidx[off] = b;
+            X.apos[b] = act ? off : -1;
+            if (act) {
+                X.aidx[off] = b;
+                X.acon[off] = only;
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -1169,88 +1300,162 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
         __syncthreads();
     }
     const int na = cnt[0];
-    // gather this CTA's rows of the active block G_A (only this CTA reads them)
+    X.na = na;
+    if (threadIdx.x == 0 && na > 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(X.mbar), "r"(na));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cl.sync();   // every CTA's exchange mbarrier is initialised before any remote arrive
+    cr_stamp(24);
     {
         const int per = (na + kCluster - 1) / kCluster;
-        const int i0 = cl.block_rank() * per, i1 = min(na, i0 + per);
-        for (int e = threadIdx.x; e < (i1 - i0) * na; e += blockDim.x) {
-            const int i = i0 + e / na, jj = e % na;
-            GA[(size_t)i * na + jj] = G[(size_t)sv.aidx[i] * ns + sv.aidx[jj]];
+        X.i0 = min(na, (int)cl.block_rank() * per);
+        X.i1 = min(na, X.i0 + per);
+        X.gA_smem = (size_t)(X.i1 - X.i0) * na <= (size_t)gA_cap;
+        X.GAg = GA;
+        double* dst = X.gA_smem ? X.gA : GA + (size_t)X.i0 * na;
+        for (int e = threadIdx.x; e < (X.i1 - X.i0) * na; e += blockDim.x) {
+            const int i = X.i0 + e / na, jj = e % na;
+            dst[e] = __ldg(&G[(size_t)X.aidx[i] * ns + X.aidx[jj]]);
         }
     }
     __syncthreads();
-    double rr, dummy;
-    block_dot2(sv.r, sv.r, sv.r, sv.r, m, sv.red, rr, dummy);
+    cr_stamp(2);
+    double rr = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRpt; ++k) rr = fma(p[k], p[k], rr);
+    rr = block_sum(rr, X.red);
+    // CR with one block reduction per iteration: after Ar = S r the three dots
+    // r.Ar, Ar.Ar, Ar.Ap give beta and |Ap_new|^2 = Ar.Ar + 2 beta Ar.Ap +
+    // beta^2 |Ap|^2 (algebraically identical to the direct form of the oracle).
     if (rr > 0.0 && P.cr_iters > 0) {
-        int buf = 0;
-        cr_apply(cl, sv, L, na, sv.r, sv.Ar, C, scp, sci, scw, GA, buf);
-        buf ^= 1;
-        for (int j = threadIdx.x; j < m; j += blockDim.x) sv.Ap[j] = sv.Ar[j];
-        __syncthreads();
-        double rAr, ApAp;
-        block_dot2(sv.r, sv.Ar, sv.Ap, sv.Ap, m, sv.red, rAr, ApAp);
+        cr_stamp(25);
+        cr_apply(cl, X, m, C, scp, sci, scw, (int)X.phase, Ar);
+        cr_stamp(26);
+        double rAr = 0.0, ApAp = 0.0;
+#pragma unroll
+        for (int k = 0; k < kRpt; ++k) {
+            const int j = threadIdx.x + kCrThreads * k;
+            Ap[k] = Ar[k];
+            if (j < m) {
+                rAr = fma(X.r[j], Ar[k], rAr);
+                ApAp = fma(Ap[k], Ap[k], ApAp);
+            }
+        }
+        block_sum2(rAr, ApAp, X.red, rAr, ApAp);
         for (int it = 0; it < P.cr_iters; ++it) {
             if (ApAp <= 1e-300 || fabs(rAr) <= 1e-300) break;
             const double alpha = rAr / ApAp;
-            for (int j = threadIdx.x; j < m; j += blockDim.x) {
-                sv.z[j] += alpha * sv.p[j];
-                sv.r[j] -= alpha * sv.Ap[j];
+#pragma unroll
+            for (int k = 0; k < kRpt; ++k) {
+                const int j = threadIdx.x + kCrThreads * k;
+                if (j < m) {
+                    z[k] += alpha * p[k];
+                    X.r[j] -= alpha * Ap[k];
+                }
             }
             __syncthreads();
             if (it == P.cr_iters - 1) break;
-            cr_apply(cl, sv, L, na, sv.r, sv.Ar, C, scp, sci, scw, GA, buf);
-            buf ^= 1;
-            double rAr_new, t2;
-            block_dot2(sv.r, sv.Ar, sv.r, sv.r, m, sv.red, rAr_new, t2);
-            const double beta = rAr_new / rAr;
-            rAr = rAr_new;
-            for (int j = threadIdx.x; j < m; j += blockDim.x) {
-                sv.p[j] = sv.r[j] + beta * sv.p[j];
-                sv.Ap[j] = sv.Ar[j] + beta * sv.Ap[j];
+            cr_apply(cl, X, m, C, scp, sci, scw, (int)X.phase, Ar);
+            double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int k = 0; k < kRpt; ++k) {
+                const int j = threadIdx.x + kCrThreads * k;
+                if (j < m) {
+                    s1 = fma(X.r[j], Ar[k], s1);
+                    s2 = fma(Ar[k], Ar[k], s2);
+                    s3 = fma(Ar[k], Ap[k], s3);
+                }
             }
-            __syncthreads();
-            double t1;
-            block_dot2(sv.Ap, sv.Ap, sv.Ap, sv.Ap, m, sv.red, ApAp, t1);
+            s1 = warp_sum(s1);
+            s2 = warp_sum(s2);
+            s3 = warp_sum(s3);
+            {
+                const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+                __syncthreads();
+                if (l == 0) { X.red[3 * w] = s1; X.red[3 * w + 1] = s2; X.red[3 * w + 2] = s3; }
+                __syncthreads();
+                s1 = s2 = s3 = 0.0;
+                for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+                    s1 += X.red[3 * q];
+                    s2 += X.red[3 * q + 1];
+                    s3 += X.red[3 * q + 2];
+                }
+            }
+            const double beta = s1 / rAr;
+            rAr = s1;
+            ApAp = s2 + 2.0 * beta * s3 + beta * beta * ApAp;
+#pragma unroll
+            for (int k = 0; k < kRpt; ++k) {
+                p[k] = (threadIdx.x + kCrThreads * k < m ? X.r[min(threadIdx.x + kCrThreads * k, m - 1)] : 0.0) +
+                       beta * p[k];
+                Ap[k] = Ar[k] + beta * Ap[k];
+            }
+            cr_stamp(3 + it);
+        }
+    }
+    cr_stamp(20);
+    double res = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRpt; ++k) {
+        const int j = threadIdx.x + kCrThreads * k;
+        if (j < m) res = fma(X.r[j], X.r[j], res);
+    }
+    res = block_sum(res, X.red);
+    cr_stamp(27);
+    // epilogue split over the cluster (every CTA holds the identical z):
+    // lambda += z / h^2 (reading A11) for this CTA's rows; z to shared memory (reuse r)
+    const int rank = cl.block_rank();
+    const int rper = (m + kCluster - 1) / kCluster;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRpt; ++k) {
+        const int j = threadIdx.x + kCrThreads * k;
+        if (j < m) {
+            X.r[j] = z[k];
+            if (j / rper == rank) cs.lam[j] = lamr[k] + z[k] / (h * h);
         }
     }
     __syncthreads();
-    block_dot2(sv.r, sv.r, sv.r, sv.r, m, sv.red, rr, dummy);
-    if (cl.block_rank() != 0) {
-        cl.sync();   // keep DSMEM alive until everyone is done
-        return;
-    }
-    // lambda += z / h^2 (reading A11), wz_b = sum w theta z c  (for y += K H^T z)
-    for (int j = threadIdx.x; j < m; j += blockDim.x) cs.lam[j] += sv.z[j] / (h * h);
-    for (int b = threadIdx.x; b < ns; b += blockDim.x) {
+    cr_stamp(28);
+    // wz_b = sum w theta z c  (for y += K H^T z), this CTA's slots
+    const int sper = (ns + kCluster - 1) / kCluster;
+    for (int b = rank * sper + threadIdx.x; b < min(ns, (rank + 1) * sper); b += blockDim.x) {
         double w0 = 0, w1 = 0, w2 = 0;
-        for (int p = scp[b]; p < scp[b + 1]; ++p) {
-            const int c = sci[p];
-            const double wt = scw[p];
-            const DContact& ct = C[c];
+        const int only = __ldg(&cc.c1[b]);
+        const int qa = only >= 0 ? 0 : scp[b], qb = only >= 0 ? 1 : scp[b + 1];
+        for (int q = qa; q < qb; ++q) {
+            const int c = only >= 0 ? only : sci[q];
+            const double wt = only >= 0 ? 1.0 : (double)scw[q];
+            const float* c9 = X.c9 + 9 * c;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const double tv = wt * (double)sv.th[3 * c + k] * sv.z[3 * c + k];
-                w0 += tv * ct.c[k][0];
-                w1 += tv * ct.c[k][1];
-                w2 += tv * ct.c[k][2];
+                const double tv = wt * (double)X.th[3 * c + k] * X.r[3 * c + k];
+                w0 += tv * (double)c9[3 * k];
+                w1 += tv * (double)c9[3 * k + 1];
+                w2 += tv * (double)c9[3 * k + 2];
             }
         }
         cs.wz[3 * b] = w0;
         cs.wz[3 * b + 1] = w1;
         cs.wz[3 * b + 2] = w2;
     }
-    if (threadIdx.x == 0) cs.cr_res[0] = sqrt(rr);
-    cl.sync();
+    if (threadIdx.x == 0 && rank == 0) cs.cr_res[0] = sqrt(res);
+    cr_stamp(21);
+    // no trailing cluster barrier: after its last exchange wait no CTA touches a peer's shared memory
+}
+
+int read_cr_clock(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_cr_clock, sizeof(unsigned long long) * 32);
 }
 
 size_t cr_smem_bytes(int nc, int ns) { return CrLayout(nc, ns).total; }
 
-int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t* slot_vtx,
+int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc, const int32_t* slot_vtx,
               const int32_t* scp, const int32_t* sci, const float* scw, const double* G, double* GA,
               const double4* x, ContactState cs) {
     if (P.nc == 0) return 0;
     static bool attr = false;
-    const size_t smem = cr_smem_bytes(P.nc, P.ns);
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_cr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return (int)e;
@@ -1258,7 +1463,9 @@ int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t
         if (e != cudaSuccess) return (int)e;
         attr = true;
     }
-    k_cr<<<kCluster, kCrThreads, smem, st>>>(P, c, slot_vtx, scp, sci, scw, G, GA, x, cs);
+    const size_t base = cr_smem_bytes(P.nc, P.ns);
+    const int cap = (int)((kCrMaxSmem - base) / sizeof(double));
+    k_cr<<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap);
     return (int)cudaGetLastError();
 }
 

@@ -16,7 +16,8 @@ constexpr int kMaxSlots = 1024;      // distinct contact vertices
 constexpr int kCluster = 16;         // CTAs in the CR cluster (non-portable size)
 constexpr int kCrThreads = 512;
 constexpr size_t kCrMaxSmem = 232448;  // 227 KB opt-in shared memory per CTA (sm_100)
-size_t cr_smem_bytes(int nc, int ns);  // the CR cluster's shared-memory footprint for (nc, ns)
+size_t cr_smem_bytes(int nc, int ns);
+int read_cr_clock(unsigned long long* out);   // phase timestamps of the last CR call (debug)  // the CR cluster's shared-memory footprint for (nc, ns)
 
 // one contact on the device (internal vertex ids, slot ids into the sorted contact-vertex list)
 struct DContact {
@@ -73,7 +74,14 @@ void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_
 void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
                       const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
                       const float4* y, double* dxt);
-int launch_cr(cudaStream_t st, const Params& P, const DContact* c, const int32_t* slot_vtx,
+// compact per-contact arrays for the CR: rows' directions, single-vertex slot / vertex (-1 otherwise)
+struct CrContacts {
+    const float* c9;   // [nc][3][3] rows n, t1, t2
+    const int* s0;     // [nc] slot of a single-vertex weight-1 contact, else -1
+    const int* v0;     // [nc] its vertex, else -1
+    const int* c1;     // [ns] the only contact on a slot if it is single-vertex weight-1, else -1
+};
+int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc, const int32_t* slot_vtx,
               const int32_t* scp, const int32_t* sci, const float* scw, const double* G, double* GA,
               const double4* x, ContactState cs);
 // y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s over the rows of ulist (int4 {row, s0, s1, -})
