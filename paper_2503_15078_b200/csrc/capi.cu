@@ -618,7 +618,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
                               H->sci.p, H->scw.p, H->G.p, H->GA.p, H->x.p, cs); nk++;
             if (e) return -e;
             MARK(KK_SCATTER);
-            launch_scatter(st, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
+            launch_scatter(st, H->n_f, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
         }
         MARK(KK_KPASS2);
         launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->meta.p, H->Krow.p, H->y.p, H->x.p, H->xt.p,

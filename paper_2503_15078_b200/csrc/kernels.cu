@@ -470,6 +470,19 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool val
     const int n = valid ? 4 : 0;
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
 }
+// K entries are streamed once per pass: evict-first in L2 so the pass does not flush the
+// state, vectors, contact data and kernel code that the latency-bound kernels reuse
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void cp_async4_stream(void* smem, const void* gmem, bool valid, unsigned long long pol) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2, %3;\n" ::"r"(s), "l"(gmem), "r"(n),
+                 "l"(pol));
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     const int n = valid ? 16 : 0;
@@ -492,7 +505,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ it
                                                    double* __restrict__ part, int* __restrict__ counters) {
     extern __shared__ __align__(16) unsigned char k1smem[];
     KTile* tiles = reinterpret_cast<KTile*>(k1smem) + (threadIdx.x >> 5) * kStages;
-    double (*s_red)[kWarps][32] = reinterpret_cast<double (*)[kWarps][32]>(k1smem + sizeof(KTile) * kStages * kWarps);
+    double (*s_red)[kWarps][32] = reinterpret_cast<double (*)[kWarps][32]>(k1smem);   // aliases the tiles after the loop
     __shared__ int s_last;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const P1Item it = items[blockIdx.x];
@@ -500,6 +513,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ it
     const bool act = lane < it.nrows;
     const int base = lane - depth[it.r0];
     const int nchunk = (it.c1 - it.c0 + 31) >> 5;
+    const unsigned long long pol = l2_evict_first();
     // this warp owns chunks w, w + 8, ...; issue = u entries (16 B each), then the 32x32 K tile
     auto issue = [&](int ci, KTile& T) {
         const int jc = it.c0 + 32 * ci;
@@ -511,7 +525,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ it
         for (int q = 0; q < 32; ++q) {
             const int cq = __shfl_sync(0xffffffffu, cbj, q);
             const bool ok = act && (jc + q < it.c1) && (jc + q <= r);
-            cp_async4(&T.k[q][lane], &Kcol[ok ? cq + base : 0], ok);
+            cp_async4_stream(&T.k[q][lane], &Kcol[ok ? cq + base : 0], ok, pol);
         }
     };
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -543,6 +557,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ it
         __syncwarp();
     }
     cp_async_wait<0>();
+    __syncthreads();   // all warps are done with their tiles before s_red overwrites them
     s_red[0][w][lane] = a0;
     s_red[1][w][lane] = a1;
     s_red[2][w][lane] = a2;
@@ -578,7 +593,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ it
     if (t == 0) counters[it.block] = 0;
 }
 
-constexpr size_t kKpassSmem = sizeof(KTile) * kStages * kWarps + sizeof(double) * 3 * kWarps * 32;
+constexpr size_t kKpassSmem = sizeof(KTile) * kStages * kWarps;   // >= 3 * kWarps * 32 doubles for s_red
 
 void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* Kcol,
                    const int32_t* depth, const float4* u, float4* y, double* part, int* counters) {
@@ -603,13 +618,14 @@ __global__ void __launch_bounds__(256, 2) k_kpass2(const P2Block* __restrict__ b
                                                    double4* __restrict__ v, double inv_h, int finalize_v) {
     extern __shared__ __align__(16) unsigned char k2smem[];
     KTile* tiles = reinterpret_cast<KTile*>(k2smem) + (threadIdx.x >> 5) * kStages;
-    double (*s_red)[kWarps][32] = reinterpret_cast<double (*)[kWarps][32]>(k2smem + sizeof(KTile) * kStages * kWarps);
+    double (*s_red)[kWarps][32] = reinterpret_cast<double (*)[kWarps][32]>(k2smem);   // aliases the tiles after the loop
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const P2Block b = blocks[blockIdx.x];
     const int j = b.c0 + lane;
     const bool act = lane < b.ncols;
     const int nrow = b.list1 - b.list0;
     const int nchunk = (nrow + 31) >> 5;
+    const unsigned long long pol = l2_evict_first();
     auto issue = [&](int ci, KTile& T) {
         const int k = b.list0 + 32 * ci + lane;
         const bool okr = k < b.list1;
@@ -622,7 +638,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass2(const P2Block* __restrict__ b
             const int rbq = __shfl_sync(0xffffffffu, m.x, q);
             const int fq = __shfl_sync(0xffffffffu, m.y, q);
             const bool ok = act && (32 * ci + q < nrow) && j >= fq && j <= rq;
-            cp_async4(&T.k[q][lane], &Krow[ok ? rbq + j : 0], ok);
+            cp_async4_stream(&T.k[q][lane], &Krow[ok ? rbq + j : 0], ok, pol);
         }
     };
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -654,6 +670,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass2(const P2Block* __restrict__ b
         __syncwarp();
     }
     cp_async_wait<0>();
+    __syncthreads();   // all warps are done with their tiles before s_red overwrites them
     s_red[0][w][lane] = a0;
     s_red[1][w][lane] = a1;
     s_red[2][w][lane] = a2;
@@ -694,18 +711,20 @@ void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_
 // chain dot: dxt_s = (K^T y)_{a_s} = sum_{k} Kcol[colptr_a + k] y[chain_rows[off_s + k]]
 // (column a of K is contiguous in Kcol; its rows are a's ancestor chain)
 // ----------------------------------------------------------------------------
-__global__ void k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx, const float* __restrict__ Kcol,
-                            const int64_t* __restrict__ colptr, const int32_t* __restrict__ chain_off,
-                            const int32_t* __restrict__ chain_rows, const float4* __restrict__ y,
-                            double* __restrict__ dxt) {
-    const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (s >= ns) return;
+__global__ void __launch_bounds__(256) k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx,
+                                                   const float* __restrict__ Kcol, const int64_t* __restrict__ colptr,
+                                                   const int32_t* __restrict__ chain_off,
+                                                   const int32_t* __restrict__ chain_rows, const float4* __restrict__ y,
+                                                   double* __restrict__ dxt) {
+    // one CTA per contact vertex; its 8 warps take interleaved 128-entry slices of the chain
+    __shared__ double s_red[3][kWarps];
+    const int s = blockIdx.x;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int a = slot_vtx[s];
     const float* col = Kcol + colptr[a];
     const int o0 = chain_off[s], len = chain_off[s + 1] - o0;
     double a0 = 0, a1 = 0, a2 = 0;
-    for (int k0 = 0; k0 < len; k0 += 128) {   // 4 independent gathers in flight per lane
+    for (int k0 = 128 * w; k0 < len; k0 += 128 * kWarps) {   // 4 independent gathers in flight per lane
         int rw[4];
         float kv[4];
 #pragma unroll
@@ -732,9 +751,16 @@ __global__ void k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx, const 
     a1 = warp_sum(a1);
     a2 = warp_sum(a2);
     if (lane == 0) {
-        dxt[3 * s] = a0;
-        dxt[3 * s + 1] = a1;
-        dxt[3 * s + 2] = a2;
+        s_red[0][w] = a0;
+        s_red[1][w] = a1;
+        s_red[2][w] = a2;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q) t += s_red[threadIdx.x][q];
+        dxt[3 * s + threadIdx.x] = t;
     }
 }
 
@@ -742,7 +768,7 @@ void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const fl
                       const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
                       const float4* y, double* dxt) {
     if (ns == 0) return;
-    k_chain_dot<<<(ns + 7) / 8, 256, 0, st>>>(ns, slot_vtx, Kcol, colptr, chain_off, chain_rows, y, dxt);
+    k_chain_dot<<<ns, 32 * kWarps, 0, st>>>(ns, slot_vtx, Kcol, colptr, chain_off, chain_rows, y, dxt);
 }
 
 // per-contact-set: chain rows of every slot (walk panel runs) + row flags
@@ -823,17 +849,24 @@ __global__ void k_scatter(const int* __restrict__ ucount, const int4* __restrict
         const int4 u = ulist[e];
         const float* zr = Zc + u.w - u.y;   // zr[s] = K[i][a_s]
         double a0 = 0, a1 = 0, a2 = 0;
-        for (int s0 = u.y; s0 < u.z; s0 += 64) {   // 2 independent iterations in flight
-            const int sa = s0 + lane, sb = s0 + 32 + lane;
-            const double ka = sa < u.z ? (double)__ldg(&zr[sa]) : 0.0;
-            const double kb = sb < u.z ? (double)__ldg(&zr[sb]) : 0.0;
-            const int ia = min(sa, u.z - 1), ib = min(sb, u.z - 1);
-            a0 = fma(ka, wz[3 * ia], a0);
-            a1 = fma(ka, wz[3 * ia + 1], a1);
-            a2 = fma(ka, wz[3 * ia + 2], a2);
-            a0 = fma(kb, wz[3 * ib], a0);
-            a1 = fma(kb, wz[3 * ib + 1], a1);
-            a2 = fma(kb, wz[3 * ib + 2], a2);
+        for (int s0 = u.y; s0 < u.z; s0 += 128) {   // 4 independent loads in flight per lane
+            double kv[4], w0[4], w1[4], w2[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int sq = s0 + 32 * q + lane;
+                const bool ok = sq < u.z;
+                const int iq = ok ? sq : u.y;
+                kv[q] = ok ? (double)__ldg(&zr[sq]) : 0.0;
+                w0[q] = __ldg(&wz[3 * iq]);
+                w1[q] = __ldg(&wz[3 * iq + 1]);
+                w2[q] = __ldg(&wz[3 * iq + 2]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a0 = fma(kv[q], w0[q], a0);
+                a1 = fma(kv[q], w1[q], a1);
+                a2 = fma(kv[q], w2[q], a2);
+            }
         }
         a0 = warp_sum(a0);
         a1 = warp_sum(a1);
@@ -845,9 +878,9 @@ __global__ void k_scatter(const int* __restrict__ ucount, const int4* __restrict
     }
 }
 
-void launch_scatter(cudaStream_t st, const int* ucount, const int4* ulist, const float* Zc, const double* wz,
-                    float4* y) {
-    k_scatter<<<148 * 4, 256, 0, st>>>(ucount, ulist, Zc, wz, y);
+void launch_scatter(cudaStream_t st, int max_rows, const int* ucount, const int4* ulist, const float* Zc,
+                    const double* wz, float4* y) {
+    k_scatter<<<(max_rows + 7) / 8, 256, 0, st>>>(ucount, ulist, Zc, wz, y);
 }
 
 // ----------------------------------------------------------------------------
@@ -994,7 +1027,7 @@ void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const double* G) {
 //   (S v)_j = theta_j c_j . sum_{a in j} w_ja q_a + C_j v_j,
 //   q_a = sum_b G_ab W_b,   W_b = sum_{rows k at b} w_kb theta_k c_k v_k.
 // ----------------------------------------------------------------------------
-constexpr int kRpt = 6;   // rows per thread: m = 3 nc <= kRpt * kCrThreads
+constexpr int kRptMax = 6;   // rows per thread: m = 3 nc <= kRpt * kCrThreads (kernel templated on kRpt)
 
 struct CrLayout {
     int m, nc, ns;
@@ -1008,7 +1041,7 @@ struct CrLayout {
         W = take(8 * 3 * (size_t)ns); q = take(8 * 2 * 3 * (size_t)ns);
         aidx = take(4 * (size_t)ns); apos = take(4 * (size_t)ns); acon = take(4 * (size_t)ns);
         red = take(8 * 3 * (kCrThreads / 32) + 4 * (kCrThreads / 32 + 1));   // 3 doubles/warp + scan ints
-        mbar = take(16);
+        mbar = take(32);   // two exchange mbarriers (one per q buffer)
         gA = o;
         total = o;
     }
@@ -1037,22 +1070,37 @@ __device__ __forceinline__ void block_sum2(double s1, double s2, double* red, do
     o2 = t2;
 }
 
+__device__ unsigned long long g_cr_clock[32];   // phase timestamps (ns) of the last CR call, rank 0
+__device__ __forceinline__ void cr_stamp(int i) {
+    if (threadIdx.x == 0 && cg::this_cluster().block_rank() == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_cr_clock[i] = t;
+    }
+}
+
 struct CrCtx {
     double *r, *W, *q, *red, *gA;
     float *th, *cd, *c9;
     int *s0, *aidx, *apos, *acon;
-    int na, i0, i1, gA_smem;
-    unsigned mbar;   // shared-window address of this CTA's exchange mbarrier
-    unsigned phase;  // parity of the exchange phase being waited for
+    int na, ns, i0, i1, gA_smem;
+    unsigned mbar;   // shared-window address of this CTA's exchange mbarriers (2 x 8 B, one per q buffer)
+    unsigned phase;  // q buffer / barrier used by the next exchange (alternates)
+    unsigned par0, par1;   // phase parity of each barrier (scalars: no dynamic indexing)
+    int stamp;       // >= 0: write fine-grained phase stamps of this apply at g_cr_clock[stamp..]
     const double* GAg;   // global fallback for this CTA's G_A rows
 };
 
 // Ar = S r for this thread's rows (registers); r is read from shared memory
+template <int kRpt>
 __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m, const DContact* __restrict__ C,
                                          const int32_t* __restrict__ scp, const int32_t* __restrict__ sci,
                                          const float* __restrict__ scw, int buf, double (&Ar)[kRpt]) {
     const int na = X.na;
-    double* qb = X.q + (size_t)buf * 3 * na;
+    double* qb = X.q + (size_t)buf * 3 * X.ns;   // SoA: q0 | q1 | q2 (conflict-free reads in Sv)
+    const unsigned bar = X.mbar + 8u * (unsigned)buf;
+    if (threadIdx.x == 0 && na > 0)   // this phase expects 32 bytes per row of G_A from the peers
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(24 * na) : "memory");
     for (int i = threadIdx.x; i < na; i += blockDim.x) {
         double w0 = 0.0, w1 = 0.0, w2 = 0.0;
         const int c1 = X.acon[i];
@@ -1085,6 +1133,7 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
         X.W[2 * na + i] = w2;
     }
     __syncthreads();
+    if (X.stamp >= 0) cr_stamp(X.stamp);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int i = X.i0 + wid; i < X.i1; i += nw) {
         const double* g = X.gA_smem ? X.gA + (size_t)(i - X.i0) * na : X.GAg + (size_t)i * na;
@@ -1108,29 +1157,39 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
         d1 = warp_sum(d1);
         d2 = warp_sum(d2);
         if (lane < kCluster) {
-            // write q_i into CTA `lane`, then arrive (release) on that CTA's mbarrier:
-            // each peer expects exactly na arrivals per exchange (one per row of G_A)
-            double* rq = cl.map_shared_rank(qb, lane);
-            rq[3 * i] = d0;
-            rq[3 * i + 1] = d1;
-            rq[3 * i + 2] = d2;
-            unsigned remote;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(X.mbar), "r"(lane));
-            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+            // asynchronous 32-byte store of q_i into CTA `lane`, completing 32 tx bytes on
+            // that CTA's mbarrier for this buffer (no fences, no cluster barrier)
+            const unsigned l0 = (unsigned)__cvta_generic_to_shared(qb + i);
+            const unsigned l1 = (unsigned)__cvta_generic_to_shared(qb + na + i);
+            const unsigned l2 = (unsigned)__cvta_generic_to_shared(qb + 2 * na + i);
+            unsigned r0, r1, r2, rb;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r0) : "r"(l0), "r"(lane));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r1) : "r"(l1), "r"(lane));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r2) : "r"(l2), "r"(lane));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(bar), "r"(lane));
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n"
+                         ::"r"(r0), "d"(d0), "r"(rb) : "memory");
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n"
+                         ::"r"(r1), "d"(d1), "r"(rb) : "memory");
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n"
+                         ::"r"(r2), "d"(d2), "r"(rb) : "memory");
         }
     }
-    if (threadIdx.x == 0 && na > 0) {   // wait for all na rows of q (acquire), then release the CTA
+    if (X.stamp >= 0) cr_stamp(X.stamp + 1);
+    if (threadIdx.x == 0 && na > 0) {   // wait until all na rows have landed here (acquire)
         unsigned done = 0;
         while (!done) {
             asm volatile(
                 "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
                 " selp.u32 %0, 1, 0, p;\n}\n"
                 : "=r"(done)
-                : "r"(X.mbar), "r"(X.phase)
+                : "r"(bar), "r"(buf ? X.par1 : X.par0)
                 : "memory");
         }
     }
+    if (buf) X.par1 ^= 1u; else X.par0 ^= 1u;
     __syncthreads();
+    if (X.stamp >= 0) cr_stamp(X.stamp + 2);
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) {
         const int j = min(threadIdx.x + kCrThreads * k, m - 1);   // rows >= m are padding (never used)
@@ -1142,13 +1201,13 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
             const int sl0 = X.s0[c];
             if (sl0 >= 0) {
                 const int ip = X.apos[sl0];
-                acc = (double)cc[0] * qb[3 * ip] + (double)cc[1] * qb[3 * ip + 1] + (double)cc[2] * qb[3 * ip + 2];
+                acc = (double)cc[0] * qb[ip] + (double)cc[1] * qb[na + ip] + (double)cc[2] * qb[2 * na + ip];
             } else {
                 const DContact& ct = C[c];
                 for (int p = 0; p < ct.nv; ++p) {
                     const int ip = X.apos[ct.slot[p]];
-                    acc += ct.w[p] * ((double)cc[0] * qb[3 * ip] + (double)cc[1] * qb[3 * ip + 1] +
-                                      (double)cc[2] * qb[3 * ip + 2]);
+                    acc += ct.w[p] * ((double)cc[0] * qb[ip] + (double)cc[1] * qb[na + ip] +
+                                      (double)cc[2] * qb[2 * na + ip]);
                 }
             }
         }
@@ -1157,15 +1216,8 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
     X.phase ^= 1u;
 }
 
-__device__ unsigned long long g_cr_clock[32];   // phase timestamps (ns) of the last CR call, rank 0
-__device__ __forceinline__ void cr_stamp(int i) {
-    if (threadIdx.x == 0 && cg::this_cluster().block_rank() == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        g_cr_clock[i] = t;
-    }
-}
 
+template <int kRpt>
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1)
     k_cr(Params P, const DContact* __restrict__ C, CrContacts cc, const int32_t* __restrict__ slot_vtx,
          const int32_t* __restrict__ scp, const int32_t* __restrict__ sci, const float* __restrict__ scw,
@@ -1195,46 +1247,25 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
     cp_async_commit();
     X.mbar = (unsigned)__cvta_generic_to_shared(smraw + L.mbar);
     X.phase = 0u;
+    X.stamp = -1;
     cr_stamp(22);
     // rho_j = h_j - theta_j c_j . x~_c, x~ = x^k + K^T y at the contact vertices (owner rows)
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
-    // independent loads first (no early exit, so they overlap), then the x/dxt gathers
-    int v0r[kRpt], s0r[kRpt];
-    double thr[kRpt], hvr[kRpt], cdr[kRpt], lamr[kRpt];
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) {
         z[k] = p[k] = Ap[k] = Ar[k] = 0.0;
         const int j = threadIdx.x + kCrThreads * k;
-        const bool ok = j < m;
-        const int c = ok ? j / 3 : 0;
-        v0r[k] = ok ? __ldg(&cc.v0[c]) : -1;
-        s0r[k] = ok ? __ldg(&cc.s0[c]) : -1;
-        thr[k] = ok ? cs.theta[j] : 0.0;
-        hvr[k] = ok ? cs.hvec[j] : 0.0;
-        cdr[k] = ok ? cs.cdiag[j] : 0.0;
-        lamr[k] = ok ? cs.lam[j] : 0.0;
-    }
-    cr_stamp(23);
-    double4 xar[kRpt];
-    double d0r[kRpt], d1r[kRpt], d2r[kRpt];
-#pragma unroll
-    for (int k = 0; k < kRpt; ++k) {
-        const bool single = v0r[k] >= 0;
-        xar[k] = single ? x[v0r[k]] : make_double4(0, 0, 0, 0);
-        d0r[k] = single ? cs.dxt[3 * s0r[k]] : 0.0;
-        d1r[k] = single ? cs.dxt[3 * s0r[k] + 1] : 0.0;
-        d2r[k] = single ? cs.dxt[3 * s0r[k] + 2] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < kRpt; ++k) {
-        const int j = threadIdx.x + kCrThreads * k;
         if (j < m) {
             const int c = j / 3, kk = j - 3 * c;
+            const int v0 = __ldg(&cc.v0[c]);
+            const double th = cs.theta[j];
             double xs0, xs1, xs2;
-            if (v0r[k] >= 0) {
-                xs0 = xar[k].x + d0r[k];
-                xs1 = xar[k].y + d1r[k];
-                xs2 = xar[k].z + d2r[k];
+            if (v0 >= 0) {
+                const int sl = __ldg(&cc.s0[c]);
+                const double4 xa = x[v0];
+                xs0 = xa.x + cs.dxt[3 * sl];
+                xs1 = xa.y + cs.dxt[3 * sl + 1];
+                xs2 = xa.z + cs.dxt[3 * sl + 2];
             } else {   // general multi-vertex contact
                 const DContact& ct = C[c];
                 xs0 = xs1 = xs2 = 0.0;
@@ -1247,10 +1278,10 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
                 }
             }
             const float* c3 = cc.c9 + 9 * c + 3 * kk;
-            const double rho = hvr[k] - thr[k] * ((double)__ldg(&c3[0]) * xs0 + (double)__ldg(&c3[1]) * xs1 +
+            const double rho = cs.hvec[j] - th * ((double)__ldg(&c3[0]) * xs0 + (double)__ldg(&c3[1]) * xs1 +
                                                   (double)__ldg(&c3[2]) * xs2);
-            X.th[j] = (float)thr[k];
-            X.cd[j] = (float)cdr[k];
+            X.th[j] = (float)th;
+            X.cd[j] = (float)cs.cdiag[j];
             X.r[j] = rho;
             p[k] = rho;
         }
@@ -1301,12 +1332,16 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
     }
     const int na = cnt[0];
     X.na = na;
-    if (threadIdx.x == 0 && na > 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(X.mbar), "r"(na));
+    X.ns = ns;
+    X.par0 = X.par1 = 0u;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(X.mbar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(X.mbar + 8u));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     cl.sync();   // every CTA's exchange mbarrier is initialised before any remote arrive
     cr_stamp(24);
+    if (threadIdx.x == 0 && cl.block_rank() == 0) g_cr_clock[31] = g_cr_clock[0] + 1000ull * na;   // na (debug)
     {
         const int per = (na + kCluster - 1) / kCluster;
         X.i0 = min(na, (int)cl.block_rank() * per);
@@ -1356,7 +1391,10 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
             }
             __syncthreads();
             if (it == P.cr_iters - 1) break;
+            X.stamp = it == 3 ? 13 : -1;
+            if (it == 3) cr_stamp(12);
             cr_apply(cl, X, m, C, scp, sci, scw, (int)X.phase, Ar);
+            if (it == 3) cr_stamp(16);
             double s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
             for (int k = 0; k < kRpt; ++k) {
@@ -1391,7 +1429,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
                        beta * p[k];
                 Ap[k] = Ar[k] + beta * Ap[k];
             }
-            cr_stamp(3 + it);
+            if (it == 3) cr_stamp(17);
+            if (it < 9 && it != 3) cr_stamp(3 + it);
         }
     }
     cr_stamp(20);
@@ -1413,7 +1452,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
         const int j = threadIdx.x + kCrThreads * k;
         if (j < m) {
             X.r[j] = z[k];
-            if (j / rper == rank) cs.lam[j] = lamr[k] + z[k] / (h * h);
+            if (j / rper == rank) cs.lam[j] += z[k] / (h * h);
         }
     }
     __syncthreads();
@@ -1457,15 +1496,26 @@ int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc
     if (P.nc == 0) return 0;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_cr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return (int)e;
-        e = cudaFuncSetAttribute(k_cr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrMaxSmem);
-        if (e != cudaSuccess) return (int)e;
+        void* fns[kRptMax] = {(void*)k_cr<1>, (void*)k_cr<2>, (void*)k_cr<3>, (void*)k_cr<4>, (void*)k_cr<5>, (void*)k_cr<6>};
+        for (void* f : fns) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return (int)e;
+            e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrMaxSmem);
+            if (e != cudaSuccess) return (int)e;
+        }
         attr = true;
     }
     const size_t base = cr_smem_bytes(P.nc, P.ns);
     const int cap = (int)((kCrMaxSmem - base) / sizeof(double));
-    k_cr<<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap);
+    const int rpt = (3 * P.nc + kCrThreads - 1) / kCrThreads;
+    switch (rpt) {
+        case 1: k_cr<1><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
+        case 2: k_cr<2><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
+        case 3: k_cr<3><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
+        case 4: k_cr<4><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
+        case 5: k_cr<5><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
+        default: k_cr<6><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
+    }
     return (int)cudaGetLastError();
 }
 

@@ -85,8 +85,8 @@ int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc
               const int32_t* scp, const int32_t* sci, const float* scw, const double* G, double* GA,
               const double4* x, ContactState cs);
 // y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s over the rows of ulist (int4 {row, s0, s1, -})
-void launch_scatter(cudaStream_t st, const int* ucount, const int4* ulist, const float* Zc, const double* wz,
-                    float4* y);
+void launch_scatter(cudaStream_t st, int max_rows, const int* ucount, const int4* ulist, const float* Zc,
+                    const double* wz, float4* y);
 
 // --- per-contact-set kernels ----------------------------------------------------
 void launch_delassus(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,

@@ -22,4 +22,5 @@ x, v = s.get_state()
 print("max|x-X|", float(np.abs(x - sc.mesh.X).max()), "finite", bool(np.isfinite(x).all()), "max|v|", float(np.abs(v).max()))
 from paper_2503_15078_b200._lib import debug_cr_timeline
 tl = debug_cr_timeline(s)
-print("CR timeline us:", " ".join(f"{v:.1f}" for v in tl[:14]), "end", f"{tl[20]:.1f} {tl[21]:.1f}", "sub", " ".join(f"{v:.1f}" for v in tl[22:29]))
+print("CR timeline us:", " ".join(f"{v:.1f}" for v in tl[:12]), "| it3: start %.1f W %.1f mv %.1f wait %.1f Sv %.1f end %.1f" % tuple(tl[12:18]), "| end", f"{tl[20]:.1f} {tl[21]:.1f}", "na", int(tl[31]), "sub", " ".join(f"{v:.1f}" for v in tl[22:29]))
+from paper_2503_15078_b200._lib import lib as _L
