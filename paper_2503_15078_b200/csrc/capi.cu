@@ -125,7 +125,24 @@ struct sim_handle {
     int kernels_per_frame = 0;
     int64_t frames_done = 0;
     int64_t h2d_contact_bytes = 0;   // bytes uploaded by the last sim_set_contacts
+    // pinned staging for asynchronous sim_set_contacts uploads (reused once the last copy is done)
+    unsigned char* stage = nullptr;
+    size_t stage_cap = 0, stage_used = 0;
+    cudaEvent_t stage_free = nullptr;
+    double set_contacts_host_us = 0;
 };
+
+// copy n elements of src into the pinned staging area and enqueue the H2D copy to dst
+template <class T>
+static cudaError_t stage_upload(sim_handle* H, T* dst, const T* src, size_t n) {
+    if (n == 0) return cudaSuccess;
+    const size_t bytes = n * sizeof(T);
+    const size_t at = (H->stage_used + 15) & ~size_t(15);
+    if (at + bytes > H->stage_cap) return cudaErrorMemoryAllocation;   // caller sized the area
+    memcpy(H->stage + at, src, bytes);
+    H->stage_used = at + bytes;
+    return cudaMemcpyAsync(dst, H->stage + at, bytes, cudaMemcpyHostToDevice, H->stream);
+}
 
 // ---------------------------------------------------------------------------
 static int validate_create(const sim_mesh* m, const sim_material* mat, double h) {
@@ -224,6 +241,8 @@ extern "C" void sim_destroy(sim_handle* H) {
         H->theta.release(); H->cdiag.release(); H->hvec.release(); H->hl.release(); H->dxt.release();
         H->wz.release(); H->phi_abs.release(); H->cr_res.release();
         for (auto e : H->pev) cudaEventDestroy(e);
+        if (H->stage_free) cudaEventDestroy(H->stage_free);
+        if (H->stage) cudaFreeHost(H->stage);
         if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
     }
     delete H;
@@ -423,6 +442,7 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
     if (H->host_only) return fail(SIM_E_STATE, "host-only handle");
     if (n < 0 || (n > 0 && !cs)) return fail(SIM_E_INVALID, "bad contact array");
     if (n > kMaxContacts) return fail(SIM_E_LIMIT, "at most %d contacts per handle", kMaxContacts);
+    auto th0 = std::chrono::steady_clock::now();
     std::vector<DContact> hc(n);
     std::vector<int32_t> verts;
     for (int c = 0; c < n; ++c) {
@@ -491,7 +511,22 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
     for (int s = 0; s < ns; ++s) vcp[verts[s] + 1] = scp[s + 1] - scp[s];
     for (int i = 0; i < H->n_f; ++i) vcp[i + 1] += vcp[i];
     cudaStream_t st = H->stream;
-    CK(H->dc.upload(hc.data(), n, st));
+    // asynchronous uploads through pinned staging: wait only for the previous call's copies
+    {
+        const size_t need = n * sizeof(DContact) + 64 * (size_t)n + 32 * (size_t)ns + 16 * sci.size() +
+                            4 * ((size_t)H->n_f + 1) + 1024;
+        if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
+        CK(cudaEventSynchronize(H->stage_free));
+        if (need > H->stage_cap) {
+            if (H->stage) CK(cudaFreeHost(H->stage));
+            H->stage = nullptr;
+            H->stage_cap = 0;
+            CK(cudaMallocHost((void**)&H->stage, 2 * need));
+            H->stage_cap = 2 * need;
+        }
+        H->stage_used = 0;
+    }
+    CK(stage_upload(H, H->dc.p, hc.data(), n));
     {
         std::vector<float> c9(9 * (size_t)n);
         std::vector<int32_t> s0(n), v0(n);
@@ -502,22 +537,21 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
             s0[q] = single ? hc[q].slot[0] : -1;
             v0[q] = single ? hc[q].vtx[0] : -1;
         }
-        CK(H->cc9.upload(c9.data(), c9.size(), st));
-        CK(H->cs0.upload(s0.data(), n, st));
-        CK(H->cv0.upload(v0.data(), n, st));
+        CK(stage_upload(H, H->cc9.p, c9.data(), c9.size()));
+        CK(stage_upload(H, H->cs0.p, s0.data(), n));
+        CK(stage_upload(H, H->cv0.p, v0.data(), n));
         std::vector<int32_t> c1(ns, -1);
         for (int s = 0; s < ns; ++s)
             if (scp[s + 1] - scp[s] == 1 && s0[sci[scp[s]]] == s) c1[s] = sci[scp[s]];
-        CK(H->cc1.upload(c1.data(), ns, st));
-        CK(cudaStreamSynchronize(st));   // host staging vectors go out of scope
+        CK(stage_upload(H, H->cc1.p, c1.data(), ns));
     }
-    CK(H->slot_vtx.upload(verts.data(), ns, st));
-    CK(H->scp.upload(scp.data(), ns + 1, st));
-    CK(H->sci.upload(sci.data(), sci.size(), st));
-    CK(H->scw.upload(scw.data(), scw.size(), st));
-    CK(H->vcp.upload(vcp.data(), H->n_f + 1, st));
-    CK(H->vci.upload(sci.data(), sci.size(), st));   // slots are sorted by vertex: same order
-    CK(H->vcw.upload(scw.data(), scw.size(), st));
+    CK(stage_upload(H, H->slot_vtx.p, verts.data(), ns));
+    CK(stage_upload(H, H->scp.p, scp.data(), ns + 1));
+    CK(stage_upload(H, H->sci.p, sci.data(), sci.size()));
+    CK(stage_upload(H, H->scw.p, scw.data(), scw.size()));
+    CK(stage_upload(H, H->vcp.p, vcp.data(), (size_t)H->n_f + 1));
+    CK(stage_upload(H, H->vci.p, sci.data(), sci.size()));   // slots are sorted by vertex: same order
+    CK(stage_upload(H, H->vcw.p, scw.data(), scw.size()));
     H->h2d_contact_bytes = (int64_t)(n * sizeof(DContact) + ns * sizeof(int32_t) + (ns + 1) * sizeof(int32_t) +
                                      2 * sci.size() * (sizeof(int32_t) + sizeof(float)) +
                                      (H->n_f + 1) * sizeof(int32_t));
@@ -530,7 +564,8 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
         CK(H->Zc.alloc(H->chain_rows.n));
         H->contact_gen++;
     }
-    CK(H->chain_off.upload(coff.data(), ns + 1, st));
+    CK(stage_upload(H, H->chain_off.p, coff.data(), ns + 1));
+    CK(cudaEventRecord(H->stage_free, st));
     CK(cudaMemsetAsync(H->flag.p, 0, H->n_f, st));
     CK(cudaMemsetAsync(H->ucount.p, 0, 2 * sizeof(int), st));
     launch_chain_rows(st, ns, H->slot_vtx.p, H->chain_off.p, H->parent.p, H->ptop.p, H->chain_rows.p, H->flag.p);
@@ -545,9 +580,8 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
     H->row_lo = ns ? verts[0] : H->n_f;
     H->hc = hc;
     H->slot_vtx_h = verts;
-    // keep the host staging alive until the async copies complete
-    CK(cudaStreamSynchronize(st));
-    return SIM_OK;
+    H->set_contacts_host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count();
+    return SIM_OK;   // asynchronous: the copies and kernels are ordered on the handle's stream
 }
 
 // ---------------------------------------------------------------------------

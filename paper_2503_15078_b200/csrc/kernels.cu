@@ -889,6 +889,7 @@ void launch_scatter(cudaStream_t st, int max_rows, const int* ucount, const int4
 // d <= depth(lca(a_s, a_t)) of Z[d][s] Z[d][t], Z[d][s] = Kcol[colptr_s + depth_s - d].
 // 32x32 tiles of slot pairs, depth staged in chunks of 32 levels.
 // ----------------------------------------------------------------------------
+
 __device__ int lca_depth(int a, int b, const int32_t* parent, const int32_t* ptop, const int32_t* depth) {
     // a <= b in postorder: lca = first ancestor run of a whose top >= b, at row max(i, b)
     if (a > b) { int t = a; a = b; b = t; }
