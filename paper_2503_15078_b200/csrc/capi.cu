@@ -65,6 +65,8 @@ struct sim_handle {
     bool host_only = false;
     int device = -1;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;            // fork branch inside the frame graph
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     bool own_stream = false;
     int state = 0;   // 0 created, 1 built
     // host copies
@@ -78,6 +80,7 @@ struct sim_handle {
     std::vector<int32_t> int2orig, orig2int;
     simhost::Inverse K;
     simhost::WorkLists wl;
+    std::vector<float> T1h, T2h;
     int64_t nnzL = 0;
     double build_seconds = 0;
     double vpin[3] = {0, 0, 0};
@@ -89,7 +92,7 @@ struct sim_handle {
     DBuf<float4> fc, u, y;
     DBuf<int32_t> adjp, adj;
     // device: K
-    DBuf<float> Krow, Kcol;
+    DBuf<float> Krow, Kcol, T1, T2;   // K row/column-major + the two passes' tile streams
     DBuf<int64_t> colptr;
     DBuf<int32_t> cb, depth, parent, ptop, cover;
     DBuf<int2> meta;                 // {rowptr[i] - first[i], first[i]}
@@ -205,6 +208,9 @@ static int create_common(const sim_mesh* m, const sim_material* mat, double h, s
             if (e == cudaSuccess && ndev == 0) e = cudaErrorNoDevice;
         }
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&H->aux, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&H->fork_ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&H->join_ev, cudaEventDisableTiming);
         if (e != cudaSuccess) {
             delete H;
             return fail(SIM_E_CUDA, "no usable CUDA device: %s", cudaGetErrorString(e));
@@ -231,7 +237,7 @@ extern "C" void sim_destroy(sim_handle* H) {
         if (H->gexec) cudaGraphExecDestroy(H->gexec);
         H->x.release(); H->xt.release(); H->v.release(); H->s.release(); H->M.release();
         H->tet.release(); H->Bm.release(); H->hw2.release(); H->fc.release(); H->u.release(); H->y.release();
-        H->adjp.release(); H->adj.release(); H->Krow.release(); H->Kcol.release(); H->meta.release();
+        H->adjp.release(); H->adj.release(); H->Krow.release(); H->Kcol.release(); H->T1.release(); H->T2.release(); H->meta.release();
         H->colptr.release(); H->cb.release(); H->cover.release(); H->depth.release(); H->parent.release();
         H->ptop.release(); H->p1.release(); H->p1b.release(); H->p2b.release();
         H->part1.release(); H->counters.release();
@@ -242,6 +248,9 @@ extern "C" void sim_destroy(sim_handle* H) {
         H->wz.release(); H->phi_abs.release(); H->cr_res.release();
         for (auto e : H->pev) cudaEventDestroy(e);
         if (H->stage_free) cudaEventDestroy(H->stage_free);
+        if (H->fork_ev) cudaEventDestroy(H->fork_ev);
+        if (H->join_ev) cudaEventDestroy(H->join_ev);
+        if (H->aux) cudaStreamDestroy(H->aux);
         if (H->stage) cudaFreeHost(H->stage);
         if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
     }
@@ -321,6 +330,8 @@ static int upload_all(sim_handle* H) {
     const simhost::Inverse& K = H->K;
     CK(H->Krow.alloc(K.nnz)); CK(H->Krow.upload(K.Krow.data(), K.nnz, st));
     CK(H->Kcol.alloc(K.nnz)); CK(H->Kcol.upload(K.Kcol.data(), K.nnz, st));
+    CK(H->T1.alloc(H->T1h.size())); CK(H->T1.upload(H->T1h.data(), H->T1h.size(), st));
+    CK(H->T2.alloc(H->T2h.size())); CK(H->T2.upload(H->T2h.data(), H->T2h.size(), st));
     std::vector<int32_t> cb(nf);
     std::vector<int2> meta(nf);
     for (int j = 0; j < nf; ++j) {
@@ -401,6 +412,7 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     if (H->K.nnz >= (int64_t)INT32_MAX)
         return fail(SIM_E_LIMIT, "nnz(K) = %lld exceeds the int32 offset limit", (long long)H->K.nnz);
     simhost::build_worklists(H->K, H->wl, 1024);
+    simhost::build_tiles(H->K, H->wl, H->T1h, H->T2h);
     H->n_f = nf;
     H->int2orig.assign(nv, -1);
     H->orig2int.assign(nv, -1);
@@ -630,19 +642,31 @@ static int enqueue_frame(sim_handle* H, int iters) {
         return (int)cudaEventRecordWithFlags(H->pev[ev++], st, cudaEventRecordExternal);
     };
 #define MARK(k) do { int r_ = mark(k); if (r_) return -r_; } while (0)
+#define CKR(call) do { cudaError_t r_ = (call); if (r_ != cudaSuccess) return -(int)r_; } while (0)
     MARK(KK_PREDICT);
     launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->lam.p, 3 * H->nc); nk++;
     const bool con = H->nc > 0;
     for (int k = 0; k < iters; ++k) {
-        if (con) { MARK(KK_CONTACT); launch_contact_eval(st, P, H->dc.p, H->x.p, H->xt.p, cs); nk++; }
+        // contact evaluation and the local step only read x^k: run them as two graph
+        // branches (serial when profiling, so the per-kernel events stay meaningful)
+        const bool fork = con && !H->profiling;
+        if (fork) {
+            CKR(cudaEventRecord(H->fork_ev, st));
+            CKR(cudaStreamWaitEvent(H->aux, H->fork_ev, 0));
+            launch_contact_eval(H->aux, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
+            CKR(cudaEventRecord(H->join_ev, H->aux));
+        } else if (con) {
+            MARK(KK_CONTACT); launch_contact_eval(st, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
+        }
         MARK(KK_LOCAL);
         launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, H->x.p, H->fc.p, nullptr); nk++;
+        if (fork) CKR(cudaStreamWaitEvent(st, H->join_ev, 0));
         MARK(KK_GATHER);
         launch_gather(st, P, H->adjp.p, H->adj.p, H->fc.p, H->M.p, H->x.p, H->s.p, con ? H->vcp.p : nullptr,
                       H->vci.p, H->vcw.p, H->hl.p, H->cb.p, H->u.p, nullptr); nk++;
         MARK(KK_KPASS1);
-        launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->Kcol.p, H->depth.p, H->u.p, H->y.p,
-                      H->part1.p, H->counters.p); nk++;
+        launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->T1.p, H->u.p, H->y.p, H->part1.p,
+                      H->counters.p); nk++;
         if (con) {
             MARK(KK_CHAIN);
             launch_chain_dot(st, H->ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
@@ -655,11 +679,12 @@ static int enqueue_frame(sim_handle* H, int iters) {
             launch_scatter(st, H->n_f, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
         }
         MARK(KK_KPASS2);
-        launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->meta.p, H->Krow.p, H->y.p, H->x.p, H->xt.p,
-                      H->v.p, 1.0 / H->h, k == iters - 1); nk++;
+        launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->T2.p, H->y.p, H->x.p, H->xt.p, H->v.p,
+                      1.0 / H->h, k == iters - 1); nk++;
     }
     MARK(KK_N);
 #undef MARK
+#undef CKR
     return nk;
 }
 
@@ -865,10 +890,8 @@ extern "C" int sim_debug_apply_inverse(sim_handle* H, const double* b, double* x
     CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(H->u.p, hu.data(), nf * sizeof(float4), cudaMemcpyHostToDevice));
     CK(cudaMemset(dx.p, 0, nf * sizeof(double4)));
-    launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->Kcol.p, H->depth.p, H->u.p, H->y.p,
-                  H->part1.p, H->counters.p);
-    launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->meta.p, H->Krow.p, H->y.p, dx.p, nullptr,
-                  nullptr, 1.0, 0);
+    launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->T1.p, H->u.p, H->y.p, H->part1.p, H->counters.p);
+    launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->T2.p, H->y.p, dx.p, nullptr, nullptr, 1.0, 0);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     std::vector<double4> hx(nf);

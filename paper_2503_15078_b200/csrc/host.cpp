@@ -394,7 +394,7 @@ void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols) {
             int bi = (int)wl.p1b.size();
             for (int c0 = f; c0 < cend; c0 += p1_chunk_cols) {
                 int c1 = std::min(cend, c0 + p1_chunk_cols);
-                wl.p1.push_back(P1Item{r0, nr, c0, c1, bi, wl.p1_parts + b.nitems});
+                wl.p1.push_back(P1Item{r0, nr, c0, c1, bi, wl.p1_parts + b.nitems, 0});
                 b.nitems++;
             }
             wl.p1_parts += b.nitems;
@@ -419,12 +419,48 @@ void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols) {
                 cov.push_back(i);
             }
         std::sort(cov.begin(), cov.end());
-        P2Block b{c0, nc, (int)wl.cover.size(), (int)(wl.cover.size() + cov.size())};
+        P2Block b{c0, nc, (int)wl.cover.size(), (int)(wl.cover.size() + cov.size()), 0};
         wl.cover.insert(wl.cover.end(), cov.begin(), cov.end());
         blocks.push_back({(int64_t)cov.size(), b});
     }
     std::stable_sort(blocks.begin(), blocks.end(), [](auto& a, auto& b) { return a.first > b.first; });
     for (auto& b : blocks) wl.p2b.push_back(b.second);
+}
+
+void build_tiles(const Inverse& K, WorkLists& wl, std::vector<float>& T1, std::vector<float>& T2) {
+    auto kval = [&](int r, int j) -> float {   // K[r][j], 0 outside the skyline
+        if (j < K.first[r] || j > r) return 0.f;
+        return K.Krow[K.rowptr[r] + (j - K.first[r])];
+    };
+    int64_t n1 = 0;
+    for (auto& it : wl.p1) n1 += (int64_t)it.nrows * 32 * ((it.c1 - it.c0 + 31) / 32);
+    T1.assign(n1, 0.f);
+    int64_t o = 0;
+    for (auto& it : wl.p1) {
+        it.toff = o;
+        for (int jc = it.c0; jc < it.c1; jc += 32) {
+            for (int q = 0; q < 32; ++q) {
+                const int j = jc + q;
+                if (j >= it.c1) continue;
+                for (int l = 0; l < it.nrows; ++l) T1[o + (int64_t)q * it.nrows + l] = kval(it.r0 + l, j);
+            }
+            o += (int64_t)it.nrows * 32;
+        }
+    }
+    int64_t n2 = 0;
+    for (auto& b : wl.p2b) n2 += 1024LL * ((b.list1 - b.list0 + 31) / 32);
+    T2.assign(n2, 0.f);
+    o = 0;
+    for (auto& b : wl.p2b) {
+        b.toff = o;
+        for (int k0 = b.list0; k0 < b.list1; k0 += 32) {
+            for (int q = 0; q < 32 && k0 + q < b.list1; ++q) {
+                const int r = wl.cover[k0 + q];
+                for (int l = 0; l < b.ncols; ++l) T2[o + 32 * q + l] = kval(r, b.c0 + l);
+            }
+            o += 1024;
+        }
+    }
 }
 
 }  // namespace simhost

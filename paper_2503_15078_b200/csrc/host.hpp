@@ -73,11 +73,11 @@ void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads)
 
 // ---------------- K-pass work lists (one CTA per item) ----------------------
 // pass 1 (y = K u, column-major K): item = (<= 32 rows of one panel) x (<= 1024 columns)
-struct P1Item { int32_t r0, nrows, c0, c1, block, part; };
+struct P1Item { int32_t r0, nrows, c0, c1, block, part; int64_t toff; };   // toff: tile stream offset (floats)
 struct P1Block { int32_t r0, nrows, nitems, part0; };
 // pass 2 (x += K^T y, row-major K): one item per 32-column block, its cover rows
 // (rows i >= c0 with first(i) <= c0 + 31) in cover[list0, list1)
-struct P2Block { int32_t c0, ncols, list0, list1; };
+struct P2Block { int32_t c0, ncols, list0, list1; int64_t toff; };
 
 struct WorkLists {
     std::vector<P1Item> p1;
@@ -88,5 +88,14 @@ struct WorkLists {
 };
 
 void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols);
+
+// K re-laid out as tile streams in the exact order each pass consumes them, so a pass
+// streams contiguous 4 KB tiles with bulk (TMA) copies:
+//   pass 1 item (rows r0..r0+nr-1, columns c0..c1-1): tiles of 32 columns, tile[q][l] =
+//     K[r0 + l][jc + q]  (nr x 32 floats, zero outside the skyline)
+//   pass 2 block (32 columns c0..): tiles of 32 cover rows, tile[q][l] = K[row_q][c0 + l]
+//     (32 x 32 floats, zero outside [first(row), row])
+// Fills wl.p1[*].toff / wl.p2b[*].toff.
+void build_tiles(const Inverse& K, WorkLists& wl, std::vector<float>& T1, std::vector<float>& T2);
 
 }  // namespace simhost

@@ -12,6 +12,7 @@
 // No tensor cores: every step is sparse / memory- or latency-bound.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 
@@ -463,7 +464,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 // Memory pipeline: each warp streams its 32x32 tiles of K (and the matching
 // 32 vector entries) into shared memory with cp.async (4-byte, zero-fill for
 // entries outside the skyline), kStages tiles in flight per warp.
-constexpr int kStages = 2;
+constexpr int kStages = 3;       // pass-1 tiles in flight per warp
+constexpr int kStages2 = 3;      // pass-2 tiles in flight per warp
+constexpr int kWarps2 = 6;       // pass-2 warps per CTA
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -497,169 +500,257 @@ struct __align__(16) KTile {
     float4 v[32];       // vector entry q (u_j for pass 1, y_r for pass 2); .w of u carries cb[j]
 };
 
+// ---- bulk (TMA 1-D) copy helpers ---------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+// global -> shared bulk copy completing `bytes` on `bar`; evict-first in L2 when `stream`
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar, bool stream,
+                                         unsigned long long pol) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    if (stream)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+            "%4;\n" ::"r"(s),
+            "l"(gmem), "r"(bytes), "r"(b), "l"(pol)
+            : "memory");
+    else
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(s),
+                     "l"(gmem), "r"(bytes), "r"(b)
+                     : "memory");
+}
+
 // ---- pass 1 ----------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ items,
+// Persistent warps: warp g of G processes items g, g + G, ... (items are sorted by size,
+// so the round robin balances).  An item is <= 32 rows of a panel x <= 1024 columns; its
+// K tiles are contiguous in consumption order (T1, tile = [32 columns][nr rows]).  Each
+// warp streams its tiles with 1-D bulk copies issued by one lane, kStages tiles in flight,
+// and the issue cursor runs ahead across item boundaries so the pipeline never drains.
+// Rows split over several items are combined by the last-arriving warp in fixed order.
+__device__ __forceinline__ int p1_ntiles(const P1Item& it) { return (it.c1 - it.c0 + 31) >> 5; }
+
+__global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ items, int nitems,
                                                    const P1Block* __restrict__ blocks,
-                                                   const float* __restrict__ Kcol, const int32_t* __restrict__ depth,
-                                                   const float4* __restrict__ u, float4* __restrict__ y,
-                                                   double* __restrict__ part, int* __restrict__ counters) {
-    extern __shared__ __align__(16) unsigned char k1smem[];
+                                                   const float* __restrict__ T1, const float4* __restrict__ u,
+                                                   float4* __restrict__ y, double* __restrict__ part,
+                                                   int* __restrict__ counters) {
+    extern __shared__ __align__(128) unsigned char k1smem[];
+    __shared__ __align__(8) uint64_t bars[kWarps][kStages];
     KTile* tiles = reinterpret_cast<KTile*>(k1smem) + (threadIdx.x >> 5) * kStages;
-    double (*s_red)[kWarps][32] = reinterpret_cast<double (*)[kWarps][32]>(k1smem);   // aliases the tiles after the loop
-    __shared__ int s_last;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const P1Item it = items[blockIdx.x];
-    const int r = it.r0 + lane;
-    const bool act = lane < it.nrows;
-    const int base = lane - depth[it.r0];
-    const int nchunk = (it.c1 - it.c0 + 31) >> 5;
+    const int G = gridDim.x * kWarps;
+    const int gw = blockIdx.x * kWarps + w;
+    if (gw >= nitems) return;
     const unsigned long long pol = l2_evict_first();
-    // this warp owns chunks w, w + 8, ...; issue = u entries (16 B each), then the 32x32 K tile
-    auto issue = [&](int ci, KTile& T) {
-        const int jc = it.c0 + 32 * ci;
-        const int j = jc + lane;
-        cp_async16(&T.v[lane], &u[min(j, it.c1 - 1)], j < it.c1);
-        // K addresses need cb[j] = u[j].w: read it from global (L1/L2) for the issuing lane's column
-        const int cbj = j < it.c1 ? __float_as_int(__ldg(&u[j]).w) : 0;
-#pragma unroll 8
-        for (int q = 0; q < 32; ++q) {
-            const int cq = __shfl_sync(0xffffffffu, cbj, q);
-            const bool ok = act && (jc + q < it.c1) && (jc + q <= r);
-            cp_async4_stream(&T.k[q][lane], &Kcol[ok ? cq + base : 0], ok, pol);
+    for (int s = 0; s < kStages; ++s) tiles[s].v[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lane == 0)
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[w][s], 1);
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    // issue cursor
+    int ik = gw, itl = 0;
+    P1Item iI = items[ik];
+    int ntI = p1_ntiles(iI);
+    int n_issued = 0;
+    auto issue_next = [&]() {
+        if (ik >= nitems) return;
+        const int s = n_issued % kStages;
+        const int jc = iI.c0 + 32 * itl;
+        const int ncol = min(32, iI.c1 - jc);
+        if (lane == 0) {
+            mbar_expect_tx(&bars[w][s], (unsigned)(iI.nrows * 128 + ncol * 16));
+            bulk_g2s(tiles[s].k, T1 + iI.toff + (int64_t)itl * iI.nrows * 32, (unsigned)(iI.nrows * 128), &bars[w][s],
+                     true, pol);
+            bulk_g2s(tiles[s].v, u + jc, (unsigned)(ncol * 16), &bars[w][s], false, pol);
+        }
+        ++n_issued;
+        if (++itl == ntI) {
+            itl = 0;
+            ik += G;
+            if (ik < nitems) {
+                iI = items[ik];
+                ntI = p1_ntiles(iI);
+            }
         }
     };
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) issue_next();
+    // compute cursor
+    int ck = gw, ctl = 0;
+    P1Item cI = iI;
+    cI = items[ck];
+    int ntC = p1_ntiles(cI);
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    const int mine = (nchunk - w + kWarps - 1) / kWarps;   // chunks of this warp
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
-        if (s < mine) issue(w + kWarps * s, tiles[s]);
-        cp_async_commit();
-    }
-    for (int t = 0; t < mine; ++t) {
-        const int nx = t + kStages - 1;
-        if (nx < mine) issue(w + kWarps * nx, tiles[nx % kStages]);
-        cp_async_commit();
-        cp_async_wait<kStages - 1>();
-        __syncwarp();
-        const KTile& T = tiles[t % kStages];
+    unsigned par = 0;
+    for (int n_done = 0; ck < nitems; ++n_done) {
+        issue_next();
+        const int s = n_done % kStages;
+        mbar_wait(&bars[w][s], (par >> s) & 1u);
+        par ^= 1u << s;
+        const int nr = cI.nrows;
+        const float* kk = &tiles[s].k[0][0];
+        const float4* vv = tiles[s].v;
         float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+        if (lane < nr) {
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
-            const float kq = T.k[q][lane];
-            const float4 uq = T.v[q];
-            f0 = fmaf(kq, uq.x, f0);
-            f1 = fmaf(kq, uq.y, f1);
-            f2 = fmaf(kq, uq.z, f2);
+            for (int q = 0; q < 32; ++q) {
+                const float kq = kk[q * nr + lane];
+                const float4 uq = vv[q];
+                f0 = fmaf(kq, uq.x, f0);
+                f1 = fmaf(kq, uq.y, f1);
+                f2 = fmaf(kq, uq.z, f2);
+            }
         }
         a0 += (double)f0;
         a1 += (double)f1;
         a2 += (double)f2;
-        __syncwarp();
+        __syncwarp();   // stage s may be refilled by the next issue
+        if (++ctl < ntC) continue;
+        // ---- item complete: write y, or a partial + fixed-order reduction by the last warp
+        const P1Block b = blocks[cI.block];
+        if (b.nitems == 1) {
+            if (lane < nr) y[cI.r0 + lane] = make_float4((float)a0, (float)a1, (float)a2, 0.f);
+        } else {
+            double* pp = part + (size_t)cI.part * 96 + lane;
+            pp[0] = a0;
+            pp[32] = a1;
+            pp[64] = a2;
+            __threadfence();
+            __syncwarp();
+            int old = 0;
+            if (lane == 0) old = atomicAdd(&counters[cI.block], 1);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old == b.nitems - 1) {
+                __threadfence();
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+                for (int q = 0; q < b.nitems; ++q) {
+                    const double* pq = part + (size_t)(b.part0 + q) * 96 + lane;
+                    s0 += __ldcg(pq);
+                    s1 += __ldcg(pq + 32);
+                    s2 += __ldcg(pq + 64);
+                }
+                if (lane < nr) y[cI.r0 + lane] = make_float4((float)s0, (float)s1, (float)s2, 0.f);
+                if (lane == 0) counters[cI.block] = 0;
+            }
+        }
+        a0 = a1 = a2 = 0.0;
+        ctl = 0;
+        ck += G;
+        if (ck < nitems) {
+            cI = items[ck];
+            ntC = p1_ntiles(cI);
+        }
     }
-    cp_async_wait<0>();
-    __syncthreads();   // all warps are done with their tiles before s_red overwrites them
-    s_red[0][w][lane] = a0;
-    s_red[1][w][lane] = a1;
-    s_red[2][w][lane] = a2;
-    __syncthreads();
-    const P1Block b = blocks[it.block];
-    const int t = threadIdx.x;
-    double tot = 0.0;
-    if (t < 96) {
-#pragma unroll
-        for (int q = 0; q < kWarps; ++q) tot += s_red[t >> 5][q][t & 31];
-    }
-    if (b.nitems == 1) {
-        __syncthreads();
-        if (t < 96) s_red[t >> 5][0][t & 31] = tot;
-        __syncthreads();
-        if (t < it.nrows) y[it.r0 + t] = make_float4((float)s_red[0][0][t], (float)s_red[1][0][t], (float)s_red[2][0][t], 0.f);
-        return;
-    }
-    if (t < 96) part[(size_t)it.part * 96 + t] = tot;
-    __threadfence();
-    __syncthreads();
-    if (t == 0) s_last = atomicAdd(&counters[it.block], 1) == b.nitems - 1;
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (t < 96) {
-        double s = 0.0;
-        for (int q = 0; q < b.nitems; ++q) s += __ldcg(&part[(size_t)(b.part0 + q) * 96 + t]);
-        s_red[t >> 5][0][t & 31] = s;
-    }
-    __syncthreads();
-    if (t < it.nrows) y[it.r0 + t] = make_float4((float)s_red[0][0][t], (float)s_red[1][0][t], (float)s_red[2][0][t], 0.f);
-    if (t == 0) counters[it.block] = 0;
 }
 
 constexpr size_t kKpassSmem = sizeof(KTile) * kStages * kWarps;   // >= 3 * kWarps * 32 doubles for s_red
+constexpr int kP2MaxRows = 1536;                                   // cover rows whose y is staged in smem
+constexpr size_t kKpass2Tiles = sizeof(KTile) * kStages2 * kWarps2;  // >= 3 * kWarps2 * 32 doubles
+constexpr size_t kKpass2Smem = kKpass2Tiles + 16 * kP2MaxRows;
 
-void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* Kcol,
-                   const int32_t* depth, const float4* u, float4* y, double* part, int* counters) {
+void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* T1,
+                   const float4* u, float4* y, double* part, int* counters) {
     static bool attr = false;
+    static int nsm = 148;
     if (!attr) {
         cudaFuncSetAttribute(k_kpass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpassSmem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         attr = true;
     }
-    k_kpass1<<<nitems, 32 * kWarps, kKpassSmem, st>>>(it, bl, Kcol, depth, u, y, part, counters);
+    const int ctas = std::min((nitems + kWarps - 1) / kWarps, 2 * nsm);   // persistent: 2 CTAs per SM
+    k_kpass1<<<ctas, 32 * kWarps, kKpassSmem, st>>>(it, nitems, bl, T1, u, y, part, counters);
 }
 
 // ----------------------------------------------------------------------------
-// K-pass 2: x += K^T y.  One CTA per 32-column block (lane = column), warps
-// take interleaved 32-row chunks of the block's cover rows.  K is row-major:
-// K[r][j] = Krow[rb(r) + j], rb(r) = rowptr[r] - first(r) (meta[r] = {rb, first}).
+// K-pass 2: x += K^T y.  One CTA per 32-column block (lane = column).  The block's
+// cover-row tiles ([32 rows][32 columns], consumption order, T2) are streamed with 1-D
+// bulk copies; the y values of all cover rows are staged once in shared memory.
 // No partial sums, no atomics: the CTA owns its 32 columns.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) k_kpass2(const P2Block* __restrict__ blocks,
-                                                   const int32_t* __restrict__ cover, const int2* __restrict__ meta,
-                                                   const float* __restrict__ Krow, const float4* __restrict__ y,
-                                                   double4* __restrict__ x, const double4* __restrict__ xt,
-                                                   double4* __restrict__ v, double inv_h, int finalize_v) {
-    extern __shared__ __align__(16) unsigned char k2smem[];
-    KTile* tiles = reinterpret_cast<KTile*>(k2smem) + (threadIdx.x >> 5) * kStages;
-    double (*s_red)[kWarps][32] = reinterpret_cast<double (*)[kWarps][32]>(k2smem);   // aliases the tiles after the loop
+__global__ void __launch_bounds__(32 * kWarps2, 2) k_kpass2(const P2Block* __restrict__ blocks,
+                                                   const int32_t* __restrict__ cover, const float* __restrict__ T2,
+                                                   const float4* __restrict__ y, double4* __restrict__ x,
+                                                   const double4* __restrict__ xt, double4* __restrict__ v,
+                                                   double inv_h, int finalize_v) {
+    extern __shared__ __align__(128) unsigned char k2smem[];
+    __shared__ __align__(8) uint64_t bars[kWarps2][kStages2];
+    KTile* tiles = reinterpret_cast<KTile*>(k2smem) + (threadIdx.x >> 5) * kStages2;
+    double (*s_red)[kWarps2][32] = reinterpret_cast<double (*)[kWarps2][32]>(k2smem);   // aliases the tiles after the loop
+    float4* s_y = reinterpret_cast<float4*>(k2smem + kKpass2Tiles);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const P2Block b = blocks[blockIdx.x];
-    const int j = b.c0 + lane;
-    const bool act = lane < b.ncols;
     const int nrow = b.list1 - b.list0;
-    const int nchunk = (nrow + 31) >> 5;
+    const int nt = (nrow + 31) >> 5;
+    const int mine = (nt - w + kWarps2 - 1) / kWarps2;
+    const bool staged = nrow <= kP2MaxRows;
     const unsigned long long pol = l2_evict_first();
-    auto issue = [&](int ci, KTile& T) {
-        const int k = b.list0 + 32 * ci + lane;
-        const bool okr = k < b.list1;
-        const int r = okr ? __ldg(&cover[k]) : 0;
-        const int2 m = okr ? __ldg(&meta[r]) : make_int2(0, 1 << 30);
-        cp_async16(&T.v[lane], &y[r], okr);
-#pragma unroll 8
-        for (int q = 0; q < 32; ++q) {
-            const int rq = __shfl_sync(0xffffffffu, r, q);
-            const int rbq = __shfl_sync(0xffffffffu, m.x, q);
-            const int fq = __shfl_sync(0xffffffffu, m.y, q);
-            const bool ok = act && (32 * ci + q < nrow) && j >= fq && j <= rq;
-            cp_async4_stream(&T.k[q][lane], &Krow[ok ? rbq + j : 0], ok, pol);
-        }
-    };
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    const int mine = (nchunk - w + kWarps - 1) / kWarps;
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
-        if (s < mine) issue(w + kWarps * s, tiles[s]);
+    if (lane == 0)
+        for (int s = 0; s < kStages2; ++s) mbar_init(&bars[w][s], 1);
+    if (staged) {
+        for (int q = threadIdx.x; q < 32 * nt; q += blockDim.x)
+            cp_async16(&s_y[q], &y[q < nrow ? __ldg(&cover[b.list0 + q]) : 0], q < nrow);
         cp_async_commit();
     }
+    __syncwarp();
+    auto issue = [&](int t) {
+        const int ti = w + kWarps2 * t;
+        const int s = t % kStages2;
+        if (lane == 0) {
+            mbar_expect_tx(&bars[w][s], 4096u);
+            bulk_g2s(tiles[s].k, T2 + b.toff + (int64_t)ti * 1024, 4096u, &bars[w][s], true, pol);
+        }
+    };
+#pragma unroll
+    for (int t = 0; t < kStages2 - 1; ++t)
+        if (t < mine) issue(t);
+    if (staged) {
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    unsigned par = 0;
     for (int t = 0; t < mine; ++t) {
-        const int nx = t + kStages - 1;
-        if (nx < mine) issue(w + kWarps * nx, tiles[nx % kStages]);
-        cp_async_commit();
-        cp_async_wait<kStages - 1>();
-        __syncwarp();
-        const KTile& T = tiles[t % kStages];
+        if (t + kStages2 - 1 < mine) issue(t + kStages2 - 1);
+        const int s = t % kStages2;
+        const int ti = w + kWarps2 * t;
+        const float4* yy;
+        if (staged) {
+            yy = s_y + 32 * ti;
+        } else {   // very tall trees: gather this tile's y into the tile's vector slot
+            const int kq = 32 * ti + lane;
+            tiles[s].v[lane] = kq < nrow ? __ldg(&y[__ldg(&cover[b.list0 + kq])]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            __syncwarp();
+            yy = tiles[s].v;
+        }
+        mbar_wait(&bars[w][s], (par >> s) & 1u);
+        par ^= 1u << s;
+        const float* kk = &tiles[s].k[0][0];
         float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
-            const float kq = T.k[q][lane];
-            const float4 yq = T.v[q];
+            const float kq = kk[32 * q + lane];
+            const float4 yq = yy[q];
             f0 = fmaf(kq, yq.x, f0);
             f1 = fmaf(kq, yq.y, f1);
             f2 = fmaf(kq, yq.z, f2);
@@ -669,7 +760,6 @@ __global__ void __launch_bounds__(256, 2) k_kpass2(const P2Block* __restrict__ b
         a2 += (double)f2;
         __syncwarp();
     }
-    cp_async_wait<0>();
     __syncthreads();   // all warps are done with their tiles before s_red overwrites them
     s_red[0][w][lane] = a0;
     s_red[1][w][lane] = a1;
@@ -679,7 +769,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass2(const P2Block* __restrict__ b
     if (t < 96) {
         double tot = 0.0;
 #pragma unroll
-        for (int q = 0; q < kWarps; ++q) tot += s_red[t >> 5][q][t & 31];
+        for (int q = 0; q < kWarps2; ++q) tot += s_red[t >> 5][q][t & 31];
         s_red[t >> 5][0][t & 31] = tot;   // each thread owns its (comp, lane) slot: no race
     }
     __syncthreads();
@@ -696,15 +786,14 @@ __global__ void __launch_bounds__(256, 2) k_kpass2(const P2Block* __restrict__ b
     }
 }
 
-void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const int2* meta,
-                   const float* Krow, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
-                   int finalize_v) {
+void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const float* T2,
+                   const float4* y, double4* x, const double4* xt, double4* v, double inv_h, int finalize_v) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_kpass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpassSmem);
+        cudaFuncSetAttribute(k_kpass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpass2Smem);
         attr = true;
     }
-    k_kpass2<<<nblocks, 32 * kWarps, kKpassSmem, st>>>(bl, cover, meta, Krow, y, x, xt, v, inv_h, finalize_v);
+    k_kpass2<<<nblocks, 32 * kWarps2, kKpass2Smem, st>>>(bl, cover, T2, y, x, xt, v, inv_h, finalize_v);
 }
 
 // ----------------------------------------------------------------------------

@@ -65,12 +65,11 @@ void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const 
                    const float4* fc, const double* M, const double4* x, const double4* s,
                    const int32_t* vcp, const int32_t* vci, const float* vcw, const double* hl,
                    const int32_t* cb, float4* u, double* resid_dbg);
-// u[j].w carries cb[j] = colptr[j] + depth[j] as int bits (column base for pass 1)
-void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* Kcol,
-                   const int32_t* depth, const float4* u, float4* y, double* part, int* counters);
-void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const int2* meta,
-                   const float* Krow, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
-                   int finalize_v);
+// K-passes over the tile streams T1 / T2 (see simhost::build_tiles)
+void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* T1,
+                   const float4* u, float4* y, double* part, int* counters);
+void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const float* T2,
+                   const float4* y, double4* x, const double4* xt, double4* v, double inv_h, int finalize_v);
 void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
                       const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
                       const float4* y, double* dxt);
