@@ -163,8 +163,8 @@ int sim_set_stream(sim_handle *h, void *cuda_stream);
 /* Kernel timing: when on, the captured frame graph records an event between
  * consecutive kernels; sim_get_kernel_times then returns, per kernel kind
  * (0 predict, 1 contact_eval, 2 local, 3 gather, 4 kpass1, 5 chain_dot, 6 cr,
- * 7 scatter, 8 kpass2), the summed device ms of the most recent frame.
- * out must hold >= 9 doubles. */
+ * 7 scatter, 8 kpass2, 9 active-set + G_A gather), the summed device ms of
+ * the most recent frame.  out must hold >= 10 doubles. */
 int sim_set_profiling(sim_handle *h, int on);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 

@@ -18,7 +18,7 @@ EXPORTED_SYMBOLS = [
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline",
 ]
-KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2"]
+KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
 
 class SimMesh(C.Structure):

@@ -111,7 +111,8 @@ struct sim_handle {
     DBuf<int32_t> slot_vtx, scp, sci, vcp, vci;
     DBuf<float> scw, vcw;
     DBuf<double> G, GA;   // Delassus Gram and the CR's active-block scratch
-    DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res;
+    DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res, rho;
+    DBuf<int> act_na, act_idx, act_pos, act_con;   // CR active set (k_active)
     DBuf<int32_t> chain_off, chain_rows;
     DBuf<uint8_t> flag;
     DBuf<int> ucount;
@@ -245,7 +246,8 @@ extern "C" void sim_destroy(sim_handle* H) {
         H->dc.release(); H->cc9.release(); H->cs0.release(); H->cv0.release(); H->cc1.release(); H->slot_vtx.release(); H->scp.release(); H->sci.release(); H->vcp.release();
         H->vci.release(); H->scw.release(); H->vcw.release(); H->G.release(); H->GA.release(); H->lam.release();
         H->theta.release(); H->cdiag.release(); H->hvec.release(); H->hl.release(); H->dxt.release();
-        H->wz.release(); H->phi_abs.release(); H->cr_res.release();
+        H->wz.release(); H->phi_abs.release(); H->cr_res.release(); H->rho.release();
+        H->act_na.release(); H->act_idx.release(); H->act_pos.release(); H->act_con.release();
         for (auto e : H->pev) cudaEventDestroy(e);
         if (H->stage_free) cudaEventDestroy(H->stage_free);
         if (H->fork_ev) cudaEventDestroy(H->fork_ev);
@@ -369,6 +371,8 @@ static int upload_all(sim_handle* H) {
     CK(H->lam.alloc(3 * kMaxContacts)); CK(H->theta.alloc(3 * kMaxContacts)); CK(H->cdiag.alloc(3 * kMaxContacts));
     CK(H->hvec.alloc(3 * kMaxContacts)); CK(H->hl.alloc(3 * kMaxContacts)); CK(H->dxt.alloc(3 * kMaxSlots));
     CK(H->wz.alloc(3 * kMaxSlots)); CK(H->phi_abs.alloc(kMaxContacts)); CK(H->cr_res.alloc(1));
+    CK(H->rho.alloc(3 * kMaxContacts)); CK(H->act_na.alloc(1)); CK(H->act_idx.alloc(kMaxSlots));
+    CK(H->act_pos.alloc(kMaxSlots)); CK(H->act_con.alloc(kMaxSlots));
     CK(H->chain_off.alloc(kMaxSlots + 1)); CK(H->flag.alloc(nf)); CK(H->ucount.alloc(2)); CK(H->ulist.alloc(nf));
     CK(cudaMemsetAsync(H->ucount.p, 0, 2 * sizeof(int), st));
     CK(cudaMemsetAsync(H->lam.p, 0, 3 * kMaxContacts * sizeof(double), st));
@@ -617,16 +621,18 @@ static Params make_params(const sim_handle* H) {
 }
 
 static ContactState cstate(sim_handle* H) {
-    return ContactState{H->lam.p, H->theta.p, H->cdiag.p, H->hvec.p, H->hl.p, H->dxt.p, H->wz.p, H->phi_abs.p, H->cr_res.p};
+    return ContactState{H->lam.p, H->theta.p, H->cdiag.p, H->hvec.p, H->hl.p, H->dxt.p, H->wz.p, H->phi_abs.p, H->cr_res.p, H->rho.p};
 }
 
 // enqueue one frame (predict + iters x L-G); returns kernel count or negative
-enum { KK_PREDICT, KK_CONTACT, KK_LOCAL, KK_GATHER, KK_KPASS1, KK_CHAIN, KK_CR, KK_SCATTER, KK_KPASS2, KK_N };
+enum { KK_PREDICT, KK_CONTACT, KK_LOCAL, KK_GATHER, KK_KPASS1, KK_CHAIN, KK_CR, KK_SCATTER, KK_KPASS2, KK_ACTIVE, KK_N };
 
 static int enqueue_frame(sim_handle* H, int iters) {
     cudaStream_t st = H->stream;
     Params P = make_params(H);
     ContactState cs = cstate(H);
+    const CrContacts ccr{H->cc9.p, H->cs0.p, H->cv0.p, H->cc1.p};
+    const CrActive act{H->act_na.p, H->act_idx.p, H->act_pos.p, H->act_con.p};
     int nk = 0;
     size_t ev = 0;
     H->pkind.clear();
@@ -654,9 +660,11 @@ static int enqueue_frame(sim_handle* H, int iters) {
             CKR(cudaEventRecord(H->fork_ev, st));
             CKR(cudaStreamWaitEvent(H->aux, H->fork_ev, 0));
             launch_contact_eval(H->aux, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
+            launch_active(H->aux, H->ns, ccr, H->scp.p, H->sci.p, cs, act, H->G.p, H->GA.p); nk += 2;
             CKR(cudaEventRecord(H->join_ev, H->aux));
         } else if (con) {
             MARK(KK_CONTACT); launch_contact_eval(st, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
+            MARK(KK_ACTIVE); launch_active(st, H->ns, ccr, H->scp.p, H->sci.p, cs, act, H->G.p, H->GA.p); nk += 2;
         }
         MARK(KK_LOCAL);
         launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, H->x.p, H->fc.p, nullptr); nk++;
@@ -670,10 +678,9 @@ static int enqueue_frame(sim_handle* H, int iters) {
         if (con) {
             MARK(KK_CHAIN);
             launch_chain_dot(st, H->ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
-                             H->y.p, H->dxt.p); nk++;
+                             H->y.p, H->dxt.p, ccr, H->x.p, cs); nk++;
             MARK(KK_CR);
-            int e = launch_cr(st, P, H->dc.p, CrContacts{H->cc9.p, H->cs0.p, H->cv0.p, H->cc1.p}, H->slot_vtx.p, H->scp.p,
-                              H->sci.p, H->scw.p, H->G.p, H->GA.p, H->x.p, cs); nk++;
+            int e = launch_cr(st, P, H->dc.p, ccr, H->scp.p, H->sci.p, H->scw.p, H->GA.p, H->x.p, cs, act); nk++;
             if (e) return -e;
             MARK(KK_SCATTER);
             launch_scatter(st, H->n_f, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;

@@ -804,7 +804,8 @@ __global__ void __launch_bounds__(256) k_chain_dot(int ns, const int32_t* __rest
                                                    const float* __restrict__ Kcol, const int64_t* __restrict__ colptr,
                                                    const int32_t* __restrict__ chain_off,
                                                    const int32_t* __restrict__ chain_rows, const float4* __restrict__ y,
-                                                   double* __restrict__ dxt) {
+                                                   double* __restrict__ dxt, CrContacts cc,
+                                                   const double4* __restrict__ x, ContactState cs) {
     // one CTA per contact vertex; its 8 warps take interleaved 128-entry slices of the chain
     __shared__ double s_red[3][kWarps];
     const int s = blockIdx.x;
@@ -845,19 +846,102 @@ __global__ void __launch_bounds__(256) k_chain_dot(int ns, const int32_t* __rest
         s_red[2][w] = a2;
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
-        double t = 0.0;
+    if (threadIdx.x == 0) {
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
-        for (int q = 0; q < kWarps; ++q) t += s_red[threadIdx.x][q];
-        dxt[3 * s + threadIdx.x] = t;
+        for (int q = 0; q < kWarps; ++q) { t0 += s_red[0][q]; t1 += s_red[1][q]; t2 += s_red[2][q]; }
+        dxt[3 * s] = t0;
+        dxt[3 * s + 1] = t1;
+        dxt[3 * s + 2] = t2;
+        // Schur RHS rho = h - theta J x~, x~ = x^k + K^T y, for the single contact on this slot
+        // (other contacts are handled in the CR prologue)
+        const int c = cc.c1[s];
+        if (c >= 0) {
+            const double4 xa = x[cc.v0[c]];
+            const double xs0 = xa.x + t0, xs1 = xa.y + t1, xs2 = xa.z + t2;
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) {
+                const float* c3 = cc.c9 + 9 * c + 3 * kk;
+                cs.rho[3 * c + kk] = cs.hvec[3 * c + kk] - cs.theta[3 * c + kk] * ((double)c3[0] * xs0 +
+                                                                                   (double)c3[1] * xs1 +
+                                                                                   (double)c3[2] * xs2);
+            }
+        }
     }
 }
 
 void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
                       const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
-                      const float4* y, double* dxt) {
+                      const float4* y, double* dxt, CrContacts cc, const double4* x, ContactState cs) {
     if (ns == 0) return;
-    k_chain_dot<<<ns, 32 * kWarps, 0, st>>>(ns, slot_vtx, Kcol, colptr, chain_off, chain_rows, y, dxt);
+    k_chain_dot<<<ns, 32 * kWarps, 0, st>>>(ns, slot_vtx, Kcol, colptr, chain_off, chain_rows, y, dxt, cc, x, cs);
+}
+
+// ----------------------------------------------------------------------------
+// active contact vertices of this iteration (any incident row with theta != 0), in
+// ascending slot order, and the active block G_A of the Delassus Gram.  These depend only
+// on theta, so they run in a graph branch beside the RHS gather and K-pass 1.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_active(int ns, CrContacts cc, const int32_t* __restrict__ scp,
+                                                 const int32_t* __restrict__ sci, ContactState cs, CrActive act) {
+    __shared__ int wsum[32];
+    __shared__ int base;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < ns; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        bool on = false;
+        int only = -1;
+        if (b < ns) {
+            only = cc.c1[b];
+            if (only >= 0) {
+                on = cs.theta[3 * only] != 0.0 || cs.theta[3 * only + 1] != 0.0 || cs.theta[3 * only + 2] != 0.0;
+            } else {
+                for (int q = scp[b]; q < scp[b + 1] && !on; ++q) {
+                    const int c = sci[q];
+                    on = cs.theta[3 * c] != 0.0 || cs.theta[3 * c + 1] != 0.0 || cs.theta[3 * c + 2] != 0.0;
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        int off = base;
+        for (int q = 0; q < wid; ++q) off += wsum[q];
+        off += __popc(bal & ((1u << lane) - 1u));
+        if (b < ns) {
+            act.apos[b] = on ? off : -1;
+            if (on) {
+                act.aidx[off] = b;
+                act.acon[off] = only;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = base;
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += wsum[q];
+            base = t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) act.na[0] = base;
+}
+
+__global__ void __launch_bounds__(256) k_gather_ga(int ns, const double* __restrict__ G, CrActive act,
+                                                   double* __restrict__ GA) {
+    const int na = act.na[0];
+    const int i = blockIdx.x;
+    if (i >= na) return;
+    const size_t row = (size_t)act.aidx[i] * ns;
+    for (int j = threadIdx.x; j < na; j += blockDim.x) GA[(size_t)i * na + j] = G[row + act.aidx[j]];
+}
+
+void launch_active(cudaStream_t st, int ns, CrContacts cc, const int32_t* scp, const int32_t* sci, ContactState cs,
+                   CrActive act, const double* G, double* GA) {
+    if (ns == 0) return;
+    k_active<<<1, 1024, 0, st>>>(ns, cc, scp, sci, cs, act);
+    k_gather_ga<<<ns, 256, 0, st>>>(ns, G, act, GA);
 }
 
 // per-contact-set: chain rows of every slot (walk panel runs) + row flags
@@ -1102,20 +1186,18 @@ void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const double* G) {
 // CR (Saad Alg. 6.20) on S = Theta D Theta + C, z0 = 0, exactly N_CR matvecs
 // (reading A19), in ONE cluster of kCluster CTAs.
 //
-// * Theta-sparsity: rows with theta = 0 (separated contacts, inactive
-//   friction) contribute nothing to Theta D Theta, so the D product only runs
-//   over the "active" contact vertices (any row with theta != 0).  The active
-//   block G_A of G is gathered once per CR call (exact, not an approximation),
-//   into shared memory when this CTA's rows fit.
-// * Every CTA runs the O(m) recurrences redundantly (dot products come out
-//   identical everywhere without communication).  Each thread owns rows
-//   j = tid + 512 k: z, p, Ap, Ar live in its registers; only r (read by the
-//   W gather) is in shared memory.  q = G_A W is split by rows of G_A and
-//   exchanged through DSMEM (one cluster barrier per matvec).
-// * fp64 in the D product: G = A_v^-1 is a smoothing kernel, so G W cancels
-//   heavily for the oscillatory Krylov vectors (fp32 W or fp32 sums cost ~3e-3).
-//   (S v)_j = theta_j c_j . sum_{a in j} w_ja q_a + C_j v_j,
-//   q_a = sum_b G_ab W_b,   W_b = sum_{rows k at b} w_kb theta_k c_k v_k.
+// * Theta-sparsity: rows with theta = 0 contribute nothing to Theta D Theta, so the D
+//   product runs over the active contact vertices only (k_active / k_gather_ga build the
+//   active block G_A of G in a graph branch; exact, not an approximation).
+// * Every CTA runs the O(m) recurrences redundantly (dot products come out identical
+//   everywhere without communication).  Thread t owns rows t + 512 k: z, p, Ap, Ar are
+//   registers, r (read by the W gather) is in shared memory.  q = G_A W is split by rows
+//   of G_A and exchanged with st.async + mbarrier transaction counts (no cluster barrier).
+// * One block reduction per iteration: after Ar = S r the three dots r.Ar, Ar.Ar, Ar.Ap
+//   give beta and |Ap_new|^2 = Ar.Ar + 2 beta Ar.Ap + beta^2 |Ap|^2 (algebraically the
+//   oracle's direct form).
+// * fp64 in the D product: G = A_v^-1 is a smoothing kernel, so G W cancels heavily for
+//   the oscillatory Krylov vectors (fp32 W or fp32 sums cost ~3e-3).
 // ----------------------------------------------------------------------------
 constexpr int kRptMax = 6;   // rows per thread: m = 3 nc <= kRpt * kCrThreads (kernel templated on kRpt)
 
@@ -1130,35 +1212,12 @@ struct CrLayout {
         c9 = take(4 * 9 * (size_t)nc); s0 = take(4 * (size_t)nc);
         W = take(8 * 3 * (size_t)ns); q = take(8 * 2 * 3 * (size_t)ns);
         aidx = take(4 * (size_t)ns); apos = take(4 * (size_t)ns); acon = take(4 * (size_t)ns);
-        red = take(8 * 3 * (kCrThreads / 32) + 4 * (kCrThreads / 32 + 1));   // 3 doubles/warp + scan ints
-        mbar = take(32);   // two exchange mbarriers (one per q buffer)
+        red = take(8 * 2 * 3 * (kCrThreads / 32));   // double-buffered 3 doubles per warp
+        mbar = take(32);                              // two exchange mbarriers (one per q buffer)
         gA = o;
         total = o;
     }
 };
-
-__device__ __forceinline__ double block_sum(double s, double* red) {
-    s = warp_sum(s);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) red[w] = s;
-    __syncthreads();
-    double t = 0.0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
-    return t;
-}
-__device__ __forceinline__ void block_sum2(double s1, double s2, double* red, double& o1, double& o2) {
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) { red[2 * w] = s1; red[2 * w + 1] = s2; }
-    __syncthreads();
-    double t1 = 0.0, t2 = 0.0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) { t1 += red[2 * k]; t2 += red[2 * k + 1]; }
-    o1 = t1;
-    o2 = t2;
-}
 
 __device__ unsigned long long g_cr_clock[32];   // phase timestamps (ns) of the last CR call, rank 0
 __device__ __forceinline__ void cr_stamp(int i) {
@@ -1174,12 +1233,23 @@ struct CrCtx {
     float *th, *cd, *c9;
     int *s0, *aidx, *apos, *acon;
     int na, ns, i0, i1, gA_smem;
-    unsigned mbar;   // shared-window address of this CTA's exchange mbarriers (2 x 8 B, one per q buffer)
-    unsigned phase;  // q buffer / barrier used by the next exchange (alternates)
-    unsigned par0, par1;   // phase parity of each barrier (scalars: no dynamic indexing)
-    int stamp;       // >= 0: write fine-grained phase stamps of this apply at g_cr_clock[stamp..]
-    const double* GAg;   // global fallback for this CTA's G_A rows
+    unsigned mbar;         // shared-window address of the 2 exchange mbarriers
+    unsigned par0, par1;   // phase parity of each barrier
+    int stamp;             // >= 0: fine-grained phase stamps of this apply at g_cr_clock[stamp..]
+    const double* GAg;     // G_A in global memory (fallback when this CTA's rows do not fit)
 };
+
+// single-barrier block sum of 3 doubles (red is double-buffered by the caller)
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* red) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_sum(c);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { red[3 * w] = a; red[3 * w + 1] = b; red[3 * w + 2] = c; }
+    __syncthreads();
+    a = b = c = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { a += red[3 * q]; b += red[3 * q + 1]; c += red[3 * q + 2]; }
+}
 
 // Ar = S r for this thread's rows (registers); r is read from shared memory
 template <int kRpt>
@@ -1187,14 +1257,14 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
                                          const int32_t* __restrict__ scp, const int32_t* __restrict__ sci,
                                          const float* __restrict__ scw, int buf, double (&Ar)[kRpt]) {
     const int na = X.na;
-    double* qb = X.q + (size_t)buf * 3 * X.ns;   // SoA: q0 | q1 | q2 (conflict-free reads in Sv)
+    double* qb = X.q + (size_t)buf * 3 * X.ns;   // SoA: q0 | q1 | q2
     const unsigned bar = X.mbar + 8u * (unsigned)buf;
-    if (threadIdx.x == 0 && na > 0)   // this phase expects 32 bytes per row of G_A from the peers
+    if (threadIdx.x == 0 && na > 0)   // this phase expects 24 bytes per row of G_A from the peers
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(24 * na) : "memory");
     for (int i = threadIdx.x; i < na; i += blockDim.x) {
         double w0 = 0.0, w1 = 0.0, w2 = 0.0;
         const int c1 = X.acon[i];
-        if (c1 >= 0) {   // a single single-vertex contact on this slot (weight 1)
+        if (c1 >= 0) {   // the single single-vertex contact on this slot (weight 1)
             const float* cc = X.c9 + 9 * c1;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
@@ -1247,8 +1317,7 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
         d1 = warp_sum(d1);
         d2 = warp_sum(d2);
         if (lane < kCluster) {
-            // asynchronous 32-byte store of q_i into CTA `lane`, completing 32 tx bytes on
-            // that CTA's mbarrier for this buffer (no fences, no cluster barrier)
+            // asynchronous stores of q_i into CTA `lane`, completing 24 tx bytes on its mbarrier
             const unsigned l0 = (unsigned)__cvta_generic_to_shared(qb + i);
             const unsigned l1 = (unsigned)__cvta_generic_to_shared(qb + na + i);
             const unsigned l2 = (unsigned)__cvta_generic_to_shared(qb + 2 * na + i);
@@ -1257,12 +1326,15 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
             asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r1) : "r"(l1), "r"(lane));
             asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r2) : "r"(l2), "r"(lane));
             asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(bar), "r"(lane));
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n"
-                         ::"r"(r0), "d"(d0), "r"(rb) : "memory");
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n"
-                         ::"r"(r1), "d"(d1), "r"(rb) : "memory");
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n"
-                         ::"r"(r2), "d"(d2), "r"(rb) : "memory");
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(r0),
+                         "d"(d0), "r"(rb)
+                         : "memory");
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(r1),
+                         "d"(d1), "r"(rb)
+                         : "memory");
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(r2),
+                         "d"(d2), "r"(rb)
+                         : "memory");
         }
     }
     if (X.stamp >= 0) cr_stamp(X.stamp + 1);
@@ -1303,16 +1375,13 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
         }
         Ar[k] = th * acc + (double)X.cd[j] * X.r[j];
     }
-    X.phase ^= 1u;
 }
-
 
 template <int kRpt>
 __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1)
-    k_cr(Params P, const DContact* __restrict__ C, CrContacts cc, const int32_t* __restrict__ slot_vtx,
-         const int32_t* __restrict__ scp, const int32_t* __restrict__ sci, const float* __restrict__ scw,
-         const double* __restrict__ G, double* __restrict__ GA, const double4* __restrict__ x, ContactState cs,
-         int gA_cap) {
+    k_cr(Params P, const DContact* __restrict__ C, CrContacts cc, const int32_t* __restrict__ scp,
+         const int32_t* __restrict__ sci, const float* __restrict__ scw, const double* __restrict__ GA,
+         const double4* __restrict__ x, ContactState cs, CrActive act, int gA_cap) {
     extern __shared__ __align__(16) unsigned char smraw[];
     const CrLayout L(P.nc, P.ns);
     cg::cluster_group cl = cg::this_cluster();
@@ -1332,33 +1401,46 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
     X.acon = (int*)(smraw + L.acon);
     X.red = (double*)(smraw + L.red);
     X.gA = (double*)(smraw + L.gA);
+    X.mbar = (unsigned)__cvta_generic_to_shared(smraw + L.mbar);
+    X.par0 = X.par1 = 0u;
+    X.stamp = -1;
+    X.ns = ns;
+    X.GAg = GA;
+    // everything the prologue needs is precomputed (chain dot, k_active): plain loads only
     for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[e], true);
     for (int c = threadIdx.x; c < nc; c += blockDim.x) cp_async4(&X.s0[c], &cc.s0[c], true);
+    for (int b = threadIdx.x; b < ns; b += blockDim.x) {
+        cp_async4(&X.aidx[b], &act.aidx[b], true);
+        cp_async4(&X.apos[b], &act.apos[b], true);
+        cp_async4(&X.acon[b], &act.acon[b], true);
+    }
     cp_async_commit();
-    X.mbar = (unsigned)__cvta_generic_to_shared(smraw + L.mbar);
-    X.phase = 0u;
-    X.stamp = -1;
-    cr_stamp(22);
-    // rho_j = h_j - theta_j c_j . x~_c, x~ = x^k + K^T y at the contact vertices (owner rows)
+    const int na = act.na[0];
+    X.na = na;
+    {
+        const int per = (na + kCluster - 1) / kCluster;
+        X.i0 = min(na, (int)cl.block_rank() * per);
+        X.i1 = min(na, X.i0 + per);
+        X.gA_smem = (size_t)(X.i1 - X.i0) * na <= (size_t)gA_cap;
+        if (X.gA_smem)
+            for (int e = threadIdx.x; e < (X.i1 - X.i0) * na; e += blockDim.x)
+                X.gA[e] = __ldcg(&GA[(size_t)X.i0 * na + e]);
+    }
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) {
         z[k] = p[k] = Ap[k] = Ar[k] = 0.0;
         const int j = threadIdx.x + kCrThreads * k;
         if (j < m) {
-            const int c = j / 3, kk = j - 3 * c;
-            const int v0 = __ldg(&cc.v0[c]);
+            const int c = j / 3;
             const double th = cs.theta[j];
-            double xs0, xs1, xs2;
-            if (v0 >= 0) {
-                const int sl = __ldg(&cc.s0[c]);
-                const double4 xa = x[v0];
-                xs0 = xa.x + cs.dxt[3 * sl];
-                xs1 = xa.y + cs.dxt[3 * sl + 1];
-                xs2 = xa.z + cs.dxt[3 * sl + 2];
-            } else {   // general multi-vertex contact
+            double rho = cs.rho[j];
+            const int v0 = __ldg(&cc.v0[c]);
+            const bool viaSlot = v0 >= 0 && __ldg(&cc.c1[__ldg(&cc.s0[c])]) == c;
+            if (!viaSlot) {   // rho of contacts the chain dot did not cover
+                const int kk = j - 3 * c;
                 const DContact& ct = C[c];
-                xs0 = xs1 = xs2 = 0.0;
+                double xs0 = 0.0, xs1 = 0.0, xs2 = 0.0;
                 for (int q = 0; q < ct.nv; ++q) {
                     const double4 xa = x[ct.vtx[q]];
                     const int sl = ct.slot[q];
@@ -1366,10 +1448,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
                     xs1 += ct.w[q] * (xa.y + cs.dxt[3 * sl + 1]);
                     xs2 += ct.w[q] * (xa.z + cs.dxt[3 * sl + 2]);
                 }
+                rho = cs.hvec[j] - th * (ct.c[kk][0] * xs0 + ct.c[kk][1] * xs1 + ct.c[kk][2] * xs2);
             }
-            const float* c3 = cc.c9 + 9 * c + 3 * kk;
-            const double rho = cs.hvec[j] - th * ((double)__ldg(&c3[0]) * xs0 + (double)__ldg(&c3[1]) * xs1 +
-                                                  (double)__ldg(&c3[2]) * xs2);
             X.th[j] = (float)th;
             X.cd[j] = (float)cs.cdiag[j];
             X.r[j] = rho;
@@ -1377,87 +1457,26 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
         }
     }
     cp_async_wait<0>();
-    __syncthreads();
-    cr_stamp(1);
-    // active slots: any incident row with theta != 0, ascending slot order (block scan)
-    int* cnt = reinterpret_cast<int*>(X.red + 3 * (kCrThreads / 32));
-    if (threadIdx.x == 0) cnt[0] = 0;
-    __syncthreads();
-    for (int b0 = 0; b0 < ns; b0 += blockDim.x) {
-        const int b = b0 + threadIdx.x;
-        bool act = false;
-        int only = -1;
-        if (b < ns) {
-            only = __ldg(&cc.c1[b]);
-            if (only >= 0) {
-                act = X.th[3 * only] != 0.f || X.th[3 * only + 1] != 0.f || X.th[3 * only + 2] != 0.f;
-            } else {
-                for (int q = scp[b]; q < scp[b + 1] && !act; ++q) {
-                    const int c = sci[q];
-                    act = X.th[3 * c] != 0.f || X.th[3 * c + 1] != 0.f || X.th[3 * c + 2] != 0.f;
-                }
-            }
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, act);
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-        if (lane == 0) cnt[1 + wid] = __popc(bal);
-        __syncthreads();
-        int off = cnt[0];
-        for (int q = 0; q < wid; ++q) off += cnt[1 + q];
-        off += __popc(bal & ((1u << lane) - 1u));
-        if (b < ns) {
-            X.apos[b] = act ? off : -1;
-            if (act) {
-                X.aidx[off] = b;
-                X.acon[off] = only;
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int tot = cnt[0];
-            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += cnt[1 + q];
-            cnt[0] = tot;
-        }
-        __syncthreads();
-    }
-    const int na = cnt[0];
-    X.na = na;
-    X.ns = ns;
-    X.par0 = X.par1 = 0u;
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(X.mbar));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(X.mbar + 8u));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    cl.sync();   // every CTA's exchange mbarrier is initialised before any remote arrive
-    cr_stamp(24);
+    cl.sync();   // smem staged everywhere; every CTA's exchange mbarriers initialised
+    cr_stamp(1);
     if (threadIdx.x == 0 && cl.block_rank() == 0) g_cr_clock[31] = g_cr_clock[0] + 1000ull * na;   // na (debug)
-    {
-        const int per = (na + kCluster - 1) / kCluster;
-        X.i0 = min(na, (int)cl.block_rank() * per);
-        X.i1 = min(na, X.i0 + per);
-        X.gA_smem = (size_t)(X.i1 - X.i0) * na <= (size_t)gA_cap;
-        X.GAg = GA;
-        double* dst = X.gA_smem ? X.gA : GA + (size_t)X.i0 * na;
-        for (int e = threadIdx.x; e < (X.i1 - X.i0) * na; e += blockDim.x) {
-            const int i = X.i0 + e / na, jj = e % na;
-            dst[e] = __ldg(&G[(size_t)X.aidx[i] * ns + X.aidx[jj]]);
-        }
-    }
-    __syncthreads();
-    cr_stamp(2);
-    double rr = 0.0;
+    double rr = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) rr = fma(p[k], p[k], rr);
-    rr = block_sum(rr, X.red);
-    // CR with one block reduction per iteration: after Ar = S r the three dots
-    // r.Ar, Ar.Ar, Ar.Ap give beta and |Ap_new|^2 = Ar.Ar + 2 beta Ar.Ap +
-    // beta^2 |Ap|^2 (algebraically identical to the direct form of the oracle).
+    int rb = 0;   // reduction buffer
+    block_sum3(rr, t1, t2, X.red + rb * 3 * (kCrThreads / 32));
+    rb ^= 1;
+    cr_stamp(2);
     if (rr > 0.0 && P.cr_iters > 0) {
-        cr_stamp(25);
-        cr_apply(cl, X, m, C, scp, sci, scw, (int)X.phase, Ar);
-        cr_stamp(26);
-        double rAr = 0.0, ApAp = 0.0;
+        int buf = 0;
+        cr_apply<kRpt>(cl, X, m, C, scp, sci, scw, buf, Ar);
+        buf ^= 1;
+        double rAr = 0.0, ApAp = 0.0, dummy = 0.0;
 #pragma unroll
         for (int k = 0; k < kRpt; ++k) {
             const int j = threadIdx.x + kCrThreads * k;
@@ -1467,7 +1486,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
                 ApAp = fma(Ap[k], Ap[k], ApAp);
             }
         }
-        block_sum2(rAr, ApAp, X.red, rAr, ApAp);
+        block_sum3(rAr, ApAp, dummy, X.red + rb * 3 * (kCrThreads / 32));
+        rb ^= 1;
         for (int it = 0; it < P.cr_iters; ++it) {
             if (ApAp <= 1e-300 || fabs(rAr) <= 1e-300) break;
             const double alpha = rAr / ApAp;
@@ -1483,7 +1503,8 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
             if (it == P.cr_iters - 1) break;
             X.stamp = it == 3 ? 13 : -1;
             if (it == 3) cr_stamp(12);
-            cr_apply(cl, X, m, C, scp, sci, scw, (int)X.phase, Ar);
+            cr_apply<kRpt>(cl, X, m, C, scp, sci, scw, buf, Ar);
+            buf ^= 1;
             if (it == 3) cr_stamp(16);
             double s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
@@ -1495,28 +1516,15 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
                     s3 = fma(Ar[k], Ap[k], s3);
                 }
             }
-            s1 = warp_sum(s1);
-            s2 = warp_sum(s2);
-            s3 = warp_sum(s3);
-            {
-                const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-                __syncthreads();
-                if (l == 0) { X.red[3 * w] = s1; X.red[3 * w + 1] = s2; X.red[3 * w + 2] = s3; }
-                __syncthreads();
-                s1 = s2 = s3 = 0.0;
-                for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-                    s1 += X.red[3 * q];
-                    s2 += X.red[3 * q + 1];
-                    s3 += X.red[3 * q + 2];
-                }
-            }
+            block_sum3(s1, s2, s3, X.red + rb * 3 * (kCrThreads / 32));
+            rb ^= 1;
             const double beta = s1 / rAr;
             rAr = s1;
             ApAp = s2 + 2.0 * beta * s3 + beta * beta * ApAp;
 #pragma unroll
             for (int k = 0; k < kRpt; ++k) {
-                p[k] = (threadIdx.x + kCrThreads * k < m ? X.r[min(threadIdx.x + kCrThreads * k, m - 1)] : 0.0) +
-                       beta * p[k];
+                const int j = min(threadIdx.x + kCrThreads * k, m - 1);
+                p[k] = X.r[j] + beta * p[k];
                 Ap[k] = Ar[k] + beta * Ap[k];
             }
             if (it == 3) cr_stamp(17);
@@ -1524,13 +1532,13 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
         }
     }
     cr_stamp(20);
-    double res = 0.0;
+    double res = 0.0, u1 = 0.0, u2 = 0.0;
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) {
         const int j = threadIdx.x + kCrThreads * k;
         if (j < m) res = fma(X.r[j], X.r[j], res);
     }
-    res = block_sum(res, X.red);
+    block_sum3(res, u1, u2, X.red + rb * 3 * (kCrThreads / 32));
     cr_stamp(27);
     // epilogue split over the cluster (every CTA holds the identical z):
     // lambda += z / h^2 (reading A11) for this CTA's rows; z to shared memory (reuse r)
@@ -1580,9 +1588,9 @@ int read_cr_clock(unsigned long long* out) {
 
 size_t cr_smem_bytes(int nc, int ns) { return CrLayout(nc, ns).total; }
 
-int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc, const int32_t* slot_vtx,
-              const int32_t* scp, const int32_t* sci, const float* scw, const double* G, double* GA,
-              const double4* x, ContactState cs) {
+int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc, const int32_t* scp,
+              const int32_t* sci, const float* scw, const double* GA, const double4* x, ContactState cs,
+              CrActive act) {
     if (P.nc == 0) return 0;
     static bool attr = false;
     if (!attr) {
@@ -1598,14 +1606,16 @@ int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc
     const size_t base = cr_smem_bytes(P.nc, P.ns);
     const int cap = (int)((kCrMaxSmem - base) / sizeof(double));
     const int rpt = (3 * P.nc + kCrThreads - 1) / kCrThreads;
+#define CRL(R) k_cr<R><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, scp, sci, scw, GA, x, cs, act, cap)
     switch (rpt) {
-        case 1: k_cr<1><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
-        case 2: k_cr<2><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
-        case 3: k_cr<3><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
-        case 4: k_cr<4><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
-        case 5: k_cr<5><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
-        default: k_cr<6><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, slot_vtx, scp, sci, scw, G, GA, x, cs, cap); break;
+        case 1: CRL(1); break;
+        case 2: CRL(2); break;
+        case 3: CRL(3); break;
+        case 4: CRL(4); break;
+        case 5: CRL(5); break;
+        default: CRL(6); break;
     }
+#undef CRL
     return (int)cudaGetLastError();
 }
 

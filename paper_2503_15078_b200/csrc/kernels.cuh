@@ -52,6 +52,15 @@ struct ContactState {
     double* wz;       // [ns][3]  sum_rows w theta z c per slot
     double* phi_abs;  // [nc] |phi_n| (stats)
     double* cr_res;   // [1]
+    double* rho;      // [3 nc] Schur RHS h - Theta J x~ (from the chain dot)
+};
+
+// active contact vertices of the current iteration (theta != 0 on an incident row)
+struct CrActive {
+    int* na;     // [1]
+    int* aidx;   // [ns] active position -> slot
+    int* apos;   // [ns] slot -> active position or -1
+    int* acon;   // [ns] active position -> its single single-vertex contact or -1
 };
 
 // --- frame kernels -----------------------------------------------------------
@@ -70,9 +79,6 @@ void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block*
                    const float4* u, float4* y, double* part, int* counters);
 void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const float* T2,
                    const float4* y, double4* x, const double4* xt, double4* v, double inv_h, int finalize_v);
-void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
-                      const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
-                      const float4* y, double* dxt);
 // compact per-contact arrays for the CR: rows' directions, single-vertex slot / vertex (-1 otherwise)
 struct CrContacts {
     const float* c9;   // [nc][3][3] rows n, t1, t2
@@ -80,9 +86,15 @@ struct CrContacts {
     const int* v0;     // [nc] its vertex, else -1
     const int* c1;     // [ns] the only contact on a slot if it is single-vertex weight-1, else -1
 };
-int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc, const int32_t* slot_vtx,
-              const int32_t* scp, const int32_t* sci, const float* scw, const double* G, double* GA,
-              const double4* x, ContactState cs);
+void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
+                      const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
+                      const float4* y, double* dxt, CrContacts cc, const double4* x, ContactState cs);
+
+void launch_active(cudaStream_t st, int ns, CrContacts cc, const int32_t* scp, const int32_t* sci, ContactState cs,
+                   CrActive act, const double* G, double* GA);
+int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc, const int32_t* scp,
+              const int32_t* sci, const float* scw, const double* GA, const double4* x, ContactState cs,
+              CrActive act);
 // y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s over the rows of ulist (int4 {row, s0, s1, -})
 void launch_scatter(cudaStream_t st, int max_rows, const int* ucount, const int4* ulist, const float* Zc,
                     const double* wz, float4* y);
