@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--instances", type=int, default=1,
+                    help="cfg5: scenes per GPU sharing K (1 = the single-scene cfg3 workload)")
     return ap.parse_args()
 
 
@@ -184,18 +186,26 @@ def run_ours(args):
     torch.cuda.set_stream(stream)
 
     sc = scenes.make_scene("cfg3")
-    rng = np.random.default_rng(1000 + rank)
-    v0 = 0.01 * rng.standard_normal(sc.mesh.X.shape) * (1 - sc.mesh.fixed[:, None])
-    s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+    S = max(1, args.instances)
+    s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, n_instances=S)
     s.set_stream(stream.cuda_stream)
     s.set_pin_velocity(sc.pin_velocity)
-    packed = s.pack_contacts(sc.contacts)
-    s.set_contacts(sc.contacts)
-    s.set_state(sc.mesh.X, v0)
+    # cfg5 instances rank * S + i: own initial velocity and obstacle offset (scenes.batch_instance_params)
+    base = simlib.contacts_to_array(sc.contacts)
+    arrs, v0s = [], np.empty((S, sc.mesh.n_v, 3))
+    for i in range(S):
+        v0s[i], delta = scenes.batch_instance_params(sc, rank * S + i)
+        a = base.copy()
+        if S > 1:   # the single-scene workload keeps cfg3's obstacles
+            a["offset"] += a["normal"][:, 2] * delta
+        arrs.append(a)
+    packed = (np.concatenate(arrs), np.full(S, len(base), np.int32))
+    s.set_contacts_batch(packed=packed)
+    s.set_states(np.broadcast_to(sc.mesh.X, (S,) + sc.mesh.X.shape), v0s)
     st0 = s.stats()
 
     def step():
-        s.set_contacts(packed=packed)
+        s.set_contacts_batch(packed=packed)
         s.step(1, ITERS)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > L2
@@ -236,7 +246,7 @@ def run_ours(args):
         dist.all_gather(allt, t)                 # NCCL: gather per-rank timings only
         total_ms = max(float(a.item()) for a in allt)
     ms_per_step = total_ms / args.steps
-    scenes_total = ws
+    scenes_total = ws * S
     value = scenes_total * args.steps * ITERS / (total_ms / 1000.0)
 
     # ---- e2e through the public API with host buffers: contacts in, state out
@@ -245,9 +255,10 @@ def run_ours(args):
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    xh = np.empty((S, sc.mesh.n_v, 3))
     for _ in range(e2e_steps):
         step()
-        xh, vh = s.get_state()
+        s.get_positions(out=xh)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
@@ -259,7 +270,7 @@ def run_ours(args):
     e2e_value = scenes_total * e2e_steps * ITERS / (e2e_ms / 1000.0)
     st = s.stats()
     h2d = int(st["h2d_contact_bytes"])
-    d2h = 2 * 32 * sc.mesh.n_v
+    d2h = 32 * sc.mesh.n_v * S
 
     if rank != 0:
         if ws > 1:
@@ -270,18 +281,31 @@ def run_ours(args):
     peak, peak_kind = measured_peak()
     nnz, nf = int(st0["nnz_K"]), int(st0["n_free"])
     launches = args.steps * ITERS
-    bytes_k1 = 4 * nnz + 16 * nf + 16 * nf            # K (column-major) + u + y
-    bytes_k2 = 4 * nnz + 16 * nf + 2 * 32 * nf        # K (row-major) + y + x read/write
     share = {k: v / max(1e-12, sum(ktimes.values())) for k, v in ktimes.items()}
     dom = max(["kpass1", "kpass2"], key=lambda k: ktimes[k])
-    dom_bytes = bytes_k1 if dom == "kpass1" else bytes_k2
     avg_s = ktimes[dom] / launches / 1000.0
-    achieved = dom_bytes / avg_s / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(dom), "kernel": dom, "peak_source": peak_kind,
-                "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": avg_s * 1e6,
-                "note": "K (fp32 values-only, 2 copies = %.1f MB) vs 126 MB L2: passes re-read from HBM; "
-                        "dominant HBM-bound kernel (k_cr is latency-bound, see kernel_us_per_step)" % (8 * nnz / 1e6)}
+    if S == 1:
+        bytes_k1 = 4 * nnz + 16 * nf + 16 * nf            # K (column-major) + u + y
+        bytes_k2 = 4 * nnz + 16 * nf + 2 * 32 * nf        # K (row-major) + y + x read/write
+        dom_bytes = bytes_k1 if dom == "kpass1" else bytes_k2
+        achieved = dom_bytes / avg_s / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": ncu_traffic(dom), "kernel": dom, "peak_source": peak_kind,
+                    "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": avg_s * 1e6,
+                    "note": "K (fp32 values-only, 2 copies = %.1f MB) vs 126 MB L2: passes re-read from HBM; "
+                            "dominant HBM-bound kernel (k_cr is latency-bound, see kernel_us_per_step)"
+                            % (8 * nnz / 1e6)}
+    else:
+        # batched passes: each K value meets 3 S right-hand sides -> FP32 FMA-issue bound
+        flops = 2.0 * 3 * nnz * S
+        sm_mhz = 1965.0
+        fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # TFLOP/s: 148 SMs x 128 FP32 lanes x FMA
+        achieved = flops / avg_s / 1e12
+        roofline = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp32_peak, "traffic": ncu_traffic(dom + "_batched"), "kernel": dom,
+                    "peak_source": "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1965 MHz (B200_PROFILING.md)",
+                    "algorithmic_flops_per_launch": flops, "avg_launch_us": avg_s * 1e6,
+                    "note": "K read once per 128-instance chunk; 6 flop per nnz per instance"}
     kernels_us = {k: 1000.0 * v / args.steps for k, v in ktimes.items()}
 
     cpu = None
@@ -296,11 +320,13 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "cfg3 gingerbread-class slab 19691 v / 93600 t, 800 contacts x 3 rows, "
+        "config": {"workload": ("cfg5: %d x " % (ws * S) if S > 1 else "") +
+                               "cfg3 gingerbread-class slab 19691 v / 93600 t, 800 contacts x 3 rows, "
                                "NH E=1e6 nu=0.3, h=0.01, 5 L-G + 10 CR per frame, set_contacts every frame",
-                   "global_batch": ws, "scenes_per_gpu": 1, "parallelism": f"replicas{ws}",
+                   "global_batch": ws * S, "scenes_per_gpu": S,
+                   "parallelism": f"instances{S}xdp{ws}" if S > 1 else f"replicas{ws}",
                    "l2": "flushed (256 MB write) between timed steps"},
-        "ms_per_lg_iteration": ms_per_step / ITERS,
+        "ms_per_lg_iteration": ms_per_step / ITERS,   # all S instances of one GPU advance together
         "paper_context_ms_per_iteration": 11.95,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms / e2e_steps, "wall_s": wall_e2e},

@@ -26,6 +26,11 @@
  *    library's internal (elimination-tree postorder) numbering is hidden.
  *  - Results are deterministic for a given device and configuration (fixed
  *    reduction orders, no floating-point atomics).
+ *  - Instances: one handle may hold n_instances independent scenes that share
+ *    the mesh topology, rest shape, material, h and therefore K (BASELINE
+ *    config 5).  Each instance has its own state and contact set;
+ *    every sim_step advances all of them.  The K-passes then read each K tile
+ *    once for all instances (3 x n_instances right-hand sides).
  */
 #ifndef SIM_H_
 #define SIM_H_
@@ -51,13 +56,15 @@ typedef struct sim_handle sim_handle;
 
 /* Tetrahedral mesh.  rest_positions [n_vertices][3] in metres;
  * tets [n_tets][4] (orientation not required); fixed [n_vertices] Dirichlet
- * mask (nonzero = pinned) or NULL. */
+ * mask (nonzero = pinned) or NULL.  n_instances: scenes sharing this mesh
+ * (0 or 1 = one scene; at most 65535). */
 typedef struct {
     int32_t n_vertices;
     int32_t n_tets;
     const double  *rest_positions;
     const int32_t *tets;
     const uint8_t *fixed;
+    int32_t n_instances;
 } sim_mesh;
 
 /* Material models of the local step (eq. PD local). */
@@ -103,14 +110,15 @@ typedef struct {
     int64_t nnz_L;
     int32_t etree_height;
     int32_t n_panels;          /* fundamental supernodes (rows sharing their first column)               */
-    int32_t n_contacts, n_contact_vertices;
+    int32_t n_contacts, n_contact_vertices;   /* summed over instances */
     int64_t frames_done;
-    double  last_cr_residual;  /* |r| of the last CR solve (fp64), -1 if none                            */
+    double  last_cr_residual;  /* max over instances of |r| of the last CR solve (fp64), -1 if none      */
     double  max_abs_phi_n;     /* max |phi_FB| over unilateral contacts at the last evaluated iterate   */
     int32_t n_active, n_stick, n_slip;   /* frame-end classification (lambda_n > 0; stick / slip)        */
     int32_t kernels_per_frame; /* kernel launches in one captured frame                                  */
     double  build_seconds;     /* host time of sim_build_sparse_inverse                                  */
-    int64_t h2d_contact_bytes; /* host->device bytes of the last sim_set_contacts                        */
+    int64_t h2d_contact_bytes; /* host->device bytes of the last contact commit                          */
+    int32_t n_instances;
 } sim_stats;
 
 /* Validate the mesh and material, compute rest data (Dm^-1, volumes, lumped
@@ -126,13 +134,19 @@ int sim_create(const sim_mesh *mesh, const sim_material *mat, double h, sim_hand
  * |K_ij| < tol |K_jj| are zeroed (0 = exact Theorem-1 pattern). */
 int sim_build_sparse_inverse(sim_handle *h, double drop_tolerance);
 
-/* Replace the contact set (n may be 0).  Builds rows, uploads them and
- * computes on the device G = K[:,Vc]^T K[:,Vc], the Delassus diagonal and the
- * preconditioner r_n = h^2 D_jj, r_f = h D_jj.  Limits: n <= 1024 contacts on
- * <= 1024 distinct vertices, and the CR cluster's fp64 working set
+/* Replace the contact set of one instance (n may be 0).  Validates and builds
+ * the rows on the host; the next sim_step (or debug accessor) uploads the
+ * contact sets of all instances in one batch and computes on the device
+ * G = K[:,Vc]^T K[:,Vc] per instance, the Delassus diagonal and the
+ * preconditioner r_n = h^2 D_jj, r_f = h D_jj.  Limits per instance: n <= 1024
+ * contacts on <= 1024 distinct vertices, and the CR's fp64 working set
  * 184 n + 72 n_vertices bytes must fit 227 KB (about 900 single-vertex
  * contacts); SIM_E_LIMIT otherwise. */
-int sim_set_contacts(sim_handle *h, const sim_contact *contacts, int32_t n);
+int sim_set_contacts(sim_handle *h, int32_t instance, const sim_contact *contacts, int32_t n);
+/* The same for instances first .. first+count-1 at once: counts[count],
+ * contacts concatenated in instance order.  All-or-nothing on error. */
+int sim_set_contacts_batch(sim_handle *h, int32_t first, int32_t count, const int32_t *counts,
+                           const sim_contact *contacts);
 
 /* Advance `frames` frames of `iterations` local-global iterations each
  * (Alg. 4).  Pinned vertices move by h * pin_velocity per frame.  Enqueued on
@@ -147,13 +161,19 @@ int sim_synchronize(sim_handle *h);
 /* Constant velocity (m/s) of all pinned vertices (moving Dirichlet handle). */
 int sim_set_pin_velocity(sim_handle *h, const double v[3]);
 
-/* x, v: [n_vertices][3] in original vertex order (caller buffers). */
-int sim_get_state(sim_handle *h, double *x, double *v);
-int sim_set_state(sim_handle *h, const double *x, const double *v);
+/* x, v: [n_vertices][3] of one instance in original vertex order (caller
+ * buffers; either may be NULL). */
+int sim_get_state(sim_handle *h, int32_t instance, double *x, double *v);
+int sim_set_state(sim_handle *h, int32_t instance, const double *x, const double *v);
+/* Positions of all instances: x [n_instances][n_vertices][3]. */
+int sim_get_positions(sim_handle *h, double *x);
+/* States of all instances: x, v [n_instances][n_vertices][3] (either may be NULL). */
+int sim_set_states(sim_handle *h, const double *x, const double *v);
 
 /* lambda: [rows] = (lambda_n, lambda_f1, lambda_f2) per unilateral contact,
- * (lambda_b) per bilateral contact, in the order given to sim_set_contacts. */
-int sim_get_lambda(sim_handle *h, double *lambda, int32_t capacity);
+ * (lambda_b) per bilateral contact of one instance, in the order given to
+ * sim_set_contacts, from the most recent step. */
+int sim_get_lambda(sim_handle *h, int32_t instance, double *lambda, int32_t capacity);
 
 int sim_get_stats(sim_handle *h, sim_stats *out);
 
@@ -183,26 +203,27 @@ int sim_debug_get_inverse(sim_handle *h, int32_t *perm, int32_t *parent, int64_t
 /* Create a handle that only runs the host precompute (no device). */
 int sim_create_host(const sim_mesh *mesh, const sim_material *mat, double h, sim_handle **out);
 /* x_out = A^-1 b on the device via the two K-passes (y = K P b, x = P^T K^T y),
- * b and x_out [n_vertices][3]; rows of pinned vertices are ignored / zero.
- * b is rounded to fp32 (the K-pass input precision) before the product. */
+ * b and x_out [n_instances][n_vertices][3] (the batched passes when
+ * n_instances > 1); rows of pinned vertices are ignored / zero.  b is rounded
+ * to fp32 (the K-pass input precision) before the product. */
 int sim_debug_apply_inverse(sim_handle *h, const double *b, double *x_out);
-/* One local step at positions x [n_vertices][3] with prediction s
+/* (single-instance handles) One local step at positions x [n_vertices][3] with prediction s
  * [n_vertices][3]: returns the per-tet projection P [n_tets][9] (row-major
  * 3x3; NULL to skip) and the global-step residual r = b - A x
  * = M(s - x) + h^2 sum_i w_i G_i^T (P_i - F_i)  [n_vertices][3] (0 on pinned
  * rows; NULL to skip).  Does not modify the simulation state. */
 int sim_debug_local(sim_handle *h, const double *x, const double *s, float *P, double *resid);
-/* G = K[:,Vc]^T K[:,Vc] for the current contact set: returns the contact
- * vertex list (original ids) and G (row-major, n_cv x n_cv). */
-int sim_debug_get_delassus(sim_handle *h, int32_t *cv, float *G, int32_t capacity);
+/* G = K[:,Vc]^T K[:,Vc] for an instance's current contact set: returns the
+ * contact vertex list (original ids) and G (row-major, n_cv x n_cv). */
+int sim_debug_get_delassus(sim_handle *h, int32_t instance, int32_t *cv, float *G, int32_t capacity);
 
 /* Contact scratch of the most recent L-G iteration (after sim_step):
  * theta, C diagonal and h-vector per row ([3 * n_contacts], rows n, t1, t2;
  * bilateral contacts pad rows 1-2 with theta 0, C 1), dxt = (A^-1 r) at each
  * contact vertex ([n_cv][3]), the contact vertices (original ids, [n_cv]) and
  * D_jj per contact ([n_contacts]).  Any pointer may be NULL. */
-int sim_debug_contact_state(sim_handle *h, double *theta, double *cdiag, double *hvec, double *dxt,
-                            int32_t *slot_vertex, double *djj);
+int sim_debug_contact_state(sim_handle *h, int32_t instance, double *theta, double *cdiag, double *hvec,
+                            double *dxt, int32_t *slot_vertex, double *djj);
 /* Phase timestamps (us since the CR kernel started) of the most recent CR
  * solve: [1] rho built, [2] active set + G_A gathered, [3 + it] after CR
  * iteration it, [20] loop end, [21] epilogue end.  out must hold 32 doubles. */

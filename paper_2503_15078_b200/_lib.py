@@ -16,7 +16,8 @@ EXPORTED_SYMBOLS = [
     "sim_synchronize", "sim_set_pin_velocity", "sim_get_state", "sim_set_state", "sim_get_lambda",
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
-    "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline",
+    "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
+    "sim_get_positions", "sim_set_states",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -24,7 +25,7 @@ KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_d
 class SimMesh(C.Structure):
     _fields_ = [("n_vertices", C.c_int32), ("n_tets", C.c_int32),
                 ("rest_positions", C.POINTER(C.c_double)), ("tets", C.POINTER(C.c_int32)),
-                ("fixed", C.POINTER(C.c_uint8))]
+                ("fixed", C.POINTER(C.c_uint8)), ("n_instances", C.c_int32)]
 
 
 class SimMaterial(C.Structure):
@@ -40,6 +41,36 @@ class SimContact(C.Structure):
                 ("obstacle_velocity", C.c_double * 3), ("mu", C.c_double), ("compliance", C.c_double)]
 
 
+# numpy twin of SimContact (same layout) for vectorised packing of large batches
+CONTACT_DTYPE = np.dtype([("kind", "<i4"), ("n_verts", "<i4"), ("verts", "<i4", 4), ("weights", "<f8", 4),
+                          ("normal", "<f8", 3), ("tangent1", "<f8", 3), ("tangent2", "<f8", 3),
+                          ("offset", "<f8"), ("obstacle_velocity", "<f8", 3), ("mu", "<f8"),
+                          ("compliance", "<f8")])
+assert CONTACT_DTYPE.itemsize == C.sizeof(SimContact)
+
+
+def contacts_to_array(contacts):
+    """Contact objects -> CONTACT_DTYPE array (argument marshalling only)."""
+    a = np.zeros(len(contacts), CONTACT_DTYPE)
+    for i, ct in enumerate(contacts):
+        n = len(ct.verts)
+        a[i]["kind"] = int(getattr(ct, "kind", 0))
+        a[i]["n_verts"] = n
+        a[i]["verts"][:n] = [int(v) for v in ct.verts]
+        a[i]["weights"][:n] = [float(w) for w in ct.weights]
+        a[i]["normal"] = ct.normal
+        t1, t2 = getattr(ct, "tangent1", None), getattr(ct, "tangent2", None)
+        if t1 is not None:
+            a[i]["tangent1"] = t1
+        if t2 is not None:
+            a[i]["tangent2"] = t2
+        a[i]["offset"] = float(ct.offset)
+        a[i]["obstacle_velocity"] = np.asarray(getattr(ct, "obstacle_velocity", np.zeros(3)))
+        a[i]["mu"] = float(getattr(ct, "mu", 0.0))
+        a[i]["compliance"] = float(getattr(ct, "compliance", 0.0))
+    return a
+
+
 class SimStats(C.Structure):
     _fields_ = [("n_vertices", C.c_int64), ("n_free", C.c_int64), ("n_tets", C.c_int64),
                 ("nnz_K", C.c_int64), ("nnz_L", C.c_int64), ("etree_height", C.c_int32),
@@ -47,7 +78,7 @@ class SimStats(C.Structure):
                 ("frames_done", C.c_int64), ("last_cr_residual", C.c_double), ("max_abs_phi_n", C.c_double),
                 ("n_active", C.c_int32), ("n_stick", C.c_int32), ("n_slip", C.c_int32),
                 ("kernels_per_frame", C.c_int32), ("build_seconds", C.c_double),
-                ("h2d_contact_bytes", C.c_int64)]
+                ("h2d_contact_bytes", C.c_int64), ("n_instances", C.c_int32)]
 
 
 class SimError(RuntimeError):
@@ -64,22 +95,25 @@ def _load():
         "sim_create": [C.POINTER(SimMesh), C.POINTER(SimMaterial), C.c_double, C.POINTER(H)],
         "sim_create_host": [C.POINTER(SimMesh), C.POINTER(SimMaterial), C.c_double, C.POINTER(H)],
         "sim_build_sparse_inverse": [H, C.c_double],
-        "sim_set_contacts": [H, C.POINTER(SimContact), C.c_int32],
+        "sim_set_contacts": [H, C.c_int32, C.POINTER(SimContact), C.c_int32],
+        "sim_set_contacts_batch": [H, C.c_int32, C.c_int32, ip, C.POINTER(SimContact)],
+        "sim_get_positions": [H, dp],
+        "sim_set_states": [H, dp, dp],
         "sim_step": [H, C.c_int32, C.c_int32],
         "sim_synchronize": [H],
         "sim_set_pin_velocity": [H, dp],
-        "sim_get_state": [H, dp, dp],
-        "sim_set_state": [H, dp, dp],
-        "sim_get_lambda": [H, dp, C.c_int32],
+        "sim_get_state": [H, C.c_int32, dp, dp],
+        "sim_set_state": [H, C.c_int32, dp, dp],
+        "sim_get_lambda": [H, C.c_int32, dp, C.c_int32],
         "sim_get_stats": [H, C.POINTER(SimStats)],
         "sim_set_stream": [H, C.c_void_p],
         "sim_debug_get_inverse": [H, ip, ip, C.POINTER(C.c_int64), fp],
         "sim_debug_apply_inverse": [H, dp, dp],
         "sim_debug_local": [H, dp, dp, fp, dp],
-        "sim_debug_get_delassus": [H, ip, fp, C.c_int32],
+        "sim_debug_get_delassus": [H, C.c_int32, ip, fp, C.c_int32],
         "sim_set_profiling": [H, C.c_int],
         "sim_get_kernel_times": [H, dp, C.c_int32],
-        "sim_debug_contact_state": [H, dp, dp, dp, dp, ip, dp],
+        "sim_debug_contact_state": [H, C.c_int32, dp, dp, dp, dp, ip, dp],
         "sim_debug_cr_timeline": [H, dp],
     }
     for name, args in sig.items():
@@ -106,16 +140,17 @@ def _dptr(a):
 
 
 class Sim:
-    """One simulated object (mesh + material + h) bound to the current device."""
+    """n_instances scenes sharing one mesh + material + h (and K), bound to the current device."""
 
-    def __init__(self, X, T, fixed, material, h, drop_tolerance=0.0, host_only=False):
+    def __init__(self, X, T, fixed, material, h, drop_tolerance=0.0, host_only=False, n_instances=1):
         X = np.ascontiguousarray(X, dtype=np.float64)
         T = np.ascontiguousarray(T, dtype=np.int32)
         fixed = np.ascontiguousarray(fixed if fixed is not None else np.zeros(X.shape[0]), dtype=np.uint8)
         self.n_v, self.n_t = X.shape[0], T.shape[0]
+        self.n_instances = int(n_instances)
         self._keep = (X, T, fixed)
         m = SimMesh(self.n_v, self.n_t, _dptr(X), T.ctypes.data_as(C.POINTER(C.c_int32)),
-                    fixed.ctypes.data_as(C.POINTER(C.c_uint8)))
+                    fixed.ctypes.data_as(C.POINTER(C.c_uint8)), self.n_instances)
         g = (C.c_double * 3)(*[float(v) for v in material.gravity])
         mat = SimMaterial(int(material.model), float(material.density), float(material.youngs),
                           float(material.poisson), float(material.proj_stiffness), g,
@@ -129,8 +164,12 @@ class Sim:
         except Exception:
             self.close()
             raise
-        self.nc = 0
-        self._contacts = []
+        self._nc = [0] * self.n_instances
+        self._contacts = [None] * self.n_instances
+
+    @property
+    def nc(self):
+        return self._nc[0]
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -170,12 +209,36 @@ class Sim:
             arr[i] = self._contact_struct(ct)
         return arr, len(contacts)
 
-    def set_contacts(self, contacts=None, packed=None):
+    def set_contacts(self, contacts=None, packed=None, instance=0):
         arr, n = packed if packed is not None else self.pack_contacts(contacts)
-        _check(lib.sim_set_contacts(self._h, arr, n))
-        self.nc = n
-        if contacts is not None:
-            self._contacts = list(contacts)
+        _check(lib.sim_set_contacts(self._h, int(instance), arr, n))
+        self._nc[instance] = n
+        self._contacts[instance] = list(contacts) if contacts is not None else None
+
+    def pack_contacts_batch(self, per_instance):
+        """per_instance: list (one entry per instance) of contact lists -> packed batch."""
+        counts = np.array([len(c) for c in per_instance], np.int32)
+        arr = (SimContact * max(1, int(counts.sum())))()
+        i = 0
+        for cl in per_instance:
+            for ct in cl:
+                arr[i] = self._contact_struct(ct)
+                i += 1
+        return arr, counts
+
+    def set_contacts_batch(self, per_instance=None, packed=None, first=0):
+        """per_instance: list of contact lists, or packed = (contacts, counts) where contacts
+        is a ctypes SimContact array or a CONTACT_DTYPE numpy array (concatenated)."""
+        arr, counts = packed if packed is not None else self.pack_contacts_batch(per_instance)
+        counts = np.ascontiguousarray(counts, dtype=np.int32)
+        if isinstance(arr, np.ndarray):
+            assert arr.dtype == CONTACT_DTYPE and arr.flags.c_contiguous
+            arr = arr.ctypes.data_as(C.POINTER(SimContact))
+        _check(lib.sim_set_contacts_batch(self._h, int(first), len(counts),
+                                          counts.ctypes.data_as(C.POINTER(C.c_int32)), arr))
+        for k, n in enumerate(counts.tolist()):
+            self._nc[first + k] = n
+            self._contacts[first + k] = list(per_instance[k]) if per_instance is not None else None
 
     def step(self, frames=1, iterations=5):
         _check(lib.sim_step(self._h, int(frames), int(iterations)))
@@ -187,22 +250,37 @@ class Sim:
         a = np.ascontiguousarray(v, dtype=np.float64)
         _check(lib.sim_set_pin_velocity(self._h, _dptr(a)))
 
-    def get_state(self):
+    def get_state(self, instance=0):
         x = np.empty((self.n_v, 3))
         v = np.empty((self.n_v, 3))
-        _check(lib.sim_get_state(self._h, _dptr(x), _dptr(v)))
+        _check(lib.sim_get_state(self._h, int(instance), _dptr(x), _dptr(v)))
         return x, v
 
-    def set_state(self, x, v):
+    def set_state(self, x, v, instance=0):
         x = np.ascontiguousarray(x, dtype=np.float64)
         v = np.ascontiguousarray(v, dtype=np.float64)
-        _check(lib.sim_set_state(self._h, _dptr(x), _dptr(v)))
+        _check(lib.sim_set_state(self._h, int(instance), _dptr(x), _dptr(v)))
 
-    def get_lambda(self):
-        cap = 3 * max(1, self.nc)
+    def set_states(self, x=None, v=None):
+        """States of all instances, [n_instances][n_vertices][3] each (None = keep)."""
+        xa = None if x is None else np.ascontiguousarray(x, dtype=np.float64)
+        va = None if v is None else np.ascontiguousarray(v, dtype=np.float64)
+        _check(lib.sim_set_states(self._h, None if xa is None else _dptr(xa), None if va is None else _dptr(va)))
+
+    def get_positions(self, out=None):
+        """Positions of all instances, [n_instances][n_vertices][3]."""
+        if out is None:
+            out = np.empty((self.n_instances, self.n_v, 3))
+        _check(lib.sim_get_positions(self._h, _dptr(out)))
+        return out
+
+    def get_lambda(self, instance=0):
+        nc = self._nc[instance]
+        cap = 3 * max(1, nc)
         out = np.empty(cap)
-        _check(lib.sim_get_lambda(self._h, _dptr(out), cap))
-        rows = sum(1 if getattr(c, "kind", 0) == 1 else 3 for c in self._contacts) if self._contacts else 3 * self.nc
+        _check(lib.sim_get_lambda(self._h, int(instance), _dptr(out), cap))
+        cl = self._contacts[instance]
+        rows = sum(1 if getattr(c, "kind", 0) == 1 else 3 for c in cl) if cl else 3 * nc
         return out[:rows]
 
     def stats(self):
@@ -236,8 +314,9 @@ class Sim:
         return perm, parent, rowptr, vals
 
     def debug_apply_inverse(self, b):
+        """b: [n_v][3] (single instance) or [n_instances][n_v][3]."""
         b = np.ascontiguousarray(b, dtype=np.float64)
-        x = np.empty((self.n_v, 3))
+        x = np.empty(b.shape)
         _check(lib.sim_debug_apply_inverse(self._h, _dptr(b), _dptr(x)))
         return x
 
@@ -249,24 +328,29 @@ class Sim:
         _check(lib.sim_debug_local(self._h, _dptr(x), _dptr(s), P.ctypes.data_as(C.POINTER(C.c_float)), _dptr(r)))
         return P, r
 
-    def debug_delassus(self):
-        ns = int(self.stats()["n_contact_vertices"])
+    def _ns(self, instance):
+        cl = self._contacts[instance]
+        if cl is None:
+            raise ValueError("contact list of this instance unknown (set from a packed array)")
+        return len({int(v) for c in cl for v in c.verts})
+
+    def debug_delassus(self, instance=0):
+        ns = self._ns(instance)
         cv = np.empty(max(1, ns), np.int32)
         G = np.empty((max(1, ns), max(1, ns)), np.float32)
-        _check(lib.sim_debug_get_delassus(self._h, cv.ctypes.data_as(C.POINTER(C.c_int32)),
+        _check(lib.sim_debug_get_delassus(self._h, int(instance), cv.ctypes.data_as(C.POINTER(C.c_int32)),
                                           G.ctypes.data_as(C.POINTER(C.c_float)), max(1, ns)))
         return cv[:ns], G[:ns, :ns]
 
 
-def debug_contact_state(sim):
+def debug_contact_state(sim, instance=0):
     """Contact scratch of the last L-G iteration (see sim_debug_contact_state)."""
-    st = sim.stats()
-    nc, ns = int(st["n_contacts"]), int(st["n_contact_vertices"])
+    nc, ns = sim._nc[instance], sim._ns(instance)
     th, cd, hv = np.empty(3 * nc), np.empty(3 * nc), np.empty(3 * nc)
     dxt = np.empty((max(1, ns), 3))
     sv = np.empty(max(1, ns), np.int32)
     djj = np.empty(max(1, nc))
-    _check(lib.sim_debug_contact_state(sim._h, _dptr(th), _dptr(cd), _dptr(hv), _dptr(dxt),
+    _check(lib.sim_debug_contact_state(sim._h, int(instance), _dptr(th), _dptr(cd), _dptr(hv), _dptr(dxt),
                                        sv.ctypes.data_as(C.POINTER(C.c_int32)), _dptr(djj)))
     return {"theta": th, "cdiag": cd, "hvec": hv, "dxt": dxt[:ns], "slot_vertex": sv[:ns], "djj": djj[:nc]}
 

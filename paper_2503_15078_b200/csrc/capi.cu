@@ -54,16 +54,38 @@ struct DBuf {
         if (cnt == 0) return cudaSuccess;
         return cudaMemcpyAsync(p, h, cnt * sizeof(T), cudaMemcpyHostToDevice, st);
     }
+    // grow to at least cnt elements (contents not preserved); sets grew when reallocated
+    cudaError_t ensure(size_t cnt, bool& grew) {
+        if (cnt <= n && p) return cudaSuccess;
+        grew = true;
+        return alloc(std::max<size_t>(cnt + cnt / 4, 16));
+    }
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
     }
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+};
+
+// one instance's contact set, host side, in instance-local numbering (validated)
+struct InstContacts {
+    std::vector<DContact> hc;        // slot[] local, vtx internal
+    std::vector<int32_t> verts;      // slot -> internal vertex (ascending)
+    std::vector<int32_t> scp, sci;   // slot -> local contacts
+    std::vector<float> scw;
+    std::vector<float> c9;
+    std::vector<int32_t> s0, v0, c1; // local slot / vertex / local contact
+    int64_t chain_total = 0;         // sum over slots of (depth + 1)
 };
 
 struct sim_handle {
     bool host_only = false;
     int device = -1;
+    int S = 1;                             // instances sharing mesh, material and K
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;            // fork branch inside the frame graph
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
@@ -81,10 +103,13 @@ struct sim_handle {
     simhost::Inverse K;
     simhost::WorkLists wl;
     std::vector<float> T1h, T2h;
+    std::vector<simhost::BUnit> bu1, bu2;   // batched K-pass units (S > 1)
+    std::vector<float> T1ph;
+    int bparts = 0, bblocks1 = 0;
     int64_t nnzL = 0;
     double build_seconds = 0;
     double vpin[3] = {0, 0, 0};
-    // device: state
+    // device: state, [entity][S]
     DBuf<double4> x, xt, v, s;
     DBuf<double> M;
     DBuf<int4> tet;
@@ -92,28 +117,32 @@ struct sim_handle {
     DBuf<float4> fc, u, y;
     DBuf<int32_t> adjp, adj;
     // device: K
-    DBuf<float> Krow, Kcol, T1, T2;   // K row/column-major + the two passes' tile streams
+    DBuf<float> Krow, Kcol, T1, T2, T1p;   // K row/column-major + the passes' tile streams
     DBuf<int64_t> colptr;
-    DBuf<int32_t> cb, depth, parent, ptop, cover;
+    DBuf<int32_t> depth, parent, ptop, cover;
     DBuf<int2> meta;                 // {rowptr[i] - first[i], first[i]}
     DBuf<P1Item> p1;
     DBuf<P1Block> p1b;
     DBuf<P2Block> p2b;
+    DBuf<simhost::BUnit> bu1d, bu2d;
     DBuf<double> part1;
     DBuf<int> counters;
-    // contacts
-    int nc = 0, ns = 0, row_lo = 0;
-    std::vector<DContact> hc;
-    std::vector<int32_t> slot_vtx_h;
+    // contacts: host per instance, device packed over instances
+    std::vector<InstContacts> ic;
+    bool dirty = false;
+    int C = 0, NS = 0, nc_max = 0, ns_max = 0, urows_max = 0;
+    std::vector<int> coff_h, soff_h;
     DBuf<DContact> dc;
     DBuf<float> cc9;
     DBuf<int32_t> cs0, cv0, cc1;
-    DBuf<int32_t> slot_vtx, scp, sci, vcp, vci;
-    DBuf<float> scw, vcw;
-    DBuf<double> G, GA;   // Delassus Gram and the CR's active-block scratch
+    DBuf<int32_t> slot_vtx, slot_inst, scp, sci;
+    DBuf<float> scw;
+    DBuf<int> coff, soff, uoff;
+    DBuf<int64_t> goff, zoff;
+    DBuf<float> G, GA;   // Delassus Gram blocks and the CR's active blocks (fp32-exact values)
     DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res, rho;
     DBuf<int> act_na, act_idx, act_pos, act_con;   // CR active set (k_active)
-    DBuf<int32_t> chain_off, chain_rows;
+    DBuf<int32_t> chain_off, chain_rows, slotmap;
     DBuf<uint8_t> flag;
     DBuf<int> ucount;
     DBuf<int4> ulist;
@@ -121,15 +150,15 @@ struct sim_handle {
     int contact_gen = 0;
     // graph
     cudaGraphExec_t gexec = nullptr;
-    int g_iters = -1, g_nc = -1, g_ns = -1, g_prof = -1, g_gen = -1;
+    int g_iters = -1, g_C = -1, g_NS = -1, g_ncm = -1, g_nsm = -1, g_um = -1, g_prof = -1, g_gen = -1;
     // in-graph kernel timing (event record nodes between kernels)
     int profiling = 0;
     std::vector<cudaEvent_t> pev;
     std::vector<int> pkind;   // kind of the kernel that follows event i
     int kernels_per_frame = 0;
     int64_t frames_done = 0;
-    int64_t h2d_contact_bytes = 0;   // bytes uploaded by the last sim_set_contacts
-    // pinned staging for asynchronous sim_set_contacts uploads (reused once the last copy is done)
+    int64_t h2d_contact_bytes = 0;   // bytes uploaded by the last contact commit
+    // pinned staging for asynchronous contact uploads (reused once the last copy is done)
     unsigned char* stage = nullptr;
     size_t stage_cap = 0, stage_used = 0;
     cudaEvent_t stage_free = nullptr;
@@ -145,6 +174,7 @@ static cudaError_t stage_upload(sim_handle* H, T* dst, const T* src, size_t n) {
     if (at + bytes > H->stage_cap) return cudaErrorMemoryAllocation;   // caller sized the area
     memcpy(H->stage + at, src, bytes);
     H->stage_used = at + bytes;
+    H->h2d_contact_bytes += (int64_t)bytes;
     return cudaMemcpyAsync(dst, H->stage + at, bytes, cudaMemcpyHostToDevice, H->stream);
 }
 
@@ -153,6 +183,7 @@ static int validate_create(const sim_mesh* m, const sim_material* mat, double h)
     if (!m || !mat) return fail(SIM_E_INVALID, "null mesh or material");
     if (m->n_vertices <= 0 || m->n_tets <= 0 || !m->rest_positions || !m->tets)
         return fail(SIM_E_INVALID, "empty mesh or null arrays");
+    if (m->n_instances < 0 || m->n_instances > 65535) return fail(SIM_E_INVALID, "n_instances must be in [0, 65535]");
     if (!(h > 0) || !std::isfinite(h)) return fail(SIM_E_INVALID, "h must be > 0");
     if (mat->model < 0 || mat->model > 2) return fail(SIM_E_INVALID, "unknown material model %d", mat->model);
     if (!(mat->density > 0) || !(mat->youngs > 0) || !std::isfinite(mat->youngs))
@@ -165,6 +196,8 @@ static int validate_create(const sim_mesh* m, const sim_material* mat, double h)
         if (!std::isfinite(m->rest_positions[i])) return fail(SIM_E_INVALID, "rest position %lld not finite", (long long)i);
     for (int64_t i = 0; i < 4LL * m->n_tets; ++i)
         if (m->tets[i] < 0 || m->tets[i] >= m->n_vertices) return fail(SIM_E_INVALID, "tet index out of range");
+    if ((int64_t)m->n_tets * 4 * std::max(1, m->n_instances) >= (int64_t)INT32_MAX)
+        return fail(SIM_E_LIMIT, "n_tets x 4 x n_instances exceeds the int32 index range");
     return SIM_OK;
 }
 
@@ -176,6 +209,7 @@ static int create_common(const sim_mesh* m, const sim_material* mat, double h, s
     sim_handle* H = new (std::nothrow) sim_handle();
     if (!H) return fail(SIM_E_OOM, "host allocation");
     H->host_only = host_only;
+    H->S = std::max(1, m->n_instances);
     H->n_v = m->n_vertices;
     H->n_t = m->n_tets;
     H->X.assign(m->rest_positions, m->rest_positions + 3 * (size_t)H->n_v);
@@ -189,6 +223,7 @@ static int create_common(const sim_mesh* m, const sim_material* mat, double h, s
     H->mu_l = mat->youngs / (2.0 * (1.0 + mat->poisson));
     H->lam_l = mat->youngs * mat->poisson / ((1.0 + mat->poisson) * (1.0 - 2.0 * mat->poisson));
     H->kproj = mat->proj_stiffness > 0 ? mat->proj_stiffness : 2.0 * H->mu_l;
+    H->ic.resize(H->S);
     int bad = -1;
     std::string msg = simhost::rest_data(H->n_v, H->n_t, H->X.data(), H->T.data(), mat->density, H->kproj, H->rd, bad);
     if (!msg.empty()) {
@@ -236,18 +271,6 @@ extern "C" void sim_destroy(sim_handle* H) {
     if (!H->host_only) {
         if (H->stream) cudaStreamSynchronize(H->stream);
         if (H->gexec) cudaGraphExecDestroy(H->gexec);
-        H->x.release(); H->xt.release(); H->v.release(); H->s.release(); H->M.release();
-        H->tet.release(); H->Bm.release(); H->hw2.release(); H->fc.release(); H->u.release(); H->y.release();
-        H->adjp.release(); H->adj.release(); H->Krow.release(); H->Kcol.release(); H->T1.release(); H->T2.release(); H->meta.release();
-        H->colptr.release(); H->cb.release(); H->cover.release(); H->depth.release(); H->parent.release();
-        H->ptop.release(); H->p1.release(); H->p1b.release(); H->p2b.release();
-        H->part1.release(); H->counters.release();
-        H->chain_off.release(); H->chain_rows.release(); H->flag.release(); H->ucount.release(); H->ulist.release(); H->Zc.release();
-        H->dc.release(); H->cc9.release(); H->cs0.release(); H->cv0.release(); H->cc1.release(); H->slot_vtx.release(); H->scp.release(); H->sci.release(); H->vcp.release();
-        H->vci.release(); H->scw.release(); H->vcw.release(); H->G.release(); H->GA.release(); H->lam.release();
-        H->theta.release(); H->cdiag.release(); H->hvec.release(); H->hl.release(); H->dxt.release();
-        H->wz.release(); H->phi_abs.release(); H->cr_res.release(); H->rho.release();
-        H->act_na.release(); H->act_idx.release(); H->act_pos.release(); H->act_con.release();
         for (auto e : H->pev) cudaEventDestroy(e);
         if (H->stage_free) cudaEventDestroy(H->stage_free);
         if (H->fork_ev) cudaEventDestroy(H->fork_ev);
@@ -256,7 +279,7 @@ extern "C" void sim_destroy(sim_handle* H) {
         if (H->stage) cudaFreeHost(H->stage);
         if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
     }
-    delete H;
+    delete H;   // device buffers are released by their destructors
 }
 
 extern "C" int sim_set_stream(sim_handle* H, void* st) {
@@ -278,18 +301,26 @@ extern "C" int sim_set_stream(sim_handle* H, void* st) {
 // ---------------------------------------------------------------------------
 static int upload_all(sim_handle* H) {
     cudaStream_t st = H->stream;
-    const int nv = H->n_v, nt = H->n_t, nf = H->n_f;
-    // state: rest, v = 0
-    std::vector<double4> xs(nv), zero(nv, make_double4(0, 0, 0, 0));
+    const int nv = H->n_v, nt = H->n_t, nf = H->n_f, S = H->S;
+    // state: rest, v = 0, replicated over the instances ([vertex][instance])
+    std::vector<double4> xs(nv);
     for (int i = 0; i < nv; ++i) {
         int o = H->int2orig[i];
         xs[i] = make_double4(H->X[3 * o], H->X[3 * o + 1], H->X[3 * o + 2], 0.0);
     }
-    CK(H->x.alloc(nv)); CK(H->xt.alloc(nv)); CK(H->v.alloc(nv)); CK(H->s.alloc(nv));
-    CK(H->x.upload(xs.data(), nv, st));
-    CK(H->xt.upload(xs.data(), nv, st));
-    CK(H->v.upload(zero.data(), nv, st));
-    CK(H->s.upload(xs.data(), nv, st));
+    const size_t nvS = (size_t)nv * S;
+    CK(H->x.alloc(nvS)); CK(H->xt.alloc(nvS)); CK(H->v.alloc(nvS)); CK(H->s.alloc(nvS));
+    {
+        DBuf<double4> x1;
+        CK(x1.alloc(nv));
+        CK(x1.upload(xs.data(), nv, st));
+        launch_replicate(st, x1.p, H->x.p, nv, S);
+        launch_replicate(st, x1.p, H->xt.p, nv, S);
+        launch_replicate(st, x1.p, H->s.p, nv, S);
+        CK(cudaMemsetAsync(H->v.p, 0, nvS * sizeof(double4), st));
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+    }
     std::vector<double> M(nf);
     for (int i = 0; i < nf; ++i) M[i] = H->rd.mass[H->int2orig[i]];
     CK(H->M.alloc(nf));
@@ -306,18 +337,17 @@ static int upload_all(sim_handle* H) {
     CK(H->tet.alloc(nt)); CK(H->tet.upload(tv.data(), nt, st));
     CK(H->Bm.alloc((size_t)9 * nt)); CK(H->Bm.upload(Bm.data(), (size_t)9 * nt, st));
     CK(H->hw2.alloc(nt)); CK(H->hw2.upload(hw.data(), nt, st));
-    CK(H->fc.alloc((size_t)4 * nt));
-    CK(H->u.alloc(nf)); CK(H->y.alloc(nf));
+    CK(H->fc.alloc((size_t)4 * nt * S));
+    CK(H->u.alloc((size_t)nf * S)); CK(H->y.alloc((size_t)nf * S));
+    CK(cudaMemsetAsync(H->u.p, 0, (size_t)nf * S * sizeof(float4), st));
+    CK(cudaMemsetAsync(H->y.p, 0, (size_t)nf * S * sizeof(float4), st));
     // vertex -> (tet, corner) adjacency for free vertices, ascending tet order
     std::vector<int32_t> adjp(nf + 1, 0), adj;
-    for (int t = 0; t < nt; ++t)
-        for (int c = 0; c < 4; ++c) {
-            int a = tv[t].x;
-            if (c == 1) a = tv[t].y;
-            if (c == 2) a = tv[t].z;
-            if (c == 3) a = tv[t].w;
-            if (a < nf) adjp[a + 1]++;
-        }
+    for (int t = 0; t < nt; ++t) {
+        int q[4] = {tv[t].x, tv[t].y, tv[t].z, tv[t].w};
+        for (int c = 0; c < 4; ++c)
+            if (q[c] < nf) adjp[q[c] + 1]++;
+    }
     for (int i = 0; i < nf; ++i) adjp[i + 1] += adjp[i];
     adj.resize(adjp[nf]);
     std::vector<int32_t> fill(adjp.begin(), adjp.end() - 1);
@@ -332,52 +362,47 @@ static int upload_all(sim_handle* H) {
     const simhost::Inverse& K = H->K;
     CK(H->Krow.alloc(K.nnz)); CK(H->Krow.upload(K.Krow.data(), K.nnz, st));
     CK(H->Kcol.alloc(K.nnz)); CK(H->Kcol.upload(K.Kcol.data(), K.nnz, st));
-    CK(H->T1.alloc(H->T1h.size())); CK(H->T1.upload(H->T1h.data(), H->T1h.size(), st));
     CK(H->T2.alloc(H->T2h.size())); CK(H->T2.upload(H->T2h.data(), H->T2h.size(), st));
-    std::vector<int32_t> cb(nf);
     std::vector<int2> meta(nf);
-    for (int j = 0; j < nf; ++j) {
-        cb[j] = (int32_t)(K.colptr[j] + K.depth[j]);
-        meta[j] = make_int2((int32_t)(K.rowptr[j] - K.first[j]), K.first[j]);
-    }
+    for (int j = 0; j < nf; ++j) meta[j] = make_int2((int32_t)(K.rowptr[j] - K.first[j]), K.first[j]);
     CK(H->colptr.alloc(nf + 1)); CK(H->colptr.upload(K.colptr.data(), nf + 1, st));
-    CK(H->cb.alloc(nf)); CK(H->cb.upload(cb.data(), nf, st));
     CK(H->meta.alloc(nf)); CK(H->meta.upload(meta.data(), nf, st));
     CK(H->depth.alloc(nf)); CK(H->depth.upload(K.depth.data(), nf, st));
     CK(H->parent.alloc(nf)); CK(H->parent.upload(K.parent.data(), nf, st));
     CK(H->ptop.alloc(nf)); CK(H->ptop.upload(K.ptop.data(), nf, st));
     const simhost::WorkLists& W = H->wl;
-    CK(H->p1.alloc(W.p1.size())); CK(H->p1.upload(W.p1.data(), W.p1.size(), st));
-    CK(H->p1b.alloc(W.p1b.size())); CK(H->p1b.upload(W.p1b.data(), W.p1b.size(), st));
     CK(H->p2b.alloc(W.p2b.size())); CK(H->p2b.upload(W.p2b.data(), W.p2b.size(), st));
     CK(H->cover.alloc(W.cover.size())); CK(H->cover.upload(W.cover.data(), W.cover.size(), st));
-    CK(H->part1.alloc((size_t)std::max(1, W.p1_parts) * 32 * 3));
-    size_t ncnt = W.p1b.size();
-    CK(H->counters.alloc(ncnt));
-    CK(cudaMemsetAsync(H->counters.p, 0, ncnt * sizeof(int), st));
-    // contact buffers at capacity (pointers stay fixed for graph reuse)
-    CK(H->dc.alloc(kMaxContacts));
-    CK(H->cc9.alloc(9 * kMaxContacts)); CK(H->cs0.alloc(kMaxContacts)); CK(H->cv0.alloc(kMaxContacts));
-    CK(H->cc1.alloc(kMaxSlots));
-    CK(H->slot_vtx.alloc(kMaxSlots));
-    CK(H->scp.alloc(kMaxSlots + 1));
-    CK(H->sci.alloc(4 * kMaxContacts));
-    CK(H->scw.alloc(4 * kMaxContacts));
-    CK(H->vcp.alloc(nf + 1));
-    CK(H->vci.alloc(4 * kMaxContacts));
-    CK(H->vcw.alloc(4 * kMaxContacts));
-    CK(H->G.alloc((size_t)kMaxSlots * kMaxSlots));
-    CK(H->GA.alloc((size_t)kMaxSlots * kMaxSlots));
-    CK(H->lam.alloc(3 * kMaxContacts)); CK(H->theta.alloc(3 * kMaxContacts)); CK(H->cdiag.alloc(3 * kMaxContacts));
-    CK(H->hvec.alloc(3 * kMaxContacts)); CK(H->hl.alloc(3 * kMaxContacts)); CK(H->dxt.alloc(3 * kMaxSlots));
-    CK(H->wz.alloc(3 * kMaxSlots)); CK(H->phi_abs.alloc(kMaxContacts)); CK(H->cr_res.alloc(1));
-    CK(H->rho.alloc(3 * kMaxContacts)); CK(H->act_na.alloc(1)); CK(H->act_idx.alloc(kMaxSlots));
-    CK(H->act_pos.alloc(kMaxSlots)); CK(H->act_con.alloc(kMaxSlots));
-    CK(H->chain_off.alloc(kMaxSlots + 1)); CK(H->flag.alloc(nf)); CK(H->ucount.alloc(2)); CK(H->ulist.alloc(nf));
-    CK(cudaMemsetAsync(H->ucount.p, 0, 2 * sizeof(int), st));
-    CK(cudaMemsetAsync(H->lam.p, 0, 3 * kMaxContacts * sizeof(double), st));
-    CK(cudaMemsetAsync(H->vcp.p, 0, (nf + 1) * sizeof(int32_t), st));
-    CK(cudaMemsetAsync(H->cr_res.p, 0, sizeof(double), st));
+    if (S == 1) {
+        CK(H->T1.alloc(H->T1h.size())); CK(H->T1.upload(H->T1h.data(), H->T1h.size(), st));
+        CK(H->p1.alloc(W.p1.size())); CK(H->p1.upload(W.p1.data(), W.p1.size(), st));
+        CK(H->p1b.alloc(W.p1b.size())); CK(H->p1b.upload(W.p1b.data(), W.p1b.size(), st));
+        CK(H->part1.alloc((size_t)std::max(1, W.p1_parts) * 32 * 3));
+        size_t ncnt = W.p1b.size();
+        CK(H->counters.alloc(ncnt));
+        CK(cudaMemsetAsync(H->counters.p, 0, ncnt * sizeof(int), st));
+    } else {
+        CK(H->T1p.alloc(H->T1ph.size())); CK(H->T1p.upload(H->T1ph.data(), H->T1ph.size(), st));
+        CK(H->bu1d.alloc(H->bu1.size())); CK(H->bu1d.upload(H->bu1.data(), H->bu1.size(), st));
+        CK(H->bu2d.alloc(H->bu2.size())); CK(H->bu2d.upload(H->bu2.data(), H->bu2.size(), st));
+        CK(H->part1.alloc((size_t)std::max(1, H->bparts) * 3 * 32 * S));
+        const int nch = (S + 127) / 128;
+        size_t ncnt = (size_t)H->bblocks1 * nch;
+        CK(H->counters.alloc(ncnt));
+        CK(cudaMemsetAsync(H->counters.p, 0, ncnt * sizeof(int), st));
+    }
+    // per-instance contact scalars
+    CK(H->coff.alloc(S + 1)); CK(H->soff.alloc(S + 1)); CK(H->uoff.alloc(S + 1));
+    CK(H->goff.alloc(S + 1)); CK(H->zoff.alloc(S + 1));
+    CK(H->cr_res.alloc(S)); CK(H->act_na.alloc(S)); CK(H->ucount.alloc(2 * (size_t)S));
+    CK(cudaMemsetAsync(H->coff.p, 0, (S + 1) * sizeof(int), st));
+    CK(cudaMemsetAsync(H->soff.p, 0, (S + 1) * sizeof(int), st));
+    CK(cudaMemsetAsync(H->cr_res.p, 0, S * sizeof(double), st));
+    CK(H->flag.alloc((size_t)S * nf));
+    CK(H->slotmap.alloc((size_t)nf * S));
+    CK(cudaMemsetAsync(H->slotmap.p, 0xff, (size_t)nf * S * sizeof(int32_t), st));
+    H->coff_h.assign(S + 1, 0);
+    H->soff_h.assign(S + 1, 0);
     CK(cudaStreamSynchronize(st));
     return SIM_OK;
 }
@@ -395,6 +420,8 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
             freev.push_back(i);
         }
     const int nf = (int)freev.size();
+    if ((int64_t)nf * H->S >= (int64_t)INT32_MAX / 4)
+        return fail(SIM_E_LIMIT, "n_free x n_instances exceeds the int32 index range");
     simhost::Csr A = simhost::assemble_Av(nv, H->n_t, H->T.data(), H->rd, H->h, vid, nf);
     std::vector<double> coords(3 * (size_t)nf);
     for (int k = 0; k < nf; ++k)
@@ -417,6 +444,7 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
         return fail(SIM_E_LIMIT, "nnz(K) = %lld exceeds the int32 offset limit", (long long)H->K.nnz);
     simhost::build_worklists(H->K, H->wl, 1024);
     simhost::build_tiles(H->K, H->wl, H->T1h, H->T2h);
+    if (H->S > 1) H->bparts = simhost::build_batched(H->K, H->wl, 64, H->bu1, H->T1ph, H->bu2, H->bblocks1);
     H->n_f = nf;
     H->int2orig.assign(nv, -1);
     H->orig2int.assign(nv, -1);
@@ -435,7 +463,8 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
 }
 
 // ---------------------------------------------------------------------------
-// contacts
+// contacts: validated per instance on the host, committed to the device for all
+// instances at once (packed arrays + batched Delassus) before the next step
 // ---------------------------------------------------------------------------
 static void gram_schmidt(const double n[3], double t1[3], double t2[3]) {
     int a = 0;
@@ -452,32 +481,37 @@ static void gram_schmidt(const double n[3], double t1[3], double t2[3]) {
     t2[2] = n[0] * t1[1] - n[1] * t1[0];
 }
 
-extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n) {
-    if (!H) return fail(SIM_E_INVALID, "null handle");
-    if (H->state != 1) return fail(SIM_E_STATE, "build the sparse inverse first");
-    if (H->host_only) return fail(SIM_E_STATE, "host-only handle");
-    if (n < 0 || (n > 0 && !cs)) return fail(SIM_E_INVALID, "bad contact array");
-    if (n > kMaxContacts) return fail(SIM_E_LIMIT, "at most %d contacts per handle", kMaxContacts);
-    auto th0 = std::chrono::steady_clock::now();
-    std::vector<DContact> hc(n);
+// validate one instance's contacts and build its local arrays; returns SIM_OK or an error
+// code with the message in `err` (thread-safe: no globals touched)
+static int build_inst(const sim_handle* H, const sim_contact* cs, int n, InstContacts& I, std::string& err) {
+    char buf[256];
+    auto bad = [&](int code, const char* fmt, int c, int v = 0) {
+        snprintf(buf, sizeof buf, fmt, c, v);
+        err = buf;
+        return code;
+    };
+    if (n < 0 || (n > 0 && !cs)) { err = "bad contact array"; return SIM_E_INVALID; }
+    if (n > kMaxContacts) return bad(SIM_E_LIMIT, "at most %d contacts per instance", kMaxContacts);
+    I = InstContacts();
+    I.hc.resize(n);
     std::vector<int32_t> verts;
     for (int c = 0; c < n; ++c) {
         const sim_contact& s = cs[c];
-        if (s.kind != 0 && s.kind != 1) return fail(SIM_E_INVALID, "contact %d: kind must be 0 or 1", c);
-        if (s.n_verts < 1 || s.n_verts > 4) return fail(SIM_E_INVALID, "contact %d: 1..4 vertices", c);
+        if (s.kind != 0 && s.kind != 1) return bad(SIM_E_INVALID, "contact %d: kind must be 0 or 1", c);
+        if (s.n_verts < 1 || s.n_verts > 4) return bad(SIM_E_INVALID, "contact %d: 1..4 vertices", c);
         double nn = std::sqrt(s.normal[0] * s.normal[0] + s.normal[1] * s.normal[1] + s.normal[2] * s.normal[2]);
-        if (!(std::fabs(nn - 1.0) < 1e-6)) return fail(SIM_E_INVALID, "contact %d: normal not unit", c);
-        if (!(s.mu >= 0) || !std::isfinite(s.mu)) return fail(SIM_E_INVALID, "contact %d: mu must be >= 0", c);
-        if (!(s.compliance >= 0)) return fail(SIM_E_INVALID, "contact %d: compliance must be >= 0", c);
-        if (!std::isfinite(s.offset)) return fail(SIM_E_INVALID, "contact %d: offset not finite", c);
-        DContact& d = hc[c];
+        if (!(std::fabs(nn - 1.0) < 1e-6)) return bad(SIM_E_INVALID, "contact %d: normal not unit", c);
+        if (!(s.mu >= 0) || !std::isfinite(s.mu)) return bad(SIM_E_INVALID, "contact %d: mu must be >= 0", c);
+        if (!(s.compliance >= 0)) return bad(SIM_E_INVALID, "contact %d: compliance must be >= 0", c);
+        if (!std::isfinite(s.offset)) return bad(SIM_E_INVALID, "contact %d: offset not finite", c);
+        DContact& d = I.hc[c];
         memset(&d, 0, sizeof d);
         d.kind = s.kind;
         d.nv = s.n_verts;
         for (int q = 0; q < s.n_verts; ++q) {
-            if (s.verts[q] < 0 || s.verts[q] >= H->n_v) return fail(SIM_E_INVALID, "contact %d: vertex out of range", c);
-            if (H->fixed[s.verts[q]]) return fail(SIM_E_INVALID, "contact %d: vertex %d is pinned", c, s.verts[q]);
-            if (!std::isfinite(s.weights[q])) return fail(SIM_E_INVALID, "contact %d: weight not finite", c);
+            if (s.verts[q] < 0 || s.verts[q] >= H->n_v) return bad(SIM_E_INVALID, "contact %d: vertex out of range", c);
+            if (H->fixed[s.verts[q]]) return bad(SIM_E_INVALID, "contact %d: vertex %d is pinned", c, s.verts[q]);
+            if (!std::isfinite(s.weights[q])) return bad(SIM_E_INVALID, "contact %d: weight not finite", c);
             d.vtx[q] = H->orig2int[s.verts[q]];
             d.w[q] = s.weights[q];
             verts.push_back(d.vtx[q]);
@@ -503,125 +537,272 @@ extern "C" int sim_set_contacts(sim_handle* H, const sim_contact* cs, int32_t n)
     }
     std::sort(verts.begin(), verts.end());
     verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
-    if ((int)verts.size() > kMaxSlots) return fail(SIM_E_LIMIT, "at most %d contact vertices", kMaxSlots);
-    if (cr_smem_bytes(n, (int)verts.size()) > kCrMaxSmem)
-        return fail(SIM_E_LIMIT, "%d contacts on %d vertices exceed the CR cluster's shared memory (%zu > %zu B)", n,
-                    (int)verts.size(), cr_smem_bytes(n, (int)verts.size()), kCrMaxSmem);
     const int ns = (int)verts.size();
-    std::vector<int32_t> slot_of(H->n_f, -1);
-    for (int s = 0; s < ns; ++s) slot_of[verts[s]] = s;
-    // slot -> (contact, weight) and vertex -> (contact, weight) lists
-    std::vector<std::vector<std::pair<int, float>>> sl(ns);
+    if (ns > kMaxSlots) return bad(SIM_E_LIMIT, "at most %d contact vertices per instance", kMaxSlots);
+    if (cr_smem_bytes(n, ns) > kCrMaxSmem) {
+        snprintf(buf, sizeof buf, "%d contacts on %d vertices exceed the CR's shared memory (%zu > %zu B)", n, ns,
+                 cr_smem_bytes(n, ns), kCrMaxSmem);
+        err = buf;
+        return SIM_E_LIMIT;
+    }
+    // slot -> (contact, weight) lists in contact order
+    std::vector<int> cnt(ns + 1, 0);
+    auto slot_of = [&](int v) { return (int)(std::lower_bound(verts.begin(), verts.end(), v) - verts.begin()); };
     for (int c = 0; c < n; ++c)
-        for (int q = 0; q < hc[c].nv; ++q) {
-            hc[c].slot[q] = slot_of[hc[c].vtx[q]];
-            sl[hc[c].slot[q]].push_back({c, (float)hc[c].w[q]});
+        for (int q = 0; q < I.hc[c].nv; ++q) {
+            I.hc[c].slot[q] = slot_of(I.hc[c].vtx[q]);
+            cnt[I.hc[c].slot[q] + 1]++;
         }
-    std::vector<int32_t> scp(ns + 1, 0), sci;
-    std::vector<float> scw;
-    for (int s = 0; s < ns; ++s) {
-        for (auto& e : sl[s]) { sci.push_back(e.first); scw.push_back(e.second); }
-        scp[s + 1] = (int)sci.size();
-    }
-    std::vector<int32_t> vcp(H->n_f + 1, 0);
-    for (int s = 0; s < ns; ++s) vcp[verts[s] + 1] = scp[s + 1] - scp[s];
-    for (int i = 0; i < H->n_f; ++i) vcp[i + 1] += vcp[i];
-    cudaStream_t st = H->stream;
-    // asynchronous uploads through pinned staging: wait only for the previous call's copies
-    {
-        const size_t need = n * sizeof(DContact) + 64 * (size_t)n + 32 * (size_t)ns + 16 * sci.size() +
-                            4 * ((size_t)H->n_f + 1) + 1024;
-        if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
-        CK(cudaEventSynchronize(H->stage_free));
-        if (need > H->stage_cap) {
-            if (H->stage) CK(cudaFreeHost(H->stage));
-            H->stage = nullptr;
-            H->stage_cap = 0;
-            CK(cudaMallocHost((void**)&H->stage, 2 * need));
-            H->stage_cap = 2 * need;
+    I.scp.assign(ns + 1, 0);
+    for (int s = 0; s < ns; ++s) I.scp[s + 1] = I.scp[s] + cnt[s + 1];
+    I.sci.resize(I.scp[ns]);
+    I.scw.resize(I.scp[ns]);
+    std::vector<int> fillp(I.scp.begin(), I.scp.end() - 1);
+    for (int c = 0; c < n; ++c)
+        for (int q = 0; q < I.hc[c].nv; ++q) {
+            const int s = I.hc[c].slot[q];
+            I.sci[fillp[s]] = c;
+            I.scw[fillp[s]++] = (float)I.hc[c].w[q];
         }
-        H->stage_used = 0;
+    I.c9.resize(9 * (size_t)n);
+    I.s0.resize(n);
+    I.v0.resize(n);
+    for (int q = 0; q < n; ++q) {
+        for (int a = 0; a < 3; ++a)
+            for (int d = 0; d < 3; ++d) I.c9[9 * q + 3 * a + d] = (float)I.hc[q].c[a][d];
+        const bool single = I.hc[q].nv == 1 && I.hc[q].w[0] == 1.0;
+        I.s0[q] = single ? I.hc[q].slot[0] : -1;
+        I.v0[q] = single ? I.hc[q].vtx[0] : -1;
     }
-    CK(stage_upload(H, H->dc.p, hc.data(), n));
-    {
-        std::vector<float> c9(9 * (size_t)n);
-        std::vector<int32_t> s0(n), v0(n);
-        for (int q = 0; q < n; ++q) {
-            for (int a = 0; a < 3; ++a)
-                for (int d = 0; d < 3; ++d) c9[9 * q + 3 * a + d] = (float)hc[q].c[a][d];
-            const bool single = hc[q].nv == 1 && hc[q].w[0] == 1.0;
-            s0[q] = single ? hc[q].slot[0] : -1;
-            v0[q] = single ? hc[q].vtx[0] : -1;
-        }
-        CK(stage_upload(H, H->cc9.p, c9.data(), c9.size()));
-        CK(stage_upload(H, H->cs0.p, s0.data(), n));
-        CK(stage_upload(H, H->cv0.p, v0.data(), n));
-        std::vector<int32_t> c1(ns, -1);
-        for (int s = 0; s < ns; ++s)
-            if (scp[s + 1] - scp[s] == 1 && s0[sci[scp[s]]] == s) c1[s] = sci[scp[s]];
-        CK(stage_upload(H, H->cc1.p, c1.data(), ns));
-    }
-    CK(stage_upload(H, H->slot_vtx.p, verts.data(), ns));
-    CK(stage_upload(H, H->scp.p, scp.data(), ns + 1));
-    CK(stage_upload(H, H->sci.p, sci.data(), sci.size()));
-    CK(stage_upload(H, H->scw.p, scw.data(), scw.size()));
-    CK(stage_upload(H, H->vcp.p, vcp.data(), (size_t)H->n_f + 1));
-    CK(stage_upload(H, H->vci.p, sci.data(), sci.size()));   // slots are sorted by vertex: same order
-    CK(stage_upload(H, H->vcw.p, scw.data(), scw.size()));
-    H->h2d_contact_bytes = (int64_t)(n * sizeof(DContact) + ns * sizeof(int32_t) + (ns + 1) * sizeof(int32_t) +
-                                     2 * sci.size() * (sizeof(int32_t) + sizeof(float)) +
-                                     (H->n_f + 1) * sizeof(int32_t));
-    // ancestor chains of the contact vertices (for chain_dot / scatter)
-    std::vector<int32_t> coff(ns + 1, 0);
-    for (int s = 0; s < ns; ++s) coff[s + 1] = coff[s] + H->K.depth[verts[s]] + 1;
-    if ((size_t)coff[ns] > H->chain_rows.n) {
-        CK(cudaStreamSynchronize(st));
-        CK(H->chain_rows.alloc(std::max<size_t>(coff[ns], 2 * H->chain_rows.n)));
-        CK(H->Zc.alloc(H->chain_rows.n));
-        H->contact_gen++;
-    }
-    CK(stage_upload(H, H->chain_off.p, coff.data(), ns + 1));
-    CK(cudaEventRecord(H->stage_free, st));
-    CK(cudaMemsetAsync(H->flag.p, 0, H->n_f, st));
-    CK(cudaMemsetAsync(H->ucount.p, 0, 2 * sizeof(int), st));
-    launch_chain_rows(st, ns, H->slot_vtx.p, H->chain_off.p, H->parent.p, H->ptop.p, H->chain_rows.p, H->flag.p);
-    launch_ulist(st, H->n_f, ns, H->flag.p, H->slot_vtx.p, H->meta.p, H->ucount.p, H->ulist.p, H->Krow.p, H->Zc.p);
-    H->h2d_contact_bytes += (ns + 1) * sizeof(int32_t);
-    // Delassus Gram and D_jj on the device
-    launch_delassus(st, ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
-    launch_djj(st, n, ns, H->dc.p, H->G.p);
-    CK(cudaGetLastError());
-    H->nc = n;
-    H->ns = ns;
-    H->row_lo = ns ? verts[0] : H->n_f;
-    H->hc = hc;
-    H->slot_vtx_h = verts;
-    H->set_contacts_host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count();
-    return SIM_OK;   // asynchronous: the copies and kernels are ordered on the handle's stream
+    I.c1.assign(ns, -1);
+    for (int s = 0; s < ns; ++s)
+        if (I.scp[s + 1] - I.scp[s] == 1 && I.s0[I.sci[I.scp[s]]] == s) I.c1[s] = I.sci[I.scp[s]];
+    I.verts = std::move(verts);
+    I.chain_total = 0;
+    for (int s = 0; s < ns; ++s) I.chain_total += H->K.depth[I.verts[s]] + 1;
+    return SIM_OK;
 }
 
-// ---------------------------------------------------------------------------
-// frame driver
-// ---------------------------------------------------------------------------
+static int check_contact_call(sim_handle* H) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (H->state != 1) return fail(SIM_E_STATE, "build the sparse inverse first");
+    if (H->host_only) return fail(SIM_E_STATE, "host-only handle");
+    return SIM_OK;
+}
+
+extern "C" int sim_set_contacts(sim_handle* H, int32_t instance, const sim_contact* cs, int32_t n) {
+    int rc = check_contact_call(H);
+    if (rc) return rc;
+    if (instance < 0 || instance >= H->S) return fail(SIM_E_INVALID, "instance %d out of range [0, %d)", instance, H->S);
+    auto th0 = std::chrono::steady_clock::now();
+    InstContacts I;
+    std::string err;
+    rc = build_inst(H, cs, n, I, err);
+    if (rc) return fail(rc, "%s", err.c_str());
+    H->ic[instance] = std::move(I);
+    H->dirty = true;
+    H->set_contacts_host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count();
+    return SIM_OK;
+}
+
+extern "C" int sim_set_contacts_batch(sim_handle* H, int32_t first, int32_t count, const int32_t* counts,
+                                      const sim_contact* cs) {
+    int rc = check_contact_call(H);
+    if (rc) return rc;
+    if (first < 0 || count < 0 || first + count > H->S) return fail(SIM_E_INVALID, "instance range out of bounds");
+    if (count > 0 && !counts) return fail(SIM_E_INVALID, "null counts");
+    auto th0 = std::chrono::steady_clock::now();
+    std::vector<int64_t> at(count + 1, 0);
+    for (int i = 0; i < count; ++i) {
+        if (counts[i] < 0) return fail(SIM_E_INVALID, "negative count for instance %d", first + i);
+        at[i + 1] = at[i] + counts[i];
+    }
+    if (at[count] > 0 && !cs) return fail(SIM_E_INVALID, "null contacts");
+    std::vector<InstContacts> tmp(count);
+    std::vector<int> codes(count, SIM_OK);
+    std::vector<std::string> errs(count);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int i = 0; i < count; ++i) codes[i] = build_inst(H, cs + at[i], counts[i], tmp[i], errs[i]);
+    for (int i = 0; i < count; ++i)
+        if (codes[i]) return fail(codes[i], "instance %d: %s", first + i, errs[i].c_str());
+    for (int i = 0; i < count; ++i) H->ic[first + i] = std::move(tmp[i]);
+    H->dirty = true;
+    H->set_contacts_host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count();
+    return SIM_OK;
+}
+
+static InstOff inst_off(sim_handle* H) {
+    return InstOff{H->coff.p, H->soff.p, H->goff.p, H->uoff.p, H->zoff.p};
+}
+static Slots slots(sim_handle* H) { return Slots{H->slot_vtx.p, H->slot_inst.p, H->scp.p, H->sci.p, H->scw.p}; }
+static CrContacts cr_contacts(sim_handle* H) { return CrContacts{H->cc9.p, H->cs0.p, H->cv0.p, H->cc1.p}; }
+
 static Params make_params(const sim_handle* H) {
     Params P;
     P.n_v = H->n_v;
     P.n_f = H->n_f;
     P.n_t = H->n_t;
+    P.S = H->S;
     P.h = H->h;
     for (int d = 0; d < 3; ++d) { P.g[d] = H->mat.gravity[d]; P.vpin[d] = H->vpin[d]; }
     P.model = H->mat.model;
     P.k = (float)H->kproj;
     P.mu = (float)H->mu_l;
     P.lam = (float)H->lam_l;
-    P.nc = H->nc;
-    P.ns = H->ns;
+    P.C = H->C;
+    P.NS = H->NS;
+    P.nc_max = H->nc_max;
+    P.ns_max = H->ns_max;
     P.cr_iters = H->mat.cr_iterations;
     return P;
 }
 
+// pack every instance's contacts, upload them asynchronously and build the per-contact-set
+// device data (chains, row lists, Delassus Gram, D_jj) for all instances in batched launches
+static int commit_contacts(sim_handle* H) {
+    if (!H->dirty) return SIM_OK;
+    const int S = H->S, nf = H->n_f;
+    cudaStream_t st = H->stream;
+    std::vector<int> coff(S + 1, 0), soff(S + 1, 0), uoff(S + 1, 0);
+    std::vector<int64_t> goff(S + 1, 0), zoff(S + 1, 0);
+    int ncm = 0, nsm = 0, um = 0;
+    for (int i = 0; i < S; ++i) {
+        const InstContacts& I = H->ic[i];
+        const int n = (int)I.hc.size(), ns = (int)I.verts.size();
+        coff[i + 1] = coff[i] + n;
+        soff[i + 1] = soff[i] + ns;
+        goff[i + 1] = goff[i] + (int64_t)ns * ns;
+        zoff[i + 1] = zoff[i] + I.chain_total;
+        const int urows = (int)std::min<int64_t>(nf, I.chain_total);
+        uoff[i + 1] = uoff[i] + urows;
+        ncm = std::max(ncm, n);
+        nsm = std::max(nsm, ns);
+        um = std::max(um, urows);
+    }
+    if (zoff[S] >= (int64_t)INT32_MAX) return fail(SIM_E_LIMIT, "total ancestor-chain entries exceed int32");
+    const int Ct = coff[S], NSt = soff[S];
+    bool grew = false;
+    const size_t cC = std::max(Ct, 1), cS = std::max(NSt, 1);
+    CK(H->dc.ensure(cC, grew)); CK(H->cc9.ensure(9 * cC, grew)); CK(H->cs0.ensure(cC, grew));
+    CK(H->cv0.ensure(cC, grew)); CK(H->cc1.ensure(cS, grew)); CK(H->slot_vtx.ensure(cS, grew));
+    CK(H->slot_inst.ensure(cS, grew)); CK(H->scp.ensure(cS + 1, grew)); CK(H->sci.ensure(4 * cC, grew));
+    CK(H->scw.ensure(4 * cC, grew)); CK(H->G.ensure(std::max<int64_t>(goff[S], 1), grew));
+    CK(H->GA.ensure(std::max<int64_t>(goff[S], 1), grew));
+    CK(H->lam.ensure(3 * cC, grew)); CK(H->theta.ensure(3 * cC, grew)); CK(H->cdiag.ensure(3 * cC, grew));
+    CK(H->hvec.ensure(3 * cC, grew)); CK(H->hl.ensure(3 * cC, grew)); CK(H->rho.ensure(3 * cC, grew));
+    CK(H->phi_abs.ensure(cC, grew)); CK(H->dxt.ensure(3 * cS, grew)); CK(H->wz.ensure(3 * cS, grew));
+    CK(H->act_idx.ensure(cS, grew)); CK(H->act_pos.ensure(cS, grew)); CK(H->act_con.ensure(cS, grew));
+    CK(H->chain_off.ensure(cS + 1, grew)); CK(H->chain_rows.ensure(std::max<int64_t>(zoff[S], 1), grew));
+    CK(H->Zc.ensure(std::max<int64_t>(zoff[S], 1), grew)); CK(H->ulist.ensure(std::max(uoff[S], 1), grew));
+    if (grew) H->contact_gen++;   // captured pointers changed
+    // pack
+    std::vector<DContact> dc(Ct);
+    std::vector<float> c9(9 * (size_t)Ct), scw;
+    std::vector<int32_t> s0(Ct), v0(Ct), c1(NSt), svtx(NSt), sinst(NSt), scp(NSt + 1, 0), sci, choff(NSt + 1, 0);
+    sci.reserve(4 * (size_t)Ct);
+    scw.reserve(4 * (size_t)Ct);
+    for (int i = 0; i < S; ++i) {
+        const InstContacts& I = H->ic[i];
+        const int cb = coff[i], sb = soff[i], n = (int)I.hc.size(), ns = (int)I.verts.size();
+        for (int c = 0; c < n; ++c) {
+            DContact d = I.hc[c];
+            d.inst = i;
+            for (int q = 0; q < d.nv; ++q) d.slot[q] += sb;
+            dc[cb + c] = d;
+            s0[cb + c] = I.s0[c] >= 0 ? I.s0[c] + sb : -1;
+            v0[cb + c] = I.v0[c];
+        }
+        std::copy(I.c9.begin(), I.c9.end(), c9.begin() + 9 * (size_t)cb);
+        for (int s = 0; s < ns; ++s) {
+            const int g = sb + s;
+            c1[g] = I.c1[s] >= 0 ? I.c1[s] + cb : -1;
+            svtx[g] = I.verts[s];
+            sinst[g] = i;
+            for (int p = I.scp[s]; p < I.scp[s + 1]; ++p) {
+                sci.push_back(I.sci[p] + cb);
+                scw.push_back(I.scw[p]);
+            }
+            scp[g + 1] = (int)sci.size();
+            choff[g + 1] = choff[g] + H->K.depth[I.verts[s]] + 1;
+        }
+    }
+    // staging (wait only for the previous commit's copies)
+    const size_t need = (size_t)Ct * (sizeof(DContact) + 36 + 8) + (size_t)NSt * 24 + sci.size() * 8 +
+                        (size_t)(S + 1) * 32 + 4096;
+    if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
+    CK(cudaEventSynchronize(H->stage_free));
+    if (need > H->stage_cap) {
+        if (H->stage) CK(cudaFreeHost(H->stage));
+        H->stage = nullptr;
+        H->stage_cap = 0;
+        CK(cudaMallocHost((void**)&H->stage, 2 * need));
+        H->stage_cap = 2 * need;
+    }
+    H->stage_used = 0;
+    H->h2d_contact_bytes = 0;
+    CK(stage_upload(H, H->dc.p, dc.data(), Ct));
+    CK(stage_upload(H, H->cc9.p, c9.data(), c9.size()));
+    CK(stage_upload(H, H->cs0.p, s0.data(), Ct));
+    CK(stage_upload(H, H->cv0.p, v0.data(), Ct));
+    CK(stage_upload(H, H->cc1.p, c1.data(), NSt));
+    CK(stage_upload(H, H->slot_vtx.p, svtx.data(), NSt));
+    CK(stage_upload(H, H->slot_inst.p, sinst.data(), NSt));
+    CK(stage_upload(H, H->scp.p, scp.data(), NSt + 1));
+    CK(stage_upload(H, H->sci.p, sci.data(), sci.size()));
+    CK(stage_upload(H, H->scw.p, scw.data(), scw.size()));
+    CK(stage_upload(H, H->chain_off.p, choff.data(), NSt + 1));
+    CK(stage_upload(H, H->coff.p, coff.data(), S + 1));
+    CK(stage_upload(H, H->soff.p, soff.data(), S + 1));
+    CK(stage_upload(H, H->uoff.p, uoff.data(), S + 1));
+    CK(stage_upload(H, H->goff.p, goff.data(), S + 1));
+    CK(stage_upload(H, H->zoff.p, zoff.data(), S + 1));
+    CK(cudaEventRecord(H->stage_free, st));
+    H->C = Ct;
+    H->NS = NSt;
+    H->nc_max = ncm;
+    H->ns_max = nsm;
+    H->urows_max = um;
+    H->coff_h = coff;
+    H->soff_h = soff;
+    CK(cudaMemsetAsync(H->flag.p, 0, (size_t)S * nf, st));
+    CK(cudaMemsetAsync(H->slotmap.p, 0xff, (size_t)nf * S * sizeof(int32_t), st));
+    CK(cudaMemsetAsync(H->ucount.p, 0, 2 * (size_t)S * sizeof(int), st));
+    CK(cudaMemsetAsync(H->cr_res.p, 0, S * sizeof(double), st));
+    Params P = make_params(H);
+    const InstOff off = inst_off(H);
+    const Slots sl = slots(H);
+    launch_chain_rows(st, P, sl, H->chain_off.p, H->parent.p, H->ptop.p, H->chain_rows.p, H->flag.p, H->slotmap.p);
+    launch_ulist(st, P, off, H->flag.p, sl, H->meta.p, H->ucount.p, H->ulist.p, H->Krow.p, H->Zc.p);
+    launch_delassus(st, P, off, sl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
+    launch_djj(st, P, off, H->dc.p, H->G.p);
+    CK(cudaGetLastError());
+    H->dirty = false;
+    return SIM_OK;   // asynchronous: the copies and kernels are ordered on the handle's stream
+}
+
+// ---------------------------------------------------------------------------
+// frame driver
+// ---------------------------------------------------------------------------
 static ContactState cstate(sim_handle* H) {
-    return ContactState{H->lam.p, H->theta.p, H->cdiag.p, H->hvec.p, H->hl.p, H->dxt.p, H->wz.p, H->phi_abs.p, H->cr_res.p, H->rho.p};
+    return ContactState{H->lam.p, H->theta.p, H->cdiag.p, H->hvec.p, H->hl.p, H->dxt.p, H->wz.p, H->phi_abs.p,
+                        H->cr_res.p, H->rho.p};
+}
+
+static void enqueue_kpass1(sim_handle* H, cudaStream_t st) {
+    if (H->S == 1)
+        launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->T1.p, H->u.p, H->y.p, H->part1.p,
+                      H->counters.p);
+    else
+        launch_kpass1_batched(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1p.p, H->u.p, H->y.p,
+                              H->part1.p, H->counters.p);
+}
+static void enqueue_kpass2(sim_handle* H, cudaStream_t st, double4* x, const double4* xt, double4* v, double inv_h,
+                           int fin) {
+    if (H->S == 1)
+        launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->T2.p, H->y.p, x, xt, v, inv_h, fin);
+    else
+        launch_kpass2_batched(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2.p, H->y.p, x, xt,
+                              v, inv_h, fin);
 }
 
 // enqueue one frame (predict + iters x L-G); returns kernel count or negative
@@ -631,8 +812,10 @@ static int enqueue_frame(sim_handle* H, int iters) {
     cudaStream_t st = H->stream;
     Params P = make_params(H);
     ContactState cs = cstate(H);
-    const CrContacts ccr{H->cc9.p, H->cs0.p, H->cv0.p, H->cc1.p};
+    const CrContacts ccr = cr_contacts(H);
     const CrActive act{H->act_na.p, H->act_idx.p, H->act_pos.p, H->act_con.p};
+    const InstOff off = inst_off(H);
+    const Slots sl = slots(H);
     int nk = 0;
     size_t ev = 0;
     H->pkind.clear();
@@ -650,44 +833,42 @@ static int enqueue_frame(sim_handle* H, int iters) {
 #define MARK(k) do { int r_ = mark(k); if (r_) return -r_; } while (0)
 #define CKR(call) do { cudaError_t r_ = (call); if (r_ != cudaSuccess) return -(int)r_; } while (0)
     MARK(KK_PREDICT);
-    launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->lam.p, 3 * H->nc); nk++;
-    const bool con = H->nc > 0;
+    launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->lam.p, 3 * H->C); nk++;
+    const bool con = H->C > 0;
     for (int k = 0; k < iters; ++k) {
-        // contact evaluation and the local step only read x^k: run them as two graph
+        // contact evaluation (+ active set) and the local step only read x^k: two graph
         // branches (serial when profiling, so the per-kernel events stay meaningful)
         const bool fork = con && !H->profiling;
         if (fork) {
             CKR(cudaEventRecord(H->fork_ev, st));
             CKR(cudaStreamWaitEvent(H->aux, H->fork_ev, 0));
             launch_contact_eval(H->aux, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
-            launch_active(H->aux, H->ns, ccr, H->scp.p, H->sci.p, cs, act, H->G.p, H->GA.p); nk += 2;
+            launch_active(H->aux, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += 2;
             CKR(cudaEventRecord(H->join_ev, H->aux));
         } else if (con) {
             MARK(KK_CONTACT); launch_contact_eval(st, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
-            MARK(KK_ACTIVE); launch_active(st, H->ns, ccr, H->scp.p, H->sci.p, cs, act, H->G.p, H->GA.p); nk += 2;
+            MARK(KK_ACTIVE); launch_active(st, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += 2;
         }
         MARK(KK_LOCAL);
         launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, H->x.p, H->fc.p, nullptr); nk++;
         if (fork) CKR(cudaStreamWaitEvent(st, H->join_ev, 0));
         MARK(KK_GATHER);
-        launch_gather(st, P, H->adjp.p, H->adj.p, H->fc.p, H->M.p, H->x.p, H->s.p, con ? H->vcp.p : nullptr,
-                      H->vci.p, H->vcw.p, H->hl.p, H->cb.p, H->u.p, nullptr); nk++;
+        launch_gather(st, P, H->adjp.p, H->adj.p, H->fc.p, H->M.p, H->x.p, H->s.p, con ? H->slotmap.p : nullptr, sl,
+                      H->hl.p, H->u.p, nullptr); nk++;
         MARK(KK_KPASS1);
-        launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->T1.p, H->u.p, H->y.p, H->part1.p,
-                      H->counters.p); nk++;
+        enqueue_kpass1(H, st); nk++;
         if (con) {
             MARK(KK_CHAIN);
-            launch_chain_dot(st, H->ns, H->slot_vtx.p, H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
-                             H->y.p, H->dxt.p, ccr, H->x.p, cs); nk++;
+            launch_chain_dot(st, P, H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p, H->y.p, sl, ccr, H->x.p,
+                             cs); nk++;
             MARK(KK_CR);
-            int e = launch_cr(st, P, H->dc.p, ccr, H->scp.p, H->sci.p, H->scw.p, H->GA.p, H->x.p, cs, act); nk++;
+            int e = launch_cr(st, P, off, H->dc.p, ccr, sl, H->GA.p, H->x.p, cs, act); nk++;
             if (e) return -e;
             MARK(KK_SCATTER);
-            launch_scatter(st, H->n_f, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
+            launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
         }
         MARK(KK_KPASS2);
-        launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->T2.p, H->y.p, H->x.p, H->xt.p, H->v.p,
-                      1.0 / H->h, k == iters - 1); nk++;
+        enqueue_kpass2(H, st, H->x.p, H->xt.p, H->v.p, 1.0 / H->h, k == iters - 1); nk++;
     }
     MARK(KK_N);
 #undef MARK
@@ -722,8 +903,10 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     if (H->state != 1) return fail(SIM_E_STATE, "build the sparse inverse first");
     if (frames < 0 || iters < 1) return fail(SIM_E_INVALID, "frames >= 0 and iterations >= 1");
     if (frames == 0) return SIM_OK;
-    if (!H->gexec || H->g_iters != iters || H->g_nc != H->nc || H->g_ns != H->ns || H->g_prof != H->profiling ||
-        H->g_gen != H->contact_gen) {
+    int rc = commit_contacts(H);
+    if (rc) return rc;
+    if (!H->gexec || H->g_iters != iters || H->g_C != H->C || H->g_NS != H->NS || H->g_ncm != H->nc_max ||
+        H->g_nsm != H->ns_max || H->g_um != H->urows_max || H->g_prof != H->profiling || H->g_gen != H->contact_gen) {
         if (H->gexec) {
             cudaGraphExecDestroy(H->gexec);
             H->gexec = nullptr;
@@ -738,8 +921,11 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
         cudaGraphDestroy(g);
         if (ie != cudaSuccess) return fail(SIM_E_CUDA, "instantiate: %s", cudaGetErrorString(ie));
         H->g_iters = iters;
-        H->g_nc = H->nc;
-        H->g_ns = H->ns;
+        H->g_C = H->C;
+        H->g_NS = H->NS;
+        H->g_ncm = H->nc_max;
+        H->g_nsm = H->ns_max;
+        H->g_um = H->urows_max;
         H->g_prof = H->profiling;
         H->g_gen = H->contact_gen;
         H->kernels_per_frame = nk;
@@ -768,13 +954,30 @@ extern "C" int sim_set_pin_velocity(sim_handle* H, const double v[3]) {
     return SIM_OK;
 }
 
-extern "C" int sim_get_state(sim_handle* H, double* x, double* v) {
+static int check_instance(sim_handle* H, int inst) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
+    if (inst < 0 || inst >= H->S) return fail(SIM_E_INVALID, "instance %d out of range [0, %d)", inst, H->S);
+    return SIM_OK;
+}
+
+// one instance's column of a [vertex][instance] double4 array
+static cudaError_t copy_column_d2h(sim_handle* H, const double4* src, int inst, double4* dst) {
+    return cudaMemcpy2D(dst, sizeof(double4), src + inst, sizeof(double4) * H->S, sizeof(double4), H->n_v,
+                        cudaMemcpyDeviceToHost);
+}
+static cudaError_t copy_column_h2d(sim_handle* H, const double4* src, int inst, double4* dst) {
+    return cudaMemcpy2D(dst + inst, sizeof(double4) * H->S, src, sizeof(double4), sizeof(double4), H->n_v,
+                        cudaMemcpyHostToDevice);
+}
+
+extern "C" int sim_get_state(sim_handle* H, int32_t inst, double* x, double* v) {
+    int rc = check_instance(H, inst);
+    if (rc) return rc;
     std::vector<double4> hx(H->n_v), hv(H->n_v);
     CK(cudaStreamSynchronize(H->stream));
-    CK(cudaMemcpy(hx.data(), H->x.p, H->n_v * sizeof(double4), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(hv.data(), H->v.p, H->n_v * sizeof(double4), cudaMemcpyDeviceToHost));
+    if (x) CK(copy_column_d2h(H, H->x.p, inst, hx.data()));
+    if (v) CK(copy_column_d2h(H, H->v.p, inst, hv.data()));
     for (int i = 0; i < H->n_v; ++i) {
         int o = H->int2orig[i];
         if (x) { x[3 * o] = hx[i].x; x[3 * o + 1] = hx[i].y; x[3 * o + 2] = hx[i].z; }
@@ -783,44 +986,89 @@ extern "C" int sim_get_state(sim_handle* H, double* x, double* v) {
     return SIM_OK;
 }
 
-extern "C" int sim_set_state(sim_handle* H, const double* x, const double* v) {
-    if (!H) return fail(SIM_E_INVALID, "null handle");
-    if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
-    std::vector<double4> hx(H->n_v), hv(H->n_v);
+// positions of all instances: x [n_instances][n_vertices][3] (original vertex order)
+extern "C" int sim_get_positions(sim_handle* H, double* x) {
+    int rc = check_instance(H, 0);
+    if (rc) return rc;
+    if (!x) return fail(SIM_E_INVALID, "null argument");
+    const size_t n = (size_t)H->n_v * H->S;
+    std::vector<double4> hx(n);
     CK(cudaStreamSynchronize(H->stream));
-    CK(cudaMemcpy(hx.data(), H->x.p, H->n_v * sizeof(double4), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(hv.data(), H->v.p, H->n_v * sizeof(double4), cudaMemcpyDeviceToHost));
-    for (int i = 0; i < H->n_v; ++i) {
-        int o = H->int2orig[i];
-        if (x) {
-            for (int d = 0; d < 3; ++d)
-                if (!std::isfinite(x[3 * o + d])) return fail(SIM_E_INVALID, "x not finite");
-            hx[i] = make_double4(x[3 * o], x[3 * o + 1], x[3 * o + 2], 0.0);
+    CK(cudaMemcpy(hx.data(), H->x.p, n * sizeof(double4), cudaMemcpyDeviceToHost));
+    const int S = H->S, nv = H->n_v;
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < S; ++i)
+        for (int k = 0; k < nv; ++k) {
+            const double4 a = hx[(size_t)k * S + i];
+            double* o = x + ((size_t)i * nv + H->int2orig[k]) * 3;
+            o[0] = a.x; o[1] = a.y; o[2] = a.z;
         }
-        if (v) {
-            for (int d = 0; d < 3; ++d)
-                if (!std::isfinite(v[3 * o + d])) return fail(SIM_E_INVALID, "v not finite");
-            hv[i] = make_double4(v[3 * o], v[3 * o + 1], v[3 * o + 2], 0.0);
-        }
-    }
-    CK(cudaMemcpy(H->x.p, hx.data(), H->n_v * sizeof(double4), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(H->v.p, hv.data(), H->n_v * sizeof(double4), cudaMemcpyHostToDevice));
     return SIM_OK;
 }
 
-extern "C" int sim_get_lambda(sim_handle* H, double* lam, int32_t cap) {
-    if (!H || !lam) return fail(SIM_E_INVALID, "null argument");
-    if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
-    int rows = 0;
-    for (int c = 0; c < H->nc; ++c) rows += H->hc[c].kind == 1 ? 1 : 3;
-    if (cap < rows) return fail(SIM_E_INVALID, "capacity %d < %d rows", cap, rows);
-    std::vector<double> l(3 * (size_t)H->nc);
+// states of all instances: x, v [n_instances][n_vertices][3] (either may be NULL)
+extern "C" int sim_set_states(sim_handle* H, const double* x, const double* v) {
+    int rc = check_instance(H, 0);
+    if (rc) return rc;
+    const int S = H->S, nv = H->n_v;
+    const size_t n3 = 3 * (size_t)nv * S;
+    for (size_t i = 0; i < n3; ++i) {
+        if (x && !std::isfinite(x[i])) return fail(SIM_E_INVALID, "x not finite");
+        if (v && !std::isfinite(v[i])) return fail(SIM_E_INVALID, "v not finite");
+    }
     CK(cudaStreamSynchronize(H->stream));
-    if (H->nc) CK(cudaMemcpy(l.data(), H->lam.p, l.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<double4> h((size_t)nv * S);
+    for (int pass = 0; pass < 2; ++pass) {
+        const double* src = pass == 0 ? x : v;
+        if (!src) continue;
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < S; ++i)
+            for (int k = 0; k < nv; ++k) {
+                const double* a = src + ((size_t)i * nv + H->int2orig[k]) * 3;
+                h[(size_t)k * S + i] = make_double4(a[0], a[1], a[2], 0.0);
+            }
+        CK(cudaMemcpy(pass == 0 ? H->x.p : H->v.p, h.data(), h.size() * sizeof(double4), cudaMemcpyHostToDevice));
+    }
+    return SIM_OK;
+}
+
+extern "C" int sim_set_state(sim_handle* H, int32_t inst, const double* x, const double* v) {
+    int rc = check_instance(H, inst);
+    if (rc) return rc;
+    for (int i = 0; i < 3 * H->n_v; ++i) {
+        if (x && !std::isfinite(x[i])) return fail(SIM_E_INVALID, "x not finite");
+        if (v && !std::isfinite(v[i])) return fail(SIM_E_INVALID, "v not finite");
+    }
+    std::vector<double4> hx(H->n_v), hv(H->n_v);
+    for (int i = 0; i < H->n_v; ++i) {
+        int o = H->int2orig[i];
+        if (x) hx[i] = make_double4(x[3 * o], x[3 * o + 1], x[3 * o + 2], 0.0);
+        if (v) hv[i] = make_double4(v[3 * o], v[3 * o + 1], v[3 * o + 2], 0.0);
+    }
+    CK(cudaStreamSynchronize(H->stream));
+    if (x) CK(copy_column_h2d(H, hx.data(), inst, H->x.p));
+    if (v) CK(copy_column_h2d(H, hv.data(), inst, H->v.p));
+    return SIM_OK;
+}
+
+extern "C" int sim_get_lambda(sim_handle* H, int32_t inst, double* lam, int32_t cap) {
+    int rc = check_instance(H, inst);
+    if (rc) return rc;
+    if (!lam) return fail(SIM_E_INVALID, "null argument");
+    if (H->dirty) return fail(SIM_E_STATE, "contacts changed since the last step");
+    const InstContacts& I = H->ic[inst];
+    const int nc = (int)I.hc.size();
+    int rows = 0;
+    for (int c = 0; c < nc; ++c) rows += I.hc[c].kind == 1 ? 1 : 3;
+    if (cap < rows) return fail(SIM_E_INVALID, "capacity %d < %d rows", cap, rows);
+    std::vector<double> l(3 * (size_t)nc);
+    CK(cudaStreamSynchronize(H->stream));
+    if (nc) CK(cudaMemcpy(l.data(), H->lam.p + 3 * (size_t)H->coff_h[inst], l.size() * sizeof(double),
+                          cudaMemcpyDeviceToHost));
     int r = 0;
-    for (int c = 0; c < H->nc; ++c) {
+    for (int c = 0; c < nc; ++c) {
         lam[r++] = l[3 * c];
-        if (H->hc[c].kind != 1) {
+        if (I.hc[c].kind != 1) {
             lam[r++] = l[3 * c + 1];
             lam[r++] = l[3 * c + 2];
         }
@@ -838,27 +1086,32 @@ extern "C" int sim_get_stats(sim_handle* H, sim_stats* o) {
     o->nnz_L = H->nnzL;
     o->etree_height = H->K.height;
     o->n_panels = H->K.panel_start.empty() ? 0 : (int)H->K.panel_start.size() - 1;
-    o->n_contacts = H->nc;
-    o->n_contact_vertices = H->ns;
+    o->n_instances = H->S;
+    int nc = 0, ns = 0;
+    for (auto& I : H->ic) { nc += (int)I.hc.size(); ns += (int)I.verts.size(); }
+    o->n_contacts = nc;
+    o->n_contact_vertices = ns;
     o->frames_done = H->frames_done;
     o->kernels_per_frame = H->kernels_per_frame;
     o->build_seconds = H->build_seconds;
     o->h2d_contact_bytes = H->h2d_contact_bytes;
     o->last_cr_residual = -1;
-    if (!H->host_only && H->state == 1 && H->nc > 0) {
+    if (!H->host_only && H->state == 1 && H->C > 0 && !H->dirty) {
         CK(cudaStreamSynchronize(H->stream));
-        double r;
-        CK(cudaMemcpy(&r, H->cr_res.p, sizeof r, cudaMemcpyDeviceToHost));
-        o->last_cr_residual = r;
-        std::vector<double> ph(H->nc), l(3 * (size_t)H->nc);
-        CK(cudaMemcpy(ph.data(), H->phi_abs.p, H->nc * sizeof(double), cudaMemcpyDeviceToHost));
+        std::vector<double> r(H->S), ph(H->C), l(3 * (size_t)H->C);
+        std::vector<DContact> hc(H->C);
+        CK(cudaMemcpy(r.data(), H->cr_res.p, H->S * sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ph.data(), H->phi_abs.p, H->C * sizeof(double), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(l.data(), H->lam.p, l.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        o->last_cr_residual = *std::max_element(r.begin(), r.end());
         double mx = 0;
         int act = 0;
-        for (int c = 0; c < H->nc; ++c) {
-            mx = std::max(mx, ph[c]);
-            act += (H->hc[c].kind == 0 && l[3 * c] > 0);
-        }
+        for (int i = 0; i < H->S; ++i)
+            for (int c = 0; c < (int)H->ic[i].hc.size(); ++c) {
+                const int g = H->coff_h[i] + c;
+                mx = std::max(mx, ph[g]);
+                act += (H->ic[i].hc[c].kind == 0 && l[3 * g] > 0);
+            }
         o->max_abs_phi_n = mx;
         o->n_active = act;
     }
@@ -879,44 +1132,43 @@ extern "C" int sim_debug_get_inverse(sim_handle* H, int32_t* perm, int32_t* pare
     return SIM_OK;
 }
 
+// b, x_out: [n_instances][n_vertices][3]
 extern "C" int sim_debug_apply_inverse(sim_handle* H, const double* b, double* xo) {
     if (!H || !b || !xo) return fail(SIM_E_INVALID, "null argument");
     if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
-    const int nf = H->n_f;
-    std::vector<float4> hu(nf);
-    for (int k = 0; k < nf; ++k) {
-        int o = H->int2orig[k];
-        int32_t cbk = (int32_t)(H->K.colptr[k] + H->K.depth[k]);
-        float cbf;
-        memcpy(&cbf, &cbk, sizeof cbf);
-        hu[k] = make_float4((float)b[3 * o], (float)b[3 * o + 1], (float)b[3 * o + 2], cbf);
-    }
+    const int nf = H->n_f, nv = H->n_v, S = H->S;
+    std::vector<float4> hu((size_t)nf * S);
+    for (int i = 0; i < S; ++i)
+        for (int k = 0; k < nf; ++k) {
+            const double* bb = b + ((size_t)i * nv + H->int2orig[k]) * 3;
+            hu[(size_t)k * S + i] = make_float4((float)bb[0], (float)bb[1], (float)bb[2], 0.f);
+        }
     DBuf<double4> dx;
-    CK(dx.alloc(nf));
+    CK(dx.alloc((size_t)nf * S));
     cudaStream_t st = H->stream;
     CK(cudaStreamSynchronize(st));
-    CK(cudaMemcpy(H->u.p, hu.data(), nf * sizeof(float4), cudaMemcpyHostToDevice));
-    CK(cudaMemset(dx.p, 0, nf * sizeof(double4)));
-    launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->T1.p, H->u.p, H->y.p, H->part1.p, H->counters.p);
-    launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->T2.p, H->y.p, dx.p, nullptr, nullptr, 1.0, 0);
+    CK(cudaMemcpy(H->u.p, hu.data(), hu.size() * sizeof(float4), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dx.p, 0, (size_t)nf * S * sizeof(double4)));
+    enqueue_kpass1(H, st);
+    enqueue_kpass2(H, st, dx.p, nullptr, nullptr, 1.0, 0);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
-    std::vector<double4> hx(nf);
-    CK(cudaMemcpy(hx.data(), dx.p, nf * sizeof(double4), cudaMemcpyDeviceToHost));
-    dx.release();
-    for (int i = 0; i < 3 * H->n_v; ++i) xo[i] = 0.0;
-    for (int k = 0; k < nf; ++k) {
-        int o = H->int2orig[k];
-        xo[3 * o] = hx[k].x;
-        xo[3 * o + 1] = hx[k].y;
-        xo[3 * o + 2] = hx[k].z;
-    }
+    std::vector<double4> hx((size_t)nf * S);
+    CK(cudaMemcpy(hx.data(), dx.p, hx.size() * sizeof(double4), cudaMemcpyDeviceToHost));
+    for (size_t q = 0; q < 3 * (size_t)nv * S; ++q) xo[q] = 0.0;
+    for (int i = 0; i < S; ++i)
+        for (int k = 0; k < nf; ++k) {
+            double* o = xo + ((size_t)i * nv + H->int2orig[k]) * 3;
+            const double4 a = hx[(size_t)k * S + i];
+            o[0] = a.x; o[1] = a.y; o[2] = a.z;
+        }
     return SIM_OK;
 }
 
 extern "C" int sim_debug_local(sim_handle* H, const double* x, const double* s, float* Pout, double* resid) {
     if (!H || !x || !s) return fail(SIM_E_INVALID, "null argument");
     if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
+    if (H->S != 1) return fail(SIM_E_STATE, "sim_debug_local needs a single-instance handle");
     const int nv = H->n_v, nf = H->n_f, nt = H->n_t;
     std::vector<double4> hx(nv), hs(nv);
     for (int i = 0; i < nv; ++i) {
@@ -934,8 +1186,7 @@ extern "C" int sim_debug_local(sim_handle* H, const double* x, const double* s, 
     CK(cudaMemcpy(ds.p, hs.data(), nv * sizeof(double4), cudaMemcpyHostToDevice));
     Params P = make_params(H);
     launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, dx.p, H->fc.p, dP.p);
-    launch_gather(st, P, H->adjp.p, H->adj.p, H->fc.p, H->M.p, dx.p, ds.p, nullptr, nullptr, nullptr, nullptr,
-                  H->cb.p, H->u.p, dr.p);
+    launch_gather(st, P, H->adjp.p, H->adj.p, H->fc.p, H->M.p, dx.p, ds.p, nullptr, slots(H), nullptr, H->u.p, dr.p);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     if (Pout) CK(cudaMemcpy(Pout, dP.p, (size_t)9 * nt * sizeof(float), cudaMemcpyDeviceToHost));
@@ -948,48 +1199,55 @@ extern "C" int sim_debug_local(sim_handle* H, const double* x, const double* s, 
             for (int d = 0; d < 3; ++d) resid[3 * o + d] = hr[3 * k + d];
         }
     }
-    dx.release(); ds.release(); dP.release(); dr.release();
     return SIM_OK;
 }
 
-extern "C" int sim_debug_get_delassus(sim_handle* H, int32_t* cv, float* G, int32_t cap) {
-    if (!H) return fail(SIM_E_INVALID, "null handle");
-    if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
-    if (cap < H->ns) return fail(SIM_E_INVALID, "capacity %d < %d contact vertices", cap, H->ns);
+extern "C" int sim_debug_get_delassus(sim_handle* H, int32_t inst, int32_t* cv, float* G, int32_t cap) {
+    int rc = check_instance(H, inst);
+    if (rc) return rc;
+    rc = commit_contacts(H);
+    if (rc) return rc;
+    const InstContacts& I = H->ic[inst];
+    const int ns = (int)I.verts.size();
+    if (cap < ns) return fail(SIM_E_INVALID, "capacity %d < %d contact vertices", cap, ns);
     CK(cudaStreamSynchronize(H->stream));
-    if (cv) for (int s = 0; s < H->ns; ++s) cv[s] = H->int2orig[H->slot_vtx_h[s]];
-    if (G && H->ns) {
-        std::vector<double> g((size_t)H->ns * H->ns);
-        CK(cudaMemcpy(g.data(), H->G.p, g.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        for (size_t q = 0; q < g.size(); ++q) G[q] = (float)g[q];
+    if (cv) for (int s = 0; s < ns; ++s) cv[s] = H->int2orig[I.verts[s]];
+    if (G && ns) {
+        int64_t go = 0;
+        for (int i = 0; i < inst; ++i) go += (int64_t)H->ic[i].verts.size() * H->ic[i].verts.size();
+        CK(cudaMemcpy(G, H->G.p + go, (size_t)ns * ns * sizeof(float), cudaMemcpyDeviceToHost));
     }
     return SIM_OK;
 }
 
 // contact scratch of the last evaluated L-G iteration: per row (3 per contact)
 // theta, C diagonal, h-vector; per slot dxt = (K^T y) at the slot vertex; slot vertices
-extern "C" int sim_debug_contact_state(sim_handle* H, double* theta, double* cdiag, double* hvec, double* dxt,
-                                       int32_t* slot_vertex, double* djj) {
-    if (!H) return fail(SIM_E_INVALID, "null handle");
-    if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
+extern "C" int sim_debug_contact_state(sim_handle* H, int32_t inst, double* theta, double* cdiag, double* hvec,
+                                       double* dxt, int32_t* slot_vertex, double* djj) {
+    int rc = check_instance(H, inst);
+    if (rc) return rc;
+    if (H->dirty) return fail(SIM_E_STATE, "contacts changed since the last step");
     CK(cudaStreamSynchronize(H->stream));
-    size_t m = 3 * (size_t)H->nc;
-    if (theta && m) CK(cudaMemcpy(theta, H->theta.p, m * sizeof(double), cudaMemcpyDeviceToHost));
-    if (cdiag && m) CK(cudaMemcpy(cdiag, H->cdiag.p, m * sizeof(double), cudaMemcpyDeviceToHost));
-    if (hvec && m) CK(cudaMemcpy(hvec, H->hvec.p, m * sizeof(double), cudaMemcpyDeviceToHost));
-    if (dxt && H->ns) CK(cudaMemcpy(dxt, H->dxt.p, 3 * (size_t)H->ns * sizeof(double), cudaMemcpyDeviceToHost));
-    if (slot_vertex) for (int s = 0; s < H->ns; ++s) slot_vertex[s] = H->int2orig[H->slot_vtx_h[s]];
-    if (djj && H->nc) {
-        std::vector<DContact> hc(H->nc);
-        CK(cudaMemcpy(hc.data(), H->dc.p, H->nc * sizeof(DContact), cudaMemcpyDeviceToHost));
-        for (int c = 0; c < H->nc; ++c) djj[c] = hc[c].Djj;
+    const InstContacts& I = H->ic[inst];
+    const int nc = (int)I.hc.size(), ns = (int)I.verts.size();
+    const size_t cb = H->coff_h[inst], sb = H->soff_h[inst];
+    size_t m = 3 * (size_t)nc;
+    if (theta && m) CK(cudaMemcpy(theta, H->theta.p + 3 * cb, m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (cdiag && m) CK(cudaMemcpy(cdiag, H->cdiag.p + 3 * cb, m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (hvec && m) CK(cudaMemcpy(hvec, H->hvec.p + 3 * cb, m * sizeof(double), cudaMemcpyDeviceToHost));
+    if (dxt && ns) CK(cudaMemcpy(dxt, H->dxt.p + 3 * sb, 3 * (size_t)ns * sizeof(double), cudaMemcpyDeviceToHost));
+    if (slot_vertex) for (int s = 0; s < ns; ++s) slot_vertex[s] = H->int2orig[I.verts[s]];
+    if (djj && nc) {
+        std::vector<DContact> hc(nc);
+        CK(cudaMemcpy(hc.data(), H->dc.p + cb, nc * sizeof(DContact), cudaMemcpyDeviceToHost));
+        for (int c = 0; c < nc; ++c) djj[c] = hc[c].Djj;
     }
     return SIM_OK;
 }
 
-// phase timestamps (ns, %globaltimer) of the most recent CR call: [0] start,
-// [1] after rho, [2] after active set + G_A gather, [3 + it] after CR iteration it,
-// [20] loop end, [21] epilogue end.  out must hold 32 values.
+// phase timestamps (ns, %globaltimer) of the most recent CR call (instance 0): [0] start,
+// [1] staged, [2] first reduction, [3 + it] after CR iteration it, [20] loop end,
+// [21] epilogue end.  out must hold 32 values.
 extern "C" int sim_debug_cr_timeline(sim_handle* H, double* out) {
     if (!H || !out) return fail(SIM_E_INVALID, "null argument");
     if (H->host_only) return fail(SIM_E_STATE, "no device");

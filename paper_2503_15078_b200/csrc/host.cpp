@@ -463,4 +463,68 @@ void build_tiles(const Inverse& K, WorkLists& wl, std::vector<float>& T1, std::v
     }
 }
 
+int build_batched(const Inverse& K, const WorkLists& wl, int unit_tiles, std::vector<BUnit>& u1,
+                  std::vector<float>& T1p, std::vector<BUnit>& u2, int& nblocks1) {
+    auto kval = [&](int r, int j) -> float {
+        if (j < K.first[r] || j > r) return 0.f;
+        return K.Krow[K.rowptr[r] + (j - K.first[r])];
+    };
+    u1.clear();
+    u2.clear();
+    int64_t ntot = 0;
+    for (auto& b : wl.p1b) {
+        const int c0 = K.first[b.r0], c1 = b.r0 + b.nrows;   // columns [c0, c1)
+        ntot += (c1 - c0 + 31) / 32;
+    }
+    T1p.assign(ntot * 1024, 0.f);
+    int64_t o = 0;
+    int nparts = 0;
+    nblocks1 = (int)wl.p1b.size();
+    for (int bi = 0; bi < (int)wl.p1b.size(); ++bi) {
+        const P1Block& b = wl.p1b[bi];
+        const int c0 = K.first[b.r0], c1 = b.r0 + b.nrows;
+        const int nt = (c1 - c0 + 31) / 32;
+        const int nu = (nt + unit_tiles - 1) / unit_tiles;
+        const int part0 = nu > 1 ? nparts : -1;
+        for (int u = 0; u < nu; ++u) {
+            BUnit U{};
+            U.r0 = b.r0;
+            U.nr = b.nrows;
+            U.c0 = c0 + 32 * unit_tiles * u;
+            U.ntiles = std::min(unit_tiles, nt - unit_tiles * u);
+            U.list0 = part0;
+            U.block = bi;
+            U.part = nu > 1 ? nparts++ : -1;
+            U.nparts = nu;
+            U.toff = o + (int64_t)1024 * unit_tiles * u;
+            u1.push_back(U);
+        }
+        for (int t = 0; t < nt; ++t)
+            for (int q = 0; q < 32; ++q) {
+                const int j = c0 + 32 * t + q;
+                if (j >= c1) break;
+                for (int l = 0; l < b.nrows; ++l) T1p[o + 1024LL * t + 32 * q + l] = kval(b.r0 + l, j);
+            }
+        o += 1024LL * nt;
+    }
+    // longest units first (the tail of each instance chunk is then short)
+    std::stable_sort(u1.begin(), u1.end(), [](const BUnit& a, const BUnit& b) { return a.ntiles > b.ntiles; });
+    for (auto& b : wl.p2b) {
+        BUnit U{};
+        U.r0 = b.c0;
+        U.nr = b.ncols;
+        U.c0 = b.c0;
+        U.nlist = b.list1 - b.list0;
+        U.ntiles = (U.nlist + 31) / 32;
+        U.list0 = b.list0;
+        U.block = -1;
+        U.part = -1;
+        U.nparts = 1;
+        U.toff = b.toff;
+        u2.push_back(U);
+    }
+    std::stable_sort(u2.begin(), u2.end(), [](const BUnit& a, const BUnit& b) { return a.ntiles > b.ntiles; });
+    return nparts;
+}
+
 }  // namespace simhost

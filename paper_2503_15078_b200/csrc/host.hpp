@@ -98,4 +98,16 @@ void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols);
 // Fills wl.p1[*].toff / wl.p2b[*].toff.
 void build_tiles(const Inverse& K, WorkLists& wl, std::vector<float>& T1, std::vector<float>& T2);
 
+// ---------------- batched K-passes (S instances share K) --------------------
+// A unit is one CTA's share of a pass for one chunk of instances:
+//   pass 1: rows r0..r0+nr-1 of one block x tiles [c0 + 32 t, +32), t < ntiles; tiles of the
+//           padded stream T1p, tile[q][l] = K[r0 + l][c0 + 32 t + q] (32 x 32, zero-padded);
+//           a block split over nparts units writes partials part..; list0 = the block's first part
+//   pass 2: columns c0..c0+nr-1, cover rows cover[list0 .. list0 + nlist), T2 tiles at toff
+struct BUnit { int32_t r0, nr, c0, ntiles, list0, nlist, block, part, nparts, pad; int64_t toff; };
+
+// unit_tiles: max tiles per pass-1 unit (bounds the longest CTA); returns the number of partials
+int build_batched(const Inverse& K, const WorkLists& wl, int unit_tiles, std::vector<BUnit>& u1,
+                  std::vector<float>& T1p, std::vector<BUnit>& u2, int& nblocks1);
+
 }  // namespace simhost

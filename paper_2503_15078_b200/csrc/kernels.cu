@@ -27,13 +27,13 @@ namespace simdev {
 // ----------------------------------------------------------------------------
 __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict__ xt,
                           double4* __restrict__ v, double4* __restrict__ s, double* __restrict__ lam, int nlam) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;   // (vertex, instance), instance-minor
     if (i < nlam) lam[i] = 0.0;   // lambda^0 = 0 (reading A10)
-    if (i >= P.n_v) return;
+    if (i >= P.n_v * P.S) return;
     double4 xi = x[i];
     xt[i] = xi;
     double h = P.h;
-    if (i < P.n_f) {
+    if (i < P.n_f * P.S) {
         double4 vi = v[i];
         double4 si = make_double4(xi.x + h * vi.x + h * h * P.g[0], xi.y + h * vi.y + h * h * P.g[1],
                                   xi.z + h * vi.z + h * h * P.g[2], 0.0);
@@ -47,8 +47,20 @@ __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict
 
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
                     double* lam, int nlam) {
-    int n = P.n_v > nlam ? P.n_v : nlam;
+    int n = P.n_v * P.S > nlam ? P.n_v * P.S : nlam;
     k_predict<<<(n + 255) / 256, 256, 0, st>>>(P, x, xt, v, s, lam, nlam);
+}
+
+// dst[e * S + i] = src[e] for every instance i (state initialisation)
+__global__ void k_replicate(const double4* __restrict__ src, double4* __restrict__ dst, int n, int S) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < (size_t)n * S) dst[i] = src[i / S];
+}
+
+void launch_replicate(cudaStream_t st, const double4* src, double4* dst, int n, int S) {
+    const size_t tot = (size_t)n * S;
+    if (tot == 0) return;
+    k_replicate<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, dst, n, S);
 }
 
 // ----------------------------------------------------------------------------
@@ -199,15 +211,18 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
     d[2] = p[2] - sg[2];
 }
 
-// one thread per tet: f_a = h^2 w (P - F) g_a, written per corner
+// one thread per (tet, instance), instance-minor: the instances of one tet share its rest
+// data (broadcast loads) and read consecutive state entries.  f_a = h^2 w (P - F) g_a per corner
 __global__ void __launch_bounds__(128) k_local(Params P, const int4* __restrict__ tet, const float* __restrict__ Bm,
                                                const float* __restrict__ hw2, const double4* __restrict__ x,
                                                float4* __restrict__ fc, float* __restrict__ Pdbg) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= P.n_t) return;
+    const int SI = P.S;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gt >= P.n_t * SI) return;
+    const int t = gt / SI, inst = gt - t * SI;
     const int nt = P.n_t;
     int4 tv = __ldg(&tet[t]);
-    double4 x0 = x[tv.x], x1 = x[tv.y], x2 = x[tv.z], x3 = x[tv.w];
+    double4 x0 = x[tv.x * SI + inst], x1 = x[tv.y * SI + inst], x2 = x[tv.z * SI + inst], x3 = x[tv.w * SI + inst];
     // Ds columns (fp64 differences, then fp32)
     float D[3][3];
     D[0][0] = (float)(x1.x - x0.x); D[1][0] = (float)(x1.y - x0.y); D[2][0] = (float)(x1.z - x0.z);
@@ -297,16 +312,16 @@ __global__ void __launch_bounds__(128) k_local(Params P, const int4* __restrict_
     for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int i = 0; i < 3; ++i) f[a][i] = Q[i][0] * B[3 * a + 0] + Q[i][1] * B[3 * a + 1] + Q[i][2] * B[3 * a + 2];
-    float4* o = fc + 4 * (size_t)t;
+    float4* o = fc + 4 * (size_t)t * SI + inst;   // [tet][corner][instance]
     o[0] = make_float4(-(f[0][0] + f[1][0] + f[2][0]), -(f[0][1] + f[1][1] + f[2][1]), -(f[0][2] + f[1][2] + f[2][2]), 0.f);
-    o[1] = make_float4(f[0][0], f[0][1], f[0][2], 0.f);
-    o[2] = make_float4(f[1][0], f[1][1], f[1][2], 0.f);
-    o[3] = make_float4(f[2][0], f[2][1], f[2][2], 0.f);
+    o[SI] = make_float4(f[0][0], f[0][1], f[0][2], 0.f);
+    o[2 * SI] = make_float4(f[1][0], f[1][1], f[1][2], 0.f);
+    o[3 * SI] = make_float4(f[2][0], f[2][1], f[2][2], 0.f);
 }
 
 void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
                   const double4* x, float4* fc, float* Pdbg) {
-    k_local<<<(P.n_t + 127) / 128, 128, 0, st>>>(P, tet, Bm, hw2, x, fc, Pdbg);
+    k_local<<<(P.n_t * P.S + 127) / 128, 128, 0, st>>>(P, tet, Bm, hw2, x, fc, Pdbg);
 }
 
 // ----------------------------------------------------------------------------
@@ -314,13 +329,14 @@ void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float
 // ----------------------------------------------------------------------------
 __global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const double4* __restrict__ x,
                                const double4* __restrict__ xt, ContactState cs) {
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= P.nc) return;
+    int c = blockIdx.x * blockDim.x + threadIdx.x;   // global contact id
+    if (c >= P.C) return;
     const DContact& ct = C[c];
     double h = P.h;
     double xc[3] = {0, 0, 0}, xtc[3] = {0, 0, 0};
     for (int q = 0; q < ct.nv; ++q) {
-        double4 a = x[ct.vtx[q]], b = xt[ct.vtx[q]];
+        const int iv = ct.vtx[q] * P.S + ct.inst;
+        double4 a = x[iv], b = xt[iv];
         xc[0] += ct.w[q] * a.x; xc[1] += ct.w[q] * a.y; xc[2] += ct.w[q] * a.z;
         xtc[0] += ct.w[q] * b.x; xtc[1] += ct.w[q] * b.y; xtc[2] += ct.w[q] * b.z;
     }
@@ -387,8 +403,8 @@ __global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const d
 
 void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, const double4* x,
                          const double4* xt, ContactState cs) {
-    if (P.nc == 0) return;
-    k_contact_eval<<<(P.nc + 127) / 128, 128, 0, st>>>(P, c, x, xt, cs);
+    if (P.C == 0) return;
+    k_contact_eval<<<(P.C + 127) / 128, 128, 0, st>>>(P, c, x, xt, cs);
 }
 
 // ----------------------------------------------------------------------------
@@ -397,19 +413,19 @@ void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, co
 // ----------------------------------------------------------------------------
 __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32_t* __restrict__ adj,
                          const float4* __restrict__ fc, const double* __restrict__ M, const double4* __restrict__ x,
-                         const double4* __restrict__ s, const int32_t* __restrict__ vcp,
-                         const int32_t* __restrict__ vci, const float* __restrict__ vcw,
-                         const double* __restrict__ hl, const int32_t* __restrict__ cb, float4* __restrict__ u,
-                         double* __restrict__ resid) {
-    int a = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= P.n_f) return;
-    double4 xa = x[a], sa = s[a];
+                         const double4* __restrict__ s, const int32_t* __restrict__ slotmap, Slots sl,
+                         const double* __restrict__ hl, float4* __restrict__ u, double* __restrict__ resid) {
+    const int S = P.S;
+    const int gi = blockIdx.x * blockDim.x + threadIdx.x;   // (free vertex, instance), instance-minor
+    if (gi >= P.n_f * S) return;
+    const int a = gi / S, inst = gi - a * S;
+    double4 xa = x[gi], sa = s[gi];
     double m = M[a];
     double r0 = m * (sa.x - xa.x), r1 = m * (sa.y - xa.y), r2 = m * (sa.z - xa.z);
     int p0 = adjp[a], p1 = adjp[a + 1];
     float f0 = 0.f, f1 = 0.f, f2 = 0.f;
     for (int p = p0; p < p1; ++p) {
-        float4 f = __ldg(&fc[adj[p]]);
+        float4 f = __ldg(&fc[(size_t)__ldg(&adj[p]) * S + inst]);
         f0 += f.x;
         f1 += f.y;
         f2 += f.z;
@@ -418,28 +434,30 @@ __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32
     r1 += f1;
     r2 += f2;
     if (resid) {
-        resid[3 * (size_t)a] = r0;
-        resid[3 * (size_t)a + 1] = r1;
-        resid[3 * (size_t)a + 2] = r2;
+        resid[3 * (size_t)gi] = r0;
+        resid[3 * (size_t)gi + 1] = r1;
+        resid[3 * (size_t)gi + 2] = r2;
     }
-    if (vcp) {
-        double hh = P.h * P.h;
-        for (int p = vcp[a]; p < vcp[a + 1]; ++p) {
-            int c = vci[p];
-            double w = vcw[p];
-            r0 += hh * w * hl[3 * c];
-            r1 += hh * w * hl[3 * c + 1];
-            r2 += hh * w * hl[3 * c + 2];
+    if (slotmap) {   // h^2 H^T Theta lambda at contact vertices (slot -> contacts, fixed order)
+        const int b = slotmap[gi];
+        if (b >= 0) {
+            double hh = P.h * P.h;
+            for (int p = sl.scp[b]; p < sl.scp[b + 1]; ++p) {
+                int c = sl.sci[p];
+                double w = sl.scw[p];
+                r0 += hh * w * hl[3 * c];
+                r1 += hh * w * hl[3 * c + 1];
+                r2 += hh * w * hl[3 * c + 2];
+            }
         }
     }
-    u[a] = make_float4((float)r0, (float)r1, (float)r2, __int_as_float(cb[a]));
+    u[gi] = make_float4((float)r0, (float)r1, (float)r2, 0.f);
 }
 
 void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
                    const float4* fc, const double* M, const double4* x, const double4* s,
-                   const int32_t* vcp, const int32_t* vci, const float* vcw, const double* hl,
-                   const int32_t* cb, float4* u, double* resid_dbg) {
-    k_gather<<<(P.n_f + 255) / 256, 256, 0, st>>>(P, adjp, adj, fc, M, x, s, vcp, vci, vcw, hl, cb, u, resid_dbg);
+                   const int32_t* slotmap, Slots sl, const double* hl, float4* u, double* resid_dbg) {
+    k_gather<<<(P.n_f * P.S + 255) / 256, 256, 0, st>>>(P, adjp, adj, fc, M, x, s, slotmap, sl, hl, u, resid_dbg);
 }
 
 // ----------------------------------------------------------------------------
@@ -797,20 +815,213 @@ void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_
 }
 
 // ----------------------------------------------------------------------------
+// Batched K-passes (S > 1 instances sharing K): every K tile is read once per chunk of
+// 128 instances and applied to 3 x 128 right-hand sides, so the passes become SpMM and
+// turn FP32-issue-bound instead of HBM-bound.  One CTA = (unit, instance chunk); the unit's
+// 32 x 32 K tiles and the matching 32 vector rows of the chunk (32 x 128 float4) are staged
+// by 1-D bulk copies (2 stages).  Warp w: outputs 16 (w & 1) .. +15, instances 32 (w >> 1) +
+// lane; per reduction index q it reads its 16 K values as 4 broadcast float4s and one
+// float4 of the vector.  fp32 FMAs per tile, folded into fp64 once per tile (as in S = 1).
+//   pass 1: out = rows of a block,    reduction over columns  (T1p, vector u, out y)
+//   pass 2: out = 32 columns,         reduction over cover rows (T2, vector y, out x += .)
+// Instances are the fastest grid dimension inside a unit chunk: chunk-major launch order
+// keeps one chunk's vectors (n_f x 128 x 16 B) resident in L2 while its units run.
+// ----------------------------------------------------------------------------
+constexpr int kBInst = 128;                 // instances per CTA
+constexpr int kBStages = 2;
+constexpr size_t kBStageBytes = 4096 + 32 * kBInst * 16;
+constexpr size_t kBSmem = kBStages * kBStageBytes;
+
+template <int PASS>
+__global__ void __launch_bounds__(256, 1)
+    k_kpass_b(int S, int n_f, const BUnit* __restrict__ units, const float* __restrict__ T,
+              const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
+              double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
+              const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v) {
+    extern __shared__ __align__(128) unsigned char bsm[];
+    __shared__ __align__(8) uint64_t full[kBStages];
+    __shared__ int s_last;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int half = w & 1, ig = w >> 1;
+    const BUnit U = units[blockIdx.x];
+    const int chunk = blockIdx.y;
+    const int i0 = chunk * kBInst;
+    const int ni = min(kBInst, S - i0);
+    const int li = 32 * ig + lane;           // instance within the chunk
+    const unsigned long long pol = l2_evict_first();
+    auto ktile = [&](int s) { return reinterpret_cast<float*>(bsm + s * kBStageBytes); };
+    auto vtile = [&](int s) { return reinterpret_cast<float4*>(bsm + s * kBStageBytes + 4096); };
+    // zero the vector tiles once: rows / instances that are never copied must read as 0
+    for (int e = threadIdx.x; e < kBStages * 32 * kBInst; e += blockDim.x)
+        vtile(e / (32 * kBInst))[e % (32 * kBInst)] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // zero fill before the bulk copies
+    __syncthreads();
+    auto nvalid = [&](int t) {   // vector rows present in tile t
+        if (PASS == 1) return max(0, min(32, n_f - (U.c0 + 32 * t)));
+        return min(32, U.nlist - 32 * t);
+    };
+    auto issue = [&](int t) {   // warp 0 only
+        const int s = t % kBStages;
+        const int nv = nvalid(t);
+        if (lane == 0) mbar_expect_tx(&full[s], 4096u + (unsigned)(nv * ni * 16));
+        __syncwarp();
+        if (lane == 0) bulk_g2s(ktile(s), T + U.toff + (int64_t)t * 1024, 4096u, &full[s], true, pol);
+        if (lane < nv) {
+            const int idx = PASS == 1 ? U.c0 + 32 * t + lane : __ldg(&cover[U.list0 + 32 * t + lane]);
+            bulk_g2s(vtile(s) + lane * kBInst, vin + (size_t)idx * S + i0, (unsigned)(ni * 16), &full[s], false, pol);
+        }
+    };
+    if (w == 0)
+        for (int t = 0; t < kBStages && t < U.ntiles; ++t) issue(t);
+    double d[16][3];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) d[r][0] = d[r][1] = d[r][2] = 0.0;
+    for (int t = 0; t < U.ntiles; ++t) {
+        const int s = t % kBStages;
+        mbar_wait(&full[s], (t / kBStages) & 1);
+        const float* kt = ktile(s) + 16 * half;
+        const float4* vt = vtile(s) + li;
+        float a[16][3];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) a[r][0] = a[r][1] = a[r][2] = 0.f;
+#pragma unroll 4
+        for (int q = 0; q < 32; ++q) {
+            const float4 vq = vt[q * kBInst];
+            const float4* kq = reinterpret_cast<const float4*>(kt + 32 * q);
+#pragma unroll
+            for (int r4 = 0; r4 < 4; ++r4) {
+                const float4 kk = kq[r4];
+                const float kv[4] = {kk.x, kk.y, kk.z, kk.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    a[4 * r4 + e][0] = fmaf(kv[e], vq.x, a[4 * r4 + e][0]);
+                    a[4 * r4 + e][1] = fmaf(kv[e], vq.y, a[4 * r4 + e][1]);
+                    a[4 * r4 + e][2] = fmaf(kv[e], vq.z, a[4 * r4 + e][2]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            d[r][0] += (double)a[r][0];
+            d[r][1] += (double)a[r][1];
+            d[r][2] += (double)a[r][2];
+        }
+        __syncthreads();   // every warp is done with stage s
+        if (w == 0 && t + kBStages < U.ntiles) issue(t + kBStages);
+    }
+    const bool live = li < ni;
+    const int inst = i0 + li;
+    if (PASS == 2) {
+        if (!live) return;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int l = 16 * half + r;
+            if (l < U.nr) {
+                const size_t j = (size_t)(U.c0 + l) * S + inst;
+                double4 xj = x[j];
+                xj.x += d[r][0];
+                xj.y += d[r][1];
+                xj.z += d[r][2];
+                x[j] = xj;
+                if (finalize_v) {   // v = (x - x_t) / h
+                    const double4 t0 = xt[j];
+                    v[j] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
+                }
+            }
+        }
+        return;
+    }
+    if (U.nparts == 1) {
+        if (!live) return;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int l = 16 * half + r;
+            if (l < U.nr)
+                yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)d[r][0], (float)d[r][1], (float)d[r][2], 0.f);
+        }
+        return;
+    }
+    // block split over several units: fp64 partials, combined in fixed order by the last unit
+    const size_t pstride = (size_t)32 * S;   // one (part, component) plane: [row][instance]
+    if (live) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int l = 16 * half + r;
+            double* pp = part + (size_t)U.part * 3 * pstride + (size_t)l * S + inst;
+            pp[0] = d[r][0];
+            pp[pstride] = d[r][1];
+            pp[2 * pstride] = d[r][2];
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int old = atomicAdd(&counters[U.block * nchunks + chunk], 1);
+        s_last = old == U.nparts - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (live) {
+        for (int r = 0; r < 16; ++r) {
+            const int l = 16 * half + r;
+            if (l >= U.nr) continue;
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            for (int q = 0; q < U.nparts; ++q) {
+                const double* pq = part + (size_t)(U.list0 + q) * 3 * pstride + (size_t)l * S + inst;
+                t0 += __ldcg(pq);
+                t1 += __ldcg(pq + pstride);
+                t2 += __ldcg(pq + 2 * pstride);
+            }
+            yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
+        }
+    }
+    if (threadIdx.x == 0) counters[U.block * nchunks + chunk] = 0;
+}
+
+void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1p,
+                           const float4* u, float4* y, double* part, int* counters) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_kpass_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
+        attr = true;
+    }
+    const int nch = (S + kBInst - 1) / kBInst;
+    k_kpass_b<1><<<dim3(nunits, nch), 256, kBSmem, st>>>(S, n_f, units, T1p, nullptr, u, y, part, counters, nch,
+                                                         nullptr, nullptr, nullptr, 0.0, 0);
+}
+
+void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
+                           const float* T2, const float4* y, double4* x, const double4* xt, double4* v,
+                           double inv_h, int finalize_v) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_kpass_b<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
+        attr = true;
+    }
+    const int nch = (S + kBInst - 1) / kBInst;
+    k_kpass_b<2><<<dim3(nunits, nch), 256, kBSmem, st>>>(S, n_f, units, T2, cover, y, nullptr, nullptr, nullptr, nch,
+                                                         x, xt, v, inv_h, finalize_v);
+}
+
+// ----------------------------------------------------------------------------
 // chain dot: dxt_s = (K^T y)_{a_s} = sum_{k} Kcol[colptr_a + k] y[chain_rows[off_s + k]]
 // (column a of K is contiguous in Kcol; its rows are a's ancestor chain)
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_chain_dot(int ns, const int32_t* __restrict__ slot_vtx,
-                                                   const float* __restrict__ Kcol, const int64_t* __restrict__ colptr,
+__global__ void __launch_bounds__(256) k_chain_dot(int S, const float* __restrict__ Kcol,
+                                                   const int64_t* __restrict__ colptr,
                                                    const int32_t* __restrict__ chain_off,
                                                    const int32_t* __restrict__ chain_rows, const float4* __restrict__ y,
-                                                   double* __restrict__ dxt, CrContacts cc,
-                                                   const double4* __restrict__ x, ContactState cs) {
-    // one CTA per contact vertex; its 8 warps take interleaved 128-entry slices of the chain
+                                                   Slots sl, CrContacts cc, const double4* __restrict__ x,
+                                                   ContactState cs) {
+    // one CTA per contact vertex (global slot); its 8 warps take interleaved 128-entry slices of the chain
     __shared__ double s_red[3][kWarps];
     const int s = blockIdx.x;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int a = slot_vtx[s];
+    const int a = sl.vtx[s];
+    const int inst = sl.inst[s];
     const float* col = Kcol + colptr[a];
     const int o0 = chain_off[s], len = chain_off[s + 1] - o0;
     double a0 = 0, a1 = 0, a2 = 0;
@@ -825,7 +1036,8 @@ __global__ void __launch_bounds__(256) k_chain_dot(int ns, const int32_t* __rest
         }
         float4 yy[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) yy[u] = rw[u] >= 0 ? __ldg(&y[rw[u]]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < 4; ++u)
+            yy[u] = rw[u] >= 0 ? __ldg(&y[(size_t)rw[u] * S + inst]) : make_float4(0.f, 0.f, 0.f, 0.f);
         float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -850,14 +1062,14 @@ __global__ void __launch_bounds__(256) k_chain_dot(int ns, const int32_t* __rest
         double t0 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
         for (int q = 0; q < kWarps; ++q) { t0 += s_red[0][q]; t1 += s_red[1][q]; t2 += s_red[2][q]; }
-        dxt[3 * s] = t0;
-        dxt[3 * s + 1] = t1;
-        dxt[3 * s + 2] = t2;
+        cs.dxt[3 * s] = t0;
+        cs.dxt[3 * s + 1] = t1;
+        cs.dxt[3 * s + 2] = t2;
         // Schur RHS rho = h - theta J x~, x~ = x^k + K^T y, for the single contact on this slot
         // (other contacts are handled in the CR prologue)
         const int c = cc.c1[s];
         if (c >= 0) {
-            const double4 xa = x[cc.v0[c]];
+            const double4 xa = x[(size_t)cc.v0[c] * S + inst];
             const double xs0 = xa.x + t0, xs1 = xa.y + t1, xs2 = xa.z + t2;
 #pragma unroll
             for (int kk = 0; kk < 3; ++kk) {
@@ -870,11 +1082,11 @@ __global__ void __launch_bounds__(256) k_chain_dot(int ns, const int32_t* __rest
     }
 }
 
-void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
-                      const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows,
-                      const float4* y, double* dxt, CrContacts cc, const double4* x, ContactState cs) {
-    if (ns == 0) return;
-    k_chain_dot<<<ns, 32 * kWarps, 0, st>>>(ns, slot_vtx, Kcol, colptr, chain_off, chain_rows, y, dxt, cc, x, cs);
+void launch_chain_dot(cudaStream_t st, const Params& P, const float* Kcol, const int64_t* colptr,
+                      const int32_t* chain_off, const int32_t* chain_rows, const float4* y, Slots sl,
+                      CrContacts cc, const double4* x, ContactState cs) {
+    if (P.NS == 0) return;
+    k_chain_dot<<<P.NS, 32 * kWarps, 0, st>>>(P.S, Kcol, colptr, chain_off, chain_rows, y, sl, cc, x, cs);
 }
 
 // ----------------------------------------------------------------------------
@@ -882,10 +1094,12 @@ void launch_chain_dot(cudaStream_t st, int ns, const int32_t* slot_vtx, const fl
 // ascending slot order, and the active block G_A of the Delassus Gram.  These depend only
 // on theta, so they run in a graph branch beside the RHS gather and K-pass 1.
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_active(int ns, CrContacts cc, const int32_t* __restrict__ scp,
-                                                 const int32_t* __restrict__ sci, ContactState cs, CrActive act) {
+__global__ void __launch_bounds__(1024) k_active(InstOff off, CrContacts cc, Slots sl, ContactState cs,
+                                                 CrActive act) {
     __shared__ int wsum[32];
     __shared__ int base;
+    const int inst = blockIdx.x;
+    const int sb = off.soff[inst], ns = off.soff[inst + 1] - sb, cb = off.coff[inst];
     if (threadIdx.x == 0) base = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -894,12 +1108,12 @@ __global__ void __launch_bounds__(1024) k_active(int ns, CrContacts cc, const in
         bool on = false;
         int only = -1;
         if (b < ns) {
-            only = cc.c1[b];
+            only = cc.c1[sb + b];
             if (only >= 0) {
                 on = cs.theta[3 * only] != 0.0 || cs.theta[3 * only + 1] != 0.0 || cs.theta[3 * only + 2] != 0.0;
             } else {
-                for (int q = scp[b]; q < scp[b + 1] && !on; ++q) {
-                    const int c = sci[q];
+                for (int q = sl.scp[sb + b]; q < sl.scp[sb + b + 1] && !on; ++q) {
+                    const int c = sl.sci[q];
                     on = cs.theta[3 * c] != 0.0 || cs.theta[3 * c + 1] != 0.0 || cs.theta[3 * c + 2] != 0.0;
                 }
             }
@@ -907,14 +1121,14 @@ __global__ void __launch_bounds__(1024) k_active(int ns, CrContacts cc, const in
         const unsigned bal = __ballot_sync(0xffffffffu, on);
         if (lane == 0) wsum[wid] = __popc(bal);
         __syncthreads();
-        int off = base;
-        for (int q = 0; q < wid; ++q) off += wsum[q];
-        off += __popc(bal & ((1u << lane) - 1u));
+        int pos = base;
+        for (int q = 0; q < wid; ++q) pos += wsum[q];
+        pos += __popc(bal & ((1u << lane) - 1u));
         if (b < ns) {
-            act.apos[b] = on ? off : -1;
+            act.apos[sb + b] = on ? pos : -1;
             if (on) {
-                act.aidx[off] = b;
-                act.acon[off] = only;
+                act.aidx[sb + pos] = b;
+                act.acon[sb + pos] = only >= 0 ? only - cb : -1;
             }
         }
         __syncthreads();
@@ -925,101 +1139,115 @@ __global__ void __launch_bounds__(1024) k_active(int ns, CrContacts cc, const in
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) act.na[0] = base;
+    if (threadIdx.x == 0) act.na[inst] = base;
 }
 
-__global__ void __launch_bounds__(256) k_gather_ga(int ns, const double* __restrict__ G, CrActive act,
-                                                   double* __restrict__ GA) {
-    const int na = act.na[0];
+// G_A[i][j] = G[aidx_i][aidx_j] (instance blockIdx.y, active row blockIdx.x)
+__global__ void __launch_bounds__(256) k_gather_ga(InstOff off, const float* __restrict__ G, CrActive act,
+                                                   float* __restrict__ GA) {
+    const int inst = blockIdx.y;
+    const int na = act.na[inst];
     const int i = blockIdx.x;
     if (i >= na) return;
-    const size_t row = (size_t)act.aidx[i] * ns;
-    for (int j = threadIdx.x; j < na; j += blockDim.x) GA[(size_t)i * na + j] = G[row + act.aidx[j]];
+    const int sb = off.soff[inst], ns = off.soff[inst + 1] - sb;
+    const float* Gi = G + off.goff[inst] + (size_t)act.aidx[sb + i] * ns;
+    float* GAi = GA + off.goff[inst] + (size_t)i * na;
+    for (int j = threadIdx.x; j < na; j += blockDim.x) GAi[j] = Gi[act.aidx[sb + j]];
 }
 
-void launch_active(cudaStream_t st, int ns, CrContacts cc, const int32_t* scp, const int32_t* sci, ContactState cs,
-                   CrActive act, const double* G, double* GA) {
-    if (ns == 0) return;
-    k_active<<<1, 1024, 0, st>>>(ns, cc, scp, sci, cs, act);
-    k_gather_ga<<<ns, 256, 0, st>>>(ns, G, act, GA);
+void launch_active(cudaStream_t st, const Params& P, InstOff off, CrContacts cc, Slots sl, ContactState cs,
+                   CrActive act, const float* G, float* GA) {
+    if (P.NS == 0) return;
+    k_active<<<P.S, 1024, 0, st>>>(off, cc, sl, cs, act);
+    k_gather_ga<<<dim3(P.ns_max, P.S), 256, 0, st>>>(off, G, act, GA);
 }
 
-// per-contact-set: chain rows of every slot (walk panel runs) + row flags
-__global__ void k_chain_rows(int ns, const int32_t* __restrict__ slot_vtx, const int32_t* __restrict__ chain_off,
+// per-contact-set: chain rows of every slot (walk panel runs), per-instance row flags, slot map
+__global__ void k_chain_rows(Params P, Slots sl, const int32_t* __restrict__ chain_off,
                              const int32_t* __restrict__ parent, const int32_t* __restrict__ ptop,
-                             int32_t* __restrict__ chain_rows, uint8_t* __restrict__ flag) {
+                             int32_t* __restrict__ chain_rows, uint8_t* __restrict__ flag,
+                             int32_t* __restrict__ slotmap) {
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (s >= ns) return;
+    if (s >= P.NS) return;
+    const int inst = sl.inst[s];
+    uint8_t* fl = flag + (size_t)inst * P.n_f;
+    if (lane == 0) slotmap[(size_t)sl.vtx[s] * P.S + inst] = s;
     int pos = chain_off[s];
-    for (int i = slot_vtx[s]; i >= 0;) {
+    for (int i = sl.vtx[s]; i >= 0;) {
         const int top = ptop[i];
         const int len = top - i + 1;
         for (int o = lane; o < len; o += 32) {
             chain_rows[pos + o] = i + o;
-            flag[i + o] = 1;
+            fl[i + o] = 1;
         }
         pos += len;
         i = parent[top];
     }
 }
 
-void launch_chain_rows(cudaStream_t st, int ns, const int32_t* slot_vtx, const int32_t* chain_off,
-                       const int32_t* parent, const int32_t* ptop, int32_t* chain_rows, uint8_t* flag) {
-    if (ns == 0) return;
-    k_chain_rows<<<(ns + 7) / 8, 256, 0, st>>>(ns, slot_vtx, chain_off, parent, ptop, chain_rows, flag);
+void launch_chain_rows(cudaStream_t st, const Params& P, Slots sl, const int32_t* chain_off, const int32_t* parent,
+                       const int32_t* ptop, int32_t* chain_rows, uint8_t* flag, int32_t* slotmap) {
+    if (P.NS == 0) return;
+    k_chain_rows<<<(P.NS + 7) / 8, 256, 0, st>>>(P, sl, chain_off, parent, ptop, chain_rows, flag, slotmap);
 }
 
-// rows on any chain, with the slot range in their subtree [first(i), i] and an
-// offset into the compact copy Zc of K[i][a_s], s in [s0, s1)
-__global__ void k_ulist(int n_f, int ns, const uint8_t* __restrict__ flag, const int32_t* __restrict__ slot_vtx,
+// rows on any chain of instance blockIdx.y, with the (global) slot range in their subtree
+// [first(i), i] and an offset into the compact copy Zc of K[i][a_s], s in [s0, s1)
+__global__ void k_ulist(int n_f, InstOff off, const uint8_t* __restrict__ flag, Slots sl,
                         const int2* __restrict__ meta, int* __restrict__ ucount, int4* __restrict__ ulist) {
+    const int inst = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_f || !flag[i]) return;
+    if (i >= n_f || !flag[(size_t)inst * n_f + i]) return;
+    const int sb = off.soff[inst], se = off.soff[inst + 1];
     const int f = meta[i].y;
-    int lo = 0, hi = ns;
-    while (lo < hi) { int m = (lo + hi) >> 1; if (slot_vtx[m] < f) lo = m + 1; else hi = m; }
+    int lo = sb, hi = se;
+    while (lo < hi) { int m = (lo + hi) >> 1; if (sl.vtx[m] < f) lo = m + 1; else hi = m; }
     const int s0 = lo;
-    hi = ns;
-    while (lo < hi) { int m = (lo + hi) >> 1; if (slot_vtx[m] <= i) lo = m + 1; else hi = m; }
+    hi = se;
+    while (lo < hi) { int m = (lo + hi) >> 1; if (sl.vtx[m] <= i) lo = m + 1; else hi = m; }
     // list order and offsets are arbitrary but each row's values stay contiguous
-    const int idx = atomicAdd(&ucount[0], 1);
-    const int off = atomicAdd(&ucount[1], lo - s0);
-    ulist[idx] = make_int4(i, s0, lo, off);
+    const int idx = atomicAdd(&ucount[2 * inst], 1);
+    const int o = atomicAdd(&ucount[2 * inst + 1], lo - s0);
+    ulist[off.uoff[inst] + idx] = make_int4(i, s0, lo, (int)(off.zoff[inst] + o));
 }
 
 // Zc[off + s - s0] = K[i][a_s]  (one warp per listed row)
-__global__ void k_zfill(const int* __restrict__ ucount, const int4* __restrict__ ulist,
-                        const int32_t* __restrict__ slot_vtx, const float* __restrict__ Krow,
-                        const int2* __restrict__ meta, float* __restrict__ Zc) {
+__global__ void k_zfill(InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist, Slots sl,
+                        const float* __restrict__ Krow, const int2* __restrict__ meta, float* __restrict__ Zc) {
+    const int inst = blockIdx.y;
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * (blockDim.x >> 5);
-    const int cnt = ucount[0];
+    const int cnt = ucount[2 * inst];
+    const int4* ul = ulist + off.uoff[inst];
     for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
-        const int4 u = ulist[e];
+        const int4 u = ul[e];
         const float* row = Krow + meta[u.x].x;
-        for (int s = u.y + lane; s < u.z; s += 32) Zc[u.w + s - u.y] = row[slot_vtx[s]];
+        for (int s = u.y + lane; s < u.z; s += 32) Zc[u.w + s - u.y] = row[sl.vtx[s]];
     }
 }
 
-void launch_ulist(cudaStream_t st, int n_f, int ns, const uint8_t* flag, const int32_t* slot_vtx,
-                  const int2* meta, int* ucount, int4* ulist, const float* Krow, float* Zc) {
-    if (ns == 0) return;
-    k_ulist<<<(n_f + 255) / 256, 256, 0, st>>>(n_f, ns, flag, slot_vtx, meta, ucount, ulist);
-    k_zfill<<<148 * 4, 256, 0, st>>>(ucount, ulist, slot_vtx, Krow, meta, Zc);
+void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* flag, Slots sl, const int2* meta,
+                  int* ucount, int4* ulist, const float* Krow, float* Zc) {
+    if (P.NS == 0) return;
+    k_ulist<<<dim3((P.n_f + 255) / 256, P.S), 256, 0, st>>>(P.n_f, off, flag, sl, meta, ucount, ulist);
+    const int gx = P.S >= 148 ? 4 : (148 * 4 + P.S - 1) / P.S;
+    k_zfill<<<dim3(gx, P.S), 256, 0, st>>>(off, ucount, ulist, sl, Krow, meta, Zc);
 }
 
 // ----------------------------------------------------------------------------
 // scatter (P:L956 correction, delta form): y_i += sum_{s0 <= s < s1} K[i][a_s] wz_s
-// for the rows i on the contact vertices' chains (warp per row, grid-stride)
+// for the rows i on the contact vertices' chains (warp per row, grid-stride per instance)
 // ----------------------------------------------------------------------------
-__global__ void k_scatter(const int* __restrict__ ucount, const int4* __restrict__ ulist,
+__global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist,
                           const float* __restrict__ Zc, const double* __restrict__ wz, float4* __restrict__ y) {
+    const int inst = blockIdx.y;
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * (blockDim.x >> 5);
-    const int cnt = ucount[0];
+    const int cnt = ucount[2 * inst];
+    const int4* ul = ulist + off.uoff[inst];
     for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
-        const int4 u = ulist[e];
+        const int4 u = ul[e];
         const float* zr = Zc + u.w - u.y;   // zr[s] = K[i][a_s]
         double a0 = 0, a1 = 0, a2 = 0;
         for (int s0 = u.y; s0 < u.z; s0 += 128) {   // 4 independent loads in flight per lane
@@ -1045,15 +1273,19 @@ __global__ void k_scatter(const int* __restrict__ ucount, const int4* __restrict
         a1 = warp_sum(a1);
         a2 = warp_sum(a2);
         if (lane == 0) {
-            const float4 yi = y[u.x];
-            y[u.x] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), yi.w);
+            const size_t iy = (size_t)u.x * S + inst;
+            const float4 yi = y[iy];
+            y[iy] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), yi.w);
         }
     }
 }
 
-void launch_scatter(cudaStream_t st, int max_rows, const int* ucount, const int4* ulist, const float* Zc,
-                    const double* wz, float4* y) {
-    k_scatter<<<(max_rows + 7) / 8, 256, 0, st>>>(ucount, ulist, Zc, wz, y);
+void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off, const int* ucount,
+                    const int4* ulist, const float* Zc, const double* wz, float4* y) {
+    if (P.NS == 0) return;
+    int gx = (max_rows + 7) / 8;
+    if (P.S > 1) gx = std::min(gx, std::max(1, (148 * 8 + P.S - 1) / P.S));
+    k_scatter<<<dim3(gx, P.S), 256, 0, st>>>(P.S, off, ucount, ulist, Zc, wz, y);
 }
 
 // ----------------------------------------------------------------------------
@@ -1074,12 +1306,17 @@ __device__ int lca_depth(int a, int b, const int32_t* parent, const int32_t* pto
     return -1;
 }
 
-__global__ void __launch_bounds__(256) k_delassus(int ns, const int32_t* __restrict__ slot_vtx,
+__global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __restrict__ vtx_all,
                                                   const float* __restrict__ Kcol, const int64_t* __restrict__ colptr,
                                                   const int32_t* __restrict__ depth, const int32_t* __restrict__ parent,
-                                                  const int32_t* __restrict__ ptop, double* __restrict__ G) {
-    // tile (bs, bt) with bt >= bs from a linear triangular index
+                                                  const int32_t* __restrict__ ptop, float* __restrict__ Gall) {
+    // instance blockIdx.y; tile (bs, bt) with bt >= bs from a linear triangular index
+    const int inst = blockIdx.y;
+    const int sb = off.soff[inst], ns = off.soff[inst + 1] - sb;
+    const int32_t* slot_vtx = vtx_all + sb;
+    float* G = Gall + off.goff[inst];
     const int tiles = (ns + 31) / 32;
+    if ((int)blockIdx.x >= tiles * (tiles + 1) / 2) return;
     int idx = blockIdx.x, bs = 0;
     while (idx >= tiles - bs) { idx -= tiles - bs; ++bs; }
     const int bt = bs + idx;
@@ -1151,35 +1388,38 @@ __global__ void __launch_bounds__(256) k_delassus(int ns, const int32_t* __restr
     for (int q = 0; q < 4; ++q) {
         const int t = bt * 32 + lt0 + q;
         if (s < ns && t < ns) {
-            G[(size_t)s * ns + t] = (double)acc[q];
-            G[(size_t)t * ns + s] = (double)acc[q];
+            G[(size_t)s * ns + t] = acc[q];
+            G[(size_t)t * ns + s] = acc[q];
         }
     }
 }
 
-void launch_delassus(cudaStream_t st, int ns, const int32_t* slot_vtx, const float* Kcol,
-                     const int64_t* colptr, const int32_t* depth, const int32_t* parent,
-                     const int32_t* ptop, double* G) {
-    if (ns == 0) return;
-    int tiles = (ns + 31) / 32;
-    int ntri = tiles * (tiles + 1) / 2;
-    k_delassus<<<ntri, 256, 0, st>>>(ns, slot_vtx, Kcol, colptr, depth, parent, ptop, G);
+void launch_delassus(cudaStream_t st, const Params& P, InstOff off, Slots sl, const float* Kcol,
+                     const int64_t* colptr, const int32_t* depth, const int32_t* parent, const int32_t* ptop,
+                     float* G) {
+    if (P.NS == 0) return;
+    const int tiles = (P.ns_max + 31) / 32;
+    const int ntri = tiles * (tiles + 1) / 2;
+    k_delassus<<<dim3(ntri, P.S), 256, 0, st>>>(off, sl.vtx, Kcol, colptr, depth, parent, ptop, G);
 }
 
 // D_jj = sum_{a,b in j} w_a w_b G_ab (unit directions; reading A18)
-__global__ void k_djj(int nc, int ns, DContact* C, const double* __restrict__ G) {
+__global__ void k_djj(int C, InstOff off, DContact* Cs, const float* __restrict__ G) {
     int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
-    DContact& ct = C[c];
+    if (c >= C) return;
+    DContact& ct = Cs[c];
+    const int sb = off.soff[ct.inst], ns = off.soff[ct.inst + 1] - sb;
+    const float* Gi = G + off.goff[ct.inst];
     double d = 0.0;
     for (int p = 0; p < ct.nv; ++p)
-        for (int q = 0; q < ct.nv; ++q) d += ct.w[p] * ct.w[q] * G[(size_t)ct.slot[p] * ns + ct.slot[q]];
+        for (int q = 0; q < ct.nv; ++q)
+            d += ct.w[p] * ct.w[q] * (double)Gi[(size_t)(ct.slot[p] - sb) * ns + (ct.slot[q] - sb)];
     ct.Djj = d;
 }
 
-void launch_djj(cudaStream_t st, int nc, int ns, DContact* c, const double* G) {
-    if (nc == 0) return;
-    k_djj<<<(nc + 127) / 128, 128, 0, st>>>(nc, ns, c, G);
+void launch_djj(cudaStream_t st, const Params& P, InstOff off, DContact* c, const float* G) {
+    if (P.C == 0) return;
+    k_djj<<<(P.C + 127) / 128, 128, 0, st>>>(P.C, off, c, G);
 }
 
 // ----------------------------------------------------------------------------
@@ -1219,24 +1459,33 @@ struct CrLayout {
     }
 };
 
-__device__ unsigned long long g_cr_clock[32];   // phase timestamps (ns) of the last CR call, rank 0
+__device__ unsigned long long g_cr_clock[32];   // phase timestamps (ns) of the last CR call, instance 0 rank 0
 __device__ __forceinline__ void cr_stamp(int i) {
-    if (threadIdx.x == 0 && cg::this_cluster().block_rank() == 0) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         g_cr_clock[i] = t;
     }
 }
 
+// one instance's view (local contact ids 0..nc-1, local slot ids 0..ns-1)
+struct CrInst {
+    const DContact* C;       // + cb   (slot[] global: subtract sb; vtx: state index vtx * S + inst)
+    const int32_t* scp;      // + sb   (values: global positions into sci)
+    const int32_t* sci;      // global (values: global contact ids: subtract cb)
+    const float* scw;
+    int cb, sb, S, inst;
+};
+
 struct CrCtx {
-    double *r, *W, *q, *red, *gA;
-    float *th, *cd, *c9;
+    double *r, *W, *q, *red;
+    float *gA, *th, *cd, *c9;
     int *s0, *aidx, *apos, *acon;
-    int na, ns, i0, i1, gA_smem;
+    int na, ns, i0, i1, gA_smem, csize;
     unsigned mbar;         // shared-window address of the 2 exchange mbarriers
     unsigned par0, par1;   // phase parity of each barrier
     int stamp;             // >= 0: fine-grained phase stamps of this apply at g_cr_clock[stamp..]
-    const double* GAg;     // G_A in global memory (fallback when this CTA's rows do not fit)
+    const float* GAg;      // G_A in global memory (fallback when this CTA's rows do not fit)
 };
 
 // single-barrier block sum of 3 doubles (red is double-buffered by the caller)
@@ -1253,9 +1502,7 @@ __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, doub
 
 // Ar = S r for this thread's rows (registers); r is read from shared memory
 template <int kRpt>
-__device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m, const DContact* __restrict__ C,
-                                         const int32_t* __restrict__ scp, const int32_t* __restrict__ sci,
-                                         const float* __restrict__ scw, int buf, double (&Ar)[kRpt]) {
+__device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int buf, double (&Ar)[kRpt]) {
     const int na = X.na;
     double* qb = X.q + (size_t)buf * 3 * X.ns;   // SoA: q0 | q1 | q2
     const unsigned bar = X.mbar + 8u * (unsigned)buf;
@@ -1275,9 +1522,9 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
             }
         } else {
             const int b = X.aidx[i];
-            for (int p = __ldg(&scp[b]); p < __ldg(&scp[b + 1]); ++p) {
-                const int c = __ldg(&sci[p]);
-                const double wt = __ldg(&scw[p]);
+            for (int p = __ldg(&I.scp[b]); p < __ldg(&I.scp[b + 1]); ++p) {
+                const int c = __ldg(&I.sci[p]) - I.cb;
+                const double wt = __ldg(&I.scw[p]);
                 const float* cc = X.c9 + 9 * c;
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
@@ -1296,14 +1543,14 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
     if (X.stamp >= 0) cr_stamp(X.stamp);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int i = X.i0 + wid; i < X.i1; i += nw) {
-        const double* g = X.gA_smem ? X.gA + (size_t)(i - X.i0) * na : X.GAg + (size_t)i * na;
+        const float* g = X.gA_smem ? X.gA + (size_t)(i - X.i0) * na : X.GAg + (size_t)i * na;
         double d0 = 0, d1 = 0, d2 = 0;
         for (int b0 = 0; b0 < na; b0 += 128) {
             double gv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int bb = b0 + 32 * u + lane;
-                gv[u] = bb < na ? (X.gA_smem ? g[bb] : __ldcg(&g[bb])) : 0.0;
+                gv[u] = bb < na ? (double)(X.gA_smem ? g[bb] : __ldcg(&g[bb])) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -1316,8 +1563,8 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
         d0 = warp_sum(d0);
         d1 = warp_sum(d1);
         d2 = warp_sum(d2);
-        if (lane < kCluster) {
-            // asynchronous stores of q_i into CTA `lane`, completing 24 tx bytes on its mbarrier
+        if (lane < X.csize) {
+            // asynchronous stores of q_i into CTA `lane` of the cluster, completing 24 tx bytes on its mbarrier
             const unsigned l0 = (unsigned)__cvta_generic_to_shared(qb + i);
             const unsigned l1 = (unsigned)__cvta_generic_to_shared(qb + na + i);
             const unsigned l2 = (unsigned)__cvta_generic_to_shared(qb + 2 * na + i);
@@ -1365,9 +1612,9 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
                 const int ip = X.apos[sl0];
                 acc = (double)cc[0] * qb[ip] + (double)cc[1] * qb[na + ip] + (double)cc[2] * qb[2 * na + ip];
             } else {
-                const DContact& ct = C[c];
+                const DContact& ct = I.C[c];
                 for (int p = 0; p < ct.nv; ++p) {
-                    const int ip = X.apos[ct.slot[p]];
+                    const int ip = X.apos[ct.slot[p] - I.sb];
                     acc += ct.w[p] * ((double)cc[0] * qb[ip] + (double)cc[1] * qb[na + ip] +
                                       (double)cc[2] * qb[2 * na + ip]);
                 }
@@ -1377,17 +1624,35 @@ __device__ __forceinline__ void cr_apply(cg::cluster_group& cl, CrCtx& X, int m,
     }
 }
 
+// One cluster of csize CTAs per instance (csize = 16 for a single scene, fewer when many
+// instances fill the GPU).  Launched with a runtime cluster dimension (cudaLaunchKernelEx).
 template <int kRpt>
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1)
-    k_cr(Params P, const DContact* __restrict__ C, CrContacts cc, const int32_t* __restrict__ scp,
-         const int32_t* __restrict__ sci, const float* __restrict__ scw, const double* __restrict__ GA,
-         const double4* __restrict__ x, ContactState cs, CrActive act, int gA_cap) {
+__global__ void __launch_bounds__(kCrThreads, 1)
+    k_cr(Params P, InstOff off, const DContact* __restrict__ C, CrContacts cc, Slots sl,
+         const float* __restrict__ GA, const double4* __restrict__ x, ContactState cs, CrActive act) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    const CrLayout L(P.nc, P.ns);
     cg::cluster_group cl = cg::this_cluster();
-    const int nc = P.nc, ns = P.ns, m = 3 * nc;
+    const int csize = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+    const int inst = blockIdx.x / csize;
+    const int cb = off.coff[inst], nc = off.coff[inst + 1] - cb;
+    const int sb = off.soff[inst], ns = off.soff[inst + 1] - sb;
+    if (nc == 0) {   // uniform over the cluster
+        if (threadIdx.x == 0 && rank == 0) cs.cr_res[inst] = 0.0;
+        return;
+    }
+    const CrLayout L(nc, ns);
+    const int m = 3 * nc;
     const double h = P.h;
+    const int S = P.S;
     cr_stamp(0);
+    CrInst I{C + cb, sl.scp + sb, sl.sci, sl.scw, cb, sb, S, inst};
+    double* th_g = cs.theta + 3 * cb;
+    double* cd_g = cs.cdiag + 3 * cb;
+    double* rho_g = cs.rho + 3 * cb;
+    double* hv_g = cs.hvec + 3 * cb;
+    double* lam_g = cs.lam + 3 * cb;
+    const double* dxt_g = cs.dxt + 3 * sb;
+    double* wz_g = cs.wz + 3 * sb;
     CrCtx X;
     X.r = (double*)(smraw + L.r);
     X.th = (float*)(smraw + L.th);
@@ -1400,31 +1665,38 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
     X.apos = (int*)(smraw + L.apos);
     X.acon = (int*)(smraw + L.acon);
     X.red = (double*)(smraw + L.red);
-    X.gA = (double*)(smraw + L.gA);
+    X.gA = (float*)(smraw + L.gA);
     X.mbar = (unsigned)__cvta_generic_to_shared(smraw + L.mbar);
     X.par0 = X.par1 = 0u;
     X.stamp = -1;
     X.ns = ns;
-    X.GAg = GA;
+    X.csize = csize;
+    X.GAg = GA + off.goff[inst];
     // everything the prologue needs is precomputed (chain dot, k_active): plain loads only
-    for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[e], true);
-    for (int c = threadIdx.x; c < nc; c += blockDim.x) cp_async4(&X.s0[c], &cc.s0[c], true);
+    for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[9 * cb + e], true);
     for (int b = threadIdx.x; b < ns; b += blockDim.x) {
-        cp_async4(&X.aidx[b], &act.aidx[b], true);
-        cp_async4(&X.apos[b], &act.apos[b], true);
-        cp_async4(&X.acon[b], &act.acon[b], true);
+        cp_async4(&X.aidx[b], &act.aidx[sb + b], true);
+        cp_async4(&X.apos[b], &act.apos[sb + b], true);
+        cp_async4(&X.acon[b], &act.acon[sb + b], true);
     }
     cp_async_commit();
-    const int na = act.na[0];
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+        const int s0g = cc.s0[cb + c];
+        X.s0[c] = s0g >= 0 ? s0g - sb : -1;
+    }
+    const int na = act.na[inst];
     X.na = na;
     {
-        const int per = (na + kCluster - 1) / kCluster;
-        X.i0 = min(na, (int)cl.block_rank() * per);
+        const int per = (na + csize - 1) / csize;
+        X.i0 = min(na, rank * per);
         X.i1 = min(na, X.i0 + per);
-        X.gA_smem = (size_t)(X.i1 - X.i0) * na <= (size_t)gA_cap;
-        if (X.gA_smem)
-            for (int e = threadIdx.x; e < (X.i1 - X.i0) * na; e += blockDim.x)
-                X.gA[e] = __ldcg(&GA[(size_t)X.i0 * na + e]);
+        const size_t cap = (kCrMaxSmem - L.total) / sizeof(float);
+        X.gA_smem = (size_t)(X.i1 - X.i0) * na <= cap;
+        if (X.gA_smem) {
+            const float* src = X.GAg + (size_t)X.i0 * na;
+            const int n = (X.i1 - X.i0) * na;
+            for (int e = threadIdx.x; e < n; e += blockDim.x) X.gA[e] = __ldcg(&src[e]);
+        }
     }
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
 #pragma unroll
@@ -1433,25 +1705,25 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
         const int j = threadIdx.x + kCrThreads * k;
         if (j < m) {
             const int c = j / 3;
-            const double th = cs.theta[j];
-            double rho = cs.rho[j];
-            const int v0 = __ldg(&cc.v0[c]);
-            const bool viaSlot = v0 >= 0 && __ldg(&cc.c1[__ldg(&cc.s0[c])]) == c;
+            const double th = th_g[j];
+            double rho = rho_g[j];
+            const int v0 = __ldg(&cc.v0[cb + c]);
+            const bool viaSlot = v0 >= 0 && __ldg(&cc.c1[__ldg(&cc.s0[cb + c])]) == cb + c;
             if (!viaSlot) {   // rho of contacts the chain dot did not cover
                 const int kk = j - 3 * c;
-                const DContact& ct = C[c];
+                const DContact& ct = I.C[c];
                 double xs0 = 0.0, xs1 = 0.0, xs2 = 0.0;
                 for (int q = 0; q < ct.nv; ++q) {
-                    const double4 xa = x[ct.vtx[q]];
-                    const int sl = ct.slot[q];
-                    xs0 += ct.w[q] * (xa.x + cs.dxt[3 * sl]);
-                    xs1 += ct.w[q] * (xa.y + cs.dxt[3 * sl + 1]);
-                    xs2 += ct.w[q] * (xa.z + cs.dxt[3 * sl + 2]);
+                    const double4 xa = x[(size_t)ct.vtx[q] * S + inst];
+                    const int slq = ct.slot[q] - sb;
+                    xs0 += ct.w[q] * (xa.x + dxt_g[3 * slq]);
+                    xs1 += ct.w[q] * (xa.y + dxt_g[3 * slq + 1]);
+                    xs2 += ct.w[q] * (xa.z + dxt_g[3 * slq + 2]);
                 }
-                rho = cs.hvec[j] - th * (ct.c[kk][0] * xs0 + ct.c[kk][1] * xs1 + ct.c[kk][2] * xs2);
+                rho = hv_g[j] - th * (ct.c[kk][0] * xs0 + ct.c[kk][1] * xs1 + ct.c[kk][2] * xs2);
             }
             X.th[j] = (float)th;
-            X.cd[j] = (float)cs.cdiag[j];
+            X.cd[j] = (float)cd_g[j];
             X.r[j] = rho;
             p[k] = rho;
         }
@@ -1464,7 +1736,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
     }
     cl.sync();   // smem staged everywhere; every CTA's exchange mbarriers initialised
     cr_stamp(1);
-    if (threadIdx.x == 0 && cl.block_rank() == 0) g_cr_clock[31] = g_cr_clock[0] + 1000ull * na;   // na (debug)
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_cr_clock[31] = g_cr_clock[0] + 1000ull * na;   // na (debug)
     double rr = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) rr = fma(p[k], p[k], rr);
@@ -1474,7 +1746,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
     cr_stamp(2);
     if (rr > 0.0 && P.cr_iters > 0) {
         int buf = 0;
-        cr_apply<kRpt>(cl, X, m, C, scp, sci, scw, buf, Ar);
+        cr_apply<kRpt>(X, m, I, buf, Ar);
         buf ^= 1;
         double rAr = 0.0, ApAp = 0.0, dummy = 0.0;
 #pragma unroll
@@ -1503,7 +1775,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
             if (it == P.cr_iters - 1) break;
             X.stamp = it == 3 ? 13 : -1;
             if (it == 3) cr_stamp(12);
-            cr_apply<kRpt>(cl, X, m, C, scp, sci, scw, buf, Ar);
+            cr_apply<kRpt>(X, m, I, buf, Ar);
             buf ^= 1;
             if (it == 3) cr_stamp(16);
             double s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -1542,28 +1814,27 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
     cr_stamp(27);
     // epilogue split over the cluster (every CTA holds the identical z):
     // lambda += z / h^2 (reading A11) for this CTA's rows; z to shared memory (reuse r)
-    const int rank = cl.block_rank();
-    const int rper = (m + kCluster - 1) / kCluster;
+    const int rper = (m + csize - 1) / csize;
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) {
         const int j = threadIdx.x + kCrThreads * k;
         if (j < m) {
             X.r[j] = z[k];
-            if (j / rper == rank) cs.lam[j] += z[k] / (h * h);
+            if (j / rper == rank) lam_g[j] += z[k] / (h * h);
         }
     }
     __syncthreads();
     cr_stamp(28);
     // wz_b = sum w theta z c  (for y += K H^T z), this CTA's slots
-    const int sper = (ns + kCluster - 1) / kCluster;
+    const int sper = (ns + csize - 1) / csize;
     for (int b = rank * sper + threadIdx.x; b < min(ns, (rank + 1) * sper); b += blockDim.x) {
         double w0 = 0, w1 = 0, w2 = 0;
-        const int only = __ldg(&cc.c1[b]);
-        const int qa = only >= 0 ? 0 : scp[b], qb = only >= 0 ? 1 : scp[b + 1];
+        const int onlyg = __ldg(&cc.c1[sb + b]);
+        const int qa = onlyg >= 0 ? 0 : I.scp[b], qb = onlyg >= 0 ? 1 : I.scp[b + 1];
         for (int q = qa; q < qb; ++q) {
-            const int c = only >= 0 ? only : sci[q];
-            const double wt = only >= 0 ? 1.0 : (double)scw[q];
+            const int c = onlyg >= 0 ? onlyg - cb : sl.sci[q] - cb;
+            const double wt = onlyg >= 0 ? 1.0 : (double)sl.scw[q];
             const float* c9 = X.c9 + 9 * c;
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
@@ -1573,11 +1844,11 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kCrThreads, 1
                 w2 += tv * (double)c9[3 * k + 2];
             }
         }
-        cs.wz[3 * b] = w0;
-        cs.wz[3 * b + 1] = w1;
-        cs.wz[3 * b + 2] = w2;
+        wz_g[3 * b] = w0;
+        wz_g[3 * b + 1] = w1;
+        wz_g[3 * b + 2] = w2;
     }
-    if (threadIdx.x == 0 && rank == 0) cs.cr_res[0] = sqrt(res);
+    if (threadIdx.x == 0 && rank == 0) cs.cr_res[inst] = sqrt(res);
     cr_stamp(21);
     // no trailing cluster barrier: after its last exchange wait no CTA touches a peer's shared memory
 }
@@ -1588,10 +1859,15 @@ int read_cr_clock(unsigned long long* out) {
 
 size_t cr_smem_bytes(int nc, int ns) { return CrLayout(nc, ns).total; }
 
-int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc, const int32_t* scp,
-              const int32_t* sci, const float* scw, const double* GA, const double4* x, ContactState cs,
-              CrActive act) {
-    if (P.nc == 0) return 0;
+int cr_cluster_size(int S) {
+    int c = kCluster;
+    while (c > 1 && c * S > 148) c >>= 1;   // enough CTAs per instance to fill the GPU, no more
+    return c;
+}
+
+int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, CrContacts cc, Slots sl,
+              const float* GA, const double4* x, ContactState cs, CrActive act) {
+    if (P.C == 0) return 0;
     static bool attr = false;
     if (!attr) {
         void* fns[kRptMax] = {(void*)k_cr<1>, (void*)k_cr<2>, (void*)k_cr<3>, (void*)k_cr<4>, (void*)k_cr<5>, (void*)k_cr<6>};
@@ -1603,20 +1879,31 @@ int launch_cr(cudaStream_t st, const Params& P, const DContact* c, CrContacts cc
         }
         attr = true;
     }
-    const size_t base = cr_smem_bytes(P.nc, P.ns);
-    const int cap = (int)((kCrMaxSmem - base) / sizeof(double));
-    const int rpt = (3 * P.nc + kCrThreads - 1) / kCrThreads;
-#define CRL(R) k_cr<R><<<kCluster, kCrThreads, kCrMaxSmem, st>>>(P, c, cc, scp, sci, scw, GA, x, cs, act, cap)
+    const int csize = cr_cluster_size(P.S);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.S * csize, 1, 1);
+    cfg.blockDim = dim3(kCrThreads, 1, 1);
+    cfg.dynamicSmemBytes = kCrMaxSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int rpt = (3 * P.nc_max + kCrThreads - 1) / kCrThreads;
+    cudaError_t e;
     switch (rpt) {
-        case 1: CRL(1); break;
-        case 2: CRL(2); break;
-        case 3: CRL(3); break;
-        case 4: CRL(4); break;
-        case 5: CRL(5); break;
-        default: CRL(6); break;
+        case 0:
+        case 1: e = cudaLaunchKernelEx(&cfg, k_cr<1>, P, off, c, cc, sl, GA, x, cs, act); break;
+        case 2: e = cudaLaunchKernelEx(&cfg, k_cr<2>, P, off, c, cc, sl, GA, x, cs, act); break;
+        case 3: e = cudaLaunchKernelEx(&cfg, k_cr<3>, P, off, c, cc, sl, GA, x, cs, act); break;
+        case 4: e = cudaLaunchKernelEx(&cfg, k_cr<4>, P, off, c, cc, sl, GA, x, cs, act); break;
+        case 5: e = cudaLaunchKernelEx(&cfg, k_cr<5>, P, off, c, cc, sl, GA, x, cs, act); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_cr<6>, P, off, c, cc, sl, GA, x, cs, act); break;
     }
-#undef CRL
-    return (int)cudaGetLastError();
+    return (int)e;
 }
 
 }  // namespace simdev

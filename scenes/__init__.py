@@ -28,7 +28,7 @@ import numpy as np
 __all__ = [
     "Mesh", "Material", "Contact", "Scene",
     "hex_grid", "cantilever", "incline_block", "gingerbread", "single_tet",
-    "tangent_frame", "make_scene", "random_state",
+    "tangent_frame", "make_scene", "random_state", "batch_instance", "batch_instance_params",
 ]
 
 NEOHOOKEAN, COROTATED, ARAP = 0, 1, 2
@@ -320,3 +320,22 @@ def random_state(mesh: Mesh, seed: int, amp: float = 0.1):
     x = mesh.X + amp * cell * rng.standard_normal(mesh.X.shape)
     v = 0.05 * rng.standard_normal(mesh.X.shape)
     return x, v
+
+
+def batch_instance_params(scene: Scene, i: int, v_sigma: float = 0.01, offset: float = 0.005):
+    """cfg5 instance i (seed 1000 + i): initial velocity
+    ~ N(0, v_sigma^2) per free-vertex component and an obstacle shift
+    delta ~ U(-offset, offset) along z.  Returns (v0 [n_v, 3], delta)."""
+    rng = np.random.default_rng(1000 + i)
+    v0 = v_sigma * rng.standard_normal(scene.mesh.X.shape)
+    v0[scene.mesh.fixed.astype(bool)] = 0.0
+    return v0, float(rng.uniform(-offset, offset))
+
+
+def batch_instance(scene: Scene, i: int, v_sigma: float = 0.01, offset: float = 0.005):
+    """cfg5 instance i of a scene: batch_instance_params, with the obstacles
+    shifted by delta along z, i.e. every contact's d_n grows by n . (0, 0, delta).
+    Returns (v0 [n_v, 3], contacts)."""
+    v0, delta = batch_instance_params(scene, i, v_sigma, offset)
+    cs = [dataclasses.replace(c, offset=float(c.offset + c.normal[2] * delta)) for c in scene.contacts]
+    return v0, cs

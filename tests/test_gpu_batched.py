@@ -1,0 +1,152 @@
+"""Batched instances (BASELINE config 5): S scenes share mesh,
+material and K; every instance of one handle must match the fp64 oracle run on
+that instance alone, at the single-scene tolerances (BASELINE.json north_star):
+per-SpMV 1e-5 relative, positions 1e-5 x bbox diagonal per frame, identical
+stick/slip classification.  All calls go through the C ABI.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import scenes
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def simmod():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_15078_b200 as m
+    return m
+
+
+def make(simmod, sc, S):
+    return simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, n_instances=S)
+
+
+def test_batched_apply_inverse_cfg3(simmod):
+    """Batched K-passes (SpMM over 3 S right-hand sides) == A^-1 b per instance.
+    S = 130 spans two 128-instance chunks, the second one partial."""
+    sc = scenes.make_scene("cfg3")
+    S = 130
+    s = make(simmod, sc, S)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal((S, sc.mesh.n_v, 3)).astype(np.float32).astype(np.float64)
+    x = s.debug_apply_inverse(b)
+    for i in (0, 1, 31, 32, 100, 127, 128, 129):
+        xr = o.solve(b[i][o.free])
+        err = np.abs(x[i][o.free] - xr).max() / np.abs(xr).max()
+        assert err < 1e-5, (i, err)
+        assert np.all(x[i][o.pinned] == 0)
+
+
+@pytest.mark.parametrize("S", [2, 33])
+def test_batched_apply_inverse_small(simmod, S):
+    """Small and non-multiple-of-32 instance counts on a 5k-DoF block."""
+    sc = scenes.make_scene("block", nv=7, split="kuhn6")
+    s = make(simmod, sc, S)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    rng = np.random.default_rng(S)
+    b = rng.standard_normal((S, sc.mesh.n_v, 3)).astype(np.float32).astype(np.float64)
+    x = s.debug_apply_inverse(b)
+    for i in range(S):
+        xr = o.solve(b[i][o.free])
+        assert np.abs(x[i][o.free] - xr).max() < 1e-5 * np.abs(xr).max(), i
+
+
+def test_batched_incline_instances(simmod):
+    """Three incline instances on one handle: stick (mu* + 0.05), slip
+    (mu* - 0.05) and no contact at all.  Each frame the oracle restarts from the
+    instance's GPU state (re-synced, as in the single-scene test)."""
+    th = 10.0
+    mus = math.tan(math.radians(th))
+    scs = [scenes.incline_block(theta_deg=th, mu=mus + d, nv=5, edge=0.1, youngs=1e8) for d in (0.05, -0.05)]
+    base = scs[0]
+    S = 3
+    s = make(simmod, base, S)
+    contacts = [scs[0].contacts, scs[1].contacts, []]
+    for i in range(S):
+        s.set_contacts(contacts[i], instance=i)
+    ors = []
+    for i in range(S):
+        o = O.Oracle(base.mesh, base.material, base.h, lg_iters=5)
+        if contacts[i]:
+            o.set_contacts(contacts[i])
+        ors.append(o)
+    tol = 1e-5 * base.mesh.bbox_diag()
+    xs = [base.mesh.X.copy() for _ in range(S)]
+    vs = [np.zeros_like(base.mesh.X) for _ in range(S)]
+    for f in range(5):
+        for i in range(S):
+            s.set_state(xs[i], vs[i], instance=i)
+        s.step(1, 5)
+        for i in range(S):
+            xg, vg = s.get_state(instance=i)
+            xo, vo, info = ors[i].frame(xs[i], vs[i])
+            assert np.abs(xg - xo).max() < tol, (f, i, np.abs(xg - xo).max())
+            if contacts[i]:
+                lg = s.get_lambda(instance=i)
+                assert np.array_equal(ors[i].classify(xo, xs[i], info["lam"]), ors[i].classify(xg, xs[i], lg))
+            xs[i], vs[i] = xg, vg
+
+
+def test_batched_gingerbread_cfg5(simmod):
+    """cfg5 structure on cfg3: 4 instances with their own initial velocities and
+    obstacle offsets (scenes.batch_instance), contacts set in one batch call;
+    one frame per instance against the oracle."""
+    sc = scenes.make_scene("cfg3")
+    S = 4
+    s = make(simmod, sc, S)
+    s.set_pin_velocity(sc.pin_velocity)
+    inst = [scenes.batch_instance(sc, i) for i in range(S)]
+    s.set_contacts_batch([c for _, c in inst])
+    for i, (v0, _) in enumerate(inst):
+        s.set_state(sc.mesh.X, v0, instance=i)
+    s.step(1, 5)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    for i in (0, 3):
+        v0, cs = inst[i]
+        o = O.Oracle(sc.mesh, sc.material, sc.h)
+        o.set_contacts(cs)
+        pins = sc.mesh.X[o.pinned] + sc.h * sc.pin_velocity
+        xo, vo, info = o.frame(sc.mesh.X.copy(), v0, pin_targets=pins)
+        xg, vg = s.get_state(instance=i)
+        err = np.abs(xg - xo).max()
+        assert err < tol, (i, err, tol)
+        cg = o.classify(xg, sc.mesh.X, s.get_lambda(instance=i))
+        co = o.classify(xo, sc.mesh.X, info["lam"])
+        assert (co == cg).mean() > 0.99
+    # all instances advance: positions differ between instances (different inputs)
+    P = s.get_positions()
+    assert P.shape == (S, sc.mesh.n_v, 3)
+    assert np.array_equal(P[0], s.get_state(instance=0)[0])
+    assert np.abs(P[1] - P[2]).max() > 0
+
+
+def test_batched_determinism(simmod):
+    sc = scenes.make_scene("block", nv=7, split="kuhn6")
+    S = 40
+    out = []
+    for _ in range(2):
+        s = make(simmod, sc, S)
+        for i in range(S):
+            x, v = scenes.random_state(sc.mesh, seed=i, amp=0.05)
+            s.set_state(sc.mesh.X, v, instance=i)
+        s.step(2, 5)
+        out.append(s.get_positions())
+        s.close()
+    assert np.array_equal(out[0], out[1])
+
+
+def test_instance_validation(simmod):
+    sc = scenes.make_scene("block", nv=5)
+    s = make(simmod, sc, 2)
+    with pytest.raises(simmod.SimError, match="instance"):
+        s.set_contacts([], instance=2)
+    with pytest.raises(simmod.SimError, match="instance"):
+        s.get_state(instance=-1)
