@@ -235,6 +235,22 @@ def run_ours(args):
         kt = s.kernel_times()
         for k in ktimes:
             ktimes[k] += kt[k]
+    # host / commit breakdown (diagnostic, outside the timed region)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s.set_contacts_batch(packed=packed)
+    host_set_ms = 1000 * (time.perf_counter() - t0)
+    b0, b1, b2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    b0.record(stream)
+    t0 = time.perf_counter()
+    s.step(1, ITERS)            # commit (pack + upload + Delassus) then the frame graph
+    host_step_ms = 1000 * (time.perf_counter() - t0)
+    b1.record(stream)
+    s.step(1, ITERS)            # frame graph only (contacts unchanged)
+    b2.record(stream)
+    torch.cuda.synchronize()
+    breakdown = {"host_set_contacts_ms": host_set_ms, "host_step_call_ms": host_step_ms,
+                 "device_commit_plus_frame_ms": b0.elapsed_time(b1), "device_frame_only_ms": b1.elapsed_time(b2)}
     s.set_profiling(False)
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -333,6 +349,7 @@ def run_ours(args):
         "gpu_launches": gpu_launches,
         "kernel_us_per_step": kernels_us,
         "kernel_share": share,
+        "breakdown": breakdown,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clocks,

@@ -11,6 +11,7 @@
 #include <numeric>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/sim.h"
@@ -137,8 +138,12 @@ struct sim_handle {
     DBuf<int32_t> cs0, cv0, cc1;
     DBuf<int32_t> slot_vtx, slot_inst, scp, sci;
     DBuf<float> scw;
-    DBuf<int> coff, soff, uoff;
-    DBuf<int64_t> goff, zoff;
+    DBuf<int> coff, soff, uoff, cls, csoff, cmoff, cmem;
+    DBuf<int64_t> goff, zoff, gaoff;
+    DBuf<int32_t> cvtx, ccls;        // class slots
+    DBuf<int2> it_cd, it_sc;         // grouped chain-dot / scatter work items
+    int NCL = 0, CS = 0, cm_max = 0, n_it_cd = 0, n_it_sc = 0;
+    std::vector<int64_t> gaoff_h;
     DBuf<float> G, GA;   // Delassus Gram blocks and the CR's active blocks (fp32-exact values)
     DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res, rho;
     DBuf<int> act_na, act_idx, act_pos, act_con;   // CR active set (k_active)
@@ -150,7 +155,8 @@ struct sim_handle {
     int contact_gen = 0;
     // graph
     cudaGraphExec_t gexec = nullptr;
-    int g_iters = -1, g_C = -1, g_NS = -1, g_ncm = -1, g_nsm = -1, g_um = -1, g_prof = -1, g_gen = -1;
+    std::vector<int64_t> gkey;   // what the captured graph was built for
+    int g_prof = -1;
     // in-graph kernel timing (event record nodes between kernels)
     int profiling = 0;
     std::vector<cudaEvent_t> pev;
@@ -160,23 +166,10 @@ struct sim_handle {
     int64_t h2d_contact_bytes = 0;   // bytes uploaded by the last contact commit
     // pinned staging for asynchronous contact uploads (reused once the last copy is done)
     unsigned char* stage = nullptr;
-    size_t stage_cap = 0, stage_used = 0;
+    size_t stage_cap = 0;
     cudaEvent_t stage_free = nullptr;
     double set_contacts_host_us = 0;
 };
-
-// copy n elements of src into the pinned staging area and enqueue the H2D copy to dst
-template <class T>
-static cudaError_t stage_upload(sim_handle* H, T* dst, const T* src, size_t n) {
-    if (n == 0) return cudaSuccess;
-    const size_t bytes = n * sizeof(T);
-    const size_t at = (H->stage_used + 15) & ~size_t(15);
-    if (at + bytes > H->stage_cap) return cudaErrorMemoryAllocation;   // caller sized the area
-    memcpy(H->stage + at, src, bytes);
-    H->stage_used = at + bytes;
-    H->h2d_contact_bytes += (int64_t)bytes;
-    return cudaMemcpyAsync(dst, H->stage + at, bytes, cudaMemcpyHostToDevice, H->stream);
-}
 
 // ---------------------------------------------------------------------------
 static int validate_create(const sim_mesh* m, const sim_material* mat, double h) {
@@ -392,8 +385,9 @@ static int upload_all(sim_handle* H) {
         CK(cudaMemsetAsync(H->counters.p, 0, ncnt * sizeof(int), st));
     }
     // per-instance contact scalars
-    CK(H->coff.alloc(S + 1)); CK(H->soff.alloc(S + 1)); CK(H->uoff.alloc(S + 1));
-    CK(H->goff.alloc(S + 1)); CK(H->zoff.alloc(S + 1));
+    CK(H->coff.alloc(S + 1)); CK(H->soff.alloc(S + 1)); CK(H->uoff.alloc(S + 1)); CK(H->gaoff.alloc(S + 1));
+    CK(H->goff.alloc(S + 1)); CK(H->zoff.alloc(S + 1)); CK(H->cls.alloc(S)); CK(H->csoff.alloc(S + 1));
+    CK(H->cmoff.alloc(S + 1)); CK(H->cmem.alloc(S));
     CK(H->cr_res.alloc(S)); CK(H->act_na.alloc(S)); CK(H->ucount.alloc(2 * (size_t)S));
     CK(cudaMemsetAsync(H->coff.p, 0, (S + 1) * sizeof(int), st));
     CK(cudaMemsetAsync(H->soff.p, 0, (S + 1) * sizeof(int), st));
@@ -632,8 +626,10 @@ extern "C" int sim_set_contacts_batch(sim_handle* H, int32_t first, int32_t coun
 }
 
 static InstOff inst_off(sim_handle* H) {
-    return InstOff{H->coff.p, H->soff.p, H->goff.p, H->uoff.p, H->zoff.p};
+    return InstOff{H->coff.p, H->soff.p, H->gaoff.p, H->cls.p, H->csoff.p, H->goff.p, H->uoff.p, H->zoff.p,
+                   H->cmoff.p, H->cmem.p};
 }
+static ClassSlots class_slots(sim_handle* H) { return ClassSlots{H->cvtx.p, H->ccls.p}; }
 static Slots slots(sim_handle* H) { return Slots{H->slot_vtx.p, H->slot_inst.p, H->scp.p, H->sci.p, H->scw.p}; }
 static CrContacts cr_contacts(sim_handle* H) { return CrContacts{H->cc9.p, H->cs0.p, H->cv0.p, H->cc1.p}; }
 
@@ -653,6 +649,9 @@ static Params make_params(const sim_handle* H) {
     P.NS = H->NS;
     P.nc_max = H->nc_max;
     P.ns_max = H->ns_max;
+    P.NCL = H->NCL;
+    P.CS = H->CS;
+    P.cm_max = H->cm_max;
     P.cr_iters = H->mat.cr_iterations;
     return P;
 }
@@ -663,47 +662,125 @@ static int commit_contacts(sim_handle* H) {
     if (!H->dirty) return SIM_OK;
     const int S = H->S, nf = H->n_f;
     cudaStream_t st = H->stream;
-    std::vector<int> coff(S + 1, 0), soff(S + 1, 0), uoff(S + 1, 0);
-    std::vector<int64_t> goff(S + 1, 0), zoff(S + 1, 0);
-    int ncm = 0, nsm = 0, um = 0;
+    // slot-set classes: instances with equal contact-vertex sets (hash, then exact compare)
+    std::vector<int> cls(S), rep;                 // class of instance, representative of class
+    {
+        std::unordered_map<uint64_t, std::vector<int>> byhash;
+        for (int i = 0; i < S; ++i) {
+            const std::vector<int32_t>& v = H->ic[i].verts;
+            uint64_t hsh = 1469598103934665603ull ^ v.size();
+            for (int32_t q : v) hsh = (hsh ^ (uint64_t)(uint32_t)q) * 1099511628211ull;
+            std::vector<int>& cand = byhash[hsh];
+            int found = -1;
+            for (int k : cand)
+                if (H->ic[rep[k]].verts == v) { found = k; break; }
+            if (found < 0) {
+                found = (int)rep.size();
+                rep.push_back(i);
+                cand.push_back(found);
+            }
+            cls[i] = found;
+        }
+    }
+    const int NCL = (int)rep.size();
+    std::vector<int> cmoff(NCL + 1, 0), cmem(S);
+    for (int i = 0; i < S; ++i) cmoff[cls[i] + 1]++;
+    for (int k = 0; k < NCL; ++k) cmoff[k + 1] += cmoff[k];
+    {
+        std::vector<int> fillm(cmoff.begin(), cmoff.end() - 1);
+        for (int i = 0; i < S; ++i) cmem[fillm[cls[i]]++] = i;
+    }
+    std::vector<int> coff(S + 1, 0), soff(S + 1, 0), csoff(NCL + 1, 0), uoff(NCL + 1, 0);
+    std::vector<int64_t> gaoff(S + 1, 0), goff(NCL + 1, 0), zoff(NCL + 1, 0);
+    int ncm = 0, nsm = 0, um = 0, cmm = 0;
     for (int i = 0; i < S; ++i) {
         const InstContacts& I = H->ic[i];
         const int n = (int)I.hc.size(), ns = (int)I.verts.size();
         coff[i + 1] = coff[i] + n;
         soff[i + 1] = soff[i] + ns;
-        goff[i + 1] = goff[i] + (int64_t)ns * ns;
-        zoff[i + 1] = zoff[i] + I.chain_total;
-        const int urows = (int)std::min<int64_t>(nf, I.chain_total);
-        uoff[i + 1] = uoff[i] + urows;
+        gaoff[i + 1] = gaoff[i] + (int64_t)ns * ns;
         ncm = std::max(ncm, n);
         nsm = std::max(nsm, ns);
-        um = std::max(um, urows);
     }
-    if (zoff[S] >= (int64_t)INT32_MAX) return fail(SIM_E_LIMIT, "total ancestor-chain entries exceed int32");
-    const int Ct = coff[S], NSt = soff[S];
+    for (int k = 0; k < NCL; ++k) {
+        const InstContacts& I = H->ic[rep[k]];
+        const int ns = (int)I.verts.size();
+        csoff[k + 1] = csoff[k] + ns;
+        goff[k + 1] = goff[k] + (int64_t)ns * ns;
+        zoff[k + 1] = zoff[k] + I.chain_total;
+        const int urows = (int)std::min<int64_t>(nf, I.chain_total);
+        uoff[k + 1] = uoff[k] + urows;
+        um = std::max(um, urows);
+        cmm = std::max(cmm, cmoff[k + 1] - cmoff[k]);
+    }
+    if (zoff[NCL] >= (int64_t)INT32_MAX) return fail(SIM_E_LIMIT, "total ancestor-chain entries exceed int32");
+    const int Ct = coff[S], NSt = soff[S], CSt = csoff[NCL];
+    // work items of the grouped kernels: chain dot (class slot, 32 members), scatter (class, 32 members);
+    // member-chunk-major so one chunk's vectors stay in L2
+    std::vector<int2> it_cd, it_sc;
+    for (int m = 0; m < cmm; m += 32)
+        for (int k = 0; k < NCL; ++k) {
+            const int m0 = cmoff[k] + m;
+            if (m0 >= cmoff[k + 1] || csoff[k + 1] == csoff[k]) continue;
+            it_sc.push_back(make_int2(k, m0));
+            for (int g = csoff[k]; g < csoff[k + 1]; ++g) it_cd.push_back(make_int2(g, m0));
+        }
     bool grew = false;
-    const size_t cC = std::max(Ct, 1), cS = std::max(NSt, 1);
+    const size_t cC = std::max(Ct, 1), cS = std::max(NSt, 1), cCS = std::max(CSt, 1);
     CK(H->dc.ensure(cC, grew)); CK(H->cc9.ensure(9 * cC, grew)); CK(H->cs0.ensure(cC, grew));
     CK(H->cv0.ensure(cC, grew)); CK(H->cc1.ensure(cS, grew)); CK(H->slot_vtx.ensure(cS, grew));
     CK(H->slot_inst.ensure(cS, grew)); CK(H->scp.ensure(cS + 1, grew)); CK(H->sci.ensure(4 * cC, grew));
-    CK(H->scw.ensure(4 * cC, grew)); CK(H->G.ensure(std::max<int64_t>(goff[S], 1), grew));
-    CK(H->GA.ensure(std::max<int64_t>(goff[S], 1), grew));
+    CK(H->scw.ensure(4 * cC, grew)); CK(H->G.ensure(std::max<int64_t>(goff[NCL], 1), grew));
+    CK(H->GA.ensure(std::max<int64_t>(gaoff[S], 1), grew));
     CK(H->lam.ensure(3 * cC, grew)); CK(H->theta.ensure(3 * cC, grew)); CK(H->cdiag.ensure(3 * cC, grew));
     CK(H->hvec.ensure(3 * cC, grew)); CK(H->hl.ensure(3 * cC, grew)); CK(H->rho.ensure(3 * cC, grew));
     CK(H->phi_abs.ensure(cC, grew)); CK(H->dxt.ensure(3 * cS, grew)); CK(H->wz.ensure(3 * cS, grew));
     CK(H->act_idx.ensure(cS, grew)); CK(H->act_pos.ensure(cS, grew)); CK(H->act_con.ensure(cS, grew));
-    CK(H->chain_off.ensure(cS + 1, grew)); CK(H->chain_rows.ensure(std::max<int64_t>(zoff[S], 1), grew));
-    CK(H->Zc.ensure(std::max<int64_t>(zoff[S], 1), grew)); CK(H->ulist.ensure(std::max(uoff[S], 1), grew));
+    CK(H->cvtx.ensure(cCS, grew)); CK(H->ccls.ensure(cCS, grew));
+    CK(H->chain_off.ensure(cCS + 1, grew)); CK(H->chain_rows.ensure(std::max<int64_t>(zoff[NCL], 1), grew));
+    CK(H->Zc.ensure(std::max<int64_t>(zoff[NCL], 1), grew)); CK(H->ulist.ensure(std::max(uoff[NCL], 1), grew));
+    CK(H->it_cd.ensure(std::max<size_t>(it_cd.size(), 1), grew));
+    CK(H->it_sc.ensure(std::max<size_t>(it_sc.size(), 1), grew));
     if (grew) H->contact_gen++;   // captured pointers changed
-    // pack
-    std::vector<DContact> dc(Ct);
-    std::vector<float> c9(9 * (size_t)Ct), scw;
-    std::vector<int32_t> s0(Ct), v0(Ct), c1(NSt), svtx(NSt), sinst(NSt), scp(NSt + 1, 0), sci, choff(NSt + 1, 0);
-    sci.reserve(4 * (size_t)Ct);
-    scw.reserve(4 * (size_t)Ct);
+    // per-instance positions of the slot -> contact lists
+    std::vector<int64_t> poff(S + 1, 0);
+    for (int i = 0; i < S; ++i) poff[i + 1] = poff[i] + (int64_t)H->ic[i].sci.size();
+    const int64_t NP = poff[S];
+    // staging layout: every array packed straight into pinned memory (instances in parallel)
+    struct Seg { size_t at, bytes; };
+    size_t cur = 0;
+    auto seg = [&](size_t bytes) { Seg s{cur, bytes}; cur = (cur + bytes + 255) & ~size_t(255); return s; };
+    const size_t S1 = (size_t)S + 1, C1 = (size_t)NCL + 1;
+    const Seg g_dc = seg(sizeof(DContact) * (size_t)Ct), g_c9 = seg(36 * (size_t)Ct), g_s0 = seg(4 * (size_t)Ct),
+              g_v0 = seg(4 * (size_t)Ct), g_c1 = seg(4 * (size_t)NSt), g_sv = seg(4 * (size_t)NSt),
+              g_si = seg(4 * (size_t)NSt), g_scp = seg(4 * ((size_t)NSt + 1)), g_sci = seg(4 * (size_t)NP),
+              g_scw = seg(4 * (size_t)NP), g_ch = seg(4 * ((size_t)CSt + 1)), g_cv = seg(4 * (size_t)CSt),
+              g_cc = seg(4 * (size_t)CSt), g_co = seg(4 * S1), g_so = seg(4 * S1), g_ga = seg(8 * S1),
+              g_cl = seg(4 * (size_t)S), g_cso = seg(4 * C1), g_go = seg(8 * C1), g_uo = seg(4 * C1),
+              g_zo = seg(8 * C1), g_cmo = seg(4 * C1), g_cm = seg(4 * (size_t)S), g_icd = seg(8 * it_cd.size()),
+              g_isc = seg(8 * it_sc.size());
+    const size_t need = cur + 256;
+    if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
+    CK(cudaEventSynchronize(H->stage_free));   // the previous commit's copies are done
+    if (need > H->stage_cap) {
+        if (H->stage) CK(cudaFreeHost(H->stage));
+        H->stage = nullptr;
+        H->stage_cap = 0;
+        CK(cudaMallocHost((void**)&H->stage, need + need / 4));
+        H->stage_cap = need + need / 4;
+    }
+    unsigned char* B = H->stage;
+    DContact* dc = (DContact*)(B + g_dc.at);
+    float* c9 = (float*)(B + g_c9.at);
+    int32_t *s0 = (int32_t*)(B + g_s0.at), *v0 = (int32_t*)(B + g_v0.at), *c1 = (int32_t*)(B + g_c1.at);
+    int32_t *svtx = (int32_t*)(B + g_sv.at), *sinst = (int32_t*)(B + g_si.at), *scp = (int32_t*)(B + g_scp.at);
+    int32_t* sci = (int32_t*)(B + g_sci.at);
+    float* scw = (float*)(B + g_scw.at);
+#pragma omp parallel for schedule(dynamic, 8)
     for (int i = 0; i < S; ++i) {
         const InstContacts& I = H->ic[i];
         const int cb = coff[i], sb = soff[i], n = (int)I.hc.size(), ns = (int)I.verts.size();
+        const int pb = (int)poff[i];
         for (int c = 0; c < n; ++c) {
             DContact d = I.hc[c];
             d.inst = i;
@@ -712,51 +789,68 @@ static int commit_contacts(sim_handle* H) {
             s0[cb + c] = I.s0[c] >= 0 ? I.s0[c] + sb : -1;
             v0[cb + c] = I.v0[c];
         }
-        std::copy(I.c9.begin(), I.c9.end(), c9.begin() + 9 * (size_t)cb);
+        memcpy(c9 + 9 * (size_t)cb, I.c9.data(), 36 * (size_t)n);
         for (int s = 0; s < ns; ++s) {
             const int g = sb + s;
             c1[g] = I.c1[s] >= 0 ? I.c1[s] + cb : -1;
             svtx[g] = I.verts[s];
             sinst[g] = i;
-            for (int p = I.scp[s]; p < I.scp[s + 1]; ++p) {
-                sci.push_back(I.sci[p] + cb);
-                scw.push_back(I.scw[p]);
-            }
-            scp[g + 1] = (int)sci.size();
-            choff[g + 1] = choff[g] + H->K.depth[I.verts[s]] + 1;
+            scp[g] = pb + I.scp[s];
+        }
+        for (size_t p = 0; p < I.sci.size(); ++p) {
+            sci[pb + p] = I.sci[p] + cb;
+            scw[pb + p] = I.scw[p];
         }
     }
-    // staging (wait only for the previous commit's copies)
-    const size_t need = (size_t)Ct * (sizeof(DContact) + 36 + 8) + (size_t)NSt * 24 + sci.size() * 8 +
-                        (size_t)(S + 1) * 32 + 4096;
-    if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
-    CK(cudaEventSynchronize(H->stage_free));
-    if (need > H->stage_cap) {
-        if (H->stage) CK(cudaFreeHost(H->stage));
-        H->stage = nullptr;
-        H->stage_cap = 0;
-        CK(cudaMallocHost((void**)&H->stage, 2 * need));
-        H->stage_cap = 2 * need;
+    scp[NSt] = (int32_t)NP;
+    {
+        int32_t *choff = (int32_t*)(B + g_ch.at), *cv = (int32_t*)(B + g_cv.at), *cc = (int32_t*)(B + g_cc.at);
+        const int32_t* depth = H->K.depth.data();
+        int64_t ch = 0;
+        for (int k = 0; k < NCL; ++k) {
+            const std::vector<int32_t>& v = H->ic[rep[k]].verts;
+            for (size_t s = 0; s < v.size(); ++s) {
+                const int g = csoff[k] + (int)s;
+                cv[g] = v[s];
+                cc[g] = k;
+                choff[g] = (int32_t)ch;
+                ch += depth[v[s]] + 1;
+            }
+        }
+        choff[CSt] = (int32_t)ch;
     }
-    H->stage_used = 0;
+    memcpy(B + g_co.at, coff.data(), 4 * S1);
+    memcpy(B + g_so.at, soff.data(), 4 * S1);
+    memcpy(B + g_ga.at, gaoff.data(), 8 * S1);
+    memcpy(B + g_cl.at, cls.data(), 4 * (size_t)S);
+    memcpy(B + g_cso.at, csoff.data(), 4 * C1);
+    memcpy(B + g_go.at, goff.data(), 8 * C1);
+    memcpy(B + g_uo.at, uoff.data(), 4 * C1);
+    memcpy(B + g_zo.at, zoff.data(), 8 * C1);
+    memcpy(B + g_cmo.at, cmoff.data(), 4 * C1);
+    memcpy(B + g_cm.at, cmem.data(), 4 * (size_t)S);
+    if (!it_cd.empty()) memcpy(B + g_icd.at, it_cd.data(), 8 * it_cd.size());
+    if (!it_sc.empty()) memcpy(B + g_isc.at, it_sc.data(), 8 * it_sc.size());
     H->h2d_contact_bytes = 0;
-    CK(stage_upload(H, H->dc.p, dc.data(), Ct));
-    CK(stage_upload(H, H->cc9.p, c9.data(), c9.size()));
-    CK(stage_upload(H, H->cs0.p, s0.data(), Ct));
-    CK(stage_upload(H, H->cv0.p, v0.data(), Ct));
-    CK(stage_upload(H, H->cc1.p, c1.data(), NSt));
-    CK(stage_upload(H, H->slot_vtx.p, svtx.data(), NSt));
-    CK(stage_upload(H, H->slot_inst.p, sinst.data(), NSt));
-    CK(stage_upload(H, H->scp.p, scp.data(), NSt + 1));
-    CK(stage_upload(H, H->sci.p, sci.data(), sci.size()));
-    CK(stage_upload(H, H->scw.p, scw.data(), scw.size()));
-    CK(stage_upload(H, H->chain_off.p, choff.data(), NSt + 1));
-    CK(stage_upload(H, H->coff.p, coff.data(), S + 1));
-    CK(stage_upload(H, H->soff.p, soff.data(), S + 1));
-    CK(stage_upload(H, H->uoff.p, uoff.data(), S + 1));
-    CK(stage_upload(H, H->goff.p, goff.data(), S + 1));
-    CK(stage_upload(H, H->zoff.p, zoff.data(), S + 1));
+    auto up = [&](void* dst, const Seg& g) -> cudaError_t {
+        if (g.bytes == 0) return cudaSuccess;
+        H->h2d_contact_bytes += (int64_t)g.bytes;
+        return cudaMemcpyAsync(dst, B + g.at, g.bytes, cudaMemcpyHostToDevice, st);
+    };
+    CK(up(H->dc.p, g_dc)); CK(up(H->cc9.p, g_c9)); CK(up(H->cs0.p, g_s0)); CK(up(H->cv0.p, g_v0));
+    CK(up(H->cc1.p, g_c1)); CK(up(H->slot_vtx.p, g_sv)); CK(up(H->slot_inst.p, g_si)); CK(up(H->scp.p, g_scp));
+    CK(up(H->sci.p, g_sci)); CK(up(H->scw.p, g_scw)); CK(up(H->chain_off.p, g_ch)); CK(up(H->cvtx.p, g_cv));
+    CK(up(H->ccls.p, g_cc)); CK(up(H->coff.p, g_co)); CK(up(H->soff.p, g_so)); CK(up(H->gaoff.p, g_ga));
+    CK(up(H->cls.p, g_cl)); CK(up(H->csoff.p, g_cso)); CK(up(H->goff.p, g_go)); CK(up(H->uoff.p, g_uo));
+    CK(up(H->zoff.p, g_zo)); CK(up(H->cmoff.p, g_cmo)); CK(up(H->cmem.p, g_cm)); CK(up(H->it_cd.p, g_icd));
+    CK(up(H->it_sc.p, g_isc));
     CK(cudaEventRecord(H->stage_free, st));
+    H->NCL = NCL;
+    H->CS = CSt;
+    H->cm_max = cmm;
+    H->n_it_cd = (int)it_cd.size();
+    H->n_it_sc = (int)it_sc.size();
+    H->gaoff_h = gaoff;
     H->C = Ct;
     H->NS = NSt;
     H->nc_max = ncm;
@@ -764,16 +858,18 @@ static int commit_contacts(sim_handle* H) {
     H->urows_max = um;
     H->coff_h = coff;
     H->soff_h = soff;
-    CK(cudaMemsetAsync(H->flag.p, 0, (size_t)S * nf, st));
+    CK(cudaMemsetAsync(H->flag.p, 0, (size_t)NCL * nf, st));
     CK(cudaMemsetAsync(H->slotmap.p, 0xff, (size_t)nf * S * sizeof(int32_t), st));
-    CK(cudaMemsetAsync(H->ucount.p, 0, 2 * (size_t)S * sizeof(int), st));
+    CK(cudaMemsetAsync(H->ucount.p, 0, 2 * (size_t)NCL * sizeof(int), st));
     CK(cudaMemsetAsync(H->cr_res.p, 0, S * sizeof(double), st));
     Params P = make_params(H);
     const InstOff off = inst_off(H);
     const Slots sl = slots(H);
-    launch_chain_rows(st, P, sl, H->chain_off.p, H->parent.p, H->ptop.p, H->chain_rows.p, H->flag.p, H->slotmap.p);
-    launch_ulist(st, P, off, H->flag.p, sl, H->meta.p, H->ucount.p, H->ulist.p, H->Krow.p, H->Zc.p);
-    launch_delassus(st, P, off, sl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
+    const ClassSlots csl = class_slots(H);
+    launch_chain_rows(st, P, csl, sl, H->chain_off.p, H->parent.p, H->ptop.p, H->chain_rows.p, H->flag.p,
+                      H->slotmap.p);
+    launch_ulist(st, P, off, H->flag.p, csl, H->meta.p, H->ucount.p, H->ulist.p, H->Krow.p, H->Zc.p);
+    launch_delassus(st, P, off, csl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
     launch_djj(st, P, off, H->dc.p, H->G.p);
     CK(cudaGetLastError());
     H->dirty = false;
@@ -859,13 +955,14 @@ static int enqueue_frame(sim_handle* H, int iters) {
         enqueue_kpass1(H, st); nk++;
         if (con) {
             MARK(KK_CHAIN);
-            launch_chain_dot(st, P, H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p, H->y.p, sl, ccr, H->x.p,
-                             cs); nk++;
+            launch_chain_dot(st, P, off, class_slots(H), H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
+                             H->y.p, sl, ccr, H->x.p, cs, H->n_it_cd, H->it_cd.p); nk++;
             MARK(KK_CR);
             int e = launch_cr(st, P, off, H->dc.p, ccr, sl, H->GA.p, H->x.p, cs, act); nk++;
             if (e) return -e;
             MARK(KK_SCATTER);
-            launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p); nk++;
+            launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p, H->n_it_sc,
+                           H->it_sc.p); nk++;
         }
         MARK(KK_KPASS2);
         enqueue_kpass2(H, st, H->x.p, H->xt.p, H->v.p, 1.0 / H->h, k == iters - 1); nk++;
@@ -905,8 +1002,9 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     if (frames == 0) return SIM_OK;
     int rc = commit_contacts(H);
     if (rc) return rc;
-    if (!H->gexec || H->g_iters != iters || H->g_C != H->C || H->g_NS != H->NS || H->g_ncm != H->nc_max ||
-        H->g_nsm != H->ns_max || H->g_um != H->urows_max || H->g_prof != H->profiling || H->g_gen != H->contact_gen) {
+    const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
+                                      H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc};
+    if (!H->gexec || key != H->gkey) {
         if (H->gexec) {
             cudaGraphExecDestroy(H->gexec);
             H->gexec = nullptr;
@@ -920,14 +1018,8 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
         cudaError_t ie = cudaGraphInstantiate(&H->gexec, g, 0);
         cudaGraphDestroy(g);
         if (ie != cudaSuccess) return fail(SIM_E_CUDA, "instantiate: %s", cudaGetErrorString(ie));
-        H->g_iters = iters;
-        H->g_C = H->C;
-        H->g_NS = H->NS;
-        H->g_ncm = H->nc_max;
-        H->g_nsm = H->ns_max;
-        H->g_um = H->urows_max;
+        H->gkey = key;
         H->g_prof = H->profiling;
-        H->g_gen = H->contact_gen;
         H->kernels_per_frame = nk;
     }
     for (int f = 0; f < frames; ++f) CK(cudaGraphLaunch(H->gexec, H->stream));
@@ -1213,8 +1305,10 @@ extern "C" int sim_debug_get_delassus(sim_handle* H, int32_t inst, int32_t* cv, 
     CK(cudaStreamSynchronize(H->stream));
     if (cv) for (int s = 0; s < ns; ++s) cv[s] = H->int2orig[I.verts[s]];
     if (G && ns) {
+        int cl = 0;
         int64_t go = 0;
-        for (int i = 0; i < inst; ++i) go += (int64_t)H->ic[i].verts.size() * H->ic[i].verts.size();
+        CK(cudaMemcpy(&cl, H->cls.p + inst, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&go, H->goff.p + cl, sizeof(int64_t), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(G, H->G.p + go, (size_t)ns * ns * sizeof(float), cudaMemcpyDeviceToHost));
     }
     return SIM_OK;

@@ -1007,86 +1007,135 @@ void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
 }
 
 // ----------------------------------------------------------------------------
-// chain dot: dxt_s = (K^T y)_{a_s} = sum_{k} Kcol[colptr_a + k] y[chain_rows[off_s + k]]
-// (column a of K is contiguous in Kcol; its rows are a's ancestor chain)
+// chain dot: dxt_s = (K^T y)_{a_s} = sum_k Kcol[colptr_a + k] y[chain_rows[off + k]]
+// (column a of K is contiguous in Kcol; its rows are a's ancestor chain).  One CTA per
+// (class slot, up to 32 instances of the class): the chain is read once for the group.
+//   group of 1: 8 warps take interleaved 128-entry slices, lanes split the entries;
+//   larger groups: lane = instance (coalesced y rows, instance-minor), warps split the chain.
+// Thread 0 / lane l also forms the Schur RHS rho = h - theta J x~ for the slot's single
+// single-vertex contact, x~ = x^k + K^T y (other contacts are handled in the CR prologue).
 // ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_chain_dot(int S, const float* __restrict__ Kcol,
+__device__ __forceinline__ void chain_rho(int S, int inst, int s, double t0, double t1, double t2, CrContacts cc,
+                                          const double4* __restrict__ x, ContactState cs) {
+    cs.dxt[3 * s] = t0;
+    cs.dxt[3 * s + 1] = t1;
+    cs.dxt[3 * s + 2] = t2;
+    const int c = cc.c1[s];
+    if (c >= 0) {
+        const double4 xa = x[(size_t)cc.v0[c] * S + inst];
+        const double xs0 = xa.x + t0, xs1 = xa.y + t1, xs2 = xa.z + t2;
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+            const float* c3 = cc.c9 + 9 * c + 3 * kk;
+            cs.rho[3 * c + kk] = cs.hvec[3 * c + kk] - cs.theta[3 * c + kk] * ((double)c3[0] * xs0 +
+                                                                               (double)c3[1] * xs1 +
+                                                                               (double)c3[2] * xs2);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_chain_dot(int S, InstOff off, ClassSlots csl, const float* __restrict__ Kcol,
                                                    const int64_t* __restrict__ colptr,
                                                    const int32_t* __restrict__ chain_off,
                                                    const int32_t* __restrict__ chain_rows, const float4* __restrict__ y,
-                                                   Slots sl, CrContacts cc, const double4* __restrict__ x,
-                                                   ContactState cs) {
-    // one CTA per contact vertex (global slot); its 8 warps take interleaved 128-entry slices of the chain
-    __shared__ double s_red[3][kWarps];
-    const int s = blockIdx.x;
+                                                   CrContacts cc, const double4* __restrict__ x, ContactState cs,
+                                                   const int2* __restrict__ items) {
+    __shared__ double s_red[3][kWarps][32];
+    const int2 it = items[blockIdx.x];
+    const int g = it.x, cl = csl.cls[g];
+    const int m0 = it.y, gs = min(32, off.cmoff[cl + 1] - m0);
+    const int sloc = g - off.csoff[cl];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int a = sl.vtx[s];
-    const int inst = sl.inst[s];
+    const int a = csl.vtx[g];
     const float* col = Kcol + colptr[a];
-    const int o0 = chain_off[s], len = chain_off[s + 1] - o0;
+    const int o0 = chain_off[g], len = chain_off[g + 1] - o0;
     double a0 = 0, a1 = 0, a2 = 0;
-    for (int k0 = 128 * w; k0 < len; k0 += 128 * kWarps) {   // 4 independent gathers in flight per lane
-        int rw[4];
-        float kv[4];
+    if (gs == 1) {
+        const int inst = off.cmem[m0];
+        for (int k0 = 128 * w; k0 < len; k0 += 128 * kWarps) {   // 4 independent gathers in flight per lane
+            int rw[4];
+            float kv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int k = k0 + 32 * u + lane;
-            rw[u] = k < len ? __ldg(&chain_rows[o0 + k]) : -1;
-            kv[u] = k < len ? __ldg(&col[k]) : 0.f;
+            for (int u = 0; u < 4; ++u) {
+                const int k = k0 + 32 * u + lane;
+                rw[u] = k < len ? __ldg(&chain_rows[o0 + k]) : -1;
+                kv[u] = k < len ? __ldg(&col[k]) : 0.f;
+            }
+            float4 yy[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                yy[u] = rw[u] >= 0 ? __ldg(&y[(size_t)rw[u] * S + inst]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                f0 = fmaf(kv[u], yy[u].x, f0);
+                f1 = fmaf(kv[u], yy[u].y, f1);
+                f2 = fmaf(kv[u], yy[u].z, f2);
+            }
+            a0 += (double)f0;
+            a1 += (double)f1;
+            a2 += (double)f2;
         }
-        float4 yy[4];
+        a0 = warp_sum(a0);
+        a1 = warp_sum(a1);
+        a2 = warp_sum(a2);
+        if (lane == 0) {
+            s_red[0][w][0] = a0;
+            s_red[1][w][0] = a1;
+            s_red[2][w][0] = a2;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            yy[u] = rw[u] >= 0 ? __ldg(&y[(size_t)rw[u] * S + inst]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < kWarps; ++q) { t0 += s_red[0][q][0]; t1 += s_red[1][q][0]; t2 += s_red[2][q][0]; }
+            chain_rho(S, inst, off.soff[inst] + sloc, t0, t1, t2, cc, x, cs);
+        }
+        return;
+    }
+    // lanes = instances of the group; warp w takes entries [32 w + 256 j, +32)
+    const int inst = off.cmem[m0 + min(lane, gs - 1)];
+    for (int k0 = 32 * w; k0 < len; k0 += 32 * kWarps) {
+        const int n = min(32, len - k0);
+        const int rmine = lane < n ? __ldg(&chain_rows[o0 + k0 + lane]) : 0;
+        const float kmine = lane < n ? __ldg(&col[k0 + lane]) : 0.f;
         float f0 = 0.f, f1 = 0.f, f2 = 0.f;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            f0 = fmaf(kv[u], yy[u].x, f0);
-            f1 = fmaf(kv[u], yy[u].y, f1);
-            f2 = fmaf(kv[u], yy[u].z, f2);
+#pragma unroll 8
+        for (int q = 0; q < n; ++q) {
+            const int r = __shfl_sync(0xffffffffu, rmine, q);
+            const float kv = __shfl_sync(0xffffffffu, kmine, q);
+            const float4 yv = __ldg(&y[(size_t)r * S + inst]);
+            f0 = fmaf(kv, yv.x, f0);
+            f1 = fmaf(kv, yv.y, f1);
+            f2 = fmaf(kv, yv.z, f2);
         }
         a0 += (double)f0;
         a1 += (double)f1;
         a2 += (double)f2;
     }
-    a0 = warp_sum(a0);
-    a1 = warp_sum(a1);
-    a2 = warp_sum(a2);
-    if (lane == 0) {
-        s_red[0][w] = a0;
-        s_red[1][w] = a1;
-        s_red[2][w] = a2;
-    }
+    s_red[0][w][lane] = a0;
+    s_red[1][w][lane] = a1;
+    s_red[2][w][lane] = a2;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < gs) {
         double t0 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
-        for (int q = 0; q < kWarps; ++q) { t0 += s_red[0][q]; t1 += s_red[1][q]; t2 += s_red[2][q]; }
-        cs.dxt[3 * s] = t0;
-        cs.dxt[3 * s + 1] = t1;
-        cs.dxt[3 * s + 2] = t2;
-        // Schur RHS rho = h - theta J x~, x~ = x^k + K^T y, for the single contact on this slot
-        // (other contacts are handled in the CR prologue)
-        const int c = cc.c1[s];
-        if (c >= 0) {
-            const double4 xa = x[(size_t)cc.v0[c] * S + inst];
-            const double xs0 = xa.x + t0, xs1 = xa.y + t1, xs2 = xa.z + t2;
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk) {
-                const float* c3 = cc.c9 + 9 * c + 3 * kk;
-                cs.rho[3 * c + kk] = cs.hvec[3 * c + kk] - cs.theta[3 * c + kk] * ((double)c3[0] * xs0 +
-                                                                                   (double)c3[1] * xs1 +
-                                                                                   (double)c3[2] * xs2);
-            }
+        for (int q = 0; q < kWarps; ++q) {
+            t0 += s_red[0][q][lane];
+            t1 += s_red[1][q][lane];
+            t2 += s_red[2][q][lane];
         }
+        chain_rho(S, inst, off.soff[inst] + sloc, t0, t1, t2, cc, x, cs);
     }
 }
 
-void launch_chain_dot(cudaStream_t st, const Params& P, const float* Kcol, const int64_t* colptr,
-                      const int32_t* chain_off, const int32_t* chain_rows, const float4* y, Slots sl,
-                      CrContacts cc, const double4* x, ContactState cs) {
-    if (P.NS == 0) return;
-    k_chain_dot<<<P.NS, 32 * kWarps, 0, st>>>(P.S, Kcol, colptr, chain_off, chain_rows, y, sl, cc, x, cs);
+void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
+                      const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows, const float4* y,
+                      Slots sl, CrContacts cc, const double4* x, ContactState cs, int nitems, const int2* items) {
+    if (P.NS == 0 || nitems == 0) return;
+    (void)sl;
+    k_chain_dot<<<nitems, 32 * kWarps, 0, st>>>(P.S, off, csl, Kcol, colptr, chain_off, chain_rows, y, cc, x, cs,
+                                                items);
 }
 
 // ----------------------------------------------------------------------------
@@ -1150,8 +1199,8 @@ __global__ void __launch_bounds__(256) k_gather_ga(InstOff off, const float* __r
     const int i = blockIdx.x;
     if (i >= na) return;
     const int sb = off.soff[inst], ns = off.soff[inst + 1] - sb;
-    const float* Gi = G + off.goff[inst] + (size_t)act.aidx[sb + i] * ns;
-    float* GAi = GA + off.goff[inst] + (size_t)i * na;
+    const float* Gi = G + off.goff[off.cls[inst]] + (size_t)act.aidx[sb + i] * ns;
+    float* GAi = GA + off.gaoff[inst] + (size_t)i * na;
     for (int j = threadIdx.x; j < na; j += blockDim.x) GAi[j] = Gi[act.aidx[sb + j]];
 }
 
@@ -1162,19 +1211,19 @@ void launch_active(cudaStream_t st, const Params& P, InstOff off, CrContacts cc,
     k_gather_ga<<<dim3(P.ns_max, P.S), 256, 0, st>>>(off, G, act, GA);
 }
 
-// per-contact-set: chain rows of every slot (walk panel runs), per-instance row flags, slot map
-__global__ void k_chain_rows(Params P, Slots sl, const int32_t* __restrict__ chain_off,
+// per-contact-set: chain rows of every class slot (walk panel runs), per-class row flags;
+// warp w also writes slotmap for instance slot w
+__global__ void k_chain_rows(Params P, ClassSlots csl, Slots sl, const int32_t* __restrict__ chain_off,
                              const int32_t* __restrict__ parent, const int32_t* __restrict__ ptop,
                              int32_t* __restrict__ chain_rows, uint8_t* __restrict__ flag,
                              int32_t* __restrict__ slotmap) {
     const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (s >= P.NS) return;
-    const int inst = sl.inst[s];
-    uint8_t* fl = flag + (size_t)inst * P.n_f;
-    if (lane == 0) slotmap[(size_t)sl.vtx[s] * P.S + inst] = s;
+    if (s < P.NS && lane == 0) slotmap[(size_t)sl.vtx[s] * P.S + sl.inst[s]] = s;
+    if (s >= P.CS) return;
+    uint8_t* fl = flag + (size_t)csl.cls[s] * P.n_f;
     int pos = chain_off[s];
-    for (int i = sl.vtx[s]; i >= 0;) {
+    for (int i = csl.vtx[s]; i >= 0;) {
         const int top = ptop[i];
         const int len = top - i + 1;
         for (int o = lane; o < len; o += 32) {
@@ -1186,93 +1235,126 @@ __global__ void k_chain_rows(Params P, Slots sl, const int32_t* __restrict__ cha
     }
 }
 
-void launch_chain_rows(cudaStream_t st, const Params& P, Slots sl, const int32_t* chain_off, const int32_t* parent,
-                       const int32_t* ptop, int32_t* chain_rows, uint8_t* flag, int32_t* slotmap) {
-    if (P.NS == 0) return;
-    k_chain_rows<<<(P.NS + 7) / 8, 256, 0, st>>>(P, sl, chain_off, parent, ptop, chain_rows, flag, slotmap);
+void launch_chain_rows(cudaStream_t st, const Params& P, ClassSlots csl, Slots sl, const int32_t* chain_off,
+                       const int32_t* parent, const int32_t* ptop, int32_t* chain_rows, uint8_t* flag,
+                       int32_t* slotmap) {
+    const int n = std::max(P.NS, P.CS);
+    if (n == 0) return;
+    k_chain_rows<<<(n + 7) / 8, 256, 0, st>>>(P, csl, sl, chain_off, parent, ptop, chain_rows, flag, slotmap);
 }
 
-// rows on any chain of instance blockIdx.y, with the (global) slot range in their subtree
+// rows on any chain of class blockIdx.y, with the class-local slot range in their subtree
 // [first(i), i] and an offset into the compact copy Zc of K[i][a_s], s in [s0, s1)
-__global__ void k_ulist(int n_f, InstOff off, const uint8_t* __restrict__ flag, Slots sl,
+__global__ void k_ulist(int n_f, InstOff off, const uint8_t* __restrict__ flag, ClassSlots csl,
                         const int2* __restrict__ meta, int* __restrict__ ucount, int4* __restrict__ ulist) {
-    const int inst = blockIdx.y;
+    const int c = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_f || !flag[(size_t)inst * n_f + i]) return;
-    const int sb = off.soff[inst], se = off.soff[inst + 1];
+    if (i >= n_f || !flag[(size_t)c * n_f + i]) return;
+    const int sb = off.csoff[c], ns = off.csoff[c + 1] - sb;
+    const int32_t* v = csl.vtx + sb;
     const int f = meta[i].y;
-    int lo = sb, hi = se;
-    while (lo < hi) { int m = (lo + hi) >> 1; if (sl.vtx[m] < f) lo = m + 1; else hi = m; }
+    int lo = 0, hi = ns;
+    while (lo < hi) { int m = (lo + hi) >> 1; if (v[m] < f) lo = m + 1; else hi = m; }
     const int s0 = lo;
-    hi = se;
-    while (lo < hi) { int m = (lo + hi) >> 1; if (sl.vtx[m] <= i) lo = m + 1; else hi = m; }
+    hi = ns;
+    while (lo < hi) { int m = (lo + hi) >> 1; if (v[m] <= i) lo = m + 1; else hi = m; }
     // list order and offsets are arbitrary but each row's values stay contiguous
-    const int idx = atomicAdd(&ucount[2 * inst], 1);
-    const int o = atomicAdd(&ucount[2 * inst + 1], lo - s0);
-    ulist[off.uoff[inst] + idx] = make_int4(i, s0, lo, (int)(off.zoff[inst] + o));
+    const int idx = atomicAdd(&ucount[2 * c], 1);
+    const int o = atomicAdd(&ucount[2 * c + 1], lo - s0);
+    ulist[off.uoff[c] + idx] = make_int4(i, s0, lo, (int)(off.zoff[c] + o));
 }
 
 // Zc[off + s - s0] = K[i][a_s]  (one warp per listed row)
-__global__ void k_zfill(InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist, Slots sl,
+__global__ void k_zfill(InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist, ClassSlots csl,
                         const float* __restrict__ Krow, const int2* __restrict__ meta, float* __restrict__ Zc) {
-    const int inst = blockIdx.y;
+    const int c = blockIdx.y;
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * (blockDim.x >> 5);
-    const int cnt = ucount[2 * inst];
-    const int4* ul = ulist + off.uoff[inst];
+    const int cnt = ucount[2 * c];
+    const int4* ul = ulist + off.uoff[c];
+    const int32_t* v = csl.vtx + off.csoff[c];
     for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
         const int4 u = ul[e];
         const float* row = Krow + meta[u.x].x;
-        for (int s = u.y + lane; s < u.z; s += 32) Zc[u.w + s - u.y] = row[sl.vtx[s]];
+        for (int s = u.y + lane; s < u.z; s += 32) Zc[u.w + s - u.y] = row[v[s]];
     }
 }
 
-void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* flag, Slots sl, const int2* meta,
-                  int* ucount, int4* ulist, const float* Krow, float* Zc) {
-    if (P.NS == 0) return;
-    k_ulist<<<dim3((P.n_f + 255) / 256, P.S), 256, 0, st>>>(P.n_f, off, flag, sl, meta, ucount, ulist);
-    const int gx = P.S >= 148 ? 4 : (148 * 4 + P.S - 1) / P.S;
-    k_zfill<<<dim3(gx, P.S), 256, 0, st>>>(off, ucount, ulist, sl, Krow, meta, Zc);
+void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* flag, ClassSlots csl,
+                  const int2* meta, int* ucount, int4* ulist, const float* Krow, float* Zc) {
+    if (P.CS == 0) return;
+    k_ulist<<<dim3((P.n_f + 255) / 256, P.NCL), 256, 0, st>>>(P.n_f, off, flag, csl, meta, ucount, ulist);
+    const int gx = P.NCL >= 148 ? 4 : (148 * 4 + P.NCL - 1) / P.NCL;
+    k_zfill<<<dim3(gx, P.NCL), 256, 0, st>>>(off, ucount, ulist, csl, Krow, meta, Zc);
 }
 
 // ----------------------------------------------------------------------------
 // scatter (P:L956 correction, delta form): y_i += sum_{s0 <= s < s1} K[i][a_s] wz_s
-// for the rows i on the contact vertices' chains (warp per row, grid-stride per instance)
+// for the rows i on the class's chains.  Item = (class, 32 members):
+//   group of 1: warp per row, lanes split the slot range (4 loads in flight per lane);
+//   larger groups: warp per row, lane = instance (coalesced y), slots in sequence.
 // ----------------------------------------------------------------------------
 __global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist,
-                          const float* __restrict__ Zc, const double* __restrict__ wz, float4* __restrict__ y) {
-    const int inst = blockIdx.y;
+                          const float* __restrict__ Zc, const double* __restrict__ wz, float4* __restrict__ y,
+                          const int2* __restrict__ items) {
+    const int2 it = items[blockIdx.y];
+    const int c = it.x, m0 = it.y, gs = min(32, off.cmoff[c + 1] - m0);
     const int lane = threadIdx.x & 31;
     const int nw = gridDim.x * (blockDim.x >> 5);
-    const int cnt = ucount[2 * inst];
-    const int4* ul = ulist + off.uoff[inst];
-    for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
-        const int4 u = ul[e];
-        const float* zr = Zc + u.w - u.y;   // zr[s] = K[i][a_s]
-        double a0 = 0, a1 = 0, a2 = 0;
-        for (int s0 = u.y; s0 < u.z; s0 += 128) {   // 4 independent loads in flight per lane
-            double kv[4], w0[4], w1[4], w2[4];
+    const int cnt = ucount[2 * c];
+    const int4* ul = ulist + off.uoff[c];
+    if (gs == 1) {
+        const int inst = off.cmem[m0];
+        const double* wzi = wz + 3 * (size_t)off.soff[inst];
+        for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
+            const int4 u = ul[e];
+            const float* zr = Zc + u.w - u.y;   // zr[s] = K[i][a_s]
+            double a0 = 0, a1 = 0, a2 = 0;
+            for (int s0 = u.y; s0 < u.z; s0 += 128) {
+                double kv[4], w0[4], w1[4], w2[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int sq = s0 + 32 * q + lane;
-                const bool ok = sq < u.z;
-                const int iq = ok ? sq : u.y;
-                kv[q] = ok ? (double)__ldg(&zr[sq]) : 0.0;
-                w0[q] = __ldg(&wz[3 * iq]);
-                w1[q] = __ldg(&wz[3 * iq + 1]);
-                w2[q] = __ldg(&wz[3 * iq + 2]);
+                for (int q = 0; q < 4; ++q) {
+                    const int sq = s0 + 32 * q + lane;
+                    const bool ok = sq < u.z;
+                    const int iq = ok ? sq : u.y;
+                    kv[q] = ok ? (double)__ldg(&zr[sq]) : 0.0;
+                    w0[q] = __ldg(&wzi[3 * iq]);
+                    w1[q] = __ldg(&wzi[3 * iq + 1]);
+                    w2[q] = __ldg(&wzi[3 * iq + 2]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    a0 = fma(kv[q], w0[q], a0);
+                    a1 = fma(kv[q], w1[q], a1);
+                    a2 = fma(kv[q], w2[q], a2);
+                }
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                a0 = fma(kv[q], w0[q], a0);
-                a1 = fma(kv[q], w1[q], a1);
-                a2 = fma(kv[q], w2[q], a2);
+            a0 = warp_sum(a0);
+            a1 = warp_sum(a1);
+            a2 = warp_sum(a2);
+            if (lane == 0) {
+                const size_t iy = (size_t)u.x * S + inst;
+                const float4 yi = y[iy];
+                y[iy] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), yi.w);
             }
         }
-        a0 = warp_sum(a0);
-        a1 = warp_sum(a1);
-        a2 = warp_sum(a2);
-        if (lane == 0) {
+        return;
+    }
+    const bool live = lane < gs;
+    const int inst = off.cmem[m0 + min(lane, gs - 1)];
+    const double* wzi = wz + 3 * (size_t)off.soff[inst];
+    for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
+        const int4 u = ul[e];
+        const float* zr = Zc + u.w - u.y;
+        double a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll 4
+        for (int s = u.y; s < u.z; ++s) {
+            const double kv = (double)__ldg(&zr[s]);
+            a0 = fma(kv, __ldg(&wzi[3 * s]), a0);
+            a1 = fma(kv, __ldg(&wzi[3 * s + 1]), a1);
+            a2 = fma(kv, __ldg(&wzi[3 * s + 2]), a2);
+        }
+        if (live) {
             const size_t iy = (size_t)u.x * S + inst;
             const float4 yi = y[iy];
             y[iy] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), yi.w);
@@ -1281,11 +1363,11 @@ __global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, co
 }
 
 void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off, const int* ucount,
-                    const int4* ulist, const float* Zc, const double* wz, float4* y) {
-    if (P.NS == 0) return;
+                    const int4* ulist, const float* Zc, const double* wz, float4* y, int nitems, const int2* items) {
+    if (P.NS == 0 || nitems == 0) return;
     int gx = (max_rows + 7) / 8;
-    if (P.S > 1) gx = std::min(gx, std::max(1, (148 * 8 + P.S - 1) / P.S));
-    k_scatter<<<dim3(gx, P.S), 256, 0, st>>>(P.S, off, ucount, ulist, Zc, wz, y);
+    if (nitems > 1) gx = std::min(gx, std::max(1, (148 * 8 + nitems - 1) / nitems));
+    k_scatter<<<dim3(gx, nitems), 256, 0, st>>>(P.S, off, ucount, ulist, Zc, wz, y, items);
 }
 
 // ----------------------------------------------------------------------------
@@ -1310,11 +1392,11 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
                                                   const float* __restrict__ Kcol, const int64_t* __restrict__ colptr,
                                                   const int32_t* __restrict__ depth, const int32_t* __restrict__ parent,
                                                   const int32_t* __restrict__ ptop, float* __restrict__ Gall) {
-    // instance blockIdx.y; tile (bs, bt) with bt >= bs from a linear triangular index
-    const int inst = blockIdx.y;
-    const int sb = off.soff[inst], ns = off.soff[inst + 1] - sb;
+    // class blockIdx.y; tile (bs, bt) with bt >= bs from a linear triangular index
+    const int cl = blockIdx.y;
+    const int sb = off.csoff[cl], ns = off.csoff[cl + 1] - sb;
     const int32_t* slot_vtx = vtx_all + sb;
-    float* G = Gall + off.goff[inst];
+    float* G = Gall + off.goff[cl];
     const int tiles = (ns + 31) / 32;
     if ((int)blockIdx.x >= tiles * (tiles + 1) / 2) return;
     int idx = blockIdx.x, bs = 0;
@@ -1394,13 +1476,13 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
     }
 }
 
-void launch_delassus(cudaStream_t st, const Params& P, InstOff off, Slots sl, const float* Kcol,
+void launch_delassus(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
                      const int64_t* colptr, const int32_t* depth, const int32_t* parent, const int32_t* ptop,
                      float* G) {
-    if (P.NS == 0) return;
+    if (P.CS == 0) return;
     const int tiles = (P.ns_max + 31) / 32;
     const int ntri = tiles * (tiles + 1) / 2;
-    k_delassus<<<dim3(ntri, P.S), 256, 0, st>>>(off, sl.vtx, Kcol, colptr, depth, parent, ptop, G);
+    k_delassus<<<dim3(ntri, P.NCL), 256, 0, st>>>(off, csl.vtx, Kcol, colptr, depth, parent, ptop, G);
 }
 
 // D_jj = sum_{a,b in j} w_a w_b G_ab (unit directions; reading A18)
@@ -1409,7 +1491,7 @@ __global__ void k_djj(int C, InstOff off, DContact* Cs, const float* __restrict_
     if (c >= C) return;
     DContact& ct = Cs[c];
     const int sb = off.soff[ct.inst], ns = off.soff[ct.inst + 1] - sb;
-    const float* Gi = G + off.goff[ct.inst];
+    const float* Gi = G + off.goff[off.cls[ct.inst]];
     double d = 0.0;
     for (int p = 0; p < ct.nv; ++p)
         for (int q = 0; q < ct.nv; ++q)
@@ -1671,7 +1753,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     X.stamp = -1;
     X.ns = ns;
     X.csize = csize;
-    X.GAg = GA + off.goff[inst];
+    X.GAg = GA + off.gaoff[inst];
     // everything the prologue needs is precomputed (chain dot, k_active): plain loads only
     for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[9 * cb + e], true);
     for (int b = threadIdx.x; b < ns; b += blockDim.x) {

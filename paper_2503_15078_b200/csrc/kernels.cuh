@@ -42,16 +42,30 @@ struct Params {
     float k, mu, lam;     // projection stiffness and Lame parameters
     int C, NS;            // contacts, contact slots over all instances
     int nc_max, ns_max;   // per-instance maxima
+    int NCL, CS;          // slot-set classes, class slots
+    int cm_max;           // largest class (members)
     int cr_iters;
 };
 
-// per-instance offsets of the packed contact data
+// Offsets of the packed contact data.  Instances whose contact-vertex sets are equal form
+// a slot-set class: the ancestor chains, the chain-row list, the compact K copy Zc and the
+// Delassus Gram G depend only on K and that vertex set, so they are built once per class.
 struct InstOff {
-    const int* coff;       // [S+1] contacts
-    const int* soff;       // [S+1] slots
-    const int64_t* goff;   // [S+1] Delassus Gram blocks (ns_i^2 floats each)
-    const int* uoff;       // [S+1] ulist capacity (rows on the instance's chains)
-    const int64_t* zoff;   // [S+1] Zc / chain entries
+    const int* coff;        // [S+1] contacts per instance
+    const int* soff;        // [S+1] slots per instance (slot s of instance i <-> class slot s)
+    const int64_t* gaoff;   // [S+1] active blocks G_A per instance (ns_i^2 floats)
+    const int* cls;         // [S] class of each instance
+    const int* csoff;       // [NCL+1] class slots
+    const int64_t* goff;    // [NCL+1] Delassus Gram block per class (ns^2 floats)
+    const int* uoff;        // [NCL+1] chain-row list capacity per class
+    const int64_t* zoff;    // [NCL+1] chain entries / Zc per class
+    const int* cmoff;       // [NCL+1] class members in cmem
+    const int* cmem;        // [S] instances grouped by class (ascending within a class)
+};
+// class slots (global class-slot ids): vertex and class
+struct ClassSlots {
+    const int32_t* vtx;     // [CS] internal vertex (ascending within a class)
+    const int32_t* cls;     // [CS]
 };
 
 // per-iteration contact scratch (device, packed over instances)
@@ -116,9 +130,10 @@ void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
 void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
                            const float* T2, const float4* y, double4* x, const double4* xt, double4* v,
                            double inv_h, int finalize_v);
-void launch_chain_dot(cudaStream_t st, const Params& P, const float* Kcol, const int64_t* colptr,
-                      const int32_t* chain_off, const int32_t* chain_rows, const float4* y, Slots sl,
-                      CrContacts cc, const double4* x, ContactState cs);
+// grouped: one work item per (class slot, 32 class members); items int2 {class slot, member0}
+void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
+                      const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows, const float4* y,
+                      Slots sl, CrContacts cc, const double4* x, ContactState cs, int nitems, const int2* items);
 
 void launch_active(cudaStream_t st, const Params& P, InstOff off, CrContacts cc, Slots sl, ContactState cs,
                    CrActive act, const float* G, float* GA);
@@ -126,21 +141,23 @@ int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, 
               const float* GA, const double4* x, ContactState cs, CrActive act);
 // y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s over the rows of each instance's ulist
 // (int4 {row, s0, s1, zoff}); max_rows bounds the per-instance list length
+// grouped: items int2 {class, member0} (32 members per item)
 void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off, const int* ucount,
-                    const int4* ulist, const float* Zc, const double* wz, float4* y);
+                    const int4* ulist, const float* Zc, const double* wz, float4* y, int nitems, const int2* items);
 
 // --- per-contact-set kernels (all instances at once) ----------------------------
-void launch_delassus(cudaStream_t st, const Params& P, InstOff off, Slots sl, const float* Kcol,
+void launch_delassus(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
                      const int64_t* colptr, const int32_t* depth, const int32_t* parent, const int32_t* ptop,
                      float* G);
 void launch_djj(cudaStream_t st, const Params& P, InstOff off, DContact* c, const float* G);
-// ancestor-chain rows of every slot (chain order = Kcol order); flags rows per instance
-// (flag[i * n_f + row]); builds slotmap entries
-void launch_chain_rows(cudaStream_t st, const Params& P, Slots sl, const int32_t* chain_off, const int32_t* parent,
-                       const int32_t* ptop, int32_t* chain_rows, uint8_t* flag, int32_t* slotmap);
-// ucount[2 i] = rows listed for instance i, ucount[2 i + 1] = its values in Zc (zeroed by the caller)
-void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* flag, Slots sl, const int2* meta,
-                  int* ucount, int4* ulist, const float* Krow, float* Zc);
+// ancestor-chain rows of every class slot (chain order = Kcol order); flags rows per class
+// (flag[c * n_f + row]); slotmap[vtx * S + inst] = instance slot
+void launch_chain_rows(cudaStream_t st, const Params& P, ClassSlots csl, Slots sl, const int32_t* chain_off,
+                       const int32_t* parent, const int32_t* ptop, int32_t* chain_rows, uint8_t* flag,
+                       int32_t* slotmap);
+// ucount[2 c] = rows listed for class c, ucount[2 c + 1] = its values in Zc (zeroed by the caller)
+void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* flag, ClassSlots csl,
+                  const int2* meta, int* ucount, int4* ulist, const float* Krow, float* Zc);
 
 size_t cr_smem_bytes(int nc, int ns);   // the CR CTA's shared-memory footprint for (nc, ns) without G_A
 int cr_cluster_size(int S);             // CTAs per instance in the CR launch

@@ -95,6 +95,39 @@ def test_batched_incline_instances(simmod):
             xs[i], vs[i] = xg, vg
 
 
+def test_batched_mixed_slot_classes(simmod):
+    """Instances with different contact-vertex sets (slot-set classes of sizes 2, 1, 1 and
+    an empty one) on one handle, each against the oracle, re-synced per frame."""
+    th = 10.0
+    sc = scenes.incline_block(theta_deg=th, mu=0.5, nv=5, edge=0.1, youngs=1e8)
+    full = sc.contacts
+    half = len(full) // 2
+    sets = [full, full[:half], full[half - 3:], [], full]
+    S = len(sets)
+    s = make(simmod, sc, S)
+    s.set_contacts_batch(sets)
+    ors = []
+    for cs in sets:
+        o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=5)
+        if cs:
+            o.set_contacts(cs)
+        ors.append(o)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    xs = [sc.mesh.X.copy() for _ in range(S)]
+    vs = [np.zeros_like(sc.mesh.X) for _ in range(S)]
+    for f in range(4):
+        for i in range(S):
+            s.set_state(xs[i], vs[i], instance=i)
+        s.step(1, 5)
+        for i in range(S):
+            xg, vg = s.get_state(instance=i)
+            xo, vo, info = ors[i].frame(xs[i], vs[i])
+            assert np.abs(xg - xo).max() < tol, (f, i, np.abs(xg - xo).max())
+            xs[i], vs[i] = xg, vg
+    # instances 0 and 4 (same inputs, same class) stay bit-identical
+    assert np.array_equal(xs[0], xs[4])
+
+
 def test_batched_gingerbread_cfg5(simmod):
     """cfg5 structure on cfg3: 4 instances with their own initial velocities and
     obstacle offsets (scenes.batch_instance), contacts set in one batch call;
