@@ -147,6 +147,7 @@ struct sim_handle {
     DBuf<float> G, GA;   // Delassus Gram blocks and the CR's active blocks (fp32-exact values)
     DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res, rho;
     DBuf<int> act_na, act_idx, act_pos, act_con;   // CR active set (k_active)
+    DBuf<float4> wzT;
     DBuf<int32_t> chain_off, chain_rows, slotmap;
     DBuf<uint8_t> flag;
     DBuf<int> ucount;
@@ -723,7 +724,9 @@ static int commit_contacts(sim_handle* H) {
             const int m0 = cmoff[k] + m;
             if (m0 >= cmoff[k + 1] || csoff[k + 1] == csoff[k]) continue;
             it_sc.push_back(make_int2(k, m0));
-            for (int g = csoff[k]; g < csoff[k + 1]; ++g) it_cd.push_back(make_int2(g, m0));
+            const int gs = std::min(32, cmoff[k + 1] - m0);
+            const int stride = gs == 1 ? 1 : 8;   // grouped chain dot: one warp per class slot, 8 per CTA
+            for (int g = csoff[k]; g < csoff[k + 1]; g += stride) it_cd.push_back(make_int2(g, m0));
         }
     bool grew = false;
     const size_t cC = std::max(Ct, 1), cS = std::max(NSt, 1), cCS = std::max(CSt, 1);
@@ -737,6 +740,7 @@ static int commit_contacts(sim_handle* H) {
     CK(H->phi_abs.ensure(cC, grew)); CK(H->dxt.ensure(3 * cS, grew)); CK(H->wz.ensure(3 * cS, grew));
     CK(H->act_idx.ensure(cS, grew)); CK(H->act_pos.ensure(cS, grew)); CK(H->act_con.ensure(cS, grew));
     CK(H->cvtx.ensure(cCS, grew)); CK(H->ccls.ensure(cCS, grew));
+    if (S > 1) CK(H->wzT.ensure((size_t)std::max(nsm, 1) * S, grew));
     CK(H->chain_off.ensure(cCS + 1, grew)); CK(H->chain_rows.ensure(std::max<int64_t>(zoff[NCL], 1), grew));
     CK(H->Zc.ensure(std::max<int64_t>(zoff[NCL], 1), grew)); CK(H->ulist.ensure(std::max(uoff[NCL], 1), grew));
     CK(H->it_cd.ensure(std::max<size_t>(it_cd.size(), 1), grew));
@@ -881,7 +885,7 @@ static int commit_contacts(sim_handle* H) {
 // ---------------------------------------------------------------------------
 static ContactState cstate(sim_handle* H) {
     return ContactState{H->lam.p, H->theta.p, H->cdiag.p, H->hvec.p, H->hl.p, H->dxt.p, H->wz.p, H->phi_abs.p,
-                        H->cr_res.p, H->rho.p};
+                        H->cr_res.p, H->rho.p, H->S > 1 ? H->wzT.p : nullptr};
 }
 
 static void enqueue_kpass1(sim_handle* H, cudaStream_t st) {
@@ -961,8 +965,8 @@ static int enqueue_frame(sim_handle* H, int iters) {
             int e = launch_cr(st, P, off, H->dc.p, ccr, sl, H->GA.p, H->x.p, cs, act); nk++;
             if (e) return -e;
             MARK(KK_SCATTER);
-            launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->y.p, H->n_it_sc,
-                           H->it_sc.p); nk++;
+            launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->wzT.p, H->y.p,
+                           H->n_it_sc, H->it_sc.p); nk++;
         }
         MARK(KK_KPASS2);
         enqueue_kpass2(H, st, H->x.p, H->xt.p, H->v.p, 1.0 / H->h, k == iters - 1); nk++;

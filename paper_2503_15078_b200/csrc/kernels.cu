@@ -1093,12 +1093,17 @@ __global__ void __launch_bounds__(256) k_chain_dot(int S, InstOff off, ClassSlot
         }
         return;
     }
-    // lanes = instances of the group; warp w takes entries [32 w + 256 j, +32)
+    // lanes = instances of the group; warp w walks the whole chain of class slot it.x + w
+    // (8 neighbouring slots share most of their ancestors: their y rows hit in L1)
+    const int gw = g + w;
+    if (gw >= off.csoff[cl + 1]) return;
     const int inst = off.cmem[m0 + min(lane, gs - 1)];
-    for (int k0 = 32 * w; k0 < len; k0 += 32 * kWarps) {
-        const int n = min(32, len - k0);
-        const int rmine = lane < n ? __ldg(&chain_rows[o0 + k0 + lane]) : 0;
-        const float kmine = lane < n ? __ldg(&col[k0 + lane]) : 0.f;
+    const float* colw = Kcol + colptr[csl.vtx[gw]];
+    const int ow = chain_off[gw], lw = chain_off[gw + 1] - ow;
+    for (int k0 = 0; k0 < lw; k0 += 32) {
+        const int n = min(32, lw - k0);
+        const int rmine = lane < n ? __ldg(&chain_rows[ow + k0 + lane]) : 0;
+        const float kmine = lane < n ? __ldg(&colw[k0 + lane]) : 0.f;
         float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll 8
         for (int q = 0; q < n; ++q) {
@@ -1113,20 +1118,7 @@ __global__ void __launch_bounds__(256) k_chain_dot(int S, InstOff off, ClassSlot
         a1 += (double)f1;
         a2 += (double)f2;
     }
-    s_red[0][w][lane] = a0;
-    s_red[1][w][lane] = a1;
-    s_red[2][w][lane] = a2;
-    __syncthreads();
-    if (threadIdx.x < gs) {
-        double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-#pragma unroll
-        for (int q = 0; q < kWarps; ++q) {
-            t0 += s_red[0][q][lane];
-            t1 += s_red[1][q][lane];
-            t2 += s_red[2][q][lane];
-        }
-        chain_rho(S, inst, off.soff[inst] + sloc, t0, t1, t2, cc, x, cs);
-    }
+    if (lane < gs) chain_rho(S, inst, off.soff[inst] + (gw - off.csoff[cl]), a0, a1, a2, cc, x, cs);
 }
 
 void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
@@ -1295,8 +1287,8 @@ void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* 
 //   larger groups: warp per row, lane = instance (coalesced y), slots in sequence.
 // ----------------------------------------------------------------------------
 __global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist,
-                          const float* __restrict__ Zc, const double* __restrict__ wz, float4* __restrict__ y,
-                          const int2* __restrict__ items) {
+                          const float* __restrict__ Zc, const double* __restrict__ wz,
+                          const float4* __restrict__ wzT, float4* __restrict__ y, const int2* __restrict__ items) {
     const int2 it = items[blockIdx.y];
     const int c = it.x, m0 = it.y, gs = min(32, off.cmoff[c + 1] - m0);
     const int lane = threadIdx.x & 31;
@@ -1340,19 +1332,29 @@ __global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, co
         }
         return;
     }
+    // lanes = instances: wz^T rows (instance-minor float4) read coalesced; fp32 FMAs over 32-slot
+    // chunks folded into fp64 (as the K-passes)
     const bool live = lane < gs;
     const int inst = off.cmem[m0 + min(lane, gs - 1)];
-    const double* wzi = wz + 3 * (size_t)off.soff[inst];
     for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += nw) {
         const int4 u = ul[e];
         const float* zr = Zc + u.w - u.y;
         double a0 = 0, a1 = 0, a2 = 0;
-#pragma unroll 4
-        for (int s = u.y; s < u.z; ++s) {
-            const double kv = (double)__ldg(&zr[s]);
-            a0 = fma(kv, __ldg(&wzi[3 * s]), a0);
-            a1 = fma(kv, __ldg(&wzi[3 * s + 1]), a1);
-            a2 = fma(kv, __ldg(&wzi[3 * s + 2]), a2);
+        for (int s0 = u.y; s0 < u.z; s0 += 32) {
+            const int n = min(32, u.z - s0);
+            const float zmine = lane < n ? __ldg(&zr[s0 + lane]) : 0.f;
+            float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+#pragma unroll 8
+            for (int q = 0; q < n; ++q) {
+                const float kv = __shfl_sync(0xffffffffu, zmine, q);
+                const float4 wv = __ldg(&wzT[(size_t)(s0 + q) * S + inst]);
+                f0 = fmaf(kv, wv.x, f0);
+                f1 = fmaf(kv, wv.y, f1);
+                f2 = fmaf(kv, wv.z, f2);
+            }
+            a0 += (double)f0;
+            a1 += (double)f1;
+            a2 += (double)f2;
         }
         if (live) {
             const size_t iy = (size_t)u.x * S + inst;
@@ -1363,11 +1365,12 @@ __global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, co
 }
 
 void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off, const int* ucount,
-                    const int4* ulist, const float* Zc, const double* wz, float4* y, int nitems, const int2* items) {
+                    const int4* ulist, const float* Zc, const double* wz, const float4* wzT, float4* y, int nitems,
+                    const int2* items) {
     if (P.NS == 0 || nitems == 0) return;
     int gx = (max_rows + 7) / 8;
     if (nitems > 1) gx = std::min(gx, std::max(1, (148 * 8 + nitems - 1) / nitems));
-    k_scatter<<<dim3(gx, nitems), 256, 0, st>>>(P.S, off, ucount, ulist, Zc, wz, y, items);
+    k_scatter<<<dim3(gx, nitems), 256, 0, st>>>(P.S, off, ucount, ulist, Zc, wz, wzT, y, items);
 }
 
 // ----------------------------------------------------------------------------
@@ -1929,6 +1932,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
         wz_g[3 * b] = w0;
         wz_g[3 * b + 1] = w1;
         wz_g[3 * b + 2] = w2;
+        if (cs.wzT) cs.wzT[(size_t)b * S + inst] = make_float4((float)w0, (float)w1, (float)w2, 0.f);
     }
     if (threadIdx.x == 0 && rank == 0) cs.cr_res[inst] = sqrt(res);
     cr_stamp(21);

@@ -80,6 +80,7 @@ struct ContactState {
     double* phi_abs;  // [C] |phi_n| (stats)
     double* cr_res;   // [S]
     double* rho;      // [3 C] Schur RHS h - Theta J x~ (from the chain dot)
+    float4* wzT;      // [ns_max][S] wz, class-slot-major / instance-minor (grouped scatter; S > 1)
 };
 
 // active contact vertices of the current iteration (theta != 0 on an incident row)
@@ -143,7 +144,8 @@ int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, 
 // (int4 {row, s0, s1, zoff}); max_rows bounds the per-instance list length
 // grouped: items int2 {class, member0} (32 members per item)
 void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off, const int* ucount,
-                    const int4* ulist, const float* Zc, const double* wz, float4* y, int nitems, const int2* items);
+                    const int4* ulist, const float* Zc, const double* wz, const float4* wzT, float4* y, int nitems,
+                    const int2* items);
 
 // --- per-contact-set kernels (all instances at once) ----------------------------
 void launch_delassus(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
