@@ -84,9 +84,12 @@ __device__ __forceinline__ void jacobi3(float S[3][3], float V[3][3]) {
             const int r = 3 - p - q;
             float apq = S[p][q];
             if (fabsf(apq) <= 1e-30f) continue;
-            float theta = (S[q][q] - S[p][p]) / (2.f * apq);
+            // hardware-approximate reciprocal / square root (MUFU, ~1 ulp): no IEEE fix-up paths;
+            // c and s come from the same t, so the rotation stays orthogonal to ~1e-7
+            float theta = __fdividef(S[q][q] - S[p][p], 2.f * apq);
             float at = fabsf(theta);
-            float t = at > 1e15f ? 0.5f / at : 1.f / (at + sqrtf(theta * theta + 1.f));
+            const float w = theta * theta + 1.f;
+            float t = at > 1e15f ? __fdividef(0.5f, at) : __fdividef(1.f, at + w * rsqrtf(w));
             t = theta < 0.f ? -t : t;
             float c = rsqrtf(t * t + 1.f);
             float s = t * c;
@@ -119,8 +122,9 @@ __device__ __forceinline__ void swapcol(float V[3][3], float* e, int a, int b) {
 }
 
 // NH objective in sigma space: k/2|p-sig|^2 + mu/2(|p|^2-3) - mu lnJ + lam/2 ln^2 J
+// (ln J = ln(p0 p1 p2): one hardware log2 instead of three IEEE logs)
 __device__ __forceinline__ float nh_f(const float p[3], const float sg[3], float k, float mu, float lam) {
-    float lnJ = logf(p[0]) + logf(p[1]) + logf(p[2]);
+    float lnJ = __logf(p[0] * p[1] * p[2]);
     float d0 = p[0] - sg[0], d1 = p[1] - sg[1], d2 = p[2] - sg[2];
     return 0.5f * k * (d0 * d0 + d1 * d1 + d2 * d2) +
            0.5f * mu * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2] - 3.f) - mu * lnJ + 0.5f * lam * lnJ * lnJ;
@@ -148,8 +152,8 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
     float scale = fmaxf(1.f, sqrtf(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]));
 #pragma unroll 1
     for (int it = 0; it < 16; ++it) {
-        float lnJ = logf(p[0]) + logf(p[1]) + logf(p[2]);
-        float iv[3] = {1.f / p[0], 1.f / p[1], 1.f / p[2]};
+        float lnJ = __logf(p[0] * p[1] * p[2]);
+        float iv[3] = {__fdividef(1.f, p[0]), __fdividef(1.f, p[1]), __fdividef(1.f, p[2])};
         float g[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) g[i] = k * (p[i] - sg[i]) + mu * p[i] - mu * iv[i] + lam * lnJ * iv[i];
@@ -169,7 +173,7 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
         float dd[3];
         bool ok = fabsf(det) > 0.f && isfinite(det);
         if (ok) {
-            float id = 1.f / det;
+            float id = __fdividef(1.f, det);
             float c10 = H[0][2] * H[2][1] - H[0][1] * H[2][2];
             float c11 = H[0][0] * H[2][2] - H[0][2] * H[2][0];
             float c12 = H[0][1] * H[2][0] - H[0][0] * H[2][1];
@@ -183,7 +187,7 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
             ok = slope < 0.f && isfinite(slope);
         }
         if (!ok) {
-            float s = -1.f / (k + mu);
+            float s = __fdividef(-1.f, k + mu);
             dd[0] = s * g[0];
             dd[1] = s * g[1];
             dd[2] = s * g[2];
@@ -262,17 +266,21 @@ __global__ void __launch_bounds__(128) k_local(Params P, const int4* __restrict_
 #pragma unroll
         for (int j = 0; j < 3; ++j) FV[i][j] = F[i][0] * V[0][j] + F[i][1] * V[1][j] + F[i][2] * V[2][j];
     float U[3][3];
-    float n0 = sqrtf(FV[0][0] * FV[0][0] + FV[1][0] * FV[1][0] + FV[2][0] * FV[2][0]);
-    if (n0 > 1e-30f) {
-        U[0][0] = FV[0][0] / n0; U[1][0] = FV[1][0] / n0; U[2][0] = FV[2][0] / n0;
+    const float q0 = FV[0][0] * FV[0][0] + FV[1][0] * FV[1][0] + FV[2][0] * FV[2][0];
+    float n0 = q0 > 0.f ? q0 * rsqrtf(q0) : 0.f;
+    if (q0 > 1e-36f) {
+        const float r0 = rsqrtf(q0);
+        U[0][0] = FV[0][0] * r0; U[1][0] = FV[1][0] * r0; U[2][0] = FV[2][0] * r0;
     } else {
         U[0][0] = 1.f; U[1][0] = 0.f; U[2][0] = 0.f;
     }
     float dt = U[0][0] * FV[0][1] + U[1][0] * FV[1][1] + U[2][0] * FV[2][1];
     float w0 = FV[0][1] - dt * U[0][0], w1 = FV[1][1] - dt * U[1][0], w2 = FV[2][1] - dt * U[2][0];
-    float n1 = sqrtf(w0 * w0 + w1 * w1 + w2 * w2);
+    const float q1 = w0 * w0 + w1 * w1 + w2 * w2;
+    float n1 = q1 > 0.f ? q1 * rsqrtf(q1) : 0.f;
     if (n1 > 1e-30f * fmaxf(1.f, n0)) {
-        U[0][1] = w0 / n1; U[1][1] = w1 / n1; U[2][1] = w2 / n1;
+        const float r1 = rsqrtf(q1);
+        U[0][1] = w0 * r1; U[1][1] = w1 * r1; U[2][1] = w2 * r1;
     } else {   // any unit vector orthogonal to u0
         float a0 = U[0][0], a1 = U[1][0], a2 = U[2][0];
         float e0 = fabsf(a0) < 0.577f ? 1.f : 0.f, e1 = e0 == 0.f && fabsf(a1) < 0.577f ? 1.f : 0.f;
@@ -1526,19 +1534,22 @@ void launch_djj(cudaStream_t st, const Params& P, InstOff off, DContact* c, cons
 // ----------------------------------------------------------------------------
 constexpr int kRptMax = 6;   // rows per thread: m = 3 nc <= kRpt * kCrThreads (kernel templated on kRpt)
 
+// shared-memory layout of one CR CTA; W and q are sized by the active count na, the
+// contact directions c9 are staged only when they fit next to this CTA's rows of G_A
 struct CrLayout {
     int m, nc, ns;
-    size_t r, th, cd, c9, s0, W, q, aidx, apos, acon, red, mbar, gA, total;
-    __host__ __device__ CrLayout(int nc_, int ns_) : m(3 * nc_), nc(nc_), ns(ns_) {
+    size_t r, th, cd, s0, aidx, apos, acon, red, mbar, W, q, c9, gA, total;
+    __host__ __device__ CrLayout(int nc_, int ns_, int na, bool with_c9) : m(3 * nc_), nc(nc_), ns(ns_) {
         size_t o = 0;
         auto take = [&](size_t bytes) { size_t at = o; o += (bytes + 15) & ~size_t(15); return at; };
         r = take(8 * (size_t)m);
         th = take(4 * (size_t)m); cd = take(4 * (size_t)m);
-        c9 = take(4 * 9 * (size_t)nc); s0 = take(4 * (size_t)nc);
-        W = take(8 * 3 * (size_t)ns); q = take(8 * 2 * 3 * (size_t)ns);
+        s0 = take(4 * (size_t)nc);
         aidx = take(4 * (size_t)ns); apos = take(4 * (size_t)ns); acon = take(4 * (size_t)ns);
         red = take(8 * 2 * 3 * (kCrThreads / 32));   // double-buffered 3 doubles per warp
         mbar = take(32);                              // two exchange mbarriers (one per q buffer)
+        W = take(8 * 3 * (size_t)na); q = take(8 * 2 * 3 * (size_t)na);
+        c9 = with_c9 ? take(4 * 9 * (size_t)nc) : 0;
         gA = o;
         total = o;
     }
@@ -1589,7 +1600,7 @@ __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, doub
 template <int kRpt>
 __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int buf, double (&Ar)[kRpt]) {
     const int na = X.na;
-    double* qb = X.q + (size_t)buf * 3 * X.ns;   // SoA: q0 | q1 | q2
+    double* qb = X.q + (size_t)buf * 3 * X.na;   // SoA: q0 | q1 | q2
     const unsigned bar = X.mbar + 8u * (unsigned)buf;
     if (threadIdx.x == 0 && na > 0)   // this phase expects 24 bytes per row of G_A from the peers
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(24 * na) : "memory");
@@ -1725,11 +1736,18 @@ __global__ void __launch_bounds__(kCrThreads, 1)
         if (threadIdx.x == 0 && rank == 0) cs.cr_res[inst] = 0.0;
         return;
     }
-    const CrLayout L(nc, ns);
     const int m = 3 * nc;
     const double h = P.h;
     const int S = P.S;
     cr_stamp(0);
+    const int na = act.na[inst];
+    const int per = (na + csize - 1) / csize;
+    const int i0 = min(na, rank * per), i1 = min(na, i0 + per);
+    const size_t needA = (size_t)(i1 - i0) * na * sizeof(float);
+    // prefer G_A rows in shared memory; stage c9 too when both fit
+    const bool c9s = CrLayout(nc, ns, na, true).total + needA <= kCrMaxSmem ||
+                     CrLayout(nc, ns, na, false).total + needA > kCrMaxSmem;
+    const CrLayout L(nc, ns, na, c9s);
     CrInst I{C + cb, sl.scp + sb, sl.sci, sl.scw, cb, sb, S, inst};
     double* th_g = cs.theta + 3 * cb;
     double* cd_g = cs.cdiag + 3 * cb;
@@ -1742,7 +1760,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     X.r = (double*)(smraw + L.r);
     X.th = (float*)(smraw + L.th);
     X.cd = (float*)(smraw + L.cd);
-    X.c9 = (float*)(smraw + L.c9);
+    X.c9 = c9s ? (float*)(smraw + L.c9) : const_cast<float*>(cc.c9 + 9 * (size_t)cb);
     X.s0 = (int*)(smraw + L.s0);
     X.W = (double*)(smraw + L.W);
     X.q = (double*)(smraw + L.q);
@@ -1758,7 +1776,8 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     X.csize = csize;
     X.GAg = GA + off.gaoff[inst];
     // everything the prologue needs is precomputed (chain dot, k_active): plain loads only
-    for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[9 * cb + e], true);
+    if (c9s)
+        for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[9 * cb + e], true);
     for (int b = threadIdx.x; b < ns; b += blockDim.x) {
         cp_async4(&X.aidx[b], &act.aidx[sb + b], true);
         cp_async4(&X.apos[b], &act.apos[sb + b], true);
@@ -1769,19 +1788,14 @@ __global__ void __launch_bounds__(kCrThreads, 1)
         const int s0g = cc.s0[cb + c];
         X.s0[c] = s0g >= 0 ? s0g - sb : -1;
     }
-    const int na = act.na[inst];
     X.na = na;
-    {
-        const int per = (na + csize - 1) / csize;
-        X.i0 = min(na, rank * per);
-        X.i1 = min(na, X.i0 + per);
-        const size_t cap = (kCrMaxSmem - L.total) / sizeof(float);
-        X.gA_smem = (size_t)(X.i1 - X.i0) * na <= cap;
-        if (X.gA_smem) {
-            const float* src = X.GAg + (size_t)X.i0 * na;
-            const int n = (X.i1 - X.i0) * na;
-            for (int e = threadIdx.x; e < n; e += blockDim.x) X.gA[e] = __ldcg(&src[e]);
-        }
+    X.i0 = i0;
+    X.i1 = i1;
+    X.gA_smem = L.total + needA <= kCrMaxSmem;
+    if (X.gA_smem) {
+        const float* src = X.GAg + (size_t)X.i0 * na;
+        const int n = (X.i1 - X.i0) * na;
+        for (int e = threadIdx.x; e < n; e += blockDim.x) X.gA[e] = __ldcg(&src[e]);
     }
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
 #pragma unroll
@@ -1943,7 +1957,7 @@ int read_cr_clock(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, g_cr_clock, sizeof(unsigned long long) * 32);
 }
 
-size_t cr_smem_bytes(int nc, int ns) { return CrLayout(nc, ns).total; }
+size_t cr_smem_bytes(int nc, int ns) { return CrLayout(nc, ns, ns, false).total; }
 
 int cr_cluster_size(int S) {
     int c = kCluster;
