@@ -1,16 +1,19 @@
 """Benchmark of the sparse-inverse local-global hot path (arXiv 2503.15078).
 
-Workload (BASELINE.json configs[2]): gingerbread-class
-silhouette slab, 19 691 vertices (59.1k DoF) / 93 600 tets, Neo-Hookean
-E = 1e6, nu = 0.3, rho = 1000, h = 0.01, 800 contact points (3 rows each),
-5 L-G iterations and 10 CR iterations per frame, moving head handle.
+Workload (BASELINE.json configs[4]): a batch of 1024
+independent gingerbread-class scenes (configs[2] / cfg3: 19 691 vertices,
+59.1k DoF, 93 600 tets, Neo-Hookean E = 1e6, nu = 0.3, rho = 1000, h = 0.01,
+800 contact points x 3 rows, 5 L-G and 10 CR iterations per frame, moving
+head handle), each with its own initial velocity and obstacle offset, split
+evenly over the GPUs (strong scaling; one handle per GPU holds its share as
+instances sharing K).  The single-scene latency (one cfg3 scene per GPU, the
+paper's ms per L-G iteration) is measured in the same run ("single_scene").
 
-One step = one frame of Alg. 4: sim_set_contacts (rows + Delassus Gram +
-preconditioner on the device, as the paper's per-frame `Schur.`) + predict +
-5 x (local, RHS, K-pass 1, contacts + CR, correction, K-pass 2) + integrate.
-Metric: scene-iterations/s over all ranks (= 1000 / ms per L-G iteration per
-scene at N = 1).  Multi-GPU: one independent scene replica per rank (weak
-scaling); NCCL only gathers per-rank timings after the timed region.
+One step = one frame of Alg. 4 for every scene: contact sets re-set (rows +
+Delassus Gram + preconditioner on the device, as the paper's per-frame
+`Schur.`) + predict + 5 x (local, RHS, K-pass 1, contacts + CR, correction,
+K-pass 2) + integrate.  Metric: scene-iterations/s over all ranks.  NCCL only
+reduces per-rank timings after the timed region.
 
 `--impl reference` runs the fp64 CPU oracle (oracle/) on the same workload:
 each step is one L-G iteration of cfg3 with the per-frame Delassus solve
@@ -41,8 +44,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--instances", type=int, default=1,
-                    help="cfg5: scenes per GPU sharing K (1 = the single-scene cfg3 workload)")
+    ap.add_argument("--instances", type=int, default=0,
+                    help="scenes per GPU sharing K (default: cfg5's 1024 scenes split over the GPUs)")
     return ap.parse_args()
 
 
@@ -170,33 +173,43 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
+def instance_ids(ws, rank, per_gpu=0, total=1024):
+    """Global cfg5 instance ids of this rank: the 1024-scene batch split evenly over the
+    ranks (strong scaling), or per_gpu scenes per rank (weak scaling)."""
+    S = per_gpu if per_gpu else max(1, total // ws)
+    return list(range(rank * S, rank * S + S))
+
+
+def reduce_max(v, ws, device=None):
+    """Max over ranks of a per-rank timing (NCCL on the GPU box, gloo in the CPU tests)."""
+    if ws == 1:
+        return float(v)
     import torch
     import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
+
+def measure(args, S, rank, ws, dev, stream, full=True):
+    """Time `args.steps` frames of S cfg3 instances (one handle) on this rank.
+    Returns a dict of per-rank numbers (device ms, kernel profile, e2e, ...)."""
+    import torch
     import scenes
     import paper_2503_15078_b200 as simlib
 
-    ws, rank, local = dist_env()
-    if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.Stream(dev)          # graph capture needs a non-default stream
-    torch.cuda.set_stream(stream)
-
     sc = scenes.make_scene("cfg3")
-    S = max(1, args.instances)
     s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, n_instances=S)
     s.set_stream(stream.cuda_stream)
     s.set_pin_velocity(sc.pin_velocity)
-    # cfg5 instances rank * S + i: own initial velocity and obstacle offset (scenes.batch_instance_params)
+    # cfg5 instance g = rank * S + i: own initial velocity and obstacle offset (scenes.batch_instance_params);
+    # the single-scene workload (S = 1) keeps cfg3's obstacles
     base = simlib.contacts_to_array(sc.contacts)
     arrs, v0s = [], np.empty((S, sc.mesh.n_v, 3))
-    for i in range(S):
-        v0s[i], delta = scenes.batch_instance_params(sc, rank * S + i)
+    for i, g in enumerate(instance_ids(ws, rank, per_gpu=S)):
+        v0s[i], delta = scenes.batch_instance_params(sc, g)
         a = base.copy()
-        if S > 1:   # the single-scene workload keeps cfg3's obstacles
+        if S > 1:
             a["offset"] += a["normal"][:, 2] * delta
         arrs.append(a)
     packed = (np.concatenate(arrs), np.full(S, len(base), np.int32))
@@ -205,25 +218,31 @@ def run_ours(args):
     st0 = s.stats()
 
     def step():
-        s.set_contacts_batch(packed=packed)
+        s.set_contacts_batch(packed=packed)   # contacts re-set every frame (reading A23)
         s.step(1, ITERS)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > L2
-
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if ws > 1:
-        dist.barrier()
+        torch.distributed.barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with Clocks(local) as clk:
+    with Clocks(int(str(dev).split(":")[-1]) if ":" in str(dev) else 0) as clk:
         for i in range(args.steps):
             flush.zero_()                       # untimed L2 flush between timed steps
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    total_ms = float(np.sum([a.elapsed_time(b) for a, b in ev]))
+    out = {"S": S, "total_ms": total_ms, "clocks": clk.summary(), "st0": st0, "n_v": sc.mesh.n_v}
+    if not full:
+        s.close()
+        return out
     # per-kernel device time from a separate pass with in-graph events (not in the timed region)
     ktimes = {k: 0.0 for k in simlib.KERNEL_KINDS}
     s.set_profiling(True)
@@ -235,6 +254,7 @@ def run_ours(args):
         kt = s.kernel_times()
         for k in ktimes:
             ktimes[k] += kt[k]
+    s.set_profiling(False)
     # host / commit breakdown (diagnostic, outside the timed region)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -242,56 +262,74 @@ def run_ours(args):
     host_set_ms = 1000 * (time.perf_counter() - t0)
     b0, b1, b2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     b0.record(stream)
-    t0 = time.perf_counter()
     s.step(1, ITERS)            # commit (pack + upload + Delassus) then the frame graph
-    host_step_ms = 1000 * (time.perf_counter() - t0)
     b1.record(stream)
     s.step(1, ITERS)            # frame graph only (contacts unchanged)
     b2.record(stream)
     torch.cuda.synchronize()
-    breakdown = {"host_set_contacts_ms": host_set_ms, "host_step_call_ms": host_step_ms,
-                 "device_commit_plus_frame_ms": b0.elapsed_time(b1), "device_frame_only_ms": b1.elapsed_time(b2)}
-    s.set_profiling(False)
-    torch.cuda.synchronize()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = float(np.sum(step_ms))
-    if ws > 1:
-        dist.barrier()
-        t = torch.tensor([total_ms], device=dev)
-        allt = [torch.zeros_like(t) for _ in range(ws)]
-        dist.all_gather(allt, t)                 # NCCL: gather per-rank timings only
-        total_ms = max(float(a.item()) for a in allt)
-    ms_per_step = total_ms / args.steps
-    scenes_total = ws * S
-    value = scenes_total * args.steps * ITERS / (total_ms / 1000.0)
-
-    # ---- e2e through the public API with host buffers: contacts in, state out
+    out["breakdown"] = {"host_set_contacts_ms": host_set_ms, "device_commit_plus_frame_ms": b0.elapsed_time(b1),
+                        "device_frame_only_ms": b1.elapsed_time(b2)}
+    out["ktimes"] = ktimes
+    # e2e through the public API with host buffers: contacts in (H2D), positions of all instances out (D2H)
     e2e_steps = max(3, args.steps // 2)
+    xh = np.empty((S, sc.mesh.n_v, 3))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    xh = np.empty((S, sc.mesh.n_v, 3))
     for _ in range(e2e_steps):
         step()
         s.get_positions(out=xh)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    wall_e2e = time.perf_counter() - t0
-    if ws > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = scenes_total * e2e_steps * ITERS / (e2e_ms / 1000.0)
+    out["e2e_ms"] = e0.elapsed_time(e1)
+    out["e2e_steps"] = e2e_steps
+    out["e2e_wall_s"] = time.perf_counter() - t0
     st = s.stats()
-    h2d = int(st["h2d_contact_bytes"])
-    d2h = 32 * sc.mesh.n_v * S
+    out["h2d"] = int(st["h2d_contact_bytes"])
+    out["d2h"] = 24 * sc.mesh.n_v * S
+    out["kernels_per_frame"] = int(st["kernels_per_frame"])
+    s.close()
+    return out
 
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)          # graph capture needs a non-default stream
+    torch.cuda.set_stream(stream)
+
+    # cfg5 (BASELINE configs[4]): 1024 cfg3 instances sharded over the ranks (strong scaling);
+    # --instances S fixes the per-GPU count instead (weak scaling)
+    total = 1024
+    S = args.instances if args.instances else max(1, total // ws)
+    scaling = "weak" if args.instances else "strong"
+    r = measure(args, S, rank, ws, dev, stream, full=True)
+
+    def max_over_ranks(v):   # NCCL: per-rank timings only, after the timed regions
+        return reduce_max(v, ws, dev)
+
+    total_ms = max_over_ranks(r["total_ms"])
+    e2e_ms = max_over_ranks(r["e2e_ms"])
+    # single-scene latency (cfg3, S = 1): the paper-comparable ms per L-G iteration
+    r1 = measure(args, 1, rank, ws, dev, stream, full=False) if S > 1 else r
+    single_ms = max_over_ranks(r1["total_ms"])
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
         return
+    scenes_total = ws * S
+    ms_per_step = total_ms / args.steps
+    value = scenes_total * args.steps * ITERS / (total_ms / 1000.0)
+    e2e_value = scenes_total * r["e2e_steps"] * ITERS / (e2e_ms / 1000.0)
+    ktimes = r["ktimes"]
+    st0 = r["st0"]
 
     # ---- roofline of the dominant kernel
     peak, peak_kind = measured_peak()
@@ -308,8 +346,7 @@ def run_ours(args):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": ncu_traffic(dom), "kernel": dom, "peak_source": peak_kind,
                     "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": avg_s * 1e6,
-                    "note": "K (fp32 values-only, 2 copies = %.1f MB) vs 126 MB L2: passes re-read from HBM; "
-                            "dominant HBM-bound kernel (k_cr is latency-bound, see kernel_us_per_step)"
+                    "note": "K (fp32 values-only, 2 copies = %.1f MB) vs 126 MB L2: passes re-read from HBM"
                             % (8 * nnz / 1e6)}
     else:
         # batched passes: each K value meets 3 S right-hand sides -> FP32 FMA-issue bound
@@ -321,7 +358,7 @@ def run_ours(args):
                     "frac": achieved / fp32_peak, "traffic": ncu_traffic(dom + "_batched"), "kernel": dom,
                     "peak_source": "derived: 148 SMs x 128 FP32 FMA lanes x 2 x 1965 MHz (B200_PROFILING.md)",
                     "algorithmic_flops_per_launch": flops, "avg_launch_us": avg_s * 1e6,
-                    "note": "K read once per 128-instance chunk; 6 flop per nnz per instance"}
+                    "note": "K tile read once per 128-instance chunk; 6 flop per nnz per instance (K u and K^T y)"}
     kernels_us = {k: 1000.0 * v / args.steps for k, v in ktimes.items()}
 
     cpu = None
@@ -329,30 +366,31 @@ def run_ours(args):
         cv, _, sample = oracle_sample(1)
         cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
                "host_cpus": os.cpu_count()}
-    clocks = clk.summary()
-    # + per-step set_contacts kernels: chain rows, row list, Zc fill, Delassus Gram, D_jj
-    gpu_launches = st["kernels_per_frame"] * args.steps + 5 * args.steps
+    # + per-step contact commit kernels: chain rows, row list, Zc fill, Delassus Gram, D_jj
+    gpu_launches = r["kernels_per_frame"] * args.steps + 5 * args.steps
+    wl = ("cfg5: %d x " % scenes_total if S > 1 else "") + \
+         "cfg3 gingerbread-class slab 19691 v / 93600 t, 800 contacts x 3 rows, NH E=1e6 nu=0.3, h=0.01, " \
+         "5 L-G + 10 CR per frame, contacts re-set every frame"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": ("cfg5: %d x " % (ws * S) if S > 1 else "") +
-                               "cfg3 gingerbread-class slab 19691 v / 93600 t, 800 contacts x 3 rows, "
-                               "NH E=1e6 nu=0.3, h=0.01, 5 L-G + 10 CR per frame, set_contacts every frame",
-                   "global_batch": ws * S, "scenes_per_gpu": S,
-                   "parallelism": f"instances{S}xdp{ws}" if S > 1 else f"replicas{ws}",
+        "config": {"workload": wl, "global_batch": scenes_total, "scenes_per_gpu": S,
+                   "parallelism": f"instances{S}xdp{ws}",
                    "l2": "flushed (256 MB write) between timed steps"},
-        "ms_per_lg_iteration": ms_per_step / ITERS,   # all S instances of one GPU advance together
-        "paper_context_ms_per_iteration": 11.95,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms / e2e_steps, "wall_s": wall_e2e},
+        "single_scene": {"workload": "cfg3 (one instance per GPU)",
+                         "ms_per_lg_iteration": single_ms / args.steps / ITERS,
+                         "scene_iters_per_s": args.steps * ITERS / (single_ms / 1000.0),
+                         "paper_context_ms_per_iteration": 11.95},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
+                "ms_per_step": e2e_ms / r["e2e_steps"], "wall_s": r["e2e_wall_s"]},
         "gpu_launches": gpu_launches,
         "kernel_us_per_step": kernels_us,
         "kernel_share": share,
-        "breakdown": breakdown,
+        "breakdown": r["breakdown"],
         "roofline": roofline,
         "cpu_baseline": cpu,
-        "clocks": clocks,
+        "clocks": r["clocks"],
         "nnz_K": nnz, "n_free": nf, "etree_height": int(st0["etree_height"]),
     }
     print(json.dumps(line), flush=True)

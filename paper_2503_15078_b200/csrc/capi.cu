@@ -42,6 +42,11 @@ static int fail(int code, const char* fmt, ...) {
     } while (0)
 
 template <class T>
+struct DPtr {   // a view into a device arena
+    T* p = nullptr;
+};
+
+template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
@@ -133,22 +138,26 @@ struct sim_handle {
     bool dirty = false;
     int C = 0, NS = 0, nc_max = 0, ns_max = 0, urows_max = 0;
     std::vector<int> coff_h, soff_h;
-    DBuf<DContact> dc;
-    DBuf<float> cc9;
-    DBuf<int32_t> cs0, cv0, cc1;
-    DBuf<int32_t> slot_vtx, slot_inst, scp, sci;
-    DBuf<float> scw;
-    DBuf<int> coff, soff, uoff, cls, csoff, cmoff, cmem;
-    DBuf<int64_t> goff, zoff, gaoff;
-    DBuf<int32_t> cvtx, ccls;        // class slots
-    DBuf<int2> it_cd, it_sc;         // grouped chain-dot / scatter work items
+    // uploaded contact data: one device arena with the staging layout (one H2D copy per commit)
+    DBuf<unsigned char> arena;
+    std::vector<size_t> arena_layout;
+    DPtr<DContact> dc;
+    DPtr<float> cc9;
+    DPtr<int32_t> cs0, cv0, cc1;
+    DPtr<int32_t> slot_vtx, slot_inst, scp, sci;
+    DPtr<float> scw;
+    DPtr<int> coff, soff, uoff, cls, csoff, cmoff, cmem;
+    DPtr<int64_t> goff, zoff, gaoff;
+    DPtr<int32_t> cvtx, ccls;        // class slots
+    DPtr<int2> it_cd, it_sc;         // grouped chain-dot / scatter work items
+    DPtr<int32_t> chain_off;
     int NCL = 0, CS = 0, cm_max = 0, n_it_cd = 0, n_it_sc = 0;
     std::vector<int64_t> gaoff_h;
     DBuf<float> G, GA;   // Delassus Gram blocks and the CR's active blocks (fp32-exact values)
     DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res, rho;
     DBuf<int> act_na, act_idx, act_pos, act_con;   // CR active set (k_active)
     DBuf<float4> wzT;
-    DBuf<int32_t> chain_off, chain_rows, slotmap;
+    DBuf<int32_t> chain_rows, slotmap;
     DBuf<uint8_t> flag;
     DBuf<int> ucount;
     DBuf<int4> ulist;
@@ -386,12 +395,7 @@ static int upload_all(sim_handle* H) {
         CK(cudaMemsetAsync(H->counters.p, 0, ncnt * sizeof(int), st));
     }
     // per-instance contact scalars
-    CK(H->coff.alloc(S + 1)); CK(H->soff.alloc(S + 1)); CK(H->uoff.alloc(S + 1)); CK(H->gaoff.alloc(S + 1));
-    CK(H->goff.alloc(S + 1)); CK(H->zoff.alloc(S + 1)); CK(H->cls.alloc(S)); CK(H->csoff.alloc(S + 1));
-    CK(H->cmoff.alloc(S + 1)); CK(H->cmem.alloc(S));
     CK(H->cr_res.alloc(S)); CK(H->act_na.alloc(S)); CK(H->ucount.alloc(2 * (size_t)S));
-    CK(cudaMemsetAsync(H->coff.p, 0, (S + 1) * sizeof(int), st));
-    CK(cudaMemsetAsync(H->soff.p, 0, (S + 1) * sizeof(int), st));
     CK(cudaMemsetAsync(H->cr_res.p, 0, S * sizeof(double), st));
     CK(H->flag.alloc((size_t)S * nf));
     CK(H->slotmap.alloc((size_t)nf * S));
@@ -730,22 +734,16 @@ static int commit_contacts(sim_handle* H) {
         }
     bool grew = false;
     const size_t cC = std::max(Ct, 1), cS = std::max(NSt, 1), cCS = std::max(CSt, 1);
-    CK(H->dc.ensure(cC, grew)); CK(H->cc9.ensure(9 * cC, grew)); CK(H->cs0.ensure(cC, grew));
-    CK(H->cv0.ensure(cC, grew)); CK(H->cc1.ensure(cS, grew)); CK(H->slot_vtx.ensure(cS, grew));
-    CK(H->slot_inst.ensure(cS, grew)); CK(H->scp.ensure(cS + 1, grew)); CK(H->sci.ensure(4 * cC, grew));
-    CK(H->scw.ensure(4 * cC, grew)); CK(H->G.ensure(std::max<int64_t>(goff[NCL], 1), grew));
+    CK(H->G.ensure(std::max<int64_t>(goff[NCL], 1), grew));
     CK(H->GA.ensure(std::max<int64_t>(gaoff[S], 1), grew));
     CK(H->lam.ensure(3 * cC, grew)); CK(H->theta.ensure(3 * cC, grew)); CK(H->cdiag.ensure(3 * cC, grew));
     CK(H->hvec.ensure(3 * cC, grew)); CK(H->hl.ensure(3 * cC, grew)); CK(H->rho.ensure(3 * cC, grew));
     CK(H->phi_abs.ensure(cC, grew)); CK(H->dxt.ensure(3 * cS, grew)); CK(H->wz.ensure(3 * cS, grew));
     CK(H->act_idx.ensure(cS, grew)); CK(H->act_pos.ensure(cS, grew)); CK(H->act_con.ensure(cS, grew));
-    CK(H->cvtx.ensure(cCS, grew)); CK(H->ccls.ensure(cCS, grew));
     if (S > 1) CK(H->wzT.ensure((size_t)std::max(nsm, 1) * S, grew));
-    CK(H->chain_off.ensure(cCS + 1, grew)); CK(H->chain_rows.ensure(std::max<int64_t>(zoff[NCL], 1), grew));
+    CK(H->chain_rows.ensure(std::max<int64_t>(zoff[NCL], 1), grew));
     CK(H->Zc.ensure(std::max<int64_t>(zoff[NCL], 1), grew)); CK(H->ulist.ensure(std::max(uoff[NCL], 1), grew));
-    CK(H->it_cd.ensure(std::max<size_t>(it_cd.size(), 1), grew));
-    CK(H->it_sc.ensure(std::max<size_t>(it_sc.size(), 1), grew));
-    if (grew) H->contact_gen++;   // captured pointers changed
+    (void)cC; (void)cS; (void)cCS;
     // per-instance positions of the slot -> contact lists
     std::vector<int64_t> poff(S + 1, 0);
     for (int i = 0; i < S; ++i) poff[i + 1] = poff[i] + (int64_t)H->ic[i].sci.size();
@@ -764,6 +762,28 @@ static int commit_contacts(sim_handle* H) {
               g_zo = seg(8 * C1), g_cmo = seg(4 * C1), g_cm = seg(4 * (size_t)S), g_icd = seg(8 * it_cd.size()),
               g_isc = seg(8 * it_sc.size());
     const size_t need = cur + 256;
+    CK(H->arena.ensure(need, grew));
+    {   // captured pointers change when the arena moves or any segment offset moves
+        const std::vector<size_t> lay = {g_dc.at, g_c9.at, g_s0.at, g_v0.at, g_c1.at, g_sv.at, g_si.at, g_scp.at,
+                                         g_sci.at, g_scw.at, g_ch.at, g_cv.at, g_cc.at, g_co.at, g_so.at, g_ga.at,
+                                         g_cl.at, g_cso.at, g_go.at, g_uo.at, g_zo.at, g_cmo.at, g_cm.at, g_icd.at,
+                                         g_isc.at};
+        if (grew || lay != H->arena_layout) H->contact_gen++;
+        H->arena_layout = lay;
+    }
+    {
+        unsigned char* A = H->arena.p;
+        H->dc.p = (DContact*)(A + g_dc.at); H->cc9.p = (float*)(A + g_c9.at); H->cs0.p = (int32_t*)(A + g_s0.at);
+        H->cv0.p = (int32_t*)(A + g_v0.at); H->cc1.p = (int32_t*)(A + g_c1.at);
+        H->slot_vtx.p = (int32_t*)(A + g_sv.at); H->slot_inst.p = (int32_t*)(A + g_si.at);
+        H->scp.p = (int32_t*)(A + g_scp.at); H->sci.p = (int32_t*)(A + g_sci.at); H->scw.p = (float*)(A + g_scw.at);
+        H->chain_off.p = (int32_t*)(A + g_ch.at); H->cvtx.p = (int32_t*)(A + g_cv.at);
+        H->ccls.p = (int32_t*)(A + g_cc.at); H->coff.p = (int*)(A + g_co.at); H->soff.p = (int*)(A + g_so.at);
+        H->gaoff.p = (int64_t*)(A + g_ga.at); H->cls.p = (int*)(A + g_cl.at); H->csoff.p = (int*)(A + g_cso.at);
+        H->goff.p = (int64_t*)(A + g_go.at); H->uoff.p = (int*)(A + g_uo.at); H->zoff.p = (int64_t*)(A + g_zo.at);
+        H->cmoff.p = (int*)(A + g_cmo.at); H->cmem.p = (int*)(A + g_cm.at); H->it_cd.p = (int2*)(A + g_icd.at);
+        H->it_sc.p = (int2*)(A + g_isc.at);
+    }
     if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
     CK(cudaEventSynchronize(H->stage_free));   // the previous commit's copies are done
     if (need > H->stage_cap) {
@@ -835,19 +855,8 @@ static int commit_contacts(sim_handle* H) {
     memcpy(B + g_cm.at, cmem.data(), 4 * (size_t)S);
     if (!it_cd.empty()) memcpy(B + g_icd.at, it_cd.data(), 8 * it_cd.size());
     if (!it_sc.empty()) memcpy(B + g_isc.at, it_sc.data(), 8 * it_sc.size());
-    H->h2d_contact_bytes = 0;
-    auto up = [&](void* dst, const Seg& g) -> cudaError_t {
-        if (g.bytes == 0) return cudaSuccess;
-        H->h2d_contact_bytes += (int64_t)g.bytes;
-        return cudaMemcpyAsync(dst, B + g.at, g.bytes, cudaMemcpyHostToDevice, st);
-    };
-    CK(up(H->dc.p, g_dc)); CK(up(H->cc9.p, g_c9)); CK(up(H->cs0.p, g_s0)); CK(up(H->cv0.p, g_v0));
-    CK(up(H->cc1.p, g_c1)); CK(up(H->slot_vtx.p, g_sv)); CK(up(H->slot_inst.p, g_si)); CK(up(H->scp.p, g_scp));
-    CK(up(H->sci.p, g_sci)); CK(up(H->scw.p, g_scw)); CK(up(H->chain_off.p, g_ch)); CK(up(H->cvtx.p, g_cv));
-    CK(up(H->ccls.p, g_cc)); CK(up(H->coff.p, g_co)); CK(up(H->soff.p, g_so)); CK(up(H->gaoff.p, g_ga));
-    CK(up(H->cls.p, g_cl)); CK(up(H->csoff.p, g_cso)); CK(up(H->goff.p, g_go)); CK(up(H->uoff.p, g_uo));
-    CK(up(H->zoff.p, g_zo)); CK(up(H->cmoff.p, g_cmo)); CK(up(H->cmem.p, g_cm)); CK(up(H->it_cd.p, g_icd));
-    CK(up(H->it_sc.p, g_isc));
+    H->h2d_contact_bytes = (int64_t)cur;
+    CK(cudaMemcpyAsync(H->arena.p, B, cur, cudaMemcpyHostToDevice, st));   // the whole layout at once
     CK(cudaEventRecord(H->stage_free, st));
     H->NCL = NCL;
     H->CS = CSt;
