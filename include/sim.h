@@ -138,10 +138,14 @@ int sim_build_sparse_inverse(sim_handle *h, double drop_tolerance);
  * the rows on the host; the next sim_step (or debug accessor) uploads the
  * contact sets of all instances in one batch and computes on the device
  * G = K[:,Vc]^T K[:,Vc] per instance, the Delassus diagonal and the
- * preconditioner r_n = h^2 D_jj, r_f = h D_jj.  Limits per instance: n <= 1024
- * contacts on <= 1024 distinct vertices, and the CR's fp64 working set
- * 184 n + 72 n_vertices bytes must fit 227 KB (about 900 single-vertex
- * contacts); SIM_E_LIMIT otherwise. */
+ * preconditioner r_n = h^2 D_jj, r_f = h D_jj (eq. schur-complement P:L858,
+ * eq. complementarity preconditioner P:L919-925).  The constraint solve (CR,
+ * P:L1047-1049) runs in one thread-block cluster per instance when the set
+ * has n <= 1024 contacts on <= 1024 distinct vertices and its fp64 working set
+ * 184 n + 72 n_vertices bytes fits 227 KB (about 900 single-vertex contacts).
+ * Larger sets (any size, e.g. a multi-object pile with soft-soft contact rows)
+ * use the grid CR, which needs n_instances == 1 (SIM_E_LIMIT otherwise); its
+ * Gram G is stored per etree component (G is zero across components). */
 int sim_set_contacts(sim_handle *h, int32_t instance, const sim_contact *contacts, int32_t n);
 /* The same for instances first .. first+count-1 at once: counts[count],
  * contacts concatenated in instance order.  All-or-nothing on error. */
@@ -186,6 +190,12 @@ int sim_set_stream(sim_handle *h, void *cuda_stream);
  * 7 scatter, 8 kpass2, 9 active-set + G_A gather), the summed device ms of
  * the most recent frame.  out must hold >= 10 doubles. */
 int sim_set_profiling(sim_handle *h, int on);
+
+/* Constraint-solver selection (same CR algorithm and result up to rounding
+ * order): 0 = automatic (cluster CR when the set fits, grid CR otherwise),
+ * 1 = cluster CR only (SIM_E_LIMIT if the current set does not fit),
+ * 2 = grid CR always (n_instances == 1 only).  Takes effect at the next step. */
+int sim_set_cr_mode(sim_handle *h, int32_t mode);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 
 void sim_destroy(sim_handle *h);         /* NULL-safe */

@@ -86,6 +86,7 @@ struct InstContacts {
     std::vector<float> c9;
     std::vector<int32_t> s0, v0, c1; // local slot / vertex / local contact
     int64_t chain_total = 0;         // sum over slots of (depth + 1)
+    bool large = false;              // beyond the cluster CR's limits: needs the grid CR (one scene)
 };
 
 struct sim_handle {
@@ -179,6 +180,14 @@ struct sim_handle {
     size_t stage_cap = 0;
     cudaEvent_t stage_free = nullptr;
     double set_contacts_host_us = 0;
+    // grid CR (large contact sets of one scene): Delassus groups = etree components
+    int cr_mode = 0;                 // 0 auto, 1 cluster CR only, 2 grid CR always
+    bool grid = false;               // the committed contact set uses the grid CR
+    int NG = 0, ng_max = 0;
+    std::vector<int32_t> comp_root;  // [n_f] root of each free vertex's etree component
+    DPtr<int> gcsoff, gs0, gn;       // group slot offsets [NG+1]; per slot: group start, size
+    DPtr<int64_t> ggoff, growoff;    // group G offsets [NG+1]; per slot: its G row
+    DBuf<double> g_r, g_p, g_Ap, g_z, g_Ar, g_W, g_q, g_part, g_sc;
 };
 
 // ---------------------------------------------------------------------------
@@ -452,6 +461,9 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     for (int i = 0; i < nv; ++i)
         if (H->fixed[i]) H->int2orig[q++] = i;
     for (int k = 0; k < nv; ++k) H->orig2int[H->int2orig[k]] = k;
+    // etree components (trees of the forest: one per connected object); parent[i] > i in postorder
+    H->comp_root.assign(nf, -1);
+    for (int i = nf - 1; i >= 0; --i) H->comp_root[i] = H->K.parent[i] < 0 ? i : H->comp_root[H->K.parent[i]];
     H->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (!H->host_only) {
         int rc = upload_all(H);
@@ -490,7 +502,6 @@ static int build_inst(const sim_handle* H, const sim_contact* cs, int n, InstCon
         return code;
     };
     if (n < 0 || (n > 0 && !cs)) { err = "bad contact array"; return SIM_E_INVALID; }
-    if (n > kMaxContacts) return bad(SIM_E_LIMIT, "at most %d contacts per instance", kMaxContacts);
     I = InstContacts();
     I.hc.resize(n);
     std::vector<int32_t> verts;
@@ -537,13 +548,16 @@ static int build_inst(const sim_handle* H, const sim_contact* cs, int n, InstCon
     std::sort(verts.begin(), verts.end());
     verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
     const int ns = (int)verts.size();
-    if (ns > kMaxSlots) return bad(SIM_E_LIMIT, "at most %d contact vertices per instance", kMaxSlots);
-    if (cr_smem_bytes(n, ns) > kCrMaxSmem) {
-        snprintf(buf, sizeof buf, "%d contacts on %d vertices exceed the CR's shared memory (%zu > %zu B)", n, ns,
-                 cr_smem_bytes(n, ns), kCrMaxSmem);
+    I.large = n > kMaxContacts || ns > kMaxSlots || cr_smem_bytes(n, ns) > kCrMaxSmem;
+    if (I.large && (H->S > 1 || H->cr_mode == 1)) {
+        snprintf(buf, sizeof buf,
+                 "%d contacts on %d vertices exceed the cluster CR (<= %d contacts, <= %d vertices, %zu B shared "
+                 "memory); larger sets need n_instances == 1 and the grid CR", n, ns, kMaxContacts, kMaxSlots,
+                 kCrMaxSmem);
         err = buf;
         return SIM_E_LIMIT;
     }
+    if ((int64_t)n * 3 >= (int64_t)INT32_MAX / 4) return bad(SIM_E_LIMIT, "too many contacts (%d)", n);
     // slot -> (contact, weight) lists in contact order
     std::vector<int> cnt(ns + 1, 0);
     auto slot_of = [&](int v) { return (int)(std::lower_bound(verts.begin(), verts.end(), v) - verts.begin()); };
@@ -638,6 +652,19 @@ static ClassSlots class_slots(sim_handle* H) { return ClassSlots{H->cvtx.p, H->c
 static Slots slots(sim_handle* H) { return Slots{H->slot_vtx.p, H->slot_inst.p, H->scp.p, H->sci.p, H->scw.p}; }
 static CrContacts cr_contacts(sim_handle* H) { return CrContacts{H->cc9.p, H->cs0.p, H->cv0.p, H->cc1.p}; }
 
+static GcrData gcr_data(sim_handle* H) {
+    GcrData g;
+    g.c9 = H->cc9.p;
+    g.G = H->G.p;
+    g.rowoff = H->growoff.p;
+    g.gs0 = H->gs0.p;
+    g.gn = H->gn.p;
+    g.r = H->g_r.p; g.p = H->g_p.p; g.Ap = H->g_Ap.p; g.z = H->g_z.p; g.Ar = H->g_Ar.p;
+    g.W = H->g_W.p; g.q = H->g_q.p; g.part = H->g_part.p; g.sc = H->g_sc.p;
+    g.nblk = 0;
+    return g;
+}
+
 static Params make_params(const sim_handle* H) {
     Params P;
     P.n_v = H->n_v;
@@ -688,6 +715,24 @@ static int commit_contacts(sim_handle* H) {
         }
     }
     const int NCL = (int)rep.size();
+    // grid CR: one scene whose contact set exceeds the cluster CR (or forced); the Delassus Gram
+    // is stored per etree component holding contact slots (zero across components, Theorem 1)
+    const bool grid = S == 1 && !H->ic[0].hc.empty() && (H->cr_mode == 2 || H->ic[0].large);
+    std::vector<int> gcs(1, 0);
+    std::vector<int64_t> ggo(1, 0);
+    int ngmax = 0;
+    if (grid) {
+        const std::vector<int32_t>& v = H->ic[0].verts;
+        for (size_t q = 1; q < v.size(); ++q)
+            if (H->comp_root[v[q]] != H->comp_root[v[q - 1]]) gcs.push_back((int)q);
+        gcs.push_back((int)v.size());
+        for (size_t g = 0; g + 1 < gcs.size(); ++g) {
+            const int n = gcs[g + 1] - gcs[g];
+            ggo.push_back(ggo.back() + (int64_t)n * n);
+            ngmax = std::max(ngmax, n);
+        }
+    }
+    const int NG = (int)gcs.size() - 1;
     std::vector<int> cmoff(NCL + 1, 0), cmem(S);
     for (int i = 0; i < S; ++i) cmoff[cls[i] + 1]++;
     for (int k = 0; k < NCL; ++k) cmoff[k + 1] += cmoff[k];
@@ -703,7 +748,7 @@ static int commit_contacts(sim_handle* H) {
         const int n = (int)I.hc.size(), ns = (int)I.verts.size();
         coff[i + 1] = coff[i] + n;
         soff[i + 1] = soff[i] + ns;
-        gaoff[i + 1] = gaoff[i] + (int64_t)ns * ns;
+        gaoff[i + 1] = gaoff[i] + (grid ? 0 : (int64_t)ns * ns);
         ncm = std::max(ncm, n);
         nsm = std::max(nsm, ns);
     }
@@ -711,7 +756,7 @@ static int commit_contacts(sim_handle* H) {
         const InstContacts& I = H->ic[rep[k]];
         const int ns = (int)I.verts.size();
         csoff[k + 1] = csoff[k] + ns;
-        goff[k + 1] = goff[k] + (int64_t)ns * ns;
+        goff[k + 1] = goff[k] + (grid ? ggo.back() : (int64_t)ns * ns);
         zoff[k + 1] = zoff[k] + I.chain_total;
         const int urows = (int)std::min<int64_t>(nf, I.chain_total);
         uoff[k + 1] = uoff[k] + urows;
@@ -741,6 +786,12 @@ static int commit_contacts(sim_handle* H) {
     CK(H->phi_abs.ensure(cC, grew)); CK(H->dxt.ensure(3 * cS, grew)); CK(H->wz.ensure(3 * cS, grew));
     CK(H->act_idx.ensure(cS, grew)); CK(H->act_pos.ensure(cS, grew)); CK(H->act_con.ensure(cS, grew));
     if (S > 1) CK(H->wzT.ensure((size_t)std::max(nsm, 1) * S, grew));
+    if (grid) {
+        const size_t nb = (size_t)gcr_row_blocks(Ct);
+        CK(H->g_r.ensure(3 * cC, grew)); CK(H->g_p.ensure(3 * cC, grew)); CK(H->g_Ap.ensure(3 * cC, grew));
+        CK(H->g_z.ensure(3 * cC, grew)); CK(H->g_Ar.ensure(3 * cC, grew)); CK(H->g_W.ensure(3 * cS, grew));
+        CK(H->g_q.ensure(3 * cS, grew)); CK(H->g_part.ensure(3 * nb, grew)); CK(H->g_sc.ensure(8, grew));
+    }
     CK(H->chain_rows.ensure(std::max<int64_t>(zoff[NCL], 1), grew));
     CK(H->Zc.ensure(std::max<int64_t>(zoff[NCL], 1), grew)); CK(H->ulist.ensure(std::max(uoff[NCL], 1), grew));
     (void)cC; (void)cS; (void)cCS;
@@ -761,13 +812,16 @@ static int commit_contacts(sim_handle* H) {
               g_cl = seg(4 * (size_t)S), g_cso = seg(4 * C1), g_go = seg(8 * C1), g_uo = seg(4 * C1),
               g_zo = seg(8 * C1), g_cmo = seg(4 * C1), g_cm = seg(4 * (size_t)S), g_icd = seg(8 * it_cd.size()),
               g_isc = seg(8 * it_sc.size());
+    const size_t NSg = grid ? (size_t)NSt : 0;
+    const Seg g_gcs = seg(4 * gcs.size()), g_ggo = seg(8 * ggo.size()), g_grw = seg(8 * NSg), g_gs0 = seg(4 * NSg),
+              g_gn = seg(4 * NSg);
     const size_t need = cur + 256;
     CK(H->arena.ensure(need, grew));
     {   // captured pointers change when the arena moves or any segment offset moves
         const std::vector<size_t> lay = {g_dc.at, g_c9.at, g_s0.at, g_v0.at, g_c1.at, g_sv.at, g_si.at, g_scp.at,
                                          g_sci.at, g_scw.at, g_ch.at, g_cv.at, g_cc.at, g_co.at, g_so.at, g_ga.at,
                                          g_cl.at, g_cso.at, g_go.at, g_uo.at, g_zo.at, g_cmo.at, g_cm.at, g_icd.at,
-                                         g_isc.at};
+                                         g_isc.at, g_gcs.at, g_ggo.at, g_grw.at, g_gs0.at, g_gn.at};
         if (grew || lay != H->arena_layout) H->contact_gen++;
         H->arena_layout = lay;
     }
@@ -783,6 +837,8 @@ static int commit_contacts(sim_handle* H) {
         H->goff.p = (int64_t*)(A + g_go.at); H->uoff.p = (int*)(A + g_uo.at); H->zoff.p = (int64_t*)(A + g_zo.at);
         H->cmoff.p = (int*)(A + g_cmo.at); H->cmem.p = (int*)(A + g_cm.at); H->it_cd.p = (int2*)(A + g_icd.at);
         H->it_sc.p = (int2*)(A + g_isc.at);
+        H->gcsoff.p = (int*)(A + g_gcs.at); H->ggoff.p = (int64_t*)(A + g_ggo.at);
+        H->growoff.p = (int64_t*)(A + g_grw.at); H->gs0.p = (int*)(A + g_gs0.at); H->gn.p = (int*)(A + g_gn.at);
     }
     if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
     CK(cudaEventSynchronize(H->stage_free));   // the previous commit's copies are done
@@ -855,6 +911,19 @@ static int commit_contacts(sim_handle* H) {
     memcpy(B + g_cm.at, cmem.data(), 4 * (size_t)S);
     if (!it_cd.empty()) memcpy(B + g_icd.at, it_cd.data(), 8 * it_cd.size());
     if (!it_sc.empty()) memcpy(B + g_isc.at, it_sc.data(), 8 * it_sc.size());
+    memcpy(B + g_gcs.at, gcs.data(), 4 * gcs.size());
+    memcpy(B + g_ggo.at, ggo.data(), 8 * ggo.size());
+    if (grid) {
+        int64_t* rw = (int64_t*)(B + g_grw.at);
+        int *s0g = (int*)(B + g_gs0.at), *sng = (int*)(B + g_gn.at);
+        for (int g = 0; g < NG; ++g)
+            for (int q = gcs[g]; q < gcs[g + 1]; ++q) {
+                const int n = gcs[g + 1] - gcs[g];
+                rw[q] = ggo[g] + (int64_t)(q - gcs[g]) * n;
+                s0g[q] = gcs[g];
+                sng[q] = n;
+            }
+    }
     H->h2d_contact_bytes = (int64_t)cur;
     CK(cudaMemcpyAsync(H->arena.p, B, cur, cudaMemcpyHostToDevice, st));   // the whole layout at once
     CK(cudaEventRecord(H->stage_free, st));
@@ -871,6 +940,9 @@ static int commit_contacts(sim_handle* H) {
     H->urows_max = um;
     H->coff_h = coff;
     H->soff_h = soff;
+    H->grid = grid;
+    H->NG = NG;
+    H->ng_max = ngmax;
     CK(cudaMemsetAsync(H->flag.p, 0, (size_t)NCL * nf, st));
     CK(cudaMemsetAsync(H->slotmap.p, 0xff, (size_t)nf * S * sizeof(int32_t), st));
     CK(cudaMemsetAsync(H->ucount.p, 0, 2 * (size_t)NCL * sizeof(int), st));
@@ -882,8 +954,19 @@ static int commit_contacts(sim_handle* H) {
     launch_chain_rows(st, P, csl, sl, H->chain_off.p, H->parent.p, H->ptop.p, H->chain_rows.p, H->flag.p,
                       H->slotmap.p);
     launch_ulist(st, P, off, H->flag.p, csl, H->meta.p, H->ucount.p, H->ulist.p, H->Krow.p, H->Zc.p);
-    launch_delassus(st, P, off, csl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
-    launch_djj(st, P, off, H->dc.p, H->G.p);
+    if (grid) {   // per-component Gram blocks: the class-slot kernel run over the groups
+        Params Pg = P;
+        Pg.NCL = NG;
+        Pg.ns_max = ngmax;
+        InstOff og = off;
+        og.csoff = H->gcsoff.p;
+        og.goff = H->ggoff.p;
+        launch_delassus(st, Pg, og, csl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
+        launch_djj_grid(st, P, H->dc.p, gcr_data(H));
+    } else {
+        launch_delassus(st, P, off, csl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
+        launch_djj(st, P, off, H->dc.p, H->G.p);
+    }
     CK(cudaGetLastError());
     H->dirty = false;
     return SIM_OK;   // asynchronous: the copies and kernels are ordered on the handle's stream
@@ -952,11 +1035,11 @@ static int enqueue_frame(sim_handle* H, int iters) {
             CKR(cudaEventRecord(H->fork_ev, st));
             CKR(cudaStreamWaitEvent(H->aux, H->fork_ev, 0));
             launch_contact_eval(H->aux, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
-            launch_active(H->aux, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += 2;
+            if (!H->grid) { launch_active(H->aux, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += 2; }
             CKR(cudaEventRecord(H->join_ev, H->aux));
         } else if (con) {
             MARK(KK_CONTACT); launch_contact_eval(st, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
-            MARK(KK_ACTIVE); launch_active(st, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += 2;
+            if (!H->grid) { MARK(KK_ACTIVE); launch_active(st, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += 2; }
         }
         MARK(KK_LOCAL);
         launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, H->x.p, H->fc.p, nullptr); nk++;
@@ -971,8 +1054,14 @@ static int enqueue_frame(sim_handle* H, int iters) {
             launch_chain_dot(st, P, off, class_slots(H), H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
                              H->y.p, sl, ccr, H->x.p, cs, H->n_it_cd, H->it_cd.p); nk++;
             MARK(KK_CR);
-            int e = launch_cr(st, P, off, H->dc.p, ccr, sl, H->GA.p, H->x.p, cs, act); nk++;
-            if (e) return -e;
+            if (H->grid) {
+                int e = launch_gcr(st, P, gcr_data(H), H->dc.p, ccr, sl, H->x.p, cs);
+                if (e) return -e;
+                nk += gcr_kernels_per_iteration(P.cr_iters);
+            } else {
+                int e = launch_cr(st, P, off, H->dc.p, ccr, sl, H->GA.p, H->x.p, cs, act); nk++;
+                if (e) return -e;
+            }
             MARK(KK_SCATTER);
             launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->wzT.p, H->y.p,
                            H->n_it_sc, H->it_sc.p); nk++;
@@ -984,6 +1073,18 @@ static int enqueue_frame(sim_handle* H, int iters) {
 #undef MARK
 #undef CKR
     return nk;
+}
+
+extern "C" int sim_set_cr_mode(sim_handle* H, int32_t mode) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (mode < 0 || mode > 2) return fail(SIM_E_INVALID, "CR mode must be 0 (auto), 1 (cluster) or 2 (grid)");
+    if (mode == 1)
+        for (const InstContacts& I : H->ic)
+            if (I.large) return fail(SIM_E_LIMIT, "the current contact set needs the grid CR");
+    if (mode == 2 && H->S > 1) return fail(SIM_E_LIMIT, "the grid CR needs n_instances == 1");
+    H->cr_mode = mode;
+    H->dirty = true;   // recommit (and recapture) with the new solver
+    return SIM_OK;
 }
 
 extern "C" int sim_set_profiling(sim_handle* H, int on) {
@@ -1016,7 +1117,7 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     int rc = commit_contacts(H);
     if (rc) return rc;
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
-                                      H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc};
+                                      H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG};
     if (!H->gexec || key != H->gkey) {
         if (H->gexec) {
             cudaGraphExecDestroy(H->gexec);
@@ -1317,7 +1418,20 @@ extern "C" int sim_debug_get_delassus(sim_handle* H, int32_t inst, int32_t* cv, 
     if (cap < ns) return fail(SIM_E_INVALID, "capacity %d < %d contact vertices", cap, ns);
     CK(cudaStreamSynchronize(H->stream));
     if (cv) for (int s = 0; s < ns; ++s) cv[s] = H->int2orig[I.verts[s]];
-    if (G && ns) {
+    if (G && ns && H->grid) {
+        std::vector<int> gcs(H->NG + 1);
+        std::vector<int64_t> ggo(H->NG + 1);
+        CK(cudaMemcpy(gcs.data(), H->gcsoff.p, gcs.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ggo.data(), H->ggoff.p, ggo.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        std::fill(G, G + (size_t)ns * ns, 0.f);
+        for (int g = 0; g < H->NG; ++g) {
+            const int n = gcs[g + 1] - gcs[g];
+            std::vector<float> blk((size_t)n * n);
+            CK(cudaMemcpy(blk.data(), H->G.p + ggo[g], blk.size() * sizeof(float), cudaMemcpyDeviceToHost));
+            for (int a = 0; a < n; ++a)
+                for (int b = 0; b < n; ++b) G[(size_t)(gcs[g] + a) * ns + gcs[g] + b] = blk[(size_t)a * n + b];
+        }
+    } else if (G && ns) {
         int cl = 0;
         int64_t go = 0;
         CK(cudaMemcpy(&cl, H->cls.p + inst, sizeof(int), cudaMemcpyDeviceToHost));

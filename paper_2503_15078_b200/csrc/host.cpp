@@ -117,6 +117,28 @@ struct ND {
             order.insert(order.end(), v.begin(), v.end());
             return;
         }
+        // disconnected pieces (separate objects, or parts a cut isolated) need no separator:
+        // dissect each on its own, so every object gets its own etree
+        {
+            for (int32_t i : v) side[i] = 4;
+            std::vector<std::vector<int32_t>> comps;
+            for (int32_t s0 : v) {
+                if (side[s0] != 4) continue;
+                std::vector<int32_t> cmp{s0};
+                side[s0] = 5;
+                for (size_t q = 0; q < cmp.size(); ++q) {
+                    const int32_t i = cmp[q];
+                    for (int64_t p = A.ptr[i]; p < A.ptr[i + 1]; ++p)
+                        if (side[A.col[p]] == 4) { side[A.col[p]] = 5; cmp.push_back(A.col[p]); }
+                }
+                comps.push_back(std::move(cmp));
+            }
+            for (int32_t i : v) side[i] = 0;
+            if (comps.size() > 1) {
+                for (auto& cmp : comps) run(std::move(cmp));
+                return;
+            }
+        }
         double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
         for (int32_t i : v)
             for (int d = 0; d < 3; ++d) {

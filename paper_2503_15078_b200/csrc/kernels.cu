@@ -1953,6 +1953,263 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     // no trailing cluster barrier: after its last exchange wait no CTA touches a peer's shared memory
 }
 
+// ----------------------------------------------------------------------------
+// Grid CR: the constraint solve for contact sets too large for one cluster's shared memory
+// (one scene, any number of contacts, e.g. a multi-object pile).  Same algorithm as k_cr
+// (Saad's CR from z = 0, exactly N_CR matvecs, stop only on breakdown; reading A19), with
+// the vectors in global memory and one kernel per phase:
+//   gcr_slot   W_b = sum_{(c, w) on slot b} w sum_k theta_ck v_ck c_ck       (J^T Theta v)
+//   gcr_gram   q_a = sum_b G[a][b] W_b over a's Delassus group                (A^-1 on V_c)
+//   gcr_row    (S v)_j = theta_j c_j . sum_q w_q q_{slot q} + C_j v_j, partial dots
+//   gcr_update every CTA reduces the partials in a fixed order, then the CR vector updates
+// The Delassus Gram is stored per group = etree component (a tree of the forest): K is
+// block-diagonal over the components, so G[a][b] = 0 across them (Theorem 1).
+// ----------------------------------------------------------------------------
+constexpr int kGcrThreads = 256;
+
+__device__ __forceinline__ void block_sum3_gcr(double& a, double& b, double& c, double* red) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    a = warp_sum(a); b = warp_sum(b); c = warp_sum(c);
+    if (lane == 0) { red[w] = a; red[nw + w] = b; red[2 * nw + w] = c; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0, s1 = 0, s2 = 0;
+        for (int q = 0; q < nw; ++q) { s0 += red[q]; s1 += red[nw + q]; s2 += red[2 * nw + q]; }
+        red[3 * nw] = s0; red[3 * nw + 1] = s1; red[3 * nw + 2] = s2;
+    }
+    __syncthreads();
+    a = red[3 * nw]; b = red[3 * nw + 1]; c = red[3 * nw + 2];
+}
+
+// r = rho (rho of multi-vertex contacts here; single-vertex ones come from the chain dot), z = 0
+__global__ void k_gcr_init(Params P, GcrData g, const DContact* __restrict__ C, CrContacts cc,
+                           const double4* __restrict__ x, ContactState cs) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= P.C) return;
+    const int v0 = cc.v0[c];
+    const bool viaSlot = v0 >= 0 && cc.c1[cc.s0[c]] == c;
+    double xs0 = 0.0, xs1 = 0.0, xs2 = 0.0;
+    const DContact& ct = C[c];
+    if (!viaSlot)
+        for (int q = 0; q < ct.nv; ++q) {
+            const double4 xa = x[(size_t)ct.vtx[q] * P.S + ct.inst];
+            const int s = ct.slot[q];
+            xs0 += ct.w[q] * (xa.x + cs.dxt[3 * s]);
+            xs1 += ct.w[q] * (xa.y + cs.dxt[3 * s + 1]);
+            xs2 += ct.w[q] * (xa.z + cs.dxt[3 * s + 2]);
+        }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int j = 3 * c + k;
+        const double rho = viaSlot ? cs.rho[j]
+                                   : cs.hvec[j] - cs.theta[j] * (ct.c[k][0] * xs0 + ct.c[k][1] * xs1 + ct.c[k][2] * xs2);
+        cs.rho[j] = rho;
+        g.r[j] = rho;
+        g.z[j] = 0.0;
+    }
+}
+
+// W_b = sum over the contacts on slot b of w * sum_k theta_k v_k c_k  (fixed contact order)
+__global__ void k_gcr_slot(int NS, Slots sl, CrContacts cc, const double* __restrict__ theta,
+                           const double* __restrict__ v, double* __restrict__ W) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= NS) return;
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+    for (int p = sl.scp[b]; p < sl.scp[b + 1]; ++p) {
+        const int c = sl.sci[p];
+        const double wt = (double)sl.scw[p];
+        const float* c9 = cc.c9 + 9 * (size_t)c;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double tv = wt * theta[3 * c + k] * v[3 * c + k];
+            w0 = fma(tv, (double)c9[3 * k], w0);
+            w1 = fma(tv, (double)c9[3 * k + 1], w1);
+            w2 = fma(tv, (double)c9[3 * k + 2], w2);
+        }
+    }
+    W[3 * b] = w0;
+    W[3 * b + 1] = w1;
+    W[3 * b + 2] = w2;
+}
+
+// q_a = sum_{b in group(a)} G[a][b] W_b: one warp per slot row (coalesced G row)
+__global__ void __launch_bounds__(256) k_gcr_gram(int NS, GcrData g) {
+    const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (a >= NS) return;
+    const float* row = g.G + g.rowoff[a];
+    const int b0 = g.gs0[a], n = g.gn[a];
+    const double* W = g.W + 3 * (size_t)b0;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+    for (int b = lane; b < n; b += 32) {
+        const double gv = (double)__ldg(&row[b]);
+        d0 = fma(gv, W[3 * b], d0);
+        d1 = fma(gv, W[3 * b + 1], d1);
+        d2 = fma(gv, W[3 * b + 2], d2);
+    }
+    d0 = warp_sum(d0);
+    d1 = warp_sum(d1);
+    d2 = warp_sum(d2);
+    if (lane == 0) {
+        g.q[3 * (size_t)a] = d0;
+        g.q[3 * (size_t)a + 1] = d1;
+        g.q[3 * (size_t)a + 2] = d2;
+    }
+}
+
+// Ar_j = theta_j c_j . sum_q w_q q_{slot q} + C_j r_j; per-CTA partials of r.Ar, Ar.Ar, Ar.Ap
+__global__ void __launch_bounds__(kGcrThreads) k_gcr_row(Params P, GcrData g, const DContact* __restrict__ C,
+                                                       ContactState cs, int first) {
+    __shared__ double red[3 * (kGcrThreads / 32) + 3];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (c < P.C) {
+        const DContact& ct = C[c];
+        double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+        for (int p = 0; p < ct.nv; ++p) {
+            const int s = ct.slot[p];
+            q0 += ct.w[p] * g.q[3 * s];
+            q1 += ct.w[p] * g.q[3 * s + 1];
+            q2 += ct.w[p] * g.q[3 * s + 2];
+        }
+        const float* c9 = g.c9 + 9 * (size_t)c;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int j = 3 * c + k;
+            const double th = cs.theta[j];
+            const double acc = th != 0.0 ? (double)c9[3 * k] * q0 + (double)c9[3 * k + 1] * q1 +
+                                               (double)c9[3 * k + 2] * q2
+                                         : 0.0;
+            const double rj = g.r[j];
+            const double ar = th * acc + cs.cdiag[j] * rj;
+            g.Ar[j] = ar;
+            s1 = fma(rj, ar, s1);
+            s2 = fma(ar, ar, s2);
+            if (!first) s3 = fma(ar, g.Ap[j], s3);
+        }
+    }
+    block_sum3_gcr(s1, s2, s3, red);
+    if (threadIdx.x == 0) {
+        g.part[3 * blockIdx.x] = s1;
+        g.part[3 * blockIdx.x + 1] = s2;
+        g.part[3 * blockIdx.x + 2] = s3;
+    }
+}
+
+// CR scalars from the partials (same fixed order in every CTA) and the vector updates of
+// iteration `it`: [beta, p, Ap (it > 0)], breakdown test, alpha, z += alpha p, r -= alpha Ap.
+// Scalars ping-pong between sc[.. + (it & 1)] (read) and sc[.. + ((it + 1) & 1)] (written by CTA 0).
+__global__ void __launch_bounds__(kGcrThreads) k_gcr_update(GcrData g, int m, int it) {
+    __shared__ double sh[4];
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int b = lane; b < g.nblk; b += 32) {
+            s1 += g.part[3 * b];
+            s2 += g.part[3 * b + 1];
+            s3 += g.part[3 * b + 2];
+        }
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        s3 = warp_sum(s3);
+        if (lane == 0) {
+            const int rp = it & 1, wp = rp ^ 1;
+            double rAr, ApAp, beta = 0.0;
+            double stop = it == 0 ? 0.0 : g.sc[4 + rp];
+            if (it == 0) {
+                rAr = s1;
+                ApAp = s2;
+            } else {
+                const double rAr0 = g.sc[rp], ApAp0 = g.sc[2 + rp];
+                beta = stop != 0.0 ? 0.0 : s1 / rAr0;
+                rAr = s1;
+                ApAp = s2 + 2.0 * beta * s3 + beta * beta * ApAp0;
+            }
+            if (stop == 0.0 && (ApAp <= 1e-300 || fabs(rAr) <= 1e-300)) stop = 1.0;
+            sh[0] = beta;
+            sh[1] = stop != 0.0 ? 0.0 : rAr / ApAp;
+            sh[2] = stop;
+            if (blockIdx.x == 0) {
+                g.sc[wp] = rAr;
+                g.sc[2 + wp] = ApAp;
+                g.sc[4 + wp] = stop;
+            }
+        }
+    }
+    __syncthreads();
+    const double beta = sh[0], alpha = sh[1];
+    if (sh[2] != 0.0) return;   // broken down (now or earlier): keep the iterate
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+        double p, Ap;
+        if (it == 0) {
+            p = g.r[j];
+            Ap = g.Ar[j];
+        } else {
+            p = g.r[j] + beta * g.p[j];
+            Ap = g.Ar[j] + beta * g.Ap[j];
+        }
+        g.p[j] = p;
+        g.Ap[j] = Ap;
+        g.z[j] += alpha * p;
+        g.r[j] -= alpha * Ap;
+    }
+}
+
+// lambda += z / h^2 (reading A11), |r| -> cr_res
+__global__ void __launch_bounds__(1024) k_gcr_final(GcrData g, int m, double h, double* lam, double* cr_res) {
+    __shared__ double red[3 * 32 + 3];
+    double rr = 0.0, d1 = 0.0, d2 = 0.0;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+        lam[j] += g.z[j] / (h * h);
+        rr = fma(g.r[j], g.r[j], rr);
+    }
+    block_sum3_gcr(rr, d1, d2, red);
+    if (threadIdx.x == 0) cr_res[0] = sqrt(rr);
+}
+
+// D_jj = sum_{p,q} w_p w_q G[slot p][slot q] over pairs in the same Delassus group (reading A18)
+__global__ void k_djj_grid(int C, DContact* Cs, GcrData g) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    DContact& ct = Cs[c];
+    double d = 0.0;
+    for (int p = 0; p < ct.nv; ++p)
+        for (int q = 0; q < ct.nv; ++q) {
+            const int sp = ct.slot[p], sq = ct.slot[q];
+            if (g.gs0[sp] != g.gs0[sq]) continue;
+            d += ct.w[p] * ct.w[q] * (double)g.G[g.rowoff[sp] + (sq - g.gs0[sq])];
+        }
+    ct.Djj = d;
+}
+
+void launch_djj_grid(cudaStream_t st, const Params& P, DContact* c, GcrData g) {
+    if (P.C == 0) return;
+    k_djj_grid<<<(P.C + 127) / 128, 128, 0, st>>>(P.C, c, g);
+}
+
+int gcr_row_blocks(int C) { return (C + kGcrThreads - 1) / kGcrThreads; }
+
+int launch_gcr(cudaStream_t st, const Params& P, GcrData g, const DContact* c, CrContacts cc, Slots sl,
+               const double4* x, ContactState cs) {
+    if (P.C == 0) return 0;
+    const int m = 3 * P.C, NS = P.NS;
+    const int nb = gcr_row_blocks(P.C);
+    const int ub = std::min(148, (m + kGcrThreads - 1) / kGcrThreads);
+    g.nblk = nb;
+    k_gcr_init<<<nb, kGcrThreads, 0, st>>>(P, g, c, cc, x, cs);
+    for (int it = 0; it < P.cr_iters; ++it) {
+        k_gcr_slot<<<(NS + 255) / 256, 256, 0, st>>>(NS, sl, cc, cs.theta, g.r, g.W);
+        k_gcr_gram<<<(NS + 7) / 8, 256, 0, st>>>(NS, g);
+        k_gcr_row<<<nb, kGcrThreads, 0, st>>>(P, g, c, cs, it == 0);
+        k_gcr_update<<<ub, kGcrThreads, 0, st>>>(g, m, it);
+    }
+    k_gcr_final<<<1, 1024, 0, st>>>(g, m, P.h, cs.lam, cs.cr_res);
+    k_gcr_slot<<<(NS + 255) / 256, 256, 0, st>>>(NS, sl, cc, cs.theta, g.z, cs.wz);
+    return (int)cudaGetLastError();
+}
+
+int gcr_kernels_per_iteration(int cr_iters) { return 3 + 4 * cr_iters; }
+
 int read_cr_clock(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, g_cr_clock, sizeof(unsigned long long) * 32);
 }

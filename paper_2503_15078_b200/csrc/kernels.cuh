@@ -161,6 +161,27 @@ void launch_chain_rows(cudaStream_t st, const Params& P, ClassSlots csl, Slots s
 void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* flag, ClassSlots csl,
                   const int2* meta, int* ucount, int4* ulist, const float* Krow, float* Zc);
 
+// --- grid CR (one scene, contact sets beyond the cluster CR's shared memory) ------
+// Delassus groups = etree components holding contact slots; slot a's Gram row is
+// G[rowoff[a] .. + gn[a]) over the group's slots gs0[a] .. gs0[a] + gn[a] - 1.
+struct GcrData {
+    const float* c9;          // [C][3][3] row directions
+    const float* G;           // group blocks, gn^2 floats each
+    const int64_t* rowoff;    // [NS]
+    const int* gs0;           // [NS] first slot of the slot's group
+    const int* gn;            // [NS] slots in the group
+    double *r, *p, *Ap, *z, *Ar;   // [3 C]
+    double *W, *q;                 // [NS][3]
+    double* part;                  // [row blocks][3] partial dot products
+    double* sc;                    // [6] ping-pong CR scalars rAr, ApAp, stop
+    int nblk;
+};
+int gcr_row_blocks(int C);
+int gcr_kernels_per_iteration(int cr_iters);
+int launch_gcr(cudaStream_t st, const Params& P, GcrData g, const DContact* c, CrContacts cc, Slots sl,
+               const double4* x, ContactState cs);
+void launch_djj_grid(cudaStream_t st, const Params& P, DContact* c, GcrData g);
+
 size_t cr_smem_bytes(int nc, int ns);   // the CR CTA's shared-memory footprint for (nc, ns) without G_A
 int cr_cluster_size(int S);             // CTAs per instance in the CR launch
 

@@ -12,6 +12,13 @@ of the paper's workloads (SURVEY.md §8(d) "Synthetic inputs"):
 * cfg3  gingerbread-class silhouette slab -- 63x86 raster x 6 layers, Kuhn
         6-tet split (19 691 v / 93 600 t), lying on 6 thin capsule bars,
         800 contact points (seed 1234), head handle pinned.
+* cfg4  pile of 68 cubes (16^3 cells each, 5-tet split; 334k v / 1.39M t):
+        a 4x4 grid of 4-high stacks plus 4 cubes bridging 2x2 stack tops, 1 mm
+        gaps, jitter (seed 7).  ~20k contacts: bottom-layer vertices against the
+        ground, every other bottom-face vertex against the top face of the cube
+        below (soft-soft rows: the vertex minus the barycentric point of the
+        lower face triangle, 1 + 3 vertices).  `pile(cells=3, nx=2, layers=2)`
+        is the small variant the parity tests use.
 
 Contact pairs are the output of a proximity query (collision detection is
 outside the hot path); here they are generated once from
@@ -28,7 +35,7 @@ import numpy as np
 __all__ = [
     "Mesh", "Material", "Contact", "Scene",
     "hex_grid", "cantilever", "incline_block", "gingerbread", "single_tet",
-    "tangent_frame", "make_scene", "random_state", "batch_instance", "batch_instance_params",
+    "tangent_frame", "make_scene", "pile", "random_state", "batch_instance", "batch_instance_params",
 ]
 
 NEOHOOKEAN, COROTATED, ARAP = 0, 1, 2
@@ -293,6 +300,93 @@ def gingerbread(scale: float = 0.79, layers: int = 6, cell_m: float = 0.005,
     return Scene("gingerbread", mesh, mat, 0.01, 5, contacts, np.array([0.0, 0.5, 0.0]))
 
 
+# --------------------------------------------------------------------------
+# cfg4: multi-object pile
+# --------------------------------------------------------------------------
+def pile(cells: int = 16, edge: float = 0.16, nx: int = 4, layers: int = 4, bridges: bool = True,
+         gap: float = 0.001, stack_gap: float = 0.01, jitter_xy: float = 0.002, jitter_deg: float = 3.0,
+         seed: int = 7, youngs: float = 1e7, mu: float = 0.5) -> Scene:
+    """nx x nx stacks of `layers` cubes (cells^3 hex cells of edge/cells, 5-tet split) on the
+    ground z = 0, stacks `stack_gap` apart, vertical gaps `gap`; with `bridges`, one cube on
+    top of every 2x2 block of stacks, centred over their shared corner.  Each cube gets a
+    seeded horizontal offset (+-jitter_xy) and yaw (+-jitter_deg) so faces stay horizontal.
+
+    Contacts (normal +z, mu): every bottom-face vertex of a bottom-layer cube against the
+    ground (d_n = 0); every other bottom-face vertex against the top face of the cube
+    below it, if it projects inside that face: row = x_a - sum_i b_i x_i over the
+    containing top-face triangle (weights 1, -b_0, -b_1, -b_2), d_n = 0."""
+    X0, T0 = hex_grid(cells, cells, cells, cell=(edge / cells,) * 3, split="five")
+    nv0 = X0.shape[0]
+    rng = np.random.default_rng(seed)
+    half = edge / 2.0
+    pitch = edge + stack_gap
+    cubes = []   # (centre xy, z0, yaw)
+    for layer in range(layers):
+        for i in range(nx):
+            for j in range(nx):
+                cubes.append([(i - (nx - 1) / 2.0) * pitch, (j - (nx - 1) / 2.0) * pitch, layer * (edge + gap)])
+    if bridges:
+        for i in range(0, nx - 1, 2):
+            for j in range(0, nx - 1, 2):
+                cx = (i + 0.5 - (nx - 1) / 2.0) * pitch
+                cy = (j + 0.5 - (nx - 1) / 2.0) * pitch
+                cubes.append([cx, cy, layers * (edge + gap)])
+    Xs, Ts, frames = [], [], []
+    local = X0 - np.array([half, half, 0.0])     # cube-local: centred in xy, bottom at z = 0
+    for k, (cx, cy, z0) in enumerate(cubes):
+        dx, dy = rng.uniform(-jitter_xy, jitter_xy, 2)
+        yaw = math.radians(rng.uniform(-jitter_deg, jitter_deg))
+        c, s_ = math.cos(yaw), math.sin(yaw)
+        R = np.array([[c, -s_, 0.0], [s_, c, 0.0], [0.0, 0.0, 1.0]])
+        o = np.array([cx + dx, cy + dy, z0])
+        Xs.append(local @ R.T + o)
+        Ts.append(T0 + k * nv0)
+        frames.append((o, R))
+    X = np.concatenate(Xs)
+    T = np.concatenate(Ts).astype(np.int32)
+    mesh = Mesh(X, T, np.zeros(X.shape[0], np.uint8))
+    # local grid indices of the cube's vertices (hex_grid numbering: (i, j, k) lexicographic)
+    n1 = cells + 1
+    vid = lambda i, j, k: (i * n1 + j) * n1 + k
+    bottom = np.array([vid(i, j, 0) for i in range(n1) for j in range(n1)])
+    h_cell = edge / cells
+    nz = np.array([0.0, 0.0, 1.0])
+    t1, t2 = tangent_frame(nz)
+    contacts: List[Contact] = []
+    top_z = [z0 + edge for (_, _, z0) in cubes]
+    for k, (o, R) in enumerate(frames):
+        base = k * nv0
+        if o[2] < 1e-9:      # bottom layer: the ground plane z = 0
+            for v in bottom:
+                contacts.append(Contact([int(base + v)], [1.0], nz.copy(), 0.0, mu=mu, tangent1=t1, tangent2=t2))
+            continue
+        # candidate supports: cubes whose top is just below this cube's bottom
+        below = [q for q in range(len(cubes)) if abs(top_z[q] + gap - o[2]) < 1e-9]
+        for v in bottom:
+            p = X[base + v]
+            for q in below:
+                oq, Rq = frames[q]
+                lp = Rq.T @ (p - oq) + np.array([half, half, 0.0])   # in q's grid frame
+                u, w = lp[0] / h_cell, lp[1] / h_cell
+                if not (0.0 <= u <= cells and 0.0 <= w <= cells):
+                    continue
+                i, j = min(int(u), cells - 1), min(int(w), cells - 1)
+                fu, fw = u - i, w - j
+                qb = q * nv0
+                if fu >= fw:     # triangle (i,j) (i+1,j) (i+1,j+1)
+                    tri = [vid(i, j, cells), vid(i + 1, j, cells), vid(i + 1, j + 1, cells)]
+                    bc = [1.0 - fu, fu - fw, fw]
+                else:            # triangle (i,j) (i+1,j+1) (i,j+1)
+                    tri = [vid(i, j, cells), vid(i + 1, j + 1, cells), vid(i, j + 1, cells)]
+                    bc = [1.0 - fw, fu, fw - fu]
+                contacts.append(Contact([int(base + v)] + [int(qb + t) for t in tri],
+                                        [1.0] + [-float(b) for b in bc], nz.copy(), 0.0, mu=mu,
+                                        tangent1=t1, tangent2=t2))
+                break
+    mat = Material(model=NEOHOOKEAN, density=1000.0, youngs=youngs, poisson=0.3)
+    return Scene("pile", mesh, mat, 0.01, 5, contacts, np.zeros(3))
+
+
 def make_scene(name: str, **kw) -> Scene:
     if name in ("cfg1", "cantilever"):
         m = cantilever()
@@ -302,6 +396,8 @@ def make_scene(name: str, **kw) -> Scene:
         return incline_block(**kw)
     if name in ("cfg3", "gingerbread"):
         return gingerbread(**kw)
+    if name in ("cfg4", "pile"):
+        return pile(**kw)
     if name == "block":   # small multi-purpose block used by parity tests
         nv = kw.get("nv", 6)
         X, T = hex_grid(nv - 1, nv - 1, nv - 1, cell=(0.02,) * 3, split=kw.get("split", "five"))

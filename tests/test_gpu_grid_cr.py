@@ -1,0 +1,166 @@
+"""Grid CR (contact sets beyond one cluster, include/sim.h sim_set_cr_mode) and the
+multi-object pile: GPU vs the fp64 oracle through the C ABI.
+
+The grid CR runs the same CR (Saad 6.20, exactly N_CR matvecs, reading A19) as the
+cluster CR with the vectors in global memory and the Delassus Gram stored per etree
+component; forcing it on sets the cluster CR also handles checks both against the
+oracle.  The pile has soft-soft rows (a vertex of the upper cube minus the barycentric
+point of the lower cube's face: 1 + 3 vertices with weights 1, -b), so D couples
+contacts of different objects through shared slots while G is block-diagonal.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import scenes
+from oracle import oracle as O
+
+try:
+    from paper_2503_15078_b200._lib import debug_contact_state
+except Exception:   # library not built: the gpu tests are skipped anyway
+    debug_contact_state = None
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def simmod():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_15078_b200 as m
+    return m
+
+
+def make(simmod, sc, mode):
+    s = simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+    s.set_cr_mode(mode)
+    s.set_pin_velocity(sc.pin_velocity)
+    s.set_contacts(sc.contacts)
+    return s
+
+
+def resynced_frames(s, o, sc, frames, tol):
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+    errs = []
+    for f in range(frames):
+        s.set_state(x, v)
+        s.step(1, 5)
+        xg, vg = s.get_state()
+        pins = x[o.pinned] + sc.h * sc.pin_velocity if o.pinned.size else None
+        xo, vo, info = o.frame(x, v, pin_targets=pins)
+        err = float(np.abs(xg - xo).max())
+        errs.append(err)
+        assert err < tol, (f, err, tol)
+        x, v = xg, vg
+    return errs
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_incline_both_solvers_match_oracle(simmod, mode):
+    """cfg2-like incline (E = 1e8, mu = tan 10 deg - 0.05: sliding), 6 re-synced frames."""
+    sc = scenes.incline_block(theta_deg=10.0, mu=math.tan(math.radians(10.0)) - 0.05, nv=5, edge=0.1,
+                              youngs=1e8)
+    s = make(simmod, sc, mode)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(sc.contacts)
+    resynced_frames(s, o, sc, 6, 1e-5 * sc.mesh.bbox_diag())
+
+
+def test_grid_and_cluster_cr_agree_on_cfg3(simmod):
+    """cfg3 (800 contacts): the two CR implementations give the same frame up to rounding order."""
+    sc = scenes.make_scene("cfg3")
+    out = []
+    for mode in (1, 2):
+        s = make(simmod, sc, mode)
+        s.step(2, 5)
+        x, _ = s.get_state()
+        out.append((x, s.get_lambda(), s.stats()))
+    d = np.abs(out[0][0] - out[1][0]).max()
+    assert d < 1e-6 * sc.mesh.bbox_diag(), d
+    assert out[1][2]["kernels_per_frame"] > out[0][2]["kernels_per_frame"]
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_small_pile_parity(simmod, mode):
+    """Pile of 9 cubes (3^3 cells: 2x2 stacks of 2 + 1 bridge), ground and soft-soft rows:
+    positions within 1e-5 bbox of the oracle every re-synced frame; same active set."""
+    sc = scenes.pile(cells=3, nx=2, layers=2)
+    assert any(len(c.verts) == 4 for c in sc.contacts)
+    s = make(simmod, sc, mode)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(sc.contacts)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+    for f in range(6):
+        s.set_state(x, v)
+        s.step(1, 5)
+        xg, vg = s.get_state()
+        xo, vo, info = o.frame(x, v)
+        err = float(np.abs(xg - xo).max())
+        assert err < tol, (f, err, tol)
+        lg = s.get_lambda()
+        act_o = info["lam"][0::3] > 0
+        act_g = lg[0::3] > 0
+        assert (act_o == act_g).mean() > 0.97, (f, (act_o != act_g).sum())
+        x, v = xg, vg
+
+
+def test_small_pile_delassus_blocks(simmod):
+    """Grid-mode Gram: D_jj-relevant blocks equal (A^-1)_ab on each component and are
+    exactly zero across components (K is block-diagonal over the etree forest)."""
+    sc = scenes.pile(cells=3, nx=2, layers=2)
+    s = make(simmod, sc, 2)
+    cv, G = s.debug_delassus()
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(sc.contacts)
+    pos = {int(v): i for i, v in enumerate(o.vc)}
+    idx = np.array([pos[int(v)] for v in cv])
+    Go = o.G[np.ix_(idx, idx)]
+    nv0 = 4 ** 3
+    comp = np.asarray(cv) // nv0
+    same = comp[:, None] == comp[None, :]
+    assert np.all(G[~same] == 0.0)
+    assert np.abs(G - Go).max() <= 2e-5 * np.abs(Go).max()
+
+
+def test_cfg4_full_size(simmod):
+    """cfg4 at full size (68 cubes of 16^3 cells: 334k vertices, 1.39M tets, ~18k contacts,
+    ~13k soft-soft): frames on the grid CR; sampled checks the oracle can afford at this
+    size (its dense J A^-1 J^T would need ~80 GB): K^T K b vs the oracle's sparse LU solve,
+    sampled Delassus diagonals vs sum w w (A^-1)_ab, and physical properties of the frames."""
+    sc = scenes.make_scene("cfg4")
+    s = make(simmod, sc, 0)
+    st = s.stats()
+    assert st["n_contacts"] == len(sc.contacts) > 15000
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    # apply-inverse on one seeded right-hand side (all 68 components at once)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal((sc.mesh.n_v, 3))
+    xg = s.debug_apply_inverse(b)
+    xo = o.solve(b[o.free])
+    assert np.abs(xg[o.free] - xo).max() <= 1e-5 * np.abs(xo).max()
+    # Delassus diagonal of sampled contacts (ground and soft-soft): D_jj = sum w_a w_b (A^-1)_ab
+    s.step(1, 1)
+    djj = debug_contact_state(s)["djj"]
+    pick = np.concatenate([np.arange(0, len(sc.contacts), 997), [len(sc.contacts) - 1]])
+    vs = np.unique(np.concatenate([sc.contacts[c].verts for c in pick]))
+    pos = -np.ones(sc.mesh.n_v, dtype=np.int64)
+    pos[o.free] = np.arange(o.free.size)
+    E = np.zeros((o.free.size, vs.size))
+    E[pos[vs], np.arange(vs.size)] = 1.0
+    Z = o.lu.solve(E)
+    col = {int(v): k for k, v in enumerate(vs)}
+    for c in pick:
+        ct = sc.contacts[c]
+        d = sum(wa * wb * Z[pos[a], col[b]] for a, wa in zip(ct.verts, ct.weights)
+                for b, wb in zip(ct.verts, ct.weights))
+        assert abs(djj[c] - d) <= 2e-5 * abs(d), (c, djj[c], d)
+    # two frames: finite, the pile does not sink through the ground, CR residual reported
+    s.step(2, 5)
+    x, v = s.get_state()
+    assert np.isfinite(x).all() and np.isfinite(v).all()
+    assert x[:, 2].min() > -2e-3
+    st = s.stats()
+    assert st["last_cr_residual"] >= 0 and st["n_active"] > 0
