@@ -19,8 +19,10 @@ the paper's own definitions):
                    via numpy's SVD + per-material sigma-space solve (A2-A5).
 * contacts         J rows (App. A), D = J A^-1 J^T by direct
                    solves (eq. schur-complement, plain definition),
-                   r_n = h^2 D_jj, r_f = h D_jj,
-                   FB indicators (App. B.2; readings A14-A16),
+                   r_n = h^2 D_jj, r_f = h D_jj -- or, for the
+                   ablation, the mass-inverse r from [J M^-1 J^T]_jj,
+                   FB indicators (App. B.2; readings A14-A16) --
+                   or min-map (App. B.1, P:L1594-1655),
                    Schur RHS with the Alg. 3/4 sign (A11),
                    CR (Saad Alg. 6.20) with exactly N_CR iterations (A19),
                    lambda update + corrected global solve (P:L955-956).
@@ -44,8 +46,11 @@ import scipy.sparse.linalg as spla
 __all__ = [
     "lame", "rest_data", "assemble_Av", "deformation_gradients", "signed_svd",
     "project_sigma", "project", "elastic_forces", "Oracle", "cr_solve",
-    "fb_normal", "fb_friction", "contact_rows",
+    "fb_normal", "fb_friction", "minmap_normal", "minmap_friction", "contact_rows",
 ]
+
+NCP_FB, NCP_MINMAP = 0, 1                  # NCP function (App. B)
+PRECOND_DELASSUS, PRECOND_MASS = 0, 1      # complementarity preconditioner (P:L873-880 / P:L918-925)
 
 NEOHOOKEAN, COROTATED, ARAP = 0, 1, 2
 
@@ -273,6 +278,39 @@ def fb_friction(ydot, lam_f, lam_n, mu, r):
 
 
 # ---------------------------------------------------------------------------
+# NCP functions (App. B.1, minimum map) -- the ablation of P:L1200-1214 (NEXT row 1)
+# ---------------------------------------------------------------------------
+def minmap_normal(y, lam_n, r):
+    """phi_n = y if y <= r lam else r lam;  theta_n = dphi/dy = 1 | 0;
+    E_n = dphi/dlam = 0 | r  (P:L1596-1624)."""
+    y = np.asarray(y, dtype=np.float64)
+    rl = np.asarray(r, dtype=np.float64) * np.asarray(lam_n, dtype=np.float64)
+    first = y <= rl
+    phi = np.where(first, y, rl)
+    theta = np.where(first, 1.0, 0.0)
+    E = np.where(first, 0.0, np.asarray(r, dtype=np.float64) * np.ones_like(y))
+    return phi, theta, E
+
+
+def minmap_friction(ydot, lam_f, lam_n, mu, r):
+    """theta_f = [lam_n > 0] (P:L1635-1643); E_f (P:L1644-1654) = identity if lam_n <= 0,
+    0 if |ydot| <= r (mu lam_n - |lam_f|) (stick), else (|ydot| - r (mu lam_n - |lam_f|)) /
+    (mu lam_n) (slip).  A degenerate cone mu lam_n <= 0 takes the inactive branch (reading
+    A16b, as for FB); phi_f = theta_f ydot + E_f lam_f (reading A14)."""
+    ydot = np.asarray(ydot, dtype=np.float64)
+    lam_f = np.asarray(lam_f, dtype=np.float64)
+    s = np.linalg.norm(ydot, axis=-1)
+    q = mu * lam_n - np.linalg.norm(lam_f, axis=-1)
+    act = (lam_n > 0) & (mu * lam_n > 0)
+    stick = s <= r * q
+    with np.errstate(divide="ignore", invalid="ignore"):
+        slip = (s - r * q) / np.where(act, mu * lam_n, 1.0)
+    E = np.where(act, np.where(stick, 0.0, slip), 1.0)
+    theta = np.where(act, 1.0, 0.0)
+    return theta, E
+
+
+# ---------------------------------------------------------------------------
 # Conjugate Residual (Saad, Iterative Methods, Alg. 6.20); reading A19
 # ---------------------------------------------------------------------------
 def cr_solve(apply, b: np.ndarray, n_iter: int, tiny: float = 1e-300):
@@ -368,7 +406,7 @@ class Oracle:
     """
 
     def __init__(self, mesh, material, h: float, lg_iters: int = 5,
-                 cr_iters: Optional[int] = None):
+                 cr_iters: Optional[int] = None, ncp: int = NCP_FB, precond: int = PRECOND_DELASSUS):
         self.X = np.asarray(mesh.X, dtype=np.float64)
         self.T = np.asarray(mesh.T, dtype=np.int64)
         self.fixed = np.asarray(mesh.fixed).astype(bool)
@@ -380,6 +418,8 @@ class Oracle:
         self.g = np.asarray(material.gravity, dtype=np.float64)
         self.lg_iters = int(lg_iters)
         self.cr_iters = int(material.cr_iterations if cr_iters is None else cr_iters)
+        self.ncp = int(ncp)            # FB (the paper's choice) or min-map (App. B.1)
+        self.precond = int(precond)    # Delassus diagonal (eq. complementarity preconditioner) or mass inverse
         self.Bm, self.vol, self.w, self.M = rest_data(self.X, self.T, material.density, self.k)
         self.A = assemble_Av(self.n_v, self.T, self.Bm, self.w, self.M, self.h)
         self.free = np.nonzero(~self.fixed)[0]
@@ -426,8 +466,12 @@ class Oracle:
         self.D = (Wm @ G @ Wm.T) * (C @ C.T)
         self.G, self.vc, self.Wm = G, vc, Wm
         djj = np.diag(self.D).copy()
-        # preconditioner: unilateral h^2 D_jj, frictional h D_jj
         kind = self.rows.kind
+        if self.precond == PRECOND_MASS:
+            # Macklin's choice: [J M^-1 J^T]_jj with the lumped M (A6), M = M_v (x) I_3
+            Minv = 1.0 / self.M[vc]
+            djj = (Wm * Wm) @ Minv * np.einsum("jd,jd->j", C, C)
+        # preconditioner (P:L921-922 / P:L875-876): unilateral h^2 [.]_jj, frictional h [.]_jj
         self.r_row = np.where(kind == 1, self.h * djj, self.h * self.h * djj)
         own = self.rows.contact
         self.mu_c = np.array([ct.mu for ct in self.contacts], dtype=np.float64)
@@ -485,12 +529,13 @@ class Oracle:
                 E[j0] = self.e_row[j0]
                 continue
             yn = Jx[j0] - self.d_row[j0]              # y_n = J_n x^k - d_n
-            ph, th, En = fb_normal(yn, lam[j0], self.r_row[j0])
+            nfun, ffun = (minmap_normal, minmap_friction) if self.ncp == NCP_MINMAP else (fb_normal, fb_friction)
+            ph, th, En = nfun(yn, lam[j0], self.r_row[j0])
             phi[j0], theta[j0], E[j0] = ph, th, En
             jf = [j0 + 1, j0 + 2]
             # h ydot_f = J_f (x^k - x_t) - h d_f
             ydot = (Jx[jf] - Jxt[jf]) / h - self.d_row[jf]
-            thf, Ef = fb_friction(ydot, lam[jf], lam[j0], ct.mu, self.r_row[jf[0]])
+            thf, Ef = ffun(ydot, lam[jf], lam[j0], ct.mu, self.r_row[jf[0]])
             theta[jf] = thf
             E[jf] = Ef
             phi[jf] = thf * ydot + Ef * lam[jf]       # A14

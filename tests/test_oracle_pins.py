@@ -412,3 +412,90 @@ def test_zero_penetration_at_convergence():
     lam_n = info["lam"][0::3]
     phi, _, _ = O.fb_normal(yn, lam_n, o.r_row[0::3])
     assert np.max(np.abs(phi)) < 1e-6 * max(1.0, o.r_row[0])
+
+
+# ------------------------------------------- min-map + mass-inverse ablation (NEXT row 1)
+def test_golden_minmap_values():
+    for e in GOLD["minmap_phi"]:
+        phi, _, _ = O.minmap_normal(e["y"], e["lam"], e["r"])
+        assert float(phi) == e["phi"], e["cite"]
+    for e in GOLD["minmap_normal_case"]:
+        _, th, E = O.minmap_normal(e["y"], e["lam"], e["r"])
+        assert float(th) == e["theta"] and float(E) == e["E"], e["cite"]
+
+
+def test_minmap_derivatives_and_complementarity():
+    """App. B.1: theta_n = d phi/d y and E_n = d phi/d lam off the kink y = r lam; phi = 0
+    exactly on the complementarity set {y = 0 <= lam} U {lam = 0 <= y}."""
+    rng = np.random.default_rng(11)
+    for _ in range(50):
+        y, lam, r = rng.standard_normal(), abs(rng.standard_normal()), abs(rng.standard_normal()) + 0.1
+        if abs(y - r * lam) < 1e-3:
+            continue
+        phi, th, E = O.minmap_normal(y, lam, r)
+        d = 1e-7
+        dy = (O.minmap_normal(y + d, lam, r)[0] - O.minmap_normal(y - d, lam, r)[0]) / (2 * d)
+        dl = (O.minmap_normal(y, lam + d, r)[0] - O.minmap_normal(y, lam - d, r)[0]) / (2 * d)
+        assert abs(dy - th) < 1e-6 and abs(dl - E) < 1e-6
+    for lam in (0.0, 0.3, 7.0):
+        assert float(O.minmap_normal(0.0, lam, 0.5)[0]) == 0.0
+    for y in (0.0, 0.2, 3.0):
+        assert float(O.minmap_normal(y, 0.0, 0.5)[0]) == 0.0
+
+
+def test_minmap_friction_cases():
+    """App. B.1 friction: inactive -> theta 0, E = I; stick (|ydot| <=
+    r(mu lam_n - |lam_f|)) -> E = 0; slip -> E = (|ydot| - r q)/(mu lam_n), which on the
+    cone boundary (q = 0) makes phi_f = ydot + |ydot|/(mu lam_n) lam_f vanish exactly for
+    the maximal-dissipation force lam_f = -mu lam_n ydot/|ydot|."""
+    th, E = O.minmap_friction(np.array([0.3, 0.1]), np.zeros(2), 0.0, 0.5, 0.2)
+    assert th == 0.0 and E == 1.0
+    th, E = O.minmap_friction(np.array([0.01, 0.0]), np.array([0.1, 0.0]), 1.0, 0.5, 0.2)
+    assert th == 1.0 and E == 0.0            # 0.01 <= 0.2 (0.5 - 0.1)
+    yd = np.array([0.3, -0.4])
+    lf = -0.5 * 2.0 * yd / np.linalg.norm(yd)
+    th, E = O.minmap_friction(yd, lf, 2.0, 0.5, 0.07)
+    assert abs(E - np.linalg.norm(yd) / (0.5 * 2.0)) < 1e-15
+    assert np.abs(th * yd + E * lf).max() < 1e-15
+    th, E = O.minmap_friction(np.array([0.3, 0.0]), np.zeros(2), 1.0, 0.0, 0.2)
+    assert th == 0.0 and E == 1.0
+
+
+def test_mass_inverse_preconditioner_closed_form():
+    """r_n = h^2 [J M^-1 J^T]_jj, r_f = h [J M^-1 J^T]_jj.  One vertex of mass
+    m: 1/m; a soft-soft row x_a - sum b_i x_i: 1/m_a + sum b_i^2/m_i (c unit)."""
+    mesh = scenes.single_tet()
+    vol = 0.1 ** 3 / 6.0
+    mat = scenes.Material(model=O.ARAP, density=1000.0, youngs=1e6, poisson=0.3)
+    h = 0.01
+    o = O.Oracle(mesh, mat, h, precond=O.PRECOND_MASS)
+    m = 1000.0 * vol / 4.0
+    n = np.array([0.0, 0.0, 1.0])
+    o.set_contacts([scenes.Contact([1], [1.0], n, 0.0, mu=0.5),
+                    scenes.Contact([3, 0, 1, 2], [1.0, -0.2, -0.3, -0.5], n, 0.0, mu=0.5)])
+    assert abs(o.r_row[0] - h * h / m) < 1e-12 * h * h / m
+    assert np.allclose(o.r_row[1:3], h / m, rtol=1e-12)
+    q = (1.0 + 0.04 + 0.09 + 0.25) / m
+    assert abs(o.r_row[3] - h * h * q) < 1e-12 * h * h * q and np.allclose(o.r_row[4:6], h * q, rtol=1e-12)
+    # the Delassus diagonal is larger than the mass-inverse one only through A^-1 <= M^-1 ... (A = M + h^2 L)
+    od = O.Oracle(mesh, mat, h)
+    od.set_contacts(o.contacts)
+    assert np.all(od.r_row <= o.r_row * (1 + 1e-12))
+
+
+def test_minmap_contact_statics():
+    """With min-map (App. B.1) the resting-contact statics of S:L389 hold as with FB:
+    converged sum lam_n = m g, tangential forces cancel and stay in the cone, body at rest."""
+    mesh, cs = _floor_tet(0.5)
+    mat = scenes.Material(model=O.NEOHOOKEAN, youngs=1e7)
+    o = O.Oracle(mesh, mat, 0.01, lg_iters=40, cr_iters=40, ncp=O.NCP_MINMAP)
+    o.set_contacts(cs)
+    x, v = mesh.X.copy(), np.zeros_like(mesh.X)
+    for _ in range(20):
+        x, v, info = o.frame(x, v)
+    lam = info["lam"].reshape(-1, 3)
+    mg = o.M.sum() * 9.81
+    assert abs(lam[:, 0].sum() - mg) < 1e-9 * mg
+    assert np.all(np.abs(lam[:, 1:].sum(0)) < 1e-9 * mg)
+    assert np.all(np.linalg.norm(lam[:, 1:], axis=1) <= 0.5 * lam[:, 0] + 1e-12)
+    assert np.max(np.abs(v)) < 1e-9
