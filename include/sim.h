@@ -196,6 +196,15 @@ int sim_set_profiling(sim_handle *h, int on);
  * 1 = cluster CR only (SIM_E_LIMIT if the current set does not fit),
  * 2 = grid CR always (n_instances == 1 only).  Takes effect at the next step. */
 int sim_set_cr_mode(sim_handle *h, int32_t mode);
+
+/* NCP function and complementarity preconditioner (the paper's ablation,
+ * Fig. 11, P:L883-916 / P:L1200-1214).  ncp_function: 0 = Fischer-Burmeister
+ * (App. B.2, the paper's choice), 1 = minimum map (App. B.1).
+ * preconditioner: 0 = Delassus diagonal r_n = h^2 D_jj, r_f = h D_jj
+ * (eq. complementarity preconditioner), 1 = mass inverse
+ * r = h^2 / h [J M^-1 J^T]_jj with the lumped M.  Defaults 0, 0;
+ * SIM_E_INVALID on other values.  Takes effect at the next step. */
+int sim_set_ncp(sim_handle *h, int32_t ncp_function, int32_t preconditioner);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 
 void sim_destroy(sim_handle *h);         /* NULL-safe */

@@ -17,7 +17,7 @@ EXPORTED_SYMBOLS = [
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
-    "sim_get_positions", "sim_set_states", "sim_set_cr_mode",
+    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -113,6 +113,7 @@ def _load():
         "sim_debug_get_delassus": [H, C.c_int32, ip, fp, C.c_int32],
         "sim_set_profiling": [H, C.c_int],
         "sim_set_cr_mode": [H, C.c_int32],
+        "sim_set_ncp": [H, C.c_int32, C.c_int32],
         "sim_get_kernel_times": [H, dp, C.c_int32],
         "sim_debug_contact_state": [H, C.c_int32, dp, dp, dp, dp, ip, dp],
         "sim_debug_cr_timeline": [H, dp],
@@ -292,6 +293,10 @@ class Sim:
     def set_cr_mode(self, mode: int):
         """0 automatic, 1 cluster CR, 2 grid CR (include/sim.h sim_set_cr_mode)."""
         _check(lib.sim_set_cr_mode(self._h, int(mode)))
+
+    def set_ncp(self, ncp: int = 0, precond: int = 0):
+        """NCP function 0 FB / 1 min-map; preconditioner 0 Delassus / 1 mass inverse (sim_set_ncp)."""
+        _check(lib.sim_set_ncp(self._h, int(ncp), int(precond)))
 
     def set_profiling(self, on: bool):
         _check(lib.sim_set_profiling(self._h, 1 if on else 0))

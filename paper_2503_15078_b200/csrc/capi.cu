@@ -182,6 +182,7 @@ struct sim_handle {
     double set_contacts_host_us = 0;
     // grid CR (large contact sets of one scene): Delassus groups = etree components
     int cr_mode = 0;                 // 0 auto, 1 cluster CR only, 2 grid CR always
+    int ncp = 0, precond = 0;        // NCP function / complementarity preconditioner (sim_set_ncp)
     bool grid = false;               // the committed contact set uses the grid CR
     int NG = 0, ng_max = 0;
     std::vector<int32_t> comp_root;  // [n_f] root of each free vertex's etree component
@@ -524,6 +525,7 @@ static int build_inst(const sim_handle* H, const sim_contact* cs, int n, InstCon
             if (!std::isfinite(s.weights[q])) return bad(SIM_E_INVALID, "contact %d: weight not finite", c);
             d.vtx[q] = H->orig2int[s.verts[q]];
             d.w[q] = s.weights[q];
+            d.Mjj += s.weights[q] * s.weights[q] / H->rd.mass[s.verts[q]];   // [J M^-1 J^T]_jj, unit c
             verts.push_back(d.vtx[q]);
         }
         double t1[3], t2[3];
@@ -685,6 +687,8 @@ static Params make_params(const sim_handle* H) {
     P.CS = H->CS;
     P.cm_max = H->cm_max;
     P.cr_iters = H->mat.cr_iterations;
+    P.ncp = H->ncp;
+    P.precond = H->precond;
     return P;
 }
 
@@ -1075,6 +1079,16 @@ static int enqueue_frame(sim_handle* H, int iters) {
     return nk;
 }
 
+extern "C" int sim_set_ncp(sim_handle* H, int32_t ncp_function, int32_t preconditioner) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (ncp_function < 0 || ncp_function > 1) return fail(SIM_E_INVALID, "NCP function must be 0 (FB) or 1 (min-map)");
+    if (preconditioner < 0 || preconditioner > 1)
+        return fail(SIM_E_INVALID, "preconditioner must be 0 (Delassus) or 1 (mass inverse)");
+    H->ncp = ncp_function;
+    H->precond = preconditioner;
+    return SIM_OK;   // Params are captured: the graph key includes both
+}
+
 extern "C" int sim_set_cr_mode(sim_handle* H, int32_t mode) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (mode < 0 || mode > 2) return fail(SIM_E_INVALID, "CR mode must be 0 (auto), 1 (cluster) or 2 (grid)");
@@ -1117,7 +1131,8 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     int rc = commit_contacts(H);
     if (rc) return rc;
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
-                                      H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG};
+                                      H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG,
+                                      H->ncp, H->precond};
     if (!H->gexec || key != H->gkey) {
         if (H->gexec) {
             cudaGraphExecDestroy(H->gexec);

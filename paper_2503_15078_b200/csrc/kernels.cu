@@ -365,12 +365,16 @@ __global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const d
         cs.phi_abs[c] = 0.0;
         return;
     }
-    double rn = h * h * ct.Djj, rf = h * ct.Djj;
-    // normal FB (A15)
+    const double pjj = P.precond ? ct.Mjj : ct.Djj;
+    double rn = h * h * pjj, rf = h * pjj;
     double y = Jx[0] - ct.dn, ln = lam[0];
-    double S = sqrt(y * y + rn * rn * ln * ln);
     double phin, thn, En;
-    if (S > 0.0) {
+    if (P.ncp == 1) {   // minimum map (App. B.1)
+        const bool first = y <= rn * ln;
+        phin = first ? y : rn * ln;
+        thn = first ? 1.0 : 0.0;
+        En = first ? 0.0 : rn;
+    } else if (double S = sqrt(y * y + rn * rn * ln * ln); S > 0.0) {   // normal FB (A15)
         double a = y + rn * ln;
         phin = a > 0.0 ? (2.0 * y * rn * ln) / (a + S) : a - S;
         thn = 1.0 - y / S;
@@ -387,11 +391,15 @@ __global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const d
         double lf = sqrt(lam[1] * lam[1] + lam[2] * lam[2]);
         double q = ct.mu * ln - lf;
         double R = sqrt(s * s + rf * rf * q * q);
-        double num = rf * (R - rf * q);
-        double den = s + ct.mu * rf * ln - R;
-        double fl = 1e-6 * (s + ct.mu * rf * ln);
-        den = den > fl ? den : fl;
-        Ef = den > 0.0 ? num / den : 0.0;
+        if (P.ncp == 1) {   // minimum map: stick 0, slip (|ydot| - r q) / (mu lam_n)
+            Ef = s <= rf * q ? 0.0 : (s - rf * q) / (ct.mu * ln);
+        } else {
+            double num = rf * (R - rf * q);
+            double den = s + ct.mu * rf * ln - R;
+            double fl = 1e-6 * (s + ct.mu * rf * ln);
+            den = den > fl ? den : fl;
+            Ef = den > 0.0 ? num / den : 0.0;
+        }
         thf = 1.0;
     } else {
         thf = 0.0; Ef = 1.0;

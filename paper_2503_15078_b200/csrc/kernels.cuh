@@ -30,6 +30,7 @@ struct DContact {
     double c[3][3];     // rows: n, t1, t2 (bilateral: n, 0, 0)
     double dn, df1, df2, mu, e;
     double Djj;         // D_jj (Delassus diagonal, same for the 3 unit rows)
+    double Mjj;         // [J M^-1 J^T]_jj (mass-inverse preconditioner of the ablation)
 };
 
 struct Params {
@@ -45,6 +46,8 @@ struct Params {
     int NCL, CS;          // slot-set classes, class slots
     int cm_max;           // largest class (members)
     int cr_iters;
+    int ncp;              // 0 Fischer-Burmeister (App. B.2, the paper's choice), 1 minimum map (App. B.1)
+    int precond;          // 0 Delassus diagonal, 1 mass inverse
 };
 
 // Offsets of the packed contact data.  Instances whose contact-vertex sets are equal form
