@@ -189,6 +189,9 @@ struct sim_handle {
     DPtr<int> gcsoff, gs0, gn;       // group slot offsets [NG+1]; per slot: group start, size
     DPtr<int64_t> ggoff, growoff;    // group G offsets [NG+1]; per slot: its G row
     DBuf<double> g_r, g_p, g_Ap, g_z, g_Ar, g_W, g_q, g_part, g_sc;
+    DBuf<int> g_cnt;
+    DPtr<int2> g_items;              // Gram matvec items (arena)
+    int n_g_items = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -663,6 +666,9 @@ static GcrData gcr_data(sim_handle* H) {
     g.gn = H->gn.p;
     g.r = H->g_r.p; g.p = H->g_p.p; g.Ap = H->g_Ap.p; g.z = H->g_z.p; g.Ar = H->g_Ar.p;
     g.W = H->g_W.p; g.q = H->g_q.p; g.part = H->g_part.p; g.sc = H->g_sc.p;
+    g.cnt = H->g_cnt.p;
+    g.gram_items = H->g_items.p;
+    g.n_gram_items = H->n_g_items;
     g.nblk = 0;
     return g;
 }
@@ -794,7 +800,12 @@ static int commit_contacts(sim_handle* H) {
         const size_t nb = (size_t)gcr_row_blocks(Ct);
         CK(H->g_r.ensure(3 * cC, grew)); CK(H->g_p.ensure(3 * cC, grew)); CK(H->g_Ap.ensure(3 * cC, grew));
         CK(H->g_z.ensure(3 * cC, grew)); CK(H->g_Ar.ensure(3 * cC, grew)); CK(H->g_W.ensure(3 * cS, grew));
-        CK(H->g_q.ensure(3 * cS, grew)); CK(H->g_part.ensure(3 * nb, grew)); CK(H->g_sc.ensure(8, grew));
+        CK(H->g_q.ensure(3 * cS, grew)); CK(H->g_part.ensure(3 * std::max<size_t>(nb, 148), grew));
+        CK(H->g_sc.ensure(8, grew));
+        if (!H->g_cnt.p) {
+            CK(H->g_cnt.alloc(1));
+            CK(cudaMemset(H->g_cnt.p, 0, sizeof(int)));
+        }
     }
     CK(H->chain_rows.ensure(std::max<int64_t>(zoff[NCL], 1), grew));
     CK(H->Zc.ensure(std::max<int64_t>(zoff[NCL], 1), grew)); CK(H->ulist.ensure(std::max(uoff[NCL], 1), grew));
@@ -817,15 +828,18 @@ static int commit_contacts(sim_handle* H) {
               g_zo = seg(8 * C1), g_cmo = seg(4 * C1), g_cm = seg(4 * (size_t)S), g_icd = seg(8 * it_cd.size()),
               g_isc = seg(8 * it_sc.size());
     const size_t NSg = grid ? (size_t)NSt : 0;
+    std::vector<int2> gitems;   // Gram matvec items: 32 consecutive rows of one group
+    for (int g = 0; grid && g < NG; ++g)
+        for (int q = gcs[g]; q < gcs[g + 1]; q += 32) gitems.push_back(make_int2(q, std::min(32, gcs[g + 1] - q)));
     const Seg g_gcs = seg(4 * gcs.size()), g_ggo = seg(8 * ggo.size()), g_grw = seg(8 * NSg), g_gs0 = seg(4 * NSg),
-              g_gn = seg(4 * NSg);
+              g_gn = seg(4 * NSg), g_git = seg(8 * gitems.size());
     const size_t need = cur + 256;
     CK(H->arena.ensure(need, grew));
     {   // captured pointers change when the arena moves or any segment offset moves
         const std::vector<size_t> lay = {g_dc.at, g_c9.at, g_s0.at, g_v0.at, g_c1.at, g_sv.at, g_si.at, g_scp.at,
                                          g_sci.at, g_scw.at, g_ch.at, g_cv.at, g_cc.at, g_co.at, g_so.at, g_ga.at,
                                          g_cl.at, g_cso.at, g_go.at, g_uo.at, g_zo.at, g_cmo.at, g_cm.at, g_icd.at,
-                                         g_isc.at, g_gcs.at, g_ggo.at, g_grw.at, g_gs0.at, g_gn.at};
+                                         g_isc.at, g_gcs.at, g_ggo.at, g_grw.at, g_gs0.at, g_gn.at, g_git.at};
         if (grew || lay != H->arena_layout) H->contact_gen++;
         H->arena_layout = lay;
     }
@@ -843,6 +857,7 @@ static int commit_contacts(sim_handle* H) {
         H->it_sc.p = (int2*)(A + g_isc.at);
         H->gcsoff.p = (int*)(A + g_gcs.at); H->ggoff.p = (int64_t*)(A + g_ggo.at);
         H->growoff.p = (int64_t*)(A + g_grw.at); H->gs0.p = (int*)(A + g_gs0.at); H->gn.p = (int*)(A + g_gn.at);
+        H->g_items.p = (int2*)(A + g_git.at);
     }
     if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
     CK(cudaEventSynchronize(H->stage_free));   // the previous commit's copies are done
@@ -916,6 +931,8 @@ static int commit_contacts(sim_handle* H) {
     if (!it_cd.empty()) memcpy(B + g_icd.at, it_cd.data(), 8 * it_cd.size());
     if (!it_sc.empty()) memcpy(B + g_isc.at, it_sc.data(), 8 * it_sc.size());
     memcpy(B + g_gcs.at, gcs.data(), 4 * gcs.size());
+    if (!gitems.empty()) memcpy(B + g_git.at, gitems.data(), 8 * gitems.size());
+    H->n_g_items = (int)gitems.size();
     memcpy(B + g_ggo.at, ggo.data(), 8 * ggo.size());
     if (grid) {
         int64_t* rw = (int64_t*)(B + g_grw.at);

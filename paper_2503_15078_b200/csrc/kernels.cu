@@ -1975,6 +1975,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
 // ----------------------------------------------------------------------------
 constexpr int kGcrThreads = 256;
 
+
 __device__ __forceinline__ void block_sum3_gcr(double& a, double& b, double& c, double* red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     a = warp_sum(a); b = warp_sum(b); c = warp_sum(c);
@@ -2040,28 +2041,76 @@ __global__ void k_gcr_slot(int NS, Slots sl, CrContacts cc, const double* __rest
     W[3 * b + 2] = w2;
 }
 
-// q_a = sum_{b in group(a)} G[a][b] W_b: one warp per slot row (coalesced G row)
-__global__ void __launch_bounds__(256) k_gcr_gram(int NS, GcrData g) {
-    const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (a >= NS) return;
-    const float* row = g.G + g.rowoff[a];
-    const int b0 = g.gs0[a], n = g.gn[a];
-    const double* W = g.W + 3 * (size_t)b0;
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-    for (int b = lane; b < n; b += 32) {
-        const double gv = (double)__ldg(&row[b]);
-        d0 = fma(gv, W[3 * b], d0);
-        d1 = fma(gv, W[3 * b + 1], d1);
-        d2 = fma(gv, W[3 * b + 2], d2);
+// q_a = sum_{b in group(a)} G[a][b] W_b.  One CTA per (group, 32 consecutive rows): the
+// group's W is staged in shared memory (fp64 SoA); warp w owns rows w, w+8, w+16, w+24 and
+// streams the 4 G rows together (4 independent loads in flight per lane and step).
+// Groups wider than kGramSmemSlots fall back to one warp per row reading W from L1/L2.
+constexpr int kGramSmemSlots = 2000;   // 47 KB of fp64 W (static shared memory)
+
+__global__ void __launch_bounds__(256) k_gcr_gram(int NS, GcrData g, const int2* __restrict__ items) {
+    __shared__ double Ws[3 * kGramSmemSlots];
+    const int2 it = items[blockIdx.x];   // {first row (global slot), rows}
+    const int a0 = it.x, nrows = it.y;
+    const int b0 = g.gs0[a0], n = g.gn[a0];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool smem = n <= kGramSmemSlots;
+    if (smem) {
+        for (int b = threadIdx.x; b < n; b += blockDim.x) {
+            Ws[b] = g.W[3 * (size_t)(b0 + b)];
+            Ws[kGramSmemSlots + b] = g.W[3 * (size_t)(b0 + b) + 1];
+            Ws[2 * kGramSmemSlots + b] = g.W[3 * (size_t)(b0 + b) + 2];
+        }
+        __syncthreads();
+        const float* rows[4];
+        double acc[4][3];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int r = min(w + 8 * k, nrows - 1);
+            rows[k] = g.G + g.rowoff[a0 + r];
+            acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
+        }
+        for (int b = lane; b < n; b += 32) {
+            float gv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gv[k] = __ldcs(&rows[k][b]);
+            const double w0 = Ws[b], w1 = Ws[kGramSmemSlots + b], w2 = Ws[2 * kGramSmemSlots + b];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                acc[k][0] = fma((double)gv[k], w0, acc[k][0]);
+                acc[k][1] = fma((double)gv[k], w1, acc[k][1]);
+                acc[k][2] = fma((double)gv[k], w2, acc[k][2]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double d0 = warp_sum(acc[k][0]), d1 = warp_sum(acc[k][1]), d2 = warp_sum(acc[k][2]);
+            const int r = w + 8 * k;
+            if (lane == 0 && r < nrows) {
+                g.q[3 * (size_t)(a0 + r)] = d0;
+                g.q[3 * (size_t)(a0 + r) + 1] = d1;
+                g.q[3 * (size_t)(a0 + r) + 2] = d2;
+            }
+        }
+        return;
     }
-    d0 = warp_sum(d0);
-    d1 = warp_sum(d1);
-    d2 = warp_sum(d2);
-    if (lane == 0) {
-        g.q[3 * (size_t)a] = d0;
-        g.q[3 * (size_t)a + 1] = d1;
-        g.q[3 * (size_t)a + 2] = d2;
+    for (int r = w; r < nrows; r += 8) {
+        const float* row = g.G + g.rowoff[a0 + r];
+        const double* W = g.W + 3 * (size_t)b0;
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+        for (int b = lane; b < n; b += 32) {
+            const double gv = (double)__ldg(&row[b]);
+            d0 = fma(gv, W[3 * b], d0);
+            d1 = fma(gv, W[3 * b + 1], d1);
+            d2 = fma(gv, W[3 * b + 2], d2);
+        }
+        d0 = warp_sum(d0);
+        d1 = warp_sum(d1);
+        d2 = warp_sum(d2);
+        if (lane == 0) {
+            g.q[3 * (size_t)(a0 + r)] = d0;
+            g.q[3 * (size_t)(a0 + r) + 1] = d1;
+            g.q[3 * (size_t)(a0 + r) + 2] = d2;
+        }
     }
 }
 
@@ -2163,16 +2212,30 @@ __global__ void __launch_bounds__(kGcrThreads) k_gcr_update(GcrData g, int m, in
     }
 }
 
-// lambda += z / h^2 (reading A11), |r| -> cr_res
-__global__ void __launch_bounds__(1024) k_gcr_final(GcrData g, int m, double h, double* lam, double* cr_res) {
-    __shared__ double red[3 * 32 + 3];
+// lambda += z / h^2 (reading A11); |r| -> cr_res by the last CTA to finish (partials summed
+// in CTA order, so the value is deterministic)
+__global__ void __launch_bounds__(kGcrThreads) k_gcr_final(GcrData g, int m, double h, double* lam, double* cr_res) {
+    __shared__ double red[3 * (kGcrThreads / 32) + 3];
+    __shared__ bool last;
     double rr = 0.0, d1 = 0.0, d2 = 0.0;
-    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
         lam[j] += g.z[j] / (h * h);
         rr = fma(g.r[j], g.r[j], rr);
     }
     block_sum3_gcr(rr, d1, d2, red);
-    if (threadIdx.x == 0) cr_res[0] = sqrt(rr);
+    if (threadIdx.x == 0) {
+        g.part[3 * blockIdx.x] = rr;
+        __threadfence();
+        last = atomicAdd(g.cnt, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double t = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(&g.part[3 * b]);
+        cr_res[0] = sqrt(t);
+        *g.cnt = 0;
+    }
 }
 
 // D_jj = sum_{p,q} w_p w_q G[slot p][slot q] over pairs in the same Delassus group (reading A18)
@@ -2207,11 +2270,11 @@ int launch_gcr(cudaStream_t st, const Params& P, GcrData g, const DContact* c, C
     k_gcr_init<<<nb, kGcrThreads, 0, st>>>(P, g, c, cc, x, cs);
     for (int it = 0; it < P.cr_iters; ++it) {
         k_gcr_slot<<<(NS + 255) / 256, 256, 0, st>>>(NS, sl, cc, cs.theta, g.r, g.W);
-        k_gcr_gram<<<(NS + 7) / 8, 256, 0, st>>>(NS, g);
+        k_gcr_gram<<<g.n_gram_items, 256, 0, st>>>(NS, g, g.gram_items);
         k_gcr_row<<<nb, kGcrThreads, 0, st>>>(P, g, c, cs, it == 0);
         k_gcr_update<<<ub, kGcrThreads, 0, st>>>(g, m, it);
     }
-    k_gcr_final<<<1, 1024, 0, st>>>(g, m, P.h, cs.lam, cs.cr_res);
+    k_gcr_final<<<ub, kGcrThreads, 0, st>>>(g, m, P.h, cs.lam, cs.cr_res);
     k_gcr_slot<<<(NS + 255) / 256, 256, 0, st>>>(NS, sl, cc, cs.theta, g.z, cs.wz);
     return (int)cudaGetLastError();
 }
