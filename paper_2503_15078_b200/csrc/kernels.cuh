@@ -177,6 +177,9 @@ struct GcrData {
     double *W, *q;                 // [NS][3]
     double* part;                  // [row blocks][3] partial dot products
     double* sc;                    // [6] ping-pong CR scalars rAr, ApAp, stop
+    int* cnt;                      // [1] arrival counter of the final reduction (zero between launches)
+    const int2* gram_items;        // Gram matvec items {first slot row, rows <= 32} within one group
+    int n_gram_items;
     int nblk;
 };
 int gcr_row_blocks(int C);
