@@ -406,7 +406,8 @@ class Oracle:
     """
 
     def __init__(self, mesh, material, h: float, lg_iters: int = 5,
-                 cr_iters: Optional[int] = None, ncp: int = NCP_FB, precond: int = PRECOND_DELASSUS):
+                 cr_iters: Optional[int] = None, ncp: int = NCP_FB, precond: int = PRECOND_DELASSUS,
+                 admm: bool = False):
         self.X = np.asarray(mesh.X, dtype=np.float64)
         self.T = np.asarray(mesh.T, dtype=np.int64)
         self.fixed = np.asarray(mesh.fixed).astype(bool)
@@ -420,6 +421,9 @@ class Oracle:
         self.cr_iters = int(material.cr_iterations if cr_iters is None else cr_iters)
         self.ncp = int(ncp)            # FB (the paper's choice) or min-map (App. B.1)
         self.precond = int(precond)    # Delassus diagonal (eq. complementarity preconditioner) or mass inverse
+        # ADMM-PD (Overby et al. 2017; "our implementations are mainly based on PD and ADMM-PD",
+        # P:L1340): per-tet dual u, reset to 0 each frame (reading A33)
+        self.admm = bool(admm)
         self.Bm, self.vol, self.w, self.M = rest_data(self.X, self.T, material.density, self.k)
         self.A = assemble_Av(self.n_v, self.T, self.Bm, self.w, self.M, self.h)
         self.free = np.nonzero(~self.fixed)[0]
@@ -557,11 +561,20 @@ class Oracle:
         lam = np.zeros(self.m)                         # lambda^0 = 0 (A10)
         F_ = self.free
         info = {"iters": [], "lam": None}
+        u = np.zeros((self.T.shape[0], 3, 3))          # ADMM dual (reading A33)
         for it in range(self.lg_iters):
             F = deformation_gradients(x, self.T, self.Bm)
-            P = project(F, self.model, self.k, self.mu, self.lam)
+            if self.admm:
+                # ADMM-PD: z = argmin psi(z) + w/2 |F + u - z|^2; u <- u + F - z;
+                # the global step targets z - u (Overby et al. 2017, Alg. 1)
+                P = project(F + u, self.model, self.k, self.mu, self.lam)
+                u = u + F - P
+                target = P - u
+            else:
+                P = project(F, self.model, self.k, self.mu, self.lam)
+                target = P
             # b = M s + h^2 sum w G^T p - A_fc x_c  (A7)
-            b = self.M[:, None] * s + gt_p(P, self.Bm, self.w, h, self.T, self.n_v)
+            b = self.M[:, None] * s + gt_p(target, self.Bm, self.w, h, self.T, self.n_v)
             b_f = b[F_]
             if self.pinned.size:
                 b_f = b_f - self.A_fc @ x[self.pinned]

@@ -499,3 +499,65 @@ def test_minmap_contact_statics():
     assert np.all(np.abs(lam[:, 1:].sum(0)) < 1e-9 * mg)
     assert np.all(np.linalg.norm(lam[:, 1:], axis=1) <= 0.5 * lam[:, 0] + 1e-12)
     assert np.max(np.abs(v)) < 1e-9
+
+
+# ------------------------------------------------------------- ADMM-PD (NEXT row 2)
+def _psi_nh(F, mu, lam):
+    """Compressible Neo-Hookean energy density (reading A3)."""
+    J = np.linalg.det(F)
+    return 0.5 * mu * (np.sum(F * F) - 3.0) - mu * np.log(J) + 0.5 * lam * np.log(J) ** 2
+
+
+def _psi_corot(F, mu, lam):
+    """Linear corotational energy density (reading A2), R = polar rotation of F."""
+    U, _, Vt = np.linalg.svd(F)
+    R = U @ Vt
+    if np.linalg.det(R) < 0:
+        U[:, -1] *= -1
+        R = U @ Vt
+    return mu * np.sum((F - R) ** 2) + 0.5 * lam * np.trace(R.T @ F - np.eye(3)) ** 2
+
+
+def _implicit_euler_gradient(o, x, s, psi):
+    """h^2 * grad of E(x) = 1/(2h^2) |x - s|_M^2 + sum_i vol_i psi(F_i(x))  (eq. implicit
+    euler) at the free vertices; dpsi/dF by central differences, written out
+    per tet from Dm and Ds (no oracle helper)."""
+    r = o.M[:, None] * (x - s)
+    for t in range(o.T.shape[0]):
+        v = o.T[t]
+        Dm = np.stack([o.X[v[i]] - o.X[v[0]] for i in (1, 2, 3)], 1)
+        Bm = np.linalg.inv(Dm)
+        F = np.stack([x[v[i]] - x[v[0]] for i in (1, 2, 3)], 1) @ Bm
+        vol = abs(np.linalg.det(Dm)) / 6.0
+        P = np.zeros((3, 3))
+        e = 1e-6
+        for i in range(3):
+            for j in range(3):
+                Fp, Fm = F.copy(), F.copy()
+                Fp[i, j] += e
+                Fm[i, j] -= e
+                P[i, j] = (psi(Fp) - psi(Fm)) / (2 * e)
+        g = vol * P @ Bm.T
+        for a in range(3):
+            r[v[a + 1]] += o.h ** 2 * g[:, a]
+        r[v[0]] -= o.h ** 2 * g.sum(1)
+    return r[o.free]
+
+
+@pytest.mark.parametrize("model,psi", [(O.NEOHOOKEAN, _psi_nh), (O.COROTATED, _psi_corot)])
+def test_admm_pd_fixed_point_is_implicit_euler(model, psi):
+    """ADMM-PD (Overby et al. 2017): at its fixed point z = F and u = grad psi / k,
+    so the global step is the stationarity condition M (x - s) + h^2 sum vol G^T dpsi/dF = 0
+    of the implicit-Euler objective -- which plain PD without the dual misses (reading A32,
+    the Moreau-envelope bias).  Cantilever (cfg1), one frame from rest, 60 L-G iterations."""
+    sc = scenes.make_scene("cfg1", model=model)
+    res = {}
+    for admm in (False, True):
+        o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=60, admm=admm)
+        x0, v0 = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+        s = x0 + sc.h * v0 + sc.h ** 2 * o.g
+        x, _, _ = o.frame(x0, v0)
+        scale = np.abs(o.M[:, None] * (x - s))[o.free].max()
+        res[admm] = np.abs(_implicit_euler_gradient(o, x, s, lambda F: psi(F, o.mu, o.lam))).max() / scale
+    assert res[True] < 1e-5, res
+    assert res[False] > 100 * res[True], res
