@@ -205,6 +205,15 @@ int sim_set_cr_mode(sim_handle *h, int32_t mode);
  * r = h^2 / h [J M^-1 J^T]_jj with the lumped M.  Defaults 0, 0;
  * SIM_E_INVALID on other values.  Takes effect at the next step. */
 int sim_set_ncp(sim_handle *h, int32_t ncp_function, int32_t preconditioner);
+
+/* Local-global variant: 0 = projective dynamics (Alg. 1/4; default),
+ * 1 = ADMM-PD (Overby et al. 2017, which the paper's implementation is based on,
+ * P:L1052 / P:L1340): per-tet dual u (9 floats per tet and instance, allocated
+ * here, reset to 0 at every frame), local step on F + u, u <- u + F - p, global
+ * step on p - u.  Its fixed point is the implicit-Euler solution (plain PD's
+ * is the Moreau-envelope one).  Needs a built handle (SIM_E_STATE otherwise);
+ * SIM_E_OOM if the dual cannot be allocated.  Takes effect at the next step. */
+int sim_set_admm(sim_handle *h, int32_t on);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 
 void sim_destroy(sim_handle *h);         /* NULL-safe */

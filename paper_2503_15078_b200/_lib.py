@@ -17,7 +17,7 @@ EXPORTED_SYMBOLS = [
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
-    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp",
+    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -114,6 +114,7 @@ def _load():
         "sim_set_profiling": [H, C.c_int],
         "sim_set_cr_mode": [H, C.c_int32],
         "sim_set_ncp": [H, C.c_int32, C.c_int32],
+        "sim_set_admm": [H, C.c_int32],
         "sim_get_kernel_times": [H, dp, C.c_int32],
         "sim_debug_contact_state": [H, C.c_int32, dp, dp, dp, dp, ip, dp],
         "sim_debug_cr_timeline": [H, dp],
@@ -297,6 +298,10 @@ class Sim:
     def set_ncp(self, ncp: int = 0, precond: int = 0):
         """NCP function 0 FB / 1 min-map; preconditioner 0 Delassus / 1 mass inverse (sim_set_ncp)."""
         _check(lib.sim_set_ncp(self._h, int(ncp), int(precond)))
+
+    def set_admm(self, on: bool = True):
+        """ADMM-PD local-global variant (sim_set_admm)."""
+        _check(lib.sim_set_admm(self._h, 1 if on else 0))
 
     def set_profiling(self, on: bool):
         _check(lib.sim_set_profiling(self._h, 1 if on else 0))

@@ -183,6 +183,8 @@ struct sim_handle {
     // grid CR (large contact sets of one scene): Delassus groups = etree components
     int cr_mode = 0;                 // 0 auto, 1 cluster CR only, 2 grid CR always
     int ncp = 0, precond = 0;        // NCP function / complementarity preconditioner (sim_set_ncp)
+    int admm = 0;                    // ADMM-PD local-global (sim_set_admm)
+    DBuf<float> du;                  // ADMM dual, [9][n_t S]
     bool grid = false;               // the committed contact set uses the grid CR
     int NG = 0, ng_max = 0;
     std::vector<int32_t> comp_root;  // [n_f] root of each free vertex's etree component
@@ -1063,7 +1065,8 @@ static int enqueue_frame(sim_handle* H, int iters) {
             if (!H->grid) { MARK(KK_ACTIVE); launch_active(st, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += 2; }
         }
         MARK(KK_LOCAL);
-        launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, H->x.p, H->fc.p, nullptr); nk++;
+        launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, H->x.p, H->fc.p, nullptr, H->admm ? H->du.p : nullptr,
+                     k == 0); nk++;
         if (fork) CKR(cudaStreamWaitEvent(st, H->join_ev, 0));
         MARK(KK_GATHER);
         launch_gather(st, P, H->adjp.p, H->adj.p, H->fc.p, H->M.p, H->x.p, H->s.p, con ? H->slotmap.p : nullptr, sl,
@@ -1104,6 +1107,15 @@ extern "C" int sim_set_ncp(sim_handle* H, int32_t ncp_function, int32_t precondi
     H->ncp = ncp_function;
     H->precond = preconditioner;
     return SIM_OK;   // Params are captured: the graph key includes both
+}
+
+extern "C" int sim_set_admm(sim_handle* H, int32_t on) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (on != 0 && on != 1) return fail(SIM_E_INVALID, "ADMM flag must be 0 or 1");
+    if (on && H->state == 1 && !H->host_only && !H->du.p) CK(H->du.alloc((size_t)9 * H->n_t * H->S));
+    if (on && H->state != 1) return fail(SIM_E_STATE, "build the sparse inverse first");
+    H->admm = on;
+    return SIM_OK;
 }
 
 extern "C" int sim_set_cr_mode(sim_handle* H, int32_t mode) {
@@ -1149,7 +1161,7 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     if (rc) return rc;
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
                                       H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG,
-                                      H->ncp, H->precond};
+                                      H->ncp, H->precond, H->admm};
     if (!H->gexec || key != H->gkey) {
         if (H->gexec) {
             cudaGraphExecDestroy(H->gexec);

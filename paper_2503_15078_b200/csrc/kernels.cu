@@ -217,9 +217,13 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
 
 // one thread per (tet, instance), instance-minor: the instances of one tet share its rest
 // data (broadcast loads) and read consecutive state entries.  f_a = h^2 w (P - F) g_a per corner
+// ADMM-PD (du != nullptr; Overby et al. 2017): project F + u, u <- u + F - P = -(P - F - u),
+// and the global step targets P - u_new, i.e. the force block is h^2 w (2 (P - F - u) + u) g_a.
+// du is [9][n_t S] (plane per entry, instance-minor); admm_first: u = 0 (reading A33, reset per frame).
 __global__ void __launch_bounds__(128) k_local(Params P, const int4* __restrict__ tet, const float* __restrict__ Bm,
                                                const float* __restrict__ hw2, const double4* __restrict__ x,
-                                               float4* __restrict__ fc, float* __restrict__ Pdbg) {
+                                               float4* __restrict__ fc, float* __restrict__ Pdbg,
+                                               float* __restrict__ du, int admm_first) {
     const int SI = P.S;
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
     if (gt >= P.n_t * SI) return;
@@ -240,6 +244,16 @@ __global__ void __launch_bounds__(128) k_local(Params P, const int4* __restrict_
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j) F[i][j] = D[i][0] * B[0 * 3 + j] + D[i][1] * B[1 * 3 + j] + D[i][2] * B[2 * 3 + j];
+    float uo[9];
+    const size_t plane = (size_t)nt * SI;
+    if (du) {
+#pragma unroll
+        for (int e = 0; e < 9; ++e) uo[e] = admm_first ? 0.f : du[e * plane + gt];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) F[i][j] += uo[3 * i + j];   // project F + u
+    }
     // S = F^T F, eigenvectors V
     float S[3][3];
 #pragma unroll
@@ -298,14 +312,27 @@ __global__ void __launch_bounds__(128) k_local(Params P, const int4* __restrict_
     for (int j = 0; j < 3; ++j) sg[j] = U[0][j] * FV[0][j] + U[1][j] * FV[1][j] + U[2][j] * FV[2][j];
     float dlt[3];
     project_sigma(P.model, sg, P.k, P.mu, P.lam, dlt);
-    // Q = hw2 * U diag(delta) V^T  (= h^2 w (P - F))
+    // Q = hw2 * U diag(delta) V^T  (= h^2 w (P - F); ADMM: h^2 w (2 (P - F - u) + u))
     float hw = __ldg(&hw2[t]);
     float Q[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            Q[i][j] = hw * (U[i][0] * dlt[0] * V[j][0] + U[i][1] * dlt[1] * V[j][1] + U[i][2] * dlt[2] * V[j][2]);
+            Q[i][j] = U[i][0] * dlt[0] * V[j][0] + U[i][1] * dlt[1] * V[j][1] + U[i][2] * dlt[2] * V[j][2];
+    if (du) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                du[(3 * i + j) * plane + gt] = -Q[i][j];   // u_new = u + F - P = -(P - F - u)
+                Q[i][j] = 2.f * Q[i][j] + uo[3 * i + j];
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Q[i][j] *= hw;
     if (Pdbg) {
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -328,8 +355,8 @@ __global__ void __launch_bounds__(128) k_local(Params P, const int4* __restrict_
 }
 
 void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
-                  const double4* x, float4* fc, float* Pdbg) {
-    k_local<<<(P.n_t * P.S + 127) / 128, 128, 0, st>>>(P, tet, Bm, hw2, x, fc, Pdbg);
+                  const double4* x, float4* fc, float* Pdbg, float* du, int admm_first) {
+    k_local<<<(P.n_t * P.S + 127) / 128, 128, 0, st>>>(P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
 }
 
 // ----------------------------------------------------------------------------

@@ -115,8 +115,9 @@ struct Slots {
 void launch_replicate(cudaStream_t st, const double4* src, double4* dst, int n, int S);
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
                     double* lam, int nlam);
+// du: ADMM-PD dual [9][n_t S] or nullptr (plain PD); admm_first: treat u as 0 (first iteration of a frame)
 void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
-                  const double4* x, float4* fc, float* Pdbg);
+                  const double4* x, float4* fc, float* Pdbg, float* du = nullptr, int admm_first = 0);
 void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, const double4* x,
                          const double4* xt, ContactState cs);
 // slotmap[a * S + i] = global slot of vertex a in instance i, or -1
