@@ -214,6 +214,11 @@ int sim_set_ncp(sim_handle *h, int32_t ncp_function, int32_t preconditioner);
  * is the Moreau-envelope one).  Needs a built handle (SIM_E_STATE otherwise);
  * SIM_E_OOM if the dual cannot be allocated.  Takes effect at the next step. */
 int sim_set_admm(sim_handle *h, int32_t on);
+
+/* Batched K-passes (n_instances > 1): 0 = tcgen05 tensor cores (kind::tf32, 3xTF32 split,
+ * TMEM accumulators; default), 1 = CUDA-core FP32 FMAs.  Same K and operands; results agree
+ * to fp32 rounding.  n_instances == 1 always uses the HBM-streaming SpMV kernels. */
+int sim_set_kpass_mode(sim_handle *h, int32_t mode);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 
 void sim_destroy(sim_handle *h);         /* NULL-safe */

@@ -17,7 +17,7 @@ EXPORTED_SYMBOLS = [
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
-    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm",
+    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -115,6 +115,7 @@ def _load():
         "sim_set_cr_mode": [H, C.c_int32],
         "sim_set_ncp": [H, C.c_int32, C.c_int32],
         "sim_set_admm": [H, C.c_int32],
+        "sim_set_kpass_mode": [H, C.c_int32],
         "sim_get_kernel_times": [H, dp, C.c_int32],
         "sim_debug_contact_state": [H, C.c_int32, dp, dp, dp, dp, ip, dp],
         "sim_debug_cr_timeline": [H, dp],
@@ -302,6 +303,10 @@ class Sim:
     def set_admm(self, on: bool = True):
         """ADMM-PD local-global variant (sim_set_admm)."""
         _check(lib.sim_set_admm(self._h, 1 if on else 0))
+
+    def set_kpass_mode(self, mode: int):
+        """Batched K-passes: 0 tensor cores (tcgen05), 1 CUDA-core FP32 (sim_set_kpass_mode)."""
+        _check(lib.sim_set_kpass_mode(self._h, int(mode)))
 
     def set_profiling(self, on: bool):
         _check(lib.sim_set_profiling(self._h, 1 if on else 0))

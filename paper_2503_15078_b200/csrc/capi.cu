@@ -125,6 +125,9 @@ struct sim_handle {
     DBuf<int32_t> adjp, adj;
     // device: K
     DBuf<float> Krow, Kcol, T1, T2, T1p;   // K row/column-major + the passes' tile streams
+    DBuf<float> T1tc, T2tc;                // tensor-core copies of T1p / T2 (S > 1)
+    int kpass_mode = 0;                    // S > 1: 0 tensor cores (tcgen05), 1 CUDA-core FP32
+    int tc_drain = 4;                      // tensor-core K-pass: tiles per fp32 TMEM accumulation (2.4e-6 rel. on cfg3)
     DBuf<int64_t> colptr;
     DBuf<int32_t> depth, parent, ptop, cover;
     DBuf<int2> meta;                 // {rowptr[i] - first[i], first[i]}
@@ -401,6 +404,15 @@ static int upload_all(sim_handle* H) {
         CK(cudaMemsetAsync(H->counters.p, 0, ncnt * sizeof(int), st));
     } else {
         CK(H->T1p.alloc(H->T1ph.size())); CK(H->T1p.upload(H->T1ph.data(), H->T1ph.size(), st));
+        {
+            std::vector<float> tc;
+            simhost::tc_tiles(H->T1ph, tc);
+            CK(H->T1tc.alloc(tc.size())); CK(H->T1tc.upload(tc.data(), tc.size(), st));
+            CK(cudaStreamSynchronize(st));
+            simhost::tc_tiles(H->T2h, tc);
+            CK(H->T2tc.alloc(tc.size())); CK(H->T2tc.upload(tc.data(), tc.size(), st));
+            CK(cudaStreamSynchronize(st));
+        }
         CK(H->bu1d.alloc(H->bu1.size())); CK(H->bu1d.upload(H->bu1.data(), H->bu1.size(), st));
         CK(H->bu2d.alloc(H->bu2.size())); CK(H->bu2d.upload(H->bu2.data(), H->bu2.size(), st));
         CK(H->part1.alloc((size_t)std::max(1, H->bparts) * 3 * 32 * S));
@@ -1007,6 +1019,9 @@ static void enqueue_kpass1(sim_handle* H, cudaStream_t st) {
     if (H->S == 1)
         launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->T1.p, H->u.p, H->y.p, H->part1.p,
                       H->counters.p);
+    else if (H->kpass_mode == 0)
+        launch_kpass1_tc(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1tc.p, H->u.p, H->y.p, H->part1.p,
+                         H->counters.p, H->tc_drain);
     else
         launch_kpass1_batched(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1p.p, H->u.p, H->y.p,
                               H->part1.p, H->counters.p);
@@ -1015,6 +1030,9 @@ static void enqueue_kpass2(sim_handle* H, cudaStream_t st, double4* x, const dou
                            int fin) {
     if (H->S == 1)
         launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->T2.p, H->y.p, x, xt, v, inv_h, fin);
+    else if (H->kpass_mode == 0)
+        launch_kpass2_tc(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2tc.p, H->y.p, x, xt, v,
+                         inv_h, fin, H->tc_drain);
     else
         launch_kpass2_batched(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2.p, H->y.p, x, xt,
                               v, inv_h, fin);
@@ -1118,6 +1136,19 @@ extern "C" int sim_set_admm(sim_handle* H, int32_t on) {
     return SIM_OK;
 }
 
+extern "C" int sim_set_kpass_mode(sim_handle* H, int32_t mode) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    // mode 0 | 1; mode >= 16: tensor cores with (mode >> 4) tiles per fp32 TMEM accumulation (tuning)
+    if (mode >= 16) {
+        H->kpass_mode = 0;
+        H->tc_drain = std::max(1, mode >> 4);
+        return SIM_OK;
+    }
+    if (mode != 0 && mode != 1) return fail(SIM_E_INVALID, "K-pass mode must be 0 (tensor cores) or 1 (FP32)");
+    H->kpass_mode = mode;
+    return SIM_OK;
+}
+
 extern "C" int sim_set_cr_mode(sim_handle* H, int32_t mode) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (mode < 0 || mode > 2) return fail(SIM_E_INVALID, "CR mode must be 0 (auto), 1 (cluster) or 2 (grid)");
@@ -1161,7 +1192,7 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     if (rc) return rc;
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
                                       H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG,
-                                      H->ncp, H->precond, H->admm};
+                                      H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain};
     if (!H->gexec || key != H->gkey) {
         if (H->gexec) {
             cudaGraphExecDestroy(H->gexec);

@@ -549,4 +549,31 @@ int build_batched(const Inverse& K, const WorkLists& wl, int unit_tiles, std::ve
     return nparts;
 }
 
+void tc_tiles(const std::vector<float>& T, std::vector<float>& Ttc) {
+    const size_t nt = T.size() / 1024;
+    Ttc.assign(2048 * nt, 0.f);
+#pragma omp parallel for schedule(static)
+    for (long long t = 0; t < (long long)nt; ++t) {
+        const float* src = T.data() + 1024 * (size_t)t;
+        float* hi = Ttc.data() + 2048 * (size_t)t;
+        float* lo = hi + 1024;
+        for (int q = 0; q < 32; ++q)
+            for (int l = 0; l < 32; ++l) {
+                const float v = src[q * 32 + l];
+                auto rn = [](float a) {   // round to nearest tf32
+                    uint32_t b;
+                    std::memcpy(&b, &a, 4);
+                    b = (b + 0x1000u) & 0xFFFFE000u;
+                    float r;
+                    std::memcpy(&r, &b, 4);
+                    return r;
+                };
+                const float h = rn(v);
+                const int d = (l / 8) * 256 + (q / 4) * 32 + (l % 8) * 4 + (q % 4);
+                hi[d] = h;
+                lo[d] = rn(v - h);
+            }
+    }
+}
+
 }  // namespace simhost

@@ -110,4 +110,10 @@ struct BUnit { int32_t r0, nr, c0, ntiles, list0, nlist, block, part, nparts, pa
 int build_batched(const Inverse& K, const WorkLists& wl, int unit_tiles, std::vector<BUnit>& u1,
                   std::vector<float>& T1p, std::vector<BUnit>& u2, int& nblocks1);
 
+// Tensor-core copy of a tile stream (1024-float tiles, tile[q * 32 + l], q = reduction index,
+// l = output): per tile 2048 floats = the tf32 "hi" tile then the "lo" tile (v - hi), both
+// rounded to nearest tf32, each in the tcgen05 SWIZZLE_NONE K-major core-matrix layout
+// [l / 8][q / 4][l % 8][q % 4].
+void tc_tiles(const std::vector<float>& T, std::vector<float>& Ttc);
+
 }  // namespace simhost

@@ -1050,6 +1050,296 @@ void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
 }
 
 // ----------------------------------------------------------------------------
+// Batched K-passes on the 5th-generation tensor cores (tcgen05.mma kind::tf32, accumulators
+// in TMEM).  With S instances sharing K each 32 x 32 K tile multiplies a 32 x 128 block of
+// right-hand sides per component, a dense contraction: D_c[inst][out] += sum_q V_c[inst][q]
+// K[q][out] is one M = 128 (instances) x N = 32 (outputs) x K = 32 (reduction) MMA per tile
+// and component.  Near-fp32 accuracy from the 3xTF32 split (a = a_hi + a_lo, both rounded to
+// nearest tf32, |a - a_hi - a_lo| <= 2^-22 |a|): D += V_hi K_hi + V_lo K_hi + V_hi K_lo (the
+// dropped V_lo K_lo is <= 2^-22 relative); the TMEM accumulators (fp32) are folded into fp64
+// registers every `drain` tiles and restarted, units combined in fp64 as in k_kpass_b.
+//   operands in shared memory, SWIZZLE_NONE K-major canonical layout: core matrix = 8 rows
+//   x 16 B (4 tf32 along K); LBO = 128 B between K chunks, SBO = 1024 B between 8-row groups.
+//   A (vectors, 128 x 32 per component, hi and lo): written by all 256 threads from the
+//   gathered rows (float4 loads, coalesced over instances); B (K tile hi / lo, 4 KB each):
+//   pre-laid out on the host, one 8 KB bulk copy per tile.  Two stages: while the tensor
+//   core runs tile t the threads stage tile t + 1; tcgen05.commit frees a stage.
+//   thread 0 issues the 36 MMAs per tile (3 components x 4 K-steps x 3 products).
+//   epilogue: warp w reads TMEM lanes 32 (w % 4) .. (instances) and columns 16 (w / 4) ..
+//   (outputs) of every component with tcgen05.ld.32x32b.x16.
+// ----------------------------------------------------------------------------
+constexpr int kTcInst = 128;
+constexpr uint32_t kTcAplane = kTcInst * 32 * 4;                  // 16 KB
+constexpr uint32_t kTcStage = 6 * kTcAplane + 2 * 4096;           // 104 KB
+constexpr size_t kTcSmem = 2 * (size_t)kTcStage + 128;
+constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ uint64_t umma_desc_k(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128u >> 4) << 16) | ((uint64_t)(1024u >> 4) << 32) |
+           ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t dt, uint64_t da, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+        "l"(da), "l"(db), "r"(kIdescTf32), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+// round-to-nearest to tf32 (10 explicit mantissa bits): the split v = hi + lo with both parts
+// exactly representable in tf32 up to 2^-22 |v| (the tensor core ignores the low 13 bits)
+__device__ __forceinline__ float tf32_rn(float v) {
+    return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(256, 1)
+    k_kpass_tc(int S, int n_f, const BUnit* __restrict__ units, const float* __restrict__ Ttc,
+               const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
+               double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
+               const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
+    extern __shared__ unsigned char tsm_raw[];
+    __shared__ __align__(8) uint64_t bfull[2], mdone[2];
+    __shared__ uint32_t tmem_base_s;
+    __shared__ int s_last;
+    unsigned char* tsm = tsm_raw + ((128u - ((unsigned)__cvta_generic_to_shared(tsm_raw) & 127u)) & 127u);
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const BUnit U = units[blockIdx.x];
+    const int chunk = blockIdx.y;
+    const int i0 = chunk * kTcInst;
+    const int ni = min(kTcInst, S - i0);
+    const unsigned long long pol = l2_evict_first();
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&tmem_base_s)),
+                     "r"(128u)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bfull[0], 1);
+        mbar_init(&bfull[1], 1);
+        mbar_init(&mdone[0], 1);
+        mbar_init(&mdone[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = tmem_base_s;
+    auto aplane = [&](int st, int c, int hl) { return tsm + st * kTcStage + (2 * c + hl) * kTcAplane; };
+    auto bplane = [&](int st, int hl) { return tsm + st * kTcStage + 6 * kTcAplane + hl * 4096; };
+    auto issueB = [&](int t) {
+        const int st = t & 1;
+        mbar_expect_tx(&bfull[st], 8192u);
+        bulk_g2s(bplane(st, 0), Ttc + 2 * U.toff + (int64_t)t * 2048, 8192u, &bfull[st], true, pol);
+    };
+    if (tid == 0) {
+        issueB(0);
+        if (U.ntiles > 1) issueB(1);
+    }
+    const int il = tid & (kTcInst - 1), jb = tid >> 7;   // producer: instance, first K chunk
+    const bool ilive = il < ni;
+    const uint32_t aoff = (uint32_t)((il >> 3) * 1024 + (il & 7) * 16);
+    // epilogue mapping: warp w owns TMEM lanes 32 (w % 4) .. and output columns 16 (w / 4) ..
+    const int q4 = w & 3, half = w >> 2;
+    double dacc[3][16];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) dacc[c][e] = 0.0;
+    // fold the TMEM accumulators (fp32 over <= drain tiles) into fp64 registers
+    auto fold = [&]() {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const uint32_t ta = tmem + ((uint32_t)(32 * q4) << 16) + 32u * c + 16u * half;
+            uint32_t r[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                "%14, %15}, [%16];\n"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15])
+                : "r"(ta));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+            for (int e = 0; e < 16; ++e) dacc[c][e] += (double)__uint_as_float(r[e]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    };
+    for (int t = 0; t < U.ntiles; ++t) {
+        const int st = t & 1;
+        if (t > 0 && t % drain == 0) {   // accumulators complete up to tile t - 1: fold, restart
+            mbar_wait(&mdone[(t - 1) & 1], ((t - 1) >> 1) & 1);
+            fold();
+        }
+        if (t >= 2) {
+            mbar_wait(&mdone[st], ((t - 2) >> 1) & 1);   // the tensor core is done with stage st
+            if (tid == 0) issueB(t);
+        }
+        const int nv = PASS == 1 ? max(0, min(32, n_f - (U.c0 + 32 * t))) : min(32, U.nlist - 32 * t);
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+            const int j = jb + 2 * it;
+            float4 r[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int q = 4 * j + e;
+                r[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (ilive && q < nv) {
+                    const int idx = PASS == 1 ? U.c0 + 32 * t + q : __ldg(&cover[U.list0 + 32 * t + q]);
+                    r[e] = __ldg(&vin[(size_t)idx * S + i0 + il]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                float a[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) a[e] = c == 0 ? r[e].x : (c == 1 ? r[e].y : r[e].z);
+                float4 hi, lo;
+                hi.x = tf32_rn(a[0]); hi.y = tf32_rn(a[1]); hi.z = tf32_rn(a[2]); hi.w = tf32_rn(a[3]);
+                lo.x = tf32_rn(a[0] - hi.x); lo.y = tf32_rn(a[1] - hi.y);
+                lo.z = tf32_rn(a[2] - hi.z); lo.w = tf32_rn(a[3] - hi.w);
+                *reinterpret_cast<float4*>(aplane(st, c, 0) + aoff + j * 128) = hi;
+                *reinterpret_cast<float4*>(aplane(st, c, 1) + aoff + j * 128) = lo;
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> tensor core
+        __syncthreads();
+        if (tid == 0) {
+            mbar_wait(&bfull[st], (t >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint32_t b0 = (unsigned)__cvta_generic_to_shared(bplane(st, 0));
+            const uint32_t b1 = (unsigned)__cvta_generic_to_shared(bplane(st, 1));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const uint32_t a0 = (unsigned)__cvta_generic_to_shared(aplane(st, c, 0));
+                const uint32_t a1 = (unsigned)__cvta_generic_to_shared(aplane(st, c, 1));
+                const uint32_t dt = tmem + 32u * c;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t o = 256u * kk;
+                    umma_tf32(dt, umma_desc_k(a0 + o), umma_desc_k(b0 + o), (t % drain != 0 || kk > 0) ? 1u : 0u);
+                    umma_tf32(dt, umma_desc_k(a1 + o), umma_desc_k(b0 + o), 1u);
+                    umma_tf32(dt, umma_desc_k(a0 + o), umma_desc_k(b1 + o), 1u);
+                }
+            }
+            umma_commit(&mdone[st]);
+        }
+    }
+    {
+        const int last = U.ntiles - 1;
+        if (last >= 0) {
+            mbar_wait(&mdone[last & 1], (last >> 1) & 1);
+            fold();
+        }
+    }
+    __syncthreads();
+    if (w == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(128u) : "memory");
+    const int li = 32 * q4 + lane;
+    const bool live = li < ni;
+    const int inst = i0 + li;
+    if (PASS == 2) {
+        if (!live) return;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int l = 16 * half + r;
+            if (l < U.nr) {
+                const size_t jx = (size_t)(U.c0 + l) * S + inst;
+                double4 xj = x[jx];
+                xj.x += dacc[0][r];
+                xj.y += dacc[1][r];
+                xj.z += dacc[2][r];
+                x[jx] = xj;
+                if (finalize_v) {   // v = (x - x_t) / h
+                    const double4 t0 = xt[jx];
+                    v[jx] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
+                }
+            }
+        }
+        return;
+    }
+    if (U.nparts == 1) {
+        if (!live) return;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int l = 16 * half + r;
+            if (l < U.nr)
+                yout[(size_t)(U.r0 + l) * S + inst] =
+                    make_float4((float)dacc[0][r], (float)dacc[1][r], (float)dacc[2][r], 0.f);
+        }
+        return;
+    }
+    // block split over several units: fp64 partials, combined in fixed order by the last unit
+    const size_t pstride = (size_t)32 * S;
+    if (live) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int l = 16 * half + r;
+            double* pp = part + (size_t)U.part * 3 * pstride + (size_t)l * S + inst;
+            pp[0] = dacc[0][r];
+            pp[pstride] = dacc[1][r];
+            pp[2 * pstride] = dacc[2][r];
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int old = atomicAdd(&counters[U.block * nchunks + chunk], 1);
+        s_last = old == U.nparts - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (live) {
+        for (int r = 0; r < 16; ++r) {
+            const int l = 16 * half + r;
+            if (l >= U.nr) continue;
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            for (int q = 0; q < U.nparts; ++q) {
+                const double* pq = part + (size_t)(U.list0 + q) * 3 * pstride + (size_t)l * S + inst;
+                t0 += __ldcg(pq);
+                t1 += __ldcg(pq + pstride);
+                t2 += __ldcg(pq + 2 * pstride);
+            }
+            yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
+        }
+    }
+    if (threadIdx.x == 0) counters[U.block * nchunks + chunk] = 0;
+}
+
+void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
+                      const float4* u, float4* y, double* part, int* counters, int drain) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_kpass_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+        attr = true;
+    }
+    const int nch = (S + kTcInst - 1) / kTcInst;
+    k_kpass_tc<1><<<dim3(nunits, nch), 256, kTcSmem, st>>>(S, n_f, units, T1tc, nullptr, u, y, part, counters, nch,
+                                                           nullptr, nullptr, nullptr, 0.0, 0, drain);
+}
+
+void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
+                      const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
+                      int finalize_v, int drain) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_kpass_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+        attr = true;
+    }
+    const int nch = (S + kTcInst - 1) / kTcInst;
+    k_kpass_tc<2><<<dim3(nunits, nch), 256, kTcSmem, st>>>(S, n_f, units, T2tc, cover, y, nullptr, nullptr, nullptr,
+                                                           nch, x, xt, v, inv_h, finalize_v, drain);
+}
+
+// ----------------------------------------------------------------------------
 // chain dot: dxt_s = (K^T y)_{a_s} = sum_k Kcol[colptr_a + k] y[chain_rows[off + k]]
 // (column a of K is contiguous in Kcol; its rows are a's ancestor chain).  One CTA per
 // (class slot, up to 32 instances of the class): the chain is read once for the group.

@@ -135,6 +135,13 @@ void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
 void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
                            const float* T2, const float4* y, double4* x, const double4* xt, double4* v,
                            double inv_h, int finalize_v);
+// the same on the tensor cores (tcgen05 kind::tf32, 3xTF32): tile streams re-laid out by
+// simhost::tc_tiles (hi and lo tiles in the K-major core-matrix layout, 2048 floats per tile)
+void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
+                      const float4* u, float4* y, double* part, int* counters, int drain);
+void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
+                      const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
+                      int finalize_v, int drain);   // drain: tiles accumulated in TMEM (fp32) per fp64 fold
 // grouped: one work item per (class slot, 32 class members); items int2 {class slot, member0}
 void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
                       const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows, const float4* y,

@@ -183,3 +183,24 @@ def test_instance_validation(simmod):
         s.set_contacts([], instance=2)
     with pytest.raises(simmod.SimError, match="instance"):
         s.get_state(instance=-1)
+
+
+def test_tensor_core_and_fp32_kpasses_agree(simmod):
+    """The tcgen05 (kind::tf32, 3xTF32, TMEM) batched K-passes and the CUDA-core FP32 ones
+    (include/sim.h sim_set_kpass_mode) on the same right-hand sides: both match the oracle's
+    A^-1 b within 1e-5 relative, and agree with each other to fp32 rounding."""
+    sc = scenes.make_scene("block", nv=7, split="kuhn6")
+    S = 130
+    s = make(simmod, sc, S)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    rng = np.random.default_rng(9)
+    b = rng.standard_normal((S, sc.mesh.n_v, 3)).astype(np.float32).astype(np.float64)
+    out = {}
+    for mode in (0, 1):
+        s.set_kpass_mode(mode)
+        out[mode] = s.debug_apply_inverse(b)
+    for i in (0, 63, 127, 128, 129):
+        xr = o.solve(b[i][o.free])
+        for mode in (0, 1):
+            assert np.abs(out[mode][i][o.free] - xr).max() < 1e-5 * np.abs(xr).max(), (mode, i)
+    assert np.abs(out[0] - out[1]).max() < 1e-5 * np.abs(out[1]).max()
