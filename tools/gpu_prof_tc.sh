@@ -1,0 +1,9 @@
+#!/bin/bash
+# ncu of the cfg5 bench kernels at S = 1024: --set full of k_local / k_kpass_tc and FP32 op counts of k_local
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_local|k_kpass_tc" -s 3 -c 3 -o gpurun_out/full_b1024 -f \
+  python tools/prof_batched.py 1024 1 > gpurun_out/full_b1024.log 2>&1; tail -2 gpurun_out/full_b1024.log
+timeout 600 ncu --metrics gpu__time_duration.sum,smsp__sass_thread_inst_executed_op_ffma_pred_on.sum,smsp__sass_thread_inst_executed_op_fadd_pred_on.sum,smsp__sass_thread_inst_executed_op_fmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__inst_executed_pipe_xu.sum,smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+  --clock-control none -k regex:"k_local" -s 1 -c 2 --csv --log-file gpurun_out/local_ops.csv python tools/prof_batched.py 1024 1 > gpurun_out/local_ops.log 2>&1; tail -2 gpurun_out/local_ops.log
+true
