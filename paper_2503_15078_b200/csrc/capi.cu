@@ -1141,7 +1141,7 @@ extern "C" int sim_set_kpass_mode(sim_handle* H, int32_t mode) {
     // mode 0 | 1; mode >= 16: tensor cores with (mode >> 4) tiles per fp32 TMEM accumulation (tuning)
     if (mode >= 16) {
         H->kpass_mode = 0;
-        H->tc_drain = std::max(1, mode >> 4);
+        H->tc_drain = std::max(2, mode >> 4);
         return SIM_OK;
     }
     if (mode != 0 && mode != 1) return fail(SIM_E_INVALID, "K-pass mode must be 0 (tensor cores) or 1 (FP32)");

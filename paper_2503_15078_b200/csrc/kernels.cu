@@ -1060,15 +1060,17 @@ void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
 // registers every `drain` tiles and restarted, units combined in fp64 as in k_kpass_b.
 //   operands in shared memory, SWIZZLE_NONE K-major canonical layout: core matrix = 8 rows
 //   x 16 B (4 tf32 along K); LBO = 128 B between K chunks, SBO = 1024 B between 8-row groups.
-//   A (vectors, 128 x 32 per component, hi and lo): written by all 256 threads from the
-//   gathered rows (float4 loads, coalesced over instances); B (K tile hi / lo, 4 KB each):
+//   A (vectors, 128 x 32 per component, hi and lo): written by all 512 threads from the
+//   gathered rows (float4 loads, coalesced over instances, 8 per thread in flight: the whole
+//   64 KB tile is requested at once); B (K tile hi / lo, 4 KB each):
 //   pre-laid out on the host, one 8 KB bulk copy per tile.  Two stages: while the tensor
 //   core runs tile t the threads stage tile t + 1; tcgen05.commit frees a stage.
 //   thread 0 issues the 36 MMAs per tile (3 components x 4 K-steps x 3 products).
-//   epilogue: warp w reads TMEM lanes 32 (w % 4) .. (instances) and columns 16 (w / 4) ..
-//   (outputs) of every component with tcgen05.ld.32x32b.x16.
+//   fold / epilogue: warp w reads TMEM lanes 32 (w % 4) .. (instances) and columns 8 (w / 4) ..
+//   (outputs) of every component with tcgen05.ld.32x32b.x8.
 // ----------------------------------------------------------------------------
 constexpr int kTcInst = 128;
+constexpr int kTcThreads = 512;                                   // 16 warps: 4 per TMEM lane quadrant
 constexpr uint32_t kTcAplane = kTcInst * 32 * 4;                  // 16 KB
 constexpr uint32_t kTcStage = 6 * kTcAplane + 2 * 4096;           // 104 KB
 constexpr size_t kTcSmem = 2 * (size_t)kTcStage + 128;
@@ -1097,26 +1099,27 @@ __device__ __forceinline__ float tf32_rn(float v) {
 }
 
 template <int PASS>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kTcThreads + 32, 1)
     k_kpass_tc(int S, int n_f, const BUnit* __restrict__ units, const float* __restrict__ Ttc,
                const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
                double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
                const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
     extern __shared__ unsigned char tsm_raw[];
-    __shared__ __align__(8) uint64_t bfull[2], mdone[2];
+    __shared__ __align__(8) uint64_t bfull[2], mdone[2], afull[2];
     __shared__ uint32_t tmem_base_s;
     __shared__ int s_last;
     unsigned char* tsm = tsm_raw + ((128u - ((unsigned)__cvta_generic_to_shared(tsm_raw) & 127u)) & 127u);
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const bool mma_warp = w == kTcThreads / 32;   // the extra warp issues the MMAs; warps 0-15 produce
     const BUnit U = units[blockIdx.x];
     const int chunk = blockIdx.y;
     const int i0 = chunk * kTcInst;
     const int ni = min(kTcInst, S - i0);
     const unsigned long long pol = l2_evict_first();
-    if (w == 0) {
+    if (w == 0) {   // two accumulator sets of 3 x 32 columns (one folds while the other accumulates)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                          (unsigned)__cvta_generic_to_shared(&tmem_base_s)),
-                     "r"(128u)
+                     "r"(256u)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
@@ -1125,6 +1128,8 @@ __global__ void __launch_bounds__(256, 1)
         mbar_init(&bfull[1], 1);
         mbar_init(&mdone[0], 1);
         mbar_init(&mdone[1], 1);
+        mbar_init(&afull[0], kTcThreads);
+        mbar_init(&afull[1], kTcThreads);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -1142,65 +1147,94 @@ __global__ void __launch_bounds__(256, 1)
         issueB(0);
         if (U.ntiles > 1) issueB(1);
     }
-    const int il = tid & (kTcInst - 1), jb = tid >> 7;   // producer: instance, first K chunk
+    // producer: instance il, K chunks jb and jb + 4 (4 reduction rows each): 8 float4 loads in flight
+    const int il = tid & (kTcInst - 1), jb = tid >> 7;
     const bool ilive = il < ni;
     const uint32_t aoff = (uint32_t)((il >> 3) * 1024 + (il & 7) * 16);
-    // epilogue mapping: warp w owns TMEM lanes 32 (w % 4) .. and output columns 16 (w / 4) ..
-    const int q4 = w & 3, half = w >> 2;
-    double dacc[3][16];
+    // fold mapping: warp w owns TMEM lanes 32 (w % 4) .. +31 (instances) and output columns 8 (w / 4) .. +7
+    const int q4 = w & 3, oct = w >> 2;
+    double dacc[3][8];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) dacc[c][e] = 0.0;
-    // fold the TMEM accumulators (fp32 over <= drain tiles) into fp64 registers
-    auto fold = [&]() {
+        for (int e = 0; e < 8; ++e) dacc[c][e] = 0.0;
+    // tiles are accumulated in groups of `drain` (>= 2) into TMEM set (group % 2); group g is
+    // folded into fp64 registers while group g + 1 accumulates, once its last MMA has completed
+    auto fold = [&](int g) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const uint32_t ta = tmem + ((uint32_t)(32 * q4) << 16) + 32u * c + 16u * half;
-            uint32_t r[16];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-                "%14, %15}, [%16];\n"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                  "=r"(r[15])
-                : "r"(ta));
+            const uint32_t ta = tmem + ((uint32_t)(32 * q4) << 16) + 128u * (g & 1) + 32u * c + 8u * oct;
+            uint32_t r[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                           "=r"(r[7])
+                         : "r"(ta));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-            for (int e = 0; e < 16; ++e) dacc[c][e] += (double)__uint_as_float(r[e]);
+            for (int e = 0; e < 8; ++e) dacc[c][e] += (double)__uint_as_float(r[e]);
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     };
+    if (mma_warp) {
+        // single issuing thread: per tile, wait for the 512 producers' A planes and the B tile,
+        // then 36 MMAs into the TMEM accumulators and a commit that frees the stage
+        if (lane == 0) {
+            for (int t = 0; t < U.ntiles; ++t) {
+                const int st = t & 1;
+                mbar_wait(&afull[st], (t >> 1) & 1);
+                mbar_wait(&bfull[st], (t >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                const uint32_t b0 = (unsigned)__cvta_generic_to_shared(bplane(st, 0));
+                const uint32_t b1 = (unsigned)__cvta_generic_to_shared(bplane(st, 1));
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const uint32_t a0 = (unsigned)__cvta_generic_to_shared(aplane(st, c, 0));
+                    const uint32_t a1 = (unsigned)__cvta_generic_to_shared(aplane(st, c, 1));
+                    const uint32_t dt = tmem + 128u * ((t / drain) & 1) + 32u * c;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint32_t o = 256u * kk;
+                        umma_tf32(dt, umma_desc_k(a0 + o), umma_desc_k(b0 + o),
+                                  (t % drain != 0 || kk > 0) ? 1u : 0u);
+                        umma_tf32(dt, umma_desc_k(a1 + o), umma_desc_k(b0 + o), 1u);
+                        umma_tf32(dt, umma_desc_k(a0 + o), umma_desc_k(b1 + o), 1u);
+                    }
+                }
+                umma_commit(&mdone[st]);
+            }
+        }
+        __syncwarp();
+    } else {
     for (int t = 0; t < U.ntiles; ++t) {
         const int st = t & 1;
-        if (t > 0 && t % drain == 0) {   // accumulators complete up to tile t - 1: fold, restart
-            mbar_wait(&mdone[(t - 1) & 1], ((t - 1) >> 1) & 1);
-            fold();
-        }
-        if (t >= 2) {
-            mbar_wait(&mdone[st], ((t - 2) >> 1) & 1);   // the tensor core is done with stage st
-            if (tid == 0) issueB(t);
-        }
         const int nv = PASS == 1 ? max(0, min(32, n_f - (U.c0 + 32 * t))) : min(32, U.nlist - 32 * t);
+        // issue this thread's 8 row loads first (they do not touch shared memory)
+        float4 r[2][4];
 #pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const int j = jb + 2 * it;
-            float4 r[4];
+        for (int it = 0; it < 2; ++it)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int q = 4 * j + e;
-                r[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int q = 4 * (jb + 4 * it) + e;
+                r[it][e] = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (ilive && q < nv) {
                     const int idx = PASS == 1 ? U.c0 + 32 * t + q : __ldg(&cover[U.list0 + 32 * t + q]);
-                    r[e] = __ldg(&vin[(size_t)idx * S + i0 + il]);
+                    r[it][e] = __ldg(&vin[(size_t)idx * S + i0 + il]);
                 }
             }
+        if (t >= 2) {
+            mbar_wait(&mdone[st], ((t - 2) >> 1) & 1);   // the tensor core is done with stage st (tile t - 2)
+            if (tid == 0) issueB(t);
+            if ((t - 1) % drain == 0) fold((t - 2) / drain);   // tile t - 2 closed its group
+        }
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int j = jb + 4 * it;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 float a[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) a[e] = c == 0 ? r[e].x : (c == 1 ? r[e].y : r[e].z);
+                for (int e = 0; e < 4; ++e) a[e] = c == 0 ? r[it][e].x : (c == 1 ? r[it][e].y : r[it][e].z);
                 float4 hi, lo;
                 hi.x = tf32_rn(a[0]); hi.y = tf32_rn(a[1]); hi.z = tf32_rn(a[2]); hi.w = tf32_rn(a[3]);
                 lo.x = tf32_rn(a[0] - hi.x); lo.y = tf32_rn(a[1] - hi.y);
@@ -1209,47 +1243,37 @@ __global__ void __launch_bounds__(256, 1)
                 *reinterpret_cast<float4*>(aplane(st, c, 1) + aoff + j * 128) = lo;
             }
         }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> tensor core
-        __syncthreads();
-        if (tid == 0) {
-            mbar_wait(&bfull[st], (t >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t b0 = (unsigned)__cvta_generic_to_shared(bplane(st, 0));
-            const uint32_t b1 = (unsigned)__cvta_generic_to_shared(bplane(st, 1));
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const uint32_t a0 = (unsigned)__cvta_generic_to_shared(aplane(st, c, 0));
-                const uint32_t a1 = (unsigned)__cvta_generic_to_shared(aplane(st, c, 1));
-                const uint32_t dt = tmem + 32u * c;
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint32_t o = 256u * kk;
-                    umma_tf32(dt, umma_desc_k(a0 + o), umma_desc_k(b0 + o), (t % drain != 0 || kk > 0) ? 1u : 0u);
-                    umma_tf32(dt, umma_desc_k(a1 + o), umma_desc_k(b0 + o), 1u);
-                    umma_tf32(dt, umma_desc_k(a0 + o), umma_desc_k(b1 + o), 1u);
-                }
-            }
-            umma_commit(&mdone[st]);
-        }
+        // generic-proxy writes (and the fold's TMEM reads) -> visible to the tensor core, then arrive
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&afull[st]))
+                     : "memory");
     }
     {
         const int last = U.ntiles - 1;
         if (last >= 0) {
             mbar_wait(&mdone[last & 1], (last >> 1) & 1);
-            fold();
+            // groups not folded in the loop: the last one, and the one before it when the loop
+            // ended before reaching its fold point (tile index last group start + 1)
+            const int glast = last / drain;
+            const int gdone = last >= 1 ? (last - 1) / drain : 0;   // groups folded: those whose fold tile <= last
+            for (int g = gdone; g <= glast; ++g) fold(g);
         }
     }
+    }   // producers
     __syncthreads();
     if (w == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(128u) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256u) : "memory");
+    if (mma_warp) return;
     const int li = 32 * q4 + lane;
     const bool live = li < ni;
     const int inst = i0 + li;
     if (PASS == 2) {
         if (!live) return;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int l = 16 * half + r;
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
             if (l < U.nr) {
                 const size_t jx = (size_t)(U.c0 + l) * S + inst;
                 double4 xj = x[jx];
@@ -1268,8 +1292,8 @@ __global__ void __launch_bounds__(256, 1)
     if (U.nparts == 1) {
         if (!live) return;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int l = 16 * half + r;
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
             if (l < U.nr)
                 yout[(size_t)(U.r0 + l) * S + inst] =
                     make_float4((float)dacc[0][r], (float)dacc[1][r], (float)dacc[2][r], 0.f);
@@ -1280,8 +1304,8 @@ __global__ void __launch_bounds__(256, 1)
     const size_t pstride = (size_t)32 * S;
     if (live) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int l = 16 * half + r;
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
             double* pp = part + (size_t)U.part * 3 * pstride + (size_t)l * S + inst;
             pp[0] = dacc[0][r];
             pp[pstride] = dacc[1][r];
@@ -1298,8 +1322,8 @@ __global__ void __launch_bounds__(256, 1)
     if (!s_last) return;
     __threadfence();
     if (live) {
-        for (int r = 0; r < 16; ++r) {
-            const int l = 16 * half + r;
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
             if (l >= U.nr) continue;
             double t0 = 0.0, t1 = 0.0, t2 = 0.0;
             for (int q = 0; q < U.nparts; ++q) {
@@ -1322,7 +1346,7 @@ void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
         attr = true;
     }
     const int nch = (S + kTcInst - 1) / kTcInst;
-    k_kpass_tc<1><<<dim3(nunits, nch), 256, kTcSmem, st>>>(S, n_f, units, T1tc, nullptr, u, y, part, counters, nch,
+    k_kpass_tc<1><<<dim3(nunits, nch), kTcThreads + 32, kTcSmem, st>>>(S, n_f, units, T1tc, nullptr, u, y, part, counters, nch,
                                                            nullptr, nullptr, nullptr, 0.0, 0, drain);
 }
 
@@ -1335,7 +1359,7 @@ void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
         attr = true;
     }
     const int nch = (S + kTcInst - 1) / kTcInst;
-    k_kpass_tc<2><<<dim3(nunits, nch), 256, kTcSmem, st>>>(S, n_f, units, T2tc, cover, y, nullptr, nullptr, nullptr,
+    k_kpass_tc<2><<<dim3(nunits, nch), kTcThreads + 32, kTcSmem, st>>>(S, n_f, units, T2tc, cover, y, nullptr, nullptr, nullptr,
                                                            nch, x, xt, v, inv_h, finalize_v, drain);
 }
 
