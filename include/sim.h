@@ -119,6 +119,7 @@ typedef struct {
     double  build_seconds;     /* host time of sim_build_sparse_inverse                                  */
     int64_t h2d_contact_bytes; /* host->device bytes of the last contact commit                          */
     int32_t n_instances;
+    int64_t nonfinite_rollbacks; /* instance-frames rolled back to x_t, v_t (non-finite x or v), total    */
 } sim_stats;
 
 /* Validate the mesh and material, compute rest data (Dm^-1, volumes, lumped
@@ -159,7 +160,11 @@ int sim_set_contacts_batch(sim_handle *h, int32_t first, int32_t count, const in
 int sim_step(sim_handle *h, int32_t frames, int32_t iterations);
 
 /* Block until all work enqueued on the handle's stream is done; checks the
- * device-side non-finite flag. */
+ * device-side failure counter: every frame ends with a check of x and v, and an
+ * instance whose frame produced a non-finite value is rolled back to its
+ * frame-start state (x_t, v_t) on the device.  Returns SIM_E_NONFINITE (once,
+ * with the count in sim_last_error) if any instance-frame was rolled back since
+ * the previous call; the running total is sim_stats.nonfinite_rollbacks. */
 int sim_synchronize(sim_handle *h);
 
 /* Constant velocity (m/s) of all pinned vertices (moving Dirichlet handle). */
@@ -261,6 +266,11 @@ int sim_debug_contact_state(sim_handle *h, int32_t instance, double *theta, doub
  * solve: [1] rho built, [2] active set + G_A gathered, [3 + it] after CR
  * iteration it, [20] loop end, [21] epilogue end.  out must hold 32 doubles. */
 int sim_debug_cr_timeline(sim_handle *h, double *out);
+/* Failure-injection hook: the next frame (run outside the captured graph) writes a NaN into
+ * vertex 0 of `instance` right after the prediction step, so the end-of-frame check must roll
+ * that instance back to its frame-start state and sim_synchronize must report
+ * SIM_E_NONFINITE.  SIM_E_INVALID / SIM_E_STATE as the other per-instance accessors. */
+int sim_debug_poison(sim_handle *h, int32_t instance);
 
 #ifdef __cplusplus
 }

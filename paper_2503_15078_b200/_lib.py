@@ -17,7 +17,7 @@ EXPORTED_SYMBOLS = [
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
-    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode",
+    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -78,7 +78,8 @@ class SimStats(C.Structure):
                 ("frames_done", C.c_int64), ("last_cr_residual", C.c_double), ("max_abs_phi_n", C.c_double),
                 ("n_active", C.c_int32), ("n_stick", C.c_int32), ("n_slip", C.c_int32),
                 ("kernels_per_frame", C.c_int32), ("build_seconds", C.c_double),
-                ("h2d_contact_bytes", C.c_int64), ("n_instances", C.c_int32)]
+                ("h2d_contact_bytes", C.c_int64), ("n_instances", C.c_int32),
+                ("nonfinite_rollbacks", C.c_int64)]
 
 
 class SimError(RuntimeError):
@@ -116,6 +117,7 @@ def _load():
         "sim_set_ncp": [H, C.c_int32, C.c_int32],
         "sim_set_admm": [H, C.c_int32],
         "sim_set_kpass_mode": [H, C.c_int32],
+        "sim_debug_poison": [H, C.c_int32],
         "sim_get_kernel_times": [H, dp, C.c_int32],
         "sim_debug_contact_state": [H, C.c_int32, dp, dp, dp, dp, ip, dp],
         "sim_debug_cr_timeline": [H, dp],
@@ -307,6 +309,10 @@ class Sim:
     def set_kpass_mode(self, mode: int):
         """Batched K-passes: 0 tensor cores (tcgen05), 1 CUDA-core FP32 (sim_set_kpass_mode)."""
         _check(lib.sim_set_kpass_mode(self._h, int(mode)))
+
+    def debug_poison(self, instance=0):
+        """Inject a NaN into the next frame of `instance` (sim_debug_poison)."""
+        _check(lib.sim_debug_poison(self._h, int(instance)))
 
     def set_profiling(self, on: bool):
         _check(lib.sim_set_profiling(self._h, 1 if on else 0))

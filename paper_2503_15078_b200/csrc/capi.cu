@@ -118,6 +118,11 @@ struct sim_handle {
     double vpin[3] = {0, 0, 0};
     // device: state, [entity][S]
     DBuf<double4> x, xt, v, s;
+    DBuf<double4> vt;                // frame-start velocity (rollback on a non-finite frame)
+    DBuf<int> bad;                   // [S] per-instance failure flags of the current frame
+    DBuf<int> rollbacks;             // device counter of rolled-back instance-frames (read by sim_synchronize)
+    int64_t rollbacks_total = 0;
+    int poison_inst = -1;            // sim_debug_poison: instance whose next frame gets a NaN
     DBuf<double> M;
     DBuf<int4> tet;
     DBuf<float> Bm, hw2;
@@ -331,6 +336,10 @@ static int upload_all(sim_handle* H) {
     }
     const size_t nvS = (size_t)nv * S;
     CK(H->x.alloc(nvS)); CK(H->xt.alloc(nvS)); CK(H->v.alloc(nvS)); CK(H->s.alloc(nvS));
+    CK(H->vt.alloc(nvS)); CK(H->bad.alloc(S));
+    CK(cudaMemsetAsync(H->bad.p, 0, S * sizeof(int), st));
+    CK(H->rollbacks.alloc(1));
+    CK(cudaMemsetAsync(H->rollbacks.p, 0, sizeof(int), st));
     {
         DBuf<double4> x1;
         CK(x1.alloc(nv));
@@ -1066,7 +1075,8 @@ static int enqueue_frame(sim_handle* H, int iters) {
 #define MARK(k) do { int r_ = mark(k); if (r_) return -r_; } while (0)
 #define CKR(call) do { cudaError_t r_ = (call); if (r_ != cudaSuccess) return -(int)r_; } while (0)
     MARK(KK_PREDICT);
-    launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->lam.p, 3 * H->C); nk++;
+    launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->lam.p, 3 * H->C, H->vt.p, H->bad.p); nk++;
+    if (H->poison_inst >= 0) launch_poison(st, H->x.p, H->poison_inst, H->S);   // test hook (not captured)
     const bool con = H->C > 0;
     for (int k = 0; k < iters; ++k) {
         // contact evaluation (+ active set) and the local step only read x^k: two graph
@@ -1111,6 +1121,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
         MARK(KK_KPASS2);
         enqueue_kpass2(H, st, H->x.p, H->xt.p, H->v.p, 1.0 / H->h, k == iters - 1); nk++;
     }
+    launch_finite_guard(st, H->n_v, H->S, H->x.p, H->v.p, H->xt.p, H->vt.p, H->bad.p, H->rollbacks.p); nk += 2;
     MARK(KK_N);
 #undef MARK
 #undef CKR
@@ -1133,6 +1144,15 @@ extern "C" int sim_set_admm(sim_handle* H, int32_t on) {
     if (on && H->state == 1 && !H->host_only && !H->du.p) CK(H->du.alloc((size_t)9 * H->n_t * H->S));
     if (on && H->state != 1) return fail(SIM_E_STATE, "build the sparse inverse first");
     H->admm = on;
+    return SIM_OK;
+}
+
+static int check_instance(sim_handle* H, int inst);
+
+extern "C" int sim_debug_poison(sim_handle* H, int32_t inst) {
+    int rc = check_instance(H, inst);
+    if (rc) return rc;
+    H->poison_inst = inst;
     return SIM_OK;
 }
 
@@ -1190,6 +1210,13 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     if (frames == 0) return SIM_OK;
     int rc = commit_contacts(H);
     if (rc) return rc;
+    if (H->poison_inst >= 0) {   // sim_debug_poison: this one frame runs uncaptured with a NaN injected
+        const int nk = enqueue_frame(H, iters);
+        H->poison_inst = -1;
+        if (nk < 0) return fail(SIM_E_CUDA, "launch failed: %s", cudaGetErrorString((cudaError_t)(-nk)));
+        H->frames_done += 1;
+        if (--frames == 0) return SIM_OK;
+    }
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
                                       H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG,
                                       H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain};
@@ -1220,6 +1247,16 @@ extern "C" int sim_synchronize(sim_handle* H) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (H->host_only) return SIM_OK;
     CK(cudaStreamSynchronize(H->stream));
+    if (H->rollbacks.p) {
+        int n = 0;
+        CK(cudaMemcpy(&n, H->rollbacks.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (n > 0) {
+            CK(cudaMemset(H->rollbacks.p, 0, sizeof(int)));
+            H->rollbacks_total += n;
+            return fail(SIM_E_NONFINITE, "%d instance-frame(s) became non-finite and were rolled back to their "
+                        "frame-start state", n);
+        }
+    }
     return SIM_OK;
 }
 
@@ -1376,6 +1413,13 @@ extern "C" int sim_get_stats(sim_handle* H, sim_stats* o) {
     o->kernels_per_frame = H->kernels_per_frame;
     o->build_seconds = H->build_seconds;
     o->h2d_contact_bytes = H->h2d_contact_bytes;
+    o->nonfinite_rollbacks = H->rollbacks_total;
+    if (!H->host_only && H->rollbacks.p) {
+        int n = 0;
+        CK(cudaStreamSynchronize(H->stream));
+        CK(cudaMemcpy(&n, H->rollbacks.p, sizeof(int), cudaMemcpyDeviceToHost));
+        o->nonfinite_rollbacks += n;
+    }
     o->last_cr_residual = -1;
     if (!H->host_only && H->state == 1 && H->C > 0 && !H->dirty) {
         CK(cudaStreamSynchronize(H->stream));

@@ -26,12 +26,15 @@ namespace simdev {
 // predict: s = x_t + h v_t + h^2 g; x^0 = s; pinned: x = x_t + h v_pin
 // ----------------------------------------------------------------------------
 __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict__ xt,
-                          double4* __restrict__ v, double4* __restrict__ s, double* __restrict__ lam, int nlam) {
+                          double4* __restrict__ v, double4* __restrict__ s, double* __restrict__ lam, int nlam,
+                          double4* __restrict__ vt, int* __restrict__ bad) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;   // (vertex, instance), instance-minor
     if (i < nlam) lam[i] = 0.0;   // lambda^0 = 0 (reading A10)
+    if (bad && i < P.S) bad[i] = 0;
     if (i >= P.n_v * P.S) return;
     double4 xi = x[i];
     xt[i] = xi;
+    if (vt) vt[i] = v[i];   // frame-start velocity, restored if the frame turns non-finite
     double h = P.h;
     if (i < P.n_f * P.S) {
         double4 vi = v[i];
@@ -46,9 +49,48 @@ __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict
 }
 
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
-                    double* lam, int nlam) {
+                    double* lam, int nlam, double4* vt, int* bad) {
     int n = P.n_v * P.S > nlam ? P.n_v * P.S : nlam;
-    k_predict<<<(n + 255) / 256, 256, 0, st>>>(P, x, xt, v, s, lam, nlam);
+    n = n > P.S ? n : P.S;
+    k_predict<<<(n + 255) / 256, 256, 0, st>>>(P, x, xt, v, s, lam, nlam, vt, bad);
+}
+
+// ----------------------------------------------------------------------------
+// failure detection: an instance whose frame produced a non-finite position or
+// velocity is rolled back to its frame-start state (x_t, v_t); `rollbacks` (host-mapped)
+// counts the rolled-back instance-frames for sim_synchronize to report
+// ----------------------------------------------------------------------------
+__global__ void k_finite_check(int n, int S, const double4* __restrict__ x, const double4* __restrict__ v,
+                               int* __restrict__ bad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * S) return;
+    const double4 a = x[i], b = v[i];
+    const bool ok = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(b.x) && isfinite(b.y) && isfinite(b.z);
+    if (!ok) atomicOr(&bad[i % S], 1);
+}
+
+__global__ void k_rollback(int n, int S, double4* __restrict__ x, double4* __restrict__ v,
+                           const double4* __restrict__ xt, const double4* __restrict__ vt,
+                           const int* __restrict__ bad, int* rollbacks) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * S) return;
+    const int inst = i % S;
+    if (!bad[inst]) return;
+    x[i] = xt[i];
+    v[i] = vt[i];
+    if (i < S) atomicAdd(rollbacks, 1);   // vertex 0 of the instance
+}
+
+__global__ void k_poison(double4* x, int inst, int S) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) x[inst].x = __longlong_as_double(0x7ff8000000000000ll);
+}
+void launch_poison(cudaStream_t st, double4* x, int inst, int S) { k_poison<<<1, 32, 0, st>>>(x, inst, S); }
+
+void launch_finite_guard(cudaStream_t st, int n_v, int S, double4* x, double4* v, const double4* xt,
+                         const double4* vt, int* bad, int* rollbacks) {
+    const int blocks = (int)(((size_t)n_v * S + 255) / 256);
+    k_finite_check<<<blocks, 256, 0, st>>>(n_v, S, x, v, bad);
+    k_rollback<<<blocks, 256, 0, st>>>(n_v, S, x, v, xt, vt, bad, rollbacks);
 }
 
 // dst[e * S + i] = src[e] for every instance i (state initialisation)

@@ -113,8 +113,13 @@ struct Slots {
 
 // --- frame kernels -----------------------------------------------------------
 void launch_replicate(cudaStream_t st, const double4* src, double4* dst, int n, int S);
+// vt (nullable): frame-start velocity copy; bad (nullable): per-instance failure flags, zeroed here
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
-                    double* lam, int nlam);
+                    double* lam, int nlam, double4* vt = nullptr, int* bad = nullptr);
+void launch_poison(cudaStream_t st, double4* x, int inst, int S);   // test hook: x[vertex 0] of inst = NaN
+// end of frame: instances with a non-finite x or v get x = x_t, v = v_t; *rollbacks += count
+void launch_finite_guard(cudaStream_t st, int n_v, int S, double4* x, double4* v, const double4* xt,
+                         const double4* vt, int* bad, int* rollbacks);
 // du: ADMM-PD dual [9][n_t S] or nullptr (plain PD); admm_first: treat u as 0 (first iteration of a frame)
 void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
                   const double4* x, float4* fc, float* Pdbg, float* du = nullptr, int admm_first = 0);

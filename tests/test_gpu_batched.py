@@ -204,3 +204,34 @@ def test_tensor_core_and_fp32_kpasses_agree(simmod):
         for mode in (0, 1):
             assert np.abs(out[mode][i][o.free] - xr).max() < 1e-5 * np.abs(xr).max(), (mode, i)
     assert np.abs(out[0] - out[1]).max() < 1e-5 * np.abs(out[1]).max()
+
+
+def test_nonfinite_frame_rolls_back_one_instance(simmod):
+    """Failure detection (include/sim.h sim_synchronize, SIM_E_NONFINITE): an instance whose
+    frame turns non-finite (NaN injected after the prediction by the sim_debug_poison hook) is
+    restored to its frame-start x, v on the device; the other instance advances as the oracle
+    says; the error is reported once and counted in the stats; the next frame is normal."""
+    sc = scenes.make_scene("block", nv=5)
+    s = make(simmod, sc, 2)
+    xs, vs = scenes.random_state(sc.mesh, seed=4, amp=0.05)
+    fx = sc.mesh.fixed.astype(bool)
+    xs[fx] = sc.mesh.X[fx]
+    vs[fx] = 0.0
+    for i in range(2):
+        s.set_state(xs, vs, instance=i)
+    s.debug_poison(0)
+    s.step(1, 5)
+    with pytest.raises(simmod.SimError, match="-7"):
+        s.synchronize()
+    s.synchronize()                   # reported once
+    x0, v0 = s.get_state(instance=0)
+    assert np.array_equal(x0, xs) and np.array_equal(v0, vs)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    xo, vo, _ = o.frame(xs, vs)
+    x1, _ = s.get_state(instance=1)
+    assert np.abs(x1 - xo).max() < 1e-5 * sc.mesh.bbox_diag()
+    assert s.stats()["nonfinite_rollbacks"] == 1
+    s.step(1, 5)                      # graph replay again, both instances healthy
+    s.synchronize()
+    x0, _ = s.get_state(instance=0)
+    assert np.abs(x0 - xo).max() < 1e-5 * sc.mesh.bbox_diag()
