@@ -18,6 +18,10 @@
 
 #include "kernels.cuh"
 
+#ifndef SIM_JACOBI_SWEEPS
+#define SIM_JACOBI_SWEEPS 6   // cap of the cyclic Jacobi sweeps of the local step's SVD
+#endif
+
 namespace cg = cooperative_groups;
 
 namespace simdev {
@@ -115,7 +119,7 @@ __device__ __forceinline__ void jacobi3(float S[3][3], float V[3][3]) {
 #pragma unroll
         for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.f : 0.f;
 #pragma unroll 1
-    for (int sweep = 0; sweep < 6; ++sweep) {
+    for (int sweep = 0; sweep < SIM_JACOBI_SWEEPS; ++sweep) {
         float off = fabsf(S[0][1]) + fabsf(S[0][2]) + fabsf(S[1][2]);
         float dia = fabsf(S[0][0]) + fabsf(S[1][1]) + fabsf(S[2][2]);
         if (off <= 1e-9f * dia) break;
