@@ -176,6 +176,15 @@ int sim_get_state(sim_handle *h, int32_t instance, double *x, double *v);
 int sim_set_state(sim_handle *h, int32_t instance, const double *x, const double *v);
 /* Positions of all instances: x [n_instances][n_vertices][3]. */
 int sim_get_positions(sim_handle *h, double *x);
+/* The same positions, asynchronously: enqueued on the handle's stream after the frames
+ * already enqueued, packed on the device into one of two staging buffers and copied to
+ * host_dst (caller-owned; pinned memory for real overlap) on a separate copy stream, so the
+ * transfer overlaps the next frames.  host_dst must stay valid until sim_wait_positions.
+ * Two calls may be in flight (the third waits for the first copy on the device). */
+int sim_get_positions_async(sim_handle *h, double *host_dst);
+/* Completion of the last sim_get_positions_async: block_host != 0 blocks the calling
+ * thread; 0 makes the handle's stream wait (device-side join, for event timing). */
+int sim_wait_positions(sim_handle *h, int32_t block_host);
 /* States of all instances: x, v [n_instances][n_vertices][3] (either may be NULL). */
 int sim_set_states(sim_handle *h, const double *x, const double *v);
 

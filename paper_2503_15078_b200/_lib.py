@@ -17,7 +17,8 @@ EXPORTED_SYMBOLS = [
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
-    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison",
+    "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison", "sim_get_positions_async",
+    "sim_wait_positions",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -118,6 +119,8 @@ def _load():
         "sim_set_admm": [H, C.c_int32],
         "sim_set_kpass_mode": [H, C.c_int32],
         "sim_debug_poison": [H, C.c_int32],
+        "sim_get_positions_async": [H, C.c_void_p],
+        "sim_wait_positions": [H, C.c_int32],
         "sim_get_kernel_times": [H, dp, C.c_int32],
         "sim_debug_contact_state": [H, C.c_int32, dp, dp, dp, dp, ip, dp],
         "sim_debug_cr_timeline": [H, dp],
@@ -279,6 +282,14 @@ class Sim:
             out = np.empty((self.n_instances, self.n_v, 3))
         _check(lib.sim_get_positions(self._h, _dptr(out)))
         return out
+
+    def get_positions_async(self, out_ptr: int):
+        """Enqueue the read-back of all positions into caller memory at address out_ptr
+        ([n_instances][n_vertices][3] float64; pinned for overlap), sim_get_positions_async."""
+        _check(lib.sim_get_positions_async(self._h, C.c_void_p(int(out_ptr))))
+
+    def wait_positions(self, block_host: bool = True):
+        _check(lib.sim_wait_positions(self._h, 1 if block_host else 0))
 
     def get_lambda(self, instance=0):
         nc = self._nc[instance]

@@ -123,6 +123,13 @@ struct sim_handle {
     DBuf<int> rollbacks;             // device counter of rolled-back instance-frames (read by sim_synchronize)
     int64_t rollbacks_total = 0;
     int poison_inst = -1;            // sim_debug_poison: instance whose next frame gets a NaN
+    // asynchronous position read-back (sim_get_positions_async): double-buffered device staging
+    // in the caller's layout, copied to the host on a copy stream while the next frames compute
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t pos_ready[2] = {nullptr, nullptr}, pos_copied[2] = {nullptr, nullptr};
+    DBuf<double> pos_stage[2];
+    DBuf<int32_t> o2i;               // original vertex -> internal index (device)
+    int pos_slot = 0, pos_last = -1;
     DBuf<double> M;
     DBuf<int4> tet;
     DBuf<float> Bm, hw2;
@@ -300,6 +307,12 @@ extern "C" void sim_destroy(sim_handle* H) {
         for (auto e : H->pev) cudaEventDestroy(e);
         if (H->stage_free) cudaEventDestroy(H->stage_free);
         if (H->fork_ev) cudaEventDestroy(H->fork_ev);
+        if (H->copy_stream) cudaStreamSynchronize(H->copy_stream);
+        for (int k = 0; k < 2; ++k) {
+            if (H->pos_ready[k]) cudaEventDestroy(H->pos_ready[k]);
+            if (H->pos_copied[k]) cudaEventDestroy(H->pos_copied[k]);
+        }
+        if (H->copy_stream) cudaStreamDestroy(H->copy_stream);
         if (H->join_ev) cudaEventDestroy(H->join_ev);
         if (H->aux) cudaStreamDestroy(H->aux);
         if (H->stage) cudaFreeHost(H->stage);
@@ -1276,6 +1289,46 @@ static int check_instance(sim_handle* H, int inst) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
     if (inst < 0 || inst >= H->S) return fail(SIM_E_INVALID, "instance %d out of range [0, %d)", inst, H->S);
+    return SIM_OK;
+}
+
+// x [n_instances][n_vertices][3] (original vertex order) into a caller-pinned host buffer,
+// asynchronously: a packing kernel on the handle's stream fills one of two device staging
+// buffers, the copy stream moves it to the host while the following frames run
+extern "C" int sim_get_positions_async(sim_handle* H, double* host_dst) {
+    int rc = check_instance(H, 0);
+    if (rc) return rc;
+    if (!host_dst) return fail(SIM_E_INVALID, "null argument");
+    const size_t n = (size_t)H->n_v * H->S * 3;
+    if (!H->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&H->copy_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaEventCreateWithFlags(&H->pos_ready[k], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&H->pos_copied[k], cudaEventDisableTiming));
+            CK(cudaEventRecord(H->pos_copied[k], H->copy_stream));
+            CK(H->pos_stage[k].alloc(n));
+        }
+        CK(H->o2i.alloc(H->n_v));
+        CK(cudaMemcpy(H->o2i.p, H->orig2int.data(), H->n_v * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    const int k = H->pos_slot;
+    CK(cudaStreamWaitEvent(H->stream, H->pos_copied[k], 0));   // staging k no longer being read
+    launch_pack_positions(H->stream, H->x.p, H->o2i.p, H->n_v, H->S, H->pos_stage[k].p);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(H->pos_ready[k], H->stream));
+    CK(cudaStreamWaitEvent(H->copy_stream, H->pos_ready[k], 0));
+    CK(cudaMemcpyAsync(host_dst, H->pos_stage[k].p, n * sizeof(double), cudaMemcpyDeviceToHost, H->copy_stream));
+    CK(cudaEventRecord(H->pos_copied[k], H->copy_stream));
+    H->pos_last = k;
+    H->pos_slot ^= 1;
+    return SIM_OK;
+}
+
+extern "C" int sim_wait_positions(sim_handle* H, int32_t block_host) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (H->pos_last < 0) return SIM_OK;
+    if (block_host) CK(cudaEventSynchronize(H->pos_copied[H->pos_last]));
+    else CK(cudaStreamWaitEvent(H->stream, H->pos_copied[H->pos_last], 0));
     return SIM_OK;
 }
 

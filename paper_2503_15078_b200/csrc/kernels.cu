@@ -90,6 +90,22 @@ __global__ void k_poison(double4* x, int inst, int S) {
 }
 void launch_poison(cudaStream_t st, double4* x, int inst, int S) { k_poison<<<1, 32, 0, st>>>(x, inst, S); }
 
+// dst[(inst * n_v + v) * 3 + d] = x[o2i[v] * S + inst].d  (the caller's layout, original order)
+__global__ void k_pack_positions(const double4* __restrict__ x, const int32_t* __restrict__ o2i, int n_v, int S,
+                                 double* __restrict__ dst) {
+    const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;   // (instance, vertex)
+    if (e >= (size_t)n_v * S) return;
+    const int inst = (int)(e / n_v), vtx = (int)(e - (size_t)inst * n_v);
+    const double4 a = x[(size_t)o2i[vtx] * S + inst];
+    dst[3 * e] = a.x;
+    dst[3 * e + 1] = a.y;
+    dst[3 * e + 2] = a.z;
+}
+void launch_pack_positions(cudaStream_t st, const double4* x, const int32_t* o2i, int n_v, int S, double* dst) {
+    const size_t n = (size_t)n_v * S;
+    if (n) k_pack_positions<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, o2i, n_v, S, dst);
+}
+
 void launch_finite_guard(cudaStream_t st, int n_v, int S, double4* x, double4* v, const double4* xt,
                          const double4* vt, int* bad, int* rollbacks) {
     const int blocks = (int)(((size_t)n_v * S + 255) / 256);

@@ -116,7 +116,8 @@ void launch_replicate(cudaStream_t st, const double4* src, double4* dst, int n, 
 // vt (nullable): frame-start velocity copy; bad (nullable): per-instance failure flags, zeroed here
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
                     double* lam, int nlam, double4* vt = nullptr, int* bad = nullptr);
-void launch_poison(cudaStream_t st, double4* x, int inst, int S);   // test hook: x[vertex 0] of inst = NaN
+void launch_poison(cudaStream_t st, double4* x, int inst, int S);
+void launch_pack_positions(cudaStream_t st, const double4* x, const int32_t* o2i, int n_v, int S, double* dst);   // test hook: x[vertex 0] of inst = NaN
 // end of frame: instances with a non-finite x or v get x = x_t, v = v_t; *rollbacks += count
 void launch_finite_guard(cudaStream_t st, int n_v, int S, double4* x, double4* v, const double4* xt,
                          const double4* vt, int* bad, int* rollbacks);

@@ -235,3 +235,22 @@ def test_nonfinite_frame_rolls_back_one_instance(simmod):
     s.synchronize()
     x0, _ = s.get_state(instance=0)
     assert np.abs(x0 - xo).max() < 1e-5 * sc.mesh.bbox_diag()
+
+
+def test_async_position_readback(simmod):
+    """sim_get_positions_async / sim_wait_positions: double-buffered pinned read-back matches
+    the synchronous sim_get_positions after each of several frames."""
+    import torch
+    sc = scenes.make_scene("block", nv=5)
+    S = 3
+    s = make(simmod, sc, S)
+    bufs = [torch.empty((S, sc.mesh.n_v, 3), dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    ref = []
+    for f in range(4):
+        s.step(1, 5)
+        s.get_positions_async(bufs[f % 2].data_ptr())
+        if f % 2 == 1:
+            s.wait_positions(True)
+            assert np.array_equal(bufs[0].numpy(), ref[-1])
+            assert np.array_equal(bufs[1].numpy(), s.get_positions())
+        ref.append(s.get_positions())
