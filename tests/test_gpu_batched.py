@@ -254,3 +254,65 @@ def test_async_position_readback(simmod):
             assert np.array_equal(bufs[0].numpy(), ref[-1])
             assert np.array_equal(bufs[1].numpy(), s.get_positions())
         ref.append(s.get_positions())
+
+
+def test_cfg5_full_size_sampled(simmod):
+    """cfg5 in the bench's launch configuration: 1024 cfg3 instances on one handle (tensor-core
+    K-passes in 8 chunks of 128, one CR CTA per instance), own initial velocities and obstacle
+    offsets, contacts committed in one batch; one frame; sampled instances (first, middle of the
+    last-but-one chunk, last) against the oracle within 1e-5 bbox."""
+    sc = scenes.make_scene("cfg3")
+    S = 1024
+    s = make(simmod, sc, S)
+    s.set_pin_velocity(sc.pin_velocity)
+    base = simmod.contacts_to_array(sc.contacts)
+    arrs, v0s = [], np.empty((S, sc.mesh.n_v, 3))
+    for i in range(S):
+        v0s[i], delta = scenes.batch_instance_params(sc, i)
+        a = base.copy()
+        a["offset"] += a["normal"][:, 2] * delta
+        arrs.append(a)
+    s.set_contacts_batch(packed=(np.concatenate(arrs), np.full(S, len(base), np.int32)))
+    s.set_states(np.broadcast_to(sc.mesh.X, (S,) + sc.mesh.X.shape), v0s)
+    s.step(1, 5)
+    P = s.get_positions()
+    assert np.isfinite(P).all()
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    for i in (0, 700, 1023):
+        _, cs = scenes.batch_instance(sc, i)
+        o = O.Oracle(sc.mesh, sc.material, sc.h)
+        o.set_contacts(cs)
+        pins = sc.mesh.X[o.pinned] + sc.h * sc.pin_velocity
+        xo, _, _ = o.frame(sc.mesh.X.copy(), v0s[i], pin_targets=pins)
+        assert np.abs(P[i] - xo).max() < tol, (i, np.abs(P[i] - xo).max())
+
+
+@pytest.mark.parametrize("model", [1, 2])
+def test_batched_materials_with_contacts(simmod, model):
+    """Corotated and ARAP (closed-form local steps, their own k_local instantiations) with
+    frictional contact on two instances sharing K, re-synced frames vs the oracle."""
+    th = 10.0
+    sc = scenes.incline_block(theta_deg=th, mu=math.tan(math.radians(th)) - 0.05, nv=5, edge=0.1, youngs=1e7)
+    sc.material.model = model
+    S = 2
+    s = make(simmod, sc, S)
+    for i in range(S):
+        s.set_contacts(sc.contacts, instance=i)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(sc.contacts)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    # instance 1 starts sliding down the slope at 5 cm/s (a randomly perturbed, partly
+    # penetrating start is outside the parity envelope: 5 fixed iterations do not resolve a
+    # 0.8 mm penetration and the FB switching amplifies fp32 rounding, on S = 1 as well)
+    down = -np.array([math.cos(math.radians(th)), 0.0, math.sin(math.radians(th))])
+    xs = [sc.mesh.X.copy(), sc.mesh.X.copy()]
+    vs = [np.zeros_like(sc.mesh.X), np.tile(0.05 * down, (sc.mesh.n_v, 1))]
+    for f in range(4):
+        for i in range(S):
+            s.set_state(xs[i], vs[i], instance=i)
+        s.step(1, 5)
+        for i in range(S):
+            xg, vg = s.get_state(instance=i)
+            xo, _, _ = o.frame(xs[i], vs[i])
+            assert np.abs(xg - xo).max() < tol, (f, i, np.abs(xg - xo).max())
+            xs[i], vs[i] = xg, vg
