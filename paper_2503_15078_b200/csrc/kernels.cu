@@ -18,6 +18,33 @@
 
 #include "kernels.cuh"
 
+// Programmatic dependent launch (PDL): every hot-path kernel starts by waiting for its
+// stream predecessor to complete (griddepcontrol.wait: a no-op without the launch attribute)
+// and then lets its own successor launch, so consecutive kernels of the frame graph overlap
+// their launch and prologue with the tail of the previous grid.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#ifdef SIM_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 #ifndef SIM_JACOBI_SWEEPS
 #define SIM_JACOBI_SWEEPS 6   // cap of the cyclic Jacobi sweeps of the local step's SVD
 #endif
@@ -32,6 +59,7 @@ namespace simdev {
 __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict__ xt,
                           double4* __restrict__ v, double4* __restrict__ s, double* __restrict__ lam, int nlam,
                           double4* __restrict__ vt, int* __restrict__ bad) {
+    pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;   // (vertex, instance), instance-minor
     if (i < nlam) lam[i] = 0.0;   // lambda^0 = 0 (reading A10)
     if (bad && i < P.S) bad[i] = 0;
@@ -66,6 +94,7 @@ void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, d
 // ----------------------------------------------------------------------------
 __global__ void k_finite_check(int n, int S, const double4* __restrict__ x, const double4* __restrict__ v,
                                int* __restrict__ bad) {
+    pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n * S) return;
     const double4 a = x[i], b = v[i];
@@ -76,6 +105,7 @@ __global__ void k_finite_check(int n, int S, const double4* __restrict__ x, cons
 __global__ void k_rollback(int n, int S, double4* __restrict__ x, double4* __restrict__ v,
                            const double4* __restrict__ xt, const double4* __restrict__ vt,
                            const int* __restrict__ bad, int* rollbacks) {
+    pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n * S) return;
     const int inst = i % S;
@@ -109,8 +139,8 @@ void launch_pack_positions(cudaStream_t st, const double4* x, const int32_t* o2i
 void launch_finite_guard(cudaStream_t st, int n_v, int S, double4* x, double4* v, const double4* xt,
                          const double4* vt, int* bad, int* rollbacks) {
     const int blocks = (int)(((size_t)n_v * S + 255) / 256);
-    k_finite_check<<<blocks, 256, 0, st>>>(n_v, S, x, v, bad);
-    k_rollback<<<blocks, 256, 0, st>>>(n_v, S, x, v, xt, vt, bad, rollbacks);
+    launch_pdl(k_finite_check, dim3(blocks), dim3(256), 0, st, n_v, S, x, v, bad);
+    launch_pdl(k_rollback, dim3(blocks), dim3(256), 0, st, n_v, S, x, v, xt, vt, bad, rollbacks);
 }
 
 // dst[e * S + i] = src[e] for every instance i (state initialisation)
@@ -289,6 +319,7 @@ __global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, con
                                                const float* __restrict__ hw2, const double4* __restrict__ x,
                                                float4* __restrict__ fc, float* __restrict__ Pdbg,
                                                float* __restrict__ du, int admm_first) {
+    pdl_enter();
     const int SI = P.S;
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
     if (gt >= P.n_t * SI) return;
@@ -423,11 +454,11 @@ void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float
                   const double4* x, float4* fc, float* Pdbg, float* du, int admm_first) {
     const unsigned g = (unsigned)((P.n_t * (size_t)P.S + 127) / 128);
     if (P.model == 1)
-        k_local<1><<<g, 128, 0, st>>>(P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
+        launch_pdl(k_local<1>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
     else if (P.model == 2)
-        k_local<2><<<g, 128, 0, st>>>(P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
+        launch_pdl(k_local<2>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
     else
-        k_local<0><<<g, 128, 0, st>>>(P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
+        launch_pdl(k_local<0>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
 }
 
 // ----------------------------------------------------------------------------
@@ -435,6 +466,7 @@ void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float
 // ----------------------------------------------------------------------------
 __global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const double4* __restrict__ x,
                                const double4* __restrict__ xt, ContactState cs) {
+    pdl_enter();
     int c = blockIdx.x * blockDim.x + threadIdx.x;   // global contact id
     if (c >= P.C) return;
     const DContact& ct = C[c];
@@ -529,6 +561,7 @@ __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32
                          const float4* __restrict__ fc, const double* __restrict__ M, const double4* __restrict__ x,
                          const double4* __restrict__ s, const int32_t* __restrict__ slotmap, Slots sl,
                          const double* __restrict__ hl, float4* __restrict__ u, double* __restrict__ resid) {
+    pdl_enter();
     const int S = P.S;
     const int gi = blockIdx.x * blockDim.x + threadIdx.x;   // (free vertex, instance), instance-minor
     if (gi >= P.n_f * S) return;
@@ -571,7 +604,8 @@ __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32
 void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
                    const float4* fc, const double* M, const double4* x, const double4* s,
                    const int32_t* slotmap, Slots sl, const double* hl, float4* u, double* resid_dbg) {
-    k_gather<<<(P.n_f * P.S + 255) / 256, 256, 0, st>>>(P, adjp, adj, fc, M, x, s, slotmap, sl, hl, u, resid_dbg);
+    launch_pdl(k_gather, dim3((P.n_f * P.S + 255) / 256), dim3(256), 0, st, P, adjp, adj, fc, M, x, s, slotmap, sl, hl, u,
+               resid_dbg);
 }
 
 // ----------------------------------------------------------------------------
@@ -685,6 +719,7 @@ __global__ void __launch_bounds__(256, 2) k_kpass1(const P1Item* __restrict__ it
                                                    const float* __restrict__ T1, const float4* __restrict__ u,
                                                    float4* __restrict__ y, double* __restrict__ part,
                                                    int* __restrict__ counters) {
+    pdl_enter();
     extern __shared__ __align__(128) unsigned char k1smem[];
     __shared__ __align__(8) uint64_t bars[kWarps][kStages];
     KTile* tiles = reinterpret_cast<KTile*>(k1smem) + (threadIdx.x >> 5) * kStages;
@@ -811,7 +846,7 @@ void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block*
         attr = true;
     }
     const int ctas = std::min((nitems + kWarps - 1) / kWarps, 2 * nsm);   // persistent: 2 CTAs per SM
-    k_kpass1<<<ctas, 32 * kWarps, kKpassSmem, st>>>(it, nitems, bl, T1, u, y, part, counters);
+    launch_pdl(k_kpass1, dim3(ctas), dim3(32 * kWarps), kKpassSmem, st, it, nitems, bl, T1, u, y, part, counters);
 }
 
 // ----------------------------------------------------------------------------
@@ -825,6 +860,7 @@ __global__ void __launch_bounds__(32 * kWarps2, 2) k_kpass2(const P2Block* __res
                                                    const float4* __restrict__ y, double4* __restrict__ x,
                                                    const double4* __restrict__ xt, double4* __restrict__ v,
                                                    double inv_h, int finalize_v) {
+    pdl_enter();
     extern __shared__ __align__(128) unsigned char k2smem[];
     __shared__ __align__(8) uint64_t bars[kWarps2][kStages2];
     KTile* tiles = reinterpret_cast<KTile*>(k2smem) + (threadIdx.x >> 5) * kStages2;
@@ -925,7 +961,7 @@ void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_
         cudaFuncSetAttribute(k_kpass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpass2Smem);
         attr = true;
     }
-    k_kpass2<<<nblocks, 32 * kWarps2, kKpass2Smem, st>>>(bl, cover, T2, y, x, xt, v, inv_h, finalize_v);
+    launch_pdl(k_kpass2, dim3(nblocks), dim3(32 * kWarps2), kKpass2Smem, st, bl, cover, T2, y, x, xt, v, inv_h, finalize_v);
 }
 
 // ----------------------------------------------------------------------------
@@ -952,6 +988,7 @@ __global__ void __launch_bounds__(256, 1)
               const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
               double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
               const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v) {
+    pdl_enter();
     extern __shared__ __align__(128) unsigned char bsm[];
     __shared__ __align__(8) uint64_t full[kBStages];
     __shared__ int s_last;
@@ -1103,8 +1140,8 @@ void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
         attr = true;
     }
     const int nch = (S + kBInst - 1) / kBInst;
-    k_kpass_b<1><<<dim3(nunits, nch), 256, kBSmem, st>>>(S, n_f, units, T1p, nullptr, u, y, part, counters, nch,
-                                                         nullptr, nullptr, nullptr, 0.0, 0);
+    launch_pdl(k_kpass_b<1>, dim3(nunits, nch), dim3(256), kBSmem, st, S, n_f, units, T1p, (const int32_t*)nullptr, u, y,
+               part, counters, nch, (double4*)nullptr, (const double4*)nullptr, (double4*)nullptr, 0.0, 0);
 }
 
 void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
@@ -1116,8 +1153,8 @@ void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
         attr = true;
     }
     const int nch = (S + kBInst - 1) / kBInst;
-    k_kpass_b<2><<<dim3(nunits, nch), 256, kBSmem, st>>>(S, n_f, units, T2, cover, y, nullptr, nullptr, nullptr, nch,
-                                                         x, xt, v, inv_h, finalize_v);
+    launch_pdl(k_kpass_b<2>, dim3(nunits, nch), dim3(256), kBSmem, st, S, n_f, units, T2, cover, y, (float4*)nullptr,
+               (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v);
 }
 
 // ----------------------------------------------------------------------------
@@ -1175,6 +1212,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
                const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
                double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
                const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
+    pdl_enter();
     extern __shared__ unsigned char tsm_raw[];
     __shared__ __align__(8) uint64_t bfull[2], mdone[2], afull[2];
     __shared__ uint32_t tmem_base_s;
@@ -1417,8 +1455,9 @@ void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
         attr = true;
     }
     const int nch = (S + kTcInst - 1) / kTcInst;
-    k_kpass_tc<1><<<dim3(nunits, nch), kTcThreads + 32, kTcSmem, st>>>(S, n_f, units, T1tc, nullptr, u, y, part, counters, nch,
-                                                           nullptr, nullptr, nullptr, 0.0, 0, drain);
+    launch_pdl(k_kpass_tc<1>, dim3(nunits, nch), dim3(kTcThreads + 32), kTcSmem, st, S, n_f, units, T1tc,
+               (const int32_t*)nullptr, u, y, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
+               (double4*)nullptr, 0.0, 0, drain);
 }
 
 void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
@@ -1430,8 +1469,8 @@ void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
         attr = true;
     }
     const int nch = (S + kTcInst - 1) / kTcInst;
-    k_kpass_tc<2><<<dim3(nunits, nch), kTcThreads + 32, kTcSmem, st>>>(S, n_f, units, T2tc, cover, y, nullptr, nullptr, nullptr,
-                                                           nch, x, xt, v, inv_h, finalize_v, drain);
+    launch_pdl(k_kpass_tc<2>, dim3(nunits, nch), dim3(kTcThreads + 32), kTcSmem, st, S, n_f, units, T2tc, cover, y,
+               (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain);
 }
 
 // ----------------------------------------------------------------------------
@@ -1468,6 +1507,7 @@ __global__ void __launch_bounds__(256) k_chain_dot(int S, InstOff off, ClassSlot
                                                    const int32_t* __restrict__ chain_rows, const float4* __restrict__ y,
                                                    CrContacts cc, const double4* __restrict__ x, ContactState cs,
                                                    const int2* __restrict__ items) {
+    pdl_enter();
     __shared__ double s_red[3][kWarps][32];
     const int2 it = items[blockIdx.x];
     const int g = it.x, cl = csl.cls[g];
@@ -1554,8 +1594,8 @@ void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots 
                       Slots sl, CrContacts cc, const double4* x, ContactState cs, int nitems, const int2* items) {
     if (P.NS == 0 || nitems == 0) return;
     (void)sl;
-    k_chain_dot<<<nitems, 32 * kWarps, 0, st>>>(P.S, off, csl, Kcol, colptr, chain_off, chain_rows, y, cc, x, cs,
-                                                items);
+    launch_pdl(k_chain_dot, dim3(nitems), dim3(32 * kWarps), 0, st, P.S, off, csl, Kcol, colptr, chain_off, chain_rows,
+               y, cc, x, cs, items);
 }
 
 // ----------------------------------------------------------------------------
@@ -1565,6 +1605,7 @@ void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots 
 // ----------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_active(InstOff off, CrContacts cc, Slots sl, ContactState cs,
                                                  CrActive act) {
+    pdl_enter();
     __shared__ int wsum[32];
     __shared__ int base;
     const int inst = blockIdx.x;
@@ -1614,6 +1655,7 @@ __global__ void __launch_bounds__(1024) k_active(InstOff off, CrContacts cc, Slo
 // G_A[i][j] = G[aidx_i][aidx_j] (instance blockIdx.y, active row blockIdx.x)
 __global__ void __launch_bounds__(256) k_gather_ga(InstOff off, const float* __restrict__ G, CrActive act,
                                                    float* __restrict__ GA) {
+    pdl_enter();
     const int inst = blockIdx.y;
     const int na = act.na[inst];
     const int i = blockIdx.x;
@@ -1717,6 +1759,7 @@ void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* 
 __global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist,
                           const float* __restrict__ Zc, const double* __restrict__ wz,
                           const float4* __restrict__ wzT, float4* __restrict__ y, const int2* __restrict__ items) {
+    pdl_enter();
     const int2 it = items[blockIdx.y];
     const int c = it.x, m0 = it.y, gs = min(32, off.cmoff[c + 1] - m0);
     const int lane = threadIdx.x & 31;
@@ -1798,7 +1841,7 @@ void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off,
     if (P.NS == 0 || nitems == 0) return;
     int gx = (max_rows + 7) / 8;
     if (nitems > 1) gx = std::min(gx, std::max(1, (148 * 8 + nitems - 1) / nitems));
-    k_scatter<<<dim3(gx, nitems), 256, 0, st>>>(P.S, off, ucount, ulist, Zc, wz, wzT, y, items);
+    launch_pdl(k_scatter, dim3(gx, nitems), dim3(256), 0, st, P.S, off, ucount, ulist, Zc, wz, wzT, y, items);
 }
 
 // ----------------------------------------------------------------------------
@@ -2146,6 +2189,7 @@ template <int kRpt>
 __global__ void __launch_bounds__(kCrThreads, 1)
     k_cr(Params P, InstOff off, const DContact* __restrict__ C, CrContacts cc, Slots sl,
          const float* __restrict__ GA, const double4* __restrict__ x, ContactState cs, CrActive act) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char smraw[];
     cg::cluster_group cl = cg::this_cluster();
     const int csize = (int)cl.num_blocks(), rank = (int)cl.block_rank();
@@ -2405,6 +2449,7 @@ __device__ __forceinline__ void block_sum3_gcr(double& a, double& b, double& c, 
 // r = rho (rho of multi-vertex contacts here; single-vertex ones come from the chain dot), z = 0
 __global__ void k_gcr_init(Params P, GcrData g, const DContact* __restrict__ C, CrContacts cc,
                            const double4* __restrict__ x, ContactState cs) {
+    pdl_enter();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= P.C) return;
     const int v0 = cc.v0[c];
@@ -2433,6 +2478,7 @@ __global__ void k_gcr_init(Params P, GcrData g, const DContact* __restrict__ C, 
 // W_b = sum over the contacts on slot b of w * sum_k theta_k v_k c_k  (fixed contact order)
 __global__ void k_gcr_slot(int NS, Slots sl, CrContacts cc, const double* __restrict__ theta,
                            const double* __restrict__ v, double* __restrict__ W) {
+    pdl_enter();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= NS) return;
     double w0 = 0.0, w1 = 0.0, w2 = 0.0;
@@ -2460,6 +2506,7 @@ __global__ void k_gcr_slot(int NS, Slots sl, CrContacts cc, const double* __rest
 constexpr int kGramSmemSlots = 2000;   // 47 KB of fp64 W (static shared memory)
 
 __global__ void __launch_bounds__(256) k_gcr_gram(int NS, GcrData g, const int2* __restrict__ items) {
+    pdl_enter();
     __shared__ double Ws[3 * kGramSmemSlots];
     const int2 it = items[blockIdx.x];   // {first row (global slot), rows}
     const int a0 = it.x, nrows = it.y;
@@ -2529,6 +2576,7 @@ __global__ void __launch_bounds__(256) k_gcr_gram(int NS, GcrData g, const int2*
 // Ar_j = theta_j c_j . sum_q w_q q_{slot q} + C_j r_j; per-CTA partials of r.Ar, Ar.Ar, Ar.Ap
 __global__ void __launch_bounds__(kGcrThreads) k_gcr_row(Params P, GcrData g, const DContact* __restrict__ C,
                                                        ContactState cs, int first) {
+    pdl_enter();
     __shared__ double red[3 * (kGcrThreads / 32) + 3];
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     double s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -2569,6 +2617,7 @@ __global__ void __launch_bounds__(kGcrThreads) k_gcr_row(Params P, GcrData g, co
 // iteration `it`: [beta, p, Ap (it > 0)], breakdown test, alpha, z += alpha p, r -= alpha Ap.
 // Scalars ping-pong between sc[.. + (it & 1)] (read) and sc[.. + ((it + 1) & 1)] (written by CTA 0).
 __global__ void __launch_bounds__(kGcrThreads) k_gcr_update(GcrData g, int m, int it) {
+    pdl_enter();
     __shared__ double sh[4];
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
@@ -2627,6 +2676,7 @@ __global__ void __launch_bounds__(kGcrThreads) k_gcr_update(GcrData g, int m, in
 // lambda += z / h^2 (reading A11); |r| -> cr_res by the last CTA to finish (partials summed
 // in CTA order, so the value is deterministic)
 __global__ void __launch_bounds__(kGcrThreads) k_gcr_final(GcrData g, int m, double h, double* lam, double* cr_res) {
+    pdl_enter();
     __shared__ double red[3 * (kGcrThreads / 32) + 3];
     __shared__ bool last;
     double rr = 0.0, d1 = 0.0, d2 = 0.0;
@@ -2679,15 +2729,17 @@ int launch_gcr(cudaStream_t st, const Params& P, GcrData g, const DContact* c, C
     const int nb = gcr_row_blocks(P.C);
     const int ub = std::min(148, (m + kGcrThreads - 1) / kGcrThreads);
     g.nblk = nb;
-    k_gcr_init<<<nb, kGcrThreads, 0, st>>>(P, g, c, cc, x, cs);
+    launch_pdl(k_gcr_init, dim3(nb), dim3(kGcrThreads), 0, st, P, g, c, cc, x, cs);
     for (int it = 0; it < P.cr_iters; ++it) {
-        k_gcr_slot<<<(NS + 255) / 256, 256, 0, st>>>(NS, sl, cc, cs.theta, g.r, g.W);
-        k_gcr_gram<<<g.n_gram_items, 256, 0, st>>>(NS, g, g.gram_items);
-        k_gcr_row<<<nb, kGcrThreads, 0, st>>>(P, g, c, cs, it == 0);
-        k_gcr_update<<<ub, kGcrThreads, 0, st>>>(g, m, it);
+        launch_pdl(k_gcr_slot, dim3((NS + 255) / 256), dim3(256), 0, st, NS, sl, cc, (const double*)cs.theta,
+                   (const double*)g.r, g.W);
+        launch_pdl(k_gcr_gram, dim3(g.n_gram_items), dim3(256), 0, st, NS, g, g.gram_items);
+        launch_pdl(k_gcr_row, dim3(nb), dim3(kGcrThreads), 0, st, P, g, c, cs, (int)(it == 0));
+        launch_pdl(k_gcr_update, dim3(ub), dim3(kGcrThreads), 0, st, g, m, it);
     }
-    k_gcr_final<<<ub, kGcrThreads, 0, st>>>(g, m, P.h, cs.lam, cs.cr_res);
-    k_gcr_slot<<<(NS + 255) / 256, 256, 0, st>>>(NS, sl, cc, cs.theta, g.z, cs.wz);
+    launch_pdl(k_gcr_final, dim3(ub), dim3(kGcrThreads), 0, st, g, m, P.h, cs.lam, cs.cr_res);
+    launch_pdl(k_gcr_slot, dim3((NS + 255) / 256), dim3(256), 0, st, NS, sl, cc, (const double*)cs.theta,
+               (const double*)g.z, cs.wz);
     return (int)cudaGetLastError();
 }
 
@@ -2725,13 +2777,15 @@ int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, 
     cfg.blockDim = dim3(kCrThreads, 1, 1);
     cfg.dynamicSmemBytes = kCrMaxSmem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = csize;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     const int rpt = (3 * P.nc_max + kCrThreads - 1) / kCrThreads;
     cudaError_t e;
     switch (rpt) {
