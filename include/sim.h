@@ -104,6 +104,20 @@ typedef struct {
     double  compliance;
 } sim_contact;
 
+/* Analytic obstacle for the GPU proximity query (sim_detect_contacts; the paper's
+ * "simple proximity queries").  kind 0 plane: point a, unit normal b (the
+ * solid side is -b); kind 1 sphere: centre a, radius; kind 2 capsule: segment a-b, radius.
+ * mu: Coulomb coefficient of its contacts; velocity: rigid obstacle velocity (d_f). */
+typedef struct {
+    int32_t kind;
+    int32_t pad;
+    double  a[3];
+    double  b[3];
+    double  radius;
+    double  mu;
+    double  velocity[3];
+} sim_obstacle;
+
 typedef struct {
     int64_t n_vertices, n_free, n_tets;
     int64_t nnz_K;             /* nnz of the vertex-level K = L^-1 (stored twice: row- and column-major) */
@@ -152,6 +166,25 @@ int sim_set_contacts(sim_handle *h, int32_t instance, const sim_contact *contact
  * contacts concatenated in instance order.  All-or-nothing on error. */
 int sim_set_contacts_batch(sim_handle *h, int32_t first, int32_t count, const int32_t *counts,
                            const sim_contact *contacts);
+
+/* Proximity query on the device: for every candidate vertex (original
+ * ids, n_cand of them, e.g. the surface; pinned vertices are skipped) of `instance`, the
+ * signed distance to each obstacle surface at the current positions; the nearest obstacle
+ * wins (one contact per vertex, reading A31) and a unilateral contact is created when the
+ * distance is below `margin` (metres): normal = outward surface normal at the closest point
+ * p, offset d_n = n . p (so y = n . x - d_n is the signed distance), Gram-Schmidt tangents,
+ * the obstacle's mu and velocity.  The contacts replace the instance's set in candidate
+ * order (as sim_set_contacts); *n_found (may be NULL) receives their count.  Candidates and
+ * obstacles are borrowed for the call.  SIM_E_INVALID on bad kinds, non-unit plane normals,
+ * negative radii / margin, candidate ids out of range; SIM_E_LIMIT as sim_set_contacts. */
+/* The instance's current contact set as stored (original vertex ids, the normalised normal,
+ * the tangents in use, offset, mu, compliance; obstacle_velocity is returned as its tangential
+ * part d_f1 t1 + d_f2 t2, the only part the method uses).  *n (may be NULL) receives the
+ * count; out may be NULL to query it; SIM_E_INVALID if cap < count. */
+int sim_get_contacts(sim_handle *h, int32_t instance, sim_contact *out, int32_t capacity, int32_t *n);
+
+int sim_detect_contacts(sim_handle *h, int32_t instance, const sim_obstacle *obstacles, int32_t n_obstacles,
+                        const int32_t *candidates, int32_t n_candidates, double margin, int32_t *n_found);
 
 /* Advance `frames` frames of `iterations` local-global iterations each
  * (Alg. 4).  Pinned vertices move by h * pin_velocity per frame.  Enqueued on

@@ -18,7 +18,7 @@ EXPORTED_SYMBOLS = [
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
     "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison", "sim_get_positions_async",
-    "sim_wait_positions",
+    "sim_wait_positions", "sim_detect_contacts", "sim_get_contacts",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -72,6 +72,14 @@ def contacts_to_array(contacts):
     return a
 
 
+class SimObstacle(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("pad", C.c_int32), ("a", C.c_double * 3), ("b", C.c_double * 3),
+                ("radius", C.c_double), ("mu", C.c_double), ("velocity", C.c_double * 3)]
+
+
+OBSTACLE_PLANE, OBSTACLE_SPHERE, OBSTACLE_CAPSULE = 0, 1, 2
+
+
 class SimStats(C.Structure):
     _fields_ = [("n_vertices", C.c_int64), ("n_free", C.c_int64), ("n_tets", C.c_int64),
                 ("nnz_K", C.c_int64), ("nnz_L", C.c_int64), ("etree_height", C.c_int32),
@@ -121,6 +129,9 @@ def _load():
         "sim_debug_poison": [H, C.c_int32],
         "sim_get_positions_async": [H, C.c_void_p],
         "sim_wait_positions": [H, C.c_int32],
+        "sim_get_contacts": [H, C.c_int32, C.POINTER(SimContact), C.c_int32, C.POINTER(C.c_int32)],
+        "sim_detect_contacts": [H, C.c_int32, C.POINTER(SimObstacle), C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                                C.c_double, C.POINTER(C.c_int32)],
         "sim_get_kernel_times": [H, dp, C.c_int32],
         "sim_debug_contact_state": [H, C.c_int32, dp, dp, dp, dp, ip, dp],
         "sim_debug_cr_timeline": [H, dp],
@@ -290,6 +301,37 @@ class Sim:
 
     def wait_positions(self, block_host: bool = True):
         _check(lib.sim_wait_positions(self._h, 1 if block_host else 0))
+
+    def detect_contacts(self, obstacles, candidates, margin, instance=0):
+        """GPU proximity query (sim_detect_contacts).  obstacles: list of dicts with kind
+        (0 plane, 1 sphere, 2 capsule), a, b, radius, mu, velocity; candidates: original
+        vertex ids.  Replaces the instance's contact set; returns the contact count."""
+        arr = (SimObstacle * max(1, len(obstacles)))()
+        for i, o in enumerate(obstacles):
+            arr[i].kind = int(o["kind"])
+            for k in range(3):
+                arr[i].a[k] = float(o.get("a", (0, 0, 0))[k])
+                arr[i].b[k] = float(o.get("b", (0, 0, 0))[k])
+                arr[i].velocity[k] = float(o.get("velocity", (0, 0, 0))[k])
+            arr[i].radius = float(o.get("radius", 0.0))
+            arr[i].mu = float(o.get("mu", 0.0))
+        cand = np.ascontiguousarray(candidates, dtype=np.int32)
+        nf = C.c_int32(0)
+        _check(lib.sim_detect_contacts(self._h, int(instance), arr, len(obstacles),
+                                       cand.ctypes.data_as(C.POINTER(C.c_int32)), int(cand.size), float(margin),
+                                       C.byref(nf)))
+        self._nc[instance] = nf.value
+        self._contacts[instance] = None
+        return nf.value
+
+    def get_contacts(self, instance=0):
+        """The stored contact set of an instance as a CONTACT_DTYPE array (sim_get_contacts)."""
+        n = C.c_int32(0)
+        _check(lib.sim_get_contacts(self._h, int(instance), None, 0, C.byref(n)))
+        arr = np.zeros(max(1, n.value), CONTACT_DTYPE)
+        _check(lib.sim_get_contacts(self._h, int(instance), arr.ctypes.data_as(C.POINTER(SimContact)),
+                                    int(arr.size), C.byref(n)))
+        return arr[:n.value]
 
     def get_lambda(self, instance=0):
         nc = self._nc[instance]

@@ -659,6 +659,112 @@ extern "C" int sim_set_contacts(sim_handle* H, int32_t instance, const sim_conta
     return SIM_OK;
 }
 
+static Params make_params(const sim_handle* H);
+
+extern "C" int sim_detect_contacts(sim_handle* H, int32_t inst, const sim_obstacle* obs, int32_t nobs,
+                                   const int32_t* cand, int32_t ncand, double margin, int32_t* n_found) {
+    int rc = check_contact_call(H);
+    if (rc) return rc;
+    if (inst < 0 || inst >= H->S) return fail(SIM_E_INVALID, "instance %d out of range [0, %d)", inst, H->S);
+    if (nobs < 0 || ncand < 0 || (nobs > 0 && !obs) || (ncand > 0 && !cand))
+        return fail(SIM_E_INVALID, "bad obstacle or candidate arrays");
+    if (!(margin >= 0) || !std::isfinite(margin)) return fail(SIM_E_INVALID, "margin must be >= 0");
+    std::vector<DObstacle> dob(nobs);
+    for (int o = 0; o < nobs; ++o) {
+        const sim_obstacle& q = obs[o];
+        if (q.kind < 0 || q.kind > 2) return fail(SIM_E_INVALID, "obstacle %d: kind must be 0, 1 or 2", o);
+        if (!(q.radius >= 0) || !(q.mu >= 0)) return fail(SIM_E_INVALID, "obstacle %d: radius and mu must be >= 0", o);
+        if (q.kind == 0) {
+            const double nn = std::sqrt(q.b[0] * q.b[0] + q.b[1] * q.b[1] + q.b[2] * q.b[2]);
+            if (!(std::fabs(nn - 1.0) < 1e-6)) return fail(SIM_E_INVALID, "obstacle %d: plane normal not unit", o);
+        }
+        DObstacle& d = dob[o];
+        d.kind = q.kind;
+        d.pad = 0;
+        for (int k = 0; k < 3; ++k) { d.a[k] = q.a[k]; d.b[k] = q.b[k]; d.v[k] = q.velocity[k]; }
+        d.radius = q.radius;
+        d.mu = q.mu;
+    }
+    std::vector<int32_t> ci;   // internal ids of the free candidates, candidate order
+    std::vector<int32_t> co;
+    for (int c = 0; c < ncand; ++c) {
+        if (cand[c] < 0 || cand[c] >= H->n_v) return fail(SIM_E_INVALID, "candidate %d out of range", c);
+        if (H->fixed[cand[c]]) continue;
+        ci.push_back(H->orig2int[cand[c]]);
+        co.push_back(cand[c]);
+    }
+    const int nc = (int)ci.size();
+    DBuf<DObstacle> dobs;
+    DBuf<int32_t> dci;
+    DBuf<int> dbest;
+    DBuf<double> dgap;
+    DBuf<double3> dn, dp;
+    CK(dobs.alloc(std::max(nobs, 1))); CK(dci.alloc(std::max(nc, 1))); CK(dbest.alloc(std::max(nc, 1)));
+    CK(dgap.alloc(std::max(nc, 1))); CK(dn.alloc(std::max(nc, 1))); CK(dp.alloc(std::max(nc, 1)));
+    cudaStream_t st = H->stream;
+    CK(dobs.upload(dob.data(), nobs, st));
+    CK(dci.upload(ci.data(), nc, st));
+    launch_proximity(st, make_params(H), H->x.p, inst, dci.p, nc, dobs.p, nobs, margin, dbest.p, dgap.p, dn.p, dp.p);
+    CK(cudaGetLastError());
+    std::vector<int> best(nc);
+    std::vector<double3> hn(nc), hp(nc);
+    CK(cudaStreamSynchronize(st));
+    if (nc) {
+        CK(cudaMemcpy(best.data(), dbest.p, nc * sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hn.data(), dn.p, nc * sizeof(double3), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(hp.data(), dp.p, nc * sizeof(double3), cudaMemcpyDeviceToHost));
+    }
+    std::vector<sim_contact> cs;
+    for (int c = 0; c < nc; ++c) {
+        if (best[c] < 0) continue;
+        const DObstacle& o = dob[best[c]];
+        sim_contact k;
+        memset(&k, 0, sizeof k);
+        k.kind = 0;
+        k.n_verts = 1;
+        k.verts[0] = co[c];
+        k.weights[0] = 1.0;
+        const double n[3] = {hn[c].x, hn[c].y, hn[c].z}, p[3] = {hp[c].x, hp[c].y, hp[c].z};
+        for (int d = 0; d < 3; ++d) { k.normal[d] = n[d]; k.obstacle_velocity[d] = o.v[d]; }
+        k.offset = n[0] * p[0] + n[1] * p[1] + n[2] * p[2];
+        k.mu = o.mu;
+        cs.push_back(k);
+    }
+    rc = sim_set_contacts(H, inst, cs.data(), (int32_t)cs.size());
+    if (rc) return rc;
+    if (n_found) *n_found = (int32_t)cs.size();
+    return SIM_OK;
+}
+
+extern "C" int sim_get_contacts(sim_handle* H, int32_t inst, sim_contact* out, int32_t cap, int32_t* n) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (inst < 0 || inst >= H->S) return fail(SIM_E_INVALID, "instance %d out of range [0, %d)", inst, H->S);
+    const InstContacts& I = H->ic[inst];
+    const int nc = (int)I.hc.size();
+    if (n) *n = nc;
+    if (!out) return SIM_OK;
+    if (cap < nc) return fail(SIM_E_INVALID, "capacity %d < %d contacts", cap, nc);
+    for (int c = 0; c < nc; ++c) {
+        const DContact& d = I.hc[c];
+        sim_contact& k = out[c];
+        memset(&k, 0, sizeof k);
+        k.kind = d.kind;
+        k.n_verts = d.nv;
+        for (int q = 0; q < d.nv; ++q) { k.verts[q] = H->int2orig[d.vtx[q]]; k.weights[q] = d.w[q]; }
+        for (int e = 0; e < 3; ++e) {
+            k.normal[e] = d.c[0][e];
+            k.tangent1[e] = d.c[1][e];
+            k.tangent2[e] = d.c[2][e];
+        }
+        k.offset = d.dn;
+        k.mu = d.mu;
+        k.compliance = d.e;
+        // obstacle velocity is stored as its tangential projections d_f = t . v only
+        for (int e = 0; e < 3; ++e) k.obstacle_velocity[e] = d.df1 * d.c[1][e] + d.df2 * d.c[2][e];
+    }
+    return SIM_OK;
+}
+
 extern "C" int sim_set_contacts_batch(sim_handle* H, int32_t first, int32_t count, const int32_t* counts,
                                       const sim_contact* cs) {
     int rc = check_contact_call(H);

@@ -136,6 +136,61 @@ void launch_pack_positions(cudaStream_t st, const double4* x, const int32_t* o2i
     if (n) k_pack_positions<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, o2i, n_v, S, dst);
 }
 
+// ----------------------------------------------------------------------------
+// proximity query ("simple proximity queries"): signed distance of each
+// candidate vertex to analytic obstacle surfaces; nearest obstacle wins (reading A31)
+// ----------------------------------------------------------------------------
+__global__ void k_proximity(Params P, const double4* __restrict__ x, int inst, const int32_t* __restrict__ cand,
+                            int ncand, const DObstacle* __restrict__ obs, int nobs, double margin,
+                            int* __restrict__ best, double* __restrict__ gapo, double3* __restrict__ no,
+                            double3* __restrict__ pto) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncand) return;
+    const double4 xa = x[(size_t)cand[c] * P.S + inst];
+    int bi = -1;
+    double bg = 0.0, bn[3] = {0, 0, 0}, bp[3] = {0, 0, 0};
+    for (int o = 0; o < nobs; ++o) {
+        const DObstacle& ob = obs[o];
+        double q[3], n[3], g;
+        const double p[3] = {xa.x, xa.y, xa.z};
+        if (ob.kind == 0) {   // plane through a with unit normal b
+            g = (p[0] - ob.a[0]) * ob.b[0] + (p[1] - ob.a[1]) * ob.b[1] + (p[2] - ob.a[2]) * ob.b[2];
+            for (int k = 0; k < 3; ++k) { n[k] = ob.b[k]; q[k] = p[k] - g * ob.b[k]; }
+        } else {              // sphere (centre a) or capsule (segment a-b): distance to the core point
+            double cpt[3] = {ob.a[0], ob.a[1], ob.a[2]};
+            if (ob.kind == 2) {
+                const double d[3] = {ob.b[0] - ob.a[0], ob.b[1] - ob.a[1], ob.b[2] - ob.a[2]};
+                const double dd = d[0] * d[0] + d[1] * d[1] + d[2] * d[2];
+                double t = dd > 0.0 ? ((p[0] - ob.a[0]) * d[0] + (p[1] - ob.a[1]) * d[1] + (p[2] - ob.a[2]) * d[2]) / dd
+                                    : 0.0;
+                t = fmin(fmax(t, 0.0), 1.0);
+                for (int k = 0; k < 3; ++k) cpt[k] = ob.a[k] + t * d[k];
+            }
+            const double v[3] = {p[0] - cpt[0], p[1] - cpt[1], p[2] - cpt[2]};
+            const double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+            if (!(dist > 0.0)) continue;   // on the core: no defined normal
+            for (int k = 0; k < 3; ++k) n[k] = v[k] / dist;
+            g = dist - ob.radius;
+            for (int k = 0; k < 3; ++k) q[k] = cpt[k] + ob.radius * n[k];
+        }
+        if (g < margin && (bi < 0 || g < bg)) {
+            bi = o;
+            bg = g;
+            for (int k = 0; k < 3; ++k) { bn[k] = n[k]; bp[k] = q[k]; }
+        }
+    }
+    best[c] = bi;
+    gapo[c] = bg;
+    no[c] = make_double3(bn[0], bn[1], bn[2]);
+    pto[c] = make_double3(bp[0], bp[1], bp[2]);
+}
+
+void launch_proximity(cudaStream_t st, const Params& P, const double4* x, int inst, const int32_t* cand, int ncand,
+                      const DObstacle* obs, int nobs, double margin, int* best, double* gap, double3* n, double3* pt) {
+    if (ncand > 0)
+        k_proximity<<<(ncand + 127) / 128, 128, 0, st>>>(P, x, inst, cand, ncand, obs, nobs, margin, best, gap, n, pt);
+}
+
 void launch_finite_guard(cudaStream_t st, int n_v, int S, double4* x, double4* v, const double4* xt,
                          const double4* vt, int* bad, int* rollbacks) {
     const int blocks = (int)(((size_t)n_v * S + 255) / 256);

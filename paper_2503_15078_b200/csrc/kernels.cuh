@@ -164,6 +164,16 @@ void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off,
                     const int4* ulist, const float* Zc, const double* wz, const float4* wzT, float4* y, int nitems,
                     const int2* items);
 
+// --- proximity query ------------------------------------------------------------------
+struct DObstacle {   // device copy of sim_obstacle
+    int kind, pad;
+    double a[3], b[3], radius, mu, v[3];
+};
+// per candidate c (internal vertex cand[c] of instance inst): best[c] = index of the nearest
+// obstacle within margin or -1, with its outward normal n[c] and closest surface point p[c]
+void launch_proximity(cudaStream_t st, const Params& P, const double4* x, int inst, const int32_t* cand, int ncand,
+                      const DObstacle* obs, int nobs, double margin, int* best, double* gap, double3* n, double3* pt);
+
 // --- per-contact-set kernels (all instances at once) ----------------------------
 void launch_delassus(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
                      const int64_t* colptr, const int32_t* depth, const int32_t* parent, const int32_t* ptop,

@@ -99,6 +99,8 @@ class Scene:
     contacts: List[Contact]
     pin_velocity: np.ndarray           # [3] m/s applied to all fixed vertices
     v0: Optional[np.ndarray] = None    # [n_v,3] initial velocity
+    obstacles: Optional[list] = None   # analytic obstacles the contacts were generated from:
+                                       # dicts kind (0 plane, 1 sphere, 2 capsule), a, b, radius, mu
 
 
 # --------------------------------------------------------------------------
@@ -216,7 +218,8 @@ def incline_block(theta_deg: float = 10.0, mu: float = 0.5, nv: int = 10,
     contacts = [Contact([int(v)], [1.0], n.copy(), 0.0, mu=mu, tangent1=t1, tangent2=t2)
                 for v in bottom]
     mat = Material(model=NEOHOOKEAN, density=1000.0, youngs=youngs, poisson=0.3)
-    return Scene("incline", mesh, mat, 0.01, 5, contacts, np.zeros(3))
+    plane = {"kind": 0, "a": np.zeros(3), "b": n.copy(), "radius": 0.0, "mu": mu}
+    return Scene("incline", mesh, mat, 0.01, 5, contacts, np.zeros(3), obstacles=[plane])
 
 
 # --------------------------------------------------------------------------
@@ -297,7 +300,8 @@ def gingerbread(scale: float = 0.79, layers: int = 6, cell_m: float = 0.005,
         contacts.append(Contact([int(bottom[i])], [1.0], n.copy(), float(best_d[i]), mu=mu,
                                 tangent1=t1, tangent2=t2))
     mat = Material(model=NEOHOOKEAN, density=1000.0, youngs=youngs, poisson=0.3)
-    return Scene("gingerbread", mesh, mat, 0.01, 5, contacts, np.array([0.0, 0.5, 0.0]))
+    obst = [{"kind": 2, "a": a, "b": c, "radius": r, "mu": mu} for (a, c, r) in bars]
+    return Scene("gingerbread", mesh, mat, 0.01, 5, contacts, np.array([0.0, 0.5, 0.0]), obstacles=obst)
 
 
 # --------------------------------------------------------------------------
