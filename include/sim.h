@@ -134,6 +134,8 @@ typedef struct {
     int64_t h2d_contact_bytes; /* host->device bytes of the last contact commit                          */
     int32_t n_instances;
     int64_t nonfinite_rollbacks; /* instance-frames rolled back to x_t, v_t (non-finite x or v), total    */
+    int64_t gram_rows_computed;  /* last contact commit: Delassus Gram rows computed ...                  */
+    int64_t gram_rows_reused;    /* ... and rows copied from the previous commit (sim_set_schur_reuse)    */
 } sim_stats;
 
 /* Validate the mesh and material, compute rest data (Dm^-1, volumes, lumped
@@ -266,6 +268,14 @@ int sim_set_admm(sim_handle *h, int32_t on);
  * TMEM accumulators; default), 1 = CUDA-core FP32 FMAs.  Same K and operands; results agree
  * to fp32 rounding.  n_instances == 1 always uses the HBM-streaming SpMV kernels. */
 int sim_set_kpass_mode(sim_handle *h, int32_t mode);
+
+/* Delassus reuse across contact commits (the "reuse strategy ... to exploit shared contact data
+ * between consecutive time steps" the paper implements, P:L863 / P:L1016): G[a][b] depends only
+ * on the vertex pair, so entries of pairs already in the previous commit of the instance's
+ * class are copied and only the rows of new contact vertices are computed (same fp32
+ * accumulation order: bitwise the full recomputation).  Off by default (reading A23: the bench
+ * recomputes D at every commit).  Cluster-CR scenes only; the grid CR always recomputes. */
+int sim_set_schur_reuse(sim_handle *h, int32_t on);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 
 void sim_destroy(sim_handle *h);         /* NULL-safe */

@@ -19,6 +19,7 @@ EXPORTED_SYMBOLS = [
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
     "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison", "sim_get_positions_async",
     "sim_wait_positions", "sim_detect_contacts", "sim_get_contacts",
+    "sim_set_schur_reuse",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -88,7 +89,8 @@ class SimStats(C.Structure):
                 ("n_active", C.c_int32), ("n_stick", C.c_int32), ("n_slip", C.c_int32),
                 ("kernels_per_frame", C.c_int32), ("build_seconds", C.c_double),
                 ("h2d_contact_bytes", C.c_int64), ("n_instances", C.c_int32),
-                ("nonfinite_rollbacks", C.c_int64)]
+                ("nonfinite_rollbacks", C.c_int64), ("gram_rows_computed", C.c_int64),
+                ("gram_rows_reused", C.c_int64)]
 
 
 class SimError(RuntimeError):
@@ -129,6 +131,7 @@ def _load():
         "sim_debug_poison": [H, C.c_int32],
         "sim_get_positions_async": [H, C.c_void_p],
         "sim_wait_positions": [H, C.c_int32],
+        "sim_set_schur_reuse": [H, C.c_int32],
         "sim_get_contacts": [H, C.c_int32, C.POINTER(SimContact), C.c_int32, C.POINTER(C.c_int32)],
         "sim_detect_contacts": [H, C.c_int32, C.POINTER(SimObstacle), C.c_int32, C.POINTER(C.c_int32), C.c_int32,
                                 C.c_double, C.POINTER(C.c_int32)],
@@ -367,6 +370,10 @@ class Sim:
         """Inject a NaN into the next frame of `instance` (sim_debug_poison)."""
         _check(lib.sim_debug_poison(self._h, int(instance)))
 
+    def set_schur_reuse(self, on: bool = True):
+        """Delassus Gram reuse across contact commits (sim_set_schur_reuse)."""
+        _check(lib.sim_set_schur_reuse(self._h, 1 if on else 0))
+
     def set_profiling(self, on: bool):
         _check(lib.sim_set_profiling(self._h, 1 if on else 0))
 
@@ -408,10 +415,9 @@ class Sim:
         return P, r
 
     def _ns(self, instance):
-        cl = self._contacts[instance]
-        if cl is None:
-            raise ValueError("contact list of this instance unknown (set from a packed array)")
-        return len({int(v) for c in cl for v in c.verts})
+        """Distinct contact vertices of an instance (from the stored set, sim_get_contacts)."""
+        arr = self.get_contacts(instance)
+        return len({int(v) for r in arr for v in r["verts"][:int(r["n_verts"])]})
 
     def debug_delassus(self, instance=0):
         ns = self._ns(instance)

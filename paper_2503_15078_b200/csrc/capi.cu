@@ -170,6 +170,17 @@ struct sim_handle {
     int NCL = 0, CS = 0, cm_max = 0, n_it_cd = 0, n_it_sc = 0;
     std::vector<int64_t> gaoff_h;
     DBuf<float> G, GA;   // Delassus Gram blocks and the CR's active blocks (fp32-exact values)
+    // Gram reuse across commits (sim_set_schur_reuse): the previous commit's class blocks
+    bool schur_reuse = false, have_prev = false;
+    std::vector<std::vector<int32_t>> prev_cls_verts;
+    std::vector<int64_t> prev_goff;
+    std::vector<int> prev_cls_of_inst;
+    int64_t prev_gsize = 0;
+    DBuf<float> Gprev;
+    int64_t gram_rows_computed = 0, gram_rows_reused = 0;   // statistics of the last commit
+    DPtr<int> rmap, pns;
+    DPtr<int64_t> pgoff;
+    DPtr<int2> newslots;
     DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res, rho;
     DBuf<int> act_na, act_idx, act_pos, act_con;   // CR active set (k_active)
     DBuf<float4> wzT;
@@ -885,6 +896,34 @@ static int commit_contacts(sim_handle* H) {
         }
     }
     const int NG = (int)gcs.size() - 1;
+    // Gram reuse: every class maps to the previous class of its representative instance
+    bool reuse = H->schur_reuse && !grid && H->have_prev && (int)H->prev_cls_of_inst.size() == S;
+    std::vector<int> rmap_h, pns_h(NCL, 0);
+    std::vector<int64_t> pgoff_h(NCL, 0);
+    std::vector<int2> news_h;
+    if (reuse) {
+        for (int k = 0; k < NCL && reuse; ++k) {
+            const int ko = H->prev_cls_of_inst[rep[k]];
+            if (ko < 0 || ko >= (int)H->prev_cls_verts.size()) { reuse = false; break; }
+            const std::vector<int32_t>& vo = H->prev_cls_verts[ko];
+            const std::vector<int32_t>& vn = H->ic[rep[k]].verts;
+            size_t q = 0;
+            for (size_t sidx = 0; sidx < vn.size(); ++sidx) {   // both lists ascending
+                while (q < vo.size() && vo[q] < vn[sidx]) ++q;
+                const int m = (q < vo.size() && vo[q] == vn[sidx]) ? (int)q : -1;
+                rmap_h.push_back(m);
+                if (m < 0) news_h.push_back(make_int2(k, (int)sidx));
+            }
+            pgoff_h[k] = H->prev_goff[ko];
+            pns_h[k] = (int)vo.size();
+        }
+        if (!reuse) { rmap_h.clear(); news_h.clear(); }
+    }
+    if (reuse) {   // keep the previous blocks: G may be reallocated below
+        bool g2 = false;
+        CK(H->Gprev.ensure(std::max<int64_t>(H->prev_gsize, 1), g2));
+        if (H->prev_gsize) CK(cudaMemcpyAsync(H->Gprev.p, H->G.p, H->prev_gsize * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    }
     std::vector<int> cmoff(NCL + 1, 0), cmem(S);
     for (int i = 0; i < S; ++i) cmoff[cls[i] + 1]++;
     for (int k = 0; k < NCL; ++k) cmoff[k + 1] += cmoff[k];
@@ -970,6 +1009,8 @@ static int commit_contacts(sim_handle* H) {
               g_zo = seg(8 * C1), g_cmo = seg(4 * C1), g_cm = seg(4 * (size_t)S), g_icd = seg(8 * it_cd.size()),
               g_isc = seg(8 * it_sc.size());
     const size_t NSg = grid ? (size_t)NSt : 0;
+    const Seg g_rm = seg(4 * rmap_h.size()), g_pg = seg(8 * pgoff_h.size()), g_pn = seg(4 * pns_h.size()),
+              g_nw = seg(8 * news_h.size());
     std::vector<int2> gitems;   // Gram matvec items: 32 consecutive rows of one group
     for (int g = 0; grid && g < NG; ++g)
         for (int q = gcs[g]; q < gcs[g + 1]; q += 32) gitems.push_back(make_int2(q, std::min(32, gcs[g + 1] - q)));
@@ -981,7 +1022,8 @@ static int commit_contacts(sim_handle* H) {
         const std::vector<size_t> lay = {g_dc.at, g_c9.at, g_s0.at, g_v0.at, g_c1.at, g_sv.at, g_si.at, g_scp.at,
                                          g_sci.at, g_scw.at, g_ch.at, g_cv.at, g_cc.at, g_co.at, g_so.at, g_ga.at,
                                          g_cl.at, g_cso.at, g_go.at, g_uo.at, g_zo.at, g_cmo.at, g_cm.at, g_icd.at,
-                                         g_isc.at, g_gcs.at, g_ggo.at, g_grw.at, g_gs0.at, g_gn.at, g_git.at};
+                                         g_isc.at, g_gcs.at, g_ggo.at, g_grw.at, g_gs0.at, g_gn.at, g_git.at,
+                                         g_rm.at, g_pg.at, g_pn.at, g_nw.at};
         if (grew || lay != H->arena_layout) H->contact_gen++;
         H->arena_layout = lay;
     }
@@ -1000,6 +1042,8 @@ static int commit_contacts(sim_handle* H) {
         H->gcsoff.p = (int*)(A + g_gcs.at); H->ggoff.p = (int64_t*)(A + g_ggo.at);
         H->growoff.p = (int64_t*)(A + g_grw.at); H->gs0.p = (int*)(A + g_gs0.at); H->gn.p = (int*)(A + g_gn.at);
         H->g_items.p = (int2*)(A + g_git.at);
+        H->rmap.p = (int*)(A + g_rm.at); H->pgoff.p = (int64_t*)(A + g_pg.at); H->pns.p = (int*)(A + g_pn.at);
+        H->newslots.p = (int2*)(A + g_nw.at);
     }
     if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
     CK(cudaEventSynchronize(H->stage_free));   // the previous commit's copies are done
@@ -1074,6 +1118,10 @@ static int commit_contacts(sim_handle* H) {
     if (!it_sc.empty()) memcpy(B + g_isc.at, it_sc.data(), 8 * it_sc.size());
     memcpy(B + g_gcs.at, gcs.data(), 4 * gcs.size());
     if (!gitems.empty()) memcpy(B + g_git.at, gitems.data(), 8 * gitems.size());
+    if (!rmap_h.empty()) memcpy(B + g_rm.at, rmap_h.data(), 4 * rmap_h.size());
+    if (!pgoff_h.empty()) memcpy(B + g_pg.at, pgoff_h.data(), 8 * pgoff_h.size());
+    if (!pns_h.empty()) memcpy(B + g_pn.at, pns_h.data(), 4 * pns_h.size());
+    if (!news_h.empty()) memcpy(B + g_nw.at, news_h.data(), 8 * news_h.size());
     H->n_g_items = (int)gitems.size();
     memcpy(B + g_ggo.at, ggo.data(), 8 * ggo.size());
     if (grid) {
@@ -1127,9 +1175,22 @@ static int commit_contacts(sim_handle* H) {
         launch_delassus(st, Pg, og, csl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
         launch_djj_grid(st, P, H->dc.p, gcr_data(H));
     } else {
-        launch_delassus(st, P, off, csl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
+        if (reuse)
+            launch_gram_reuse(st, P, off, csl.vtx, H->rmap.p, H->pgoff.p, H->pns.p, H->Gprev.p, H->newslots.p,
+                              (int)news_h.size(), H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
+        else
+            launch_delassus(st, P, off, csl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
         launch_djj(st, P, off, H->dc.p, H->G.p);
     }
+    H->gram_rows_computed = reuse ? (int64_t)news_h.size() : CSt;
+    H->gram_rows_reused = reuse ? (int64_t)CSt - (int64_t)news_h.size() : 0;
+    // remember this commit's blocks for the next one
+    H->have_prev = !grid;
+    H->prev_cls_verts.assign(NCL, {});
+    for (int k = 0; k < NCL; ++k) H->prev_cls_verts[k] = H->ic[rep[k]].verts;
+    H->prev_goff.assign(goff.begin(), goff.end() - 1);
+    H->prev_cls_of_inst = cls;
+    H->prev_gsize = goff[NCL];
     CK(cudaGetLastError());
     H->dirty = false;
     return SIM_OK;   // asynchronous: the copies and kernels are ordered on the handle's stream
@@ -1272,6 +1333,13 @@ extern "C" int sim_debug_poison(sim_handle* H, int32_t inst) {
     int rc = check_instance(H, inst);
     if (rc) return rc;
     H->poison_inst = inst;
+    return SIM_OK;
+}
+
+extern "C" int sim_set_schur_reuse(sim_handle* H, int32_t on) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (on != 0 && on != 1) return fail(SIM_E_INVALID, "flag must be 0 or 1");
+    H->schur_reuse = on != 0;
     return SIM_OK;
 }
 
@@ -1573,6 +1641,8 @@ extern "C" int sim_get_stats(sim_handle* H, sim_stats* o) {
     o->build_seconds = H->build_seconds;
     o->h2d_contact_bytes = H->h2d_contact_bytes;
     o->nonfinite_rollbacks = H->rollbacks_total;
+    o->gram_rows_computed = H->gram_rows_computed;
+    o->gram_rows_reused = H->gram_rows_reused;
     if (!H->host_only && H->rollbacks.p) {
         int n = 0;
         CK(cudaStreamSynchronize(H->stream));

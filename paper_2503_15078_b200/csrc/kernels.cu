@@ -2014,6 +2014,71 @@ void launch_delassus(cudaStream_t st, const Params& P, InstOff off, ClassSlots c
     k_delassus<<<dim3(ntri, P.NCL), 256, 0, st>>>(off, csl.vtx, Kcol, colptr, depth, parent, ptop, G);
 }
 
+// ----------------------------------------------------------------------------
+// Gram reuse across commits ("reuse strategy ... to exploit shared contact data between
+// consecutive time steps"): G[a][b] depends only on the vertex pair, so the
+// entries of vertex pairs present in the previous contact set are copied and only the rows of
+// new contact vertices are computed -- with the same fp32 accumulation order as k_delassus,
+// so the result is bitwise the full recomputation.
+//   rmap[class slot] = slot of the same vertex in the previous block of the class, or -1
+// ----------------------------------------------------------------------------
+__global__ void k_gram_copy(InstOff off, const int* __restrict__ rmap, const int64_t* __restrict__ pgoff,
+                            const int* __restrict__ pns, const float* __restrict__ Gprev, float* __restrict__ G) {
+    const int cl = blockIdx.y;
+    const int sb = off.csoff[cl], ns = off.csoff[cl + 1] - sb;
+    const int nso = pns[cl];
+    float* Gc = G + off.goff[cl];
+    const float* Go = Gprev + pgoff[cl];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ns * ns; e += gridDim.x * blockDim.x) {
+        const int sa = e / ns, tb = e - sa * ns;
+        const int ma = rmap[sb + sa], mb = rmap[sb + tb];
+        if (ma >= 0 && mb >= 0) Gc[e] = Go[(size_t)ma * nso + mb];
+    }
+}
+
+// rows (and columns) of the new slots: one warp per (new slot, 32 partner slots), lane = partner
+__global__ void k_gram_rows(InstOff off, const int32_t* __restrict__ vtx_all, const int* __restrict__ rmap,
+                            const int2* __restrict__ newslots, int nnew, const float* __restrict__ Kcol,
+                            const int64_t* __restrict__ colptr, const int32_t* __restrict__ depth,
+                            const int32_t* __restrict__ parent, const int32_t* __restrict__ ptop, float* __restrict__ G) {
+    const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int ni = wg / 32, chunk = wg % 32;   // up to 32 chunks of 32 partners per new slot
+    if (ni >= nnew) return;
+    const int2 ns_ = newslots[ni];             // {class, class-local slot}
+    const int cl = ns_.x, s = ns_.y;
+    const int sb = off.csoff[cl], ns = off.csoff[cl + 1] - sb;
+    float* Gc = G + off.goff[cl];
+    const int a = vtx_all[sb + s];
+    const float* ca = Kcol + colptr[a] + depth[a];   // K at depth d: ca[-d]
+    for (int t = 32 * chunk + lane; t < ns; t += 32 * 32) {
+        // pairs with an older partner of lower index are owned by this row; two new slots: the
+        // lower one writes (keeps one writer per entry)
+        if (rmap[sb + t] < 0 && t < s) continue;
+        const int b = vtx_all[sb + t];
+        const int dl = lca_depth(a, b, parent, ptop, depth);
+        const float* cb = Kcol + colptr[b] + depth[b];
+        float acc = 0.f;
+        for (int d = 0; d <= dl; ++d) acc = fmaf(__ldg(ca - d), __ldg(cb - d), acc);
+        Gc[(size_t)s * ns + t] = acc;
+        Gc[(size_t)t * ns + s] = acc;
+    }
+}
+
+void launch_gram_reuse(cudaStream_t st, const Params& P, InstOff off, const int32_t* vtx_all, const int* rmap,
+                       const int64_t* pgoff, const int* pns, const float* Gprev, const int2* newslots, int nnew,
+                       const float* Kcol, const int64_t* colptr, const int32_t* depth, const int32_t* parent,
+                       const int32_t* ptop, float* G) {
+    if (P.CS == 0) return;
+    const int gx = std::max(1, std::min(64, (P.ns_max * P.ns_max + 255) / 256));
+    k_gram_copy<<<dim3(gx, P.NCL), 256, 0, st>>>(off, rmap, pgoff, pns, Gprev, G);
+    if (nnew > 0) {
+        const int warps = nnew * 32;
+        k_gram_rows<<<(warps + 7) / 8, 256, 0, st>>>(off, vtx_all, rmap, newslots, nnew, Kcol, colptr, depth, parent,
+                                                     ptop, G);
+    }
+}
+
 // D_jj = sum_{a,b in j} w_a w_b G_ab (unit directions; reading A18)
 __global__ void k_djj(int C, InstOff off, DContact* Cs, const float* __restrict__ G) {
     int c = blockIdx.x * blockDim.x + threadIdx.x;

@@ -179,6 +179,12 @@ void launch_delassus(cudaStream_t st, const Params& P, InstOff off, ClassSlots c
                      const int64_t* colptr, const int32_t* depth, const int32_t* parent, const int32_t* ptop,
                      float* G);
 void launch_djj(cudaStream_t st, const Params& P, InstOff off, DContact* c, const float* G);
+// Gram reuse: copy entries of vertex pairs from the previous blocks (rmap, pgoff, pns), compute
+// the rows of the new slots (newslots: {class, class-local slot}); bitwise = launch_delassus
+void launch_gram_reuse(cudaStream_t st, const Params& P, InstOff off, const int32_t* vtx_all, const int* rmap,
+                       const int64_t* pgoff, const int* pns, const float* Gprev, const int2* newslots, int nnew,
+                       const float* Kcol, const int64_t* colptr, const int32_t* depth, const int32_t* parent,
+                       const int32_t* ptop, float* G);
 // ancestor-chain rows of every class slot (chain order = Kcol order); flags rows per class
 // (flag[c * n_f + row]); slotmap[vtx * S + inst] = instance slot
 void launch_chain_rows(cudaStream_t st, const Params& P, ClassSlots csl, Slots sl, const int32_t* chain_off,

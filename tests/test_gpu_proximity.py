@@ -118,3 +118,36 @@ def test_closed_loop_incline(simmod):
         xo, _, _ = o.frame(x, v)
         assert np.abs(xg - xo).max() < tol, (f, np.abs(xg - xo).max())
         x, v = xg, vg
+
+
+def test_schur_reuse_is_bitwise_recompute(simmod):
+    """Delassus reuse across commits (include/sim.h sim_set_schur_reuse): a
+    block dropping onto a capsule detects its contacts every frame (the set grows and shifts);
+    the handle that copies the Gram entries of known vertex pairs and computes only new rows
+    produces the same G (bitwise) and the same frames (bitwise) as the one recomputing."""
+    sc = scenes.make_scene("block", nv=7, pinned=False)
+    X = sc.mesh.X
+    obst = [{"kind": 2, "a": (-0.02, 0.06, -0.006), "b": (0.14, 0.05, -0.004), "radius": 0.005, "mu": 0.4},
+            {"kind": 0, "a": (0, 0, -0.03), "b": (0, 0, 1.0), "mu": 0.4}]
+    cand = np.arange(sc.mesh.n_v)
+    hs = []
+    for reuse in (False, True):
+        s = simmod.Sim(X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+        s.set_schur_reuse(reuse)
+        hs.append(s)
+    reused_any = False
+    for f in range(12):
+        counts = [s.detect_contacts(obst, cand, 4e-3) for s in hs]
+        assert counts[0] == counts[1]
+        if counts[0]:
+            cv0, G0 = hs[0].debug_delassus()
+            cv1, G1 = hs[1].debug_delassus()
+            assert np.array_equal(cv0, cv1) and np.array_equal(G0, G1), f
+            st = hs[1].stats()
+            reused_any |= st["gram_rows_reused"] > 0 and st["gram_rows_computed"] < st["n_contact_vertices"]
+        for s in hs:
+            s.step(1, 5)
+        x0, v0 = hs[0].get_state()
+        x1, v1 = hs[1].get_state()
+        assert np.array_equal(x0, x1) and np.array_equal(v0, v1), f
+    assert reused_any
