@@ -136,6 +136,7 @@ typedef struct {
     int64_t nonfinite_rollbacks; /* instance-frames rolled back to x_t, v_t (non-finite x or v), total    */
     int64_t gram_rows_computed;  /* last contact commit: Delassus Gram rows computed ...                  */
     int64_t gram_rows_reused;    /* ... and rows copied from the previous commit (sim_set_schur_reuse)    */
+    double  build_phase_seconds[5]; /* precompute: assemble A_v, ordering, Cholesky, K = L^-1, tile layouts  */
 } sim_stats;
 
 /* Validate the mesh and material, compute rest data (Dm^-1, volumes, lumped

@@ -90,7 +90,7 @@ class SimStats(C.Structure):
                 ("kernels_per_frame", C.c_int32), ("build_seconds", C.c_double),
                 ("h2d_contact_bytes", C.c_int64), ("n_instances", C.c_int32),
                 ("nonfinite_rollbacks", C.c_int64), ("gram_rows_computed", C.c_int64),
-                ("gram_rows_reused", C.c_int64)]
+                ("gram_rows_reused", C.c_int64), ("build_phase_seconds", C.c_double * 5)]
 
 
 class SimError(RuntimeError):
@@ -348,7 +348,9 @@ class Sim:
     def stats(self):
         s = SimStats()
         _check(lib.sim_get_stats(self._h, C.byref(s)))
-        return {k: getattr(s, k) for k, _ in SimStats._fields_}
+        out = {k: getattr(s, k) for k, _ in SimStats._fields_}
+        out["build_phase_seconds"] = list(s.build_phase_seconds)
+        return out
 
     def set_cr_mode(self, mode: int):
         """0 automatic, 1 cluster CR, 2 grid CR (include/sim.h sim_set_cr_mode)."""

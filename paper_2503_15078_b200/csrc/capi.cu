@@ -122,6 +122,8 @@ struct sim_handle {
     DBuf<int> bad;                   // [S] per-instance failure flags of the current frame
     DBuf<int> rollbacks;             // device counter of rolled-back instance-frames (read by sim_synchronize)
     int64_t rollbacks_total = 0;
+    double build_phase[5] = {0, 0, 0, 0, 0};   // assemble, ordering, Cholesky, K = L^-1, work lists + tiles
+    bool inverse_on_device = false;
     int poison_inst = -1;            // sim_debug_poison: instance whose next frame gets a NaN
     // asynchronous position read-back (sim_get_positions_async): double-buffered device staging
     // in the caller's layout, copied to the host on a copy stream while the next frames compute
@@ -466,6 +468,33 @@ static int upload_all(sim_handle* H) {
     return SIM_OK;
 }
 
+static int device_inverse(sim_handle* H, const simhost::Factor& F, double drop_tol) {
+    const simhost::Inverse& K = H->K;
+    const int n = F.n;
+    const int64_t nnzL = F.Lp[n];
+    cudaStream_t st = H->stream;
+    DBuf<int64_t> Lp, colptr, rowptr;
+    DBuf<int32_t> Li, parent, depth, first;
+    DBuf<double> Lx;
+    DBuf<float> Kc, Kr;
+    CK(Lp.alloc(n + 1)); CK(Lp.upload(F.Lp.data(), n + 1, st));
+    CK(Li.alloc(nnzL)); CK(Li.upload(F.Li.data(), nnzL, st));
+    CK(Lx.alloc(nnzL)); CK(Lx.upload(F.Lx.data(), nnzL, st));
+    CK(parent.alloc(n)); CK(parent.upload(F.parent.data(), n, st));
+    CK(depth.alloc(n)); CK(depth.upload(K.depth.data(), n, st));
+    CK(first.alloc(n)); CK(first.upload(K.first.data(), n, st));
+    CK(colptr.alloc(n + 1)); CK(colptr.upload(K.colptr.data(), n + 1, st));
+    CK(rowptr.alloc(n + 1)); CK(rowptr.upload(K.rowptr.data(), n + 1, st));
+    CK(Kc.alloc(K.nnz)); CK(Kr.alloc(K.nnz));
+    const int e = launch_inverse_columns(st, n, K.height, Lp.p, Li.p, Lx.p, parent.p, depth.p, first.p, colptr.p,
+                                         rowptr.p, drop_tol, Kc.p, Kr.p);
+    if (e) return fail(SIM_E_CUDA, "device inverse: %s", cudaGetErrorString((cudaError_t)e));
+    CK(cudaMemcpyAsync(H->K.Kcol.data(), Kc.p, K.nnz * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(H->K.Krow.data(), Kr.p, K.nnz * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return SIM_OK;
+}
+
 extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (H->state != 0) return fail(SIM_E_STATE, "sparse inverse already built");
@@ -481,11 +510,20 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     const int nf = (int)freev.size();
     if ((int64_t)nf * H->S >= (int64_t)INT32_MAX / 4)
         return fail(SIM_E_LIMIT, "n_free x n_instances exceeds the int32 index range");
+    // phase timings of the precompute (sim_stats.build_phase_seconds)
+    auto tp = std::chrono::steady_clock::now();
+    auto lap = [&](int k) {
+        const auto now = std::chrono::steady_clock::now();
+        H->build_phase[k] = std::chrono::duration<double>(now - tp).count();
+        tp = now;
+    };
     simhost::Csr A = simhost::assemble_Av(nv, H->n_t, H->T.data(), H->rd, H->h, vid, nf);
+    lap(0);
     std::vector<double> coords(3 * (size_t)nf);
     for (int k = 0; k < nf; ++k)
         for (int d = 0; d < 3; ++d) coords[3 * k + d] = H->X[3 * (size_t)freev[k] + d];
     std::vector<int32_t> nd = simhost::nested_dissection(A, coords);
+    lap(1);
     simhost::Csr C = simhost::permute_sym(A, nd);
     std::vector<int32_t> par = simhost::etree(C);
     std::vector<int32_t> post = simhost::postorder(par);
@@ -494,16 +532,28 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     C = simhost::permute_sym(A, perm);
     par = simhost::etree(C);
     simhost::Factor F;
-    if (!simhost::cholesky(C, par, F))
+    const bool chol_ok = simhost::cholesky(C, par, F);
+    lap(2);
+    if (!chol_ok)
         return fail(SIM_E_NOT_SPD, "non-positive pivot at column %d", F.bad_col);
     H->nnzL = (int64_t)F.Lp[nf];
     int nthr = (int)std::max(1u, std::thread::hardware_concurrency());
-    simhost::sparse_inverse(F, drop_tol, H->K, nthr);
+    if (H->host_only) {
+        simhost::sparse_inverse(F, drop_tol, H->K, nthr);
+        H->inverse_on_device = false;
+    } else {   // K = L^-1 on the device (bitwise the host result), values read back for the tile layouts
+        simhost::sparse_inverse_structure(F, H->K);
+        int rc = device_inverse(H, F, drop_tol);
+        if (rc) return rc;
+        H->inverse_on_device = true;
+    }
+    lap(3);
     if (H->K.nnz >= (int64_t)INT32_MAX)
         return fail(SIM_E_LIMIT, "nnz(K) = %lld exceeds the int32 offset limit", (long long)H->K.nnz);
     simhost::build_worklists(H->K, H->wl, 1024);
     simhost::build_tiles(H->K, H->wl, H->T1h, H->T2h);
     if (H->S > 1) H->bparts = simhost::build_batched(H->K, H->wl, 64, H->bu1, H->T1ph, H->bu2, H->bblocks1);
+    lap(4);
     H->n_f = nf;
     H->int2orig.assign(nv, -1);
     H->orig2int.assign(nv, -1);
@@ -1643,6 +1693,7 @@ extern "C" int sim_get_stats(sim_handle* H, sim_stats* o) {
     o->nonfinite_rollbacks = H->rollbacks_total;
     o->gram_rows_computed = H->gram_rows_computed;
     o->gram_rows_reused = H->gram_rows_reused;
+    for (int k = 0; k < 5; ++k) o->build_phase_seconds[k] = H->build_phase[k];
     if (!H->host_only && H->rollbacks.p) {
         int n = 0;
         CK(cudaStreamSynchronize(H->stream));

@@ -277,30 +277,42 @@ std::vector<int32_t> postorder(const std::vector<int32_t>& parent) {
 }
 
 // up-looking Cholesky (row k of L from a sparse triangular solve over ereach(k))
+// Up-looking Cholesky.  Rows of different elimination trees never interact (the etree of a
+// block-diagonal A is a forest, and in postorder every tree is a contiguous index range), so
+// the trees are factorised in parallel, each by the same sequential row loop.
 bool cholesky(const Csr& A, const std::vector<int32_t>& parent, Factor& f) {
-    int n = A.n;
+    const int n = A.n;
     f.n = n;
     f.parent = parent;
-    std::vector<int32_t> mark(n, -1), cnt(n, 1), stack;
+    // tree ranges [lo, root] (postorder: a subtree occupies root - size + 1 .. root)
+    std::vector<int32_t> size(n, 1);
+    for (int i = 0; i < n; ++i)
+        if (parent[i] >= 0) size[parent[i]] += size[i];
+    std::vector<std::pair<int32_t, int32_t>> trees;
+    for (int i = 0; i < n; ++i)
+        if (parent[i] < 0) trees.push_back({i - size[i] + 1, i});
+    const int nt = (int)trees.size();
+    std::vector<int32_t> cnt(n, 1);
     // pass 1: column counts
-    std::vector<int32_t> pattern;
-    auto ereach = [&](int k, std::vector<int32_t>& out) {
-        out.clear();
-        mark[k] = k;
-        for (int64_t p = A.ptr[k]; p < A.ptr[k + 1]; ++p) {
-            int j = A.col[p];
-            if (j >= k) continue;
-            while (j != -1 && mark[j] != k) {
-                out.push_back(j);
-                mark[j] = k;
-                j = parent[j];
+#pragma omp parallel
+    {
+        std::vector<int32_t> mark(n, -1), pattern;
+#pragma omp for schedule(dynamic, 1)
+        for (int t = 0; t < nt; ++t)
+            for (int k = trees[t].first; k <= trees[t].second; ++k) {
+                pattern.clear();
+                mark[k] = k;
+                for (int64_t p = A.ptr[k]; p < A.ptr[k + 1]; ++p) {
+                    int j = A.col[p];
+                    if (j >= k) continue;
+                    while (j != -1 && mark[j] != k) {
+                        pattern.push_back(j);
+                        mark[j] = k;
+                        j = parent[j];
+                    }
+                }
+                for (int j : pattern) cnt[j]++;
             }
-        }
-        std::sort(out.begin(), out.end());
-    };
-    for (int k = 0; k < n; ++k) {
-        ereach(k, pattern);
-        for (int j : pattern) cnt[j]++;
     }
     f.Lp.assign(n + 1, 0);
     for (int j = 0; j < n; ++j) f.Lp[j + 1] = f.Lp[j] + cnt[j];
@@ -308,36 +320,63 @@ bool cholesky(const Csr& A, const std::vector<int32_t>& parent, Factor& f) {
     f.Lx.assign(f.Lp[n], 0.0);
     std::vector<int64_t> fill(n);
     for (int j = 0; j < n; ++j) fill[j] = f.Lp[j] + 1;   // slot 0 of each column = diagonal
-    std::fill(mark.begin(), mark.end(), -1);
-    std::vector<double> x(n, 0.0);
-    for (int k = 0; k < n; ++k) {
-        ereach(k, pattern);
-        double d = 0.0;
-        for (int64_t p = A.ptr[k]; p < A.ptr[k + 1]; ++p) {
-            int j = A.col[p];
-            if (j < k) x[j] = A.val[p];
-            else if (j == k) d = A.val[p];
-        }
-        for (int j : pattern) {
-            double lkj = x[j] / f.Lx[f.Lp[j]];
-            x[j] = 0.0;
-            for (int64_t p = f.Lp[j] + 1; p < fill[j]; ++p) x[f.Li[p]] -= f.Lx[p] * lkj;
-            d -= lkj * lkj;
-            f.Li[fill[j]] = k;
-            f.Lx[fill[j]] = lkj;
-            fill[j]++;
-        }
-        if (!(d > 0.0) || !std::isfinite(d)) {
-            f.bad_col = k;
+    std::vector<int> bad(nt, -1);
+#pragma omp parallel
+    {
+        std::vector<int32_t> mark(n, -1), pattern;
+        std::vector<double> x(n, 0.0);
+#pragma omp for schedule(dynamic, 1)
+        for (int t = 0; t < nt; ++t)
+            for (int k = trees[t].first; k <= trees[t].second; ++k) {
+                pattern.clear();
+                mark[k] = k;
+                for (int64_t p = A.ptr[k]; p < A.ptr[k + 1]; ++p) {
+                    int j = A.col[p];
+                    if (j >= k) continue;
+                    while (j != -1 && mark[j] != k) {
+                        pattern.push_back(j);
+                        mark[j] = k;
+                        j = parent[j];
+                    }
+                }
+                std::sort(pattern.begin(), pattern.end());
+                double d = 0.0;
+                for (int64_t p = A.ptr[k]; p < A.ptr[k + 1]; ++p) {
+                    int j = A.col[p];
+                    if (j < k) x[j] = A.val[p];
+                    else if (j == k) d = A.val[p];
+                }
+                for (int j : pattern) {
+                    double lkj = x[j] / f.Lx[f.Lp[j]];
+                    x[j] = 0.0;
+                    for (int64_t p = f.Lp[j] + 1; p < fill[j]; ++p) x[f.Li[p]] -= f.Lx[p] * lkj;
+                    d -= lkj * lkj;
+                    f.Li[fill[j]] = k;
+                    f.Lx[fill[j]] = lkj;
+                    fill[j]++;
+                }
+                if (!(d > 0.0) || !std::isfinite(d)) {
+                    bad[t] = k;
+                    break;
+                }
+                f.Li[f.Lp[k]] = k;
+                f.Lx[f.Lp[k]] = std::sqrt(d);
+            }
+    }
+    for (int t = 0; t < nt; ++t)
+        if (bad[t] >= 0) {
+            f.bad_col = bad[t];
             return false;
         }
-        f.Li[f.Lp[k]] = k;
-        f.Lx[f.Lp[k]] = std::sqrt(d);
-    }
     return true;
 }
 
 void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads) {
+    sparse_inverse_structure(f, K);
+    sparse_inverse_values(f, drop_tol, K, n_threads);
+}
+
+void sparse_inverse_structure(const Factor& f, Inverse& K) {
     int n = f.n;
     K.n = n;
     K.parent = f.parent;
@@ -373,6 +412,10 @@ void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads)
         for (int i = K.panel_start[p]; i < K.panel_start[p + 1]; ++i) K.ptop[i] = K.panel_start[p + 1] - 1;
     K.Krow.assign(K.nnz, 0.f);
     K.Kcol.assign(K.nnz, 0.f);
+}
+
+void sparse_inverse_values(const Factor& f, double drop_tol, Inverse& K, int n_threads) {
+    const int n = f.n;
 #ifdef _OPENMP
     if (n_threads > 0) omp_set_num_threads(n_threads);
 #endif

@@ -70,6 +70,10 @@ struct Inverse {
 
 // K = L^-1 (fp64 compute, fp32 store); drop |K_ij| < tol |K_jj| (tol > 0)
 void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads);
+// the two halves: index structure (depth, first, row/column offsets, panels; values zeroed) and
+// the values column by column (the device variant is simdev::launch_inverse_columns)
+void sparse_inverse_structure(const Factor& f, Inverse& K);
+void sparse_inverse_values(const Factor& f, double drop_tol, Inverse& K, int n_threads);
 
 // ---------------- K-pass work lists (one CTA per item) ----------------------
 // pass 1 (y = K u, column-major K): item = (<= 32 rows of one panel) x (<= 1024 columns)

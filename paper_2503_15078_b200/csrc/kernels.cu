@@ -2079,6 +2079,71 @@ void launch_gram_reuse(cudaStream_t st, const Params& P, InstOff off, const int3
     }
 }
 
+// ----------------------------------------------------------------------------
+// K = L^-1 on the device: column j of K is the solution of L k = e_j,
+// nonzero on the ancestor chain of j only (Theorem 1; Fig. 4 "ancestor"
+// traversal).  One warp per column walks the chain: k_l = w_l / L_ll, then the
+// lanes scatter w_i -= L_il k_l over column l of L (all rows i are ancestors of l, so on the
+// chain, at position depth(j) - depth(i)).  The per-element update order is the host's
+// (simhost::sparse_inverse_values) and products are not contracted into FMAs, so the fp64
+// values and their fp32 storage are bitwise the host's.
+// ----------------------------------------------------------------------------
+constexpr int kInvWarps = 8;
+
+__global__ void __launch_bounds__(32 * kInvWarps) k_inverse_cols(int n, int hmax, const int64_t* __restrict__ Lp,
+                                                                 const int32_t* __restrict__ Li,
+                                                                 const double* __restrict__ Lx,
+                                                                 const int32_t* __restrict__ parent,
+                                                                 const int32_t* __restrict__ depth,
+                                                                 const int32_t* __restrict__ first,
+                                                                 const int64_t* __restrict__ colptr,
+                                                                 const int64_t* __restrict__ rowptr, double drop_tol,
+                                                                 float* __restrict__ Kcol, float* __restrict__ Krow) {
+    extern __shared__ double wsh[];
+    const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* w = wsh + (size_t)wl * hmax;
+    for (int j = blockIdx.x * kInvWarps + wl; j < n; j += gridDim.x * kInvWarps) {
+        const int D = depth[j];
+        for (int q = lane; q <= D; q += 32) w[q] = q == 0 ? 1.0 : 0.0;
+        __syncwarp();
+        double kjj = 0.0;
+        int q = 0;
+        for (int l = j; l != -1; l = parent[l], ++q) {
+            const double kl = __ddiv_rn(w[q], Lx[Lp[l]]);
+            if (q == 0) kjj = kl;
+            for (int64_t p = Lp[l] + 1 + lane; p < Lp[l + 1]; p += 32) {
+                const int i = Li[p];
+                const int pos = D - depth[i];
+                w[pos] = __dsub_rn(w[pos], __dmul_rn(Lx[p], kl));
+            }
+            if (lane == 0) {
+                double kv = kl;
+                if (drop_tol > 0 && fabs(kv) < drop_tol * fabs(kjj)) kv = 0.0;
+                const float kf = (float)kv;
+                Kcol[colptr[j] + q] = kf;
+                Krow[rowptr[l] + (j - first[l])] = kf;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+int launch_inverse_columns(cudaStream_t st, int n, int hmax, const int64_t* Lp, const int32_t* Li, const double* Lx,
+                           const int32_t* parent, const int32_t* depth, const int32_t* first, const int64_t* colptr,
+                           const int64_t* rowptr, double drop_tol, float* Kcol, float* Krow) {
+    const size_t smem = (size_t)kInvWarps * hmax * sizeof(double);
+    if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;   // etree too tall for the per-warp chain buffer
+    cudaError_t e = cudaFuncSetAttribute(k_inverse_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = std::min((n + kInvWarps - 1) / kInvWarps, nsm * 8);
+    k_inverse_cols<<<blocks, 32 * kInvWarps, smem, st>>>(n, hmax, Lp, Li, Lx, parent, depth, first, colptr, rowptr,
+                                                          drop_tol, Kcol, Krow);
+    return (int)cudaGetLastError();
+}
+
 // D_jj = sum_{a,b in j} w_a w_b G_ab (unit directions; reading A18)
 __global__ void k_djj(int C, InstOff off, DContact* Cs, const float* __restrict__ G) {
     int c = blockIdx.x * blockDim.x + threadIdx.x;

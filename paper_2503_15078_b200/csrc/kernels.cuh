@@ -179,6 +179,11 @@ void launch_delassus(cudaStream_t st, const Params& P, InstOff off, ClassSlots c
                      const int64_t* colptr, const int32_t* depth, const int32_t* parent, const int32_t* ptop,
                      float* G);
 void launch_djj(cudaStream_t st, const Params& P, InstOff off, DContact* c, const float* G);
+// K = L^-1 column by column on the device (bitwise the host's simhost::sparse_inverse_values);
+// L in CSC with the diagonal first in each column; hmax = etree height; returns a cudaError_t
+int launch_inverse_columns(cudaStream_t st, int n, int hmax, const int64_t* Lp, const int32_t* Li, const double* Lx,
+                           const int32_t* parent, const int32_t* depth, const int32_t* first, const int64_t* colptr,
+                           const int64_t* rowptr, double drop_tol, float* Kcol, float* Krow);
 // Gram reuse: copy entries of vertex pairs from the previous blocks (rmap, pgoff, pns), compute
 // the rows of the new slots (newslots: {class, class-local slot}); bitwise = launch_delassus
 void launch_gram_reuse(cudaStream_t st, const Params& P, InstOff off, const int32_t* vtx_all, const int* rmap,

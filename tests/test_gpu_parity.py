@@ -217,3 +217,20 @@ def test_contact_validation(simmod):
     bad2 = scenes.Contact([0], [1.0], np.array([0, 0, 2.0]), 0.0)
     with pytest.raises(simmod.SimError, match="unit"):
         s.set_contacts([bad2])
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3"])
+def test_device_sparse_inverse_is_bitwise_host(simmod, name):
+    """K = L^-1 computed on the device (one warp per column along its ancestor chain, SURVEY
+    §8(f) row 3) equals the host computation bitwise (same update order, no FMA contraction);
+    both drop-tolerance settings."""
+    sc = SCENES[name]() if name in SCENES else scenes.make_scene(name)
+    for tol in (0.0, 1e-3):
+        kw = {"drop_tolerance": tol} if tol else {}
+        d = simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, **kw)
+        h = simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, host_only=True, **kw)
+        assert d.stats()["nnz_K"] == h.stats()["nnz_K"]
+        pd, _, rd, vd = d.debug_inverse()
+        ph, _, rh, vh = h.debug_inverse()
+        assert np.array_equal(pd, ph) and np.array_equal(rd, rh)
+        assert np.array_equal(vd, vh), (tol, np.abs(vd - vh).max())

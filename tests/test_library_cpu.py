@@ -112,3 +112,29 @@ def test_cfg3_structure():
     st = s.stats()
     assert st["n_free"] == 19691 - int(sc.mesh.fixed.sum())
     assert 1.0e7 < st["nnz_K"] < 2.5e7
+
+
+def test_forest_of_objects_sparse_inverse():
+    """Several disconnected objects (SURVEY §8(d) cfg4 structure): the ordering dissects each
+    connected component separately, the etree is a forest (one root per object), the Cholesky
+    factorises the trees in parallel, and K^T K = A^-1 with K block-diagonal (Theorem 1)."""
+    X, T = scenes.hex_grid(3, 3, 3, cell=(0.02,) * 3)
+    n = X.shape[0]
+    X3 = np.concatenate([X, X + [0.1, 0.0, 0.0], X + [0.0, 0.1, 0.01]])
+    T3 = np.concatenate([T, T + n, T + 2 * n]).astype(np.int32)
+    mesh = scenes.Mesh(X3, T3, np.zeros(X3.shape[0], np.uint8))
+    mat = scenes.Material()
+    s = Sim(mesh.X, mesh.T, mesh.fixed, mat, 0.01, host_only=True)
+    perm, parent, rowptr, vals = s.debug_inverse()
+    nf = perm.size
+    assert np.sum(parent == -1) == 3
+    first = np.arange(nf) - (rowptr[1:] - rowptr[:-1]) + 1
+    K = np.zeros((nf, nf))
+    for i in range(nf):
+        K[i, first[i]:i + 1] = vals[rowptr[i]:rowptr[i + 1]]
+    obj = perm // n                       # object of each internal index
+    assert np.all((K == 0) | (obj[:, None] == obj[None, :]))
+    o = O.Oracle(mesh, mat, 0.01)
+    A = o.A_ff.toarray()[np.ix_(perm, perm)]
+    Ainv = np.linalg.inv(A)
+    assert np.abs(K.T @ K - Ainv).max() <= 2e-6 * np.abs(Ainv).max()
