@@ -174,6 +174,9 @@ struct sim_handle {
     DBuf<float> G, GA;   // Delassus Gram blocks and the CR's active blocks (fp32-exact values)
     // Gram reuse across commits (sim_set_schur_reuse): the previous commit's class blocks
     bool schur_reuse = false, have_prev = false;
+    bool dev_pending = false;        // host half of a contact commit done, device half not yet
+    bool pend_reuse = false;
+    int pend_nnew = 0;
     std::vector<std::vector<int32_t>> prev_cls_verts;
     std::vector<int64_t> prev_goff;
     std::vector<int> prev_cls_of_inst;
@@ -705,6 +708,8 @@ static int check_contact_call(sim_handle* H) {
     return SIM_OK;
 }
 
+static int commit_host(sim_handle* H);
+
 extern "C" int sim_set_contacts(sim_handle* H, int32_t instance, const sim_contact* cs, int32_t n) {
     int rc = check_contact_call(H);
     if (rc) return rc;
@@ -717,6 +722,9 @@ extern "C" int sim_set_contacts(sim_handle* H, int32_t instance, const sim_conta
     H->ic[instance] = std::move(I);
     H->dirty = true;
     H->set_contacts_host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count();
+    // every instance's set is now known: pack and start the upload right away (it overlaps the
+    // frames already enqueued); the device half runs at the next step
+    if (H->S == 1) return commit_host(H);
     return SIM_OK;
 }
 
@@ -849,6 +857,7 @@ extern "C" int sim_set_contacts_batch(sim_handle* H, int32_t first, int32_t coun
     for (int i = 0; i < count; ++i) H->ic[first + i] = std::move(tmp[i]);
     H->dirty = true;
     H->set_contacts_host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count();
+    if (count == H->S) return commit_host(H);   // all instances set: pack + upload now (see sim_set_contacts)
     return SIM_OK;
 }
 
@@ -903,7 +912,11 @@ static Params make_params(const sim_handle* H) {
 
 // pack every instance's contacts, upload them asynchronously and build the per-contact-set
 // device data (chains, row lists, Delassus Gram, D_jj) for all instances in batched launches
-static int commit_contacts(sim_handle* H) {
+static int commit_device(sim_handle* H);
+
+// host half of a contact commit: classes, layouts, packing into pinned staging and one
+// asynchronous H2D copy of the whole arena (enqueued on the handle's stream)
+static int commit_host(sim_handle* H) {
     if (!H->dirty) return SIM_OK;
     const int S = H->S, nf = H->n_f;
     cudaStream_t st = H->stream;
@@ -1204,6 +1217,28 @@ static int commit_contacts(sim_handle* H) {
     H->grid = grid;
     H->NG = NG;
     H->ng_max = ngmax;
+    H->pend_reuse = reuse;
+    H->pend_nnew = (int)news_h.size();
+    H->gram_rows_computed = reuse ? (int64_t)news_h.size() : CSt;
+    H->gram_rows_reused = reuse ? (int64_t)CSt - (int64_t)news_h.size() : 0;
+    // remember this commit's blocks for the next one
+    H->have_prev = !grid;
+    H->prev_cls_verts.assign(NCL, {});
+    for (int k = 0; k < NCL; ++k) H->prev_cls_verts[k] = H->ic[rep[k]].verts;
+    H->prev_goff.assign(goff.begin(), goff.end() - 1);
+    H->prev_cls_of_inst = cls;
+    H->prev_gsize = goff[NCL];
+    H->dirty = false;
+    H->dev_pending = true;
+    return SIM_OK;
+}
+
+// device half: the per-contact-set kernels (chain rows, row lists, Delassus Gram, D_jj)
+static int commit_device(sim_handle* H) {
+    if (!H->dev_pending) return SIM_OK;
+    cudaStream_t st = H->stream;
+    const int S = H->S, nf = H->n_f, NCL = H->NCL, NG = H->NG, ngmax = H->ng_max;
+    const bool grid = H->grid, reuse = H->pend_reuse;
     CK(cudaMemsetAsync(H->flag.p, 0, (size_t)NCL * nf, st));
     CK(cudaMemsetAsync(H->slotmap.p, 0xff, (size_t)nf * S * sizeof(int32_t), st));
     CK(cudaMemsetAsync(H->ucount.p, 0, 2 * (size_t)NCL * sizeof(int), st));
@@ -1227,23 +1262,20 @@ static int commit_contacts(sim_handle* H) {
     } else {
         if (reuse)
             launch_gram_reuse(st, P, off, csl.vtx, H->rmap.p, H->pgoff.p, H->pns.p, H->Gprev.p, H->newslots.p,
-                              (int)news_h.size(), H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
+                              H->pend_nnew, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
         else
             launch_delassus(st, P, off, csl, H->Kcol.p, H->colptr.p, H->depth.p, H->parent.p, H->ptop.p, H->G.p);
         launch_djj(st, P, off, H->dc.p, H->G.p);
     }
-    H->gram_rows_computed = reuse ? (int64_t)news_h.size() : CSt;
-    H->gram_rows_reused = reuse ? (int64_t)CSt - (int64_t)news_h.size() : 0;
-    // remember this commit's blocks for the next one
-    H->have_prev = !grid;
-    H->prev_cls_verts.assign(NCL, {});
-    for (int k = 0; k < NCL; ++k) H->prev_cls_verts[k] = H->ic[rep[k]].verts;
-    H->prev_goff.assign(goff.begin(), goff.end() - 1);
-    H->prev_cls_of_inst = cls;
-    H->prev_gsize = goff[NCL];
     CK(cudaGetLastError());
-    H->dirty = false;
+    H->dev_pending = false;
     return SIM_OK;   // asynchronous: the copies and kernels are ordered on the handle's stream
+}
+
+static int commit_contacts(sim_handle* H) {
+    int rc = commit_host(H);
+    if (rc) return rc;
+    return commit_device(H);
 }
 
 // ---------------------------------------------------------------------------
@@ -1650,7 +1682,7 @@ extern "C" int sim_get_lambda(sim_handle* H, int32_t inst, double* lam, int32_t 
     int rc = check_instance(H, inst);
     if (rc) return rc;
     if (!lam) return fail(SIM_E_INVALID, "null argument");
-    if (H->dirty) return fail(SIM_E_STATE, "contacts changed since the last step");
+    if (H->dirty || H->dev_pending) return fail(SIM_E_STATE, "contacts changed since the last step");
     const InstContacts& I = H->ic[inst];
     const int nc = (int)I.hc.size();
     int rows = 0;
@@ -1701,7 +1733,7 @@ extern "C" int sim_get_stats(sim_handle* H, sim_stats* o) {
         o->nonfinite_rollbacks += n;
     }
     o->last_cr_residual = -1;
-    if (!H->host_only && H->state == 1 && H->C > 0 && !H->dirty) {
+    if (!H->host_only && H->state == 1 && H->C > 0 && !H->dirty && !H->dev_pending) {
         CK(cudaStreamSynchronize(H->stream));
         std::vector<double> r(H->S), ph(H->C), l(3 * (size_t)H->C);
         std::vector<DContact> hc(H->C);
@@ -1846,7 +1878,7 @@ extern "C" int sim_debug_contact_state(sim_handle* H, int32_t inst, double* thet
                                        double* dxt, int32_t* slot_vertex, double* djj) {
     int rc = check_instance(H, inst);
     if (rc) return rc;
-    if (H->dirty) return fail(SIM_E_STATE, "contacts changed since the last step");
+    if (H->dirty || H->dev_pending) return fail(SIM_E_STATE, "contacts changed since the last step");
     CK(cudaStreamSynchronize(H->stream));
     const InstContacts& I = H->ic[inst];
     const int nc = (int)I.hc.size(), ns = (int)I.verts.size();
