@@ -140,7 +140,7 @@ struct sim_handle {
     // device: K
     DBuf<float> Krow, Kcol, T1, T2, T1p;   // K row/column-major + the passes' tile streams
     DBuf<float> T1tc, T2tc;                // tensor-core copies of T1p / T2 (S > 1)
-    int kpass_mode = 0;                    // S > 1: 0 tensor cores (tcgen05), 1 CUDA-core FP32
+    int kpass_mode = 2;                    // S > 1: 2 tcgen05 with TMEM operands, 0 tcgen05 SMEM operands, 1 FP32
     int tc_drain = 4;                      // tensor-core K-pass: tiles per fp32 TMEM accumulation (2.4e-6 rel. on cfg3)
     DBuf<int64_t> colptr;
     DBuf<int32_t> depth, parent, ptop, cover;
@@ -1290,6 +1290,9 @@ static void enqueue_kpass1(sim_handle* H, cudaStream_t st) {
     if (H->S == 1)
         launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->T1.p, H->u.p, H->y.p, H->part1.p,
                       H->counters.p);
+    else if (H->kpass_mode == 2)
+        launch_kpass1_ts(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1tc.p, H->u.p, H->y.p, H->part1.p,
+                         H->counters.p, H->tc_drain);
     else if (H->kpass_mode == 0)
         launch_kpass1_tc(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1tc.p, H->u.p, H->y.p, H->part1.p,
                          H->counters.p, H->tc_drain);
@@ -1301,6 +1304,9 @@ static void enqueue_kpass2(sim_handle* H, cudaStream_t st, double4* x, const dou
                            int fin) {
     if (H->S == 1)
         launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->T2.p, H->y.p, x, xt, v, inv_h, fin);
+    else if (H->kpass_mode == 2)
+        launch_kpass2_ts(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2tc.p, H->y.p, x, xt, v,
+                         inv_h, fin, H->tc_drain);
     else if (H->kpass_mode == 0)
         launch_kpass2_tc(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2tc.p, H->y.p, x, xt, v,
                          inv_h, fin, H->tc_drain);
@@ -1429,11 +1435,12 @@ extern "C" int sim_set_kpass_mode(sim_handle* H, int32_t mode) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     // mode 0 | 1; mode >= 16: tensor cores with (mode >> 4) tiles per fp32 TMEM accumulation (tuning)
     if (mode >= 16) {
-        H->kpass_mode = 0;
+        H->kpass_mode = (mode & 15) == 2 ? 2 : 0;
         H->tc_drain = std::max(2, mode >> 4);
         return SIM_OK;
     }
-    if (mode != 0 && mode != 1) return fail(SIM_E_INVALID, "K-pass mode must be 0 (tensor cores) or 1 (FP32)");
+    if (mode < 0 || mode > 2)
+        return fail(SIM_E_INVALID, "K-pass mode must be 0 (tensor cores), 1 (FP32) or 2 (tensor cores, TMEM operands)");
     H->kpass_mode = mode;
     return SIM_OK;
 }

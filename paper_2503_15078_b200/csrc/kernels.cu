@@ -1502,6 +1502,266 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     if (threadIdx.x == 0) counters[U.block * nchunks + chunk] = 0;
 }
 
+// ----------------------------------------------------------------------------
+// TS variant: the right-hand-side operand (A, hi and lo, 3 components) goes from registers to
+// TMEM with tcgen05.st instead of through shared memory, and the MMAs read A from TMEM
+// (tcgen05.mma ... [d], [a_tmem], b_desc): shared memory only holds the K tiles.  TMEM: the
+// accumulators in columns [0, 96), A stage s in [128 + 192 s, 320 + 192 s) as 6 planes of 32
+// columns (component c hi / lo), lane = instance.  One accumulator set: it is folded into
+// fp64 every `drain` tiles while the pipeline waits.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void umma_tf32_ts(uint32_t dt, uint32_t at, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dt),
+        "r"(at), "l"(db), "r"(kIdescTf32), "r"(acc)
+        : "memory");
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(kTcThreads + 32, 1)
+    k_kpass_ts(int S, int n_f, const BUnit* __restrict__ units, const float* __restrict__ Ttc,
+               const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
+               double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
+               const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
+    pdl_enter();
+    __shared__ __align__(128) unsigned char bsm[2][8192];
+    __shared__ __align__(8) uint64_t bfull[2], mdone[2], afull[2];
+    __shared__ uint32_t tmem_base_s;
+    __shared__ int s_last;
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const bool mma_warp = w == kTcThreads / 32;
+    const BUnit U = units[blockIdx.x];
+    const int chunk = blockIdx.y;
+    const int i0 = chunk * kTcInst;
+    const int ni = min(kTcInst, S - i0);
+    const unsigned long long pol = l2_evict_first();
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&tmem_base_s)),
+                     "r"(512u)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bfull[0], 1);
+        mbar_init(&bfull[1], 1);
+        mbar_init(&mdone[0], 1);
+        mbar_init(&mdone[1], 1);
+        mbar_init(&afull[0], kTcThreads);
+        mbar_init(&afull[1], kTcThreads);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = tmem_base_s;
+    auto acol = [&](int st, int c, int hl) { return 128u + 192u * st + 32u * (2 * c + hl); };
+    auto issueB = [&](int t) {
+        const int st = t & 1;
+        mbar_expect_tx(&bfull[st], 8192u);
+        bulk_g2s(bsm[st], Ttc + 2 * U.toff + (int64_t)t * 2048, 8192u, &bfull[st], true, pol);
+    };
+    if (tid == 0) {
+        issueB(0);
+        if (U.ntiles > 1) issueB(1);
+    }
+    const int q4 = w & 3, oct = w >> 2;    // TMEM lane quadrant; producer row octet / fold column octet
+    const int il = 32 * q4 + lane;         // instance of this thread (TMEM lane)
+    const bool ilive = il < ni;
+    double dacc[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dacc[c][e] = 0.0;
+    auto fold = [&]() {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const uint32_t ta = tmem + ((uint32_t)(32 * q4) << 16) + 32u * c + 8u * oct;
+            uint32_t r[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                           "=r"(r[7])
+                         : "r"(ta));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dacc[c][e] += (double)__uint_as_float(r[e]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    };
+    if (mma_warp) {
+        if (lane == 0) {
+            for (int t = 0; t < U.ntiles; ++t) {
+                const int st = t & 1;
+                mbar_wait(&afull[st], (t >> 1) & 1);
+                mbar_wait(&bfull[st], (t >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                const uint32_t b0 = (unsigned)__cvta_generic_to_shared(bsm[st]);
+                const uint32_t b1 = b0 + 4096u;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const uint32_t dt = tmem + 32u * c;
+                    const uint32_t ah = tmem + acol(st, c, 0), al = tmem + acol(st, c, 1);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t dbh = umma_desc_k(b0 + 256u * kk), dbl = umma_desc_k(b1 + 256u * kk);
+                        umma_tf32_ts(dt, ah + 8u * kk, dbh, (t % drain != 0 || kk > 0) ? 1u : 0u);
+                        umma_tf32_ts(dt, al + 8u * kk, dbh, 1u);
+                        umma_tf32_ts(dt, ah + 8u * kk, dbl, 1u);
+                    }
+                }
+                umma_commit(&mdone[st]);
+            }
+        }
+        __syncwarp();
+    } else {
+        for (int t = 0; t < U.ntiles; ++t) {
+            const int st = t & 1;
+            const int nv = PASS == 1 ? max(0, min(32, n_f - (U.c0 + 32 * t))) : min(32, U.nlist - 32 * t);
+            float4 r[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int q = 8 * oct + e;
+                r[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (ilive && q < nv) {
+                    const int idx = PASS == 1 ? U.c0 + 32 * t + q : __ldg(&cover[U.list0 + 32 * t + q]);
+                    r[e] = __ldg(&vin[(size_t)idx * S + i0 + il]);
+                }
+            }
+            if (t > 0 && t % drain == 0) {   // accumulators complete up to tile t - 1: fold, restart
+                mbar_wait(&mdone[(t - 1) & 1], ((t - 1) >> 1) & 1);
+                fold();
+            }
+            if (t >= 2) {
+                mbar_wait(&mdone[st], ((t - 2) >> 1) & 1);   // the tensor core is done with A / B stage st
+                if (tid == 0) issueB(t);
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                uint32_t hi[8], lo[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float a = c == 0 ? r[e].x : (c == 1 ? r[e].y : r[e].z);
+                    const float h = tf32_rn(a);
+                    hi[e] = __float_as_uint(h);
+                    lo[e] = __float_as_uint(tf32_rn(a - h));
+                }
+                const uint32_t lanebase = tmem + ((uint32_t)(32 * q4) << 16) + 8u * oct;
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
+                                 lanebase + acol(st, c, 0)),
+                             "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]),
+                             "r"(hi[7])
+                             : "memory");
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
+                                 lanebase + acol(st, c, 1)),
+                             "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]),
+                             "r"(lo[7])
+                             : "memory");
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(&afull[st]))
+                         : "memory");
+        }
+        const int last = U.ntiles - 1;
+        if (last >= 0) {
+            mbar_wait(&mdone[last & 1], (last >> 1) & 1);
+            fold();
+        }
+    }
+    __syncthreads();
+    if (w == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u) : "memory");
+    if (mma_warp) return;
+    const int li = il;
+    const bool live = li < ni;
+    const int inst = i0 + li;
+    if (PASS == 2) {
+        if (!live) return;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
+            if (l < U.nr) {
+                const size_t jx = (size_t)(U.c0 + l) * S + inst;
+                double4 xj = x[jx];
+                xj.x += dacc[0][r];
+                xj.y += dacc[1][r];
+                xj.z += dacc[2][r];
+                x[jx] = xj;
+                if (finalize_v) {
+                    const double4 t0 = xt[jx];
+                    v[jx] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
+                }
+            }
+        }
+        return;
+    }
+    if (U.nparts == 1) {
+        if (!live) return;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
+            if (l < U.nr)
+                yout[(size_t)(U.r0 + l) * S + inst] =
+                    make_float4((float)dacc[0][r], (float)dacc[1][r], (float)dacc[2][r], 0.f);
+        }
+        return;
+    }
+    const size_t pstride = (size_t)32 * S;
+    if (live) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
+            double* pp = part + (size_t)U.part * 3 * pstride + (size_t)l * S + inst;
+            pp[0] = dacc[0][r];
+            pp[pstride] = dacc[1][r];
+            pp[2 * pstride] = dacc[2][r];
+        }
+    }
+    __threadfence();
+    asm volatile("bar.sync 1, %0;\n" ::"r"(kTcThreads));   // producers only (the MMA warp has left)
+    if (threadIdx.x == 0) {
+        const int old = atomicAdd(&counters[U.block * nchunks + chunk], 1);
+        s_last = old == U.nparts - 1;
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"r"(kTcThreads));
+    if (!s_last) return;
+    __threadfence();
+    if (live) {
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
+            if (l >= U.nr) continue;
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            for (int q = 0; q < U.nparts; ++q) {
+                const double* pq = part + (size_t)(U.list0 + q) * 3 * pstride + (size_t)l * S + inst;
+                t0 += __ldcg(pq);
+                t1 += __ldcg(pq + pstride);
+                t2 += __ldcg(pq + 2 * pstride);
+            }
+            yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
+        }
+    }
+    if (threadIdx.x == 0) counters[U.block * nchunks + chunk] = 0;
+}
+
+void launch_kpass1_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
+                      const float4* u, float4* y, double* part, int* counters, int drain) {
+    const int nch = (S + kTcInst - 1) / kTcInst;
+    launch_pdl(k_kpass_ts<1>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, n_f, units, T1tc,
+               (const int32_t*)nullptr, u, y, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
+               (double4*)nullptr, 0.0, 0, drain);
+}
+
+void launch_kpass2_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
+                      const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
+                      int finalize_v, int drain) {
+    const int nch = (S + kTcInst - 1) / kTcInst;
+    launch_pdl(k_kpass_ts<2>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, n_f, units, T2tc, cover, y,
+               (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain);
+}
+
 void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
                       const float4* u, float4* y, double* part, int* counters, int drain) {
     static bool attr = false;

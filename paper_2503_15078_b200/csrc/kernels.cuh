@@ -148,6 +148,12 @@ void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
 void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
                       const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
                       int finalize_v, int drain);   // drain: tiles accumulated in TMEM (fp32) per fp64 fold
+// TS variant: right-hand sides staged in TMEM (tcgen05.st) instead of shared memory
+void launch_kpass1_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
+                      const float4* u, float4* y, double* part, int* counters, int drain);
+void launch_kpass2_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
+                      const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
+                      int finalize_v, int drain);
 // grouped: one work item per (class slot, 32 class members); items int2 {class slot, member0}
 void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
                       const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows, const float4* y,

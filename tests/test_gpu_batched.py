@@ -196,14 +196,15 @@ def test_tensor_core_and_fp32_kpasses_agree(simmod):
     rng = np.random.default_rng(9)
     b = rng.standard_normal((S, sc.mesh.n_v, 3)).astype(np.float32).astype(np.float64)
     out = {}
-    for mode in (0, 1):
+    for mode in (0, 1, 2):
         s.set_kpass_mode(mode)
         out[mode] = s.debug_apply_inverse(b)
     for i in (0, 63, 127, 128, 129):
         xr = o.solve(b[i][o.free])
-        for mode in (0, 1):
+        for mode in (0, 1, 2):
             assert np.abs(out[mode][i][o.free] - xr).max() < 1e-5 * np.abs(xr).max(), (mode, i)
     assert np.abs(out[0] - out[1]).max() < 1e-5 * np.abs(out[1]).max()
+    assert np.abs(out[2] - out[1]).max() < 1e-5 * np.abs(out[1]).max()
 
 
 def test_nonfinite_frame_rolls_back_one_instance(simmod):

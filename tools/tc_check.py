@@ -15,7 +15,7 @@ for name, S in (("block", 33), ("cfg3", 130)):
     rng = np.random.default_rng(5)
     b = rng.standard_normal((S, sc.mesh.n_v, 3)).astype(np.float32).astype(np.float64)
     res = {}
-    modes = (1, 32, 64, 128, 1024)
+    modes = (1, 64, 66, 130)
     for mode in modes:
         s.set_kpass_mode(mode)
         res[mode] = s.debug_apply_inverse(b)
@@ -32,7 +32,7 @@ s.set_pin_velocity(sc.pin_velocity)
 base = simlib.contacts_to_array(sc.contacts)
 packed = (np.concatenate([base] * S), np.full(S, len(base), np.int32))
 s.set_contacts_batch(packed=packed)
-for mode in (1, 32, 64, 128):
+for mode in (1, 64, 66, 130):
     s.set_kpass_mode(mode)
     s.step(1, 5)
     s.set_profiling(True)
