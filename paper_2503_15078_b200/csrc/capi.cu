@@ -175,6 +175,13 @@ struct sim_handle {
     // Gram reuse across commits (sim_set_schur_reuse): the previous commit's class blocks
     bool schur_reuse = false, have_prev = false;
     bool dev_pending = false;        // host half of a contact commit done, device half not yet
+    // contact passes on the tensor cores (S > 1, one slot-set class): work lists + tiles
+    bool tc_contact = false;
+    std::vector<int32_t> tc_verts;   // the class vertex set the tiles were built for
+    DBuf<simhost::BUnit> tcu_c, tcu_s;
+    DBuf<int32_t> tc_cover, tc_rows;
+    DBuf<float> tc_Tc, tc_Ts;
+    int tc_nuc = 0, tc_nus = 0, tc_ns = 0;
     bool pend_reuse = false;
     int pend_nnew = 0;
     std::vector<std::vector<int32_t>> prev_cls_verts;
@@ -1217,6 +1224,28 @@ static int commit_host(sim_handle* H) {
     H->grid = grid;
     H->NG = NG;
     H->ng_max = ngmax;
+    // chain dot and scatter on the tensor cores: S > 1 instances all in one slot-set class
+    H->tc_contact = S > 1 && NCL == 1 && Ct > 0 && H->kpass_mode == 2;
+    if (H->tc_contact && H->ic[rep[0]].verts != H->tc_verts) {   // tiles depend on K and the vertex set only
+        simhost::ContactPasses cp;
+        simhost::build_contact_passes(H->K, H->ic[rep[0]].verts, cp);
+        std::vector<float> tc, ts;
+        simhost::tc_tiles(cp.Tc, tc);
+        simhost::tc_tiles(cp.Ts, ts);
+        CK(H->tcu_c.alloc(std::max<size_t>(cp.uc.size(), 1))); CK(H->tcu_c.upload(cp.uc.data(), cp.uc.size(), st));
+        CK(H->tcu_s.alloc(std::max<size_t>(cp.us.size(), 1))); CK(H->tcu_s.upload(cp.us.data(), cp.us.size(), st));
+        CK(H->tc_cover.alloc(std::max<size_t>(cp.cover.size(), 1)));
+        CK(H->tc_cover.upload(cp.cover.data(), cp.cover.size(), st));
+        CK(H->tc_rows.alloc(std::max<size_t>(cp.rows.size(), 1))); CK(H->tc_rows.upload(cp.rows.data(), cp.rows.size(), st));
+        CK(H->tc_Tc.alloc(std::max<size_t>(tc.size(), 1))); CK(H->tc_Tc.upload(tc.data(), tc.size(), st));
+        CK(H->tc_Ts.alloc(std::max<size_t>(ts.size(), 1))); CK(H->tc_Ts.upload(ts.data(), ts.size(), st));
+        CK(cudaStreamSynchronize(st));   // the host vectors die here
+        H->tc_nuc = (int)cp.uc.size();
+        H->tc_nus = (int)cp.us.size();
+        H->tc_ns = (int)H->ic[rep[0]].verts.size();
+        H->tc_verts = H->ic[rep[0]].verts;
+        H->contact_gen++;   // captured pointers changed
+    }
     H->pend_reuse = reuse;
     H->pend_nnew = (int)news_h.size();
     H->gram_rows_computed = reuse ? (int64_t)news_h.size() : CSt;
@@ -1371,8 +1400,13 @@ static int enqueue_frame(sim_handle* H, int iters) {
         enqueue_kpass1(H, st); nk++;
         if (con) {
             MARK(KK_CHAIN);
-            launch_chain_dot(st, P, off, class_slots(H), H->Kcol.p, H->colptr.p, H->chain_off.p, H->chain_rows.p,
-                             H->y.p, sl, ccr, H->x.p, cs, H->n_it_cd, H->it_cd.p); nk++;
+            if (H->tc_contact)
+                launch_chain_pass_ts(st, H->S, H->tc_nuc, H->tcu_c.p, H->tc_Tc.p, H->tc_cover.p, H->y.p, H->soff.p,
+                                     ccr, H->x.p, cs, 1);   // fold every tile: the Schur RHS is sensitive
+            else
+                launch_chain_dot(st, P, off, class_slots(H), H->Kcol.p, H->colptr.p, H->chain_off.p,
+                                 H->chain_rows.p, H->y.p, sl, ccr, H->x.p, cs, H->n_it_cd, H->it_cd.p);
+            nk++;
             MARK(KK_CR);
             if (H->grid) {
                 int e = launch_gcr(st, P, gcr_data(H), H->dc.p, ccr, sl, H->x.p, cs);
@@ -1383,8 +1417,13 @@ static int enqueue_frame(sim_handle* H, int iters) {
                 if (e) return -e;
             }
             MARK(KK_SCATTER);
-            launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->wzT.p, H->y.p,
-                           H->n_it_sc, H->it_sc.p); nk++;
+            if (H->tc_contact)
+                launch_scatter_pass_ts(st, H->S, H->tc_ns, H->tc_nus, H->tcu_s.p, H->tc_Ts.p, H->tc_rows.p, H->wzT.p,
+                                       H->y.p, 1);
+            else
+                launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->wzT.p, H->y.p,
+                               H->n_it_sc, H->it_sc.p);
+            nk++;
         }
         MARK(KK_KPASS2);
         enqueue_kpass2(H, st, H->x.p, H->xt.p, H->v.p, 1.0 / H->h, k == iters - 1); nk++;
@@ -1495,7 +1534,8 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     }
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
                                       H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG,
-                                      H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain};
+                                      H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain, H->cr_mode,
+                                      H->tc_contact};
     if (!H->gexec || key != H->gkey) {
         if (H->gexec) {
             cudaGraphExecDestroy(H->gexec);

@@ -619,4 +619,79 @@ void tc_tiles(const std::vector<float>& T, std::vector<float>& Ttc) {
     }
 }
 
+void build_contact_passes(const Inverse& K, const std::vector<int32_t>& sv, ContactPasses& cp) {
+    cp = ContactPasses();
+    const int ns = (int)sv.size();
+    auto is_anc = [&](int r, int a) { return K.first[r] <= a && a <= r; };   // r ancestor-or-self of a
+    auto kval = [&](int r, int a) { return K.Krow[K.rowptr[r] + (a - K.first[r])]; };
+    // chain pass: blocks of 32 slots
+    std::vector<int32_t> mark(K.n, -1), rows;
+    for (int c0 = 0; c0 < ns; c0 += 32) {
+        const int nb = std::min(32, ns - c0);
+        rows.clear();
+        for (int s = c0; s < c0 + nb; ++s)
+            for (int r = sv[s]; r >= 0; r = K.parent[r])
+                if (mark[r] != c0) { mark[r] = c0; rows.push_back(r); }
+        std::sort(rows.begin(), rows.end());
+        BUnit u{};
+        u.c0 = c0;
+        u.nr = nb;
+        u.list0 = (int32_t)cp.cover.size();
+        u.nlist = (int32_t)rows.size();
+        u.ntiles = (u.nlist + 31) / 32;
+        u.part = 0;
+        u.nparts = 1;
+        u.toff = (int64_t)cp.Tc.size();
+        cp.cover.insert(cp.cover.end(), rows.begin(), rows.end());
+        for (int t = 0; t < u.ntiles; ++t) {
+            const size_t base = cp.Tc.size();
+            cp.Tc.resize(base + 1024, 0.f);
+            for (int q = 0; q < 32 && 32 * t + q < u.nlist; ++q) {
+                const int r = rows[32 * t + q];
+                for (int l = 0; l < nb; ++l)
+                    if (is_anc(r, sv[c0 + l])) cp.Tc[base + 32 * q + l] = kval(r, sv[c0 + l]);
+            }
+        }
+        cp.uc.push_back(u);
+    }
+    // scatter pass: the union of all chains, blocks of 32 rows; each row reaches the slots whose
+    // vertex lies in its subtree [first(r), r], a contiguous slot range (slots ascending)
+    std::fill(mark.begin(), mark.end(), -1);
+    for (int s = 0; s < ns; ++s)
+        for (int r = sv[s]; r >= 0 && mark[r] < 0; r = K.parent[r]) { mark[r] = 1; cp.rows.push_back(r); }
+    std::sort(cp.rows.begin(), cp.rows.end());
+    const int nu = (int)cp.rows.size();
+    for (int r0 = 0; r0 < nu; r0 += 32) {
+        const int nb = std::min(32, nu - r0);
+        int lo = ns, hi = 0;
+        for (int l = 0; l < nb; ++l) {
+            const int r = cp.rows[r0 + l];
+            const int a = (int)(std::lower_bound(sv.begin(), sv.end(), K.first[r]) - sv.begin());
+            const int b = (int)(std::upper_bound(sv.begin(), sv.end(), r) - sv.begin());
+            if (a < b) { lo = std::min(lo, a); hi = std::max(hi, b); }
+        }
+        if (lo >= hi) continue;
+        BUnit u{};
+        u.r0 = r0;
+        u.nr = nb;
+        u.c0 = lo;
+        u.ntiles = (hi - lo + 31) / 32;
+        u.part = 0;
+        u.nparts = 1;
+        u.toff = (int64_t)cp.Ts.size();
+        for (int t = 0; t < u.ntiles; ++t) {
+            const size_t base = cp.Ts.size();
+            cp.Ts.resize(base + 1024, 0.f);
+            for (int q = 0; q < 32 && lo + 32 * t + q < ns; ++q) {
+                const int a = sv[lo + 32 * t + q];
+                for (int l = 0; l < nb; ++l) {
+                    const int r = cp.rows[r0 + l];
+                    if (is_anc(r, a)) cp.Ts[base + 32 * q + l] = kval(r, a);
+                }
+            }
+        }
+        cp.us.push_back(u);
+    }
+}
+
 }  // namespace simhost

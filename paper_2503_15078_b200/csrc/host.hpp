@@ -114,6 +114,20 @@ struct BUnit { int32_t r0, nr, c0, ntiles, list0, nlist, block, part, nparts, pa
 int build_batched(const Inverse& K, const WorkLists& wl, int unit_tiles, std::vector<BUnit>& u1,
                   std::vector<float>& T1p, std::vector<BUnit>& u2, int& nblocks1);
 
+// ---------------- contact passes of a slot-set class on the tensor cores (S > 1) -------------
+// With Z[s][r] = K[r][a_s] (r on the ancestor chain of the contact vertex a_s):
+//   chain pass   dxt[s] = sum_r Z[s][r] y[r]   -- units like pass 2: 32 slots (c0, nr), their
+//                sorted chain-row union in cover[list0 .. list0 + nlist), tiles tile[q][l] = Z[c0+l][cover q]
+//   scatter pass y[r] += sum_s Z[s][r] wz[s]    -- units like pass 1: 32 chain rows rows[r0 .. r0 + nr),
+//                slots c0 .. c0 + 32 ntiles, tiles tile[q][l] = Z[c0 + 32 t + q][rows[r0 + l]]
+// Tile streams are in the plain tile[q][l] order (tc_tiles re-lays them out).
+struct ContactPasses {
+    std::vector<BUnit> uc, us;
+    std::vector<int32_t> cover, rows;
+    std::vector<float> Tc, Ts;
+};
+void build_contact_passes(const Inverse& K, const std::vector<int32_t>& slot_vtx, ContactPasses& cp);
+
 // Tensor-core copy of a tile stream (1024-float tiles, tile[q * 32 + l], q = reduction index,
 // l = output): per tile 2048 floats = the tf32 "hi" tile then the "lo" tile (v - hi), both
 // rounded to nearest tf32, each in the tcgen05 SWIZZLE_NONE K-major core-matrix layout

@@ -1510,6 +1510,9 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
 // columns (component c hi / lo), lane = instance.  One accumulator set: it is folded into
 // fp64 every `drain` tiles while the pipeline waits.
 // ----------------------------------------------------------------------------
+__device__ __forceinline__ void chain_rho(int S, int inst, int s, double t0, double t1, double t2, CrContacts cc,
+                                          const double4* __restrict__ x, ContactState cs);
+
 __device__ __forceinline__ void umma_tf32_ts(uint32_t dt, uint32_t at, uint64_t db, uint32_t acc) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -1523,7 +1526,8 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     k_kpass_ts(int S, int n_f, const BUnit* __restrict__ units, const float* __restrict__ Ttc,
                const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
                double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
-               const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
+               const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain,
+               TsExtra ex) {
     pdl_enter();
     __shared__ __align__(128) unsigned char bsm[2][8192];
     __shared__ __align__(8) uint64_t bfull[2], mdone[2], afull[2];
@@ -1618,14 +1622,16 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     } else {
         for (int t = 0; t < U.ntiles; ++t) {
             const int st = t & 1;
-            const int nv = PASS == 1 ? max(0, min(32, n_f - (U.c0 + 32 * t))) : min(32, U.nlist - 32 * t);
+            // PASS 1 / 4: contiguous reduction indices (columns / slots); PASS 2 / 3: a cover-row list
+            constexpr bool kContig = PASS == 1 || PASS == 4;
+            const int nv = kContig ? max(0, min(32, n_f - (U.c0 + 32 * t))) : min(32, U.nlist - 32 * t);
             float4 r[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const int q = 8 * oct + e;
                 r[e] = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (ilive && q < nv) {
-                    const int idx = PASS == 1 ? U.c0 + 32 * t + q : __ldg(&cover[U.list0 + 32 * t + q]);
+                    const int idx = kContig ? U.c0 + 32 * t + q : __ldg(&cover[U.list0 + 32 * t + q]);
                     r[e] = __ldg(&vin[(size_t)idx * S + i0 + il]);
                 }
             }
@@ -1678,6 +1684,30 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     const int li = il;
     const bool live = li < ni;
     const int inst = i0 + li;
+    if (PASS == 3) {   // chain pass: dxt (and the Schur RHS of the slot's single contact) per slot
+        if (!live) return;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
+            if (l < U.nr) chain_rho(S, inst, ex.soff[inst] + U.c0 + l, dacc[0][r], dacc[1][r], dacc[2][r], ex.cc, ex.xs,
+                                    ex.cs);
+        }
+        return;
+    }
+    if (PASS == 4) {   // scatter pass: y[row] += K H^T z on the chain rows
+        if (!live) return;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int l = 8 * oct + r;
+            if (l < U.nr) {
+                const size_t iy = (size_t)ex.orows[U.r0 + l] * S + inst;
+                const float4 yi = yout[iy];
+                yout[iy] = make_float4((float)(yi.x + dacc[0][r]), (float)(yi.y + dacc[1][r]),
+                                       (float)(yi.z + dacc[2][r]), yi.w);
+            }
+        }
+        return;
+    }
     if (PASS == 2) {
         if (!live) return;
 #pragma unroll
@@ -1751,7 +1781,7 @@ void launch_kpass1_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
     const int nch = (S + kTcInst - 1) / kTcInst;
     launch_pdl(k_kpass_ts<1>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, n_f, units, T1tc,
                (const int32_t*)nullptr, u, y, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
-               (double4*)nullptr, 0.0, 0, drain);
+               (double4*)nullptr, 0.0, 0, drain, TsExtra{});
 }
 
 void launch_kpass2_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
@@ -1759,7 +1789,28 @@ void launch_kpass2_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
                       int finalize_v, int drain) {
     const int nch = (S + kTcInst - 1) / kTcInst;
     launch_pdl(k_kpass_ts<2>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, n_f, units, T2tc, cover, y,
-               (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain);
+               (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain, TsExtra{});
+}
+
+void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units, const float* Ttc,
+                          const int32_t* cover, const float4* y, const int* soff, CrContacts cc, const double4* x,
+                          ContactState cs, int drain) {
+    if (nunits == 0) return;
+    const int nch = (S + kTcInst - 1) / kTcInst;
+    TsExtra ex{nullptr, soff, cc, x, cs};
+    launch_pdl(k_kpass_ts<3>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, 0, units, Ttc, cover, y,
+               (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, (double4*)nullptr, (const double4*)nullptr,
+               (double4*)nullptr, 0.0, 0, drain, ex);
+}
+
+void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BUnit* units, const float* Ttc,
+                            const int32_t* rows, const float4* wzT, float4* y, int drain) {
+    if (nunits == 0) return;
+    const int nch = (S + kTcInst - 1) / kTcInst;
+    TsExtra ex{rows, nullptr, CrContacts{}, nullptr, ContactState{}};
+    launch_pdl(k_kpass_ts<4>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, ns, units, Ttc,
+               (const int32_t*)nullptr, wzT, y, (double*)nullptr, (int*)nullptr, nch, (double4*)nullptr,
+               (const double4*)nullptr, (double4*)nullptr, 0.0, 0, drain, ex);
 }
 
 void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,

@@ -148,6 +148,20 @@ void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
 void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
                       const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
                       int finalize_v, int drain);   // drain: tiles accumulated in TMEM (fp32) per fp64 fold
+// extra arguments of the contact passes on the tensor cores
+struct TsExtra {
+    const int32_t* orows;   // scatter pass: output rows
+    const int* soff;        // chain pass: first slot of each instance
+    CrContacts cc;
+    const double4* xs;
+    ContactState cs;
+};
+// contact passes of the single slot-set class (S > 1) on the tensor cores (simhost::ContactPasses)
+void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units, const float* Ttc,
+                          const int32_t* cover, const float4* y, const int* soff, CrContacts cc, const double4* x,
+                          ContactState cs, int drain);
+void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BUnit* units, const float* Ttc,
+                            const int32_t* rows, const float4* wzT, float4* y, int drain);
 // TS variant: right-hand sides staged in TMEM (tcgen05.st) instead of shared memory
 void launch_kpass1_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
                       const float4* u, float4* y, double* part, int* counters, int drain);
