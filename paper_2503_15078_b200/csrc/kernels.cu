@@ -213,6 +213,25 @@ void launch_replicate(cudaStream_t st, const double4* src, double4* dst, int n, 
 // ----------------------------------------------------------------------------
 // local step
 // ----------------------------------------------------------------------------
+// MUFU approximations with flush-to-zero semantics: the same hardware results as __fdividef /
+// rsqrtf / __logf for normal inputs, without the denormal range-scaling fix-ups the non-ftz
+// forms wrap around every MUFU (no denormal ever reaches them here).
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float log_ftz(float x) {   // ln x = log2(x) ln 2, as __logf
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r * 0.693147180559945309f;
+}
+
 // Jacobi eigen-decomposition of a symmetric 3x3 (cyclic, Rutishauser rotations).
 __device__ __forceinline__ void jacobi3(float S[3][3], float V[3][3]) {
 #pragma unroll
@@ -233,12 +252,12 @@ __device__ __forceinline__ void jacobi3(float S[3][3], float V[3][3]) {
             if (fabsf(apq) <= 1e-30f) continue;
             // hardware-approximate reciprocal / square root (MUFU, ~1 ulp): no IEEE fix-up paths;
             // c and s come from the same t, so the rotation stays orthogonal to ~1e-7
-            float theta = __fdividef(S[q][q] - S[p][p], 2.f * apq);
+            float theta = (S[q][q] - S[p][p]) * rcp_ftz(2.f * apq);
             float at = fabsf(theta);
             const float w = theta * theta + 1.f;
-            float t = at > 1e15f ? __fdividef(0.5f, at) : __fdividef(1.f, at + w * rsqrtf(w));
+            float t = at > 1e15f ? 0.5f * rcp_ftz(at) : rcp_ftz(at + w * rsqrt_ftz(w));
             t = theta < 0.f ? -t : t;
-            float c = rsqrtf(t * t + 1.f);
+            float c = rsqrt_ftz(t * t + 1.f);
             float s = t * c;
             S[p][p] -= t * apq;
             S[q][q] += t * apq;
@@ -271,7 +290,7 @@ __device__ __forceinline__ void swapcol(float V[3][3], float* e, int a, int b) {
 // NH objective in sigma space: k/2|p-sig|^2 + mu/2(|p|^2-3) - mu lnJ + lam/2 ln^2 J
 // (ln J = ln(p0 p1 p2): one hardware log2 instead of three IEEE logs)
 __device__ __forceinline__ float nh_f(const float p[3], const float sg[3], float k, float mu, float lam) {
-    float lnJ = __logf(p[0] * p[1] * p[2]);
+    float lnJ = log_ftz(p[0] * p[1] * p[2]);
     float d0 = p[0] - sg[0], d1 = p[1] - sg[1], d2 = p[2] - sg[2];
     return 0.5f * k * (d0 * d0 + d1 * d1 + d2 * d2) +
            0.5f * mu * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2] - 3.f) - mu * lnJ + 0.5f * lam * lnJ * lnJ;
@@ -299,8 +318,8 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
     float scale = fmaxf(1.f, sqrtf(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]));
 #pragma unroll 1
     for (int it = 0; it < 16; ++it) {
-        float lnJ = __logf(p[0] * p[1] * p[2]);
-        float iv[3] = {__fdividef(1.f, p[0]), __fdividef(1.f, p[1]), __fdividef(1.f, p[2])};
+        float lnJ = log_ftz(p[0] * p[1] * p[2]);
+        float iv[3] = {rcp_ftz(p[0]), rcp_ftz(p[1]), rcp_ftz(p[2])};
         float g[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) g[i] = k * (p[i] - sg[i]) + mu * p[i] - mu * iv[i] + lam * lnJ * iv[i];
@@ -320,7 +339,7 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
         float dd[3];
         bool ok = fabsf(det) > 0.f && isfinite(det);
         if (ok) {
-            float id = __fdividef(1.f, det);
+            float id = rcp_ftz(det);
             float c10 = H[0][2] * H[2][1] - H[0][1] * H[2][2];
             float c11 = H[0][0] * H[2][2] - H[0][2] * H[2][0];
             float c12 = H[0][1] * H[2][0] - H[0][0] * H[2][1];
@@ -334,7 +353,7 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
             ok = slope < 0.f && isfinite(slope);
         }
         if (!ok) {
-            float s = __fdividef(-1.f, k + mu);
+            float s = -rcp_ftz(k + mu);
             dd[0] = s * g[0];
             dd[1] = s * g[1];
             dd[2] = s * g[2];
@@ -432,9 +451,9 @@ __global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, con
         for (int j = 0; j < 3; ++j) FV[i][j] = F[i][0] * V[0][j] + F[i][1] * V[1][j] + F[i][2] * V[2][j];
     float U[3][3];
     const float q0 = FV[0][0] * FV[0][0] + FV[1][0] * FV[1][0] + FV[2][0] * FV[2][0];
-    float n0 = q0 > 0.f ? q0 * rsqrtf(q0) : 0.f;
+    float n0 = q0 > 0.f ? q0 * rsqrt_ftz(q0) : 0.f;
     if (q0 > 1e-36f) {
-        const float r0 = rsqrtf(q0);
+        const float r0 = rsqrt_ftz(q0);
         U[0][0] = FV[0][0] * r0; U[1][0] = FV[1][0] * r0; U[2][0] = FV[2][0] * r0;
     } else {
         U[0][0] = 1.f; U[1][0] = 0.f; U[2][0] = 0.f;
@@ -442,9 +461,9 @@ __global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, con
     float dt = U[0][0] * FV[0][1] + U[1][0] * FV[1][1] + U[2][0] * FV[2][1];
     float w0 = FV[0][1] - dt * U[0][0], w1 = FV[1][1] - dt * U[1][0], w2 = FV[2][1] - dt * U[2][0];
     const float q1 = w0 * w0 + w1 * w1 + w2 * w2;
-    float n1 = q1 > 0.f ? q1 * rsqrtf(q1) : 0.f;
+    float n1 = q1 > 0.f ? q1 * rsqrt_ftz(q1) : 0.f;
     if (n1 > 1e-30f * fmaxf(1.f, n0)) {
-        const float r1 = rsqrtf(q1);
+        const float r1 = rsqrt_ftz(q1);
         U[0][1] = w0 * r1; U[1][1] = w1 * r1; U[2][1] = w2 * r1;
     } else {   // any unit vector orthogonal to u0
         float a0 = U[0][0], a1 = U[1][0], a2 = U[2][0];
