@@ -2580,7 +2580,8 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
     const int na = X.na;
     double* qb = X.q + (size_t)buf * 3 * X.na;   // SoA: q0 | q1 | q2
     const unsigned bar = X.mbar + 8u * (unsigned)buf;
-    if (threadIdx.x == 0 && na > 0)   // this phase expects 24 bytes per row of G_A from the peers
+    const bool solo = X.csize == 1;   // one CTA per instance: q stays local, no cluster exchange
+    if (!solo && threadIdx.x == 0 && na > 0)   // this phase expects 24 bytes per row of G_A from the peers
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(24 * na) : "memory");
     for (int i = threadIdx.x; i < na; i += blockDim.x) {
         double w0 = 0.0, w1 = 0.0, w2 = 0.0;
@@ -2637,7 +2638,13 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
         d0 = warp_sum(d0);
         d1 = warp_sum(d1);
         d2 = warp_sum(d2);
-        if (lane < X.csize) {
+        if (solo) {
+            if (lane == 0) {
+                qb[i] = d0;
+                qb[na + i] = d1;
+                qb[2 * na + i] = d2;
+            }
+        } else if (lane < X.csize) {
             // asynchronous stores of q_i into CTA `lane` of the cluster, completing 24 tx bytes on its mbarrier
             const unsigned l0 = (unsigned)__cvta_generic_to_shared(qb + i);
             const unsigned l1 = (unsigned)__cvta_generic_to_shared(qb + na + i);
@@ -2659,7 +2666,7 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
         }
     }
     if (X.stamp >= 0) cr_stamp(X.stamp + 1);
-    if (threadIdx.x == 0 && na > 0) {   // wait until all na rows have landed here (acquire)
+    if (!solo && threadIdx.x == 0 && na > 0) {   // wait until all na rows have landed here (acquire)
         unsigned done = 0;
         while (!done) {
             asm volatile(
@@ -2670,7 +2677,9 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
                 : "memory");
         }
     }
-    if (buf) X.par1 ^= 1u; else X.par0 ^= 1u;
+    if (!solo) {
+        if (buf) X.par1 ^= 1u; else X.par0 ^= 1u;
+    }
     __syncthreads();
     if (X.stamp >= 0) cr_stamp(X.stamp + 2);
 #pragma unroll
@@ -2771,10 +2780,11 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     X.i0 = i0;
     X.i1 = i1;
     X.gA_smem = L.total + needA <= kCrMaxSmem;
-    if (X.gA_smem) {
+    if (X.gA_smem) {   // asynchronous 4-byte copies, all in flight (waited for with the rest below)
         const float* src = X.GAg + (size_t)X.i0 * na;
         const int n = (X.i1 - X.i0) * na;
-        for (int e = threadIdx.x; e < n; e += blockDim.x) X.gA[e] = __ldcg(&src[e]);
+        for (int e = threadIdx.x; e < n; e += blockDim.x) cp_async4(&X.gA[e], &src[e], true);
+        cp_async_commit();
     }
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
 #pragma unroll
