@@ -2617,7 +2617,52 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
     __syncthreads();
     if (X.stamp >= 0) cr_stamp(X.stamp);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int i = X.i0 + wid; i < X.i1; i += nw) {
+    if (solo) {   // the whole G_A in this CTA: four rows per warp at a time (8 G_A loads in flight per lane)
+        for (int i = wid; i < na; i += 4 * nw) {
+            double d[4][3];
+            const float* g[4];
+            bool ok[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int ik = i + k * nw;
+                ok[k] = ik < na;
+                g[k] = X.gA_smem ? X.gA + (size_t)(ok[k] ? ik : 0) * na : X.GAg + (size_t)(ok[k] ? ik : 0) * na;
+                d[k][0] = d[k][1] = d[k][2] = 0.0;
+            }
+            for (int b0 = 0; b0 < na; b0 += 64) {
+                float gv[4][2];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int bb = b0 + 32 * u + lane;
+                        gv[k][u] = (ok[k] && bb < na) ? (X.gA_smem ? g[k][bb] : __ldcg(&g[k][bb])) : 0.f;
+                    }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int bb = min(b0 + 32 * u + lane, na - 1);
+                    const double w0 = X.W[bb], w1 = X.W[na + bb], w2 = X.W[2 * na + bb];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        d[k][0] = fma((double)gv[k][u], w0, d[k][0]);
+                        d[k][1] = fma((double)gv[k][u], w1, d[k][1]);
+                        d[k][2] = fma((double)gv[k][u], w2, d[k][2]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double e0 = warp_sum(d[k][0]), e1 = warp_sum(d[k][1]), e2 = warp_sum(d[k][2]);
+                if (lane == 0 && ok[k]) {
+                    const int ik = i + k * nw;
+                    qb[ik] = e0;
+                    qb[na + ik] = e1;
+                    qb[2 * na + ik] = e2;
+                }
+            }
+        }
+    }
+    for (int i = X.i0 + wid; !solo && i < X.i1; i += nw) {
         const float* g = X.gA_smem ? X.gA + (size_t)(i - X.i0) * na : X.GAg + (size_t)i * na;
         double d0 = 0, d1 = 0, d2 = 0;
         for (int b0 = 0; b0 < na; b0 += 128) {
