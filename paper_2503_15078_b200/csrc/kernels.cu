@@ -2869,7 +2869,10 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     }
     cl.sync();   // smem staged everywhere; every CTA's exchange mbarriers initialised
     cr_stamp(1);
-    if (threadIdx.x == 0 && blockIdx.x == 0) g_cr_clock[31] = g_cr_clock[0] + 1000ull * na;   // na (debug)
+    if (threadIdx.x == 0 && blockIdx.x == 0) {   // debug: na, G_A placement (1 = shared memory), csize
+        g_cr_clock[31] = g_cr_clock[0] + 1000ull * na;
+        g_cr_clock[30] = g_cr_clock[0] + 1000ull * (X.gA_smem ? 1 : 0) + 10000ull * csize;
+    }
     double rr = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) rr = fma(p[k], p[k], rr);

@@ -17,4 +17,4 @@ for f in range(3):
     s.step(1, 5)
 s.synchronize()
 tl = debug_cr_timeline(s)
-print("S", S, "CR timeline us:", " ".join(f"{v:.1f}" for v in tl[:12]), "| it3: start %.1f W %.1f mv %.1f wait %.1f Sv %.1f end %.1f" % tuple(tl[12:18]), "| end", f"{tl[20]:.1f} {tl[21]:.1f}", "na", int(tl[31]))
+print("S", S, "CR timeline us:", " ".join(f"{v:.1f}" for v in tl[:12]), "| it3: start %.1f W %.1f mv %.1f wait %.1f Sv %.1f end %.1f" % tuple(tl[12:18]), "| end", f"{tl[20]:.1f} {tl[21]:.1f}", "na", int(tl[31]), "gA_smem+10*csize", tl[30])
