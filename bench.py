@@ -202,6 +202,19 @@ def reduce_max(v, ws, device=None):
     return float(t.item())
 
 
+def gather_stats(row, ws, device=None):
+    """All-gather of one fixed-length row of per-rank results after the timed region (NCCL over
+    NVLink on the GPU box, gloo in the CPU tests): returns the [ws][len] list on every rank."""
+    if ws == 1:
+        return [list(map(float, row))]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v) for v in row], dtype=torch.float64, device=device)
+    out = torch.empty(ws * t.numel(), dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(out, t)
+    return out.view(ws, -1).cpu().tolist()
+
+
 def measure(args, S, rank, ws, dev, stream, full=True):
     """Time `args.steps` frames of S cfg3 instances (one handle) on this rank.
     Returns a dict of per-rank numbers (device ms, kernel profile, e2e, ...)."""
@@ -310,6 +323,11 @@ def measure(args, S, rank, ws, dev, stream, full=True):
     out["h2d"] = int(st["h2d_contact_bytes"])
     out["d2h"] = 24 * sc.mesh.n_v * S
     out["kernels_per_frame"] = int(st["kernels_per_frame"])
+    # per-rank result summary for the post-run gather: instances, frames, active contacts, max CR
+    # residual, mean |x - X| over all instances (checksum of the state)
+    P = s.get_positions()
+    out["summary"] = [S, int(st["frames_done"]), int(st["n_active"]), float(st["last_cr_residual"]),
+                      float(np.abs(P - sc.mesh.X[None]).mean())]
     s.close()
     return out
 
@@ -431,6 +449,7 @@ def run_ours(args):
         return reduce_max(v, ws, dev)
 
     total_ms = max_over_ranks(r["total_ms"])
+    gathered = gather_stats(r["summary"], ws, dev)   # results and stats of every rank (NCCL all_gather)
     e2e_ms = max_over_ranks(r["e2e_ms"])
     # single-scene latency (cfg3, S = 1): the paper-comparable ms per L-G iteration
     r1 = measure(args, 1, rank, ws, dev, stream, full=False) if S > 1 else r
@@ -491,6 +510,8 @@ def run_ours(args):
         "breakdown": r["breakdown"],
         "roofline": roofline,
         "rooflines": rooflines,
+        "ranks": [{"instances": int(g[0]), "frames": int(g[1]), "active_contacts": int(g[2]),
+                   "max_cr_residual": g[3], "mean_displacement_m": g[4]} for g in gathered],
         "pile_cfg4": pile,
         "cpu_baseline": cpu,
         "clocks": r["clocks"],

@@ -23,7 +23,8 @@ def _worker(rank, ws, port, q):
     ids = bench.instance_ids(ws, rank)
     weak = bench.instance_ids(ws, rank, per_gpu=3)
     m = bench.reduce_max(10.0 + rank, ws)
-    q.put((rank, ids, weak, m))
+    g = bench.gather_stats([rank, 2.5 * rank, 7.0], ws)
+    q.put((rank, ids, weak, m, g))
     dist.destroy_process_group()
 
 
@@ -39,8 +40,10 @@ def test_cfg5_sharding_and_max_timing(ws):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    ids = [i for _, a, _, _ in out for i in a]
+    ids = [i for _, a, _, _, _ in out for i in a]
     assert sorted(ids) == list(range(1024))          # strong scaling: exact partition of the batch
-    weak = [i for _, _, w, _ in out for i in w]
+    weak = [i for _, _, w, _, _ in out for i in w]
     assert sorted(weak) == list(range(3 * ws))       # weak scaling: 3 per rank, disjoint
-    assert all(m == 10.0 + ws - 1 for *_, m in out)  # max over ranks on every rank
+    assert all(m == 10.0 + ws - 1 for *_, m, _ in out)  # max over ranks on every rank
+    for *_, g in out:                                   # every rank holds every rank's row
+        assert g == [[float(r), 2.5 * r, 7.0] for r in range(ws)]
