@@ -2812,9 +2812,11 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     if (c9s)
         for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[9 * cb + e], true);
     for (int b = threadIdx.x; b < ns; b += blockDim.x) {
-        cp_async4(&X.aidx[b], &act.aidx[sb + b], true);
         cp_async4(&X.apos[b], &act.apos[sb + b], true);
-        cp_async4(&X.acon[b], &act.acon[sb + b], true);
+        if (b < na) {   // k_active writes aidx/acon for the na active slots only
+            cp_async4(&X.aidx[b], &act.aidx[sb + b], true);
+            cp_async4(&X.acon[b], &act.acon[sb + b], true);
+        }
     }
     cp_async_commit();
     for (int c = threadIdx.x; c < nc; c += blockDim.x) {
@@ -2931,8 +2933,8 @@ __global__ void __launch_bounds__(kCrThreads, 1)
             ApAp = s2 + 2.0 * beta * s3 + beta * beta * ApAp;
 #pragma unroll
             for (int k = 0; k < kRpt; ++k) {
-                const int j = min(threadIdx.x + kCrThreads * k, m - 1);
-                p[k] = X.r[j] + beta * p[k];
+                const int j = threadIdx.x + kCrThreads * k;   // entries past m stay 0
+                p[k] = j < m ? X.r[j] + beta * p[k] : 0.0;
                 Ap[k] = Ar[k] + beta * Ap[k];
             }
             if (it == 3) cr_stamp(17);
