@@ -2516,8 +2516,10 @@ constexpr int kRptMax = 6;   // rows per thread: m = 3 nc <= kRpt * kCrThreads (
 // contact directions c9 are staged only when they fit next to this CTA's rows of G_A
 struct CrLayout {
     int m, nc, ns;
-    size_t r, th, cd, s0, aidx, apos, acon, red, mbar, W, q, c9, gA, total;
-    __host__ __device__ CrLayout(int nc_, int ns_, int na, bool with_c9) : m(3 * nc_), nc(nc_), ns(ns_) {
+    size_t r, th, cd, s0, aidx, apos, acon, red, mbar, W, q, qp, c9, gA, total;
+    // parts > 1: the solo matvec splits the columns of G_A over `parts` thread groups (partial sums in qp)
+    __host__ __device__ CrLayout(int nc_, int ns_, int na, bool with_c9, int parts = 1)
+        : m(3 * nc_), nc(nc_), ns(ns_) {
         size_t o = 0;
         auto take = [&](size_t bytes) { size_t at = o; o += (bytes + 15) & ~size_t(15); return at; };
         r = take(8 * (size_t)m);
@@ -2527,6 +2529,7 @@ struct CrLayout {
         red = take(8 * 2 * 3 * (kCrThreads / 32));   // double-buffered 3 doubles per warp
         mbar = take(32);                              // two exchange mbarriers (one per q buffer)
         W = take(8 * 3 * (size_t)na); q = take(8 * 2 * 3 * (size_t)na);
+        qp = parts > 1 ? take(8 * 3 * (size_t)na * parts) : 0;
         c9 = with_c9 ? take(4 * 9 * (size_t)nc) : 0;
         gA = o;
         total = o;
@@ -2552,10 +2555,11 @@ struct CrInst {
 };
 
 struct CrCtx {
-    double *r, *W, *q, *red;
+    double *r, *W, *q, *qp, *red;
     float *gA, *th, *cd, *c9;
     int *s0, *aidx, *apos, *acon;
     int na, ns, i0, i1, gA_smem, csize;
+    int lda, parts;        // solo path: G_A row stride in shared memory (odd), column groups
     unsigned mbar;         // shared-window address of the 2 exchange mbarriers
     unsigned par0, par1;   // phase parity of each barrier
     int stamp;             // >= 0: fine-grained phase stamps of this apply at g_cr_clock[stamp..]
@@ -2617,7 +2621,50 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
     __syncthreads();
     if (X.stamp >= 0) cr_stamp(X.stamp);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    if (solo) {   // the whole G_A in this CTA: four rows per warp at a time (8 G_A loads in flight per lane)
+    if (solo && X.gA_smem) {
+        // one row of G_A per thread (odd row stride: the 32 rows a warp reads sit in 32 banks; W is a
+        // broadcast), the columns split over `parts` groups of threads whose partial sums are added in
+        // part order (deterministic); no warp reductions
+        const int nap = (na + 31) & ~31, P = X.parts, cs = (na + P - 1) / P;
+        for (int t = threadIdx.x; t < nap * P; t += blockDim.x) {
+            const int part = t / nap, i = t - part * nap;
+            if (i >= na) continue;
+            const float* g = X.gA + (size_t)i * X.lda;
+            const int b1 = min(na, (part + 1) * cs);
+            int b = part * cs;
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+            for (; b + 4 <= b1; b += 4) {
+                float gv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) gv[u] = g[b + u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double gd = (double)gv[u];
+                    d0 = fma(gd, X.W[b + u], d0);
+                    d1 = fma(gd, X.W[na + b + u], d1);
+                    d2 = fma(gd, X.W[2 * na + b + u], d2);
+                }
+            }
+            for (; b < b1; ++b) {
+                const double gd = (double)g[b];
+                d0 = fma(gd, X.W[b], d0);
+                d1 = fma(gd, X.W[na + b], d1);
+                d2 = fma(gd, X.W[2 * na + b], d2);
+            }
+            double* o = P > 1 ? X.qp + (size_t)part * 3 * na : qb;
+            o[i] = d0;
+            o[na + i] = d1;
+            o[2 * na + i] = d2;
+        }
+        if (P > 1) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < 3 * na; e += blockDim.x) {
+                double acc = X.qp[e];
+                for (int q = 1; q < P; ++q) acc += X.qp[(size_t)q * 3 * na + e];
+                qb[e] = acc;
+            }
+        }
+    } else if (solo) {   // G_A in global memory: four rows per warp at a time (8 G_A loads in flight per lane)
         for (int i = wid; i < na; i += 4 * nw) {
             double d[4][3];
             const float* g[4];
@@ -2626,7 +2673,7 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
             for (int k = 0; k < 4; ++k) {
                 const int ik = i + k * nw;
                 ok[k] = ik < na;
-                g[k] = X.gA_smem ? X.gA + (size_t)(ok[k] ? ik : 0) * na : X.GAg + (size_t)(ok[k] ? ik : 0) * na;
+                g[k] = X.GAg + (size_t)(ok[k] ? ik : 0) * na;
                 d[k][0] = d[k][1] = d[k][2] = 0.0;
             }
             for (int b0 = 0; b0 < na; b0 += 64) {
@@ -2636,7 +2683,7 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
                         const int bb = b0 + 32 * u + lane;
-                        gv[k][u] = (ok[k] && bb < na) ? (X.gA_smem ? g[k][bb] : __ldcg(&g[k][bb])) : 0.f;
+                        gv[k][u] = (ok[k] && bb < na) ? __ldcg(&g[k][bb]) : 0.f;
                     }
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
@@ -2776,11 +2823,14 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     const int na = act.na[inst];
     const int per = (na + csize - 1) / csize;
     const int i0 = min(na, rank * per), i1 = min(na, i0 + per);
-    const size_t needA = (size_t)(i1 - i0) * na * sizeof(float);
+    const bool solo = csize == 1;
+    const int lda = solo ? (na | 1) : na;
+    const int parts = solo ? max(1, min(4, kCrThreads / max(32, (na + 31) & ~31))) : 1;
+    const size_t needA = (size_t)(i1 - i0) * lda * sizeof(float);
     // prefer G_A rows in shared memory; stage c9 too when both fit
-    const bool c9s = CrLayout(nc, ns, na, true).total + needA <= kCrMaxSmem ||
-                     CrLayout(nc, ns, na, false).total + needA > kCrMaxSmem;
-    const CrLayout L(nc, ns, na, c9s);
+    const bool c9s = CrLayout(nc, ns, na, true, parts).total + needA <= kCrMaxSmem ||
+                     CrLayout(nc, ns, na, false, parts).total + needA > kCrMaxSmem;
+    const CrLayout L(nc, ns, na, c9s, parts);
     CrInst I{C + cb, sl.scp + sb, sl.sci, sl.scw, cb, sb, S, inst};
     double* th_g = cs.theta + 3 * cb;
     double* cd_g = cs.cdiag + 3 * cb;
@@ -2797,6 +2847,9 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     X.s0 = (int*)(smraw + L.s0);
     X.W = (double*)(smraw + L.W);
     X.q = (double*)(smraw + L.q);
+    X.qp = (double*)(smraw + L.qp);
+    X.lda = lda;
+    X.parts = parts;
     X.aidx = (int*)(smraw + L.aidx);
     X.apos = (int*)(smraw + L.apos);
     X.acon = (int*)(smraw + L.acon);
@@ -2829,8 +2882,10 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     X.gA_smem = L.total + needA <= kCrMaxSmem;
     if (X.gA_smem) {   // asynchronous 4-byte copies, all in flight (waited for with the rest below)
         const float* src = X.GAg + (size_t)X.i0 * na;
-        const int n = (X.i1 - X.i0) * na;
-        for (int e = threadIdx.x; e < n; e += blockDim.x) cp_async4(&X.gA[e], &src[e], true);
+        const int rows = X.i1 - X.i0;
+        for (int rw = threadIdx.x >> 5; rw < rows; rw += blockDim.x >> 5)
+            for (int c = threadIdx.x & 31; c < na; c += 32)
+                cp_async4(&X.gA[(size_t)rw * lda + c], &src[(size_t)rw * na + c], true);
         cp_async_commit();
     }
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
