@@ -1988,8 +1988,10 @@ void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots 
 // ascending slot order, and the active block G_A of the Delassus Gram.  These depend only
 // on theta, so they run in a graph branch beside the RHS gather and K-pass 1.
 // ----------------------------------------------------------------------------
+__host__ __device__ bool cr_ga_direct(int nc, int ns, int na, int csize);
 __global__ void __launch_bounds__(1024) k_active(InstOff off, CrContacts cc, Slots sl, ContactState cs,
-                                                 CrActive act) {
+                                                 CrActive act, int csize, const float* __restrict__ G,
+                                                 float* __restrict__ GA) {
     pdl_enter();
     __shared__ int wsum[32];
     __shared__ int base;
@@ -2035,9 +2037,20 @@ __global__ void __launch_bounds__(1024) k_active(InstOff off, CrContacts cc, Slo
         __syncthreads();
     }
     if (threadIdx.x == 0) act.na[inst] = base;
+    // G_A[i][j] = G[aidx_i][aidx_j] for a lone-CTA CR whose G_A does not fit in shared memory (one
+    // warp per row; k_gather_ga serves the cluster CR); the CR gathers it into shared memory otherwise
+    const int na = base, nc = off.coff[inst + 1] - cb;
+    if (na == 0 || csize != 1 || cr_ga_direct(nc, ns, na, csize)) return;
+    const float* Gc = G + off.goff[off.cls[inst]];
+    float* GAi = GA + off.gaoff[inst];
+    for (int i = wid; i < na; i += blockDim.x >> 5) {
+        const float* Gi = Gc + (size_t)act.aidx[sb + i] * ns;
+        for (int j = lane; j < na; j += 32) GAi[(size_t)i * na + j] = Gi[act.aidx[sb + j]];
+    }
 }
 
-// G_A[i][j] = G[aidx_i][aidx_j] (instance blockIdx.y, active row blockIdx.x)
+// G_A[i][j] = G[aidx_i][aidx_j] (instance blockIdx.y, active row blockIdx.x): the cluster CR (few
+// instances), whose CTAs each copy their rows of G_A from this global copy
 __global__ void __launch_bounds__(256) k_gather_ga(InstOff off, const float* __restrict__ G, CrActive act,
                                                    float* __restrict__ GA) {
     pdl_enter();
@@ -2054,8 +2067,9 @@ __global__ void __launch_bounds__(256) k_gather_ga(InstOff off, const float* __r
 void launch_active(cudaStream_t st, const Params& P, InstOff off, CrContacts cc, Slots sl, ContactState cs,
                    CrActive act, const float* G, float* GA) {
     if (P.NS == 0) return;
-    k_active<<<P.S, 1024, 0, st>>>(off, cc, sl, cs, act);
-    k_gather_ga<<<dim3(P.ns_max, P.S), 256, 0, st>>>(off, G, act, GA);
+    const int csize = cr_cluster_size(P.S);
+    k_active<<<P.S, 1024, 0, st>>>(off, cc, sl, cs, act, csize, G, GA);
+    if (csize > 1) k_gather_ga<<<dim3(P.ns_max, P.S), 256, 0, st>>>(off, G, act, GA);
 }
 
 // per-contact-set: chain rows of every class slot (walk panel runs), per-class row flags;
@@ -2536,6 +2550,20 @@ struct CrLayout {
     }
 };
 
+// CR shape of one instance: the G_A row stride in shared memory and the column groups of the
+// one-CTA-per-instance matvec
+__host__ __device__ inline int cr_lda(int na, int csize) { return csize == 1 ? (na | 1) : na; }
+__host__ __device__ inline int cr_parts(int na, int csize) {
+    return csize == 1 ? max(1, min(4, kCrThreads / max(32, (na + 31) & ~31))) : 1;
+}
+// a lone CTA holds the whole instance and its G_A fits next to the minimal layout: it gathers
+// G_A from the class Gram itself (k_active skips the global copy)
+__host__ __device__ bool cr_ga_direct(int nc, int ns, int na, int csize) {
+    if (csize != 1) return false;
+    return CrLayout(nc, ns, na, false, cr_parts(na, csize)).total + (size_t)na * cr_lda(na, csize) * sizeof(float) <=
+           kCrMaxSmem;
+}
+
 __device__ unsigned long long g_cr_clock[32];   // phase timestamps (ns) of the last CR call, instance 0 rank 0
 __device__ __forceinline__ void cr_stamp(int i) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -2803,7 +2831,7 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
 // instances fill the GPU).  Launched with a runtime cluster dimension (cudaLaunchKernelEx).
 template <int kRpt>
 __global__ void __launch_bounds__(kCrThreads, 1)
-    k_cr(Params P, InstOff off, const DContact* __restrict__ C, CrContacts cc, Slots sl,
+    k_cr(Params P, InstOff off, const DContact* __restrict__ C, CrContacts cc, Slots sl, const float* __restrict__ G,
          const float* __restrict__ GA, const double4* __restrict__ x, ContactState cs, CrActive act) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -2824,8 +2852,8 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     const int per = (na + csize - 1) / csize;
     const int i0 = min(na, rank * per), i1 = min(na, i0 + per);
     const bool solo = csize == 1;
-    const int lda = solo ? (na | 1) : na;
-    const int parts = solo ? max(1, min(4, kCrThreads / max(32, (na + 31) & ~31))) : 1;
+    const int lda = cr_lda(na, csize);
+    const int parts = cr_parts(na, csize);
     const size_t needA = (size_t)(i1 - i0) * lda * sizeof(float);
     // prefer G_A rows in shared memory; stage c9 too when both fit
     const bool c9s = CrLayout(nc, ns, na, true, parts).total + needA <= kCrMaxSmem ||
@@ -2881,11 +2909,22 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     X.i1 = i1;
     X.gA_smem = L.total + needA <= kCrMaxSmem;
     if (X.gA_smem) {   // asynchronous 4-byte copies, all in flight (waited for with the rest below)
-        const float* src = X.GAg + (size_t)X.i0 * na;
-        const int rows = X.i1 - X.i0;
-        for (int rw = threadIdx.x >> 5; rw < rows; rw += blockDim.x >> 5)
-            for (int c = threadIdx.x & 31; c < na; c += 32)
-                cp_async4(&X.gA[(size_t)rw * lda + c], &src[(size_t)rw * na + c], true);
+        if (solo) {       // G_A[i][j] = G[aidx_i][aidx_j] straight from the class Gram (cr_ga_direct)
+            cp_async_wait<0>();
+            __syncthreads();   // aidx staged
+            const float* Gc = G + off.goff[off.cls[inst]];
+            for (int rw = threadIdx.x >> 5; rw < na; rw += blockDim.x >> 5) {
+                const float* Gi = Gc + (size_t)X.aidx[rw] * ns;
+                for (int c = threadIdx.x & 31; c < na; c += 32)
+                    cp_async4(&X.gA[(size_t)rw * lda + c], &Gi[X.aidx[c]], true);
+            }
+        } else {          // this CTA's rows of the G_A copy k_active wrote
+            const float* src = X.GAg + (size_t)X.i0 * na;
+            const int rows = X.i1 - X.i0;
+            for (int rw = threadIdx.x >> 5; rw < rows; rw += blockDim.x >> 5)
+                for (int c = threadIdx.x & 31; c < na; c += 32)
+                    cp_async4(&X.gA[(size_t)rw * lda + c], &src[(size_t)rw * na + c], true);
+        }
         cp_async_commit();
     }
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
@@ -3388,7 +3427,7 @@ int cr_cluster_size(int S) {
 }
 
 int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, CrContacts cc, Slots sl,
-              const float* GA, const double4* x, ContactState cs, CrActive act) {
+              const float* G, const float* GA, const double4* x, ContactState cs, CrActive act) {
     if (P.C == 0) return 0;
     static bool attr = false;
     if (!attr) {
@@ -3420,12 +3459,12 @@ int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, 
     cudaError_t e;
     switch (rpt) {
         case 0:
-        case 1: e = cudaLaunchKernelEx(&cfg, k_cr<1>, P, off, c, cc, sl, GA, x, cs, act); break;
-        case 2: e = cudaLaunchKernelEx(&cfg, k_cr<2>, P, off, c, cc, sl, GA, x, cs, act); break;
-        case 3: e = cudaLaunchKernelEx(&cfg, k_cr<3>, P, off, c, cc, sl, GA, x, cs, act); break;
-        case 4: e = cudaLaunchKernelEx(&cfg, k_cr<4>, P, off, c, cc, sl, GA, x, cs, act); break;
-        case 5: e = cudaLaunchKernelEx(&cfg, k_cr<5>, P, off, c, cc, sl, GA, x, cs, act); break;
-        default: e = cudaLaunchKernelEx(&cfg, k_cr<6>, P, off, c, cc, sl, GA, x, cs, act); break;
+        case 1: e = cudaLaunchKernelEx(&cfg, k_cr<1>, P, off, c, cc, sl, G, GA, x, cs, act); break;
+        case 2: e = cudaLaunchKernelEx(&cfg, k_cr<2>, P, off, c, cc, sl, G, GA, x, cs, act); break;
+        case 3: e = cudaLaunchKernelEx(&cfg, k_cr<3>, P, off, c, cc, sl, G, GA, x, cs, act); break;
+        case 4: e = cudaLaunchKernelEx(&cfg, k_cr<4>, P, off, c, cc, sl, G, GA, x, cs, act); break;
+        case 5: e = cudaLaunchKernelEx(&cfg, k_cr<5>, P, off, c, cc, sl, G, GA, x, cs, act); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_cr<6>, P, off, c, cc, sl, G, GA, x, cs, act); break;
     }
     return (int)e;
 }

@@ -175,8 +175,10 @@ void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots 
 
 void launch_active(cudaStream_t st, const Params& P, InstOff off, CrContacts cc, Slots sl, ContactState cs,
                    CrActive act, const float* G, float* GA);
+// G: the class Delassus Grams; a CTA that owns a whole instance gathers its G_A rows from G straight
+// into shared memory (cr_ga_direct), else it reads the G_A copy k_active wrote to GA
 int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, CrContacts cc, Slots sl,
-              const float* GA, const double4* x, ContactState cs, CrActive act);
+              const float* G, const float* GA, const double4* x, ContactState cs, CrActive act);
 // y_i += sum_{slots s in subtree(i)} K[i][a_s] wz_s over the rows of each instance's ulist
 // (int4 {row, s0, s1, zoff}); max_rows bounds the per-instance list length
 // grouped: items int2 {class, member0} (32 members per item)
