@@ -135,7 +135,8 @@ struct sim_handle {
     DBuf<double> M;
     DBuf<int4> tet;
     DBuf<float> Bm, hw2;
-    DBuf<float4> fc, u, y;
+    DBuf<float> fc;          // corner forces [tet][corner][xyz][instance]
+    DBuf<float4> u, y;
     DBuf<int32_t> adjp, adj;
     // device: K
     DBuf<float> Krow, Kcol, T1, T2, T1p;   // K row/column-major + the passes' tile streams
@@ -403,7 +404,7 @@ static int upload_all(sim_handle* H) {
     CK(H->tet.alloc(nt)); CK(H->tet.upload(tv.data(), nt, st));
     CK(H->Bm.alloc((size_t)9 * nt)); CK(H->Bm.upload(Bm.data(), (size_t)9 * nt, st));
     CK(H->hw2.alloc(nt)); CK(H->hw2.upload(hw.data(), nt, st));
-    CK(H->fc.alloc((size_t)4 * nt * S));
+    CK(H->fc.alloc((size_t)12 * nt * S));
     CK(H->u.alloc((size_t)nf * S)); CK(H->y.alloc((size_t)nf * S));
     CK(cudaMemsetAsync(H->u.p, 0, (size_t)nf * S * sizeof(float4), st));
     CK(cudaMemsetAsync(H->y.p, 0, (size_t)nf * S * sizeof(float4), st));

@@ -391,7 +391,7 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
 template <int MODEL>
 __global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, const int4* __restrict__ tet, const float* __restrict__ Bm,
                                                const float* __restrict__ hw2, const double4* __restrict__ x,
-                                               float4* __restrict__ fc, float* __restrict__ Pdbg,
+                                               float* __restrict__ fc, float* __restrict__ Pdbg,
                                                float* __restrict__ du, int admm_first) {
     pdl_enter();
     const int SI = P.S;
@@ -517,15 +517,17 @@ __global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, con
     for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int i = 0; i < 3; ++i) f[a][i] = Q[i][0] * B[3 * a + 0] + Q[i][1] * B[3 * a + 1] + Q[i][2] * B[3 * a + 2];
-    float4* o = fc + 4 * (size_t)t * SI + inst;   // [tet][corner][instance]
-    o[0] = make_float4(-(f[0][0] + f[1][0] + f[2][0]), -(f[0][1] + f[1][1] + f[2][1]), -(f[0][2] + f[1][2] + f[2][2]), 0.f);
-    o[SI] = make_float4(f[0][0], f[0][1], f[0][2], 0.f);
-    o[2 * SI] = make_float4(f[1][0], f[1][1], f[1][2], 0.f);
-    o[3 * SI] = make_float4(f[2][0], f[2][1], f[2][2], 0.f);
+    float* o = fc + 12 * (size_t)t * SI + inst;   // [tet][corner][component][instance], no padding
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        o[i * SI] = -(f[0][i] + f[1][i] + f[2][i]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) o[(3 * (a + 1) + i) * SI] = f[a][i];
+    }
 }
 
 void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
-                  const double4* x, float4* fc, float* Pdbg, float* du, int admm_first) {
+                  const double4* x, float* fc, float* Pdbg, float* du, int admm_first) {
     const unsigned g = (unsigned)((P.n_t * (size_t)P.S + 127) / 128);
     if (P.model == 1)
         launch_pdl(k_local<1>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
@@ -632,7 +634,7 @@ void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, co
 // (colour-free: each free vertex sums its incident tets in a fixed order)
 // ----------------------------------------------------------------------------
 __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32_t* __restrict__ adj,
-                         const float4* __restrict__ fc, const double* __restrict__ M, const double4* __restrict__ x,
+                         const float* __restrict__ fc, const double* __restrict__ M, const double4* __restrict__ x,
                          const double4* __restrict__ s, const int32_t* __restrict__ slotmap, Slots sl,
                          const double* __restrict__ hl, float4* __restrict__ u, double* __restrict__ resid) {
     pdl_enter();
@@ -646,10 +648,10 @@ __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32
     int p0 = adjp[a], p1 = adjp[a + 1];
     float f0 = 0.f, f1 = 0.f, f2 = 0.f;
     for (int p = p0; p < p1; ++p) {
-        float4 f = __ldg(&fc[(size_t)__ldg(&adj[p]) * S + inst]);
-        f0 += f.x;
-        f1 += f.y;
-        f2 += f.z;
+        const float* f = fc + (size_t)__ldg(&adj[p]) * 3 * S + inst;   // (tet, corner) entry, 3 planes of S
+        f0 += __ldg(f);
+        f1 += __ldg(f + S);
+        f2 += __ldg(f + 2 * S);
     }
     r0 += f0;
     r1 += f1;
@@ -676,7 +678,7 @@ __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32
 }
 
 void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
-                   const float4* fc, const double* M, const double4* x, const double4* s,
+                   const float* fc, const double* M, const double4* x, const double4* s,
                    const int32_t* slotmap, Slots sl, const double* hl, float4* u, double* resid_dbg) {
     launch_pdl(k_gather, dim3((P.n_f * P.S + 255) / 256), dim3(256), 0, st, P, adjp, adj, fc, M, x, s, slotmap, sl, hl, u,
                resid_dbg);

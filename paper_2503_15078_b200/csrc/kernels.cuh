@@ -123,12 +123,12 @@ void launch_finite_guard(cudaStream_t st, int n_v, int S, double4* x, double4* v
                          const double4* vt, int* bad, int* rollbacks);
 // du: ADMM-PD dual [9][n_t S] or nullptr (plain PD); admm_first: treat u as 0 (first iteration of a frame)
 void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
-                  const double4* x, float4* fc, float* Pdbg, float* du = nullptr, int admm_first = 0);
+                  const double4* x, float* fc, float* Pdbg, float* du = nullptr, int admm_first = 0);
 void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, const double4* x,
                          const double4* xt, ContactState cs);
 // slotmap[a * S + i] = global slot of vertex a in instance i, or -1
 void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
-                   const float4* fc, const double* M, const double4* x, const double4* s,
+                   const float* fc, const double* M, const double4* x, const double4* s,
                    const int32_t* slotmap, Slots sl, const double* hl, float4* u, double* resid_dbg);
 // K-passes over the tile streams T1 / T2 (see simhost::build_tiles); S = 1
 void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* T1,
