@@ -289,8 +289,8 @@ __device__ __forceinline__ void swapcol(float V[3][3], float* e, int a, int b) {
 
 // NH objective in sigma space: k/2|p-sig|^2 + mu/2(|p|^2-3) - mu lnJ + lam/2 ln^2 J
 // (ln J = ln(p0 p1 p2): one hardware log2 instead of three IEEE logs)
-__device__ __forceinline__ float nh_f(const float p[3], const float sg[3], float k, float mu, float lam) {
-    float lnJ = log_ftz(p[0] * p[1] * p[2]);
+__device__ __forceinline__ float nh_f(const float p[3], const float sg[3], float k, float mu, float lam,
+                                     float lnJ) {
     float d0 = p[0] - sg[0], d1 = p[1] - sg[1], d2 = p[2] - sg[2];
     return 0.5f * k * (d0 * d0 + d1 * d1 + d2 * d2) +
            0.5f * mu * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2] - 3.f) - mu * lnJ + 0.5f * lam * lnJ * lnJ;
@@ -316,15 +316,17 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
     // Neo-Hookean: damped Newton from p0 = max(sig, 0.05), <= 16 iterations
     float p[3] = {fmaxf(sg[0], 0.05f), fmaxf(sg[1], 0.05f), fmaxf(sg[2], 0.05f)};
     float scale = fmaxf(1.f, sqrtf(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]));
+    const float gtol = 2e-6f * k * scale;
+    // ln J and the objective at p are carried from the accepted line-search point
+    float lnJ = log_ftz(p[0] * p[1] * p[2]);
+    float f0 = nh_f(p, sg, k, mu, lam, lnJ);
 #pragma unroll 1
     for (int it = 0; it < 16; ++it) {
-        float lnJ = log_ftz(p[0] * p[1] * p[2]);
         float iv[3] = {rcp_ftz(p[0]), rcp_ftz(p[1]), rcp_ftz(p[2])};
         float g[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) g[i] = k * (p[i] - sg[i]) + mu * p[i] - mu * iv[i] + lam * lnJ * iv[i];
-        float gn = sqrtf(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
-        if (gn <= 2e-6f * k * scale) break;
+        if (g[0] * g[0] + g[1] * g[1] + g[2] * g[2] <= gtol * gtol) break;   // |g| <= gtol
         float H[3][3];
         float dg = mu - lam * lnJ;
 #pragma unroll
@@ -359,22 +361,32 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
             dd[2] = s * g[2];
         }
         float slope = dd[0] * g[0] + dd[1] * g[1] + dd[2] * g[2];
-        float f0 = nh_f(p, sg, k, mu, lam);
         float fr = 2e-6f * (k * (p[0] * p[0] + p[1] * p[1] + p[2] * p[2] + sg[0] * sg[0] + sg[1] * sg[1] +
                                  sg[2] * sg[2]) + mu * fabsf(lnJ) + lam * lnJ * lnJ + mu);
         float t = 1.f;
+        bool acc = false;
 #pragma unroll 1
         for (int ls = 0; ls < 40; ++ls) {
             float pn[3] = {p[0] + t * dd[0], p[1] + t * dd[1], p[2] + t * dd[2]};
             if (pn[0] > 0.f && pn[1] > 0.f && pn[2] > 0.f) {
-                float fn = nh_f(pn, sg, k, mu, lam);
-                if (fn <= f0 + 1e-4f * t * slope + fr) break;
+                const float lnJn = log_ftz(pn[0] * pn[1] * pn[2]);
+                const float fn = nh_f(pn, sg, k, mu, lam, lnJn);
+                if (fn <= f0 + 1e-4f * t * slope + fr) {
+                    acc = true;
+                    lnJ = lnJn;
+                    f0 = fn;
+                    break;
+                }
             }
             t *= 0.5f;
         }
         p[0] += t * dd[0];
         p[1] += t * dd[1];
         p[2] += t * dd[2];
+        if (!acc) {   // line search exhausted: tiny step, re-evaluate at the new point
+            lnJ = log_ftz(p[0] * p[1] * p[2]);
+            f0 = nh_f(p, sg, k, mu, lam, lnJ);
+        }
     }
     d[0] = p[0] - sg[0];
     d[1] = p[1] - sg[1];
