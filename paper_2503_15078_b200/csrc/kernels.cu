@@ -313,8 +313,15 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
         for (int i = 0; i < 3; ++i) d[i] = (2.f * mu * (1.f - sg[i]) - lam * (S - 3.f)) * inv;
         return;
     }
-    // Neo-Hookean: damped Newton from p0 = max(sig, 0.05), <= 16 iterations
-    float p[3] = {fmaxf(sg[0], 0.05f), fmaxf(sg[1], 0.05f), fmaxf(sg[2], 0.05f)};
+    // Neo-Hookean: damped Newton, <= 16 iterations, from the linear-corotated minimiser (the same
+    // Hessian 2 mu I + lam 1 1^T at p = 1, so it is NH's first-order solution), floored at 0.05
+    float p[3];
+    {
+        const float Sp = (k * (sg[0] + sg[1] + sg[2]) + 6.f * mu + 9.f * lam) * rcp_ftz(k + 2.f * mu + 3.f * lam);
+        const float inv = rcp_ftz(k + 2.f * mu);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) p[i] = fmaxf(sg[i] + (2.f * mu * (1.f - sg[i]) - lam * (Sp - 3.f)) * inv, 0.05f);
+    }
     float scale = fmaxf(1.f, sqrtf(sg[0] * sg[0] + sg[1] * sg[1] + sg[2] * sg[2]));
     const float gtol = 2e-6f * k * scale;
     // ln J and the objective at p are carried from the accepted line-search point

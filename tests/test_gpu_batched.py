@@ -11,6 +11,7 @@ import pytest
 
 import scenes
 from oracle import oracle as O
+from _parity import sensitivity
 
 pytestmark = pytest.mark.gpu
 
@@ -260,8 +261,17 @@ def test_async_position_readback(simmod):
 def test_cfg5_full_size_sampled(simmod):
     """cfg5 in the bench's launch configuration: 1024 cfg3 instances on one handle (tensor-core
     K-passes in 8 chunks of 128, one CR CTA per instance), own initial velocities and obstacle
-    offsets, contacts committed in one batch; one frame; sampled instances (first, middle of the
-    last-but-one chunk, last) against the oracle within 1e-5 bbox."""
+    offsets, contacts committed in one batch; one frame; sampled instances against the oracle.
+
+    First and last instance: within 1e-5 bbox.  The two instances whose bars sit closest to the
+    slab (in contact from the first frame): identical contact classification (reading A21) and
+    positions within max(1e-5 bbox, 20 x the oracle's own sensitivity), where the sensitivity is
+    how far the oracle's frame moves when only its inputs x0, v0 are rounded to fp32.  Some of
+    these frames are ill-conditioned (5 L-G / 10 CR iterations, not converged): rounding the
+    inputs alone moves the oracle by 0.3 of the tolerance on instance 221, against 2e-4 on
+    instance 0, and the fp32 path's own roundings (local projection to a 1e-6 gradient
+    tolerance) land at 5-13x that, as they do on well-conditioned frames (tests/_parity.py,
+    DESIGN.md §3 parity envelope)."""
     sc = scenes.make_scene("cfg3")
     S = 1024
     s = make(simmod, sc, S)
@@ -279,13 +289,23 @@ def test_cfg5_full_size_sampled(simmod):
     P = s.get_positions()
     assert np.isfinite(P).all()
     tol = 1e-5 * sc.mesh.bbox_diag()
-    for i in (0, 700, 1023):
+    deltas = np.array([scenes.batch_instance_params(sc, i)[1] for i in range(S)])
+    closest = [int(c) for c in np.argsort(-deltas)[:2]]   # delta <= 0: the smallest gaps
+    for i in [0, 1023] + closest:
         _, cs = scenes.batch_instance(sc, i)
         o = O.Oracle(sc.mesh, sc.material, sc.h)
         o.set_contacts(cs)
         pins = sc.mesh.X[o.pinned] + sc.h * sc.pin_velocity
-        xo, _, _ = o.frame(sc.mesh.X.copy(), v0s[i], pin_targets=pins)
-        assert np.abs(P[i] - xo).max() < tol, (i, np.abs(P[i] - xo).max())
+        xo, _, info = o.frame(sc.mesh.X.copy(), v0s[i], pin_targets=pins)
+        err = np.abs(P[i] - xo).max()
+        if i not in closest:
+            assert err < tol, (i, err, tol)
+            continue
+        sens = sensitivity(o, sc.mesh.X, v0s[i], xo, pin_targets=pins)
+        assert err < max(tol, 20.0 * sens), (i, err, tol, sens)
+        cls_o = o.classify(xo, sc.mesh.X, info["lam"])
+        cls_g = o.classify(P[i], sc.mesh.X, s.get_lambda(i))
+        assert np.array_equal(cls_o, cls_g), (i, np.flatnonzero(cls_o != cls_g))
 
 
 @pytest.mark.parametrize("model", [1, 2])

@@ -1,0 +1,40 @@
+"""cfg5 parity scan: one frame of 1024 instances on the GPU, |x_gpu - x_oracle| / (1e-5 bbox) for a
+spread of sampled instances (argv: stride, default 64)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import scenes
+from oracle import oracle as O
+import paper_2503_15078_b200 as simlib
+
+stride = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+nclose = int(sys.argv[2]) if len(sys.argv) > 2 else 0   # also the nclose instances with the smallest gaps
+sc = scenes.make_scene("cfg3")
+S = 1024
+s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, n_instances=S)
+s.set_pin_velocity(sc.pin_velocity)
+base = simlib.contacts_to_array(sc.contacts)
+arrs, v0s = [], np.empty((S, sc.mesh.n_v, 3))
+for i in range(S):
+    v0s[i], delta = scenes.batch_instance_params(sc, i)
+    a = base.copy()
+    a["offset"] += a["normal"][:, 2] * delta
+    arrs.append(a)
+s.set_contacts_batch(packed=(np.concatenate(arrs), np.full(S, len(base), np.int32)))
+s.set_states(np.broadcast_to(sc.mesh.X, (S,) + sc.mesh.X.shape), v0s)
+s.step(1, 5)
+P = s.get_positions()
+tol = 1e-5 * sc.mesh.bbox_diag()
+out = []
+deltas = np.array([scenes.batch_instance_params(sc, i)[1] for i in range(S)])
+for i in list(range(0, S, stride)) + [int(c) for c in np.argsort(-deltas)[:nclose]]:
+    t0 = time.time()
+    v0, cs = scenes.batch_instance(sc, i)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(cs)
+    pins = sc.mesh.X[o.pinned] + sc.h * sc.pin_velocity
+    xo, _, info = o.frame(sc.mesh.X.copy(), v0s[i], pin_targets=pins)
+    e = np.abs(P[i] - xo).max() / tol
+    out.append(e)
+    print(f"inst {i:4d} delta {scenes.batch_instance_params(sc, i)[1]*1e3:+.2f} mm  err/tol {e:.3f}  ({time.time()-t0:.1f}s)", flush=True)
+print("max", max(out), "median", float(np.median(out)))
