@@ -353,7 +353,7 @@ def kernel_roofline(kind, avg_s, S, nnz, nf, hbm_peak, hbm_kind, n_t=93600):
                 "traffic": ncu_traffic("local"), "algorithmic_flops_per_launch": flops, "avg_launch_us": avg_s * 1e6,
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md)",
                 "note": "%.0f FP32 flop per tet-instance (ncu FFMA/FMUL/FADD counts, NH: SVD by Jacobi + "
-                        "sigma-space Newton); issue-slot bound (78%% busy in ncu)" % fpt}
+                        "sigma-space Newton); issue-slot bound (74%% busy in ncu)" % fpt}
     if S == 1:
         b1 = 4 * nnz + 16 * nf + 16 * nf            # K (column-major tile stream) + u + y
         b2 = 4 * nnz + 16 * nf + 2 * 32 * nf        # K (row-major tile stream) + y + x read/write
