@@ -279,21 +279,31 @@ class Sim:
         _check(lib.sim_get_state(self._h, int(instance), _dptr(x), _dptr(v)))
         return x, v
 
+    def _f64(self, a, count, name):
+        """Contiguous float64 copy of a, checked to hold exactly `count` values (the C side trusts sizes)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.size != count:
+            raise ValueError(f"{name} must hold {count} values, got shape {a.shape}")
+        return a
+
     def set_state(self, x, v, instance=0):
-        x = np.ascontiguousarray(x, dtype=np.float64)
-        v = np.ascontiguousarray(v, dtype=np.float64)
+        x = self._f64(x, 3 * self.n_v, "x")
+        v = self._f64(v, 3 * self.n_v, "v")
         _check(lib.sim_set_state(self._h, int(instance), _dptr(x), _dptr(v)))
 
     def set_states(self, x=None, v=None):
         """States of all instances, [n_instances][n_vertices][3] each (None = keep)."""
-        xa = None if x is None else np.ascontiguousarray(x, dtype=np.float64)
-        va = None if v is None else np.ascontiguousarray(v, dtype=np.float64)
+        n = 3 * self.n_v * self.n_instances
+        xa = None if x is None else self._f64(x, n, "x")
+        va = None if v is None else self._f64(v, n, "v")
         _check(lib.sim_set_states(self._h, None if xa is None else _dptr(xa), None if va is None else _dptr(va)))
 
     def get_positions(self, out=None):
         """Positions of all instances, [n_instances][n_vertices][3]."""
         if out is None:
             out = np.empty((self.n_instances, self.n_v, 3))
+        if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != 3 * self.n_v * self.n_instances:
+            raise ValueError("out must be a C-contiguous float64 array of n_instances x n_vertices x 3")
         _check(lib.sim_get_positions(self._h, _dptr(out)))
         return out
 
@@ -403,7 +413,7 @@ class Sim:
 
     def debug_apply_inverse(self, b):
         """b: [n_v][3] (single instance) or [n_instances][n_v][3]."""
-        b = np.ascontiguousarray(b, dtype=np.float64)
+        b = self._f64(b, 3 * self.n_v * self.n_instances, "b")
         x = np.empty(b.shape)
         _check(lib.sim_debug_apply_inverse(self._h, _dptr(b), _dptr(x)))
         return x
