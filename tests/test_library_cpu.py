@@ -93,6 +93,19 @@ def test_input_validation():
         Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, -1.0, host_only=True)
 
 
+def test_binding_checks_array_sizes():
+    """The binding refuses arrays that do not hold n_instances x n_vertices x 3 values before the
+    C call (the ABI trusts the caller's sizes)."""
+    sc = scenes.make_scene("cfg1")
+    s = _host(sc)
+    with pytest.raises(ValueError, match="x must hold"):
+        s.set_state(sc.mesh.X[:-1], np.zeros_like(sc.mesh.X))
+    with pytest.raises(ValueError, match="b must hold"):
+        s.debug_apply_inverse(np.zeros((sc.mesh.n_v + 1, 3)))
+    with pytest.raises(ValueError, match="out must be"):
+        s.get_positions(out=np.empty((1, sc.mesh.n_v, 3), np.float32))
+
+
 def test_no_cpu_fallback_without_device():
     """sim_create (device path) must fail loudly when there is no GPU."""
     import torch
