@@ -302,7 +302,7 @@ def measure(args, S, rank, ws, dev, stream, full=True):
     # arrays (H2D through pinned staging) and reads back the positions of all instances (D2H into
     # pinned host buffers, double-buffered: the copy of step i overlaps the compute of step i + 1;
     # the timed region ends after the last copy has landed)
-    e2e_steps = max(3, args.steps // 2)
+    e2e_steps = max(3, args.steps)          # as many steps as the device-timed region
     xh = [torch.empty((S, sc.mesh.n_v, 3), dtype=torch.float64, pin_memory=True) for _ in range(2)]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
