@@ -159,6 +159,11 @@ struct sim_handle {
     std::vector<int> coff_h, soff_h;
     // uploaded contact data: one device arena with the staging layout (one H2D copy per commit)
     DBuf<unsigned char> arena;
+    // the H2D upload of a commit lands in arena_up on up_stream (overlapping the frames still
+    // running on the handle's stream); the stream then takes it with one D2D copy into arena
+    DBuf<unsigned char> arena_up;
+    cudaStream_t up_stream = nullptr;
+    cudaEvent_t up_done = nullptr, up_free = nullptr;
     std::vector<size_t> arena_layout;
     DPtr<DContact> dc;
     DPtr<float> cc9;
@@ -330,6 +335,10 @@ extern "C" void sim_destroy(sim_handle* H) {
         if (H->gexec) cudaGraphExecDestroy(H->gexec);
         for (auto e : H->pev) cudaEventDestroy(e);
         if (H->stage_free) cudaEventDestroy(H->stage_free);
+        if (H->up_stream) cudaStreamSynchronize(H->up_stream);
+        if (H->up_done) cudaEventDestroy(H->up_done);
+        if (H->up_free) cudaEventDestroy(H->up_free);
+        if (H->up_stream) cudaStreamDestroy(H->up_stream);
         if (H->fork_ev) cudaEventDestroy(H->fork_ev);
         if (H->copy_stream) cudaStreamSynchronize(H->copy_stream);
         for (int k = 0; k < 2; ++k) {
@@ -1207,8 +1216,23 @@ static int commit_host(sim_handle* H) {
             }
     }
     H->h2d_contact_bytes = (int64_t)cur;
-    CK(cudaMemcpyAsync(H->arena.p, B, cur, cudaMemcpyHostToDevice, st));   // the whole layout at once
-    CK(cudaEventRecord(H->stage_free, st));
+    // the whole layout in one H2D copy on the upload stream, then one D2D copy in stream order
+    if (!H->up_stream) {
+        CK(cudaStreamCreateWithFlags(&H->up_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&H->up_done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&H->up_free, cudaEventDisableTiming));
+    }
+    {
+        bool grew_up = false;
+        CK(H->arena_up.ensure(need, grew_up));
+    }
+    CK(cudaStreamWaitEvent(H->up_stream, H->up_free, 0));   // the previous commit's D2D has read arena_up
+    CK(cudaMemcpyAsync(H->arena_up.p, B, cur, cudaMemcpyHostToDevice, H->up_stream));
+    CK(cudaEventRecord(H->stage_free, H->up_stream));       // pinned staging reusable
+    CK(cudaEventRecord(H->up_done, H->up_stream));
+    CK(cudaStreamWaitEvent(st, H->up_done, 0));
+    CK(cudaMemcpyAsync(H->arena.p, H->arena_up.p, cur, cudaMemcpyDeviceToDevice, st));
+    CK(cudaEventRecord(H->up_free, st));
     H->NCL = NCL;
     H->CS = CSt;
     H->cm_max = cmm;
