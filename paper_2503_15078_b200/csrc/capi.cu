@@ -185,6 +185,8 @@ struct sim_handle {
     bool tc_contact = false;
     std::vector<int32_t> tc_verts;   // the class vertex set the tiles were built for
     DBuf<simhost::BUnit> tcu_c, tcu_s;
+    DBuf<double> tc_cpart;   // chain-pass partial sums (units split when few instances leave SMs idle)
+    DBuf<int> tc_ccnt;
     DBuf<int32_t> tc_cover, tc_rows;
     DBuf<float> tc_Tc, tc_Ts;
     int tc_nuc = 0, tc_nus = 0, tc_ns = 0;
@@ -1254,6 +1256,34 @@ static int commit_host(sim_handle* H) {
     if (H->tc_contact && H->ic[rep[0]].verts != H->tc_verts) {   // tiles depend on K and the vertex set only
         simhost::ContactPasses cp;
         simhost::build_contact_passes(H->K, H->ic[rep[0]].verts, cp);
+        {   // split chain units over tile ranges until about two CTAs per SM are in flight
+            const int nch = (S + 127) / 128, nu = (int)cp.uc.size();
+            const int want = nu ? std::max(1, (2 * 148 + nu * nch - 1) / (nu * nch)) : 1;
+            std::vector<simhost::BUnit> su;
+            int nslot = 0;
+            for (int b = 0; b < nu; ++b) {
+                const simhost::BUnit u = cp.uc[b];
+                const int p = std::max(1, std::min(want, u.ntiles));
+                for (int k = 0; k < p; ++k) {
+                    const int t0 = u.ntiles * k / p, t1 = u.ntiles * (k + 1) / p;
+                    simhost::BUnit v = u;
+                    v.list0 = u.list0 + 32 * t0;
+                    v.nlist = std::min(u.nlist - 32 * t0, 32 * (t1 - t0));
+                    v.ntiles = t1 - t0;
+                    v.toff = u.toff + (int64_t)t0 * 1024;
+                    v.block = b;
+                    v.nparts = p;
+                    v.part = p > 1 ? nslot + k : 0;
+                    v.pad = nslot;
+                    su.push_back(v);
+                }
+                if (p > 1) nslot += p;
+            }
+            cp.uc.swap(su);
+            CK(H->tc_cpart.alloc(std::max<size_t>((size_t)nslot * 3 * 32 * S, 1)));
+            CK(H->tc_ccnt.alloc((size_t)std::max(1, nu) * nch));
+            CK(cudaMemsetAsync(H->tc_ccnt.p, 0, sizeof(int) * (size_t)std::max(1, nu) * nch, st));
+        }
         std::vector<float> tc, ts;
         simhost::tc_tiles(cp.Tc, tc);
         simhost::tc_tiles(cp.Ts, ts);
@@ -1427,7 +1457,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
             MARK(KK_CHAIN);
             if (H->tc_contact)
                 launch_chain_pass_ts(st, H->S, H->tc_nuc, H->tcu_c.p, H->tc_Tc.p, H->tc_cover.p, H->y.p, H->soff.p,
-                                     ccr, H->x.p, cs, 1);   // fold every tile: the Schur RHS is sensitive
+                                     ccr, H->x.p, cs, 1, H->tc_cpart.p, H->tc_ccnt.p);   // fold every tile: the Schur RHS is sensitive
             else
                 launch_chain_dot(st, P, off, class_slots(H), H->Kcol.p, H->colptr.p, H->chain_off.p,
                                  H->chain_rows.p, H->y.p, sl, ccr, H->x.p, cs, H->n_it_cd, H->it_cd.p);

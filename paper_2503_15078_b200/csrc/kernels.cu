@@ -1724,7 +1724,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     const int li = il;
     const bool live = li < ni;
     const int inst = i0 + li;
-    if (PASS == 3) {   // chain pass: dxt (and the Schur RHS of the slot's single contact) per slot
+    if (PASS == 3 && U.nparts == 1) {   // chain pass: dxt (and the Schur RHS of the slot's single contact) per slot
         if (!live) return;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -1799,18 +1799,22 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     asm volatile("bar.sync 1, %0;\n" ::"r"(kTcThreads));
     if (!s_last) return;
     __threadfence();
+    const int first = PASS == 3 ? U.pad : U.list0;   // the block's first partial slot
     if (live) {
         for (int r = 0; r < 8; ++r) {
             const int l = 8 * oct + r;
             if (l >= U.nr) continue;
             double t0 = 0.0, t1 = 0.0, t2 = 0.0;
             for (int q = 0; q < U.nparts; ++q) {
-                const double* pq = part + (size_t)(U.list0 + q) * 3 * pstride + (size_t)l * S + inst;
+                const double* pq = part + (size_t)(first + q) * 3 * pstride + (size_t)l * S + inst;
                 t0 += __ldcg(pq);
                 t1 += __ldcg(pq + pstride);
                 t2 += __ldcg(pq + 2 * pstride);
             }
-            yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
+            if (PASS == 3)
+                chain_rho(S, inst, ex.soff[inst] + U.c0 + l, t0, t1, t2, ex.cc, ex.xs, ex.cs);
+            else
+                yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
         }
     }
     if (threadIdx.x == 0) counters[U.block * nchunks + chunk] = 0;
@@ -1834,12 +1838,12 @@ void launch_kpass2_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
 
 void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units, const float* Ttc,
                           const int32_t* cover, const float4* y, const int* soff, CrContacts cc, const double4* x,
-                          ContactState cs, int drain) {
+                          ContactState cs, int drain, double* part, int* counters) {
     if (nunits == 0) return;
     const int nch = (S + kTcInst - 1) / kTcInst;
     TsExtra ex{nullptr, soff, cc, x, cs};
     launch_pdl(k_kpass_ts<3>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, 0, units, Ttc, cover, y,
-               (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, (double4*)nullptr, (const double4*)nullptr,
+               (float4*)nullptr, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
                (double4*)nullptr, 0.0, 0, drain, ex);
 }
 

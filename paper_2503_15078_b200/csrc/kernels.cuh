@@ -157,9 +157,12 @@ struct TsExtra {
     ContactState cs;
 };
 // contact passes of the single slot-set class (S > 1) on the tensor cores (simhost::ContactPasses)
+// units split over several parts (nparts > 1; pad = the block's first partial slot) sum fp64
+// partials in `part` ([slot][3][32][S]); the last part of a block (counters, zero on entry and
+// reset on exit) adds them in part order and evaluates the slots' Schur right-hand sides
 void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units, const float* Ttc,
                           const int32_t* cover, const float4* y, const int* soff, CrContacts cc, const double4* x,
-                          ContactState cs, int drain);
+                          ContactState cs, int drain, double* part, int* counters);
 void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BUnit* units, const float* Ttc,
                             const int32_t* rows, const float4* wzT, float4* y, int drain);
 // TS variant: right-hand sides staged in TMEM (tcgen05.st) instead of shared memory
