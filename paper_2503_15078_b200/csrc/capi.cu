@@ -185,8 +185,8 @@ struct sim_handle {
     bool tc_contact = false;
     std::vector<int32_t> tc_verts;   // the class vertex set the tiles were built for
     DBuf<simhost::BUnit> tcu_c, tcu_s;
-    DBuf<double> tc_cpart;   // chain-pass partial sums (units split when few instances leave SMs idle)
-    DBuf<int> tc_ccnt;
+    DBuf<double> tc_cpart, tc_spart;   // chain / scatter-pass partial sums (units split when few instances
+    DBuf<int> tc_ccnt, tc_scnt;        // leave SMs idle) and their per-unit arrival counters
     DBuf<int32_t> tc_cover, tc_rows;
     DBuf<float> tc_Tc, tc_Ts;
     int tc_nuc = 0, tc_nus = 0, tc_ns = 0;
@@ -1256,19 +1256,26 @@ static int commit_host(sim_handle* H) {
     if (H->tc_contact && H->ic[rep[0]].verts != H->tc_verts) {   // tiles depend on K and the vertex set only
         simhost::ContactPasses cp;
         simhost::build_contact_passes(H->K, H->ic[rep[0]].verts, cp);
-        {   // split chain units over tile ranges until about two CTAs per SM are in flight
-            const int nch = (S + 127) / 128, nu = (int)cp.uc.size();
+        // split the units over tile ranges until about two CTAs per SM are in flight (fp64 partials,
+        // added in part order by the last part of each unit)
+        auto split = [&](std::vector<simhost::BUnit>& units, bool cover_list, DBuf<double>& part,
+                         DBuf<int>& cnt) -> cudaError_t {
+            const int nch = (S + 127) / 128, nu = (int)units.size();
             const int want = nu ? std::max(1, (2 * 148 + nu * nch - 1) / (nu * nch)) : 1;
             std::vector<simhost::BUnit> su;
             int nslot = 0;
             for (int b = 0; b < nu; ++b) {
-                const simhost::BUnit u = cp.uc[b];
+                const simhost::BUnit u = units[b];
                 const int p = std::max(1, std::min(want, u.ntiles));
                 for (int k = 0; k < p; ++k) {
                     const int t0 = u.ntiles * k / p, t1 = u.ntiles * (k + 1) / p;
                     simhost::BUnit v = u;
-                    v.list0 = u.list0 + 32 * t0;
-                    v.nlist = std::min(u.nlist - 32 * t0, 32 * (t1 - t0));
+                    if (cover_list) {   // chain pass: tiles walk the unit's cover-row list
+                        v.list0 = u.list0 + 32 * t0;
+                        v.nlist = std::min(u.nlist - 32 * t0, 32 * (t1 - t0));
+                    } else {            // scatter pass: tiles walk consecutive slots
+                        v.c0 = u.c0 + 32 * t0;
+                    }
                     v.ntiles = t1 - t0;
                     v.toff = u.toff + (int64_t)t0 * 1024;
                     v.block = b;
@@ -1279,11 +1286,14 @@ static int commit_host(sim_handle* H) {
                 }
                 if (p > 1) nslot += p;
             }
-            cp.uc.swap(su);
-            CK(H->tc_cpart.alloc(std::max<size_t>((size_t)nslot * 3 * 32 * S, 1)));
-            CK(H->tc_ccnt.alloc((size_t)std::max(1, nu) * nch));
-            CK(cudaMemsetAsync(H->tc_ccnt.p, 0, sizeof(int) * (size_t)std::max(1, nu) * nch, st));
-        }
+            units.swap(su);
+            cudaError_t e = part.alloc(std::max<size_t>((size_t)nslot * 3 * 32 * S, 1));
+            if (e == cudaSuccess) e = cnt.alloc((size_t)std::max(1, nu) * nch);
+            if (e == cudaSuccess) e = cudaMemsetAsync(cnt.p, 0, sizeof(int) * (size_t)std::max(1, nu) * nch, st);
+            return e;
+        };
+        CK(split(cp.uc, true, H->tc_cpart, H->tc_ccnt));
+        CK(split(cp.us, false, H->tc_spart, H->tc_scnt));
         std::vector<float> tc, ts;
         simhost::tc_tiles(cp.Tc, tc);
         simhost::tc_tiles(cp.Ts, ts);
@@ -1474,7 +1484,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
             MARK(KK_SCATTER);
             if (H->tc_contact)
                 launch_scatter_pass_ts(st, H->S, H->tc_ns, H->tc_nus, H->tcu_s.p, H->tc_Ts.p, H->tc_rows.p, H->wzT.p,
-                                       H->y.p, 1);
+                                       H->y.p, 1, H->tc_spart.p, H->tc_scnt.p);
             else
                 launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->wzT.p, H->y.p,
                                H->n_it_sc, H->it_sc.p);

@@ -1734,7 +1734,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
         }
         return;
     }
-    if (PASS == 4) {   // scatter pass: y[row] += K H^T z on the chain rows
+    if (PASS == 4 && U.nparts == 1) {   // scatter pass: y[row] += K H^T z on the chain rows
         if (!live) return;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -1799,7 +1799,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     asm volatile("bar.sync 1, %0;\n" ::"r"(kTcThreads));
     if (!s_last) return;
     __threadfence();
-    const int first = PASS == 3 ? U.pad : U.list0;   // the block's first partial slot
+    const int first = PASS >= 3 ? U.pad : U.list0;   // the block's first partial slot
     if (live) {
         for (int r = 0; r < 8; ++r) {
             const int l = 8 * oct + r;
@@ -1811,9 +1811,13 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
                 t1 += __ldcg(pq + pstride);
                 t2 += __ldcg(pq + 2 * pstride);
             }
-            if (PASS == 3)
+            if (PASS == 3) {
                 chain_rho(S, inst, ex.soff[inst] + U.c0 + l, t0, t1, t2, ex.cc, ex.xs, ex.cs);
-            else
+            } else if (PASS == 4) {
+                const size_t iy = (size_t)ex.orows[U.r0 + l] * S + inst;
+                const float4 yi = yout[iy];
+                yout[iy] = make_float4((float)(yi.x + t0), (float)(yi.y + t1), (float)(yi.z + t2), yi.w);
+            } else
                 yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
         }
     }
@@ -1848,12 +1852,13 @@ void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units
 }
 
 void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BUnit* units, const float* Ttc,
-                            const int32_t* rows, const float4* wzT, float4* y, int drain) {
+                            const int32_t* rows, const float4* wzT, float4* y, int drain, double* part,
+                            int* counters) {
     if (nunits == 0) return;
     const int nch = (S + kTcInst - 1) / kTcInst;
     TsExtra ex{rows, nullptr, CrContacts{}, nullptr, ContactState{}};
     launch_pdl(k_kpass_ts<4>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, ns, units, Ttc,
-               (const int32_t*)nullptr, wzT, y, (double*)nullptr, (int*)nullptr, nch, (double4*)nullptr,
+               (const int32_t*)nullptr, wzT, y, part, counters, nch, (double4*)nullptr,
                (const double4*)nullptr, (double4*)nullptr, 0.0, 0, drain, ex);
 }
 

@@ -164,7 +164,8 @@ void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units
                           const int32_t* cover, const float4* y, const int* soff, CrContacts cc, const double4* x,
                           ContactState cs, int drain, double* part, int* counters);
 void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BUnit* units, const float* Ttc,
-                            const int32_t* rows, const float4* wzT, float4* y, int drain);
+                            const int32_t* rows, const float4* wzT, float4* y, int drain, double* part,
+                            int* counters);   // split units: as launch_chain_pass_ts
 // TS variant: right-hand sides staged in TMEM (tcgen05.st) instead of shared memory
 void launch_kpass1_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
                       const float4* u, float4* y, double* part, int* counters, int drain);
