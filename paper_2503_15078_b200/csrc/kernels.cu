@@ -1575,8 +1575,13 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     __shared__ int s_last;
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const bool mma_warp = w == kTcThreads / 32;
-    const BUnit U = units[blockIdx.x];
-    const int chunk = blockIdx.y;
+    // grid order: pass 1 runs unit-fastest (the units in flight share right-hand-side columns of one
+    // instance chunk in L2: 2.3 GB of DRAM traffic per launch at S = 1024, 5.8 GB chunk-fastest);
+    // the other passes run chunk-fastest (the chunks of one unit share its K tiles in L2: pass 2
+    // 2.6 -> 2.1 GB, 1.7 % faster; chain / scatter 3 % faster)
+    constexpr bool kChunkFast = PASS != 1;
+    const BUnit U = units[kChunkFast ? blockIdx.y : blockIdx.x];
+    const int chunk = kChunkFast ? blockIdx.x : blockIdx.y;
     const int i0 = chunk * kTcInst;
     const int ni = min(kTcInst, S - i0);
     const unsigned long long pol = l2_evict_first();
@@ -1836,7 +1841,7 @@ void launch_kpass2_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
                       const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
                       int finalize_v, int drain) {
     const int nch = (S + kTcInst - 1) / kTcInst;
-    launch_pdl(k_kpass_ts<2>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, n_f, units, T2tc, cover, y,
+    launch_pdl(k_kpass_ts<2>, dim3(nch, nunits), dim3(kTcThreads + 32), 0, st, S, n_f, units, T2tc, cover, y,
                (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain, TsExtra{});
 }
 
@@ -1846,7 +1851,7 @@ void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units
     if (nunits == 0) return;
     const int nch = (S + kTcInst - 1) / kTcInst;
     TsExtra ex{nullptr, soff, cc, x, cs};
-    launch_pdl(k_kpass_ts<3>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, 0, units, Ttc, cover, y,
+    launch_pdl(k_kpass_ts<3>, dim3(nch, nunits), dim3(kTcThreads + 32), 0, st, S, 0, units, Ttc, cover, y,
                (float4*)nullptr, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
                (double4*)nullptr, 0.0, 0, drain, ex);
 }
@@ -1857,7 +1862,7 @@ void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BU
     if (nunits == 0) return;
     const int nch = (S + kTcInst - 1) / kTcInst;
     TsExtra ex{rows, nullptr, CrContacts{}, nullptr, ContactState{}};
-    launch_pdl(k_kpass_ts<4>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, ns, units, Ttc,
+    launch_pdl(k_kpass_ts<4>, dim3(nch, nunits), dim3(kTcThreads + 32), 0, st, S, ns, units, Ttc,
                (const int32_t*)nullptr, wzT, y, part, counters, nch, (double4*)nullptr,
                (const double4*)nullptr, (double4*)nullptr, 0.0, 0, drain, ex);
 }
