@@ -14,7 +14,10 @@ using simhost::BUnit;
 
 constexpr int kMaxContacts = 1024;   // per instance: the CR keeps fp64 vectors of 3*kMaxContacts rows in SMEM
 constexpr int kMaxSlots = 1024;      // distinct contact vertices per instance
-constexpr int kCluster = 16;         // max CTAs per instance in the CR cluster (non-portable size)
+#ifndef SIM_CR_CLUSTER
+#define SIM_CR_CLUSTER 16
+#endif
+constexpr int kCluster = SIM_CR_CLUSTER;   // max CTAs per instance in the CR cluster (non-portable size)
 constexpr int kCrThreads = 512;
 constexpr size_t kCrMaxSmem = 232448;  // 227 KB opt-in shared memory per CTA (sm_100)
 int read_cr_clock(unsigned long long* out);   // phase timestamps of the last CR call (debug)
