@@ -1,5 +1,6 @@
 """Small end-to-end runs for compute-sanitizer: single scene with contacts (cluster CR), grid CR,
-batched instances on the tensor-core passes, ADMM, proximity query."""
+batched instances on the tensor-core passes (S = 3 with ADMM, S = 80 with one CR CTA per
+instance), proximity query, the 9-cube pile, cfg1 batched without contacts."""
 import math, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -17,6 +18,13 @@ S = 3
 s = sl.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, n_instances=S)
 s.set_contacts_batch([sc.contacts] * S)
 s.set_admm(True)
+s.step(2, 3)
+s.synchronize()
+# S = 80: one CR CTA per instance (G_A gathered into shared memory, row-per-thread matvec),
+# tensor-core chain / scatter passes split over tile ranges
+S = 80
+s = sl.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, n_instances=S)
+s.set_contacts_batch([sc.contacts] * S)
 s.step(2, 3)
 s.synchronize()
 s = sl.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
