@@ -177,6 +177,36 @@ def test_batched_determinism(simmod):
     assert np.array_equal(out[0], out[1])
 
 
+def test_split_contact_passes_one_cta_cr(simmod):
+    """S = 96 incline instances: one CR CTA per instance (G_A gathered from the class Gram into
+    shared memory, row-per-thread matvec) and tensor-core chain / scatter passes split over tile
+    ranges (fp64 partials, per-unit arrival counters).  The same frames re-run on the same handle
+    are bitwise identical (the counters reset themselves), and instances match the oracle."""
+    sc = scenes.incline_block(theta_deg=10.0, mu=math.tan(math.radians(10.0)) - 0.05, nv=5, edge=0.1,
+                              youngs=1e8)
+    S = 96
+    s = make(simmod, sc, S)
+    s.set_contacts_batch([sc.contacts] * S)
+    # rigid initial velocities (0 to 12 mm/s along x): smooth, distinct per instance (random
+    # per-vertex velocities on this E = 1e8 block are ill-conditioned: fp32 rounding of the
+    # inputs alone moves the oracle by 258 tolerances, tools/split_parity_check.py)
+    v0 = np.zeros((S,) + sc.mesh.X.shape)
+    v0[:, :, 0] = 0.002 * (np.arange(S) % 7)[:, None]
+    v0[:, sc.mesh.fixed.astype(bool)] = 0.0
+    runs = []
+    for _ in range(2):
+        s.set_states(np.broadcast_to(sc.mesh.X, (S,) + sc.mesh.X.shape), v0)
+        s.step(1, 5)
+        runs.append(s.get_positions())
+    assert np.array_equal(runs[0], runs[1])
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(sc.contacts)
+    for i in (0, 57, S - 1):
+        xo, _, _ = o.frame(sc.mesh.X.copy(), v0[i])
+        assert np.abs(runs[0][i] - xo).max() < tol, (i, np.abs(runs[0][i] - xo).max())
+
+
 def test_instance_validation(simmod):
     sc = scenes.make_scene("block", nv=5)
     s = make(simmod, sc, 2)
