@@ -1448,11 +1448,11 @@ static int enqueue_frame(sim_handle* H, int iters) {
             CKR(cudaEventRecord(H->fork_ev, st));
             CKR(cudaStreamWaitEvent(H->aux, H->fork_ev, 0));
             launch_contact_eval(H->aux, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
-            if (!H->grid) { launch_active(H->aux, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += cr_cluster_size(P.S) > 1 ? 2 : 1; }
+            if (!H->grid) { launch_active(H->aux, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += cr_cluster_size(P.S) > 1 ? 0 : 1; }
             CKR(cudaEventRecord(H->join_ev, H->aux));
         } else if (con) {
             MARK(KK_CONTACT); launch_contact_eval(st, P, H->dc.p, H->x.p, H->xt.p, cs); nk++;
-            if (!H->grid) { MARK(KK_ACTIVE); launch_active(st, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += cr_cluster_size(P.S) > 1 ? 2 : 1; }
+            if (!H->grid) { MARK(KK_ACTIVE); launch_active(st, P, off, ccr, sl, cs, act, H->G.p, H->GA.p); nk += cr_cluster_size(P.S) > 1 ? 0 : 1; }
         }
         MARK(KK_LOCAL);
         launch_local(st, P, H->tet.p, H->Bm.p, H->hw2.p, H->x.p, H->fc.p, nullptr, H->admm ? H->du.p : nullptr,

@@ -2103,8 +2103,8 @@ void launch_active(cudaStream_t st, const Params& P, InstOff off, CrContacts cc,
                    CrActive act, const float* G, float* GA) {
     if (P.NS == 0) return;
     const int csize = cr_cluster_size(P.S);
+    if (csize > 1) return;   // the cluster CR builds the active list and G_A itself
     k_active<<<P.S, 1024, 0, st>>>(off, cc, sl, cs, act, csize, G, GA);
-    if (csize > 1) k_gather_ga<<<dim3(P.ns_max, P.S), 256, 0, st>>>(off, G, act, GA);
 }
 
 // per-contact-set: chain rows of every class slot (walk panel runs), per-class row flags;
@@ -2599,6 +2599,57 @@ __host__ __device__ bool cr_ga_direct(int nc, int ns, int na, int csize) {
            kCrMaxSmem;
 }
 
+// The active slots of one instance in slot order (the list k_active builds), computed by one CTA
+// into its shared memory: apos[b] = position or -1, aidx[pos] = b, acon[pos] = local id of the
+// slot's single single-vertex contact or -1.  Returns na (every thread).
+// scratch: >= 33 ints of shared memory (the CTA's reduction buffer; no static shared memory:
+// k_cr takes the whole 227 KB dynamically)
+__device__ int cr_active_block(int ns, int sb, int cb, const CrContacts& cc, const Slots& sl,
+                               const ContactState& cs, int* aidx, int* apos, int* acon, int* scratch) {
+    int* wsum = scratch;
+    int& sbase = scratch[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) sbase = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < ns; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        bool on = false;
+        int only = -1;
+        if (b < ns) {
+            only = cc.c1[sb + b];
+            if (only >= 0) {
+                on = cs.theta[3 * only] != 0.0 || cs.theta[3 * only + 1] != 0.0 || cs.theta[3 * only + 2] != 0.0;
+            } else {
+                for (int q = sl.scp[sb + b]; q < sl.scp[sb + b + 1] && !on; ++q) {
+                    const int c = sl.sci[q];
+                    on = cs.theta[3 * c] != 0.0 || cs.theta[3 * c + 1] != 0.0 || cs.theta[3 * c + 2] != 0.0;
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        int pos = sbase;
+        for (int q = 0; q < wid; ++q) pos += wsum[q];
+        pos += __popc(bal & ((1u << lane) - 1u));
+        if (b < ns) {
+            apos[b] = on ? pos : -1;
+            if (on) {
+                aidx[pos] = b;
+                acon[pos] = only >= 0 ? only - cb : -1;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = sbase;
+            for (int q = 0; q < nw; ++q) t += wsum[q];
+            sbase = t;
+        }
+        __syncthreads();
+    }
+    return sbase;
+}
+
 __device__ unsigned long long g_cr_clock[32];   // phase timestamps (ns) of the last CR call, instance 0 rank 0
 __device__ __forceinline__ void cr_stamp(int i) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -2867,7 +2918,7 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
 template <int kRpt>
 __global__ void __launch_bounds__(kCrThreads, 1)
     k_cr(Params P, InstOff off, const DContact* __restrict__ C, CrContacts cc, Slots sl, const float* __restrict__ G,
-         const float* __restrict__ GA, const double4* __restrict__ x, ContactState cs, CrActive act) {
+         float* GA, const double4* __restrict__ x, ContactState cs, CrActive act) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char smraw[];
     cg::cluster_group cl = cg::this_cluster();
@@ -2883,7 +2934,16 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     const double h = P.h;
     const int S = P.S;
     cr_stamp(0);
-    const int na = act.na[inst];
+    // cluster CR (few instances): every CTA builds the active list itself (no k_active /
+    // k_gather_ga launches on the single-scene critical path); one CTA per instance: k_active's list
+    int na;
+    if (csize > 1) {
+        const CrLayout L0(nc, ns, 0, false);   // the active-list offsets do not depend on na
+        na = cr_active_block(ns, sb, cb, cc, sl, cs, (int*)(smraw + L0.aidx), (int*)(smraw + L0.apos),
+                             (int*)(smraw + L0.acon), (int*)(smraw + L0.red));
+    } else {
+        na = act.na[inst];
+    }
     const int per = (na + csize - 1) / csize;
     const int i0 = min(na, rank * per), i1 = min(na, i0 + per);
     const bool solo = csize == 1;
@@ -2927,7 +2987,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     // everything the prologue needs is precomputed (chain dot, k_active): plain loads only
     if (c9s)
         for (int e = threadIdx.x; e < 9 * nc; e += blockDim.x) cp_async4(&X.c9[e], &cc.c9[9 * cb + e], true);
-    for (int b = threadIdx.x; b < ns; b += blockDim.x) {
+    for (int b = threadIdx.x; b < ns && solo; b += blockDim.x) {
         cp_async4(&X.apos[b], &act.apos[sb + b], true);
         if (b < na) {   // k_active writes aidx/acon for the na active slots only
             cp_async4(&X.aidx[b], &act.aidx[sb + b], true);
@@ -2953,14 +3013,23 @@ __global__ void __launch_bounds__(kCrThreads, 1)
                 for (int c = threadIdx.x & 31; c < na; c += 32)
                     cp_async4(&X.gA[(size_t)rw * lda + c], &Gi[X.aidx[c]], true);
             }
-        } else {          // this CTA's rows of the G_A copy k_active wrote
-            const float* src = X.GAg + (size_t)X.i0 * na;
+        } else {          // this CTA's rows of G_A from the class Gram (active list built above)
+            const float* Gc = G + off.goff[off.cls[inst]];
             const int rows = X.i1 - X.i0;
-            for (int rw = threadIdx.x >> 5; rw < rows; rw += blockDim.x >> 5)
+            for (int rw = threadIdx.x >> 5; rw < rows; rw += blockDim.x >> 5) {
+                const float* Gi = Gc + (size_t)X.aidx[X.i0 + rw] * ns;
                 for (int c = threadIdx.x & 31; c < na; c += 32)
-                    cp_async4(&X.gA[(size_t)rw * lda + c], &src[(size_t)rw * na + c], true);
+                    cp_async4(&X.gA[(size_t)rw * lda + c], &Gi[X.aidx[c]], true);
+            }
         }
         cp_async_commit();
+    } else if (!solo) {   // rows too large for shared memory: this CTA's rows of G_A into its global copy
+        const float* Gc = G + off.goff[off.cls[inst]];
+        for (int i = X.i0 + (threadIdx.x >> 5); i < X.i1; i += blockDim.x >> 5) {
+            const float* Gi = Gc + (size_t)X.aidx[i] * ns;
+            for (int c = threadIdx.x & 31; c < na; c += 32) GA[off.gaoff[inst] + (size_t)i * na + c] = Gi[X.aidx[c]];
+        }
+        __syncthreads();   // visible to this CTA's matvec (L2 loads)
     }
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
 #pragma unroll
@@ -3494,12 +3563,12 @@ int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, 
     cudaError_t e;
     switch (rpt) {
         case 0:
-        case 1: e = cudaLaunchKernelEx(&cfg, k_cr<1>, P, off, c, cc, sl, G, GA, x, cs, act); break;
-        case 2: e = cudaLaunchKernelEx(&cfg, k_cr<2>, P, off, c, cc, sl, G, GA, x, cs, act); break;
-        case 3: e = cudaLaunchKernelEx(&cfg, k_cr<3>, P, off, c, cc, sl, G, GA, x, cs, act); break;
-        case 4: e = cudaLaunchKernelEx(&cfg, k_cr<4>, P, off, c, cc, sl, G, GA, x, cs, act); break;
-        case 5: e = cudaLaunchKernelEx(&cfg, k_cr<5>, P, off, c, cc, sl, G, GA, x, cs, act); break;
-        default: e = cudaLaunchKernelEx(&cfg, k_cr<6>, P, off, c, cc, sl, G, GA, x, cs, act); break;
+        case 1: e = cudaLaunchKernelEx(&cfg, k_cr<1>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
+        case 2: e = cudaLaunchKernelEx(&cfg, k_cr<2>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
+        case 3: e = cudaLaunchKernelEx(&cfg, k_cr<3>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
+        case 4: e = cudaLaunchKernelEx(&cfg, k_cr<4>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
+        case 5: e = cudaLaunchKernelEx(&cfg, k_cr<5>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_cr<6>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
     }
     return (int)e;
 }
