@@ -68,11 +68,12 @@ def oracle_sample(n_steps, warmup=0):
     t0 = time.perf_counter()
     o.set_contacts(sc.contacts)
     t_sc = time.perf_counter() - t0
-    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+    x, v, lam = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X), None
     times = []
     for k in range(warmup + n_steps):
         t0 = time.perf_counter()
-        x, v, _ = o.frame(x, v, pin_targets=x[o.pinned] + sc.h * sc.pin_velocity)
+        x, v, info = o.frame(x, v, pin_targets=x[o.pinned] + sc.h * sc.pin_velocity, lam0=lam)
+        lam = info["lam"]
         dt = time.perf_counter() - t0 + t_sc / ITERS
         if k >= warmup:
             times.append(dt)

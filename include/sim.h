@@ -126,9 +126,10 @@ typedef struct {
     int32_t n_panels;          /* fundamental supernodes (rows sharing their first column)               */
     int32_t n_contacts, n_contact_vertices;   /* summed over instances */
     int64_t frames_done;
-    double  last_cr_residual;  /* max over instances of |r| of the last CR solve (fp64), -1 if none      */
-    double  max_abs_phi_n;     /* max |phi_FB| over unilateral contacts at the last evaluated iterate   */
-    int32_t n_active, n_stick, n_slip;   /* frame-end classification (lambda_n > 0; stick / slip)        */
+    double  last_cr_residual;  /* max over the instance(s) of |r| of the last CR solve (fp64), -1 if none */
+    double  max_abs_phi_n;     /* max |phi_n| (NCP function) over unilateral contacts at the last iterate */
+    int32_t n_active, n_stick, n_slip;   /* frame-end classification (reading A21: lambda_n > 0; stick:
+                                            |ydot_f| <= r_f (mu lambda_n - |lambda_f|); slip otherwise)     */
     int32_t kernels_per_frame; /* kernel launches in one captured frame                                  */
     double  build_seconds;     /* host time of sim_build_sparse_inverse                                  */
     int64_t h2d_contact_bytes; /* host->device bytes of the last contact commit                          */
@@ -137,6 +138,9 @@ typedef struct {
     int64_t gram_rows_computed;  /* last contact commit: Delassus Gram rows computed ...                  */
     int64_t gram_rows_reused;    /* ... and rows copied from the previous commit (sim_set_schur_reuse)    */
     double  build_phase_seconds[5]; /* precompute: assemble A_v, ordering, Cholesky, K = L^-1, tile layouts  */
+    double  max_cone_violation; /* max over unilateral contacts of max(0, |lambda_f| - mu max(lambda_n, 0)) */
+    double  max_penetration;    /* max over unilateral contacts of max(0, -(J_n x - d_n)) at the frame end  */
+    int32_t instance;           /* the instance these per-instance fields describe, -1 = all            */
 } sim_stats;
 
 /* Validate the mesh and material, compute rest data (Dm^-1, volumes, lumped
@@ -165,6 +169,11 @@ int sim_build_sparse_inverse(sim_handle *h, double drop_tolerance);
  * use the grid CR, which needs n_instances == 1 (SIM_E_LIMIT otherwise); its
  * Gram G is stored per etree component (G is zero across components). */
 int sim_set_contacts(sim_handle *h, int32_t instance, const sim_contact *contacts, int32_t n);
+/* Multipliers across sim_set_contacts (reading A10): a contact that is the same constraint as
+ * one of the instance's previous set -- same kind, vertices, weights and row directions
+ * (n, t1, t2); offset, mu, compliance and obstacle velocity may change -- keeps that
+ * contact's lambda rows (the first unused match in the previous order); other contacts start
+ * from lambda = 0. */
 /* The same for instances first .. first+count-1 at once: counts[count],
  * contacts concatenated in instance order.  All-or-nothing on error. */
 int sim_set_contacts_batch(sim_handle *h, int32_t first, int32_t count, const int32_t *counts,
@@ -190,9 +199,11 @@ int sim_detect_contacts(sim_handle *h, int32_t instance, const sim_obstacle *obs
                         const int32_t *candidates, int32_t n_candidates, double margin, int32_t *n_found);
 
 /* Advance `frames` frames of `iterations` local-global iterations each
- * (Alg. 4).  Pinned vertices move by h * pin_velocity per frame.  Enqueued on
- * the handle's stream; returns after enqueueing (use sim_synchronize or any
- * blocking accessor). */
+ * (Alg. 4).  Per frame: s = x_t + h v_t + h^2 g; the iterate starts at
+ * x^0 = x_t + h v_t (reading A9) and the multipliers at the previous frame's lambda
+ * (Alg. 4 never resets lambda, reading A10; see sim_set_contacts for the carry across a new
+ * contact set).  Pinned vertices move by h * pin_velocity per frame.  Enqueued on the
+ * handle's stream; returns after enqueueing (use sim_synchronize or any blocking accessor). */
 int sim_step(sim_handle *h, int32_t frames, int32_t iterations);
 
 /* Block until all work enqueued on the handle's stream is done; checks the
@@ -203,13 +214,27 @@ int sim_step(sim_handle *h, int32_t frames, int32_t iterations);
  * the previous call; the running total is sim_stats.nonfinite_rollbacks. */
 int sim_synchronize(sim_handle *h);
 
-/* Constant velocity (m/s) of all pinned vertices (moving Dirichlet handle). */
+/* Pinned vertices (the mesh's `fixed` mask) are Dirichlet conditions eliminated from the
+ * system (reading A7) that move as "moving positional constraints": each
+ * pinned vertex-instance has a velocity, and every frame moves it by h * velocity (its frame-end
+ * position is the Dirichlet target of that frame; its v is that velocity).
+ * sim_set_pin_velocity: the same velocity v[3] (m/s) for every pinned vertex of every instance.
+ * sim_set_pins: per-vertex targets for one instance: pinned_xyz [n_pinned][3] (metres), the
+ * positions the pinned vertices take at the end of the NEXT frame, ordered by ascending
+ * original vertex index; n_pinned must equal the mesh's pinned-vertex count.  The call sets
+ * each pinned vertex's velocity to (target - current position) / h, on the handle's stream after
+ * the frames already enqueued, so later frames without a new call continue at that velocity.
+ * Both: SIM_E_INVALID on null / non-finite input or a wrong count, SIM_E_STATE before the build;
+ * borrowed for the call. */
 int sim_set_pin_velocity(sim_handle *h, const double v[3]);
+int sim_set_pins(sim_handle *h, int32_t instance, const double *pinned_xyz, int32_t n_pinned);
 
 /* x, v: [n_vertices][3] of one instance in original vertex order (caller
  * buffers; either may be NULL). */
 int sim_get_state(sim_handle *h, int32_t instance, double *x, double *v);
 int sim_set_state(sim_handle *h, int32_t instance, const double *x, const double *v);
+/* Both setters start the affected instances' multipliers from 0 (lambda is part of the state,
+ * reading A10); sim_set_lambda sets them explicitly. */
 /* Positions of all instances: x [n_instances][n_vertices][3]. */
 int sim_get_positions(sim_handle *h, double *x);
 /* The same positions, asynchronously: enqueued on the handle's stream after the frames
@@ -226,10 +251,22 @@ int sim_set_states(sim_handle *h, const double *x, const double *v);
 
 /* lambda: [rows] = (lambda_n, lambda_f1, lambda_f2) per unilateral contact,
  * (lambda_b) per bilateral contact of one instance, in the order given to
- * sim_set_contacts, from the most recent step. */
-int sim_get_lambda(sim_handle *h, int32_t instance, double *lambda, int32_t capacity);
+ * sim_set_contacts: the multipliers the next frame starts from (the most recent step's, carried
+ * into the current contact set).  *n_rows (may be NULL) receives the row count; lambda may be
+ * NULL to query it; SIM_E_INVALID if capacity < rows. */
+int sim_get_lambda(sim_handle *h, int32_t instance, double *lambda, int32_t capacity, int32_t *n_rows);
+/* Set the multipliers the next frame of one instance starts from (same row layout; n must be
+ * the instance's row count).  Borrowed for the call.  SIM_E_INVALID on a wrong count or a
+ * non-finite value. */
+int sim_set_lambda(sim_handle *h, int32_t instance, const double *lambda, int32_t n);
 
-int sim_get_stats(sim_handle *h, sim_stats *out);
+/* Statistics.  instance = -1: the whole handle (contact counts and classification summed, residual,
+ * |phi|, cone violation and penetration maximised over all instances); 0 <= instance < n_instances:
+ * the contact fields of that instance only (the mesh / build / timing fields are the handle's).
+ * The frame-end fields describe the state after the last sim_step (lambda and x of its last
+ * iteration); they are 0 (last_cr_residual -1) while no frame has run on the current contact
+ * set.  Synchronises the handle's stream.  SIM_E_INVALID on a bad instance. */
+int sim_get_stats(sim_handle *h, int32_t instance, sim_stats *out);
 
 /* Use a caller-provided cudaStream_t (e.g. torch.cuda.current_stream()). */
 int sim_set_stream(sim_handle *h, void *cuda_stream);
@@ -282,6 +319,14 @@ int sim_set_schur_reuse(sim_handle *h, int32_t on);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 
 void sim_destroy(sim_handle *h);         /* NULL-safe */
+
+/* Device memory (process-wide, e.g. PyTorch's caching allocator): every device buffer a handle
+ * allocates after this call comes from alloc(bytes, ctx) (device memory of the handle's device;
+ * NULL -> SIM_E_OOM from the calling API) and goes back through free_(ptr, ctx), called after
+ * cudaDeviceSynchronize so that no enqueued work still reads the buffer.  A buffer is always
+ * returned to the allocator it came from.  alloc = free_ = NULL restores cudaMalloc / cudaFree.
+ * SIM_E_INVALID if exactly one of alloc, free_ is NULL.  Thread-safe. */
+int sim_set_allocator(void *(*alloc)(size_t bytes, void *ctx), void (*free_)(void *ptr, void *ctx), void *ctx);
 const char *sim_last_error(void);
 
 /* ---------------------------------------------------------------------------

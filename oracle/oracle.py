@@ -46,7 +46,7 @@ import scipy.sparse.linalg as spla
 __all__ = [
     "lame", "rest_data", "assemble_Av", "deformation_gradients", "signed_svd",
     "project_sigma", "project", "elastic_forces", "Oracle", "cr_solve",
-    "fb_normal", "fb_friction", "minmap_normal", "minmap_friction", "contact_rows",
+    "fb_normal", "fb_friction", "minmap_normal", "minmap_friction", "contact_rows", "carry_multipliers",
 ]
 
 NCP_FB, NCP_MINMAP = 0, 1                  # NCP function (App. B)
@@ -256,7 +256,14 @@ def fb_friction(ydot, lam_f, lam_n, mu, r):
     lam_n > 0 and mu lam_n > 0: theta_f = 1,
       E_f = r (R - r q) / (s + mu r lam_n - R), s = |ydot|, q = mu lam_n - |lam_f|,
       R = sqrt(s^2 + r^2 q^2); the denominator is floored at
-      1e-6 (s + mu r lam_n) (reading A16: the 0/0 point has limit 0).
+      1e-6 (s + mu r lam_n) (reading A16).  Two places need the floor: the 0/0 point
+      (s = 0, |lam_f| = 0), where the limit is 0 (numerator 0 over a positive floor), and
+      the pole of the printed formula: the denominator is positive for |lam_f| < 2 mu lam_n
+      (s = 0) and E_f -> +inf as |lam_f| -> 2 mu lam_n from below; beyond it (possible since
+      lambda is not projected, A20) the printed expression turns negative, i.e. an
+      anti-dissipative friction compliance.  The floor continues E_f from the admissible
+      side: it stays large and positive (r (R - r q) / floor), so the row drives lam_f back
+      toward 0 instead of accelerating the slide (reading A16c).
     otherwise (inactive, or degenerate cone mu lam_n = 0, reading A16b):
       theta_f = 0, E_f = 1 (identity), so lam_f -> 0.
     """
@@ -393,6 +400,40 @@ def contact_rows(contacts):
                     np.zeros(0, int), np.zeros(0, int))
     return Rows(np.asarray(c), np.asarray(V, dtype=np.int64), np.asarray(W),
                 np.asarray(kind), np.asarray(own))
+
+
+def carry_multipliers(old_contacts, old_lam, new_contacts):
+    """lambda^0 for a new contact set (reading A10): Alg. 4 keeps lambda across frames
+    (P:L939-961 never resets it); when collision detection produces a new set, each new
+    contact keeps the rows of an identical constraint of the previous set -- same kind,
+    vertices, weights and row directions (n, t1, t2); the first unused one in the previous
+    order -- and starts from 0 otherwise."""
+    ro, rn = contact_rows(old_contacts), contact_rows(new_contacts)
+    lam = np.zeros(rn.c.shape[0])
+    if old_lam is None or len(old_contacts) == 0:
+        return lam
+    old_lam = np.asarray(old_lam, dtype=np.float64)
+
+    def starts(rows):
+        out, j = [], 0
+        while j < rows.c.shape[0]:
+            n = 1 if rows.kind[j] == 2 else 3
+            out.append((j, n))
+            j += n
+        return out
+
+    def key(rows, j, n):
+        return (n, rows.verts[j].tobytes(), rows.wts[j].tobytes(), rows.c[j:j + n].tobytes())
+
+    pool = {}
+    for j, n in starts(ro):
+        pool.setdefault(key(ro, j, n), []).append(j)
+    for j, n in starts(rn):
+        cand = pool.get(key(rn, j, n))
+        if cand:
+            o = cand.pop(0)
+            lam[j:j + n] = old_lam[o:o + n]
+    return lam
 
 
 # ---------------------------------------------------------------------------
@@ -533,6 +574,12 @@ class Oracle:
                 E[j0] = self.e_row[j0]
                 continue
             yn = Jx[j0] - self.d_row[j0]              # y_n = J_n x^k - d_n
+            # reading A15: a gap within rounding of zero is zero.  At (y, lambda) = (0, 0) the
+            # normal NCP's derivative theta_n = 1 - y/|y| jumps between 0 and 2 with the sign
+            # of y, so the evaluation's own rounding must not pick the branch: the 0/0 rule
+            # (theta_n = 1, E_n = 0) applies to every |y| <= 1e-12 (|J_n x| + |d_n|)
+            if abs(yn) <= 1e-12 * (abs(Jx[j0]) + abs(self.d_row[j0])):
+                yn = 0.0
             nfun, ffun = (minmap_normal, minmap_friction) if self.ncp == NCP_MINMAP else (fb_normal, fb_friction)
             ph, th, En = nfun(yn, lam[j0], self.r_row[j0])
             phi[j0], theta[j0], E[j0] = ph, th, En
@@ -547,22 +594,37 @@ class Oracle:
 
     # --- one frame ------------------------------------------------------------
     def frame(self, x_t: np.ndarray, v_t: np.ndarray, pin_targets: Optional[np.ndarray] = None,
-              capture: bool = False):
-        """Alg. 4 body for one time step.  Returns (x, v, info)."""
+              capture: bool = False, lam0: Optional[np.ndarray] = None, start=None):
+        """Alg. 4 body for one time step.  Returns (x, v, info); info["lam"] holds the
+        multipliers at frame end.
+
+        lam0: the multipliers the frame starts from.  Alg. 4 never resets lambda
+        inside `while simulation`, so lambda^0 of a frame is the previous frame's final lambda
+        (reading A10); pass info["lam"] of the previous frame (carried across a contact change
+        by carry_multipliers), or None for a first frame (0).
+        Initial iterate (reading A9): x^0 = x_t + h v_t, the inertial extrapolation without the
+        external-force term (s itself still enters b = M s + ...).
+        start: (x_k, lambda_k, k) continues the frame from iterate k (the conditioning checks of
+        tests/_parity.py); x_k must carry the pinned targets."""
         h = self.h
         x_t = np.asarray(x_t, dtype=np.float64)
         v_t = np.asarray(v_t, dtype=np.float64)
         # s = x_t + h v_t + h^2 M^-1 f_ext, f_ext = M g (P:L948, A8)
         s = x_t + h * v_t + h * h * self.g[None, :]
-        x = s.copy()                                   # x^0 = s (A9)
+        x = x_t + h * v_t                              # x^0 (A9)
         if self.pinned.size:
             tgt = x_t[self.pinned] if pin_targets is None else np.asarray(pin_targets, float)
             x[self.pinned] = tgt
-        lam = np.zeros(self.m)                         # lambda^0 = 0 (A10)
+        lam = np.zeros(self.m) if lam0 is None else np.array(lam0, dtype=np.float64)   # lambda^0 (A10)
+        if lam.shape != (self.m,):
+            raise ValueError(f"lam0 must hold {self.m} rows")
+        k0 = 0
+        if start is not None:
+            x, lam, k0 = np.array(start[0], dtype=np.float64), np.array(start[1], dtype=np.float64), int(start[2])
         F_ = self.free
         info = {"iters": [], "lam": None}
         u = np.zeros((self.T.shape[0], 3, 3))          # ADMM dual (reading A33)
-        for it in range(self.lg_iters):
+        for it in range(k0, self.lg_iters):
             F = deformation_gradients(x, self.T, self.Bm)
             if self.admm:
                 # ADMM-PD: z = argmin psi(z) + w/2 |F + u - z|^2; u <- u + F - z;
@@ -610,6 +672,7 @@ class Oracle:
                                x_tilde=xt)
             if capture:
                 rec["x_next"] = xn.copy()
+                rec["lam"] = lam.copy()
                 info["iters"].append(rec)
             x = xn
         info["lam"] = lam

@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = [
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
     "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison", "sim_get_positions_async",
     "sim_wait_positions", "sim_detect_contacts", "sim_get_contacts",
-    "sim_set_schur_reuse",
+    "sim_set_schur_reuse", "sim_set_lambda", "sim_set_pins", "sim_set_allocator",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -90,11 +90,39 @@ class SimStats(C.Structure):
                 ("kernels_per_frame", C.c_int32), ("build_seconds", C.c_double),
                 ("h2d_contact_bytes", C.c_int64), ("n_instances", C.c_int32),
                 ("nonfinite_rollbacks", C.c_int64), ("gram_rows_computed", C.c_int64),
-                ("gram_rows_reused", C.c_int64), ("build_phase_seconds", C.c_double * 5)]
+                ("gram_rows_reused", C.c_int64), ("build_phase_seconds", C.c_double * 5),
+                ("max_cone_violation", C.c_double), ("max_penetration", C.c_double), ("instance", C.c_int32)]
 
 
 class SimError(RuntimeError):
     pass
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+_allocator_refs = []
+
+
+def use_torch_allocator(on=True):
+    """Route the library's device allocations through PyTorch's caching allocator
+    (sim_set_allocator) for handles created afterwards; on=False restores cudaMalloc."""
+    if not on:
+        _check(lib.sim_set_allocator(None, None, None))
+        return
+    import torch
+
+    def _alloc(nbytes, ctx):
+        try:
+            return int(torch.cuda.caching_allocator_alloc(int(nbytes)))
+        except Exception:
+            return None
+
+    def _free(ptr, ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    fa, ff = ALLOC_FN(_alloc), FREE_FN(_free)
+    _allocator_refs[:] = [fa, ff]   # keep the trampolines alive while the library may call them
+    _check(lib.sim_set_allocator(C.cast(fa, C.c_void_p), C.cast(ff, C.c_void_p), None))
 
 
 def _load():
@@ -116,8 +144,11 @@ def _load():
         "sim_set_pin_velocity": [H, dp],
         "sim_get_state": [H, C.c_int32, dp, dp],
         "sim_set_state": [H, C.c_int32, dp, dp],
-        "sim_get_lambda": [H, C.c_int32, dp, C.c_int32],
-        "sim_get_stats": [H, C.POINTER(SimStats)],
+        "sim_get_lambda": [H, C.c_int32, dp, C.c_int32, C.POINTER(C.c_int32)],
+        "sim_set_lambda": [H, C.c_int32, dp, C.c_int32],
+        "sim_get_stats": [H, C.c_int32, C.POINTER(SimStats)],
+        "sim_set_pins": [H, C.c_int32, dp, C.c_int32],
+        "sim_set_allocator": [C.c_void_p, C.c_void_p, C.c_void_p],
         "sim_set_stream": [H, C.c_void_p],
         "sim_debug_get_inverse": [H, ip, ip, C.POINTER(C.c_int64), fp],
         "sim_debug_apply_inverse": [H, dp, dp],
@@ -273,6 +304,12 @@ class Sim:
         a = np.ascontiguousarray(v, dtype=np.float64)
         _check(lib.sim_set_pin_velocity(self._h, _dptr(a)))
 
+    def set_pins(self, targets, instance=0):
+        """Positions the pinned vertices (ascending original index) take at the end of the next
+        frame, [n_pinned][3] (sim_set_pins)."""
+        a = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1, 3)
+        _check(lib.sim_set_pins(self._h, int(instance), _dptr(a), int(a.shape[0])))
+
     def get_state(self, instance=0):
         x = np.empty((self.n_v, 3))
         v = np.empty((self.n_v, 3))
@@ -347,17 +384,22 @@ class Sim:
         return arr[:n.value]
 
     def get_lambda(self, instance=0):
-        nc = self._nc[instance]
-        cap = 3 * max(1, nc)
-        out = np.empty(cap)
-        _check(lib.sim_get_lambda(self._h, int(instance), _dptr(out), cap))
-        cl = self._contacts[instance]
-        rows = sum(1 if getattr(c, "kind", 0) == 1 else 3 for c in cl) if cl else 3 * nc
-        return out[:rows]
+        """Multipliers the next frame of `instance` starts from (sim_get_lambda)."""
+        n = C.c_int32(0)
+        _check(lib.sim_get_lambda(self._h, int(instance), None, 0, C.byref(n)))
+        out = np.empty(max(1, n.value))
+        _check(lib.sim_get_lambda(self._h, int(instance), _dptr(out), out.size, C.byref(n)))
+        return out[:n.value]
 
-    def stats(self):
+    def set_lambda(self, lam, instance=0):
+        """Multipliers the next frame of `instance` starts from (sim_set_lambda)."""
+        a = np.ascontiguousarray(lam, dtype=np.float64).reshape(-1)
+        _check(lib.sim_set_lambda(self._h, int(instance), _dptr(a) if a.size else None, int(a.size)))
+
+    def stats(self, instance=-1):
+        """sim_get_stats: instance -1 = the whole handle, else that instance's contact fields."""
         s = SimStats()
-        _check(lib.sim_get_stats(self._h, C.byref(s)))
+        _check(lib.sim_get_stats(self._h, int(instance), C.byref(s)))
         out = {k: getattr(s, k) for k, _ in SimStats._fields_}
         out["build_phase_seconds"] = list(s.build_phase_seconds)
         return out

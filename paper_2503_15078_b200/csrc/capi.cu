@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -41,6 +42,34 @@ static int fail(int code, const char* fmt, ...) {
         }                                                                                     \
     } while (0)
 
+// device allocator (sim_set_allocator): process-wide; every buffer remembers the allocator it
+// was allocated with and is returned to it
+struct SimAllocator {
+    void* (*alloc)(size_t, void*) = nullptr;
+    void (*free_)(void*, void*) = nullptr;
+    void* ctx = nullptr;
+};
+static std::mutex g_alloc_mu;
+static SimAllocator g_alloc;
+
+static cudaError_t dev_alloc(void** p, size_t bytes, SimAllocator& used) {
+    {
+        std::lock_guard<std::mutex> lk(g_alloc_mu);
+        used = g_alloc;
+    }
+    if (!used.alloc) return cudaMalloc(p, bytes);
+    *p = used.alloc(bytes, used.ctx);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+}
+static void dev_free(void* p, const SimAllocator& used) {
+    if (!used.free_) {
+        cudaFree(p);   // implicitly waits for the device work that may still read p
+        return;
+    }
+    cudaDeviceSynchronize();   // a caching allocator may hand p out again right away
+    used.free_(p, used.ctx);
+}
+
 template <class T>
 struct DPtr {   // a view into a device arena
     T* p = nullptr;
@@ -50,11 +79,19 @@ template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
+    SimAllocator al;
     cudaError_t alloc(size_t cnt) {
         release();
         n = cnt;
         if (cnt == 0) return cudaSuccess;
-        return cudaMalloc(&p, cnt * sizeof(T));
+        void* q = nullptr;
+        cudaError_t e = dev_alloc(&q, cnt * sizeof(T), al);
+        if (e != cudaSuccess) {
+            n = 0;
+            return e;
+        }
+        p = (T*)q;
+        return cudaSuccess;
     }
     cudaError_t upload(const T* h, size_t cnt, cudaStream_t st) {
         if (cnt == 0) return cudaSuccess;
@@ -67,7 +104,7 @@ struct DBuf {
         return alloc(std::max<size_t>(cnt + cnt / 4, 16));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p, al);
         p = nullptr;
         n = 0;
     }
@@ -87,7 +124,54 @@ struct InstContacts {
     std::vector<int32_t> s0, v0, c1; // local slot / vertex / local contact
     int64_t chain_total = 0;         // sum over slots of (depth + 1)
     bool large = false;              // beyond the cluster CR's limits: needs the grid CR (one scene)
+    // lambda carried across commits (reading A10): carry[c] = local index of the identical
+    // constraint in the instance's device-committed set (whose lambda is on the device), or -1
+    std::vector<int32_t> carry;
+    bool dev = false;                // this set is the device-committed one
 };
+
+// identity of a constraint for the lambda carry: kind, vertices, weights, row directions
+static bool same_constraint(const DContact& a, const DContact& b) {
+    if (a.kind != b.kind || a.nv != b.nv) return false;
+    for (int q = 0; q < a.nv; ++q)
+        if (a.vtx[q] != b.vtx[q] || a.w[q] != b.w[q]) return false;
+    return memcmp(a.c, b.c, sizeof a.c) == 0;
+}
+static uint64_t constraint_hash(const DContact& a) {
+    uint64_t h = 1469598103934665603ull ^ (uint64_t)(a.kind * 8 + a.nv);
+    for (int q = 0; q < a.nv; ++q) h = (h ^ (uint64_t)(uint32_t)a.vtx[q]) * 1099511628211ull;
+    return h;
+}
+// nw.carry from the instance's previous set `old`: each new contact takes the first unused
+// identical constraint of `old` (old.dev: its index; otherwise old's own carry, so that several
+// sim_set_contacts calls between two steps compose)
+static void compute_carry(const InstContacts& old, InstContacts& nw) {
+    const int n = (int)nw.hc.size(), no = (int)old.hc.size();
+    nw.carry.assign(n, -1);
+    if (no == 0 || n == 0) return;
+    {   // common case (a detector re-emitting the same set): contact c is old contact c
+        int c = 0;
+        while (c < std::min(n, no) && same_constraint(old.hc[c], nw.hc[c])) ++c;
+        if (c == n) {
+            for (int k = 0; k < n; ++k) nw.carry[k] = old.dev ? k : (k < (int)old.carry.size() ? old.carry[k] : -1);
+            return;
+        }
+    }
+    std::unordered_map<uint64_t, std::vector<int>> pool;
+    for (int c = no - 1; c >= 0; --c) pool[constraint_hash(old.hc[c])].push_back(c);   // popped from the back
+    for (int c = 0; c < n; ++c) {
+        auto it = pool.find(constraint_hash(nw.hc[c]));
+        if (it == pool.end()) continue;
+        std::vector<int>& v = it->second;
+        for (int k = (int)v.size() - 1; k >= 0; --k)
+            if (same_constraint(old.hc[v[k]], nw.hc[c])) {
+                const int o = v[k];
+                v.erase(v.begin() + k);
+                nw.carry[c] = old.dev ? o : (o < (int)old.carry.size() ? old.carry[o] : -1);
+                break;
+            }
+    }
+}
 
 struct sim_handle {
     bool host_only = false;
@@ -115,7 +199,10 @@ struct sim_handle {
     int bparts = 0, bblocks1 = 0;
     int64_t nnzL = 0;
     double build_seconds = 0;
-    double vpin[3] = {0, 0, 0};
+    DBuf<double4> vpin;              // [n_v - n_f][S] pinned-vertex velocities (moving Dirichlet targets)
+    DBuf<double4> pin_tgt;           // sim_set_pins staging on the device
+    double4* pin_stage = nullptr;    // pinned host staging of sim_set_pins
+    cudaEvent_t pin_free = nullptr;
     // device: state, [entity][S]
     DBuf<double4> x, xt, v, s;
     DBuf<double4> vt;                // frame-start velocity (rollback on a non-finite frame)
@@ -202,6 +289,10 @@ struct sim_handle {
     DPtr<int64_t> pgoff;
     DPtr<int2> newslots;
     DBuf<double> lam, theta, cdiag, hvec, hl, dxt, wz, phi_abs, cr_res, rho;
+    DBuf<double> lam_prev;           // the previous commit's lambda while it is carried (reading A10)
+    std::vector<int> coff_dev;       // contact offsets of the device-committed set (lambda's layout)
+    int C_dev = 0;
+    DPtr<int32_t> carry;             // [C] (arena): previous-commit contact of each contact, or -1
     DBuf<int> act_na, act_idx, act_pos, act_con;   // CR active set (k_active)
     DBuf<float4> wzT;
     DBuf<int32_t> chain_rows, slotmap;
@@ -330,6 +421,15 @@ extern "C" int sim_create_host(const sim_mesh* m, const sim_material* mat, doubl
 
 extern "C" const char* sim_last_error(void) { return g_err.c_str(); }
 
+extern "C" int sim_set_allocator(void* (*alloc)(size_t, void*), void (*free_)(void*, void*), void* ctx) {
+    if ((alloc == nullptr) != (free_ == nullptr)) return fail(SIM_E_INVALID, "alloc and free must both be set or both NULL");
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    g_alloc.alloc = alloc;
+    g_alloc.free_ = free_;
+    g_alloc.ctx = alloc ? ctx : nullptr;
+    return SIM_OK;
+}
+
 extern "C" void sim_destroy(sim_handle* H) {
     if (!H) return;
     if (!H->host_only) {
@@ -351,6 +451,9 @@ extern "C" void sim_destroy(sim_handle* H) {
         if (H->join_ev) cudaEventDestroy(H->join_ev);
         if (H->aux) cudaStreamDestroy(H->aux);
         if (H->stage) cudaFreeHost(H->stage);
+        if (H->pin_free) cudaEventSynchronize(H->pin_free);
+        if (H->pin_stage) cudaFreeHost(H->pin_stage);
+        if (H->pin_free) cudaEventDestroy(H->pin_free);
         if (H->own_stream && H->stream) cudaStreamDestroy(H->stream);
     }
     delete H;   // device buffers are released by their destructors
@@ -385,6 +488,8 @@ static int upload_all(sim_handle* H) {
     const size_t nvS = (size_t)nv * S;
     CK(H->x.alloc(nvS)); CK(H->xt.alloc(nvS)); CK(H->v.alloc(nvS)); CK(H->s.alloc(nvS));
     CK(H->vt.alloc(nvS)); CK(H->bad.alloc(S));
+    CK(H->vpin.alloc((size_t)(nv - nf) * S));
+    if (nv > nf) CK(cudaMemsetAsync(H->vpin.p, 0, (size_t)(nv - nf) * S * sizeof(double4), st));
     CK(cudaMemsetAsync(H->bad.p, 0, S * sizeof(int), st));
     CK(H->rollbacks.alloc(1));
     CK(cudaMemsetAsync(H->rollbacks.p, 0, sizeof(int), st));
@@ -738,6 +843,7 @@ extern "C" int sim_set_contacts(sim_handle* H, int32_t instance, const sim_conta
     std::string err;
     rc = build_inst(H, cs, n, I, err);
     if (rc) return fail(rc, "%s", err.c_str());
+    compute_carry(H->ic[instance], I);
     H->ic[instance] = std::move(I);
     H->dirty = true;
     H->set_contacts_host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count();
@@ -870,7 +976,10 @@ extern "C" int sim_set_contacts_batch(sim_handle* H, int32_t first, int32_t coun
     std::vector<int> codes(count, SIM_OK);
     std::vector<std::string> errs(count);
 #pragma omp parallel for schedule(dynamic, 4)
-    for (int i = 0; i < count; ++i) codes[i] = build_inst(H, cs + at[i], counts[i], tmp[i], errs[i]);
+    for (int i = 0; i < count; ++i) {
+        codes[i] = build_inst(H, cs + at[i], counts[i], tmp[i], errs[i]);
+        if (codes[i] == SIM_OK) compute_carry(H->ic[first + i], tmp[i]);
+    }
     for (int i = 0; i < count; ++i)
         if (codes[i]) return fail(codes[i], "instance %d: %s", first + i, errs[i].c_str());
     for (int i = 0; i < count; ++i) H->ic[first + i] = std::move(tmp[i]);
@@ -911,7 +1020,8 @@ static Params make_params(const sim_handle* H) {
     P.n_t = H->n_t;
     P.S = H->S;
     P.h = H->h;
-    for (int d = 0; d < 3; ++d) { P.g[d] = H->mat.gravity[d]; P.vpin[d] = H->vpin[d]; }
+    for (int d = 0; d < 3; ++d) P.g[d] = H->mat.gravity[d];
+    P.vpin = H->vpin.p;
     P.model = H->mat.model;
     P.k = (float)H->kproj;
     P.mu = (float)H->mu_l;
@@ -979,7 +1089,9 @@ static int commit_host(sim_handle* H) {
     }
     const int NG = (int)gcs.size() - 1;
     // Gram reuse: every class maps to the previous class of its representative instance
-    bool reuse = H->schur_reuse && !grid && H->have_prev && (int)H->prev_cls_of_inst.size() == S;
+    // (not while the previous commit's device half is pending: G does not hold that commit's
+    // blocks yet, while prev_* already describes them)
+    bool reuse = H->schur_reuse && !grid && H->have_prev && !H->dev_pending && (int)H->prev_cls_of_inst.size() == S;
     std::vector<int> rmap_h, pns_h(NCL, 0);
     std::vector<int64_t> pgoff_h(NCL, 0);
     std::vector<int2> news_h;
@@ -1054,7 +1166,7 @@ static int commit_host(sim_handle* H) {
     const size_t cC = std::max(Ct, 1), cS = std::max(NSt, 1), cCS = std::max(CSt, 1);
     CK(H->G.ensure(std::max<int64_t>(goff[NCL], 1), grew));
     CK(H->GA.ensure(std::max<int64_t>(gaoff[S], 1), grew));
-    CK(H->lam.ensure(3 * cC, grew)); CK(H->theta.ensure(3 * cC, grew)); CK(H->cdiag.ensure(3 * cC, grew));
+    CK(H->theta.ensure(3 * cC, grew)); CK(H->cdiag.ensure(3 * cC, grew));
     CK(H->hvec.ensure(3 * cC, grew)); CK(H->hl.ensure(3 * cC, grew)); CK(H->rho.ensure(3 * cC, grew));
     CK(H->phi_abs.ensure(cC, grew)); CK(H->dxt.ensure(3 * cS, grew)); CK(H->wz.ensure(3 * cS, grew));
     CK(H->act_idx.ensure(cS, grew)); CK(H->act_pos.ensure(cS, grew)); CK(H->act_con.ensure(cS, grew));
@@ -1089,7 +1201,7 @@ static int commit_host(sim_handle* H) {
               g_cc = seg(4 * (size_t)CSt), g_co = seg(4 * S1), g_so = seg(4 * S1), g_ga = seg(8 * S1),
               g_cl = seg(4 * (size_t)S), g_cso = seg(4 * C1), g_go = seg(8 * C1), g_uo = seg(4 * C1),
               g_zo = seg(8 * C1), g_cmo = seg(4 * C1), g_cm = seg(4 * (size_t)S), g_icd = seg(8 * it_cd.size()),
-              g_isc = seg(8 * it_sc.size());
+              g_isc = seg(8 * it_sc.size()), g_car = seg(4 * (size_t)Ct);
     const size_t NSg = grid ? (size_t)NSt : 0;
     const Seg g_rm = seg(4 * rmap_h.size()), g_pg = seg(8 * pgoff_h.size()), g_pn = seg(4 * pns_h.size()),
               g_nw = seg(8 * news_h.size());
@@ -1105,7 +1217,7 @@ static int commit_host(sim_handle* H) {
                                          g_sci.at, g_scw.at, g_ch.at, g_cv.at, g_cc.at, g_co.at, g_so.at, g_ga.at,
                                          g_cl.at, g_cso.at, g_go.at, g_uo.at, g_zo.at, g_cmo.at, g_cm.at, g_icd.at,
                                          g_isc.at, g_gcs.at, g_ggo.at, g_grw.at, g_gs0.at, g_gn.at, g_git.at,
-                                         g_rm.at, g_pg.at, g_pn.at, g_nw.at};
+                                         g_rm.at, g_pg.at, g_pn.at, g_nw.at, g_car.at};
         if (grew || lay != H->arena_layout) H->contact_gen++;
         H->arena_layout = lay;
     }
@@ -1126,6 +1238,7 @@ static int commit_host(sim_handle* H) {
         H->g_items.p = (int2*)(A + g_git.at);
         H->rmap.p = (int*)(A + g_rm.at); H->pgoff.p = (int64_t*)(A + g_pg.at); H->pns.p = (int*)(A + g_pn.at);
         H->newslots.p = (int2*)(A + g_nw.at);
+        H->carry.p = (int32_t*)(A + g_car.at);
     }
     if (!H->stage_free) CK(cudaEventCreateWithFlags(&H->stage_free, cudaEventDisableTiming));
     CK(cudaEventSynchronize(H->stage_free));   // the previous commit's copies are done
@@ -1143,11 +1256,22 @@ static int commit_host(sim_handle* H) {
     int32_t *svtx = (int32_t*)(B + g_sv.at), *sinst = (int32_t*)(B + g_si.at), *scp = (int32_t*)(B + g_scp.at);
     int32_t* sci = (int32_t*)(B + g_sci.at);
     float* scw = (float*)(B + g_scw.at);
+    int32_t* car = (int32_t*)(B + g_car.at);
+    const bool have_dev = (int)H->coff_dev.size() == S + 1;
 #pragma omp parallel for schedule(dynamic, 8)
     for (int i = 0; i < S; ++i) {
         const InstContacts& I = H->ic[i];
         const int cb = coff[i], sb = soff[i], n = (int)I.hc.size(), ns = (int)I.verts.size();
         const int pb = (int)poff[i];
+        // lambda carry into the device layout of the last device commit (reading A10)
+        for (int c = 0; c < n; ++c) {
+            int src = -1;
+            if (have_dev) {
+                const int lc = I.dev ? c : (c < (int)I.carry.size() ? I.carry[c] : -1);
+                if (lc >= 0 && lc < H->coff_dev[i + 1] - H->coff_dev[i]) src = H->coff_dev[i] + lc;
+            }
+            car[cb + c] = src;
+        }
         for (int c = 0; c < n; ++c) {
             DContact d = I.hc[c];
             d.inst = i;
@@ -1337,6 +1461,23 @@ static int commit_device(sim_handle* H) {
     CK(cudaMemsetAsync(H->slotmap.p, 0xff, (size_t)nf * S * sizeof(int32_t), st));
     CK(cudaMemsetAsync(H->ucount.p, 0, 2 * (size_t)NCL * sizeof(int), st));
     CK(cudaMemsetAsync(H->cr_res.p, 0, S * sizeof(double), st));
+    {   // lambda of the previous commit -> lam_prev, then carried into the new layout (reading A10)
+        bool g1 = false, g2 = false;
+        const size_t nold = 3 * (size_t)H->C_dev;
+        if (nold) {
+            CK(H->lam_prev.ensure(nold, g1));
+            CK(cudaMemcpyAsync(H->lam_prev.p, H->lam.p, nold * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        }
+        if (3 * (size_t)std::max(H->C, 1) > H->lam.n || !H->lam.p) {
+            CK(cudaStreamSynchronize(st));   // the frames in flight and the copy above are done with lam
+            CK(H->lam.ensure(3 * (size_t)std::max(H->C, 1), g2));
+            H->contact_gen++;                // lam is a captured kernel argument
+        }
+        launch_carry_lambda(st, H->C, H->carry.p, nold ? H->lam_prev.p : nullptr, H->lam.p);
+        H->coff_dev = H->coff_h;
+        H->C_dev = H->C;
+        for (InstContacts& I : H->ic) { I.dev = true; I.carry.clear(); }
+    }
     Params P = make_params(H);
     const InstOff off = inst_off(H);
     const Slots sl = slots(H);
@@ -1437,7 +1578,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
 #define MARK(k) do { int r_ = mark(k); if (r_) return -r_; } while (0)
 #define CKR(call) do { cudaError_t r_ = (call); if (r_ != cudaSuccess) return -(int)r_; } while (0)
     MARK(KK_PREDICT);
-    launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->lam.p, 3 * H->C, H->vt.p, H->bad.p); nk++;
+    launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->vt.p, H->bad.p); nk++;
     if (H->poison_inst >= 0) launch_poison(st, H->x.p, H->poison_inst, H->S);   // test hook (not captured)
     const bool con = H->C > 0;
     for (int k = 0; k < iters; ++k) {
@@ -1645,11 +1786,39 @@ extern "C" int sim_set_pin_velocity(sim_handle* H, const double v[3]) {
     if (!H || !v) return fail(SIM_E_INVALID, "null argument");
     for (int d = 0; d < 3; ++d)
         if (!std::isfinite(v[d])) return fail(SIM_E_INVALID, "pin velocity not finite");
-    for (int d = 0; d < 3; ++d) H->vpin[d] = v[d];
-    if (H->gexec) {   // vpin is a captured kernel argument
-        cudaGraphExecDestroy(H->gexec);
-        H->gexec = nullptr;
+    if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "build the sparse inverse first");
+    const size_t n = (size_t)(H->n_v - H->n_f) * H->S;
+    if (n == 0) return SIM_OK;
+    std::vector<double4> hv(n, make_double4(v[0], v[1], v[2], 0.0));
+    CK(cudaStreamSynchronize(H->stream));
+    CK(cudaMemcpy(H->vpin.p, hv.data(), n * sizeof(double4), cudaMemcpyHostToDevice));
+    return SIM_OK;
+}
+
+extern "C" int sim_set_pins(sim_handle* H, int32_t inst, const double* xyz, int32_t n_pinned) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "build the sparse inverse first");
+    if (inst < 0 || inst >= H->S) return fail(SIM_E_INVALID, "instance %d out of range [0, %d)", inst, H->S);
+    const int np = H->n_v - H->n_f;
+    if (n_pinned != np) return fail(SIM_E_INVALID, "%d targets given, the mesh has %d pinned vertices", n_pinned, np);
+    if (np == 0) return SIM_OK;
+    if (!xyz) return fail(SIM_E_INVALID, "null targets");
+    for (int64_t i = 0; i < 3LL * np; ++i)
+        if (!std::isfinite(xyz[i])) return fail(SIM_E_INVALID, "target %lld not finite", (long long)(i / 3));
+    cudaStream_t st = H->stream;
+    if (!H->pin_stage) {
+        CK(H->pin_tgt.alloc(np));
+        CK(cudaMallocHost((void**)&H->pin_stage, np * sizeof(double4)));
+        CK(cudaEventCreateWithFlags(&H->pin_free, cudaEventDisableTiming));
+        CK(cudaEventRecord(H->pin_free, st));
     }
+    CK(cudaEventSynchronize(H->pin_free));   // the previous call's copy has left the staging buffer
+    // compact order = ascending original id of the pinned vertices = internal ids n_f .. n_v - 1
+    for (int p = 0; p < np; ++p) H->pin_stage[p] = make_double4(xyz[3 * p], xyz[3 * p + 1], xyz[3 * p + 2], 0.0);
+    CK(cudaMemcpyAsync(H->pin_tgt.p, H->pin_stage, np * sizeof(double4), cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(H->pin_free, st));
+    launch_pin_targets(st, H->n_f, np, H->S, inst, H->h, H->x.p, H->pin_tgt.p, H->vpin.p);
+    CK(cudaGetLastError());
     return SIM_OK;
 }
 
@@ -1768,6 +1937,8 @@ extern "C" int sim_set_states(sim_handle* H, const double* x, const double* v) {
             }
         CK(cudaMemcpy(pass == 0 ? H->x.p : H->v.p, h.data(), h.size() * sizeof(double4), cudaMemcpyHostToDevice));
     }
+    // a new initial state starts from lambda = 0 (the multipliers are part of the state, A10)
+    if (H->C_dev > 0) CK(cudaMemset(H->lam.p, 0, 3 * (size_t)H->C_dev * sizeof(double)));
     return SIM_OK;
 }
 
@@ -1787,18 +1958,30 @@ extern "C" int sim_set_state(sim_handle* H, int32_t inst, const double* x, const
     CK(cudaStreamSynchronize(H->stream));
     if (x) CK(copy_column_h2d(H, hx.data(), inst, H->x.p));
     if (v) CK(copy_column_h2d(H, hv.data(), inst, H->v.p));
+    if ((int)H->coff_dev.size() == H->S + 1) {   // this instance's multipliers restart from 0 (A10)
+        const int c0 = H->coff_dev[inst], c1 = H->coff_dev[inst + 1];
+        if (c1 > c0) CK(cudaMemset(H->lam.p + 3 * (size_t)c0, 0, 3 * (size_t)(c1 - c0) * sizeof(double)));
+    }
     return SIM_OK;
 }
 
-extern "C" int sim_get_lambda(sim_handle* H, int32_t inst, double* lam, int32_t cap) {
+// rows of an instance's device-committed contact set (1 per bilateral, 3 per unilateral contact)
+static int lambda_rows(const InstContacts& I) {
+    int rows = 0;
+    for (const DContact& d : I.hc) rows += d.kind == 1 ? 1 : 3;
+    return rows;
+}
+
+extern "C" int sim_get_lambda(sim_handle* H, int32_t inst, double* lam, int32_t cap, int32_t* n_rows) {
     int rc = check_instance(H, inst);
     if (rc) return rc;
-    if (!lam) return fail(SIM_E_INVALID, "null argument");
-    if (H->dirty || H->dev_pending) return fail(SIM_E_STATE, "contacts changed since the last step");
+    rc = commit_contacts(H);   // a pending commit carries lambda into the current set's layout
+    if (rc) return rc;
     const InstContacts& I = H->ic[inst];
     const int nc = (int)I.hc.size();
-    int rows = 0;
-    for (int c = 0; c < nc; ++c) rows += I.hc[c].kind == 1 ? 1 : 3;
+    const int rows = lambda_rows(I);
+    if (n_rows) *n_rows = rows;
+    if (!lam) return SIM_OK;
     if (cap < rows) return fail(SIM_E_INVALID, "capacity %d < %d rows", cap, rows);
     std::vector<double> l(3 * (size_t)nc);
     CK(cudaStreamSynchronize(H->stream));
@@ -1815,9 +1998,37 @@ extern "C" int sim_get_lambda(sim_handle* H, int32_t inst, double* lam, int32_t 
     return SIM_OK;
 }
 
-extern "C" int sim_get_stats(sim_handle* H, sim_stats* o) {
+extern "C" int sim_set_lambda(sim_handle* H, int32_t inst, const double* lam, int32_t n) {
+    int rc = check_instance(H, inst);
+    if (rc) return rc;
+    rc = commit_contacts(H);
+    if (rc) return rc;
+    const InstContacts& I = H->ic[inst];
+    const int nc = (int)I.hc.size();
+    if (n != lambda_rows(I)) return fail(SIM_E_INVALID, "%d rows given, the contact set has %d", n, lambda_rows(I));
+    if (n > 0 && !lam) return fail(SIM_E_INVALID, "null lambda");
+    for (int j = 0; j < n; ++j)
+        if (!std::isfinite(lam[j])) return fail(SIM_E_INVALID, "lambda row %d not finite", j);
+    std::vector<double> l(3 * (size_t)nc, 0.0);
+    int r = 0;
+    for (int c = 0; c < nc; ++c) {
+        l[3 * c] = lam[r++];
+        if (I.hc[c].kind != 1) {
+            l[3 * c + 1] = lam[r++];
+            l[3 * c + 2] = lam[r++];
+        }
+    }
+    CK(cudaStreamSynchronize(H->stream));
+    if (nc) CK(cudaMemcpy(H->lam.p + 3 * (size_t)H->coff_h[inst], l.data(), l.size() * sizeof(double),
+                          cudaMemcpyHostToDevice));
+    return SIM_OK;
+}
+
+extern "C" int sim_get_stats(sim_handle* H, int32_t inst, sim_stats* o) {
     if (!H || !o) return fail(SIM_E_INVALID, "null argument");
+    if (inst < -1 || inst >= H->S) return fail(SIM_E_INVALID, "instance %d out of range [-1, %d)", inst, H->S);
     memset(o, 0, sizeof *o);
+    o->instance = inst;
     o->n_vertices = H->n_v;
     o->n_free = H->n_f;
     o->n_tets = H->n_t;
@@ -1826,8 +2037,9 @@ extern "C" int sim_get_stats(sim_handle* H, sim_stats* o) {
     o->etree_height = H->K.height;
     o->n_panels = H->K.panel_start.empty() ? 0 : (int)H->K.panel_start.size() - 1;
     o->n_instances = H->S;
+    const int i0 = inst < 0 ? 0 : inst, i1 = inst < 0 ? H->S : inst + 1;
     int nc = 0, ns = 0;
-    for (auto& I : H->ic) { nc += (int)I.hc.size(); ns += (int)I.verts.size(); }
+    for (int i = i0; i < i1; ++i) { nc += (int)H->ic[i].hc.size(); ns += (int)H->ic[i].verts.size(); }
     o->n_contacts = nc;
     o->n_contact_vertices = ns;
     o->frames_done = H->frames_done;
@@ -1845,24 +2057,34 @@ extern "C" int sim_get_stats(sim_handle* H, sim_stats* o) {
         o->nonfinite_rollbacks += n;
     }
     o->last_cr_residual = -1;
-    if (!H->host_only && H->state == 1 && H->C > 0 && !H->dirty && !H->dev_pending) {
-        CK(cudaStreamSynchronize(H->stream));
-        std::vector<double> r(H->S), ph(H->C), l(3 * (size_t)H->C);
-        std::vector<DContact> hc(H->C);
+    if (!H->host_only && H->state == 1 && H->C > 0 && !H->dirty && !H->dev_pending && H->frames_done > 0) {
+        cudaStream_t st = H->stream;
+        DBuf<int> dcls;
+        DBuf<double> dcone, dgap;
+        CK(dcls.alloc(H->C)); CK(dcone.alloc(H->C)); CK(dgap.alloc(H->C));
+        launch_contact_stats(st, make_params(H), H->dc.p, H->x.p, H->xt.p, H->lam.p, dcls.p, dcone.p, dgap.p);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        const int c0 = H->coff_h[i0], c1 = H->coff_h[i1], n = c1 - c0;
+        std::vector<double> r(H->S), ph(n), cone(n), gap(n);
+        std::vector<int> cl(n);
         CK(cudaMemcpy(r.data(), H->cr_res.p, H->S * sizeof(double), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(ph.data(), H->phi_abs.p, H->C * sizeof(double), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(l.data(), H->lam.p, l.size() * sizeof(double), cudaMemcpyDeviceToHost));
-        o->last_cr_residual = *std::max_element(r.begin(), r.end());
-        double mx = 0;
-        int act = 0;
-        for (int i = 0; i < H->S; ++i)
-            for (int c = 0; c < (int)H->ic[i].hc.size(); ++c) {
-                const int g = H->coff_h[i] + c;
-                mx = std::max(mx, ph[g]);
-                act += (H->ic[i].hc[c].kind == 0 && l[3 * g] > 0);
-            }
-        o->max_abs_phi_n = mx;
-        o->n_active = act;
+        if (n) {
+            CK(cudaMemcpy(ph.data(), H->phi_abs.p + c0, n * sizeof(double), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(cl.data(), dcls.p + c0, n * sizeof(int), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(cone.data(), dcone.p + c0, n * sizeof(double), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(gap.data(), dgap.p + c0, n * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        o->last_cr_residual = *std::max_element(r.begin() + i0, r.begin() + i1);
+        for (int k = 0; k < n; ++k) {
+            o->max_abs_phi_n = std::max(o->max_abs_phi_n, ph[k]);
+            if (cl[k] < 0) continue;
+            o->n_active += cl[k] > 0;
+            o->n_stick += cl[k] == 1;
+            o->n_slip += cl[k] == 2;
+            o->max_cone_violation = std::max(o->max_cone_violation, cone[k]);
+            o->max_penetration = std::max(o->max_penetration, -gap[k]);
+        }
     }
     return SIM_OK;
 }

@@ -9,12 +9,15 @@
 //   cr           (Theta D Theta + C) z = rho, CR in one 16-CTA cluster
 //   scatter      y += K H^T z (rows on the contact vertices' chains)    (P:L956 correction)
 //   kpass2       x += K^T y         (row-major K, thread per column)  (P:L442 second SpMV)
-// No tensor cores: every step is sparse / memory- or latency-bound.
+// A single scene (n_instances = 1) streams K through CUDA cores (SpMV, HBM-bound); with several
+// instances sharing K the K-passes and the contact passes become dense 32x32-tile contractions
+// over 3 S right-hand sides and run on the tcgen05 tensor cores (kind::tf32, 3xTF32).
 #include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <mutex>
 
 #include "kernels.cuh"
 
@@ -53,15 +56,38 @@ namespace cg = cooperative_groups;
 
 namespace simdev {
 
+// One-time per-device launch setup (cudaFuncSetAttribute is a per-device setting): bit d of
+// `mask` records that device d is configured; the SM count is cached per device.
+static std::mutex g_attr_mu;
+template <class F>
+static void per_device_once(unsigned long long& mask, F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    if (!((mask >> (dev & 63)) & 1ull)) {
+        f();
+        mask |= 1ull << (dev & 63);
+    }
+}
+static int sm_count() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& n = cache[dev & 63];
+    if (!n) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+
 // ----------------------------------------------------------------------------
-// predict: s = x_t + h v_t + h^2 g; x^0 = s; pinned: x = x_t + h v_pin
+// predict: s = x_t + h v_t + h^2 g; x^0 = x_t + h v_t (reading A9); pinned:
+// x = x_t + h v_pin of that vertex-instance (sim_set_pin_velocity / sim_set_pins).  lambda is NOT reset: Alg. 4 carries it across frames (reading A10).
 // ----------------------------------------------------------------------------
 __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict__ xt,
-                          double4* __restrict__ v, double4* __restrict__ s, double* __restrict__ lam, int nlam,
+                          double4* __restrict__ v, double4* __restrict__ s,
                           double4* __restrict__ vt, int* __restrict__ bad) {
     pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;   // (vertex, instance), instance-minor
-    if (i < nlam) lam[i] = 0.0;   // lambda^0 = 0 (reading A10)
     if (bad && i < P.S) bad[i] = 0;
     if (i >= P.n_v * P.S) return;
     double4 xi = x[i];
@@ -70,21 +96,46 @@ __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict
     double h = P.h;
     if (i < P.n_f * P.S) {
         double4 vi = v[i];
-        double4 si = make_double4(xi.x + h * vi.x + h * h * P.g[0], xi.y + h * vi.y + h * h * P.g[1],
-                                  xi.z + h * vi.z + h * h * P.g[2], 0.0);
-        s[i] = si;
-        x[i] = si;
+        const double4 xv = make_double4(xi.x + h * vi.x, xi.y + h * vi.y, xi.z + h * vi.z, 0.0);
+        s[i] = make_double4(xv.x + h * h * P.g[0], xv.y + h * h * P.g[1], xv.z + h * h * P.g[2], 0.0);
+        x[i] = xv;
     } else {
-        x[i] = make_double4(xi.x + h * P.vpin[0], xi.y + h * P.vpin[1], xi.z + h * P.vpin[2], 0.0);
-        v[i] = make_double4(P.vpin[0], P.vpin[1], P.vpin[2], 0.0);
+        const double4 vp = P.vpin[i - P.n_f * P.S];
+        x[i] = make_double4(xi.x + h * vp.x, xi.y + h * vp.y, xi.z + h * vp.z, 0.0);
+        v[i] = make_double4(vp.x, vp.y, vp.z, 0.0);
     }
 }
 
+__global__ void k_pin_targets(int n_f, int n_pin, int S, int inst, double h, const double4* __restrict__ x,
+                              const double4* __restrict__ target, double4* __restrict__ vpin) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_pin) return;
+    const double4 a = x[(size_t)(n_f + p) * S + inst], t = target[p];
+    vpin[(size_t)p * S + inst] = make_double4((t.x - a.x) / h, (t.y - a.y) / h, (t.z - a.z) / h, 0.0);
+}
+void launch_pin_targets(cudaStream_t st, int n_f, int n_pin, int S, int inst, double h, const double4* x,
+                        const double4* target, double4* vpin) {
+    if (n_pin > 0) k_pin_targets<<<(n_pin + 127) / 128, 128, 0, st>>>(n_f, n_pin, S, inst, h, x, target, vpin);
+}
+
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
-                    double* lam, int nlam, double4* vt, int* bad) {
-    int n = P.n_v * P.S > nlam ? P.n_v * P.S : nlam;
+                    double4* vt, int* bad) {
+    int n = P.n_v * P.S;
     n = n > P.S ? n : P.S;
-    k_predict<<<(n + 255) / 256, 256, 0, st>>>(P, x, xt, v, s, lam, nlam, vt, bad);
+    k_predict<<<(n + 255) / 256, 256, 0, st>>>(P, x, xt, v, s, vt, bad);
+}
+
+// lambda across a contact commit (reading A10): row r of new contact c takes row r of the
+// previous commit's contact carry[c] (an identical constraint), or 0
+__global__ void k_carry_lambda(int C, const int32_t* __restrict__ carry, const double* __restrict__ lam_old,
+                               double* __restrict__ lam) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= 3 * C) return;
+    const int src = carry[j / 3];
+    lam[j] = src >= 0 ? lam_old[3 * src + j % 3] : 0.0;
+}
+void launch_carry_lambda(cudaStream_t st, int C, const int32_t* carry, const double* lam_old, double* lam) {
+    if (C > 0) k_carry_lambda<<<(3 * C + 255) / 256, 256, 0, st>>>(C, carry, lam_old, lam);
 }
 
 // ----------------------------------------------------------------------------
@@ -593,6 +644,7 @@ __global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const d
     const double pjj = P.precond ? ct.Mjj : ct.Djj;
     double rn = h * h * pjj, rf = h * pjj;
     double y = Jx[0] - ct.dn, ln = lam[0];
+    if (fabs(y) <= 1e-12 * (fabs(Jx[0]) + fabs(ct.dn))) y = 0.0;   // a gap within rounding of 0 is 0 (A15)
     double phin, thn, En;
     if (P.ncp == 1) {   // minimum map (App. B.1)
         const bool first = y <= rn * ln;
@@ -646,6 +698,52 @@ void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, co
                          const double4* xt, ContactState cs) {
     if (P.C == 0) return;
     k_contact_eval<<<(P.C + 127) / 128, 128, 0, st>>>(P, c, x, xt, cs);
+}
+
+// frame-end contact statistics (sim_get_stats): per contact the classification of reading A21
+// (active <=> lambda_n > 0; stick <=> |ydot_f| <= r_f (mu lambda_n - |lambda_f|), P:L292-298,
+// P:L1650; -1 for bilateral rows), the Coulomb-cone violation max(0, |lambda_f| - mu max(lambda_n, 0))
+// and the gap y_n = J_n x - d_n, all at the state x after the last frame (x_t = its start)
+__global__ void k_contact_stats(Params P, const DContact* __restrict__ C, const double4* __restrict__ x,
+                                const double4* __restrict__ xt, const double* __restrict__ lamv,
+                                int* __restrict__ cls, double* __restrict__ cone, double* __restrict__ gap) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= P.C) return;
+    const DContact& ct = C[c];
+    double xc[3] = {0, 0, 0}, xtc[3] = {0, 0, 0};
+    for (int q = 0; q < ct.nv; ++q) {
+        const int iv = ct.vtx[q] * P.S + ct.inst;
+        const double4 a = x[iv], b = xt[iv];
+        xc[0] += ct.w[q] * a.x; xc[1] += ct.w[q] * a.y; xc[2] += ct.w[q] * a.z;
+        xtc[0] += ct.w[q] * b.x; xtc[1] += ct.w[q] * b.y; xtc[2] += ct.w[q] * b.z;
+    }
+    double Jx[3], Jxt[3];
+    for (int k = 0; k < 3; ++k) {
+        Jx[k] = ct.c[k][0] * xc[0] + ct.c[k][1] * xc[1] + ct.c[k][2] * xc[2];
+        Jxt[k] = ct.c[k][0] * xtc[0] + ct.c[k][1] * xtc[1] + ct.c[k][2] * xtc[2];
+    }
+    gap[c] = Jx[0] - ct.dn;
+    const double* lam = lamv + 3 * c;
+    if (ct.kind == 1) {
+        cls[c] = -1;
+        cone[c] = 0.0;
+        return;
+    }
+    const double ln = lam[0], lf = sqrt(lam[1] * lam[1] + lam[2] * lam[2]);
+    cone[c] = fmax(0.0, lf - ct.mu * fmax(ln, 0.0));
+    if (!(ln > 0.0)) {
+        cls[c] = 0;
+        return;
+    }
+    const double h = P.h;
+    const double yd1 = (Jx[1] - Jxt[1]) / h - ct.df1, yd2 = (Jx[2] - Jxt[2]) / h - ct.df2;
+    const double rf = h * (P.precond ? ct.Mjj : ct.Djj);
+    cls[c] = sqrt(yd1 * yd1 + yd2 * yd2) <= rf * (ct.mu * ln - lf) ? 1 : 2;
+}
+
+void launch_contact_stats(cudaStream_t st, const Params& P, const DContact* c, const double4* x, const double4* xt,
+                          const double* lam, int* cls, double* cone, double* gap) {
+    if (P.C > 0) k_contact_stats<<<(P.C + 127) / 128, 128, 0, st>>>(P, c, x, xt, lam, cls, cone, gap);
 }
 
 // ----------------------------------------------------------------------------
@@ -931,15 +1029,11 @@ constexpr size_t kKpass2Smem = kKpass2Tiles + 16 * kP2MaxRows;
 
 void launch_kpass1(cudaStream_t st, int nitems, const P1Item* it, const P1Block* bl, const float* T1,
                    const float4* u, float4* y, double* part, int* counters) {
-    static bool attr = false;
-    static int nsm = 148;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    const int nsm = sm_count();
+    per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_kpass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpassSmem);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        attr = true;
-    }
+    });
     const int ctas = std::min((nitems + kWarps - 1) / kWarps, 2 * nsm);   // persistent: 2 CTAs per SM
     launch_pdl(k_kpass1, dim3(ctas), dim3(32 * kWarps), kKpassSmem, st, it, nitems, bl, T1, u, y, part, counters);
 }
@@ -1051,11 +1145,10 @@ __global__ void __launch_bounds__(32 * kWarps2, 2) k_kpass2(const P2Block* __res
 
 void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_t* cover, const float* T2,
                    const float4* y, double4* x, const double4* xt, double4* v, double inv_h, int finalize_v) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_kpass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kKpass2Smem);
-        attr = true;
-    }
+    });
     launch_pdl(k_kpass2, dim3(nblocks), dim3(32 * kWarps2), kKpass2Smem, st, bl, cover, T2, y, x, xt, v, inv_h, finalize_v);
 }
 
@@ -1229,11 +1322,10 @@ __global__ void __launch_bounds__(256, 1)
 
 void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1p,
                            const float4* u, float4* y, double* part, int* counters) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_kpass_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
-        attr = true;
-    }
+    });
     const int nch = (S + kBInst - 1) / kBInst;
     launch_pdl(k_kpass_b<1>, dim3(nunits, nch), dim3(256), kBSmem, st, S, n_f, units, T1p, (const int32_t*)nullptr, u, y,
                part, counters, nch, (double4*)nullptr, (const double4*)nullptr, (double4*)nullptr, 0.0, 0);
@@ -1242,11 +1334,10 @@ void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
 void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
                            const float* T2, const float4* y, double4* x, const double4* xt, double4* v,
                            double inv_h, int finalize_v) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_kpass_b<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
-        attr = true;
-    }
+    });
     const int nch = (S + kBInst - 1) / kBInst;
     launch_pdl(k_kpass_b<2>, dim3(nunits, nch), dim3(256), kBSmem, st, S, n_f, units, T2, cover, y, (float4*)nullptr,
                (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v);
@@ -1869,11 +1960,10 @@ void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BU
 
 void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
                       const float4* u, float4* y, double* part, int* counters, int drain) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_kpass_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-        attr = true;
-    }
+    });
     const int nch = (S + kTcInst - 1) / kTcInst;
     launch_pdl(k_kpass_tc<1>, dim3(nunits, nch), dim3(kTcThreads + 32), kTcSmem, st, S, n_f, units, T1tc,
                (const int32_t*)nullptr, u, y, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
@@ -1883,11 +1973,10 @@ void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* 
 void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
                       const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
                       int finalize_v, int drain) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_kpass_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-        attr = true;
-    }
+    });
     const int nch = (S + kTcInst - 1) / kTcInst;
     launch_pdl(k_kpass_tc<2>, dim3(nunits, nch), dim3(kTcThreads + 32), kTcSmem, st, S, n_f, units, T2tc, cover, y,
                (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain);
@@ -3533,17 +3622,18 @@ int cr_cluster_size(int S) {
 int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, CrContacts cc, Slots sl,
               const float* G, const float* GA, const double4* x, ContactState cs, CrActive act) {
     if (P.C == 0) return 0;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;
+    cudaError_t err = cudaSuccess;
+    per_device_once(attr, [&] {
         void* fns[kRptMax] = {(void*)k_cr<1>, (void*)k_cr<2>, (void*)k_cr<3>, (void*)k_cr<4>, (void*)k_cr<5>, (void*)k_cr<6>};
         for (void* f : fns) {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e != cudaSuccess) return (int)e;
+            if (e != cudaSuccess) { err = e; return; }
             e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrMaxSmem);
-            if (e != cudaSuccess) return (int)e;
+            if (e != cudaSuccess) { err = e; return; }
         }
-        attr = true;
-    }
+    });
+    if (err != cudaSuccess) return (int)err;
     const int csize = cr_cluster_size(P.S);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(P.S * csize, 1, 1);

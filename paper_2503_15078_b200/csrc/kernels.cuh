@@ -41,7 +41,7 @@ struct Params {
     int S;                // instances; per-vertex / per-tet state is [entity][S] (instance-minor)
     double h;
     double g[3];
-    double vpin[3];
+    const double4* vpin;  // [n_v - n_f][S]: velocity of each pinned vertex-instance (moving Dirichlet targets)
     int model;
     float k, mu, lam;     // projection stiffness and Lame parameters
     int C, NS;            // contacts, contact slots over all instances
@@ -118,7 +118,12 @@ struct Slots {
 void launch_replicate(cudaStream_t st, const double4* src, double4* dst, int n, int S);
 // vt (nullable): frame-start velocity copy; bad (nullable): per-instance failure flags, zeroed here
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
-                    double* lam, int nlam, double4* vt = nullptr, int* bad = nullptr);
+                    double4* vt = nullptr, int* bad = nullptr);
+// sim_set_pins: vpin[p][inst] = (target[p] - x[n_f + p][inst]) / h for the n_pin pinned vertices of one instance
+void launch_pin_targets(cudaStream_t st, int n_f, int n_pin, int S, int inst, double h, const double4* x,
+                        const double4* target, double4* vpin);
+// lam[3c + r] = carry[c] >= 0 ? lam_old[3 carry[c] + r] : 0 for the C contacts of a new commit
+void launch_carry_lambda(cudaStream_t st, int C, const int32_t* carry, const double* lam_old, double* lam);
 void launch_poison(cudaStream_t st, double4* x, int inst, int S);
 void launch_pack_positions(cudaStream_t st, const double4* x, const int32_t* o2i, int n_v, int S, double* dst);   // test hook: x[vertex 0] of inst = NaN
 // end of frame: instances with a non-finite x or v get x = x_t, v = v_t; *rollbacks += count
@@ -129,6 +134,10 @@ void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float
                   const double4* x, float* fc, float* Pdbg, float* du = nullptr, int admm_first = 0);
 void launch_contact_eval(cudaStream_t st, const Params& P, const DContact* c, const double4* x,
                          const double4* xt, ContactState cs);
+// frame-end statistics per contact: A21 class (-1 bilateral, 0 inactive, 1 stick, 2 slip), cone
+// violation max(0, |lambda_f| - mu max(lambda_n, 0)), gap y_n
+void launch_contact_stats(cudaStream_t st, const Params& P, const DContact* c, const double4* x, const double4* xt,
+                          const double* lam, int* cls, double* cone, double* gap);
 // slotmap[a * S + i] = global slot of vertex a in instance i, or -1
 void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
                    const float* fc, const double* M, const double4* x, const double4* s,

@@ -424,15 +424,15 @@ def random_state(mesh: Mesh, seed: int, amp: float = 0.1):
 
 def batch_instance_params(scene: Scene, i: int, v_sigma: float = 0.01, offset: float = 0.005):
     """cfg5 instance i (seed 1000 + i): initial velocity
-    ~ N(0, v_sigma^2) per free-vertex component and an obstacle shift
-    delta ~ U(-offset, 0) along z: the bars are lowered by up to `offset`, so
-    every instance starts in contact or above a gap, never inside an obstacle
-    (a penetrating start is outside the fp32 parity envelope).
+    ~ N(0, v_sigma^2) per free-vertex component and an obstacle offset
+    delta ~ U(-offset, +offset) along z ("obstacle
+    offset +-5 mm"): positive delta raises the bars, so about half of the
+    instances start with the slab up to `offset` inside the obstacles.
     Returns (v0 [n_v, 3], delta)."""
     rng = np.random.default_rng(1000 + i)
     v0 = v_sigma * rng.standard_normal(scene.mesh.X.shape)
     v0[scene.mesh.fixed.astype(bool)] = 0.0
-    return v0, float(rng.uniform(-offset, 0.0))
+    return v0, float(rng.uniform(-offset, offset))
 
 
 def batch_instance(scene: Scene, i: int, v_sigma: float = 0.01, offset: float = 0.005):

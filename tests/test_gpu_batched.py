@@ -11,7 +11,7 @@ import pytest
 
 import scenes
 from oracle import oracle as O
-from _parity import sensitivity
+import _parity
 
 pytestmark = pytest.mark.gpu
 
@@ -82,18 +82,21 @@ def test_batched_incline_instances(simmod):
     tol = 1e-5 * base.mesh.bbox_diag()
     xs = [base.mesh.X.copy() for _ in range(S)]
     vs = [np.zeros_like(base.mesh.X) for _ in range(S)]
+    ls = [np.zeros(3 * len(c)) for c in contacts]
     for f in range(5):
         for i in range(S):
             s.set_state(xs[i], vs[i], instance=i)
+            s.set_lambda(ls[i], instance=i)
         s.step(1, 5)
         for i in range(S):
             xg, vg = s.get_state(instance=i)
-            xo, vo, info = ors[i].frame(xs[i], vs[i])
+            xo, vo, info = ors[i].frame(xs[i], vs[i], lam0=ls[i])
             assert np.abs(xg - xo).max() < tol, (f, i, np.abs(xg - xo).max())
+            lg = s.get_lambda(instance=i)
             if contacts[i]:
-                lg = s.get_lambda(instance=i)
-                assert np.array_equal(ors[i].classify(xo, xs[i], info["lam"]), ors[i].classify(xg, xs[i], lg))
-            xs[i], vs[i] = xg, vg
+                bad, n = _parity.classification_mismatches(ors[i], xg, xs[i], lg, xo, info["lam"], tol)
+                assert bad == 0 and n > 0, (f, i, bad, n)
+            xs[i], vs[i], ls[i] = xg, vg, lg
 
 
 def test_batched_mixed_slot_classes(simmod):
@@ -130,9 +133,9 @@ def test_batched_mixed_slot_classes(simmod):
 
 
 def test_batched_gingerbread_cfg5(simmod):
-    """cfg5 structure on cfg3: 4 instances with their own initial velocities and
-    obstacle offsets (scenes.batch_instance), contacts set in one batch call;
-    one frame per instance against the oracle."""
+    """cfg5 structure on cfg3: 4 instances with their own initial velocities and obstacle
+    offsets (scenes.batch_instance), contacts set in one batch call; one frame per instance
+    against the oracle (the non-penetrating instances 0 and 3 of the seeded draw)."""
     sc = scenes.make_scene("cfg3")
     S = 4
     s = make(simmod, sc, S)
@@ -152,9 +155,9 @@ def test_batched_gingerbread_cfg5(simmod):
         xg, vg = s.get_state(instance=i)
         err = np.abs(xg - xo).max()
         assert err < tol, (i, err, tol)
-        cg = o.classify(xg, sc.mesh.X, s.get_lambda(instance=i))
-        co = o.classify(xo, sc.mesh.X, info["lam"])
-        assert (co == cg).mean() > 0.99
+        bad, n = _parity.classification_mismatches(o, xg, sc.mesh.X, s.get_lambda(instance=i), xo, info["lam"],
+                                                  tol)
+        assert bad == 0, (i, bad, n)
     # all instances advance: positions differ between instances (different inputs)
     P = s.get_positions()
     assert P.shape == (S, sc.mesh.n_v, 3)
@@ -290,52 +293,54 @@ def test_async_position_readback(simmod):
 
 def test_cfg5_full_size_sampled(simmod):
     """cfg5 in the bench's launch configuration: 1024 cfg3 instances on one handle (tensor-core
-    K-passes in 8 chunks of 128, one CR CTA per instance), own initial velocities and obstacle
-    offsets, contacts committed in one batch; one frame; sampled instances against the oracle.
+    K-passes in 8 chunks of 128, one CR CTA per instance), initial velocities N(0, 0.01^2) m/s
+    and obstacle offsets U(-5, +5) mm (about half of the instances start up
+    to 5 mm inside the bars), contacts committed in one batch.
 
-    First and last instance: within 1e-5 bbox.  The two instances whose bars sit closest to the
-    slab (in contact from the first frame): identical contact classification (reading A21) and
-    positions within max(1e-5 bbox, 20 x the oracle's own sensitivity), where the sensitivity is
-    how far the oracle's frame moves when only its inputs x0, v0 are rounded to fp32.  Some of
-    these frames are ill-conditioned (5 L-G / 10 CR iterations, not converged): rounding the
-    inputs alone moves the oracle by 0.3 of the tolerance on instance 221, against 2e-4 on
-    instance 0, and the fp32 path's own roundings (local projection to a 1e-6 gradient
-    tolerance) land at 5-13x that, as they do on well-conditioned frames (tests/_parity.py,
-    DESIGN.md §3 parity envelope)."""
+    Sampled instances: the first and last, the 3 deepest initial penetrations and the 3 smallest
+    non-negative gaps.  Every one: its first L-G iteration (a frame of 1 iteration) within
+    1e-5 bbox of the oracle with identical classification outside the tolerance band.  The
+    non-penetrating ones: the whole 5-iteration frame, the same bounds.  The 5-iteration frame of
+    a penetrating start is not compared here: the method's frame map there switches friction rows
+    on the sign of lambda_n of separating contacts (theta_f = [lambda_n > 0]), and
+    the fp64 oracle itself, continued from an iterate 1e-9 m off its own, ends tens of tolerances
+    away (tools/diag_iteration.py); tools/cfg5_parity_scan.py reports those frames."""
     sc = scenes.make_scene("cfg3")
     S = 1024
     s = make(simmod, sc, S)
     s.set_pin_velocity(sc.pin_velocity)
     base = simmod.contacts_to_array(sc.contacts)
     arrs, v0s = [], np.empty((S, sc.mesh.n_v, 3))
+    deltas = np.empty(S)
     for i in range(S):
-        v0s[i], delta = scenes.batch_instance_params(sc, i)
+        v0s[i], deltas[i] = scenes.batch_instance_params(sc, i)
         a = base.copy()
-        a["offset"] += a["normal"][:, 2] * delta
+        a["offset"] += a["normal"][:, 2] * deltas[i]
         arrs.append(a)
     s.set_contacts_batch(packed=(np.concatenate(arrs), np.full(S, len(base), np.int32)))
-    s.set_states(np.broadcast_to(sc.mesh.X, (S,) + sc.mesh.X.shape), v0s)
-    s.step(1, 5)
-    P = s.get_positions()
-    assert np.isfinite(P).all()
+    X0 = np.broadcast_to(sc.mesh.X, (S,) + sc.mesh.X.shape)
+    runs = {}
+    for iters in (1, 5):
+        s.set_states(X0, v0s)                  # also restarts every instance from lambda = 0
+        s.step(1, iters)
+        runs[iters] = (s.get_positions(), {i: s.get_lambda(i) for i in range(S)})
+        assert np.isfinite(runs[iters][0]).all()
     tol = 1e-5 * sc.mesh.bbox_diag()
-    deltas = np.array([scenes.batch_instance_params(sc, i)[1] for i in range(S)])
-    closest = [int(c) for c in np.argsort(-deltas)[:2]]   # delta <= 0: the smallest gaps
-    for i in [0, 1023] + closest:
+    order = np.argsort(-deltas)
+    gaps = [int(c) for c in np.argsort(np.where(deltas <= 0, -deltas, np.inf))[:3]]
+    sample = [0, 1023] + [int(c) for c in order[:3]] + gaps
+    for i in sample:
         _, cs = scenes.batch_instance(sc, i)
-        o = O.Oracle(sc.mesh, sc.material, sc.h)
-        o.set_contacts(cs)
-        pins = sc.mesh.X[o.pinned] + sc.h * sc.pin_velocity
-        xo, _, info = o.frame(sc.mesh.X.copy(), v0s[i], pin_targets=pins)
-        err = np.abs(P[i] - xo).max()
-        if i not in closest:
-            assert err < tol, (i, err, tol)
-            continue
-        sens = sensitivity(o, sc.mesh.X, v0s[i], xo, pin_targets=pins)
-        assert err < max(tol, 20.0 * sens), (i, err, tol, sens)
-        cls_o = o.classify(xo, sc.mesh.X, info["lam"])
-        cls_g = o.classify(P[i], sc.mesh.X, s.get_lambda(i))
-        assert np.array_equal(cls_o, cls_g), (i, np.flatnonzero(cls_o != cls_g))
+        for iters in ((1, 5) if deltas[i] <= 0 else (1,)):
+            o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=iters)
+            o.set_contacts(cs)
+            pins = sc.mesh.X[o.pinned] + sc.h * sc.pin_velocity
+            xo, _, info = o.frame(sc.mesh.X.copy(), v0s[i], pin_targets=pins)
+            P, L = runs[iters]
+            err = np.abs(P[i] - xo).max()
+            assert err <= tol, (i, iters, deltas[i], err / tol)
+            bad, n = _parity.classification_mismatches(o, P[i], sc.mesh.X, L[i], xo, info["lam"], tol)
+            assert bad == 0, (i, iters, bad, n)
 
 
 @pytest.mark.parametrize("model", [1, 2])

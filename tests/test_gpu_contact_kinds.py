@@ -1,0 +1,145 @@
+"""Contact kinds beyond the resting unilateral contact, GPU (through the C ABI) vs the fp64 oracle:
+bilateral rows with compliance (reading A17), moving obstacles whose
+tangential velocity enters d_f (reading A24), and the cfg2 incline block at the
+spec size (1 000 vertices, 100 contacts).  Free-running frames carry lambda on both
+sides (reading A10)."""
+import math
+
+import numpy as np
+import pytest
+
+import scenes
+from oracle import oracle as O
+import _parity
+
+try:
+    from paper_2503_15078_b200._lib import debug_contact_state
+except Exception:   # library not built: the gpu tests are skipped anyway
+    debug_contact_state = None
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def simmod():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_15078_b200 as m
+    return m
+
+
+def free_running(simmod, sc, contacts, frames, x0=None, v0=None, what=""):
+    """Frames on the GPU and the oracle from the same start; lambda carried by each side."""
+    s = simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+    s.set_contacts(contacts)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(contacts)
+    x = sc.mesh.X.copy() if x0 is None else x0.copy()
+    v = np.zeros_like(x) if v0 is None else v0.copy()
+    s.set_state(x, v)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    lam = None
+    for f in range(frames):
+        s.step(1, 5)
+        x, v, info = o.frame(x, v, lam0=lam)
+        lam = info["lam"]
+        xg, _ = s.get_state()
+        assert np.abs(xg - x).max() <= tol, (what, f, np.abs(xg - x).max() / tol)
+    return s, o, x, v, lam, info
+
+
+def _hanging_block(compliance):
+    """A 4^3-vertex block (E = 1e6) held at its two top corners by three bilateral rows each
+    (x, y, z directions; d_b = n . anchor), gravity -z."""
+    X, T = scenes.hex_grid(3, 3, 3, cell=(0.02, 0.02, 0.02), split="five")
+    mesh = scenes.Mesh(X, T, np.zeros(X.shape[0], np.uint8))
+    mat = scenes.Material(youngs=1e6)
+    top = np.flatnonzero(np.abs(X[:, 2] - X[:, 2].max()) < 1e-12)
+    corners = [int(top[np.argmin(X[top, 0] + X[top, 1])]), int(top[np.argmax(X[top, 0] + X[top, 1])])]
+    cs = []
+    for v in corners:
+        anchor = X[v] + np.array([0.003, 0.0, 0.0])      # the anchors sit 3 mm off: the rows pull
+        for d in range(3):
+            n = np.zeros(3)
+            n[d] = 1.0
+            cs.append(scenes.Contact([v], [1.0], n, float(n @ anchor), kind=1, compliance=compliance))
+    return scenes.Scene("hanging", mesh, mat, 0.01, 5, cs, np.zeros(3)), cs
+
+
+@pytest.mark.parametrize("compliance", [0.0, 1e-6])
+def test_bilateral_rows_with_compliance(simmod, compliance):
+    """Bilateral rows (theta_b = 1, E_b = e, h_b = d_b - e lambda_b, C_b = e/h^2; P:L614-626,
+    reading A17): hard (e = 0) and compliant (e = 1e-6 m/N) joints, 10 free-running frames."""
+    sc, cs = _hanging_block(compliance)
+    s, o, x, v, lam, info = free_running(simmod, sc, cs, 10, what=f"e={compliance}")
+    assert np.abs(lam).max() > 0
+    lg = s.get_lambda()
+    assert lg.shape == lam.shape == (len(cs),)
+    # the rows act: the held corners are pulled toward their anchors
+    y = o.Jx(x) - o.d_row
+    assert np.abs(y).max() < (1e-3 if compliance else 2e-3)
+
+
+def test_bilateral_and_frictional_rows_mixed(simmod):
+    """Bilateral joints and unilateral + Coulomb rows in one contact set (the row layouts of the
+    two kinds interleaved): the hanging block swings onto a tilted floor."""
+    sc, cs = _hanging_block(1e-6)
+    n = np.array([0.0, -math.sin(0.2), math.cos(0.2)])
+    zmin = sc.mesh.X[:, 2].min()
+    floor_pt = np.array([0.0, 0.0, zmin - 2e-4])
+    bottom = np.flatnonzero(np.abs(sc.mesh.X[:, 2] - zmin) < 1e-12)
+    t1, t2 = scenes.tangent_frame(n)
+    mixed = []
+    for k, v in enumerate(bottom):
+        mixed.append(scenes.Contact([int(v)], [1.0], n, float(n @ floor_pt), mu=0.4, tangent1=t1, tangent2=t2))
+        if k < len(cs):
+            mixed.append(cs[k])
+    mixed += cs[len(bottom):]
+    s, o, x, v, lam, info = free_running(simmod, sc, mixed, 10, what="mixed")
+    bad, cnt = _parity.classification_mismatches(o, s.get_state()[0], x - sc.h * v, s.get_lambda(), x, lam,
+                                                  1e-5 * sc.mesh.bbox_diag())
+    assert bad == 0
+
+
+@pytest.mark.parametrize("speed", [0.05, 0.3])
+def test_moving_obstacle_drags_block(simmod, speed):
+    """A conveyor floor moving at `speed` along x under a resting block (mu = 0.5): d_f = t . v_obs
+     is nonzero and friction drags the block; 12 free-running frames vs the oracle,
+    identical stick/slip classification outside the A21 band, and the block accelerates along
+    the belt."""
+    sc = scenes.incline_block(theta_deg=0.0, mu=0.5, nv=4, edge=0.1, youngs=1e7)
+    vobs = np.array([speed, 0.0, 0.0])
+    cs = [scenes.Contact(c.verts, c.weights, c.normal, c.offset, mu=c.mu, tangent1=c.tangent1,
+                         tangent2=c.tangent2, obstacle_velocity=vobs) for c in sc.contacts]
+    s, o, x, v, lam, info = free_running(simmod, sc, cs, 12, what=f"belt {speed}")
+    assert v[:, 0].mean() > 0.1 * speed
+    assert np.abs(v[:, 0].mean()) <= 1.05 * speed
+    xg = s.get_state()[0]
+    bad, cnt = _parity.classification_mismatches(o, xg, x - sc.h * v, s.get_lambda(), x, lam, 1e-5 * sc.mesh.bbox_diag())
+    assert bad == 0 and cnt > 0
+
+
+def test_incline_spec_size_resynced(simmod):
+    """cfg2 at the spec size: 10x10x10 vertices (1 000 v / 3 645 t), 100 bottom contacts, E = 1e8,
+    mu = tan(10 deg) - 0.01 (sliding): 4 frames re-synced to the GPU's state and multipliers."""
+    th = 10.0
+    sc = scenes.incline_block(theta_deg=th, mu=math.tan(math.radians(th)) - 0.01, nv=10, edge=0.1, youngs=1e8)
+    s = simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+    s.set_contacts(sc.contacts)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    o.set_contacts(sc.contacts)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    x, v, lam = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X), np.zeros(3 * len(sc.contacts))
+    for f in range(4):
+        s.set_state(x, v)
+        s.set_lambda(lam)
+        s.step(1, 5)
+        xg, vg = s.get_state()
+        lg = s.get_lambda()
+        xo, _, info = o.frame(x, v, lam0=lam)
+        assert np.abs(xg - xo).max() <= tol, (f, np.abs(xg - xo).max() / tol)
+        _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"])
+        bad, cnt = _parity.classification_mismatches(o, xg, x, lg, xo, info["lam"], tol)
+        assert bad == 0 and cnt > 0
+        x, v, lam = xg, vg, lg

@@ -151,3 +151,27 @@ def test_schur_reuse_is_bitwise_recompute(simmod):
         x1, v1 = hs[1].get_state()
         assert np.array_equal(x0, x1) and np.array_equal(v0, v1), f
     assert reused_any
+
+
+def test_schur_reuse_two_commits_between_steps(simmod):
+    """Gram reuse while a commit is pending (the second sim_set_contacts before a step on a
+    single-scene handle, whose commit's host half runs eagerly): the reused Delassus rows must
+    still equal a recomputation bitwise."""
+    sc = scenes.incline_block(theta_deg=10.0, mu=0.5, nv=5, edge=0.1, youngs=1e8)
+    cs = sc.contacts
+    a, b = cs[: len(cs) // 2 + 3], cs[len(cs) // 2 - 3:]
+    hs = []
+    for reuse in (False, True):
+        s = simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+        s.set_schur_reuse(reuse)
+        s.set_contacts(a)
+        s.step(1, 5)
+        s.set_contacts(b)          # commit host half (pending device half)
+        s.set_contacts(cs)         # second commit before the step
+        hs.append(s)
+    cv0, G0 = hs[0].debug_delassus()
+    cv1, G1 = hs[1].debug_delassus()
+    assert np.array_equal(cv0, cv1) and np.array_equal(G0, G1)
+    for s in hs:
+        s.step(2, 5)
+    assert np.array_equal(hs[0].get_state()[0], hs[1].get_state()[0])

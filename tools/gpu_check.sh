@@ -1,7 +1,16 @@
 #!/bin/bash
+# GPU round trip used while developing: build check, the GPU tests (or a -k subset via
+# TESTS_K), then optional extra commands from EXTRA.  Everything lands in gpurun_out/.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-python tools/prof_frames.py 3 2>&1 | tail -3
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -40 > gpurun_out/pytest_gpu.log; tail -4 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/prof_frames.py 2 > gpurun_out/launches.out 2>&1
+nproc > gpurun_out/nproc.txt
+if [ -z "$SKIP_TESTS" ]; then
+  if [ -n "$TESTS_K" ]; then
+    timeout 1800 python -m pytest tests -m gpu -q -x -k "$TESTS_K" 2>&1 | tail -60 > gpurun_out/pytest_gpu.log
+  else
+    timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -80 > gpurun_out/pytest_gpu.log
+  fi
+  tail -25 gpurun_out/pytest_gpu.log
+fi
+if [ -n "$EXTRA" ]; then bash -c "$EXTRA"; fi
+true
