@@ -169,7 +169,7 @@ int sim_build_sparse_inverse(sim_handle *h, double drop_tolerance);
  * use the grid CR, which needs n_instances == 1 (SIM_E_LIMIT otherwise); its
  * Gram G is stored per etree component (G is zero across components). */
 int sim_set_contacts(sim_handle *h, int32_t instance, const sim_contact *contacts, int32_t n);
-/* Multipliers across sim_set_contacts (reading A10): a contact that is the same constraint as
+/* Multipliers across sim_set_contacts (warm start, reading A10w): a contact that is the same constraint as
  * one of the instance's previous set -- same kind, vertices, weights and row directions
  * (n, t1, t2); offset, mu, compliance and obstacle velocity may change -- keeps that
  * contact's lambda rows (the first unused match in the previous order); other contacts start
@@ -199,11 +199,12 @@ int sim_detect_contacts(sim_handle *h, int32_t instance, const sim_obstacle *obs
                         const int32_t *candidates, int32_t n_candidates, double margin, int32_t *n_found);
 
 /* Advance `frames` frames of `iterations` local-global iterations each
- * (Alg. 4).  Per frame: s = x_t + h v_t + h^2 g; the iterate starts at
- * x^0 = x_t + h v_t (reading A9) and the multipliers at the previous frame's lambda
- * (Alg. 4 never resets lambda, reading A10; see sim_set_contacts for the carry across a new
- * contact set).  Pinned vertices move by h * pin_velocity per frame.  Enqueued on the
- * handle's stream; returns after enqueueing (use sim_synchronize or any blocking accessor). */
+ * (Alg. 4).  Per frame: s = x_t + h v_t + h^2 g; the iterate starts at x^0 = s with
+ * lambda^0 = 0 (readings A9, A10), or -- sim_set_warm_start(h, 1) -- at x^0 = x_t + h v_t with the
+ * previous frame's lambda (A9w, A10w: Alg. 4 never resets lambda; see sim_set_contacts for the
+ * carry across a new contact set).  Pinned vertices move by h * their pin velocity per frame.
+ * Enqueued on the handle's stream; returns after enqueueing (use sim_synchronize or any
+ * blocking accessor). */
 int sim_step(sim_handle *h, int32_t frames, int32_t iterations);
 
 /* Block until all work enqueued on the handle's stream is done; checks the
@@ -301,6 +302,13 @@ int sim_set_ncp(sim_handle *h, int32_t ncp_function, int32_t preconditioner);
  * is the Moreau-envelope one).  Needs a built handle (SIM_E_STATE otherwise);
  * SIM_E_OOM if the dual cannot be allocated.  Takes effect at the next step. */
 int sim_set_admm(sim_handle *h, int32_t on);
+
+/* Frame start: 0 (default) x^0 = s and lambda^0 = 0 every frame (readings A9,
+ * A10); 1 x^0 = x_t + h v_t and lambda^0 = the previous frame's lambda (A9w, A10w) -- the reading
+ * that reproduces the 0.001 stick/slide resolution of Fig. 11, at the price of a
+ * frame map that amplifies rounding near stick.  SIM_E_INVALID on other values.  Takes effect at
+ * the next step. */
+int sim_set_warm_start(sim_handle *h, int32_t on);
 
 /* Batched K-passes (n_instances > 1): 2 = tcgen05 tensor cores with the right-hand sides
  * staged in TMEM (tcgen05.st) and read by the MMA from TMEM (default); 0 = tcgen05 with both

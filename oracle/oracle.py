@@ -25,7 +25,11 @@ the paper's own definitions):
                    or min-map (App. B.1, P:L1594-1655),
                    Schur RHS with the Alg. 3/4 sign (A11),
                    CR (Saad Alg. 6.20) with exactly N_CR iterations (A19),
-                   lambda update + corrected global solve (P:L955-956).
+                   lambda update (no projection, A20) + corrected global solve.
+* frame            default (A9, A10): x^0 = s, lambda^0 = 0 every frame;
+                   warm_start=True (A9w, A10w): x^0 = x_t + h v_t and lambda^0 = the previous
+                   frame's lambda (Alg. 4 never resets it), carried across contact sets by
+                   carry_multipliers -- the reading that reproduces Fig. 11's 0.001.
 
 Parity pinning status (see tests/test_oracle_*.py): every function below is
 pinned by a closed form, an invariant, a library special case or brute force,
@@ -448,8 +452,9 @@ class Oracle:
 
     def __init__(self, mesh, material, h: float, lg_iters: int = 5,
                  cr_iters: Optional[int] = None, ncp: int = NCP_FB, precond: int = PRECOND_DELASSUS,
-                 admm: bool = False):
+                 admm: bool = False, warm_start: bool = False):
         self.X = np.asarray(mesh.X, dtype=np.float64)
+        self.len_scale = max(float(np.linalg.norm(self.X.max(0) - self.X.min(0))), float(np.abs(self.X).max()))
         self.T = np.asarray(mesh.T, dtype=np.int64)
         self.fixed = np.asarray(mesh.fixed).astype(bool)
         self.n_v = self.X.shape[0]
@@ -465,6 +470,8 @@ class Oracle:
         # ADMM-PD (Overby et al. 2017; "our implementations are mainly based on PD and ADMM-PD",
         # P:L1340): per-tet dual u, reset to 0 each frame (reading A33)
         self.admm = bool(admm)
+        # frame start (readings A9/A10 vs A9w/A10w)
+        self.warm_start = bool(warm_start)
         self.Bm, self.vol, self.w, self.M = rest_data(self.X, self.T, material.density, self.k)
         self.A = assemble_Av(self.n_v, self.T, self.Bm, self.w, self.M, self.h)
         self.free = np.nonzero(~self.fixed)[0]
@@ -577,8 +584,9 @@ class Oracle:
             # reading A15: a gap within rounding of zero is zero.  At (y, lambda) = (0, 0) the
             # normal NCP's derivative theta_n = 1 - y/|y| jumps between 0 and 2 with the sign
             # of y, so the evaluation's own rounding must not pick the branch: the 0/0 rule
-            # (theta_n = 1, E_n = 0) applies to every |y| <= 1e-12 (|J_n x| + |d_n|)
-            if abs(yn) <= 1e-12 * (abs(Jx[j0]) + abs(self.d_row[j0])):
+            # (theta_n = 1, E_n = 0) applies to every |y| <= 1e-12 L, L = max(rest bbox diagonal,
+            # max |rest coordinate|) (the rounding of J_n x - d_n is ~1e-16 L)
+            if abs(yn) <= 1e-12 * self.len_scale:
                 yn = 0.0
             nfun, ffun = (minmap_normal, minmap_friction) if self.ncp == NCP_MINMAP else (fb_normal, fb_friction)
             ph, th, En = nfun(yn, lam[j0], self.r_row[j0])
@@ -598,12 +606,11 @@ class Oracle:
         """Alg. 4 body for one time step.  Returns (x, v, info); info["lam"] holds the
         multipliers at frame end.
 
-        lam0: the multipliers the frame starts from.  Alg. 4 never resets lambda
-        inside `while simulation`, so lambda^0 of a frame is the previous frame's final lambda
-        (reading A10); pass info["lam"] of the previous frame (carried across a contact change
-        by carry_multipliers), or None for a first frame (0).
-        Initial iterate (reading A9): x^0 = x_t + h v_t, the inertial extrapolation without the
-        external-force term (s itself still enters b = M s + ...).
+        Default (readings A9, A10): x^0 = s, lambda^0 = 0; lam0 must be None.
+        warm_start (A9w, A10w): x^0 = x_t + h v_t (the inertial extrapolation without the
+        external-force term; s still enters b = M s + ...) and lambda^0 = lam0, the
+        previous frame's final lambda (Alg. 4, never resets lambda inside
+        `while simulation`; carried across a contact change by carry_multipliers), None = 0.
         start: (x_k, lambda_k, k) continues the frame from iterate k (the conditioning checks of
         tests/_parity.py); x_k must carry the pinned targets."""
         h = self.h
@@ -611,7 +618,9 @@ class Oracle:
         v_t = np.asarray(v_t, dtype=np.float64)
         # s = x_t + h v_t + h^2 M^-1 f_ext, f_ext = M g (A8)
         s = x_t + h * v_t + h * h * self.g[None, :]
-        x = x_t + h * v_t                              # x^0 (A9)
+        if lam0 is not None and not self.warm_start:
+            raise ValueError("lam0 needs warm_start=True (reading A10: lambda^0 = 0)")
+        x = x_t + h * v_t if self.warm_start else s.copy()   # x^0 (A9w / A9)
         if self.pinned.size:
             tgt = x_t[self.pinned] if pin_targets is None else np.asarray(pin_targets, float)
             x[self.pinned] = tgt
@@ -662,7 +671,7 @@ class Oracle:
                 Cdiag = np.where(kind == 1, E / h, E / (h * h))   # C
                 S_apply = lambda v: theta * (self.D @ (theta * v)) + Cdiag * v
                 z, res = cr_solve(S_apply, rho, self.cr_iters)
-                lam = lam + z / (h * h)                # Delta lambda = z / h^2 (A11)
+                lam = lam + z / (h * h)                # Delta lambda = z / h^2 (A11), no projection (A20)
                 # x^{k+1} = A^-1 (b + h^2 H^T lambda^{k+1})
                 xn = x.copy()
                 xn[F_] = self.solve(b_f + h * h * self.JT(theta * lam)[F_])

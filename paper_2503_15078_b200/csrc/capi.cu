@@ -189,6 +189,7 @@ struct sim_handle {
     std::vector<uint8_t> fixed;
     sim_material mat{};
     double h = 0, mu_l = 0, lam_l = 0, kproj = 0;
+    double len_scale = 0;   // max(rest bbox diagonal, max |rest coordinate|) (gap snapping, reading A15)
     simhost::RestData rd;
     std::vector<int32_t> int2orig, orig2int;
     simhost::Inverse K;
@@ -321,6 +322,7 @@ struct sim_handle {
     int cr_mode = 0;                 // 0 auto, 1 cluster CR only, 2 grid CR always
     int ncp = 0, precond = 0;        // NCP function / complementarity preconditioner (sim_set_ncp)
     int admm = 0;                    // ADMM-PD local-global (sim_set_admm)
+    int warm = 0;                    // frame start (sim_set_warm_start): readings A9/A10 or A9w/A10w
     DBuf<float> du;                  // ADMM dual, [9][n_t S]
     bool grid = false;               // the committed contact set uses the grid CR
     int NG = 0, ng_max = 0;
@@ -375,6 +377,19 @@ static int create_common(const sim_mesh* m, const sim_material* mat, double h, s
     H->mat = *mat;
     if (H->mat.cr_iterations <= 0) H->mat.cr_iterations = 10;
     H->h = h;
+    {
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300}, amax = 0.0;
+        for (int i = 0; i < H->n_v; ++i)
+            for (int d = 0; d < 3; ++d) {
+                const double c = H->X[3 * (size_t)i + d];
+                lo[d] = std::min(lo[d], c);
+                hi[d] = std::max(hi[d], c);
+                amax = std::max(amax, std::fabs(c));
+            }
+        const double dg = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                                    (hi[2] - lo[2]) * (hi[2] - lo[2]));
+        H->len_scale = std::max(dg, amax);
+    }
     H->mu_l = mat->youngs / (2.0 * (1.0 + mat->poisson));
     H->lam_l = mat->youngs * mat->poisson / ((1.0 + mat->poisson) * (1.0 - 2.0 * mat->poisson));
     H->kproj = mat->proj_stiffness > 0 ? mat->proj_stiffness : 2.0 * H->mu_l;
@@ -1035,6 +1050,8 @@ static Params make_params(const sim_handle* H) {
     P.cm_max = H->cm_max;
     P.cr_iters = H->mat.cr_iterations;
     P.ncp = H->ncp;
+    P.len_scale = H->len_scale;
+    P.warm = H->warm;
     P.precond = H->precond;
     return P;
 }
@@ -1578,7 +1595,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
 #define MARK(k) do { int r_ = mark(k); if (r_) return -r_; } while (0)
 #define CKR(call) do { cudaError_t r_ = (call); if (r_ != cudaSuccess) return -(int)r_; } while (0)
     MARK(KK_PREDICT);
-    launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->vt.p, H->bad.p); nk++;
+    launch_predict(st, P, H->x.p, H->xt.p, H->v.p, H->s.p, H->lam.p, 3 * H->C, H->vt.p, H->bad.p); nk++;
     if (H->poison_inst >= 0) launch_poison(st, H->x.p, H->poison_inst, H->S);   // test hook (not captured)
     const bool con = H->C > 0;
     for (int k = 0; k < iters; ++k) {
@@ -1669,6 +1686,13 @@ extern "C" int sim_debug_poison(sim_handle* H, int32_t inst) {
     return SIM_OK;
 }
 
+extern "C" int sim_set_warm_start(sim_handle* H, int32_t on) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (on != 0 && on != 1) return fail(SIM_E_INVALID, "flag must be 0 or 1");
+    H->warm = on;
+    return SIM_OK;
+}
+
 extern "C" int sim_set_schur_reuse(sim_handle* H, int32_t on) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (on != 0 && on != 1) return fail(SIM_E_INVALID, "flag must be 0 or 1");
@@ -1740,7 +1764,7 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     }
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
                                       H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG,
-                                      H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain, H->cr_mode,
+                                      H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain, H->cr_mode, H->warm,
                                       H->tc_contact};
     if (!H->gexec || key != H->gkey) {
         if (H->gexec) {

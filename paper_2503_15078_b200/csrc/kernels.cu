@@ -80,14 +80,16 @@ static int sm_count() {
 
 
 // ----------------------------------------------------------------------------
-// predict: s = x_t + h v_t + h^2 g; x^0 = x_t + h v_t (reading A9); pinned:
-// x = x_t + h v_pin of that vertex-instance (sim_set_pin_velocity / sim_set_pins).  lambda is NOT reset: Alg. 4 carries it across frames (reading A10).
+// predict: s = x_t + h v_t + h^2 g; pinned: x = x_t + h v_pin of that vertex-instance
+// (sim_set_pin_velocity / sim_set_pins).  Frame start: default x^0 = s, lambda^0 = 0 (readings A9,
+// A10); warm start x^0 = x_t + h v_t and lambda kept from the previous frame (A9w, A10w).
 // ----------------------------------------------------------------------------
 __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict__ xt,
-                          double4* __restrict__ v, double4* __restrict__ s,
+                          double4* __restrict__ v, double4* __restrict__ s, double* __restrict__ lam, int nlam,
                           double4* __restrict__ vt, int* __restrict__ bad) {
     pdl_enter();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;   // (vertex, instance), instance-minor
+    if (!P.warm && i < nlam) lam[i] = 0.0;
     if (bad && i < P.S) bad[i] = 0;
     if (i >= P.n_v * P.S) return;
     double4 xi = x[i];
@@ -97,8 +99,9 @@ __global__ void k_predict(Params P, double4* __restrict__ x, double4* __restrict
     if (i < P.n_f * P.S) {
         double4 vi = v[i];
         const double4 xv = make_double4(xi.x + h * vi.x, xi.y + h * vi.y, xi.z + h * vi.z, 0.0);
-        s[i] = make_double4(xv.x + h * h * P.g[0], xv.y + h * h * P.g[1], xv.z + h * h * P.g[2], 0.0);
-        x[i] = xv;
+        const double4 si = make_double4(xv.x + h * h * P.g[0], xv.y + h * h * P.g[1], xv.z + h * h * P.g[2], 0.0);
+        s[i] = si;
+        x[i] = P.warm ? xv : si;
     } else {
         const double4 vp = P.vpin[i - P.n_f * P.S];
         x[i] = make_double4(xi.x + h * vp.x, xi.y + h * vp.y, xi.z + h * vp.z, 0.0);
@@ -119,10 +122,10 @@ void launch_pin_targets(cudaStream_t st, int n_f, int n_pin, int S, int inst, do
 }
 
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
-                    double4* vt, int* bad) {
-    int n = P.n_v * P.S;
+                    double* lam, int nlam, double4* vt, int* bad) {
+    int n = P.n_v * P.S > nlam ? P.n_v * P.S : nlam;
     n = n > P.S ? n : P.S;
-    k_predict<<<(n + 255) / 256, 256, 0, st>>>(P, x, xt, v, s, vt, bad);
+    k_predict<<<(n + 255) / 256, 256, 0, st>>>(P, x, xt, v, s, lam, nlam, vt, bad);
 }
 
 // lambda across a contact commit (reading A10): row r of new contact c takes row r of the
@@ -644,7 +647,7 @@ __global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const d
     const double pjj = P.precond ? ct.Mjj : ct.Djj;
     double rn = h * h * pjj, rf = h * pjj;
     double y = Jx[0] - ct.dn, ln = lam[0];
-    if (fabs(y) <= 1e-12 * (fabs(Jx[0]) + fabs(ct.dn))) y = 0.0;   // a gap within rounding of 0 is 0 (A15)
+    if (fabs(y) <= 1e-12 * P.len_scale) y = 0.0;   // a gap within rounding of 0 is 0 (reading A15)
     double phin, thn, En;
     if (P.ncp == 1) {   // minimum map (App. B.1)
         const bool first = y <= rn * ln;

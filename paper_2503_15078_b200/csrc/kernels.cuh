@@ -49,6 +49,8 @@ struct Params {
     int NCL, CS;          // slot-set classes, class slots
     int cm_max;           // largest class (members)
     int cr_iters;
+    int warm;             // frame start: 0 x^0 = s, lambda^0 = 0 (A9, A10); 1 x^0 = x_t + h v_t, lambda kept (A9w, A10w)
+    double len_scale;     // max(rest bbox diagonal, max |rest coordinate|): gaps within 1e-12 of it are 0 (A15)
     int ncp;              // 0 Fischer-Burmeister (App. B.2, the paper's choice), 1 minimum map (App. B.1)
     int precond;          // 0 Delassus diagonal, 1 mass inverse
 };
@@ -118,7 +120,7 @@ struct Slots {
 void launch_replicate(cudaStream_t st, const double4* src, double4* dst, int n, int S);
 // vt (nullable): frame-start velocity copy; bad (nullable): per-instance failure flags, zeroed here
 void launch_predict(cudaStream_t st, const Params& P, double4* x, double4* xt, double4* v, double4* s,
-                    double4* vt = nullptr, int* bad = nullptr);
+                    double* lam, int nlam, double4* vt = nullptr, int* bad = nullptr);
 // sim_set_pins: vpin[p][inst] = (target[p] - x[n_f + p][inst]) / h for the n_pin pinned vertices of one instance
 void launch_pin_targets(cudaStream_t st, int n_f, int n_pin, int S, int inst, double h, const double4* x,
                         const double4* target, double4* vpin);

@@ -91,48 +91,6 @@ def assert_impulse_parity(o, lam_g, theta_g, lam_o, theta_o, rel=1e-4):
     return err / max(scale, 1e-300)
 
 
-def self_spread(o, x, v, xo, eps=1e-13, seed=0, **frame_kw):
-    """How far the fp64 oracle's own frame moves when its initial velocity is perturbed by a
-    relative eps (default 1e-13, a few hundred fp64 ulps): max |x_oracle(v (1 + eps N)) - xo|.
-    A frame whose result moves by a sizeable fraction of the tolerance under this perturbation
-    is not determined to the tolerance by its inputs at all (the switching of the non-smooth
-    iterate -- theta_f = [lambda_n > 0], the E_f branches -- makes the 5-iteration frame map
-    discontinuous there): no implementation, not even a second fp64 one that sums in another
-    order, can be held to 1e-5 bbox on it (well-posedness)."""
-    rng = np.random.default_rng(seed)
-    vp = np.asarray(v, float) * (1.0 + eps * rng.standard_normal(np.shape(v)))
-    xp, _, _ = o.frame(x, vp, **frame_kw)
-    return float(np.abs(xp - xo).max())
-
-
-def fp32_conditioning(o, x_t, v_t, xo, info, eps=1e-7, **frame_kw):
-    """How far the oracle's own frame end moves when its FIRST iterate x^1 is perturbed at the
-    scale of fp32 rounding (eps = 1e-7 relative of the first step x^1 - x^0), the remaining
-    iterations then run exactly (fp64): max over two perturbations -- the step scaled by
-    (1 + eps) (a coherent error, as a systematic rounding bias makes) and eps |x^1 - x^0| times
-    seeded N(0, 1) noise per entry.  Needs o.frame(..., capture=True) output `info` for xo.
-
-    A frame whose result moves by a sizeable fraction of the tolerance under this perturbation
-    is ill-conditioned for fp32 arithmetic: any implementation whose first iterate carries
-    fp32-level rounding (6e-8 per operation) lands that far from the fp64 result, however the
-    rest is computed (conditioning).  The penetrating cfg5 starts amplify such a
-    perturbation 10^4 - 10^5 times (tools/diag_iteration.py: the oracle continued from the GPU's
-    first iterate, 0.001 tolerances off, ends 73 tolerances off its own frame)."""
-    rec = info["iters"][0]
-    x1, l1 = rec["x_next"], rec["lam"]
-    x0 = np.asarray(x_t, float) + o.h * np.asarray(v_t, float)
-    if o.pinned.size:
-        x0[o.pinned] = x1[o.pinned]
-    d = x1 - x0
-    rng = np.random.default_rng(7)
-    out = 0.0
-    for xp in (x0 + d * (1.0 + eps), x1 + eps * np.abs(d) * rng.standard_normal(d.shape)):
-        xp[o.pinned] = x1[o.pinned]
-        xe, _, _ = o.frame(x_t, v_t, lam0=None, start=(xp, l1, 1), **frame_kw)
-        out = max(out, float(np.abs(xe - xo).max()))
-    return out
-
-
 def assert_frame_parity(o, x, v, xg, xo, tol, what="", **frame_kw):
     """Plain north-star position bound: max |x_gpu - x_oracle| <= tol (1e-5 x bbox diagonal)."""
     err = float(np.abs(xg - xo).max())

@@ -82,21 +82,19 @@ def test_batched_incline_instances(simmod):
     tol = 1e-5 * base.mesh.bbox_diag()
     xs = [base.mesh.X.copy() for _ in range(S)]
     vs = [np.zeros_like(base.mesh.X) for _ in range(S)]
-    ls = [np.zeros(3 * len(c)) for c in contacts]
     for f in range(5):
         for i in range(S):
             s.set_state(xs[i], vs[i], instance=i)
-            s.set_lambda(ls[i], instance=i)
         s.step(1, 5)
         for i in range(S):
             xg, vg = s.get_state(instance=i)
-            xo, vo, info = ors[i].frame(xs[i], vs[i], lam0=ls[i])
+            xo, vo, info = ors[i].frame(xs[i], vs[i])
             assert np.abs(xg - xo).max() < tol, (f, i, np.abs(xg - xo).max())
-            lg = s.get_lambda(instance=i)
             if contacts[i]:
-                bad, n = _parity.classification_mismatches(ors[i], xg, xs[i], lg, xo, info["lam"], tol)
+                bad, n = _parity.classification_mismatches(ors[i], xg, xs[i], s.get_lambda(instance=i), xo,
+                                                           info["lam"], tol)
                 assert bad == 0 and n > 0, (f, i, bad, n)
-            xs[i], vs[i], ls[i] = xg, vg, lg
+            xs[i], vs[i] = xg, vg
 
 
 def test_batched_mixed_slot_classes(simmod):

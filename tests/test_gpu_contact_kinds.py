@@ -30,7 +30,7 @@ def simmod():
 
 
 def free_running(simmod, sc, contacts, frames, x0=None, v0=None, what=""):
-    """Frames on the GPU and the oracle from the same start; lambda carried by each side."""
+    """Frames on the GPU and the oracle from the same start (readings A9/A10)."""
     s = simmod.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
     s.set_contacts(contacts)
     o = O.Oracle(sc.mesh, sc.material, sc.h)
@@ -39,10 +39,9 @@ def free_running(simmod, sc, contacts, frames, x0=None, v0=None, what=""):
     v = np.zeros_like(x) if v0 is None else v0.copy()
     s.set_state(x, v)
     tol = 1e-5 * sc.mesh.bbox_diag()
-    lam = None
     for f in range(frames):
         s.step(1, 5)
-        x, v, info = o.frame(x, v, lam0=lam)
+        x, v, info = o.frame(x, v)
         lam = info["lam"]
         xg, _ = s.get_state()
         assert np.abs(xg - x).max() <= tol, (what, f, np.abs(xg - x).max() / tol)
@@ -130,16 +129,15 @@ def test_incline_spec_size_resynced(simmod):
     o = O.Oracle(sc.mesh, sc.material, sc.h)
     o.set_contacts(sc.contacts)
     tol = 1e-5 * sc.mesh.bbox_diag()
-    x, v, lam = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X), np.zeros(3 * len(sc.contacts))
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
     for f in range(4):
         s.set_state(x, v)
-        s.set_lambda(lam)
         s.step(1, 5)
         xg, vg = s.get_state()
         lg = s.get_lambda()
-        xo, _, info = o.frame(x, v, lam0=lam)
+        xo, _, info = o.frame(x, v)
         assert np.abs(xg - xo).max() <= tol, (f, np.abs(xg - xo).max() / tol)
         _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"])
         bad, cnt = _parity.classification_mismatches(o, xg, x, lg, xo, info["lam"], tol)
         assert bad == 0 and cnt > 0
-        x, v, lam = xg, vg, lg
+        x, v = xg, vg

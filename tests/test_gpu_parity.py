@@ -133,9 +133,9 @@ def test_delassus_gram_parity(simmod):
 @pytest.mark.parametrize("dmu", [+0.05, -0.05])
 def test_incline_contact_frames_resynced(simmod, dmu):
     """cfg2-like incline (E = 1e8, 10 deg): each frame the oracle restarts from the GPU's
-    state (x, v and the multipliers lambda the frame starts from, reading A10); positions
-    within 1e-5 bbox, the per-vertex applied impulse J^T Theta lambda close, and identical
-    stick/slip classification outside the A21 band."""
+    state (readings A9/A10: x^0 = s, lambda^0 = 0); positions within 1e-5 bbox, the
+    per-vertex applied impulse J^T Theta lambda close, and identical stick/slip classification
+    outside the tolerance band."""
     th = 10.0
     mus = math.tan(math.radians(th))
     sc = scenes.incline_block(theta_deg=th, mu=mus + dmu, nv=5, edge=0.1, youngs=1e8)
@@ -144,32 +144,32 @@ def test_incline_contact_frames_resynced(simmod, dmu):
     o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=5)
     o.set_contacts(sc.contacts)
     tol = 1e-5 * sc.mesh.bbox_diag()
-    x, v, lam = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X), np.zeros(3 * len(sc.contacts))
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
     for f in range(8):
         s.set_state(x, v)
-        s.set_lambda(lam)
         s.step(1, 5)
         xg, vg = s.get_state()
         lg = s.get_lambda()
-        xo, vo, info = o.frame(x, v, lam0=lam)
+        xo, vo, info = o.frame(x, v)
         assert np.abs(xg - xo).max() < tol, (f, np.abs(xg - xo).max())
         # D of a stiff block on a plane is nearly rank-deficient (rigid modes dominate), so
         # per-row lambda is ill-determined (reading A31); the per-vertex impulse is not
         _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"])
         bad, n = _parity.classification_mismatches(o, xg, x, lg, xo, info["lam"], tol)
         assert bad == 0 and n > 0, (f, bad, n)
-        x, v, lam = xg, vg, lg
+        x, v = xg, vg
 
 
-def test_incline_free_running_warm_start(simmod):
-    """The same incline free-running for 12 frames: the GPU carries lambda from frame to frame
-    by itself (reading A10: Alg. 4 never resets it) and the oracle is handed its own previous
-    lambda; positions stay within 1e-5 bbox of each other."""
+def test_incline_warm_start_sliding(simmod):
+    """Warm-start reading (sim_set_warm_start; A9w: x^0 = x_t + h v_t, A10w: lambda carried
+    across frames by the GPU itself, the oracle handed its own previous lambda): the sliding
+    incline block (mu* - 0.05), 12 free-running frames within 1e-5 bbox."""
     th = 10.0
-    sc = scenes.incline_block(theta_deg=th, mu=math.tan(math.radians(th)) + 0.01, nv=5, edge=0.1, youngs=1e8)
+    sc = scenes.incline_block(theta_deg=th, mu=math.tan(math.radians(th)) - 0.05, nv=5, edge=0.1, youngs=1e8)
     s = make(simmod, sc)
+    s.set_warm_start(True)
     s.set_contacts(sc.contacts)
-    o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=5)
+    o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=5, warm_start=True)
     o.set_contacts(sc.contacts)
     tol = 1e-5 * sc.mesh.bbox_diag()
     x, v, lam = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X), None
@@ -180,7 +180,29 @@ def test_incline_free_running_warm_start(simmod):
         lam = info["lam"]
         xg, _ = s.get_state()
         assert np.abs(xg - x).max() < tol, (f, np.abs(xg - x).max())
-    assert np.abs(s.get_lambda() - lam).max() < 1e-3 * np.abs(lam).max()
+        _parity.assert_impulse_parity(o, s.get_lambda(), debug_contact_state(s)["theta"], lam, info["theta_last"])
+
+
+def test_warm_start_resynced_with_lambda(simmod):
+    """Warm start, re-synced: each frame both sides start from the GPU's (x, v, lambda)
+    (sim_set_lambda = the oracle's lam0); sliding incline, positions within 1e-5 bbox."""
+    th = 10.0
+    sc = scenes.incline_block(theta_deg=th, mu=math.tan(math.radians(th)) - 0.05, nv=5, edge=0.1, youngs=1e8)
+    s = make(simmod, sc)
+    s.set_warm_start(True)
+    s.set_contacts(sc.contacts)
+    o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=5, warm_start=True)
+    o.set_contacts(sc.contacts)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    x, v, lam = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X), np.zeros(3 * len(sc.contacts))
+    for f in range(6):
+        s.set_state(x, v)
+        s.set_lambda(lam)
+        s.step(1, 5)
+        xg, vg = s.get_state()
+        xo, _, info = o.frame(x, v, lam0=lam)
+        assert np.abs(xg - xo).max() < tol, (f, np.abs(xg - xo).max())
+        x, v, lam = xg, vg, s.get_lambda()
 
 
 def test_lambda_carry_across_commits(simmod):
@@ -213,7 +235,7 @@ def test_lambda_carry_across_commits(simmod):
 
 def test_gingerbread_frame_parity(simmod):
     """cfg3 at the benchmark size: 19 691 v / 93 600 t / 800 contacts, 5 L-G, 10 CR; two
-    frames, the second re-synced to the GPU's state and multipliers."""
+    frames, the second re-synced to the GPU's state."""
     sc = scenes.make_scene("cfg3")
     s = make(simmod, sc)
     s.set_pin_velocity(sc.pin_velocity)
@@ -221,21 +243,20 @@ def test_gingerbread_frame_parity(simmod):
     o = O.Oracle(sc.mesh, sc.material, sc.h)
     o.set_contacts(sc.contacts)
     tol = 1e-5 * sc.mesh.bbox_diag()
-    x, v, lam = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X), np.zeros(3 * len(sc.contacts))
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
     for f in range(2):
         s.set_state(x, v)
-        s.set_lambda(lam)
         s.step(1, 5)
         xg, vg = s.get_state()
         pins = x[o.pinned] + sc.h * sc.pin_velocity
-        xo, vo, info = o.frame(x, v, pin_targets=pins, lam0=lam)
+        xo, vo, info = o.frame(x, v, pin_targets=pins)
         err = np.abs(xg - xo).max()
         assert err < tol, (f, err, tol)
         lg = s.get_lambda()
         _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"])
         bad, n = _parity.classification_mismatches(o, xg, x, lg, xo, info["lam"], tol)
         assert bad == 0 and n > 0, (f, bad, n)
-        x, v, lam = xg, vg, lg
+        x, v = xg, vg
 
 
 def test_determinism(simmod):

@@ -6,9 +6,9 @@ mkdir -p gpurun_out
 nproc > gpurun_out/nproc.txt
 if [ -z "$SKIP_TESTS" ]; then
   if [ -n "$TESTS_K" ]; then
-    timeout 1800 python -m pytest tests -m gpu -q -x -k "$TESTS_K" 2>&1 | tail -60 > gpurun_out/pytest_gpu.log
+    timeout 1800 python -m pytest tests -m gpu -q --tb=line -p no:cacheprovider -k "$TESTS_K" 2>&1 > gpurun_out/pytest_gpu.log
   else
-    timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -80 > gpurun_out/pytest_gpu.log
+    timeout 1800 python -m pytest tests -m gpu -q --tb=line -p no:cacheprovider 2>&1 > gpurun_out/pytest_gpu.log
   fi
   tail -25 gpurun_out/pytest_gpu.log
 fi
