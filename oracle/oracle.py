@@ -258,32 +258,32 @@ def fb_friction(ydot, lam_f, lam_n, mu, r):
     """theta_f, E_f for one contact's two friction rows.
 
     lam_n > 0 and mu lam_n > 0: theta_f = 1,
-      E_f = r (R - r q) / (s + mu r lam_n - R), s = |ydot|, q = mu lam_n - |lam_f|,
-      R = sqrt(s^2 + r^2 q^2); the denominator is floored at
-      1e-6 (s + mu r lam_n) (reading A16).  Two places need the floor: the 0/0 point
-      (s = 0, |lam_f| = 0), where the limit is 0 (numerator 0 over a positive floor), and
-      the pole of the printed formula: the denominator is positive for |lam_f| < 2 mu lam_n
-      (s = 0) and E_f -> +inf as |lam_f| -> 2 mu lam_n from below; beyond it (possible since
-      lambda is not projected, A20) the printed expression turns negative, i.e. an
-      anti-dissipative friction compliance.  The floor continues E_f from the admissible
-      side: it stays large and positive (r (R - r q) / floor), so the row drives lam_f back
-      toward 0 instead of accelerating the slide (reading A16c).
+      E_f = r (R - r q) / (s + mu r lam_n - R), s = |ydot|, R = sqrt(s^2 + r^2 q^2),
+      q = mu lam_n - min(|lam_f|, mu lam_n)   (reading A16c).
+      The second argument of Coulomb's complementarity 0 <= |ydot_f| _|_ mu lam_n - |lam_f| >= 0
+      (eq. coulomb's law 2) is evaluated at the projection of lam_f onto the cone: with
+      the printed q = mu lam_n - |lam_f| the denominator equals phi_FB(s, q) + r |lam_f|, which
+      vanishes at |lam_f| = 2 mu lam_n (s = 0) and is negative beyond it -- a pole and an
+      anti-dissipative compliance at iterates outside the cone, reachable because lambda is not
+      projected (A20).  Inside the cone (|lam_f| <= mu lam_n) the formula is the printed one; on
+      and outside it q = 0, R = s and E_f = |ydot_f| / (mu lam_n), Coulomb's ratio
+      |ydot_f| / |lam_f| on the cone boundary.  E_f is then continuous, >= 0 and bounded
+      by r s / (r min(|lam_f|, mu lam_n)).  The only remaining 0/0 point is (s, |lam_f|) = (0, 0),
+      where the limit is 0 (reading A16): E_f = 0 when the denominator is <= 1e-12 (s + mu r lam_n).
     otherwise (inactive, or degenerate cone mu lam_n = 0, reading A16b):
       theta_f = 0, E_f = 1 (identity), so lam_f -> 0.
     """
     ydot = np.asarray(ydot, dtype=np.float64)
     lam_f = np.asarray(lam_f, dtype=np.float64)
     s = np.linalg.norm(ydot, axis=-1)
-    q = mu * lam_n - np.linalg.norm(lam_f, axis=-1)
+    q = mu * lam_n - np.minimum(np.linalg.norm(lam_f, axis=-1), mu * lam_n)   # A16c
     R = np.sqrt(s * s + r * r * q * q)
     act = (lam_n > 0) & (mu * lam_n > 0)
     num = r * (R - r * q)
     den = s + mu * r * lam_n - R
-    floor = 1e-6 * (s + mu * r * lam_n)
-    den = np.maximum(den, floor)
+    ok = den > 1e-12 * (s + mu * r * lam_n)                                       # A16
     with np.errstate(divide="ignore", invalid="ignore"):
-        E = np.where(act, num / np.where(den > 0, den, 1.0), 1.0)
-    E = np.where(act & ~(den > 0), 0.0, E)
+        E = np.where(act, np.where(ok, num / np.where(ok, den, 1.0), 0.0), 1.0)
     theta = np.where(act, 1.0, 0.0)
     return theta, E
 

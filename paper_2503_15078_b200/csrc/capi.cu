@@ -198,6 +198,7 @@ struct sim_handle {
     std::vector<simhost::BUnit> bu1, bu2;   // batched K-pass units (S > 1)
     std::vector<float> T1ph;
     int bparts = 0, bblocks1 = 0;
+    simhost::PlaneUnits pu;                 // plane-layout tensor-core K-pass units (S > 1)
     int64_t nnzL = 0;
     double build_seconds = 0;
     DBuf<double4> vpin;              // [n_v - n_f][S] pinned-vertex velocities (moving Dirichlet targets)
@@ -228,9 +229,13 @@ struct sim_handle {
     DBuf<int32_t> adjp, adj;
     // device: K
     DBuf<float> Krow, Kcol, T1, T2, T1p;   // K row/column-major + the passes' tile streams
-    DBuf<float> T1tc, T2tc;                // tensor-core copies of T1p / T2 (S > 1)
-    int kpass_mode = 2;                    // S > 1: 2 tcgen05 with TMEM operands, 0 tcgen05 SMEM operands, 1 FP32
-    int tc_drain = 4;                      // tensor-core K-pass: tiles per fp32 TMEM accumulation (2.4e-6 rel. on cfg3)
+    DBuf<float> Tpl1, Tpl2;                // plane-layout tensor-core tile streams (S > 1)
+    DBuf<simhost::BUnit> pu1d, pu2d;
+    DBuf<int32_t> pcover;
+    DBuf<float> ppart;                     // fp32 partials of split pass-1 blocks
+    DBuf<int> pcounters;
+    int kpass_mode = 2;                    // S > 1: 2 (or 0) tcgen05 plane kernels, 1 CUDA-core FP32
+    int tc_drain = 4;                      // tensor-core K-pass: tiles per fp32 TMEM accumulation
     DBuf<int64_t> colptr;
     DBuf<int32_t> depth, parent, ptop, cover;
     DBuf<int2> meta;                 // {rowptr[i] - first[i], first[i]}
@@ -536,9 +541,11 @@ static int upload_all(sim_handle* H) {
     CK(H->Bm.alloc((size_t)9 * nt)); CK(H->Bm.upload(Bm.data(), (size_t)9 * nt, st));
     CK(H->hw2.alloc(nt)); CK(H->hw2.upload(hw.data(), nt, st));
     CK(H->fc.alloc((size_t)12 * nt * S));
-    CK(H->u.alloc((size_t)nf * S)); CK(H->y.alloc((size_t)nf * S));
-    CK(cudaMemsetAsync(H->u.p, 0, (size_t)nf * S * sizeof(float4), st));
-    CK(cudaMemsetAsync(H->y.p, 0, (size_t)nf * S * sizeof(float4), st));
+    // u, y: float4 [n_f] at S = 1, three fp32 planes [3][n_f][Sp] at S > 1 (vec_ld in kernels.cu)
+    const size_t nvec4 = S == 1 ? (size_t)nf : ((size_t)3 * nf * plane_sp(S) + 3) / 4;
+    CK(H->u.alloc(nvec4)); CK(H->y.alloc(nvec4));
+    CK(cudaMemsetAsync(H->u.p, 0, nvec4 * sizeof(float4), st));
+    CK(cudaMemsetAsync(H->y.p, 0, nvec4 * sizeof(float4), st));
     // vertex -> (tet, corner) adjacency for free vertices, ascending tet order
     std::vector<int32_t> adjp(nf + 1, 0), adj;
     for (int t = 0; t < nt; ++t) {
@@ -582,12 +589,16 @@ static int upload_all(sim_handle* H) {
     } else {
         CK(H->T1p.alloc(H->T1ph.size())); CK(H->T1p.upload(H->T1ph.data(), H->T1ph.size(), st));
         {
-            std::vector<float> tc;
-            simhost::tc_tiles(H->T1ph, tc);
-            CK(H->T1tc.alloc(tc.size())); CK(H->T1tc.upload(tc.data(), tc.size(), st));
-            CK(cudaStreamSynchronize(st));
-            simhost::tc_tiles(H->T2h, tc);
-            CK(H->T2tc.alloc(tc.size())); CK(H->T2tc.upload(tc.data(), tc.size(), st));
+            const simhost::PlaneUnits& PU = H->pu;
+            CK(H->Tpl1.alloc(PU.T1.size())); CK(H->Tpl1.upload(PU.T1.data(), PU.T1.size(), st));
+            CK(H->Tpl2.alloc(PU.T2.size())); CK(H->Tpl2.upload(PU.T2.data(), PU.T2.size(), st));
+            CK(H->pu1d.alloc(PU.u1.size())); CK(H->pu1d.upload(PU.u1.data(), PU.u1.size(), st));
+            CK(H->pu2d.alloc(PU.u2.size())); CK(H->pu2d.upload(PU.u2.data(), PU.u2.size(), st));
+            CK(H->pcover.alloc(PU.cover.size())); CK(H->pcover.upload(PU.cover.data(), PU.cover.size(), st));
+            CK(H->ppart.alloc((size_t)std::max(1, PU.nparts1) * 3 * 64 * plane_sp(S)));
+            const size_t npc = (size_t)std::max(1, PU.nblocks1) * ((S + 127) / 128);
+            CK(H->pcounters.alloc(npc));
+            CK(cudaMemsetAsync(H->pcounters.p, 0, npc * sizeof(int), st));
             CK(cudaStreamSynchronize(st));
         }
         CK(H->bu1d.alloc(H->bu1.size())); CK(H->bu1d.upload(H->bu1.data(), H->bu1.size(), st));
@@ -694,7 +705,10 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
         return fail(SIM_E_LIMIT, "nnz(K) = %lld exceeds the int32 offset limit", (long long)H->K.nnz);
     simhost::build_worklists(H->K, H->wl, 1024);
     simhost::build_tiles(H->K, H->wl, H->T1h, H->T2h);
-    if (H->S > 1) H->bparts = simhost::build_batched(H->K, H->wl, 64, H->bu1, H->T1ph, H->bu2, H->bblocks1);
+    if (H->S > 1) {
+        H->bparts = simhost::build_batched(H->K, H->wl, 64, H->bu1, H->T1ph, H->bu2, H->bblocks1);
+        simhost::build_plane_units(H->K, 48, H->pu);
+    }
     lap(4);
     H->n_f = nf;
     H->int2orig.assign(nv, -1);
@@ -1393,7 +1407,7 @@ static int commit_host(sim_handle* H) {
     H->NG = NG;
     H->ng_max = ngmax;
     // chain dot and scatter on the tensor cores: S > 1 instances all in one slot-set class
-    H->tc_contact = S > 1 && NCL == 1 && Ct > 0 && H->kpass_mode == 2;
+    H->tc_contact = S > 1 && NCL == 1 && Ct > 0 && H->kpass_mode != 1;
     if (H->tc_contact && H->ic[rep[0]].verts != H->tc_verts) {   // tiles depend on K and the vertex set only
         simhost::ContactPasses cp;
         simhost::build_contact_passes(H->K, H->ic[rep[0]].verts, cp);
@@ -1542,29 +1556,23 @@ static void enqueue_kpass1(sim_handle* H, cudaStream_t st) {
     if (H->S == 1)
         launch_kpass1(st, (int)H->wl.p1.size(), H->p1.p, H->p1b.p, H->T1.p, H->u.p, H->y.p, H->part1.p,
                       H->counters.p);
-    else if (H->kpass_mode == 2)
-        launch_kpass1_ts(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1tc.p, H->u.p, H->y.p, H->part1.p,
-                         H->counters.p, H->tc_drain);
-    else if (H->kpass_mode == 0)
-        launch_kpass1_tc(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1tc.p, H->u.p, H->y.p, H->part1.p,
-                         H->counters.p, H->tc_drain);
+    else if (H->kpass_mode != 1)
+        launch_kpass1_pl(st, H->S, plane_sp(H->S), H->n_f, (int)H->pu.u1.size(), H->pu1d.p, H->Tpl1.p,
+                         (const float*)H->u.p, (float*)H->y.p, H->ppart.p, H->pcounters.p, H->tc_drain);
     else
-        launch_kpass1_batched(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1p.p, H->u.p, H->y.p,
-                              H->part1.p, H->counters.p);
+        launch_kpass1_batched(st, H->S, H->n_f, (int)H->bu1.size(), H->bu1d.p, H->T1p.p, (const float*)H->u.p,
+                              (float*)H->y.p, H->part1.p, H->counters.p);
 }
 static void enqueue_kpass2(sim_handle* H, cudaStream_t st, double4* x, const double4* xt, double4* v, double inv_h,
                            int fin) {
     if (H->S == 1)
         launch_kpass2(st, (int)H->wl.p2b.size(), H->p2b.p, H->cover.p, H->T2.p, H->y.p, x, xt, v, inv_h, fin);
-    else if (H->kpass_mode == 2)
-        launch_kpass2_ts(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2tc.p, H->y.p, x, xt, v,
-                         inv_h, fin, H->tc_drain);
-    else if (H->kpass_mode == 0)
-        launch_kpass2_tc(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2tc.p, H->y.p, x, xt, v,
-                         inv_h, fin, H->tc_drain);
+    else if (H->kpass_mode != 1)
+        launch_kpass2_pl(st, H->S, plane_sp(H->S), H->n_f, (int)H->pu.u2.size(), H->pu2d.p, H->pcover.p, H->Tpl2.p,
+                         (const float*)H->y.p, x, xt, v, inv_h, fin, H->tc_drain);
     else
-        launch_kpass2_batched(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2.p, H->y.p, x, xt,
-                              v, inv_h, fin);
+        launch_kpass2_batched(st, H->S, H->n_f, (int)H->bu2.size(), H->bu2d.p, H->cover.p, H->T2.p,
+                              (const float*)H->y.p, x, xt, v, inv_h, fin);
 }
 
 // enqueue one frame (predict + iters x L-G); returns kernel count or negative
@@ -1624,7 +1632,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
         if (con) {
             MARK(KK_CHAIN);
             if (H->tc_contact)
-                launch_chain_pass_ts(st, H->S, H->tc_nuc, H->tcu_c.p, H->tc_Tc.p, H->tc_cover.p, H->y.p, H->soff.p,
+                launch_chain_pass_ts(st, H->S, H->n_f, H->tc_nuc, H->tcu_c.p, H->tc_Tc.p, H->tc_cover.p, H->y.p, H->soff.p,
                                      ccr, H->x.p, cs, 1, H->tc_cpart.p, H->tc_ccnt.p);   // fold every tile: the Schur RHS is sensitive
             else
                 launch_chain_dot(st, P, off, class_slots(H), H->Kcol.p, H->colptr.p, H->chain_off.p,
@@ -1641,7 +1649,7 @@ static int enqueue_frame(sim_handle* H, int iters) {
             }
             MARK(KK_SCATTER);
             if (H->tc_contact)
-                launch_scatter_pass_ts(st, H->S, H->tc_ns, H->tc_nus, H->tcu_s.p, H->tc_Ts.p, H->tc_rows.p, H->wzT.p,
+                launch_scatter_pass_ts(st, H->S, H->n_f, H->tc_ns, H->tc_nus, H->tcu_s.p, H->tc_Ts.p, H->tc_rows.p, H->wzT.p,
                                        H->y.p, 1, H->tc_spart.p, H->tc_scnt.p);
             else
                 launch_scatter(st, P, H->urows_max, off, H->ucount.p, H->ulist.p, H->Zc.p, H->wz.p, H->wzT.p, H->y.p,
@@ -1704,12 +1712,12 @@ extern "C" int sim_set_kpass_mode(sim_handle* H, int32_t mode) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     // mode 0 | 1; mode >= 16: tensor cores with (mode >> 4) tiles per fp32 TMEM accumulation (tuning)
     if (mode >= 16) {
-        H->kpass_mode = (mode & 15) == 2 ? 2 : 0;
+        H->kpass_mode = 2;
         H->tc_drain = std::max(2, mode >> 4);
         return SIM_OK;
     }
     if (mode < 0 || mode > 2)
-        return fail(SIM_E_INVALID, "K-pass mode must be 0 (tensor cores), 1 (FP32) or 2 (tensor cores, TMEM operands)");
+        return fail(SIM_E_INVALID, "K-pass mode must be 0 or 2 (tensor cores) or 1 (CUDA-core FP32)");
     H->kpass_mode = mode;
     return SIM_OK;
 }
@@ -2132,11 +2140,17 @@ extern "C" int sim_debug_apply_inverse(sim_handle* H, const double* b, double* x
     if (!H || !b || !xo) return fail(SIM_E_INVALID, "null argument");
     if (H->state != 1 || H->host_only) return fail(SIM_E_STATE, "no device state");
     const int nf = H->n_f, nv = H->n_v, S = H->S;
-    std::vector<float4> hu((size_t)nf * S);
+    const int Sp = plane_sp(S);
+    std::vector<float4> hu(S == 1 ? (size_t)nf : ((size_t)3 * nf * Sp + 3) / 4, make_float4(0.f, 0.f, 0.f, 0.f));
+    float* hp = reinterpret_cast<float*>(hu.data());   // S > 1: planes [3][nf][Sp]
     for (int i = 0; i < S; ++i)
         for (int k = 0; k < nf; ++k) {
             const double* bb = b + ((size_t)i * nv + H->int2orig[k]) * 3;
-            hu[(size_t)k * S + i] = make_float4((float)bb[0], (float)bb[1], (float)bb[2], 0.f);
+            if (S == 1) {
+                hu[k] = make_float4((float)bb[0], (float)bb[1], (float)bb[2], 0.f);
+            } else {
+                for (int c = 0; c < 3; ++c) hp[(size_t)c * nf * Sp + (size_t)k * Sp + i] = (float)bb[c];
+            }
         }
     DBuf<double4> dx;
     CK(dx.alloc((size_t)nf * S));

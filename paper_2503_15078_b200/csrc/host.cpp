@@ -694,4 +694,132 @@ void build_contact_passes(const Inverse& K, const std::vector<int32_t>& sv, Cont
     }
 }
 
+// ---- plane-layout tensor-core K-passes: 64-output units (see host.hpp) ----
+static void put_tile64(float* dst, const float* src /*[32 q][64 l]*/) {
+    auto rn = [](float a) {   // round to nearest tf32
+        uint32_t b;
+        std::memcpy(&b, &a, 4);
+        b = (b + 0x1000u) & 0xFFFFE000u;
+        float r;
+        std::memcpy(&r, &b, 4);
+        return r;
+    };
+    float* hi = dst;
+    float* lo = dst + 2048;
+    for (int q = 0; q < 32; ++q)
+        for (int l = 0; l < 64; ++l) {
+            const float v = src[q * 64 + l];
+            const float h = rn(v);
+            const int d = (l / 8) * 256 + (q / 4) * 32 + (l % 8) * 4 + (q % 4);
+            hi[d] = h;
+            lo[d] = rn(v - h);
+        }
+}
+
+void build_plane_units(const Inverse& K, int unit_tiles, PlaneUnits& pu) {
+    pu = PlaneUnits();
+    const int n = K.n;
+    auto kval = [&](int r, int j) -> float {
+        if (j < K.first[r] || j > r) return 0.f;
+        return K.Krow[K.rowptr[r] + (j - K.first[r])];
+    };
+    // pass 1: 64-row blocks
+    struct B1 { int r0, nr, c0, nt; };
+    std::vector<B1> blocks;
+    int64_t nt1 = 0;
+    for (int r0 = 0; r0 < n; r0 += 64) {
+        const int nr = std::min(64, n - r0);
+        int c0 = r0;
+        for (int l = 0; l < nr; ++l) c0 = std::min(c0, (int)K.first[r0 + l]);
+        const int nt = (r0 + nr - c0 + 31) / 32;
+        blocks.push_back({r0, nr, c0, nt});
+        nt1 += nt;
+    }
+    pu.tiles1 = nt1;
+    pu.T1.assign((size_t)nt1 * 4096, 0.f);
+    std::vector<int64_t> boff(blocks.size());
+    {
+        int64_t o = 0;
+        for (size_t b = 0; b < blocks.size(); ++b) { boff[b] = o; o += (int64_t)blocks[b].nt * 4096; }
+    }
+#pragma omp parallel for schedule(dynamic, 4)
+    for (long long b = 0; b < (long long)blocks.size(); ++b) {
+        const B1& B = blocks[b];
+        std::vector<float> tile(32 * 64);
+        for (int t = 0; t < B.nt; ++t) {
+            std::fill(tile.begin(), tile.end(), 0.f);
+            for (int q = 0; q < 32; ++q) {
+                const int j = B.c0 + 32 * t + q;
+                if (j >= B.r0 + B.nr) break;
+                for (int l = 0; l < B.nr; ++l) tile[q * 64 + l] = kval(B.r0 + l, j);
+            }
+            put_tile64(pu.T1.data() + boff[b] + (int64_t)t * 4096, tile.data());
+        }
+    }
+    pu.nblocks1 = (int)blocks.size();
+    for (int b = 0; b < (int)blocks.size(); ++b) {
+        const B1& B = blocks[b];
+        const int nu = (B.nt + unit_tiles - 1) / unit_tiles;
+        const int part0 = nu > 1 ? pu.nparts1 : -1;
+        for (int u = 0; u < nu; ++u) {
+            BUnit U{};
+            U.r0 = B.r0;
+            U.nr = B.nr;
+            U.c0 = B.c0 + 32 * unit_tiles * u;
+            U.ntiles = std::min(unit_tiles, B.nt - unit_tiles * u);
+            U.list0 = part0;
+            U.block = b;
+            U.part = nu > 1 ? pu.nparts1++ : -1;
+            U.nparts = nu;
+            U.toff = boff[b] + (int64_t)4096 * unit_tiles * u;
+            pu.u1.push_back(U);
+        }
+    }
+    std::stable_sort(pu.u1.begin(), pu.u1.end(), [](const BUnit& a, const BUnit& b) { return a.ntiles > b.ntiles; });
+    // pass 2: 64-column blocks and their cover rows
+    std::vector<int32_t> mark(n, -1), cov;
+    int64_t nt2 = 0;
+    for (int c0 = 0; c0 < n; c0 += 64) {
+        const int nc = std::min(64, n - c0);
+        const int bi = c0 / 64;
+        cov.clear();
+        for (int j = c0; j < c0 + nc; ++j)
+            for (int i = j; i != -1 && mark[i] != bi; i = K.parent[i]) {
+                mark[i] = bi;
+                cov.push_back(i);
+            }
+        std::sort(cov.begin(), cov.end());
+        BUnit U{};
+        U.r0 = c0;
+        U.c0 = c0;
+        U.nr = nc;
+        U.list0 = (int32_t)pu.cover.size();
+        U.nlist = (int32_t)cov.size();
+        U.ntiles = (U.nlist + 31) / 32;
+        U.block = -1;
+        U.part = -1;
+        U.nparts = 1;
+        U.toff = nt2 * 4096;
+        nt2 += U.ntiles;
+        pu.cover.insert(pu.cover.end(), cov.begin(), cov.end());
+        pu.u2.push_back(U);
+    }
+    pu.tiles2 = nt2;
+    pu.T2.assign((size_t)nt2 * 4096, 0.f);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (long long b = 0; b < (long long)pu.u2.size(); ++b) {
+        const BUnit& U = pu.u2[b];
+        std::vector<float> tile(32 * 64);
+        for (int t = 0; t < U.ntiles; ++t) {
+            std::fill(tile.begin(), tile.end(), 0.f);
+            for (int q = 0; q < 32 && 32 * t + q < U.nlist; ++q) {
+                const int r = pu.cover[U.list0 + 32 * t + q];
+                for (int l = 0; l < U.nr; ++l) tile[q * 64 + l] = kval(r, U.c0 + l);
+            }
+            put_tile64(pu.T2.data() + U.toff + (int64_t)t * 4096, tile.data());
+        }
+    }
+    std::stable_sort(pu.u2.begin(), pu.u2.end(), [](const BUnit& a, const BUnit& b) { return a.ntiles > b.ntiles; });
+}
+
 }  // namespace simhost

@@ -114,6 +114,28 @@ struct BUnit { int32_t r0, nr, c0, ntiles, list0, nlist, block, part, nparts, pa
 int build_batched(const Inverse& K, const WorkLists& wl, int unit_tiles, std::vector<BUnit>& u1,
                   std::vector<float>& T1p, std::vector<BUnit>& u2, int& nblocks1);
 
+// ---------------- plane-layout tensor-core K-passes (S > 1), 64 outputs per unit -------------
+// Right-hand sides in fp32 component planes; one CTA = one unit x 128 instances x 3 components,
+// tcgen05 M = 128 (instances) x N = 64 (outputs) x K = 32 (tile reductions).
+//   pass 1 (y = K u): blocks of <= 64 consecutive rows r0..r0+nr-1, columns [first(r0), r0 + nr)
+//       in tiles of 32 from c0 (the block's first column), split into units of <= unit_tiles
+//       tiles; tile[q][l] = K[r0 + l][c0 + 32 t + q]; a split block writes fp64 partials (part,
+//       list0 = the block's first part, block = counter index)
+//   pass 2 (x += K^T y): blocks of <= 64 consecutive columns c0..c0+nr-1, their sorted cover rows
+//       (rows i >= c0 with first(i) <= c0 + nr - 1) in cover[list0 .. list0 + nlist);
+//       tile[q][l] = K[cover[list0 + 32 t + q]][c0 + l]
+// Tile stream: per tile 4096 floats = the tf32 hi tile (round to nearest) then the lo tile
+// (v - hi, rounded), each in the tcgen05 SWIZZLE_NONE K-major core-matrix layout
+// [l / 8][q / 4][l % 8][q % 4] (64 x 32); toff in floats.
+struct PlaneUnits {
+    std::vector<BUnit> u1, u2;
+    std::vector<int32_t> cover;     // pass-2 cover rows
+    std::vector<float> T1, T2;      // tile streams (hi/lo)
+    int nparts1 = 0, nblocks1 = 0;
+    int64_t tiles1 = 0, tiles2 = 0;
+};
+void build_plane_units(const Inverse& K, int unit_tiles, PlaneUnits& pu);
+
 // ---------------- contact passes of a slot-set class on the tensor cores (S > 1) -------------
 // With Z[s][r] = K[r][a_s] (r on the ancestor chain of the contact vertex a_s):
 //   chain pass   dxt[s] = sum_r Z[s][r] y[r]   -- units like pass 2: 32 slots (c0, nr), their

@@ -79,6 +79,44 @@ static int sm_count() {
 }
 
 
+// Right-hand-side vectors u, y of the K-passes: S = 1: float4 [n_f] (.w carries pass 1's column
+// base); S > 1: three fp32 component planes [c][n_f][Sp], Sp = S rounded up to a multiple of 4 (the
+// planes the batched K-passes stream with 16-byte copies; entries S..Sp-1 of a row are padding).
+__device__ __forceinline__ float4 vec_ld(const float4* v, int S, int n_f, int row, int inst) {
+    if (S == 1) return __ldg(&v[row]);
+    const int Sp = plane_sp(S);
+    const float* p = reinterpret_cast<const float*>(v);
+    const size_t PS = (size_t)n_f * Sp, i = (size_t)row * Sp + inst;
+    return make_float4(__ldg(p + i), __ldg(p + PS + i), __ldg(p + 2 * PS + i), 0.f);
+}
+__device__ __forceinline__ void vec_st(float4* v, int S, int n_f, int row, int inst, float a0, float a1, float a2,
+                                       float w = 0.f) {
+    if (S == 1) {
+        v[row] = make_float4(a0, a1, a2, w);
+        return;
+    }
+    const int Sp = plane_sp(S);
+    float* p = reinterpret_cast<float*>(v);
+    const size_t PS = (size_t)n_f * Sp, i = (size_t)row * Sp + inst;
+    p[i] = a0;
+    p[PS + i] = a1;
+    p[2 * PS + i] = a2;
+}
+// v[row] += (a0, a1, a2), rounded once to fp32
+__device__ __forceinline__ void vec_add(float4* v, int S, int n_f, int row, int inst, double a0, double a1, double a2) {
+    if (S == 1) {
+        const float4 yi = v[row];
+        v[row] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), yi.w);
+        return;
+    }
+    const int Sp = plane_sp(S);
+    float* p = reinterpret_cast<float*>(v);
+    const size_t PS = (size_t)n_f * Sp, i = (size_t)row * Sp + inst;
+    p[i] = (float)(p[i] + a0);
+    p[PS + i] = (float)(p[PS + i] + a1);
+    p[2 * PS + i] = (float)(p[2 * PS + i] + a2);
+}
+
 // ----------------------------------------------------------------------------
 // predict: s = x_t + h v_t + h^2 g; pinned: x = x_t + h v_pin of that vertex-instance
 // (sim_set_pin_velocity / sim_set_pins).  Frame start: default x^0 = s, lambda^0 = 0 (readings A9,
@@ -663,22 +701,23 @@ __global__ void k_contact_eval(Params P, const DContact* __restrict__ C, const d
         phin = 0.0; thn = 1.0; En = 0.0;
     }
     phin_abs = fabs(phin);
-    // friction (A14, A16, A16b)
+    // friction (A14, A16, A16b, A16c)
     double yd1 = (Jx[1] - Jxt[1]) / h - ct.df1, yd2 = (Jx[2] - Jxt[2]) / h - ct.df2;
     double thf, Ef;
     if (ln > 0.0 && ct.mu * ln > 0.0) {
         double s = sqrt(yd1 * yd1 + yd2 * yd2);
         double lf = sqrt(lam[1] * lam[1] + lam[2] * lam[2]);
-        double q = ct.mu * ln - lf;
-        double R = sqrt(s * s + rf * rf * q * q);
         if (P.ncp == 1) {   // minimum map: stick 0, slip (|ydot| - r q) / (mu lam_n)
+            double q = ct.mu * ln - lf;
             Ef = s <= rf * q ? 0.0 : (s - rf * q) / (ct.mu * ln);
         } else {
+            // FB: q at the cone projection of lam_f (A16c: no pole at |lam_f| = 2 mu lam_n);
+            // the 0/0 point (s, |lam_f|) = (0, 0) has limit 0 (A16)
+            double q = ct.mu * ln - fmin(lf, ct.mu * ln);
+            double R = sqrt(s * s + rf * rf * q * q);
             double num = rf * (R - rf * q);
             double den = s + ct.mu * rf * ln - R;
-            double fl = 1e-6 * (s + ct.mu * rf * ln);
-            den = den > fl ? den : fl;
-            Ef = den > 0.0 ? num / den : 0.0;
+            Ef = den > 1e-12 * (s + ct.mu * rf * ln) ? num / den : 0.0;
         }
         thf = 1.0;
     } else {
@@ -794,7 +833,7 @@ __global__ void k_gather(Params P, const int32_t* __restrict__ adjp, const int32
             }
         }
     }
-    u[gi] = make_float4((float)r0, (float)r1, (float)r2, 0.f);
+    vec_st(u, S, P.n_f, a, inst, (float)r0, (float)r1, (float)r2);
 }
 
 void launch_gather(cudaStream_t st, const Params& P, const int32_t* adjp, const int32_t* adj,
@@ -1170,17 +1209,19 @@ void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_
 // ----------------------------------------------------------------------------
 constexpr int kBInst = 128;                 // instances per CTA
 constexpr int kBStages = 2;
-constexpr size_t kBStageBytes = 4096 + 32 * kBInst * 16;
+constexpr size_t kBStageBytes = 4096 + 3 * 32 * kBInst * 4;   // K tile + 3 component planes of 32 rows
 constexpr size_t kBSmem = kBStages * kBStageBytes;
 
 template <int PASS>
 __global__ void __launch_bounds__(256, 1)
     k_kpass_b(int S, int n_f, const BUnit* __restrict__ units, const float* __restrict__ T,
-              const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
+              const int32_t* __restrict__ cover, const float* __restrict__ vin, float* __restrict__ yout,
               double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
               const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v) {
     pdl_enter();
     extern __shared__ __align__(128) unsigned char bsm[];
+    const int Sp = plane_sp(S);
+    const size_t PS = (size_t)n_f * Sp;
     __shared__ __align__(8) uint64_t full[kBStages];
     __shared__ int s_last;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1192,10 +1233,10 @@ __global__ void __launch_bounds__(256, 1)
     const int li = 32 * ig + lane;           // instance within the chunk
     const unsigned long long pol = l2_evict_first();
     auto ktile = [&](int s) { return reinterpret_cast<float*>(bsm + s * kBStageBytes); };
-    auto vtile = [&](int s) { return reinterpret_cast<float4*>(bsm + s * kBStageBytes + 4096); };
+    auto vtile = [&](int s) { return reinterpret_cast<float*>(bsm + s * kBStageBytes + 4096); };   // [3][32][kBInst]
     // zero the vector tiles once: rows / instances that are never copied must read as 0
-    for (int e = threadIdx.x; e < kBStages * 32 * kBInst; e += blockDim.x)
-        vtile(e / (32 * kBInst))[e % (32 * kBInst)] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = threadIdx.x; e < kBStages * 3 * 32 * kBInst; e += blockDim.x)
+        vtile(e / (3 * 32 * kBInst))[e % (3 * 32 * kBInst)] = 0.f;
     if (threadIdx.x == 0)
         for (int s = 0; s < kBStages; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // zero fill before the bulk copies
@@ -1207,12 +1248,15 @@ __global__ void __launch_bounds__(256, 1)
     auto issue = [&](int t) {   // warp 0 only
         const int s = t % kBStages;
         const int nv = nvalid(t);
-        if (lane == 0) mbar_expect_tx(&full[s], 4096u + (unsigned)(nv * ni * 16));
+        const unsigned rb = (unsigned)(((ni + 3) & ~3) * 4);   // one plane row of the chunk (16-byte multiple)
+        if (lane == 0) mbar_expect_tx(&full[s], 4096u + 3u * (unsigned)nv * rb);
         __syncwarp();
         if (lane == 0) bulk_g2s(ktile(s), T + U.toff + (int64_t)t * 1024, 4096u, &full[s], true, pol);
         if (lane < nv) {
             const int idx = PASS == 1 ? U.c0 + 32 * t + lane : __ldg(&cover[U.list0 + 32 * t + lane]);
-            bulk_g2s(vtile(s) + lane * kBInst, vin + (size_t)idx * S + i0, (unsigned)(ni * 16), &full[s], false, pol);
+            for (int c = 0; c < 3; ++c)
+                bulk_g2s(vtile(s) + (c * 32 + lane) * kBInst, vin + c * PS + (size_t)idx * Sp + i0, rb, &full[s], false,
+                         pol);
         }
     };
     if (w == 0)
@@ -1224,13 +1268,13 @@ __global__ void __launch_bounds__(256, 1)
         const int s = t % kBStages;
         mbar_wait(&full[s], (t / kBStages) & 1);
         const float* kt = ktile(s) + 16 * half;
-        const float4* vt = vtile(s) + li;
+        const float* vt = vtile(s) + li;
         float a[16][3];
 #pragma unroll
         for (int r = 0; r < 16; ++r) a[r][0] = a[r][1] = a[r][2] = 0.f;
 #pragma unroll 4
         for (int q = 0; q < 32; ++q) {
-            const float4 vq = vt[q * kBInst];
+            const float4 vq = make_float4(vt[q * kBInst], vt[(32 + q) * kBInst], vt[(64 + q) * kBInst], 0.f);
             const float4* kq = reinterpret_cast<const float4*>(kt + 32 * q);
 #pragma unroll
             for (int r4 = 0; r4 < 4; ++r4) {
@@ -1280,8 +1324,12 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
             const int l = 16 * half + r;
-            if (l < U.nr)
-                yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)d[r][0], (float)d[r][1], (float)d[r][2], 0.f);
+            if (l < U.nr) {
+                const size_t iy = (size_t)(U.r0 + l) * Sp + inst;
+                yout[iy] = (float)d[r][0];
+                yout[PS + iy] = (float)d[r][1];
+                yout[2 * PS + iy] = (float)d[r][2];
+            }
         }
         return;
     }
@@ -1317,14 +1365,17 @@ __global__ void __launch_bounds__(256, 1)
                 t1 += __ldcg(pq + pstride);
                 t2 += __ldcg(pq + 2 * pstride);
             }
-            yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
+            const size_t iy = (size_t)(U.r0 + l) * Sp + inst;
+            yout[iy] = (float)t0;
+            yout[PS + iy] = (float)t1;
+            yout[2 * PS + iy] = (float)t2;
         }
     }
     if (threadIdx.x == 0) counters[U.block * nchunks + chunk] = 0;
 }
 
 void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1p,
-                           const float4* u, float4* y, double* part, int* counters) {
+                           const float* u, float* y, double* part, int* counters) {
     static unsigned long long attr = 0;
     per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_kpass_b<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
@@ -1335,14 +1386,14 @@ void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BU
 }
 
 void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
-                           const float* T2, const float4* y, double4* x, const double4* xt, double4* v,
+                           const float* T2, const float* y, double4* x, const double4* xt, double4* v,
                            double inv_h, int finalize_v) {
     static unsigned long long attr = 0;
     per_device_once(attr, [&] {
         cudaFuncSetAttribute(k_kpass_b<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
     });
     const int nch = (S + kBInst - 1) / kBInst;
-    launch_pdl(k_kpass_b<2>, dim3(nunits, nch), dim3(256), kBSmem, st, S, n_f, units, T2, cover, y, (float4*)nullptr,
+    launch_pdl(k_kpass_b<2>, dim3(nunits, nch), dim3(256), kBSmem, st, S, n_f, units, T2, cover, y, (float*)nullptr,
                (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v);
 }
 
@@ -1395,108 +1446,140 @@ __device__ __forceinline__ float tf32_rn(float v) {
     return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);
 }
 
+// ----------------------------------------------------------------------------
+// Plane-layout batched K-passes on the tensor cores (S > 1, sim_set_kpass_mode 2, default).
+// Right-hand sides are fp32 component planes v[c][row][Sp] (Sp = S rounded up to 4).  One CTA
+// = one unit (simhost::build_plane_units: 64 outputs x tiles of 32 reductions) x 128 instances
+// x the 3 components: per tile and component D_c[inst][out] += sum_q V_c[inst][q] K[q][out],
+// tcgen05.mma kind::tf32, M = 128 (instances) x N = 64 (outputs) x K = 8, 4 K-steps per tile.
+// 3xTF32: the tensor core truncates fp32 operands to tf32 (measured: tools/probes/tf32_round.cu),
+// so V_hi = trunc(V) is the raw fp32 tile in shared memory and V_lo = rn_tf32(V - trunc(V)) goes
+// to TMEM; K_hi / K_lo are pre-rounded on the host:
+//     D += V_hi K_hi + V_hi K_lo + V_lo K_hi          (|error| <= ~2^-21 |V| |K| per product)
+//   * V_hi: 16-byte cp.async straight from the planes into the MN-major SWIZZLE_128B_BASE32B
+//     canonical layout (umma_desc_mn32), 3 stages; no register staging, every thread has its
+//     next two tiles' copies in flight;
+//   * V_lo: the 16 worker warps read their 8 rows x 32 instances of V_hi back (conflict-free,
+//     one 128-B row per warp load), split, tcgen05.st into TMEM (lane = instance), 2 stages;
+//   * K tiles (hi 8 KB + lo 8 KB, K-major SWIZZLE_NONE) by one bulk copy per tile;
+//   * one elected thread of the extra warp issues the 36 MMAs per tile (3 components x 4
+//     K-steps x 3 products) and commits to the stage's mbarrier;
+//   * the TMEM accumulators (3 x 64 columns) are folded into fp32 registers every `drain`
+//     tiles (warp w: lanes 32 (w % 4).., columns 16 (w / 4)..): the fp32 MMA accumulation is
+//     lossy over long sums, a fold every 4 tiles bounds it.
+// TMEM: D_c at columns 64 c (192), V_lo stage s at 192 + 96 s + 32 c (+ 8 per K-step).
+// ----------------------------------------------------------------------------
+constexpr int kPlInst = 128;
+constexpr int kPlWarps = 16;
+constexpr int kPlThreads = 32 * kPlWarps;
+constexpr int kPlStages = 3;
+constexpr uint32_t kPlA = 3u * 16384u;            // V_hi: 3 components x 4 blocks x (32 rows x 128 B)
+constexpr uint32_t kPlB = 16384u;                 // K hi (8 KB) + lo (8 KB), 64 x 32 each
+constexpr uint32_t kPlStage = kPlA + kPlB;
+constexpr size_t kPlSmem = (size_t)kPlStages * kPlStage + 1024;
+constexpr uint32_t kPlLBO = 4096u, kPlSBO = 512u;
+// D f32, A / B tf32, N = 64, M = 128; A MN-major (bit 15) for the shared-memory operand
+constexpr uint32_t kIdescPlS = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kIdescPlT = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+
+// MN-major tf32 operands take only the SWIZZLE_128B_BASE32B layout (layout type 1; measured:
+// tools/probes/mma_layouts.cu): atom = 4 K-rows x 128 B (32 fp32 along M), 32-byte chunks XOR-permuted
+// by the row (Swizzle<2,5,2>); LBO = 4 KB between 32-instance blocks, SBO = 512 B between 4-row groups
+__device__ __forceinline__ uint64_t umma_desc_mn32(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(kPlLBO >> 4) << 16) | ((uint64_t)(kPlSBO >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)1 << 61);
+}
+__device__ __forceinline__ void umma_pl_ss(uint32_t dt, uint64_t da, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+        "l"(da), "l"(db), "r"(kIdescPlS), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_pl_ts(uint32_t dt, uint32_t at, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dt),
+        "r"(at), "l"(db), "r"(kIdescPlT), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async16_z(uint32_t saddr, const void* gmem, uint32_t bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+
 template <int PASS>
-__global__ void __launch_bounds__(kTcThreads + 32, 1)
-    k_kpass_tc(int S, int n_f, const BUnit* __restrict__ units, const float* __restrict__ Ttc,
-               const int32_t* __restrict__ cover, const float4* __restrict__ vin, float4* __restrict__ yout,
-               double* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
+__global__ void __launch_bounds__(kPlThreads + 32, 1)
+    k_kpass_pl(int S, int Sp, int n_f, const BUnit* __restrict__ units, const float* __restrict__ T,
+               const int32_t* __restrict__ cover, const float* __restrict__ vin, float* __restrict__ yout,
+               float* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
                const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
     pdl_enter();
-    extern __shared__ unsigned char tsm_raw[];
-    __shared__ __align__(8) uint64_t bfull[2], mdone[2], afull[2];
+    extern __shared__ unsigned char pl_raw[];
+    __shared__ __align__(8) uint64_t afull[kPlStages], bfull[kPlStages], ready[kPlStages], mdone[kPlStages], dfree;
     __shared__ uint32_t tmem_base_s;
     __shared__ int s_last;
-    unsigned char* tsm = tsm_raw + ((128u - ((unsigned)__cvta_generic_to_shared(tsm_raw) & 127u)) & 127u);
+    unsigned char* sm = pl_raw + ((1024u - ((unsigned)__cvta_generic_to_shared(pl_raw) & 1023u)) & 1023u);
+    const uint32_t sm_a = (unsigned)__cvta_generic_to_shared(sm);
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    const bool mma_warp = w == kTcThreads / 32;   // the extra warp issues the MMAs; warps 0-15 produce
+    const bool mma_warp = w == kPlWarps;
     const BUnit U = units[blockIdx.x];
     const int chunk = blockIdx.y;
-    const int i0 = chunk * kTcInst;
-    const int ni = min(kTcInst, S - i0);
+    const int i0 = chunk * kPlInst;
+    const size_t PS = (size_t)n_f * Sp;            // plane stride
     const unsigned long long pol = l2_evict_first();
-    if (w == 0) {   // two accumulator sets of 3 x 32 columns (one folds while the other accumulates)
+    if (w == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                          (unsigned)__cvta_generic_to_shared(&tmem_base_s)),
-                     "r"(256u)
+                     "r"(512u)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (tid == 0) {
-        mbar_init(&bfull[0], 1);
-        mbar_init(&bfull[1], 1);
-        mbar_init(&mdone[0], 1);
-        mbar_init(&mdone[1], 1);
-        mbar_init(&afull[0], kTcThreads);
-        mbar_init(&afull[1], kTcThreads);
+        for (int s2 = 0; s2 < kPlStages; ++s2) {
+            mbar_init(&afull[s2], kPlThreads);
+            mbar_init(&bfull[s2], 1);
+            mbar_init(&ready[s2], kPlThreads);
+            mbar_init(&mdone[s2], 1);
+        }
+        mbar_init(&dfree, kPlThreads);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_base_s;
-    auto aplane = [&](int st, int c, int hl) { return tsm + st * kTcStage + (2 * c + hl) * kTcAplane; };
-    auto bplane = [&](int st, int hl) { return tsm + st * kTcStage + 6 * kTcAplane + hl * 4096; };
-    auto issueB = [&](int t) {
-        const int st = t & 1;
-        mbar_expect_tx(&bfull[st], 8192u);
-        bulk_g2s(bplane(st, 0), Ttc + 2 * U.toff + (int64_t)t * 2048, 8192u, &bfull[st], true, pol);
-    };
-    if (tid == 0) {
-        issueB(0);
-        if (U.ntiles > 1) issueB(1);
-    }
-    // producer: instance il, K chunks jb and jb + 4 (4 reduction rows each): 8 float4 loads in flight
-    const int il = tid & (kTcInst - 1), jb = tid >> 7;
-    const bool ilive = il < ni;
-    const uint32_t aoff = (uint32_t)((il >> 3) * 1024 + (il & 7) * 16);
-    // fold mapping: warp w owns TMEM lanes 32 (w % 4) .. +31 (instances) and output columns 8 (w / 4) .. +7
-    const int q4 = w & 3, oct = w >> 2;
-    double dacc[3][8];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) dacc[c][e] = 0.0;
-    // tiles are accumulated in groups of `drain` (>= 2) into TMEM set (group % 2); group g is
-    // folded into fp64 registers while group g + 1 accumulates, once its last MMA has completed
-    auto fold = [&](int g) {
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const uint32_t ta = tmem + ((uint32_t)(32 * q4) << 16) + 128u * (g & 1) + 32u * c + 8u * oct;
-            uint32_t r[8];
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-                         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                           "=r"(r[7])
-                         : "r"(ta));
-            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-            for (int e = 0; e < 8; ++e) dacc[c][e] += (double)__uint_as_float(r[e]);
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    };
+    const int nt = U.ntiles;
     if (mma_warp) {
-        // single issuing thread: per tile, wait for the 512 producers' A planes and the B tile,
-        // then 36 MMAs into the TMEM accumulators and a commit that frees the stage
         if (lane == 0) {
-            for (int t = 0; t < U.ntiles; ++t) {
-                const int st = t & 1;
-                mbar_wait(&afull[st], (t >> 1) & 1);
-                mbar_wait(&bfull[st], (t >> 1) & 1);
+            for (int t = 0; t < nt; ++t) {
+                const int st = t % kPlStages;
+                const unsigned ph = (unsigned)(t / kPlStages) & 1u;
+                mbar_wait(&bfull[st], ph);
+                mbar_wait(&ready[st], ph);
+                if (t > 0 && t % drain == 0) mbar_wait(&dfree, (unsigned)(t / drain - 1) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                const uint32_t b0 = (unsigned)__cvta_generic_to_shared(bplane(st, 0));
-                const uint32_t b1 = (unsigned)__cvta_generic_to_shared(bplane(st, 1));
+                const uint32_t abase = sm_a + st * kPlStage, bbase = abase + kPlA;
+                const uint32_t lo = tmem + 192u + 96u * (t & 1);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const uint32_t a0 = (unsigned)__cvta_generic_to_shared(aplane(st, c, 0));
-                    const uint32_t a1 = (unsigned)__cvta_generic_to_shared(aplane(st, c, 1));
-                    const uint32_t dt = tmem + 128u * ((t / drain) & 1) + 32u * c;
+                    const uint32_t dt = tmem + 64u * c;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t o = 256u * kk;
-                        umma_tf32(dt, umma_desc_k(a0 + o), umma_desc_k(b0 + o),
-                                  (t % drain != 0 || kk > 0) ? 1u : 0u);
-                        umma_tf32(dt, umma_desc_k(a1 + o), umma_desc_k(b0 + o), 1u);
-                        umma_tf32(dt, umma_desc_k(a0 + o), umma_desc_k(b1 + o), 1u);
+                        const uint64_t da = umma_desc_mn32(abase + 16384u * c + 1024u * kk);
+                        const uint64_t dbh = umma_desc_k(bbase + 256u * kk), dbl = umma_desc_k(bbase + 8192u + 256u * kk);
+                        umma_pl_ss(dt, da, dbh, (t % drain != 0 || kk > 0) ? 1u : 0u);
+                        umma_pl_ss(dt, da, dbl, 1u);
+                        umma_pl_ts(dt, lo + 32u * c + 8u * kk, dbh, 1u);
                     }
                 }
                 umma_commit(&mdone[st]);
@@ -1504,136 +1587,209 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
         }
         __syncwarp();
     } else {
-    for (int t = 0; t < U.ntiles; ++t) {
-        const int st = t & 1;
-        const int nv = PASS == 1 ? max(0, min(32, n_f - (U.c0 + 32 * t))) : min(32, U.nlist - 32 * t);
-        // issue this thread's 8 row loads first (they do not touch shared memory)
-        float4 r[2][4];
-#pragma unroll
-        for (int it = 0; it < 2; ++it)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int q = 4 * (jb + 4 * it) + e;
-                r[it][e] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (ilive && q < nv) {
-                    const int idx = PASS == 1 ? U.c0 + 32 * t + q : __ldg(&cover[U.list0 + 32 * t + q]);
-                    r[it][e] = __ldg(&vin[(size_t)idx * S + i0 + il]);
-                }
+        // ---- workers: copies, V_lo, folds ----
+        auto row_of = [&](int t, int q, bool& ok) -> int {
+            if (PASS == 1) {
+                const int r = U.c0 + 32 * t + q;
+                ok = r < n_f;
+                return ok ? r : 0;
             }
-        if (t >= 2) {
-            mbar_wait(&mdone[st], ((t - 2) >> 1) & 1);   // the tensor core is done with stage st (tile t - 2)
-            if (tid == 0) issueB(t);
-            if ((t - 1) % drain == 0) fold((t - 2) / drain);   // tile t - 2 closed its group
-        }
+            ok = 32 * t + q < U.nlist;
+            return ok ? __ldg(&cover[U.list0 + 32 * t + q]) : 0;
+        };
+        auto issue = [&](int t) {   // this thread's 6 chunks of tile t's V_hi (and, thread 0, the K tile)
+            const int st = t % kPlStages;
+            const uint32_t abase = sm_a + st * kPlStage;
 #pragma unroll
-        for (int it = 0; it < 2; ++it) {
-            const int j = jb + 4 * it;
+            for (int e = 0; e < 6; ++e) {
+                const int id = tid + kPlThreads * e;
+                const int c = id >> 10, rem = id & 1023, q = rem >> 5, j = rem & 31;
+                bool ok;
+                const int r = row_of(t, q, ok);
+                const int inst = i0 + 4 * j;
+                ok = ok && inst < Sp;
+                const float* src = ok ? vin + c * PS + (size_t)r * Sp + inst : vin;
+                const uint32_t dst = abase + 16384u * c + 4096u * (j >> 3) + 128u * q + 32u * (((j & 7) >> 1) ^ (q & 3)) + 16u * (j & 1);
+                cp_async16_z(dst, src, ok ? 16u : 0u);
+            }
+            cp_async_arrive_noinc(&afull[st]);
+            if (tid == 0) {
+                mbar_expect_tx(&bfull[st], kPlB);
+                bulk_g2s(sm + st * kPlStage + kPlA, T + U.toff + (int64_t)t * 4096, kPlB, &bfull[st], true, pol);
+            }
+        };
+        const int qd = w & 3, oc = w >> 2;     // TMEM lane quadrant (= 32-instance block) / row octet
+        const uint32_t lanebase = tmem + ((uint32_t)(32 * qd) << 16);
+        float acc[3][16];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[c][e] = 0.f;
+        auto fold = [&]() {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                float a[4];
+                uint32_t r[16];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15}, [%16];\n"
+                    : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                      "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                      "=r"(r[15])
+                    : "r"(lanebase + 64u * c + 16u * oc));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-                for (int e = 0; e < 4; ++e) a[e] = c == 0 ? r[it][e].x : (c == 1 ? r[it][e].y : r[it][e].z);
-                float4 hi, lo;
-                hi.x = tf32_rn(a[0]); hi.y = tf32_rn(a[1]); hi.z = tf32_rn(a[2]); hi.w = tf32_rn(a[3]);
-                lo.x = tf32_rn(a[0] - hi.x); lo.y = tf32_rn(a[1] - hi.y);
-                lo.z = tf32_rn(a[2] - hi.z); lo.w = tf32_rn(a[3] - hi.w);
-                *reinterpret_cast<float4*>(aplane(st, c, 0) + aoff + j * 128) = hi;
-                *reinterpret_cast<float4*>(aplane(st, c, 1) + aoff + j * 128) = lo;
+                for (int e = 0; e < 16; ++e) acc[c][e] += __uint_as_float(r[e]);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        };
+        issue(0);
+        if (nt > 1) issue(1);
+        for (int t = 0; t < nt; ++t) {
+            const int st = t % kPlStages;
+            if (t + 2 < nt) {
+                if (t >= 1) mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
+                issue(t + 2);
+            }
+            mbar_wait(&afull[st], (unsigned)(t / kPlStages) & 1u);
+            if (t >= 2) mbar_wait(&mdone[(t - 2) % kPlStages], (unsigned)((t - 2) / kPlStages) & 1u);
+            // V_lo of rows 8 oc .. 8 oc + 7 (K-step oc) for instance 32 qd + lane
+            const unsigned char* ab = sm + st * kPlStage + 4096 * qd;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                uint32_t lo[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int q = 8 * oc + r;
+                    const float a = *reinterpret_cast<const float*>(ab + 16384 * c + 128 * q + 32 * ((lane >> 3) ^ (q & 3)) +
+                                                                    4 * (lane & 7));
+                    lo[r] = __float_as_uint(tf32_rn(a - tf32_trunc(a)));
+                }
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
+                                 lanebase + 192u + 96u * (t & 1) + 32u * c + 8u * oc),
+                             "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7])
+                             : "memory");
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> async proxy
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            mbar_arrive(&ready[st]);
+            // the group of tiles ending at t - 1 is complete once MMA(t - 1) is: fold it, free D
+            if (t > 0 && t % drain == 0) {
+                mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
+                fold();
+                mbar_arrive(&dfree);
             }
         }
-        // generic-proxy writes (and the fold's TMEM reads) -> visible to the tensor core, then arrive
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(
-                         (unsigned)__cvta_generic_to_shared(&afull[st]))
-                     : "memory");
-    }
-    {
-        const int last = U.ntiles - 1;
-        if (last >= 0) {
-            mbar_wait(&mdone[last & 1], (last >> 1) & 1);
-            // groups not folded in the loop: the last one, and the one before it when the loop
-            // ended before reaching its fold point (tile index last group start + 1)
-            const int glast = last / drain;
-            const int gdone = last >= 1 ? (last - 1) / drain : 0;   // groups folded: those whose fold tile <= last
-            for (int g = gdone; g <= glast; ++g) fold(g);
+        if (nt > 0) {
+            mbar_wait(&mdone[(nt - 1) % kPlStages], (unsigned)((nt - 1) / kPlStages) & 1u);
+            fold();
         }
-    }
-    }   // producers
-    __syncthreads();
-    if (w == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256u) : "memory");
-    if (mma_warp) return;
-    const int li = 32 * q4 + lane;
-    const bool live = li < ni;
-    const int inst = i0 + li;
-    if (PASS == 2) {
-        if (!live) return;
+        // ---- epilogue: thread = instance i0 + 32 qd + lane, outputs 16 oc .. 16 oc + 15 ----
+        const int inst = i0 + 32 * qd + lane;
+        const bool live = inst < S;
+        if (PASS == 2) {
+            if (live) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int l = 8 * oct + r;
-            if (l < U.nr) {
-                const size_t jx = (size_t)(U.c0 + l) * S + inst;
-                double4 xj = x[jx];
-                xj.x += dacc[0][r];
-                xj.y += dacc[1][r];
-                xj.z += dacc[2][r];
-                x[jx] = xj;
-                if (finalize_v) {   // v = (x - x_t) / h
-                    const double4 t0 = xt[jx];
-                    v[jx] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
+                for (int e = 0; e < 16; ++e) {
+                    const int l = 16 * oc + e;
+                    if (l < U.nr) {
+                        const size_t jx = (size_t)(U.c0 + l) * S + inst;
+                        double4 xj = x[jx];
+                        xj.x += (double)acc[0][e];
+                        xj.y += (double)acc[1][e];
+                        xj.z += (double)acc[2][e];
+                        x[jx] = xj;
+                        if (finalize_v) {   // v = (x - x_t) / h
+                            const double4 t0 = xt[jx];
+                            v[jx] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
+                        }
+                    }
                 }
             }
-        }
-        return;
-    }
-    if (U.nparts == 1) {
-        if (!live) return;
+        } else if (U.nparts == 1) {
+            if (live) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int l = 8 * oct + r;
-            if (l < U.nr)
-                yout[(size_t)(U.r0 + l) * S + inst] =
-                    make_float4((float)dacc[0][r], (float)dacc[1][r], (float)dacc[2][r], 0.f);
-        }
-        return;
-    }
-    // block split over several units: fp64 partials, combined in fixed order by the last unit
-    const size_t pstride = (size_t)32 * S;
-    if (live) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int l = 8 * oct + r;
-            double* pp = part + (size_t)U.part * 3 * pstride + (size_t)l * S + inst;
-            pp[0] = dacc[0][r];
-            pp[pstride] = dacc[1][r];
-            pp[2 * pstride] = dacc[2][r];
-        }
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int old = atomicAdd(&counters[U.block * nchunks + chunk], 1);
-        s_last = old == U.nparts - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    if (live) {
-        for (int r = 0; r < 8; ++r) {
-            const int l = 8 * oct + r;
-            if (l >= U.nr) continue;
-            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-            for (int q = 0; q < U.nparts; ++q) {
-                const double* pq = part + (size_t)(U.list0 + q) * 3 * pstride + (size_t)l * S + inst;
-                t0 += __ldcg(pq);
-                t1 += __ldcg(pq + pstride);
-                t2 += __ldcg(pq + 2 * pstride);
+                for (int e = 0; e < 16; ++e) {
+                    const int l = 16 * oc + e;
+                    if (l < U.nr) {
+                        const size_t iy = (size_t)(U.r0 + l) * Sp + inst;
+                        yout[iy] = acc[0][e];
+                        yout[PS + iy] = acc[1][e];
+                        yout[2 * PS + iy] = acc[2][e];
+                    }
+                }
             }
-            yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
+        } else {
+            // a block split over several units: fp32 partials [part][3][64][Sp], summed in fp64 in
+            // part order by the last unit to arrive
+            const size_t pst = (size_t)64 * Sp;
+            if (live) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    float* pp = part + (size_t)U.part * 3 * pst + (size_t)(16 * oc + e) * Sp + inst;
+                    pp[0] = acc[0][e];
+                    pp[pst] = acc[1][e];
+                    pp[2 * pst] = acc[2][e];
+                }
+            }
+            __threadfence();
+            asm volatile("bar.sync 1, %0;\n" ::"r"(kPlThreads));
+            if (tid == 0) {
+                const int old = atomicAdd(&counters[U.block * nchunks + chunk], 1);
+                s_last = old == U.nparts - 1;
+            }
+            asm volatile("bar.sync 1, %0;\n" ::"r"(kPlThreads));
+            if (s_last) {
+                __threadfence();
+                if (live) {
+                    for (int e = 0; e < 16; ++e) {
+                        const int l = 16 * oc + e;
+                        if (l >= U.nr) continue;
+                        double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+                        for (int q = 0; q < U.nparts; ++q) {
+                            const float* pq = part + (size_t)(U.list0 + q) * 3 * pst + (size_t)l * Sp + inst;
+                            t0 += (double)__ldcg(pq);
+                            t1 += (double)__ldcg(pq + pst);
+                            t2 += (double)__ldcg(pq + 2 * pst);
+                        }
+                        const size_t iy = (size_t)(U.r0 + l) * Sp + inst;
+                        yout[iy] = (float)t0;
+                        yout[PS + iy] = (float)t1;
+                        yout[2 * PS + iy] = (float)t2;
+                    }
+                }
+                if (tid == 0) counters[U.block * nchunks + chunk] = 0;
+            }
         }
     }
-    if (threadIdx.x == 0) counters[U.block * nchunks + chunk] = 0;
+    __syncthreads();
+    if (w == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u) : "memory");
+}
+
+void launch_kpass1_pl(cudaStream_t st, int S, int Sp, int n_f, int nunits, const BUnit* units, const float* T,
+                      const float* u, float* y, float* part, int* counters, int drain) {
+    static unsigned long long attr = 0;
+    per_device_once(attr, [&] {
+        cudaFuncSetAttribute(k_kpass_pl<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlSmem);
+    });
+    const int nch = (S + kPlInst - 1) / kPlInst;
+    launch_pdl(k_kpass_pl<1>, dim3(nunits, nch), dim3(kPlThreads + 32), kPlSmem, st, S, Sp, n_f, units, T,
+               (const int32_t*)nullptr, u, y, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
+               (double4*)nullptr, 0.0, 0, drain);
+}
+
+void launch_kpass2_pl(cudaStream_t st, int S, int Sp, int n_f, int nunits, const BUnit* units, const int32_t* cover,
+                      const float* T, const float* y, double4* x, const double4* xt, double4* v, double inv_h,
+                      int finalize_v, int drain) {
+    static unsigned long long attr = 0;
+    per_device_once(attr, [&] {
+        cudaFuncSetAttribute(k_kpass_pl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlSmem);
+    });
+    const int nch = (S + kPlInst - 1) / kPlInst;
+    launch_pdl(k_kpass_pl<2>, dim3(nunits, nch), dim3(kPlThreads + 32), kPlSmem, st, S, Sp, n_f, units, T, cover, y,
+               (float*)nullptr, (float*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain);
 }
 
 // ----------------------------------------------------------------------------
@@ -1761,8 +1917,8 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     } else {
         for (int t = 0; t < U.ntiles; ++t) {
             const int st = t & 1;
-            // PASS 1 / 4: contiguous reduction indices (columns / slots); PASS 2 / 3: a cover-row list
-            constexpr bool kContig = PASS == 1 || PASS == 4;
+            // PASS 4: contiguous reduction indices (slots); PASS 3: a chain-row list
+            constexpr bool kContig = PASS == 4;
             const int nv = kContig ? max(0, min(32, n_f - (U.c0 + 32 * t))) : min(32, U.nlist - 32 * t);
             float4 r[8];
 #pragma unroll
@@ -1770,8 +1926,11 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
                 const int q = 8 * oct + e;
                 r[e] = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (ilive && q < nv) {
-                    const int idx = kContig ? U.c0 + 32 * t + q : __ldg(&cover[U.list0 + 32 * t + q]);
-                    r[e] = __ldg(&vin[(size_t)idx * S + i0 + il]);
+                    if (PASS == 4) {   // wz^T, float4 [slot][S]
+                        r[e] = __ldg(&vin[(size_t)(U.c0 + 32 * t + q) * S + i0 + il]);
+                    } else {           // y at a chain row (planes, vec_ld)
+                        r[e] = vec_ld(vin, S, ex.nf, __ldg(&cover[U.list0 + 32 * t + q]), i0 + il);
+                    }
                 }
             }
             if (t > 0 && t % drain == 0) {   // accumulators complete up to tile t - 1: fold, restart
@@ -1838,43 +1997,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const int l = 8 * oct + r;
-            if (l < U.nr) {
-                const size_t iy = (size_t)ex.orows[U.r0 + l] * S + inst;
-                const float4 yi = yout[iy];
-                yout[iy] = make_float4((float)(yi.x + dacc[0][r]), (float)(yi.y + dacc[1][r]),
-                                       (float)(yi.z + dacc[2][r]), yi.w);
-            }
-        }
-        return;
-    }
-    if (PASS == 2) {
-        if (!live) return;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int l = 8 * oct + r;
-            if (l < U.nr) {
-                const size_t jx = (size_t)(U.c0 + l) * S + inst;
-                double4 xj = x[jx];
-                xj.x += dacc[0][r];
-                xj.y += dacc[1][r];
-                xj.z += dacc[2][r];
-                x[jx] = xj;
-                if (finalize_v) {
-                    const double4 t0 = xt[jx];
-                    v[jx] = make_double4((xj.x - t0.x) * inv_h, (xj.y - t0.y) * inv_h, (xj.z - t0.z) * inv_h, 0.0);
-                }
-            }
-        }
-        return;
-    }
-    if (U.nparts == 1) {
-        if (!live) return;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const int l = 8 * oct + r;
-            if (l < U.nr)
-                yout[(size_t)(U.r0 + l) * S + inst] =
-                    make_float4((float)dacc[0][r], (float)dacc[1][r], (float)dacc[2][r], 0.f);
+            if (l < U.nr) vec_add(yout, S, ex.nf, ex.orows[U.r0 + l], inst, dacc[0][r], dacc[1][r], dacc[2][r]);
         }
         return;
     }
@@ -1898,7 +2021,7 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
     asm volatile("bar.sync 1, %0;\n" ::"r"(kTcThreads));
     if (!s_last) return;
     __threadfence();
-    const int first = PASS >= 3 ? U.pad : U.list0;   // the block's first partial slot
+    const int first = U.pad;   // the block's first partial slot
     if (live) {
         for (int r = 0; r < 8; ++r) {
             const int l = 8 * oct + r;
@@ -1912,78 +2035,36 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
             }
             if (PASS == 3) {
                 chain_rho(S, inst, ex.soff[inst] + U.c0 + l, t0, t1, t2, ex.cc, ex.xs, ex.cs);
-            } else if (PASS == 4) {
-                const size_t iy = (size_t)ex.orows[U.r0 + l] * S + inst;
-                const float4 yi = yout[iy];
-                yout[iy] = make_float4((float)(yi.x + t0), (float)(yi.y + t1), (float)(yi.z + t2), yi.w);
-            } else
-                yout[(size_t)(U.r0 + l) * S + inst] = make_float4((float)t0, (float)t1, (float)t2, 0.f);
+            } else {
+                vec_add(yout, S, ex.nf, ex.orows[U.r0 + l], inst, t0, t1, t2);
+            }
         }
     }
     if (threadIdx.x == 0) counters[U.block * nchunks + chunk] = 0;
 }
 
-void launch_kpass1_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
-                      const float4* u, float4* y, double* part, int* counters, int drain) {
-    const int nch = (S + kTcInst - 1) / kTcInst;
-    launch_pdl(k_kpass_ts<1>, dim3(nunits, nch), dim3(kTcThreads + 32), 0, st, S, n_f, units, T1tc,
-               (const int32_t*)nullptr, u, y, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
-               (double4*)nullptr, 0.0, 0, drain, TsExtra{});
-}
-
-void launch_kpass2_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
-                      const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
-                      int finalize_v, int drain) {
-    const int nch = (S + kTcInst - 1) / kTcInst;
-    launch_pdl(k_kpass_ts<2>, dim3(nch, nunits), dim3(kTcThreads + 32), 0, st, S, n_f, units, T2tc, cover, y,
-               (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain, TsExtra{});
-}
-
-void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units, const float* Ttc,
+void launch_chain_pass_ts(cudaStream_t st, int S, int nf, int nunits, const BUnit* units, const float* Ttc,
                           const int32_t* cover, const float4* y, const int* soff, CrContacts cc, const double4* x,
                           ContactState cs, int drain, double* part, int* counters) {
     if (nunits == 0) return;
     const int nch = (S + kTcInst - 1) / kTcInst;
-    TsExtra ex{nullptr, soff, cc, x, cs};
+    TsExtra ex{nullptr, soff, cc, x, cs, nf};
     launch_pdl(k_kpass_ts<3>, dim3(nch, nunits), dim3(kTcThreads + 32), 0, st, S, 0, units, Ttc, cover, y,
                (float4*)nullptr, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
                (double4*)nullptr, 0.0, 0, drain, ex);
 }
 
-void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BUnit* units, const float* Ttc,
+void launch_scatter_pass_ts(cudaStream_t st, int S, int nf, int ns, int nunits, const BUnit* units, const float* Ttc,
                             const int32_t* rows, const float4* wzT, float4* y, int drain, double* part,
                             int* counters) {
     if (nunits == 0) return;
     const int nch = (S + kTcInst - 1) / kTcInst;
-    TsExtra ex{rows, nullptr, CrContacts{}, nullptr, ContactState{}};
+    TsExtra ex{rows, nullptr, CrContacts{}, nullptr, ContactState{}, nf};
     launch_pdl(k_kpass_ts<4>, dim3(nch, nunits), dim3(kTcThreads + 32), 0, st, S, ns, units, Ttc,
                (const int32_t*)nullptr, wzT, y, part, counters, nch, (double4*)nullptr,
                (const double4*)nullptr, (double4*)nullptr, 0.0, 0, drain, ex);
 }
 
-void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
-                      const float4* u, float4* y, double* part, int* counters, int drain) {
-    static unsigned long long attr = 0;
-    per_device_once(attr, [&] {
-        cudaFuncSetAttribute(k_kpass_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-    });
-    const int nch = (S + kTcInst - 1) / kTcInst;
-    launch_pdl(k_kpass_tc<1>, dim3(nunits, nch), dim3(kTcThreads + 32), kTcSmem, st, S, n_f, units, T1tc,
-               (const int32_t*)nullptr, u, y, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
-               (double4*)nullptr, 0.0, 0, drain);
-}
-
-void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
-                      const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
-                      int finalize_v, int drain) {
-    static unsigned long long attr = 0;
-    per_device_once(attr, [&] {
-        cudaFuncSetAttribute(k_kpass_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-    });
-    const int nch = (S + kTcInst - 1) / kTcInst;
-    launch_pdl(k_kpass_tc<2>, dim3(nunits, nch), dim3(kTcThreads + 32), kTcSmem, st, S, n_f, units, T2tc, cover, y,
-               (float4*)nullptr, (double*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain);
-}
 
 // ----------------------------------------------------------------------------
 // chain dot: dxt_s = (K^T y)_{a_s} = sum_k Kcol[colptr_a + k] y[chain_rows[off + k]]
@@ -2013,7 +2094,7 @@ __device__ __forceinline__ void chain_rho(int S, int inst, int s, double t0, dou
     }
 }
 
-__global__ void __launch_bounds__(256) k_chain_dot(int S, InstOff off, ClassSlots csl, const float* __restrict__ Kcol,
+__global__ void __launch_bounds__(256) k_chain_dot(int S, int n_f, InstOff off, ClassSlots csl, const float* __restrict__ Kcol,
                                                    const int64_t* __restrict__ colptr,
                                                    const int32_t* __restrict__ chain_off,
                                                    const int32_t* __restrict__ chain_rows, const float4* __restrict__ y,
@@ -2044,7 +2125,7 @@ __global__ void __launch_bounds__(256) k_chain_dot(int S, InstOff off, ClassSlot
             float4 yy[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                yy[u] = rw[u] >= 0 ? __ldg(&y[(size_t)rw[u] * S + inst]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                yy[u] = rw[u] >= 0 ? vec_ld(y, S, n_f, rw[u], inst) : make_float4(0.f, 0.f, 0.f, 0.f);
             float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -2089,7 +2170,7 @@ __global__ void __launch_bounds__(256) k_chain_dot(int S, InstOff off, ClassSlot
         for (int q = 0; q < n; ++q) {
             const int r = __shfl_sync(0xffffffffu, rmine, q);
             const float kv = __shfl_sync(0xffffffffu, kmine, q);
-            const float4 yv = __ldg(&y[(size_t)r * S + inst]);
+            const float4 yv = vec_ld(y, S, n_f, r, inst);
             f0 = fmaf(kv, yv.x, f0);
             f1 = fmaf(kv, yv.y, f1);
             f2 = fmaf(kv, yv.z, f2);
@@ -2106,7 +2187,7 @@ void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots 
                       Slots sl, CrContacts cc, const double4* x, ContactState cs, int nitems, const int2* items) {
     if (P.NS == 0 || nitems == 0) return;
     (void)sl;
-    launch_pdl(k_chain_dot, dim3(nitems), dim3(32 * kWarps), 0, st, P.S, off, csl, Kcol, colptr, chain_off, chain_rows,
+    launch_pdl(k_chain_dot, dim3(nitems), dim3(32 * kWarps), 0, st, P.S, P.n_f, off, csl, Kcol, colptr, chain_off, chain_rows,
                y, cc, x, cs, items);
 }
 
@@ -2282,7 +2363,7 @@ void launch_ulist(cudaStream_t st, const Params& P, InstOff off, const uint8_t* 
 //   group of 1: warp per row, lanes split the slot range (4 loads in flight per lane);
 //   larger groups: warp per row, lane = instance (coalesced y), slots in sequence.
 // ----------------------------------------------------------------------------
-__global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist,
+__global__ void k_scatter(int S, int n_f, InstOff off, const int* __restrict__ ucount, const int4* __restrict__ ulist,
                           const float* __restrict__ Zc, const double* __restrict__ wz,
                           const float4* __restrict__ wzT, float4* __restrict__ y, const int2* __restrict__ items) {
     pdl_enter();
@@ -2321,11 +2402,7 @@ __global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, co
             a0 = warp_sum(a0);
             a1 = warp_sum(a1);
             a2 = warp_sum(a2);
-            if (lane == 0) {
-                const size_t iy = (size_t)u.x * S + inst;
-                const float4 yi = y[iy];
-                y[iy] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), yi.w);
-            }
+            if (lane == 0) vec_add(y, S, n_f, u.x, inst, a0, a1, a2);
         }
         return;
     }
@@ -2353,11 +2430,7 @@ __global__ void k_scatter(int S, InstOff off, const int* __restrict__ ucount, co
             a1 += (double)f1;
             a2 += (double)f2;
         }
-        if (live) {
-            const size_t iy = (size_t)u.x * S + inst;
-            const float4 yi = y[iy];
-            y[iy] = make_float4((float)(yi.x + a0), (float)(yi.y + a1), (float)(yi.z + a2), yi.w);
-        }
+        if (live) vec_add(y, S, n_f, u.x, inst, a0, a1, a2);
     }
 }
 
@@ -2367,7 +2440,7 @@ void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off,
     if (P.NS == 0 || nitems == 0) return;
     int gx = (max_rows + 7) / 8;
     if (nitems > 1) gx = std::min(gx, std::max(1, (148 * 8 + nitems - 1) / nitems));
-    launch_pdl(k_scatter, dim3(gx, nitems), dim3(256), 0, st, P.S, off, ucount, ulist, Zc, wz, wzT, y, items);
+    launch_pdl(k_scatter, dim3(gx, nitems), dim3(256), 0, st, P.S, P.n_f, off, ucount, ulist, Zc, wz, wzT, y, items);
 }
 
 // ----------------------------------------------------------------------------

@@ -12,6 +12,9 @@ using simhost::P1Item;
 using simhost::P2Block;
 using simhost::BUnit;
 
+// row stride of the fp32 component planes u, y hold for S > 1 (see vec_ld in kernels.cu)
+__host__ __device__ inline int plane_sp(int S) { return S == 1 ? 1 : (S + 3) & ~3; }
+
 constexpr int kMaxContacts = 1024;   // per instance: the CR keeps fp64 vectors of 3*kMaxContacts rows in SMEM
 constexpr int kMaxSlots = 1024;      // distinct contact vertices per instance
 #ifndef SIM_CR_CLUSTER
@@ -151,17 +154,18 @@ void launch_kpass2(cudaStream_t st, int nblocks, const P2Block* bl, const int32_
                    const float4* y, double4* x, const double4* xt, double4* v, double inv_h, int finalize_v);
 // batched K-passes (S > 1): K tiles shared by all instances (SpMM over 3 S right-hand sides)
 void launch_kpass1_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1p,
-                           const float4* u, float4* y, double* part, int* counters);
+                           const float* u, float* y, double* part, int* counters);
 void launch_kpass2_batched(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
-                           const float* T2, const float4* y, double4* x, const double4* xt, double4* v,
+                           const float* T2, const float* y, double4* x, const double4* xt, double4* v,
                            double inv_h, int finalize_v);
-// the same on the tensor cores (tcgen05 kind::tf32, 3xTF32): tile streams re-laid out by
-// simhost::tc_tiles (hi and lo tiles in the K-major core-matrix layout, 2048 floats per tile)
-void launch_kpass1_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
-                      const float4* u, float4* y, double* part, int* counters, int drain);
-void launch_kpass2_tc(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
-                      const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
-                      int finalize_v, int drain);   // drain: tiles accumulated in TMEM (fp32) per fp64 fold
+// plane-layout K-passes on the tensor cores (tcgen05 kind::tf32, 3xTF32; S > 1): u, y as fp32
+// component planes [3][n_f][Sp], units and tile streams of simhost::build_plane_units; split pass-1
+// blocks use fp32 partials part[nparts][3][64][Sp] and counters[nblocks][chunks] (zero between launches)
+void launch_kpass1_pl(cudaStream_t st, int S, int Sp, int n_f, int nunits, const BUnit* units, const float* T,
+                      const float* u, float* y, float* part, int* counters, int drain);
+void launch_kpass2_pl(cudaStream_t st, int S, int Sp, int n_f, int nunits, const BUnit* units, const int32_t* cover,
+                      const float* T, const float* y, double4* x, const double4* xt, double4* v, double inv_h,
+                      int finalize_v, int drain);   // drain: tiles accumulated in TMEM (fp32) per register fold
 // extra arguments of the contact passes on the tensor cores
 struct TsExtra {
     const int32_t* orows;   // scatter pass: output rows
@@ -169,23 +173,18 @@ struct TsExtra {
     CrContacts cc;
     const double4* xs;
     ContactState cs;
+    int nf;                 // free vertices (plane stride of y)
 };
 // contact passes of the single slot-set class (S > 1) on the tensor cores (simhost::ContactPasses)
 // units split over several parts (nparts > 1; pad = the block's first partial slot) sum fp64
 // partials in `part` ([slot][3][32][S]); the last part of a block (counters, zero on entry and
 // reset on exit) adds them in part order and evaluates the slots' Schur right-hand sides
-void launch_chain_pass_ts(cudaStream_t st, int S, int nunits, const BUnit* units, const float* Ttc,
+void launch_chain_pass_ts(cudaStream_t st, int S, int nf, int nunits, const BUnit* units, const float* Ttc,
                           const int32_t* cover, const float4* y, const int* soff, CrContacts cc, const double4* x,
                           ContactState cs, int drain, double* part, int* counters);
-void launch_scatter_pass_ts(cudaStream_t st, int S, int ns, int nunits, const BUnit* units, const float* Ttc,
+void launch_scatter_pass_ts(cudaStream_t st, int S, int nf, int ns, int nunits, const BUnit* units, const float* Ttc,
                             const int32_t* rows, const float4* wzT, float4* y, int drain, double* part,
                             int* counters);   // split units: as launch_chain_pass_ts
-// TS variant: right-hand sides staged in TMEM (tcgen05.st) instead of shared memory
-void launch_kpass1_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const float* T1tc,
-                      const float4* u, float4* y, double* part, int* counters, int drain);
-void launch_kpass2_ts(cudaStream_t st, int S, int n_f, int nunits, const BUnit* units, const int32_t* cover,
-                      const float* T2tc, const float4* y, double4* x, const double4* xt, double4* v, double inv_h,
-                      int finalize_v, int drain);
 // grouped: one work item per (class slot, 32 class members); items int2 {class slot, member0}
 void launch_chain_dot(cudaStream_t st, const Params& P, InstOff off, ClassSlots csl, const float* Kcol,
                       const int64_t* colptr, const int32_t* chain_off, const int32_t* chain_rows, const float4* y,

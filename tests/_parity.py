@@ -6,7 +6,8 @@
   unilateral contact outside the exclusion band, i.e. unless the ORACLE's values lie closer to a
   switching surface than the position tolerance can resolve (classify_with_band);
 * applied impulse: the per-vertex J^T Theta lambda of the last L-G iteration (unique even where
-  the rows of D are dependent and lambda is not, reading A31).
+  the rows of D are dependent and lambda is not, reading A31), within the image of the position
+  tolerance at each contact vertex (assert_impulse_parity).
 """
 import math
 
@@ -77,18 +78,23 @@ def rows_from_triples(o, a3):
     return np.asarray(out)
 
 
-def assert_impulse_parity(o, lam_g, theta_g, lam_o, theta_o, rel=1e-4):
+def assert_impulse_parity(o, lam_g, theta_g, lam_o, theta_o, tol):
     """Per-vertex J^T Theta lambda of the last L-G iteration, GPU vs oracle (theta_g as returned
-    by the sim_debug_contact_state hook, per-contact triples): max over vertices
-    and components within `rel` of the largest per-vertex impulse.  (The impulse enters
-    x^{k+1} = A^-1 (b + h^2 J^T Theta lambda); a 1e-4 relative impulse error moves x by
-    well under the 1e-5 bbox position tolerance on the scenes tested.)"""
+    by the sim_debug_contact_state hook, per-contact triples), at every contact vertex a:
+        |f_gpu,a - f_oracle,a|_inf <= tol / (h^2 (A_v^-1)_aa).
+    The impulse enters x^{k+1} = A^-1 (b + h^2 J^T Theta lambda): an impulse error df
+    at vertex a alone moves a by h^2 (A_v^-1)_aa df, so the bound is the image of the position
+    tolerance `tol` (1e-5 bbox), as the classification band of classify_with_band.  On a stiff
+    block the impulse is ill-determined along the near-null directions of D (reading A31) and
+    the band is wide; on soft scenes it is tight.  Returns max over vertices of err / allowed."""
     fg = applied_impulse(o, np.asarray(lam_g, float), rows_from_triples(o, theta_g))
     fo = applied_impulse(o, np.asarray(lam_o, float), np.asarray(theta_o, float))
-    scale = np.abs(fo).max()
-    err = np.abs(fg - fo).max()
-    assert err <= rel * max(scale, 1e-300), (err, scale, err / max(scale, 1e-300))
-    return err / max(scale, 1e-300)
+    vc = np.asarray(o.vc)
+    err = np.abs(fg[vc] - fo[vc]).max(axis=1)
+    allowed = tol / (o.h * o.h * np.diag(o.G))
+    ratio = float((err / allowed).max()) if vc.size else 0.0
+    assert ratio <= 1.0, (ratio, int(np.argmax(err / allowed)))
+    return ratio
 
 
 def assert_frame_parity(o, x, v, xg, xo, tol, what="", **frame_kw):
@@ -96,3 +102,38 @@ def assert_frame_parity(o, x, v, xg, xo, tol, what="", **frame_kw):
     err = float(np.abs(xg - xo).max())
     assert err <= tol, (what, err, tol, err / tol)
     return err
+
+
+def gpu_iterates(s, x_t, v_t, iters, instance=0):
+    """The GPU's L-G iterates (x^k, lambda^k), k = 1..iters, of the frame that starts at (x_t, v_t):
+    frames of k iterations from the same start (the path is deterministic, so the k-iteration
+    frame passes through the iterates of the shorter ones)."""
+    out = []
+    for k in range(1, iters + 1):
+        s.set_state(x_t, v_t, instance)
+        s.step(1, k)
+        out.append((s.get_state(instance)[0].copy(), s.get_lambda(instance).copy()))
+    return out
+
+
+def assert_iteration_parity(o, x_t, v_t, pins, iterates, tol):
+    """Re-synced per L-G iteration (the body of Alg. 4): for k = 0..K-1 the oracle
+    runs ONE iteration from the GPU's own iterate (x^k, lambda^k) (Oracle.frame(start=...); k = 0
+    is the frame start of readings A9/A10) and its x^{k+1} must lie within `tol` of the GPU's.
+    This checks that every iteration the GPU takes is the method's iteration, independently of
+    how the frame map amplifies the rounding of earlier iterations (conditioning).
+    Returns the per-iteration err / tol."""
+    keep = o.lg_iters
+    errs = []
+    try:
+        prev = None
+        for k, (xg, lg) in enumerate(iterates):
+            o.lg_iters = k + 1
+            start = None if prev is None else (prev[0], prev[1], k)
+            xo, _, _ = o.frame(x_t, v_t, pin_targets=pins, start=start)
+            errs.append(float(np.abs(xg - xo).max()) / tol)
+            prev = (xg, lg)
+    finally:
+        o.lg_iters = keep
+    assert max(errs) <= 1.0, errs
+    return errs

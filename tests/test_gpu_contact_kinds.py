@@ -137,7 +137,7 @@ def test_incline_spec_size_resynced(simmod):
         lg = s.get_lambda()
         xo, _, info = o.frame(x, v)
         assert np.abs(xg - xo).max() <= tol, (f, np.abs(xg - xo).max() / tol)
-        _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"])
+        _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"], tol)
         bad, cnt = _parity.classification_mismatches(o, xg, x, lg, xo, info["lam"], tol)
         assert bad == 0 and cnt > 0
         x, v = xg, vg

@@ -154,7 +154,7 @@ def test_incline_contact_frames_resynced(simmod, dmu):
         assert np.abs(xg - xo).max() < tol, (f, np.abs(xg - xo).max())
         # D of a stiff block on a plane is nearly rank-deficient (rigid modes dominate), so
         # per-row lambda is ill-determined (reading A31); the per-vertex impulse is not
-        _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"])
+        _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"], tol)
         bad, n = _parity.classification_mismatches(o, xg, x, lg, xo, info["lam"], tol)
         assert bad == 0 and n > 0, (f, bad, n)
         x, v = xg, vg
@@ -180,7 +180,7 @@ def test_incline_warm_start_sliding(simmod):
         lam = info["lam"]
         xg, _ = s.get_state()
         assert np.abs(xg - x).max() < tol, (f, np.abs(xg - x).max())
-        _parity.assert_impulse_parity(o, s.get_lambda(), debug_contact_state(s)["theta"], lam, info["theta_last"])
+        _parity.assert_impulse_parity(o, s.get_lambda(), debug_contact_state(s)["theta"], lam, info["theta_last"], tol)
 
 
 def test_warm_start_resynced_with_lambda(simmod):
@@ -234,8 +234,16 @@ def test_lambda_carry_across_commits(simmod):
 
 
 def test_gingerbread_frame_parity(simmod):
-    """cfg3 at the benchmark size: 19 691 v / 93 600 t / 800 contacts, 5 L-G, 10 CR; two
-    frames, the second re-synced to the GPU's state."""
+    """cfg3 at the benchmark size: 19 691 v / 93 600 t / 800 contacts, 5 L-G, 10 CR.
+    Frame 0 (from rest): positions within 1e-5 bbox of the oracle's frame, the per-vertex
+    impulse within its band, identical classification outside the A21 band.  Frames 0-2, each
+    started from the GPU's own state: every L-G iteration within 1e-5 bbox of the oracle's
+    iteration from the GPU's iterate (_parity.assert_iteration_parity).  From frame 1 on the
+    bars carry the slab and the frame map is ill-conditioned: the fp64 oracle's own frame moves
+    by 0.16 (frame 1) and 0.85 (frame 2) of the tolerance when only its inputs are rounded to fp32
+    (tools/frame_conditioning.py), so whole-frame agreement there measures the
+    map's amplification of fp32 rounding, not the GPU's arithmetic; the frame-level error is
+    checked against 3x the tolerance as a guard against drift."""
     sc = scenes.make_scene("cfg3")
     s = make(simmod, sc)
     s.set_pin_velocity(sc.pin_velocity)
@@ -244,18 +252,22 @@ def test_gingerbread_frame_parity(simmod):
     o.set_contacts(sc.contacts)
     tol = 1e-5 * sc.mesh.bbox_diag()
     x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
-    for f in range(2):
+    for f in range(3):
+        pins = x[o.pinned] + sc.h * sc.pin_velocity
+        its = _parity.gpu_iterates(s, x, v, 5)
+        _parity.assert_iteration_parity(o, x, v, pins, its, tol)
         s.set_state(x, v)
         s.step(1, 5)
         xg, vg = s.get_state()
-        pins = x[o.pinned] + sc.h * sc.pin_velocity
+        assert np.array_equal(xg, its[-1][0])          # deterministic: the 5-iteration frame
         xo, vo, info = o.frame(x, v, pin_targets=pins)
         err = np.abs(xg - xo).max()
-        assert err < tol, (f, err, tol)
-        lg = s.get_lambda()
-        _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"])
-        bad, n = _parity.classification_mismatches(o, xg, x, lg, xo, info["lam"], tol)
-        assert bad == 0 and n > 0, (f, bad, n)
+        assert err < (tol if f == 0 else 3 * tol), (f, err / tol)
+        if f == 0:
+            lg = s.get_lambda()
+            _parity.assert_impulse_parity(o, lg, debug_contact_state(s)["theta"], info["lam"], info["theta_last"], tol)
+            bad, n = _parity.classification_mismatches(o, xg, x, lg, xo, info["lam"], tol)
+            assert bad == 0 and n > 0, (f, bad, n)
         x, v = xg, vg
 
 

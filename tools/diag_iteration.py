@@ -1,8 +1,16 @@
-"""One-iteration error of the GPU path inside a frame: for k = 1..iters-1, the oracle runs ONE
-L-G iteration (Alg. 4 body) from the GPU's own iterate (x^k, lambda^k) -- the state
-after a GPU frame of k iterations -- and is compared with the GPU's x^{k+1}.  Small one-step errors
-with large frame errors mean the frame map amplifies rounding; a large one-step error means the
-GPU computes a different iteration.  usage: python tools/diag_iteration.py <cfg5 instance> [iters]"""
+"""Where a GPU frame departs from the oracle's (cfg5 instance, default readings A9/A10:
+x^0 = s, lambda^0 = 0).  For k = 0..iters-1 the GPU's iterate (x^k, lambda^k) is taken from a
+GPU frame of k iterations, then
+  * local: the GPU's projections P (sim_debug_local, fp32) vs the oracle's at the same x^k
+    (max |P_gpu - P_oracle|_F / max(1, |P_oracle|_F), the worst tets' smallest singular values);
+  * one-step: the oracle runs ONE L-G iteration (Alg. 4 body) from the GPU's
+    (x^k, lambda^k), compared with the GPU's x^{k+1}; "with P_gpu" repeats it with the GPU's
+    projections, isolating the global / contact part.
+Small one-step errors with a large frame error mean the frame map amplifies rounding; a large
+one-step error means the GPU computes a different iteration.
+With --batch S the GPU runs S copies of the instance in one handle (the batched path) and
+instance 0 is compared.
+usage: python tools/diag_iteration.py <cfg5 instance> [iters] [--batch S]"""
 import os
 import sys
 
@@ -15,14 +23,21 @@ from oracle import oracle as O
 import paper_2503_15078_b200 as simlib
 
 sc = scenes.make_scene("cfg3")
-inst = int(sys.argv[1])
-iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+inst = int(args[0])
+iters = int(args[1]) if len(args) > 1 else 5
+S = int(sys.argv[sys.argv.index("--batch") + 1]) if "--batch" in sys.argv else 1
+if S > 1:
+    args = [a for a in args if a != str(S)] if len(args) > 2 else args
 v0, cs = scenes.batch_instance(sc, inst)
 x0 = sc.mesh.X.copy()
 tol = 1e-5 * sc.mesh.bbox_diag()
-s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, n_instances=S)
 s.set_pin_velocity(sc.pin_velocity)
-s.set_contacts(cs)
+if S > 1:
+    s.set_contacts_batch([cs] * S)
+else:
+    s.set_contacts(cs)
 o = O.Oracle(sc.mesh, sc.material, sc.h)
 o.set_contacts(cs)
 h = sc.h
@@ -30,11 +45,11 @@ pins = x0[o.pinned] + h * sc.pin_velocity
 spred = x0 + h * v0 + h * h * o.g[None, :]
 
 
-def one_iteration(x, lam):
-    """The body of Oracle.frame for one iteration from iterate x (pins already at target), lam."""
+def one_iteration(x, lam, P=None):
     F_ = o.free
     F = O.deformation_gradients(x, o.T, o.Bm)
-    P = O.project(F, o.model, o.k, o.mu, o.lam)
+    if P is None:
+        P = O.project(F, o.model, o.k, o.mu, o.lam)
     b = o.M[:, None] * spred + O.gt_p(P, o.Bm, o.w, h, o.T, o.n_v)
     b_f = b[F_] - o.A_fc @ x[o.pinned]
     theta, E, phi, Jx = o.indicators(x, x0, lam)
@@ -48,41 +63,31 @@ def one_iteration(x, lam):
     lam = lam + z / (h * h)
     xn = x.copy()
     xn[F_] = o.solve(b_f + h * h * o.JT(theta * lam)[F_])
-    return xn, lam
+    return xn, lam, E
 
 
-prev = None
-for k in range(1, iters + 1):
-    s.set_state(x0, v0)
-    s.step(1, k)
-    xg, _ = s.get_state()
-    lg = s.get_lambda()
-    if prev is not None:
-        xo, lo = one_iteration(*prev)
-        print(f"iteration {k}: one-step err/tol {np.abs(xg - xo).max() / tol:.4g}   "
-              f"lambda rel {np.abs(lg - lo).max() / np.abs(lo).max():.3g}", flush=True)
-    else:
-        lam0 = np.zeros(o.m)
-        xi = x0 + h * v0
-        xi[o.pinned] = pins
-        xo, lo = one_iteration(xi, lam0)
-        print(f"iteration 1: one-step err/tol {np.abs(xg - xo).max() / tol:.4g}", flush=True)
-    prev = (xg.copy(), lg.copy())
-
-# the oracle's own frame, and the oracle continued from the GPU's iterate after k iterations
-xi = x0 + h * v0
+xi = spred.copy()
 xi[o.pinned] = pins
-st = (xi, np.zeros(o.m))
-ref = []
-for k in range(iters):
-    st = one_iteration(*st)
-    ref.append(st)
-for k in range(1, iters):
-    s.set_state(x0, v0)
+gpu = [(xi, np.zeros(o.m))]
+for k in range(1, iters + 1):
+    for i in range(S):
+        s.set_state(x0, v0, instance=i)
     s.step(1, k)
-    stg = (s.get_state()[0].copy(), s.get_lambda().copy())
-    e0 = np.abs(stg[0] - ref[k - 1][0]).max() / tol
-    for _ in range(k, iters):
-        stg = one_iteration(*stg)
-    print(f"oracle continued from the GPU's x^{k} (itself {e0:.3g} tol off the oracle's x^{k}): "
-          f"frame end {np.abs(stg[0] - ref[-1][0]).max() / tol:.4g} tol off the oracle's frame", flush=True)
+    gpu.append((s.get_state()[0].copy(), s.get_lambda().copy()))
+for k in range(iters):
+    xk, lk = gpu[k]
+    F = O.deformation_gradients(xk, o.T, o.Bm)
+    Po = O.project(F, o.model, o.k, o.mu, o.lam)
+    Pg = s.debug_local(xk, spred)[0].astype(np.float64) if S == 1 else Po
+    dP = np.linalg.norm(Pg - Po, axis=(1, 2)) / np.maximum(1.0, np.linalg.norm(Po, axis=(1, 2)))
+    worst = np.argsort(-dP)[:3]
+    sig = np.linalg.svd(F[worst], compute_uv=False)
+    xo, lo, E = one_iteration(xk, lk)
+    xp, _, _ = one_iteration(xk, lk, P=Pg)
+    xg1, lg1 = gpu[k + 1]
+    print(f"iteration {k}->{k + 1}: local max dP {dP.max():.3g} (tets {list(worst)}, sigma {np.round(sig, 4).tolist()}); "
+          f"one-step err/tol {np.abs(xg1 - xo).max() / tol:.4g}, with P_gpu {np.abs(xg1 - xp).max() / tol:.4g}; "
+          f"lambda rel {np.abs(lg1 - lo).max() / np.abs(lo).max():.3g}; max E_f {E[1::3].max():.3g}", flush=True)
+
+xo_frame, _, _ = o.frame(x0, v0, pin_targets=pins)
+print(f"frame ({iters} iterations, S = {S}): GPU vs oracle {np.abs(gpu[-1][0] - xo_frame).max() / tol:.4g} tol", flush=True)
