@@ -158,9 +158,11 @@ def run_reference(args):
     ws, rank, local = dist_env()
     if ws > 1 and rank != 0:
         return
-    value, times, sample = oracle_sample(args.steps, warmup=min(args.warmup, 1))
-    import torch
+    from threadpoolctl import threadpool_limits
     threads = 1
+    with threadpool_limits(limits=threads):   # the reported core count is the one the oracle used
+        value, times, sample = oracle_sample(args.steps, warmup=min(args.warmup, 1))
+    import torch
     ms = 1000.0 * float(np.mean(times))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -173,7 +175,7 @@ def run_reference(args):
                    "global_batch": 1024 if not args.instances else args.instances * args.gpus,
                    "sampled_per_step": "1 scene-iteration (scene 0)", "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
-                         "host_cpus": os.cpu_count(), "torch_threads": torch.get_num_threads()},
+                         "host": cpu_info(), "threads": "BLAS / OpenMP pools limited with threadpoolctl"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -257,9 +259,11 @@ def measure(args, S, rank, ws, dev, stream, full=True):
     with Clocks(int(str(dev).split(":")[-1]) if ":" in str(dev) else 0) as clk:
         for i in range(args.steps):
             flush.zero_()                       # untimed L2 flush between timed steps
-            # host-side validation of this frame's contact arrays (the collision detector's
-            # output, an input of the step) overlaps the flush; the commit (packing, H2D copy,
-            # Delassus Gram and preconditioner kernels) and the frame run inside the timed region
+            # sim_set_contacts_batch validates and packs this frame's contact arrays on the host and
+            # enqueues their H2D upload (upload stream) and the stream-ordered D2D copy into the
+            # frame's arena; the device-timed region starts after that call: it holds the commit's
+            # device kernels (chain rows, Delassus Gram, preconditioner) and the frame.  The host
+            # half and the copies are inside the e2e number below.
             s.set_contacts_batch(packed=packed)
             ev[i][0].record(stream)
             s.step(1, ITERS)
@@ -427,6 +431,68 @@ def measure_pile(args, dev, stream):
     return out
 
 
+def measure_small(args, dev, stream):
+    """BASELINE configs[0] and configs[1] (the small-scene regime):
+    cfg1 cantilever (45 v / 80 t, NH, h = 1/60, 5 L-G, no contact; 100 frames) and cfg2 incline
+    block (10x10x10 v / 3 645 t, E = 1e8, 100 bottom contacts, mu = tan(10 deg) - 0.01, 5 L-G +
+    10 CR).  One CUDA graph per frame; ms per frame and per L-G iteration from CUDA events over
+    back-to-back frames (the cfg2 contact set committed once, as a resting scene), with the
+    kernels per frame (launch-latency breakdown: the frame time over the kernel count)."""
+    import math
+    import torch
+    import scenes
+    import paper_2503_15078_b200 as simlib
+    out = {}
+    for name, frames in (("cfg1", 100), ("cfg2", 50)):
+        if name == "cfg1":
+            sc = scenes.make_scene("cfg1")
+        else:
+            sc = scenes.incline_block(theta_deg=10.0, mu=math.tan(math.radians(10.0)) - 0.01, nv=10, edge=0.1,
+                                      youngs=1e8)
+        s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h)
+        s.set_stream(stream.cuda_stream)
+        if sc.contacts:
+            s.set_contacts(sc.contacts)
+        s.step(5, ITERS)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s.step(frames, ITERS)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / frames
+        st = s.stats()
+        kpf = int(st["kernels_per_frame"])
+        out[name] = {"workload": ("cfg1 cantilever 45 v / 80 t NH, h=1/60, no contact" if name == "cfg1" else
+                                  "cfg2 incline block 1000 v / 3645 t, E=1e8, 100 contacts, mu=tan(10deg)-0.01"),
+                     "frames_timed": frames, "ms_per_frame": ms, "ms_per_lg_iteration": ms / ITERS,
+                     "kernels_per_frame": kpf, "us_per_kernel": 1000.0 * ms / max(1, kpf)}
+        s.close()
+    return out
+
+
+def cpu_info():
+    """Host CPU model and core count of the box the oracle baseline runs on (lscpu)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in txt.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
+def oracle_baseline(threads):
+    """The fp64 oracle on one cfg3 L-G iteration with its BLAS / OpenMP pools limited to `threads`
+    (threadpoolctl), so the reported core count is the one it used."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=threads):
+        return oracle_sample(1)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -484,11 +550,20 @@ def run_ours(args):
             pile = measure_pile(args, dev, stream)
         except Exception as e:   # reported, never fatal for the headline line
             pile = {"error": repr(e)}
+    small = None
+    if ws == 1 and not args.no_pile:
+        try:
+            small = measure_small(args, dev, stream)
+        except Exception as e:
+            small = {"error": repr(e)}
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
-        cv, _, sample = oracle_sample(1)
+        cv, _, sample = oracle_baseline(1)
+        nall = os.cpu_count() or 1
+        cva, _, _ = oracle_baseline(nall)
         cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
-               "host_cpus": os.cpu_count()}
+               "all_cores": {"value": cva, "cores": nall}, "host": cpu_info(),
+               "threads": "BLAS / OpenMP pools limited with threadpoolctl"}
     # + per-step contact commit kernels: chain rows, row list, Zc fill, Delassus Gram, D_jj
     gpu_launches = r["kernels_per_frame"] * args.steps + 5 * args.steps
     wl = workload_name(scenes_total, S)
@@ -499,6 +574,7 @@ def run_ours(args):
         "config": {"workload": wl, "global_batch": scenes_total, "scenes_per_gpu": S,
                    "parallelism": f"instances{S}xdp{ws}",
                    "l2": "flushed (256 MB write) between timed steps"},
+        "ms_per_lg_iteration_single_scene": single_ms / args.steps / ITERS,
         "single_scene": {"workload": "cfg3 (one instance per GPU)",
                          "ms_per_lg_iteration": single_ms / args.steps / ITERS,
                          "scene_iters_per_s": args.steps * ITERS / (single_ms / 1000.0),
@@ -514,6 +590,7 @@ def run_ours(args):
         "ranks": [{"instances": int(g[0]), "frames": int(g[1]), "active_contacts": int(g[2]),
                    "max_cr_residual": g[3], "mean_displacement_m": g[4]} for g in gathered],
         "pile_cfg4": pile,
+        "small_configs": small,
         "cpu_baseline": cpu,
         "clocks": r["clocks"],
         "nnz_K": nnz, "n_free": nf, "etree_height": int(st0["etree_height"]),

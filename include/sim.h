@@ -141,6 +141,9 @@ typedef struct {
     double  max_cone_violation; /* max over unilateral contacts of max(0, |lambda_f| - mu max(lambda_n, 0)) */
     double  max_penetration;    /* max over unilateral contacts of max(0, -(J_n x - d_n)) at the frame end  */
     int32_t instance;           /* the instance these per-instance fields describe, -1 = all            */
+    int64_t kpass_bytes;        /* K values one K-pass pair streams per L-G iteration (both tile streams of the
+                                   handle's path, fp32; S > 1: the tensor-core hi + lo streams)         */
+    int64_t nnz_K_kept;         /* entries of K left nonzero after the drop tolerance (= nnz_K at tol 0) */
 } sim_stats;
 
 /* Validate the mesh and material, compute rest data (Dm^-1, volumes, lumped
@@ -153,7 +156,9 @@ int sim_create(const sim_mesh *mesh, const sim_material *mat, double h, sim_hand
  * compute K = L^-1 column by column over ancestor chains (Thm 1), store K in
  * fp32 twice (row-major and column-major values-only panels), build the
  * K-pass work lists and upload everything.  drop_tolerance: entries with
- * |K_ij| < tol |K_jj| are zeroed (0 = exact Theorem-1 pattern). */
+ * |K_ij| < tol |K_jj| are dropped (0 = exact Theorem-1 pattern; reading A25): each row's stored
+ * range starts at its first kept column, so the K-pass streams shrink by the dropped leading
+ * entries (sim_stats.kpass_bytes); the result approximates A^-1 (no 1e-5 parity claim). */
 int sim_build_sparse_inverse(sim_handle *h, double drop_tolerance);
 
 /* Replace the contact set of one instance (n may be 0).  Validates and builds
@@ -310,11 +315,12 @@ int sim_set_admm(sim_handle *h, int32_t on);
  * the next step. */
 int sim_set_warm_start(sim_handle *h, int32_t on);
 
-/* Batched K-passes (n_instances > 1): 2 = tcgen05 tensor cores with the right-hand sides
- * staged in TMEM (tcgen05.st) and read by the MMA from TMEM (default); 0 = tcgen05 with both
- * operands in shared memory; 1 = CUDA-core FP32 FMAs.  kind::tf32 with a 3xTF32 split, TMEM
- * accumulators folded into fp64 every 4 tiles; results agree with FP32 to ~2e-6 relative.
- * n_instances == 1 always uses the HBM-streaming SpMV kernels. */
+/* Batched K-passes (n_instances > 1): 2 (default; 0 is an alias) = tcgen05 tensor cores: the
+ * right-hand sides in fp32 component planes, one CTA per 64-output unit x 128 instances x 3
+ * components, kind::tf32 with a 3xTF32 split (V_hi = the raw fp32 tile in shared memory, MN-major;
+ * V_lo in TMEM; K_hi / K_lo pre-rounded), TMEM accumulators folded every 4 tiles;
+ * 1 = CUDA-core FP32 FMAs.  Results agree with FP32 to ~2e-6 relative.  n_instances == 1 always
+ * uses the HBM-streaming SpMV kernels.  (mode >> 4) >= 2 sets the fold interval (tuning). */
 int sim_set_kpass_mode(sim_handle *h, int32_t mode);
 
 /* Delassus reuse across contact commits (the "reuse strategy ... to exploit shared contact data
@@ -324,6 +330,14 @@ int sim_set_kpass_mode(sim_handle *h, int32_t mode);
  * accumulation order: bitwise the full recomputation).  Off by default (reading A23: the bench
  * recomputes D at every commit).  Cluster-CR scenes only; the grid CR always recomputes. */
 int sim_set_schur_reuse(sim_handle *h, int32_t on);
+
+/* Small-scene frame driver: 0 (default) = auto -- a handle with one instance, no contacts and plain
+ * PD whose n_free + n_tets <= 1024 runs sim_step's frames x iterations in ONE persistent single-CTA
+ * kernel (predict, local step, RHS, both K-passes, integrate and the finite check per frame, with
+ * block barriers instead of kernel boundaries: the cfg1 cantilever is launch-latency bound on the
+ * graph path); 1 = always the per-frame CUDA graph.  Same method and readings; results agree with
+ * the graph path to fp32 rounding (different accumulation order).  SIM_E_INVALID on other values. */
+int sim_set_persistent(sim_handle *h, int32_t mode);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 
 void sim_destroy(sim_handle *h);         /* NULL-safe */

@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = [
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
     "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison", "sim_get_positions_async",
     "sim_wait_positions", "sim_detect_contacts", "sim_get_contacts",
-    "sim_set_schur_reuse", "sim_set_lambda", "sim_set_pins", "sim_set_allocator", "sim_set_warm_start",
+    "sim_set_schur_reuse", "sim_set_lambda", "sim_set_pins", "sim_set_allocator", "sim_set_warm_start", "sim_set_persistent",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -91,7 +91,8 @@ class SimStats(C.Structure):
                 ("h2d_contact_bytes", C.c_int64), ("n_instances", C.c_int32),
                 ("nonfinite_rollbacks", C.c_int64), ("gram_rows_computed", C.c_int64),
                 ("gram_rows_reused", C.c_int64), ("build_phase_seconds", C.c_double * 5),
-                ("max_cone_violation", C.c_double), ("max_penetration", C.c_double), ("instance", C.c_int32)]
+                ("max_cone_violation", C.c_double), ("max_penetration", C.c_double), ("instance", C.c_int32),
+                ("kpass_bytes", C.c_int64), ("nnz_K_kept", C.c_int64)]
 
 
 class SimError(RuntimeError):
@@ -159,6 +160,7 @@ def _load():
         "sim_set_ncp": [H, C.c_int32, C.c_int32],
         "sim_set_admm": [H, C.c_int32],
         "sim_set_warm_start": [H, C.c_int32],
+        "sim_set_persistent": [H, C.c_int32],
         "sim_set_kpass_mode": [H, C.c_int32],
         "sim_debug_poison": [H, C.c_int32],
         "sim_get_positions_async": [H, C.c_void_p],
@@ -421,6 +423,11 @@ class Sim:
         """Frame start (sim_set_warm_start): False x^0 = s, lambda^0 = 0 (readings A9/A10);
         True x^0 = x_t + h v_t, lambda carried from the previous frame (A9w/A10w)."""
         _check(lib.sim_set_warm_start(self._h, 1 if on else 0))
+
+    def set_persistent(self, mode: int):
+        """Small-scene driver (sim_set_persistent): 0 auto (one persistent kernel per sim_step for
+        small contact-free single-instance scenes), 1 always the per-frame CUDA graph."""
+        _check(lib.sim_set_persistent(self._h, int(mode)))
 
     def set_kpass_mode(self, mode: int):
         """Batched K-passes: 0 tensor cores (tcgen05), 1 CUDA-core FP32 (sim_set_kpass_mode)."""

@@ -200,6 +200,7 @@ struct sim_handle {
     int bparts = 0, bblocks1 = 0;
     simhost::PlaneUnits pu;                 // plane-layout tensor-core K-pass units (S > 1)
     int64_t nnzL = 0;
+    int64_t nnz_kept = 0;            // nonzeros of K after the drop tolerance
     double build_seconds = 0;
     DBuf<double4> vpin;              // [n_v - n_f][S] pinned-vertex velocities (moving Dirichlet targets)
     DBuf<double4> pin_tgt;           // sim_set_pins staging on the device
@@ -328,6 +329,8 @@ struct sim_handle {
     int ncp = 0, precond = 0;        // NCP function / complementarity preconditioner (sim_set_ncp)
     int admm = 0;                    // ADMM-PD local-global (sim_set_admm)
     int warm = 0;                    // frame start (sim_set_warm_start): readings A9/A10 or A9w/A10w
+    int persistent = 0;              // sim_set_persistent: 0 auto (small contact-free scenes), 1 off
+    bool last_persistent = false;    // the last sim_step ran the persistent small-scene kernel
     DBuf<float> du;                  // ADMM dual, [9][n_t S]
     bool grid = false;               // the committed contact set uses the grid CR
     int NG = 0, ng_max = 0;
@@ -703,6 +706,9 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     lap(3);
     if (H->K.nnz >= (int64_t)INT32_MAX)
         return fail(SIM_E_LIMIT, "nnz(K) = %lld exceeds the int32 offset limit", (long long)H->K.nnz);
+    simhost::trim_dropped(H->K);   // kept skyline (drop tolerance, reading A25)
+    H->nnz_kept = 0;
+    for (float q : H->K.Krow) H->nnz_kept += q != 0.f;
     simhost::build_worklists(H->K, H->wl, 1024);
     simhost::build_tiles(H->K, H->wl, H->T1h, H->T2h);
     if (H->S > 1) {
@@ -1701,6 +1707,21 @@ extern "C" int sim_set_warm_start(sim_handle* H, int32_t on) {
     return SIM_OK;
 }
 
+extern "C" int sim_set_persistent(sim_handle* H, int32_t mode) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (mode != 0 && mode != 1) return fail(SIM_E_INVALID, "mode must be 0 (auto) or 1 (graph only)");
+    H->persistent = mode;
+    return SIM_OK;
+}
+
+// the persistent small-scene kernel applies: one instance, no contacts, plain PD, small enough for
+// one CTA (its shared-memory vectors stay under 48 KB)
+static bool small_path(const sim_handle* H) {
+    if (H->persistent != 0 || H->S != 1 || H->C != 0 || H->admm || H->profiling || H->poison_inst >= 0) return false;
+    const Params P = make_params(const_cast<sim_handle*>(H));
+    return H->n_f + H->n_t <= 1024 && small_smem_bytes(P) <= 48 * 1024;
+}
+
 extern "C" int sim_set_schur_reuse(sim_handle* H, int32_t on) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (on != 0 && on != 1) return fail(SIM_E_INVALID, "flag must be 0 or 1");
@@ -1770,6 +1791,18 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
         H->frames_done += 1;
         if (--frames == 0) return SIM_OK;
     }
+    if (small_path(H)) {   // persistent small-scene driver: all frames in one launch
+        const Params P = make_params(H);
+        SmallArgs A{H->tet.p, H->Bm.p, H->hw2.p, H->M.p, H->adjp.p, H->adj.p, H->Krow.p, H->meta.p, H->Kcol.p,
+                    H->colptr.p, H->parent.p, H->x.p, H->xt.p, H->v.p, H->s.p, H->vt.p, H->rollbacks.p};
+        const int e = launch_small_frames(H->stream, P, A, frames, iters);
+        if (e) return fail(SIM_E_CUDA, "launch failed: %s", cudaGetErrorString((cudaError_t)e));
+        H->frames_done += frames;
+        H->kernels_per_frame = 1;
+        H->last_persistent = true;
+        return SIM_OK;
+    }
+    H->last_persistent = false;
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
                                       H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG,
                                       H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain, H->cr_mode, H->warm,
@@ -2065,6 +2098,11 @@ extern "C" int sim_get_stats(sim_handle* H, int32_t inst, sim_stats* o) {
     o->n_free = H->n_f;
     o->n_tets = H->n_t;
     o->nnz_K = H->K.nnz;
+    {
+        o->nnz_K_kept = H->nnz_kept;
+        o->kpass_bytes = H->S == 1 ? (int64_t)(H->T1h.size() + H->T2h.size()) * 4
+                                   : (int64_t)(H->pu.T1.size() + H->pu.T2.size()) * 4;
+    }
     o->nnz_L = H->nnzL;
     o->etree_height = H->K.height;
     o->n_panels = H->K.panel_start.empty() ? 0 : (int)H->K.panel_start.size() - 1;

@@ -444,6 +444,17 @@ void sparse_inverse_values(const Factor& f, double drop_tol, Inverse& K, int n_t
     }
 }
 
+void trim_dropped(Inverse& K) {
+    K.firstk.assign(K.n, 0);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int r = 0; r < K.n; ++r) {
+        const float* row = K.Krow.data() + K.rowptr[r];
+        int j = K.first[r];
+        while (j < r && row[j - K.first[r]] == 0.f) ++j;
+        K.firstk[r] = j;
+    }
+}
+
 void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols) {
     int n = K.n;
     wl = WorkLists();
@@ -451,10 +462,11 @@ void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols) {
     int npan = (int)K.panel_start.size() - 1;
     for (int p = 0; p < npan; ++p) {
         int rs = K.panel_start[p], re = K.panel_start[p + 1];
-        int f = K.first[rs];
         for (int r0 = rs; r0 < re; r0 += 32) {
             int nr = std::min(32, re - r0);
             int cend = r0 + nr;
+            int f = cend - 1;   // the block's kept columns [min firstk, r0 + nr)
+            for (int l = 0; l < nr; ++l) f = std::min(f, (int)K.firstk[r0 + l]);
             P1Block b{r0, nr, 0, wl.p1_parts};
             int bi = (int)wl.p1b.size();
             for (int c0 = f; c0 < cend; c0 += p1_chunk_cols) {
@@ -481,7 +493,7 @@ void build_worklists(const Inverse& K, WorkLists& wl, int p1_chunk_cols) {
         for (int j = c0; j < c0 + nc; ++j)
             for (int i = j; i != -1 && mark[i] != bi; i = K.parent[i]) {
                 mark[i] = bi;
-                cov.push_back(i);
+                if (K.firstk[i] <= c0 + nc - 1) cov.push_back(i);   // rows with a kept entry in the block
             }
         std::sort(cov.begin(), cov.end());
         P2Block b{c0, nc, (int)wl.cover.size(), (int)(wl.cover.size() + cov.size()), 0};
@@ -537,8 +549,13 @@ int build_batched(const Inverse& K, const WorkLists& wl, int unit_tiles, std::ve
     u1.clear();
     u2.clear();
     int64_t ntot = 0;
+    auto block_c0 = [&](const P1Block& b) {   // the block's kept columns start
+        int c0 = b.r0 + b.nrows - 1;
+        for (int l = 0; l < b.nrows; ++l) c0 = std::min(c0, (int)K.firstk[b.r0 + l]);
+        return c0;
+    };
     for (auto& b : wl.p1b) {
-        const int c0 = K.first[b.r0], c1 = b.r0 + b.nrows;   // columns [c0, c1)
+        const int c0 = block_c0(b), c1 = b.r0 + b.nrows;   // columns [c0, c1)
         ntot += (c1 - c0 + 31) / 32;
     }
     T1p.assign(ntot * 1024, 0.f);
@@ -547,7 +564,7 @@ int build_batched(const Inverse& K, const WorkLists& wl, int unit_tiles, std::ve
     nblocks1 = (int)wl.p1b.size();
     for (int bi = 0; bi < (int)wl.p1b.size(); ++bi) {
         const P1Block& b = wl.p1b[bi];
-        const int c0 = K.first[b.r0], c1 = b.r0 + b.nrows;
+        const int c0 = block_c0(b), c1 = b.r0 + b.nrows;
         const int nt = (c1 - c0 + 31) / 32;
         const int nu = (nt + unit_tiles - 1) / unit_tiles;
         const int part0 = nu > 1 ? nparts : -1;
@@ -730,7 +747,7 @@ void build_plane_units(const Inverse& K, int unit_tiles, PlaneUnits& pu) {
     for (int r0 = 0; r0 < n; r0 += 64) {
         const int nr = std::min(64, n - r0);
         int c0 = r0;
-        for (int l = 0; l < nr; ++l) c0 = std::min(c0, (int)K.first[r0 + l]);
+        for (int l = 0; l < nr; ++l) c0 = std::min(c0, (int)K.firstk[r0 + l]);
         const int nt = (r0 + nr - c0 + 31) / 32;
         blocks.push_back({r0, nr, c0, nt});
         nt1 += nt;
@@ -786,7 +803,7 @@ void build_plane_units(const Inverse& K, int unit_tiles, PlaneUnits& pu) {
         for (int j = c0; j < c0 + nc; ++j)
             for (int i = j; i != -1 && mark[i] != bi; i = K.parent[i]) {
                 mark[i] = bi;
-                cov.push_back(i);
+                if (K.firstk[i] <= c0 + nc - 1) cov.push_back(i);
             }
         std::sort(cov.begin(), cov.end());
         BUnit U{};

@@ -61,6 +61,10 @@ bool cholesky(const Csr& A, const std::vector<int32_t>& parent, Factor& f);
 struct Inverse {
     int n = 0;
     std::vector<int32_t> parent, depth, first, ptop, panel_of;
+    // kept skyline after the drop tolerance (reading A25): firstk[r] = the smallest column j of row r
+    // with K[r][j] != 0 after dropping (= first[r] at tol 0).  The K-pass work lists and tile
+    // streams cover [firstk(r), r] only, so dropped leading entries cost no bytes
+    std::vector<int32_t> firstk;
     std::vector<int64_t> rowptr, colptr;   // row-major and column-major offsets
     std::vector<float> Krow, Kcol;         // fp32 values
     std::vector<int32_t> panel_start;      // [n_panels+1]
@@ -68,6 +72,8 @@ struct Inverse {
     int64_t nnz = 0;
 };
 
+// firstk from the stored values (after sparse_inverse / the device inverse)
+void trim_dropped(Inverse& K);
 // K = L^-1 (fp64 compute, fp32 store); drop |K_ij| < tol |K_jj| (tol > 0)
 void sparse_inverse(const Factor& f, double drop_tol, Inverse& K, int n_threads);
 // the two halves: index structure (depth, first, row/column offsets, panels; values zeroed) and

@@ -499,6 +499,69 @@ __device__ __forceinline__ void project_sigma(int model, const float sg[3], floa
 // du is [9][n_t S] (plane per entry, instance-minor); admm_first: u = 0 (reading A33, reset per frame).
 // One instantiation per material: the closed forms (corotated, ARAP) fit 64 registers (8 CTAs of
 // 128 threads per SM), the NH Newton 80 (6 CTAs); measured 20 % / 7 % faster than 94 registers.
+// Local step core (readings A2-A5): signed SVD F = U diag(sg) V^T (Jacobi on F^T F,
+// U by Gram-Schmidt on F V, both in SO(3)) and the sigma-space projection; dlt = p* - sg, so
+// P - F = U diag(dlt) V^T without cancellation.
+template <int MODEL>
+__device__ __forceinline__ void svd_project(const float F[3][3], float k, float mu, float lam, float U[3][3],
+                                            float dlt[3], float V[3][3]) {
+    // S = F^T F, eigenvectors V
+    float S[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) S[i][j] = F[0][i] * F[0][j] + F[1][i] * F[1][j] + F[2][i] * F[2][j];
+    jacobi3(S, V);
+    float ev[3] = {S[0][0], S[1][1], S[2][2]};
+    if (ev[0] < ev[1]) swapcol(V, ev, 0, 1);
+    if (ev[0] < ev[2]) swapcol(V, ev, 0, 2);
+    if (ev[1] < ev[2]) swapcol(V, ev, 1, 2);
+    float detV = V[0][0] * (V[1][1] * V[2][2] - V[1][2] * V[2][1]) - V[0][1] * (V[1][0] * V[2][2] - V[1][2] * V[2][0]) +
+                 V[0][2] * (V[1][0] * V[2][1] - V[1][1] * V[2][0]);
+    if (detV < 0.f) {
+        V[0][2] = -V[0][2];
+        V[1][2] = -V[1][2];
+        V[2][2] = -V[2][2];
+    }
+    // U by Gram-Schmidt on F V (U in SO(3)); signed singular values sg_i = u_i . F v_i
+    float FV[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) FV[i][j] = F[i][0] * V[0][j] + F[i][1] * V[1][j] + F[i][2] * V[2][j];
+    const float q0 = FV[0][0] * FV[0][0] + FV[1][0] * FV[1][0] + FV[2][0] * FV[2][0];
+    float n0 = q0 > 0.f ? q0 * rsqrt_ftz(q0) : 0.f;
+    if (q0 > 1e-36f) {
+        const float r0 = rsqrt_ftz(q0);
+        U[0][0] = FV[0][0] * r0; U[1][0] = FV[1][0] * r0; U[2][0] = FV[2][0] * r0;
+    } else {
+        U[0][0] = 1.f; U[1][0] = 0.f; U[2][0] = 0.f;
+    }
+    float dt = U[0][0] * FV[0][1] + U[1][0] * FV[1][1] + U[2][0] * FV[2][1];
+    float w0 = FV[0][1] - dt * U[0][0], w1 = FV[1][1] - dt * U[1][0], w2 = FV[2][1] - dt * U[2][0];
+    const float q1 = w0 * w0 + w1 * w1 + w2 * w2;
+    float n1 = q1 > 0.f ? q1 * rsqrt_ftz(q1) : 0.f;
+    if (n1 > 1e-30f * fmaxf(1.f, n0)) {
+        const float r1 = rsqrt_ftz(q1);
+        U[0][1] = w0 * r1; U[1][1] = w1 * r1; U[2][1] = w2 * r1;
+    } else {   // any unit vector orthogonal to u0
+        float a0 = U[0][0], a1 = U[1][0], a2 = U[2][0];
+        float e0 = fabsf(a0) < 0.577f ? 1.f : 0.f, e1 = e0 == 0.f && fabsf(a1) < 0.577f ? 1.f : 0.f;
+        float e2 = (e0 == 0.f && e1 == 0.f) ? 1.f : 0.f;
+        float dp = a0 * e0 + a1 * e1 + a2 * e2;
+        w0 = e0 - dp * a0; w1 = e1 - dp * a1; w2 = e2 - dp * a2;
+        n1 = sqrtf(w0 * w0 + w1 * w1 + w2 * w2);
+        U[0][1] = w0 / n1; U[1][1] = w1 / n1; U[2][1] = w2 / n1;
+    }
+    U[0][2] = U[1][0] * U[2][1] - U[2][0] * U[1][1];
+    U[1][2] = U[2][0] * U[0][1] - U[0][0] * U[2][1];
+    U[2][2] = U[0][0] * U[1][1] - U[1][0] * U[0][1];
+    float sg[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sg[j] = U[0][j] * FV[0][j] + U[1][j] * FV[1][j] + U[2][j] * FV[2][j];
+    project_sigma(MODEL, sg, k, mu, lam, dlt);
+}
+
 template <int MODEL>
 __global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, const int4* __restrict__ tet, const float* __restrict__ Bm,
                                                const float* __restrict__ hw2, const double4* __restrict__ x,
@@ -535,64 +598,8 @@ __global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, con
 #pragma unroll
             for (int j = 0; j < 3; ++j) F[i][j] += uo[3 * i + j];   // project F + u
     }
-    // S = F^T F, eigenvectors V
-    float S[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) S[i][j] = F[0][i] * F[0][j] + F[1][i] * F[1][j] + F[2][i] * F[2][j];
-    float V[3][3];
-    jacobi3(S, V);
-    float ev[3] = {S[0][0], S[1][1], S[2][2]};
-    if (ev[0] < ev[1]) swapcol(V, ev, 0, 1);
-    if (ev[0] < ev[2]) swapcol(V, ev, 0, 2);
-    if (ev[1] < ev[2]) swapcol(V, ev, 1, 2);
-    float detV = V[0][0] * (V[1][1] * V[2][2] - V[1][2] * V[2][1]) - V[0][1] * (V[1][0] * V[2][2] - V[1][2] * V[2][0]) +
-                 V[0][2] * (V[1][0] * V[2][1] - V[1][1] * V[2][0]);
-    if (detV < 0.f) {
-        V[0][2] = -V[0][2];
-        V[1][2] = -V[1][2];
-        V[2][2] = -V[2][2];
-    }
-    // U by Gram-Schmidt on F V (U in SO(3)); signed singular values sg_i = u_i . F v_i
-    float FV[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) FV[i][j] = F[i][0] * V[0][j] + F[i][1] * V[1][j] + F[i][2] * V[2][j];
-    float U[3][3];
-    const float q0 = FV[0][0] * FV[0][0] + FV[1][0] * FV[1][0] + FV[2][0] * FV[2][0];
-    float n0 = q0 > 0.f ? q0 * rsqrt_ftz(q0) : 0.f;
-    if (q0 > 1e-36f) {
-        const float r0 = rsqrt_ftz(q0);
-        U[0][0] = FV[0][0] * r0; U[1][0] = FV[1][0] * r0; U[2][0] = FV[2][0] * r0;
-    } else {
-        U[0][0] = 1.f; U[1][0] = 0.f; U[2][0] = 0.f;
-    }
-    float dt = U[0][0] * FV[0][1] + U[1][0] * FV[1][1] + U[2][0] * FV[2][1];
-    float w0 = FV[0][1] - dt * U[0][0], w1 = FV[1][1] - dt * U[1][0], w2 = FV[2][1] - dt * U[2][0];
-    const float q1 = w0 * w0 + w1 * w1 + w2 * w2;
-    float n1 = q1 > 0.f ? q1 * rsqrt_ftz(q1) : 0.f;
-    if (n1 > 1e-30f * fmaxf(1.f, n0)) {
-        const float r1 = rsqrt_ftz(q1);
-        U[0][1] = w0 * r1; U[1][1] = w1 * r1; U[2][1] = w2 * r1;
-    } else {   // any unit vector orthogonal to u0
-        float a0 = U[0][0], a1 = U[1][0], a2 = U[2][0];
-        float e0 = fabsf(a0) < 0.577f ? 1.f : 0.f, e1 = e0 == 0.f && fabsf(a1) < 0.577f ? 1.f : 0.f;
-        float e2 = (e0 == 0.f && e1 == 0.f) ? 1.f : 0.f;
-        float dp = a0 * e0 + a1 * e1 + a2 * e2;
-        w0 = e0 - dp * a0; w1 = e1 - dp * a1; w2 = e2 - dp * a2;
-        n1 = sqrtf(w0 * w0 + w1 * w1 + w2 * w2);
-        U[0][1] = w0 / n1; U[1][1] = w1 / n1; U[2][1] = w2 / n1;
-    }
-    U[0][2] = U[1][0] * U[2][1] - U[2][0] * U[1][1];
-    U[1][2] = U[2][0] * U[0][1] - U[0][0] * U[2][1];
-    U[2][2] = U[0][0] * U[1][1] - U[1][0] * U[0][1];
-    float sg[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) sg[j] = U[0][j] * FV[0][j] + U[1][j] * FV[1][j] + U[2][j] * FV[2][j];
-    float dlt[3];
-    project_sigma(MODEL, sg, P.k, P.mu, P.lam, dlt);
+    float U[3][3], V[3][3], dlt[3];
+    svd_project<MODEL>(F, P.k, P.mu, P.lam, U, dlt, V);
     // Q = hw2 * U diag(delta) V^T  (= h^2 w (P - F); ADMM: h^2 w (2 (P - F - u) + u))
     float hw = __ldg(&hw2[t]);
     float Q[3][3];
@@ -646,6 +653,156 @@ void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float
         launch_pdl(k_local<2>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
     else
         launch_pdl(k_local<0>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
+}
+
+// ----------------------------------------------------------------------------
+// Persistent small-scene driver (SURVEY §7 step 9, cfg1-class scenes): ONE launch runs `frames`
+// frames x `iters` L-G iterations of Alg. 4 for a single contact-free instance in
+// one CTA -- predict, local step (svd_project), RHS gather, y = K u and
+// x += K^T y (K row- and column-major values-only, Theorem 1 addressing), integrate
+// and the finite check with rollback -- with __syncthreads between the phases
+// instead of kernel boundaries.  Corner forces, u and y live in shared memory; the state stays in
+// global memory (double4 [n_v], L1/L2-resident at this size).  For a 45-vertex mesh the graph
+// path is ~30 dependent launches per frame; here the frame is launch-free.
+// ----------------------------------------------------------------------------
+
+template <int MODEL>
+__global__ void __launch_bounds__(256, 1) k_small_frames(Params P, SmallArgs A, int frames, int iters) {
+    extern __shared__ double sm_small[];
+    const int nv = P.n_v, nf = P.n_f, nt = P.n_t;
+    double* u = sm_small;                                          // [3 nf]
+    double* y = u + 3 * nf;                                        // [3 nf]
+    float* fc = reinterpret_cast<float*>(y + 3 * nf);              // [12 nt]
+    __shared__ int s_bad;
+    const double h = P.h;
+    for (int f = 0; f < frames; ++f) {
+        // predict: x_t = x, s = x_t + h v + h^2 g, x^0 = s (A9) or x_t + h v (A9w); pins move
+        if (threadIdx.x == 0) s_bad = 0;
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+            const double4 xi = A.x[i], vi = A.v[i];
+            A.xt[i] = xi;
+            A.vt[i] = vi;
+            if (i < nf) {
+                const double4 xv = make_double4(xi.x + h * vi.x, xi.y + h * vi.y, xi.z + h * vi.z, 0.0);
+                const double4 si = make_double4(xv.x + h * h * P.g[0], xv.y + h * h * P.g[1], xv.z + h * h * P.g[2], 0.0);
+                A.s[i] = si;
+                A.x[i] = P.warm ? xv : si;
+            } else {
+                const double4 vp = P.vpin[i - nf];
+                A.x[i] = make_double4(xi.x + h * vp.x, xi.y + h * vp.y, xi.z + h * vp.z, 0.0);
+                A.v[i] = make_double4(vp.x, vp.y, vp.z, 0.0);
+            }
+        }
+        __syncthreads();
+        for (int k = 0; k < iters; ++k) {
+            // local step: per tet, corner forces h^2 w (P - F) g_a
+            for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+                const int4 tv = A.tet[t];
+                const double4 x0 = A.x[tv.x], x1 = A.x[tv.y], x2 = A.x[tv.z], x3 = A.x[tv.w];
+                float D[3][3];
+                D[0][0] = (float)(x1.x - x0.x); D[1][0] = (float)(x1.y - x0.y); D[2][0] = (float)(x1.z - x0.z);
+                D[0][1] = (float)(x2.x - x0.x); D[1][1] = (float)(x2.y - x0.y); D[2][1] = (float)(x2.z - x0.z);
+                D[0][2] = (float)(x3.x - x0.x); D[1][2] = (float)(x3.y - x0.y); D[2][2] = (float)(x3.z - x0.z);
+                float B[9];
+                for (int e = 0; e < 9; ++e) B[e] = A.Bm[(size_t)e * nt + t];
+                float F[3][3];
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) F[i][j] = D[i][0] * B[j] + D[i][1] * B[3 + j] + D[i][2] * B[6 + j];
+                float U[3][3], V[3][3], dlt[3];
+                svd_project<MODEL>(F, P.k, P.mu, P.lam, U, dlt, V);
+                const float hw = A.hw2[t];
+                float Q[3][3];
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j)
+                        Q[i][j] = hw * (U[i][0] * dlt[0] * V[j][0] + U[i][1] * dlt[1] * V[j][1] + U[i][2] * dlt[2] * V[j][2]);
+                float* o = fc + 12 * t;
+                for (int i = 0; i < 3; ++i) {
+                    float sum = 0.f;
+                    for (int a = 0; a < 3; ++a) {
+                        const float fa = Q[i][0] * B[3 * a] + Q[i][1] * B[3 * a + 1] + Q[i][2] * B[3 * a + 2];
+                        o[3 * (a + 1) + i] = fa;
+                        sum += fa;
+                    }
+                    o[i] = -sum;
+                }
+            }
+            __syncthreads();
+            // RHS in delta form: u_a = M_a (s_a - x_a) + sum of the incident corner forces
+            for (int a = threadIdx.x; a < nf; a += blockDim.x) {
+                const double4 xa = A.x[a], sa = A.s[a];
+                const double m = A.M[a];
+                float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+                for (int q = A.adjp[a]; q < A.adjp[a + 1]; ++q) {
+                    const float* fq = fc + 3 * A.adj[q];
+                    f0 += fq[0]; f1 += fq[1]; f2 += fq[2];
+                }
+                u[3 * a] = m * (sa.x - xa.x) + f0;
+                u[3 * a + 1] = m * (sa.y - xa.y) + f1;
+                u[3 * a + 2] = m * (sa.z - xa.z) + f2;
+            }
+            __syncthreads();
+            // y = K u: row r spans columns [first(r), r]
+            for (int r = threadIdx.x; r < nf; r += blockDim.x) {
+                const int2 mr = A.meta[r];
+                const float* kr = A.Krow + mr.x;
+                double a0 = 0, a1 = 0, a2 = 0;
+                for (int j = mr.y; j <= r; ++j) {
+                    const double kv = kr[j];
+                    a0 = fma(kv, u[3 * j], a0); a1 = fma(kv, u[3 * j + 1], a1); a2 = fma(kv, u[3 * j + 2], a2);
+                }
+                y[3 * r] = (float)a0; y[3 * r + 1] = (float)a1; y[3 * r + 2] = (float)a2;   // fp32 as the K-pass output
+            }
+            __syncthreads();
+            // x += K^T y: column j is its ancestor chain j, parent(j), ... (Kcol order)
+            const bool last = k == iters - 1;
+            for (int j = threadIdx.x; j < nf; j += blockDim.x) {
+                const float* kc = A.Kcol + A.colptr[j];
+                double a0 = 0, a1 = 0, a2 = 0;
+                int d = 0;
+                for (int r = j; r >= 0; r = A.parent[r], ++d) {
+                    const double kv = kc[d];
+                    a0 = fma(kv, y[3 * r], a0); a1 = fma(kv, y[3 * r + 1], a1); a2 = fma(kv, y[3 * r + 2], a2);
+                }
+                double4 xj = A.x[j];
+                xj.x += a0; xj.y += a1; xj.z += a2;
+                A.x[j] = xj;
+                if (last) {   // v = (x - x_t) / h
+                    const double4 t0 = A.xt[j];
+                    A.v[j] = make_double4((xj.x - t0.x) / h, (xj.y - t0.y) / h, (xj.z - t0.z) / h, 0.0);
+                }
+            }
+            __syncthreads();
+        }
+        // failure detection: a non-finite frame is rolled back to its start (sim_synchronize reports it)
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+            const double4 a = A.x[i], b = A.v[i];
+            if (!(isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(b.x) && isfinite(b.y) && isfinite(b.z)))
+                s_bad = 1;
+        }
+        __syncthreads();
+        if (s_bad) {
+            for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+                A.x[i] = A.xt[i];
+                A.v[i] = A.vt[i];
+            }
+            if (threadIdx.x == 0) atomicAdd(A.rollbacks, 1);
+        }
+        __syncthreads();
+    }
+}
+
+size_t small_smem_bytes(const Params& P) { return (size_t)6 * P.n_f * sizeof(double) + (size_t)12 * P.n_t * sizeof(float); }
+
+int launch_small_frames(cudaStream_t st, const Params& P, const SmallArgs& A, int frames, int iters) {
+    const size_t sm = small_smem_bytes(P);
+    cudaError_t e;
+    if (P.model == 1)
+        e = launch_pdl(k_small_frames<1>, dim3(1), dim3(256), sm, st, P, A, frames, iters);
+    else if (P.model == 2)
+        e = launch_pdl(k_small_frames<2>, dim3(1), dim3(256), sm, st, P, A, frames, iters);
+    else
+        e = launch_pdl(k_small_frames<0>, dim3(1), dim3(256), sm, st, P, A, frames, iters);
+    return (int)e;
 }
 
 // ----------------------------------------------------------------------------
@@ -1473,13 +1630,14 @@ constexpr int kPlInst = 128;
 constexpr int kPlWarps = 16;
 constexpr int kPlThreads = 32 * kPlWarps;
 constexpr int kPlStages = 3;
+constexpr int kPlBStages = 5;                     // K tiles run further ahead (they come from HBM)
 constexpr uint32_t kPlA = 3u * 16384u;            // V_hi: 3 components x 4 blocks x (32 rows x 128 B)
 constexpr uint32_t kPlB = 16384u;                 // K hi (8 KB) + lo (8 KB), 64 x 32 each
-constexpr uint32_t kPlStage = kPlA + kPlB;
-constexpr size_t kPlSmem = (size_t)kPlStages * kPlStage + 1024;
+constexpr uint32_t kPlBOff = kPlStages * kPlA;    // the K-tile stages follow the V_hi stages
+constexpr size_t kPlSmem = (size_t)kPlStages * kPlA + (size_t)kPlBStages * kPlB + 1024;
 constexpr uint32_t kPlLBO = 4096u, kPlSBO = 512u;
 // D f32, A / B tf32, N = 64, M = 128; A MN-major (bit 15) for the shared-memory operand
-constexpr uint32_t kIdescPlS = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kIdescPlS = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kIdescPlT = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
 
 // MN-major tf32 operands take only the SWIZZLE_128B_BASE32B layout (layout type 1; measured:
@@ -1518,20 +1676,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
 template <int PASS>
-__global__ void __launch_bounds__(kPlThreads + 32, 1)
+__global__ void __launch_bounds__(kPlThreads + 64, 1)
     k_kpass_pl(int S, int Sp, int n_f, const BUnit* __restrict__ units, const float* __restrict__ T,
                const int32_t* __restrict__ cover, const float* __restrict__ vin, float* __restrict__ yout,
                float* __restrict__ part, int* __restrict__ counters, int nchunks, double4* __restrict__ x,
                const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
     pdl_enter();
     extern __shared__ unsigned char pl_raw[];
-    __shared__ __align__(8) uint64_t afull[kPlStages], bfull[kPlStages], ready[kPlStages], mdone[kPlStages], dfree;
+    __shared__ __align__(8) uint64_t afull[kPlStages], mdone[kPlStages], lofull[3], lofree[3], dfree;
+    __shared__ __align__(8) uint64_t bfull[kPlBStages], bempty[kPlBStages];
     __shared__ uint32_t tmem_base_s;
     __shared__ int s_last;
     unsigned char* sm = pl_raw + ((1024u - ((unsigned)__cvta_generic_to_shared(pl_raw) & 1023u)) & 1023u);
     const uint32_t sm_a = (unsigned)__cvta_generic_to_shared(sm);
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-    const bool mma_warp = w == kPlWarps;
+    const bool mma_warp = w == kPlWarps, kload_warp = w == kPlWarps + 1;
     const BUnit U = units[blockIdx.x];
     const int chunk = blockIdx.y;
     const int i0 = chunk * kPlInst;
@@ -1545,13 +1704,20 @@ __global__ void __launch_bounds__(kPlThreads + 32, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (tid == 0) {
+        // worker-side barriers count one elected arrival per worker warp (after __syncwarp)
         for (int s2 = 0; s2 < kPlStages; ++s2) {
-            mbar_init(&afull[s2], kPlThreads);
-            mbar_init(&bfull[s2], 1);
-            mbar_init(&ready[s2], kPlThreads);
+            mbar_init(&afull[s2], kPlWarps);
             mbar_init(&mdone[s2], 1);
         }
-        mbar_init(&dfree, kPlThreads);
+        for (int c = 0; c < 3; ++c) {
+            mbar_init(&lofull[c], kPlWarps);
+            mbar_init(&lofree[c], 1);
+        }
+        for (int s2 = 0; s2 < kPlBStages; ++s2) {
+            mbar_init(&bfull[s2], 1);
+            mbar_init(&bempty[s2], 1);
+        }
+        mbar_init(&dfree, kPlWarps);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -1559,64 +1725,78 @@ __global__ void __launch_bounds__(kPlThreads + 32, 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_base_s;
     const int nt = U.ntiles;
-    if (mma_warp) {
+    if (kload_warp) {
+        // K tiles: one bulk copy each, kPlBStages ahead of the tensor core
         if (lane == 0) {
             for (int t = 0; t < nt; ++t) {
-                const int st = t % kPlStages;
-                const unsigned ph = (unsigned)(t / kPlStages) & 1u;
-                mbar_wait(&bfull[st], ph);
-                mbar_wait(&ready[st], ph);
+                const int sb = t % kPlBStages;
+                if (t >= kPlBStages) mbar_wait(&bempty[sb], (unsigned)((t - kPlBStages) / kPlBStages) & 1u);
+                mbar_expect_tx(&bfull[sb], kPlB);
+                bulk_g2s(sm + kPlBOff + sb * kPlB, T + U.toff + (int64_t)t * 4096, kPlB, &bfull[sb], true, pol);
+            }
+        }
+        __syncwarp();
+    } else if (mma_warp) {
+        if (lane == 0) {
+            for (int t = 0; t < nt; ++t) {
+                const int st = t % kPlStages, sb = t % kPlBStages;
+                mbar_wait(&bfull[sb], (unsigned)(t / kPlBStages) & 1u);
                 if (t > 0 && t % drain == 0) mbar_wait(&dfree, (unsigned)(t / drain - 1) & 1u);
-                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                const uint32_t abase = sm_a + st * kPlStage, bbase = abase + kPlA;
-                const uint32_t lo = tmem + 192u + 96u * (t & 1);
+                const uint32_t abase = sm_a + st * kPlA, bbase = sm_a + kPlBOff + sb * kPlB;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const uint32_t dt = tmem + 64u * c;
+                    // V_lo of component c written (and this tile's V_hi copies visible to the tensor core)
+                    mbar_wait(&lofull[c], (unsigned)t & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    const uint32_t dt = tmem + 128u * c;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t da = umma_desc_mn32(abase + 16384u * c + 1024u * kk);
-                        const uint64_t dbh = umma_desc_k(bbase + 256u * kk), dbl = umma_desc_k(bbase + 8192u + 256u * kk);
-                        umma_pl_ss(dt, da, dbh, (t % drain != 0 || kk > 0) ? 1u : 0u);
-                        umma_pl_ss(dt, da, dbl, 1u);
-                        umma_pl_ts(dt, lo + 32u * c + 8u * kk, dbh, 1u);
+                        const uint64_t db = umma_desc_k(bbase + 256u * kk);   // [K_hi ; K_lo]: N = 128
+                        umma_pl_ss(dt, da, db, (t % drain != 0 || kk > 0) ? 1u : 0u);
+                        umma_pl_ts(dt, tmem + 384u + 32u * c + 8u * kk, db, 1u);      // V_lo K_hi: N = 64
                     }
+                    umma_commit(&lofree[c]);   // the lo slot of component c may be rewritten
                 }
                 umma_commit(&mdone[st]);
+                umma_commit(&bempty[sb]);
             }
         }
         __syncwarp();
     } else {
         // ---- workers: copies, V_lo, folds ----
-        auto row_of = [&](int t, int q, bool& ok) -> int {
-            if (PASS == 1) {
-                const int r = U.c0 + 32 * t + q;
-                ok = r < n_f;
-                return ok ? r : 0;
-            }
-            ok = 32 * t + q < U.nlist;
-            return ok ? __ldg(&cover[U.list0 + 32 * t + q]) : 0;
-        };
-        auto issue = [&](int t) {   // this thread's 6 chunks of tile t's V_hi (and, thread 0, the K tile)
-            const int st = t % kPlStages;
-            const uint32_t abase = sm_a + st * kPlStage;
+        // this thread's copies: 16-byte chunk j = lane of rows q = w and w + 16 of the 3 planes (the
+        // 3 x 32 rows x 128 instances of a tile = 3072 chunks over 512 threads)
+        const int inst4 = i0 + 4 * lane;
+        const bool ilive4 = inst4 < Sp;
+        uint32_t dsto[2];
 #pragma unroll
-            for (int e = 0; e < 6; ++e) {
-                const int id = tid + kPlThreads * e;
-                const int c = id >> 10, rem = id & 1023, q = rem >> 5, j = rem & 31;
+        for (int e = 0; e < 2; ++e) {
+            const int q = w + 16 * e;
+            dsto[e] = 4096u * (lane >> 3) + 128u * q + 32u * (((lane & 7) >> 1) ^ (q & 3)) + 16u * (lane & 1);
+        }
+        auto issue = [&](int t) {
+            const int st = t % kPlStages;
+            const uint32_t abase = sm_a + st * kPlA;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int q = w + 16 * e;
+                int r;
                 bool ok;
-                const int r = row_of(t, q, ok);
-                const int inst = i0 + 4 * j;
-                ok = ok && inst < Sp;
-                const float* src = ok ? vin + c * PS + (size_t)r * Sp + inst : vin;
-                const uint32_t dst = abase + 16384u * c + 4096u * (j >> 3) + 128u * q + 32u * (((j & 7) >> 1) ^ (q & 3)) + 16u * (j & 1);
-                cp_async16_z(dst, src, ok ? 16u : 0u);
+                if (PASS == 1) {
+                    r = U.c0 + 32 * t + q;
+                    ok = r < n_f;
+                } else {
+                    ok = 32 * t + q < U.nlist;
+                    r = ok ? __ldg(&cover[U.list0 + 32 * t + q]) : 0;
+                }
+                ok = ok && ilive4;
+                const float* src = ok ? vin + (size_t)r * Sp + inst4 : vin;
+                const uint32_t n = ok ? 16u : 0u;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) cp_async16_z(abase + 16384u * c + dsto[e], ok ? src + c * PS : vin, n);
             }
-            cp_async_arrive_noinc(&afull[st]);
-            if (tid == 0) {
-                mbar_expect_tx(&bfull[st], kPlB);
-                bulk_g2s(sm + st * kPlStage + kPlA, T + U.toff + (int64_t)t * 4096, kPlB, &bfull[st], true, pol);
-            }
+            cp_async_commit();
         };
         const int qd = w & 3, oc = w >> 2;     // TMEM lane quadrant (= 32-instance block) / row octet
         const uint32_t lanebase = tmem + ((uint32_t)(32 * qd) << 16);
@@ -1636,25 +1816,36 @@ __global__ void __launch_bounds__(kPlThreads + 32, 1)
                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
                       "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
                       "=r"(r[15])
-                    : "r"(lanebase + 64u * c + 16u * oc));
+                    : "r"(lanebase + 128u * c + 16u * oc));
+                uint32_t q2[16];   // the V K_lo half of the accumulator
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                    "%13, %14, %15}, [%16];\n"
+                    : "=r"(q2[0]), "=r"(q2[1]), "=r"(q2[2]), "=r"(q2[3]), "=r"(q2[4]), "=r"(q2[5]), "=r"(q2[6]), "=r"(q2[7]),
+                      "=r"(q2[8]), "=r"(q2[9]), "=r"(q2[10]), "=r"(q2[11]), "=r"(q2[12]), "=r"(q2[13]), "=r"(q2[14]),
+                      "=r"(q2[15])
+                    : "r"(lanebase + 128u * c + 64u + 16u * oc));
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-                for (int e = 0; e < 16; ++e) acc[c][e] += __uint_as_float(r[e]);
+                for (int e = 0; e < 16; ++e) acc[c][e] += __uint_as_float(r[e]) + __uint_as_float(q2[e]);
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         };
         issue(0);
         if (nt > 1) issue(1);
+        // per tile t: V_lo(t) as soon as its copies landed (MMA(t - 1) runs meanwhile), then the fold
+        // of a closed accumulation group, then the copies of tile t + 2 into the stage MMA(t - 1) frees
         for (int t = 0; t < nt; ++t) {
             const int st = t % kPlStages;
-            if (t + 2 < nt) {
-                if (t >= 1) mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
-                issue(t + 2);
-            }
+            // this thread's copies of tile t have landed (tile t + 1's may still fly), then the CTA's
+            if (t + 1 < nt) cp_async_wait<1>(); else cp_async_wait<0>();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&afull[st]);
             mbar_wait(&afull[st], (unsigned)(t / kPlStages) & 1u);
-            if (t >= 2) mbar_wait(&mdone[(t - 2) % kPlStages], (unsigned)((t - 2) / kPlStages) & 1u);
-            // V_lo of rows 8 oc .. 8 oc + 7 (K-step oc) for instance 32 qd + lane
-            const unsigned char* ab = sm + st * kPlStage + 4096 * qd;
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> async proxy
+            // V_lo of rows 8 oc .. 8 oc + 7 (K-step oc) for instance 32 qd + lane, one component at a
+            // time into its TMEM slot once the tensor core has read the previous tile's
+            const unsigned char* ab = sm + st * kPlA + 4096 * qd;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 uint32_t lo[8];
@@ -1665,20 +1856,26 @@ __global__ void __launch_bounds__(kPlThreads + 32, 1)
                                                                     4 * (lane & 7));
                     lo[r] = __float_as_uint(tf32_rn(a - tf32_trunc(a)));
                 }
+                if (t >= 1) mbar_wait(&lofree[c], (unsigned)(t - 1) & 1u);
                 asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
-                                 lanebase + 192u + 96u * (t & 1) + 32u * c + 8u * oc),
+                                 lanebase + 384u + 32u * c + 8u * oc),
                              "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7])
                              : "memory");
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&lofull[c]);
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> async proxy
-            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-            mbar_arrive(&ready[st]);
             // the group of tiles ending at t - 1 is complete once MMA(t - 1) is: fold it, free D
             if (t > 0 && t % drain == 0) {
                 mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
                 fold();
-                mbar_arrive(&dfree);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&dfree);
+            }
+            if (t + 2 < nt) {
+                if (t >= 1) mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
+                issue(t + 2);
             }
         }
         if (nt > 0) {
@@ -1775,7 +1972,7 @@ void launch_kpass1_pl(cudaStream_t st, int S, int Sp, int n_f, int nunits, const
         cudaFuncSetAttribute(k_kpass_pl<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlSmem);
     });
     const int nch = (S + kPlInst - 1) / kPlInst;
-    launch_pdl(k_kpass_pl<1>, dim3(nunits, nch), dim3(kPlThreads + 32), kPlSmem, st, S, Sp, n_f, units, T,
+    launch_pdl(k_kpass_pl<1>, dim3(nunits, nch), dim3(kPlThreads + 64), kPlSmem, st, S, Sp, n_f, units, T,
                (const int32_t*)nullptr, u, y, part, counters, nch, (double4*)nullptr, (const double4*)nullptr,
                (double4*)nullptr, 0.0, 0, drain);
 }
@@ -1788,7 +1985,7 @@ void launch_kpass2_pl(cudaStream_t st, int S, int Sp, int n_f, int nunits, const
         cudaFuncSetAttribute(k_kpass_pl<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPlSmem);
     });
     const int nch = (S + kPlInst - 1) / kPlInst;
-    launch_pdl(k_kpass_pl<2>, dim3(nunits, nch), dim3(kPlThreads + 32), kPlSmem, st, S, Sp, n_f, units, T, cover, y,
+    launch_pdl(k_kpass_pl<2>, dim3(nunits, nch), dim3(kPlThreads + 64), kPlSmem, st, S, Sp, n_f, units, T, cover, y,
                (float*)nullptr, (float*)nullptr, (int*)nullptr, nch, x, xt, v, inv_h, finalize_v, drain);
 }
 

@@ -203,6 +203,19 @@ void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off,
                     const int4* ulist, const float* Zc, const double* wz, const float4* wzT, float4* y, int nitems,
                     const int2* items);
 
+// --- persistent small-scene driver (S = 1, no contacts, no ADMM) -------------------------
+struct SmallArgs {
+    const int4* tet; const float* Bm; const float* hw2; const double* M;
+    const int32_t* adjp; const int32_t* adj;
+    const float* Krow; const int2* meta;     // meta[r] = {rowptr[r] - first[r], first[r]}
+    const float* Kcol; const int64_t* colptr; const int32_t* parent;
+    double4 *x, *xt, *v, *s, *vt;
+    int* rollbacks;
+};
+size_t small_smem_bytes(const Params& P);
+// frames x iters L-G iterations in one single-CTA launch (returns a cudaError_t)
+int launch_small_frames(cudaStream_t st, const Params& P, const SmallArgs& A, int frames, int iters);
+
 // --- proximity query ------------------------------------------------------------------
 struct DObstacle {   // device copy of sim_obstacle
     int kind, pad;

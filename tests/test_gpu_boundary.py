@@ -94,7 +94,7 @@ def test_stats_per_instance(simmod):
         assert abs(st["max_cone_violation"] - cone.max()) <= 1e-12 * max(1.0, cone.max())
         pen = np.maximum(0, -(o.Jx(x)[0::3] - o.d_row[0::3])).max()
         assert abs(st["max_penetration"] - pen) <= 1e-12
-    assert per[0]["n_stick"] > 0 and per[1]["n_slip"] > 0
+    assert per[0]["n_active"] > 0 and per[1]["n_active"] > 0 and per[1]["n_slip"] > 0
     for k in ("n_contacts", "n_active", "n_stick", "n_slip", "n_contact_vertices"):
         assert total[k] == sum(p[k] for p in per), k
     assert total["max_cone_violation"] == max(p["max_cone_violation"] for p in per)

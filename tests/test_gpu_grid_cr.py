@@ -15,6 +15,7 @@ import pytest
 
 import scenes
 from oracle import oracle as O
+import _parity
 
 try:
     from paper_2503_15078_b200._lib import debug_contact_state
@@ -84,8 +85,10 @@ def test_grid_and_cluster_cr_agree_on_cfg3(simmod):
 
 @pytest.mark.parametrize("mode", [0, 2])
 def test_small_pile_parity(simmod, mode):
-    """Pile of 9 cubes (3^3 cells: 2x2 stacks of 2 + 1 bridge), ground and soft-soft rows:
-    positions within 1e-5 bbox of the oracle every re-synced frame; same active set."""
+    """Pile of 9 cubes (3^3 cells: 2x2 stacks of 2 + 1 bridge), ground and soft-soft rows, 6
+    re-synced frames: every L-G iteration within 1e-5 bbox of the oracle's iteration from the
+    GPU's iterate, the frame within 1e-5 bbox (3x on frames the oracle itself shows
+    ill-conditioned, tests/_parity.py), identical A21 classification outside the band."""
     sc = scenes.pile(cells=3, nx=2, layers=2)
     assert any(len(c.verts) == 4 for c in sc.contacts)
     s = make(simmod, sc, mode)
@@ -94,16 +97,13 @@ def test_small_pile_parity(simmod, mode):
     tol = 1e-5 * sc.mesh.bbox_diag()
     x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
     for f in range(6):
-        s.set_state(x, v)
-        s.step(1, 5)
+        its = _parity.gpu_iterates(s, x, v, 5)
+        _parity.assert_iteration_parity(o, x, v, None, its, tol)
         xg, vg = s.get_state()
         xo, vo, info = o.frame(x, v)
-        err = float(np.abs(xg - xo).max())
-        assert err < tol, (f, err, tol)
-        lg = s.get_lambda()
-        act_o = info["lam"][0::3] > 0
-        act_g = lg[0::3] > 0
-        assert (act_o == act_g).mean() > 0.97, (f, (act_o != act_g).sum())
+        _parity.assert_frame_parity_conditioned(o, x, v, xg, xo, tol, what=f)
+        bad, n = _parity.classification_mismatches(o, xg, x, s.get_lambda(), xo, info["lam"], tol)
+        assert bad == 0 and n > 0, (f, bad, n)
         x, v = xg, vg
 
 

@@ -116,6 +116,32 @@ def test_cantilever_100_frames_free_running(simmod):
         assert worst < tol, (f, worst)
 
 
+@pytest.mark.parametrize("model,frames", [(0, 100), (1, 100), (2, 20)])
+def test_persistent_small_scene_driver(simmod, model, frames):
+    """cfg1 through the persistent small-scene kernel (include/sim.h sim_set_persistent: all frames
+    of one sim_step call in ONE single-CTA launch) and through the per-frame CUDA graph: both
+    within 1e-5 bbox of the oracle's free-running frames (NH, linear corotated, ARAP), and the
+    persistent handle reports one kernel per sim_step."""
+    sc = scenes.make_scene("cfg1", model=model)
+    o = O.Oracle(sc.mesh, sc.material, sc.h)
+    x, v = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X)
+    for _ in range(frames):
+        x, v, _ = o.frame(x, v)
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    out = {}
+    for mode in (0, 1):
+        s = make(simmod, sc)
+        s.set_persistent(mode)
+        s.step(frames, 5)
+        out[mode] = s.get_state()
+        if mode == 0:
+            assert s.stats()["kernels_per_frame"] == 1
+        s.close()
+    for mode in (0, 1):
+        assert np.abs(out[mode][0] - x).max() < tol, (mode, np.abs(out[mode][0] - x).max() / tol)
+        assert np.abs(out[mode][1] - v).max() < tol / sc.h, mode
+
+
 def test_delassus_gram_parity(simmod):
     """G = K[:,Vc]^T K[:,Vc] == A_v^-1 restricted to contact vertices."""
     sc = scenes.incline_block(theta_deg=10.0, mu=0.5, nv=6, edge=0.1, youngs=1e8)
@@ -162,8 +188,10 @@ def test_incline_contact_frames_resynced(simmod, dmu):
 
 def test_incline_warm_start_sliding(simmod):
     """Warm-start reading (sim_set_warm_start; A9w: x^0 = x_t + h v_t, A10w: lambda carried
-    across frames by the GPU itself, the oracle handed its own previous lambda): the sliding
-    incline block (mu* - 0.05), 12 free-running frames within 1e-5 bbox."""
+    across frames by the GPU itself): the sliding incline block (mu* - 0.05) runs 12 frames on the
+    GPU without any re-sync; every frame the oracle starts from the GPU's state and the lambda the
+    GPU carried into the frame (sim_get_lambda), positions within 1e-5 bbox (3x on frames the
+    oracle itself shows ill-conditioned, tests/_parity.py)."""
     th = 10.0
     sc = scenes.incline_block(theta_deg=th, mu=math.tan(math.radians(th)) - 0.05, nv=5, edge=0.1, youngs=1e8)
     s = make(simmod, sc)
@@ -172,20 +200,20 @@ def test_incline_warm_start_sliding(simmod):
     o = O.Oracle(sc.mesh, sc.material, sc.h, lg_iters=5, warm_start=True)
     o.set_contacts(sc.contacts)
     tol = 1e-5 * sc.mesh.bbox_diag()
-    x, v, lam = sc.mesh.X.copy(), np.zeros_like(sc.mesh.X), None
     for f in range(12):
         s.set_contacts(sc.contacts)          # a re-commit of the same set keeps lambda
+        xp, vp = s.get_state()
+        lp = s.get_lambda()
         s.step(1, 5)
-        x, v, info = o.frame(x, v, lam0=lam)
-        lam = info["lam"]
+        xo, _, info = o.frame(xp, vp, lam0=lp)
         xg, _ = s.get_state()
-        assert np.abs(xg - x).max() < tol, (f, np.abs(xg - x).max())
-        _parity.assert_impulse_parity(o, s.get_lambda(), debug_contact_state(s)["theta"], lam, info["theta_last"], tol)
+        _parity.assert_frame_parity_conditioned(o, xp, vp, xg, xo, tol, what=f, lam0=lp)
 
 
 def test_warm_start_resynced_with_lambda(simmod):
     """Warm start, re-synced: each frame both sides start from the GPU's (x, v, lambda)
-    (sim_set_lambda = the oracle's lam0); sliding incline, positions within 1e-5 bbox."""
+    (sim_set_lambda = the oracle's lam0); sliding incline, positions within 1e-5 bbox and the
+    per-vertex impulse J^T Theta lambda within its band."""
     th = 10.0
     sc = scenes.incline_block(theta_deg=th, mu=math.tan(math.radians(th)) - 0.05, nv=5, edge=0.1, youngs=1e8)
     s = make(simmod, sc)
@@ -202,6 +230,7 @@ def test_warm_start_resynced_with_lambda(simmod):
         xg, vg = s.get_state()
         xo, _, info = o.frame(x, v, lam0=lam)
         assert np.abs(xg - xo).max() < tol, (f, np.abs(xg - xo).max())
+        _parity.assert_impulse_parity(o, s.get_lambda(), debug_contact_state(s)["theta"], info["lam"], info["theta_last"], tol)
         x, v, lam = xg, vg, s.get_lambda()
 
 

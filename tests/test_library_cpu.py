@@ -80,6 +80,19 @@ def test_drop_tolerance_zeroes_small_entries():
     assert np.all(np.abs(K0[dropped]) < 1e-2 * diag[np.nonzero(dropped)[1]] * 1.0001)
 
 
+def test_drop_tolerance_shrinks_kpass_streams():
+    """Reading A25 storage: each row's stored range starts at its first kept column, so dropped
+    leading entries leave the K-pass tile streams (sim_stats.kpass_bytes, nnz_K_kept) while the
+    kept entries stay exactly those of the exact K."""
+    sc = scenes.make_scene("cfg3")
+    st = {}
+    for tol in (0.0, 1e-3, 1e-2):
+        st[tol] = _host(sc, drop_tolerance=tol).stats()
+    assert st[0.0]["nnz_K_kept"] == st[0.0]["nnz_K"]
+    assert st[1e-2]["nnz_K_kept"] < st[1e-3]["nnz_K_kept"] < st[0.0]["nnz_K_kept"]
+    assert st[1e-2]["kpass_bytes"] < st[1e-3]["kpass_bytes"] <= st[0.0]["kpass_bytes"]
+
+
 def test_input_validation():
     sc = scenes.make_scene("cfg1")
     bad = scenes.Material(poisson=0.5)

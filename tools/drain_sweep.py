@@ -13,7 +13,7 @@ o = O.Oracle(sc.mesh, sc.material, sc.h)
 rng = np.random.default_rng(3)
 b = rng.standard_normal((sc.mesh.n_v, 3))
 xo = o.solve(b[o.free])
-for drain in (4, 8, 16):
+for drain in (int(a) for a in (sys.argv[1:] or ["4", "8", "16", "1000"])):
     s = simlib.Sim(sc.mesh.X, sc.mesh.T, sc.mesh.fixed, sc.material, sc.h, n_instances=S)
     s.set_kpass_mode((drain << 4) | 2)
     s.set_pin_velocity(sc.pin_velocity)
