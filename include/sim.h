@@ -338,6 +338,12 @@ int sim_set_schur_reuse(sim_handle *h, int32_t on);
  * graph path); 1 = always the per-frame CUDA graph.  Same method and readings; results agree with
  * the graph path to fp32 rounding (different accumulation order).  SIM_E_INVALID on other values. */
 int sim_set_persistent(sim_handle *h, int32_t mode);
+
+/* Local step with n_instances > 1: 0 (default) = when n_instances is even, one thread computes a tet
+ * for two instances with packed FP32 (FFMA2 / FMUL2 / FADD2) in lockstep; 1 = one thread per
+ * tet-instance (scalar FP32).  Same formulas; results agree to fp32 rounding (FMA contraction order).
+ * ADMM-PD always uses the scalar kernel.  SIM_E_INVALID on other values. */
+int sim_set_local_mode(sim_handle *h, int32_t mode);
 int sim_get_kernel_times(sim_handle *h, double *out, int32_t capacity);
 
 void sim_destroy(sim_handle *h);         /* NULL-safe */
@@ -384,6 +390,9 @@ int sim_debug_get_delassus(sim_handle *h, int32_t instance, int32_t *cv, float *
  * D_jj per contact ([n_contacts]).  Any pointer may be NULL. */
 int sim_debug_contact_state(sim_handle *h, int32_t instance, double *theta, double *cdiag, double *hvec,
                             double *dxt, int32_t *slot_vertex, double *djj);
+/* Schur right-hand side rho = h - Theta J x~ (the CR's input) of the most recent L-G iteration,
+ * [3 * n_contacts] (rows n, t1, t2; bilateral contacts pad rows 1-2 with 0).  Test hook. */
+int sim_debug_contact_rho(sim_handle *h, int32_t instance, double *rho);
 /* Phase timestamps (us since the CR kernel started) of the most recent CR
  * solve: [1] rho built, [2] active set + G_A gathered, [3 + it] after CR
  * iteration it, [20] loop end, [21] epilogue end.  out must hold 32 doubles. */

@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = [
     "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
     "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison", "sim_get_positions_async",
     "sim_wait_positions", "sim_detect_contacts", "sim_get_contacts",
-    "sim_set_schur_reuse", "sim_set_lambda", "sim_set_pins", "sim_set_allocator", "sim_set_warm_start", "sim_set_persistent",
+    "sim_set_schur_reuse", "sim_set_lambda", "sim_set_pins", "sim_set_allocator", "sim_set_warm_start", "sim_set_persistent", "sim_set_local_mode", "sim_debug_contact_rho",
 ]
 KERNEL_KINDS = ["predict", "contact_eval", "local", "gather", "kpass1", "chain_dot", "cr", "scatter", "kpass2", "active"]
 
@@ -161,6 +161,7 @@ def _load():
         "sim_set_admm": [H, C.c_int32],
         "sim_set_warm_start": [H, C.c_int32],
         "sim_set_persistent": [H, C.c_int32],
+        "sim_set_local_mode": [H, C.c_int32],
         "sim_set_kpass_mode": [H, C.c_int32],
         "sim_debug_poison": [H, C.c_int32],
         "sim_get_positions_async": [H, C.c_void_p],
@@ -171,6 +172,7 @@ def _load():
                                 C.c_double, C.POINTER(C.c_int32)],
         "sim_get_kernel_times": [H, dp, C.c_int32],
         "sim_debug_contact_state": [H, C.c_int32, dp, dp, dp, dp, ip, dp],
+        "sim_debug_contact_rho": [H, C.c_int32, dp],
         "sim_debug_cr_timeline": [H, dp],
     }
     for name, args in sig.items():
@@ -424,6 +426,10 @@ class Sim:
         True x^0 = x_t + h v_t, lambda carried from the previous frame (A9w/A10w)."""
         _check(lib.sim_set_warm_start(self._h, 1 if on else 0))
 
+    def set_local_mode(self, mode: int):
+        """Local step with several instances (sim_set_local_mode): 0 packed-FP32 instance pairs, 1 scalar."""
+        _check(lib.sim_set_local_mode(self._h, int(mode)))
+
     def set_persistent(self, mode: int):
         """Small-scene driver (sim_set_persistent): 0 auto (one persistent kernel per sim_step for
         small contact-free single-instance scenes), 1 always the per-frame CUDA graph."""
@@ -505,6 +511,13 @@ def debug_contact_state(sim, instance=0):
     _check(lib.sim_debug_contact_state(sim._h, int(instance), _dptr(th), _dptr(cd), _dptr(hv), _dptr(dxt),
                                        sv.ctypes.data_as(C.POINTER(C.c_int32)), _dptr(djj)))
     return {"theta": th, "cdiag": cd, "hvec": hv, "dxt": dxt[:ns], "slot_vertex": sv[:ns], "djj": djj[:nc]}
+
+
+def debug_contact_rho(sim, instance=0):
+    """Schur right-hand side of the last L-G iteration (sim_debug_contact_rho), per-contact triples."""
+    out = np.empty(max(1, 3 * sim._nc[instance]))
+    _check(lib.sim_debug_contact_rho(sim._h, int(instance), _dptr(out)))
+    return out[:3 * sim._nc[instance]]
 
 
 def debug_cr_timeline(sim):

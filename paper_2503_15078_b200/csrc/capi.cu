@@ -330,6 +330,7 @@ struct sim_handle {
     int admm = 0;                    // ADMM-PD local-global (sim_set_admm)
     int warm = 0;                    // frame start (sim_set_warm_start): readings A9/A10 or A9w/A10w
     int persistent = 0;              // sim_set_persistent: 0 auto (small contact-free scenes), 1 off
+    int local_mode = 0;              // sim_set_local_mode: 0 packed-FP32 instance pairs when S is even, 1 scalar
     bool last_persistent = false;    // the last sim_step ran the persistent small-scene kernel
     DBuf<float> du;                  // ADMM dual, [9][n_t S]
     bool grid = false;               // the committed contact set uses the grid CR
@@ -1030,7 +1031,7 @@ static InstOff inst_off(sim_handle* H) {
 }
 static ClassSlots class_slots(sim_handle* H) { return ClassSlots{H->cvtx.p, H->ccls.p}; }
 static Slots slots(sim_handle* H) { return Slots{H->slot_vtx.p, H->slot_inst.p, H->scp.p, H->sci.p, H->scw.p}; }
-static CrContacts cr_contacts(sim_handle* H) { return CrContacts{H->cc9.p, H->cs0.p, H->cv0.p, H->cc1.p}; }
+static CrContacts cr_contacts(sim_handle* H) { return CrContacts{H->cc9.p, H->dc.p, H->cs0.p, H->cv0.p, H->cc1.p}; }
 
 static GcrData gcr_data(sim_handle* H) {
     GcrData g;
@@ -1073,6 +1074,7 @@ static Params make_params(const sim_handle* H) {
     P.len_scale = H->len_scale;
     P.warm = H->warm;
     P.precond = H->precond;
+    P.pair_local = H->local_mode == 0 ? 1 : 0;
     return P;
 }
 
@@ -1707,6 +1709,13 @@ extern "C" int sim_set_warm_start(sim_handle* H, int32_t on) {
     return SIM_OK;
 }
 
+extern "C" int sim_set_local_mode(sim_handle* H, int32_t mode) {
+    if (!H) return fail(SIM_E_INVALID, "null handle");
+    if (mode != 0 && mode != 1) return fail(SIM_E_INVALID, "mode must be 0 (paired) or 1 (scalar)");
+    H->local_mode = mode;
+    return SIM_OK;
+}
+
 extern "C" int sim_set_persistent(sim_handle* H, int32_t mode) {
     if (!H) return fail(SIM_E_INVALID, "null handle");
     if (mode != 0 && mode != 1) return fail(SIM_E_INVALID, "mode must be 0 (auto) or 1 (graph only)");
@@ -1805,7 +1814,7 @@ extern "C" int sim_step(sim_handle* H, int32_t frames, int32_t iters) {
     H->last_persistent = false;
     const std::vector<int64_t> key = {iters, H->C, H->NS, H->nc_max, H->ns_max, H->urows_max, H->profiling,
                                       H->contact_gen, H->NCL, H->CS, H->n_it_cd, H->n_it_sc, H->grid, H->NG,
-                                      H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain, H->cr_mode, H->warm,
+                                      H->ncp, H->precond, H->admm, H->kpass_mode, H->tc_drain, H->cr_mode, H->warm, H->local_mode,
                                       H->tc_contact};
     if (!H->gexec || key != H->gkey) {
         if (H->gexec) {
@@ -2304,6 +2313,20 @@ extern "C" int sim_debug_contact_state(sim_handle* H, int32_t inst, double* thet
         CK(cudaMemcpy(hc.data(), H->dc.p + cb, nc * sizeof(DContact), cudaMemcpyDeviceToHost));
         for (int c = 0; c < nc; ++c) djj[c] = hc[c].Djj;
     }
+    return SIM_OK;
+}
+
+// Schur right-hand side rho = h - Theta J x~ of the most recent L-G iteration ([3 * n_contacts], rows
+// n, t1, t2 per contact; bilateral contacts pad rows 1-2 with 0): the input of that iteration's CR
+extern "C" int sim_debug_contact_rho(sim_handle* H, int32_t inst, double* rho) {
+    int rc = check_instance(H, inst);
+    if (rc) return rc;
+    if (!rho) return fail(SIM_E_INVALID, "null argument");
+    if (H->dirty || H->dev_pending) return fail(SIM_E_STATE, "contacts changed since the last step");
+    CK(cudaStreamSynchronize(H->stream));
+    const InstContacts& I = H->ic[inst];
+    const size_t m = 3 * I.hc.size();
+    if (m) CK(cudaMemcpy(rho, H->rho.p + 3 * (size_t)H->coff_h[inst], m * sizeof(double), cudaMemcpyDeviceToHost));
     return SIM_OK;
 }
 

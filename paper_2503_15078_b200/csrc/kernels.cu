@@ -644,8 +644,335 @@ __global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, con
     }
 }
 
+// ----------------------------------------------------------------------------
+// Paired local step (S > 1, S even, plain PD): one thread computes the same tet for two
+// instances with Blackwell's packed FP32 (FFMA2 / FMUL2 / FADD2 on float2 pairs), halving the
+// FP32 instructions of the SVD and the projection, which issue-bound the scalar kernel.  The two
+// lanes run in lockstep: a lane that has converged (Jacobi sweep, Newton step, line search)
+// takes a null update (rotation t = 0, step dd = 0), which leaves its values exactly as the
+// scalar kernel's early exit would; per-lane MUFU (rcp, rsqrt, lg2) stay scalar.
+// ----------------------------------------------------------------------------
+struct v2 {
+    float2 a;
+    __device__ __forceinline__ v2() {}
+    __device__ __forceinline__ v2(float s) : a(make_float2(s, s)) {}
+    __device__ __forceinline__ v2(float x, float y) : a(make_float2(x, y)) {}
+    __device__ __forceinline__ v2(float2 q) : a(q) {}
+};
+__device__ __forceinline__ v2 operator+(v2 p, v2 q) { return v2(__fadd2_rn(p.a, q.a)); }
+__device__ __forceinline__ v2 operator-(v2 p, v2 q) { return v2(__ffma2_rn(q.a, make_float2(-1.f, -1.f), p.a)); }
+__device__ __forceinline__ v2 operator*(v2 p, v2 q) { return v2(__fmul2_rn(p.a, q.a)); }
+__device__ __forceinline__ v2 fma2(v2 p, v2 q, v2 r) { return v2(__ffma2_rn(p.a, q.a, r.a)); }   // p q + r
+__device__ __forceinline__ v2 rcp2(v2 p) { return v2(rcp_ftz(p.a.x), rcp_ftz(p.a.y)); }
+__device__ __forceinline__ v2 rsqrt2(v2 p) { return v2(rsqrt_ftz(p.a.x), rsqrt_ftz(p.a.y)); }
+__device__ __forceinline__ v2 log2v(v2 p) { return v2(log_ftz(p.a.x), log_ftz(p.a.y)); }
+__device__ __forceinline__ v2 abs2(v2 p) { return v2(fabsf(p.a.x), fabsf(p.a.y)); }
+__device__ __forceinline__ v2 sel2(bool bx, bool by, v2 p, v2 q) { return v2(bx ? p.a.x : q.a.x, by ? p.a.y : q.a.y); }
+
+__device__ __forceinline__ void jacobi3_2(v2 S[3][3], v2 V[3][3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) V[i][j] = v2(i == j ? 1.f : 0.f);
+#pragma unroll 1
+    for (int sweep = 0; sweep < SIM_JACOBI_SWEEPS; ++sweep) {
+        const v2 off = abs2(S[0][1]) + abs2(S[0][2]) + abs2(S[1][2]);
+        const v2 dia = abs2(S[0][0]) + abs2(S[1][1]) + abs2(S[2][2]);
+        const bool cx = off.a.x <= 1e-9f * dia.a.x, cy = off.a.y <= 1e-9f * dia.a.y;   // lane converged
+        if (cx && cy) break;
+#pragma unroll
+        for (int pq = 0; pq < 3; ++pq) {
+            const int p = pq == 2 ? 1 : 0;
+            const int q = pq == 0 ? 1 : 2;
+            const int r = 3 - p - q;
+            const v2 apq = S[p][q];
+            const bool rx = !cx && fabsf(apq.a.x) > 1e-30f, ry = !cy && fabsf(apq.a.y) > 1e-30f;   // rotate this lane
+            const v2 theta = (S[q][q] - S[p][p]) * rcp2(v2(2.f) * apq);
+            const v2 at = abs2(theta);
+            const v2 w = fma2(theta, theta, v2(1.f));
+            v2 t = rcp2(fma2(w, rsqrt2(w), at));
+            if (at.a.x > 1e15f) t.a.x = 0.5f * rcp_ftz(at.a.x);
+            if (at.a.y > 1e15f) t.a.y = 0.5f * rcp_ftz(at.a.y);
+            t = sel2(theta.a.x < 0.f, theta.a.y < 0.f, v2(-t.a.x, -t.a.y), t);
+            t = sel2(rx, ry, t, v2(0.f));   // null rotation (c = 1, s = 0) for a lane that skips
+            const v2 c = rsqrt2(fma2(t, t, v2(1.f)));
+            const v2 sn = t * c;
+            const v2 ta = t * apq;
+            S[p][p] = S[p][p] - ta;
+            S[q][q] = S[q][q] + ta;
+            S[p][q] = S[q][p] = sel2(rx, ry, v2(0.f), apq);
+            const v2 srp = S[r][p], srq = S[r][q];
+            S[r][p] = S[p][r] = fma2(c, srp, v2(0.f) - sn * srq);
+            S[r][q] = S[q][r] = fma2(sn, srp, c * srq);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const v2 vkp = V[k][p], vkq = V[k][q];
+                V[k][p] = fma2(c, vkp, v2(0.f) - sn * vkq);
+                V[k][q] = fma2(sn, vkp, c * vkq);
+            }
+        }
+    }
+}
+
+// lane-wise column swap of V and the eigenvalue list (the descending sort of the scalar kernel)
+__device__ __forceinline__ void swapcol2(v2 V[3][3], v2* e, int a, int b, bool sx, bool sy) {
+    const v2 ea = e[a], eb = e[b];
+    e[a] = sel2(sx, sy, eb, ea);
+    e[b] = sel2(sx, sy, ea, eb);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const v2 u = V[k][a], w = V[k][b];
+        V[k][a] = sel2(sx, sy, w, u);
+        V[k][b] = sel2(sx, sy, u, w);
+    }
+}
+
+__device__ __forceinline__ v2 nh_f2(const v2 p[3], const v2 sg[3], v2 k, v2 mu, v2 lam, v2 lnJ) {
+    const v2 d0 = p[0] - sg[0], d1 = p[1] - sg[1], d2 = p[2] - sg[2];
+    const v2 dd = fma2(d0, d0, fma2(d1, d1, d2 * d2));
+    const v2 pp = fma2(p[0], p[0], fma2(p[1], p[1], p[2] * p[2])) - v2(3.f);
+    return fma2(v2(0.5f) * k, dd, fma2(v2(0.5f) * mu, pp, fma2(v2(0.5f) * lam, lnJ * lnJ, v2(0.f) - mu * lnJ)));
+}
+
+template <int MODEL>
+__device__ __forceinline__ void project_sigma2(const v2 sg[3], float kf, float muf, float lamf, v2 d[3]) {
+    const v2 k(kf), mu(muf), lam(lamf);
+    if (MODEL == 2) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) d[i] = v2(1.f) - sg[i];
+        return;
+    }
+    const v2 Sp = fma2(k, sg[0] + sg[1] + sg[2], v2(6.f * muf + 9.f * lamf)) * v2(MODEL == 1 ? 1.f / (kf + 2.f * muf + 3.f * lamf) : rcp_ftz(kf + 2.f * muf + 3.f * lamf));
+    const v2 inv(MODEL == 1 ? 1.f / (kf + 2.f * muf) : rcp_ftz(kf + 2.f * muf));
+    const v2 lS3 = lam * (Sp - v2(3.f));
+    if (MODEL == 1) {   // linear corotated closed form
+#pragma unroll
+        for (int i = 0; i < 3; ++i) d[i] = (fma2(v2(2.f) * mu, v2(1.f) - sg[i], v2(0.f) - lS3)) * inv;
+        return;
+    }
+    // Neo-Hookean: damped Newton from the linear-corotated minimiser (floored at 0.05), lockstep lanes
+    v2 p[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        p[i] = sg[i] + fma2(v2(2.f) * mu, v2(1.f) - sg[i], v2(0.f) - lS3) * inv;
+        p[i] = v2(fmaxf(p[i].a.x, 0.05f), fmaxf(p[i].a.y, 0.05f));
+    }
+    const v2 sn2 = fma2(sg[0], sg[0], fma2(sg[1], sg[1], sg[2] * sg[2]));
+    const v2 scale(fmaxf(1.f, sqrtf(sn2.a.x)), fmaxf(1.f, sqrtf(sn2.a.y)));
+    const v2 gtol = v2(2e-6f * kf) * scale;
+    const v2 gtol2 = gtol * gtol;
+    v2 lnJ = log2v(p[0] * p[1] * p[2]);
+    v2 f0 = nh_f2(p, sg, k, mu, lam, lnJ);
+#pragma unroll 1
+    for (int it = 0; it < 16; ++it) {
+        const v2 iv[3] = {rcp2(p[0]), rcp2(p[1]), rcp2(p[2])};
+        v2 g[3];
+        const v2 kmu = k + mu;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) g[i] = fma2(kmu, p[i], fma2(lam * lnJ - mu, iv[i], v2(0.f) - k * sg[i]));
+        const v2 gg = fma2(g[0], g[0], fma2(g[1], g[1], g[2] * g[2]));
+        const bool dx = gg.a.x <= gtol2.a.x, dy = gg.a.y <= gtol2.a.y;   // lane converged (|g| <= gtol)
+        if (dx && dy) break;
+        v2 H[3][3];
+        const v2 dg = mu - lam * lnJ;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) H[i][j] = i == j ? fma2(lam * iv[i], iv[j], fma2(dg * iv[i], iv[i], kmu)) : lam * iv[i] * iv[j];
+        const v2 c00 = fma2(H[1][1], H[2][2], v2(0.f) - H[1][2] * H[2][1]);
+        const v2 c01 = fma2(H[1][2], H[2][0], v2(0.f) - H[1][0] * H[2][2]);
+        const v2 c02 = fma2(H[1][0], H[2][1], v2(0.f) - H[1][1] * H[2][0]);
+        const v2 det = fma2(H[0][0], c00, fma2(H[0][1], c01, H[0][2] * c02));
+        const v2 id = rcp2(det);
+        const v2 c10 = fma2(H[0][2], H[2][1], v2(0.f) - H[0][1] * H[2][2]);
+        const v2 c11 = fma2(H[0][0], H[2][2], v2(0.f) - H[0][2] * H[2][0]);
+        const v2 c12 = fma2(H[0][1], H[2][0], v2(0.f) - H[0][0] * H[2][1]);
+        const v2 c20 = fma2(H[0][1], H[1][2], v2(0.f) - H[0][2] * H[1][1]);
+        const v2 c21 = fma2(H[0][2], H[1][0], v2(0.f) - H[0][0] * H[1][2]);
+        const v2 c22 = fma2(H[0][0], H[1][1], v2(0.f) - H[0][1] * H[1][0]);
+        v2 dd[3];
+        dd[0] = v2(0.f) - fma2(c00, g[0], fma2(c10, g[1], c20 * g[2])) * id;
+        dd[1] = v2(0.f) - fma2(c01, g[0], fma2(c11, g[1], c21 * g[2])) * id;
+        dd[2] = v2(0.f) - fma2(c02, g[0], fma2(c12, g[1], c22 * g[2])) * id;
+        v2 slope = fma2(dd[0], g[0], fma2(dd[1], g[1], dd[2] * g[2]));
+        // Newton direction unusable (singular or not a descent direction): scaled gradient step
+        const bool okx = fabsf(det.a.x) > 0.f && isfinite(det.a.x) && slope.a.x < 0.f && isfinite(slope.a.x);
+        const bool oky = fabsf(det.a.y) > 0.f && isfinite(det.a.y) && slope.a.y < 0.f && isfinite(slope.a.y);
+        const v2 sgd(-rcp_ftz(kf + muf));
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            dd[i] = sel2(okx, oky, dd[i], sgd * g[i]);
+            dd[i] = sel2(dx, dy, v2(0.f), dd[i]);   // a converged lane stays where it is
+        }
+        slope = fma2(dd[0], g[0], fma2(dd[1], g[1], dd[2] * g[2]));
+        const v2 fr = v2(2e-6f) * fma2(k, fma2(p[0], p[0], fma2(p[1], p[1], fma2(p[2], p[2], sn2))),
+                                       fma2(mu, abs2(lnJ), fma2(lam * lnJ, lnJ, mu)));
+        v2 t(1.f);
+        bool ax = dx, ay = dy;                   // accepted
+        bool tx = dx, ty = dy;                   // any accepted point (a converged lane keeps its state)
+#pragma unroll 1
+        for (int ls = 0; ls < 40; ++ls) {
+            v2 pn[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) pn[i] = fma2(t, dd[i], p[i]);
+            const bool vx = pn[0].a.x > 0.f && pn[1].a.x > 0.f && pn[2].a.x > 0.f;
+            const bool vy = pn[0].a.y > 0.f && pn[1].a.y > 0.f && pn[2].a.y > 0.f;
+            const v2 prod = pn[0] * pn[1] * pn[2];
+            const v2 lnJn = v2(vx && !ax ? log_ftz(prod.a.x) : 0.f, vy && !ay ? log_ftz(prod.a.y) : 0.f);
+            const v2 fn = nh_f2(pn, sg, k, mu, lam, lnJn);
+            const v2 bound = fma2(v2(1e-4f) * t, slope, f0 + fr);
+            const bool nx = !ax && vx && fn.a.x <= bound.a.x, ny = !ay && vy && fn.a.y <= bound.a.y;
+            if (nx) { lnJ.a.x = lnJn.a.x; f0.a.x = fn.a.x; ax = true; tx = true; }
+            if (ny) { lnJ.a.y = lnJn.a.y; f0.a.y = fn.a.y; ay = true; ty = true; }
+            if (ax && ay) break;
+            if (!ax) t.a.x *= 0.5f;
+            if (!ay) t.a.y *= 0.5f;
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) p[i] = fma2(t, dd[i], p[i]);
+        if (!tx) { lnJ.a.x = log_ftz(p[0].a.x * p[1].a.x * p[2].a.x); }
+        if (!ty) { lnJ.a.y = log_ftz(p[0].a.y * p[1].a.y * p[2].a.y); }
+        if (!tx || !ty) {
+            const v2 fre = nh_f2(p, sg, k, mu, lam, lnJ);
+            if (!tx) f0.a.x = fre.a.x;
+            if (!ty) f0.a.y = fre.a.y;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) d[i] = p[i] - sg[i];
+}
+
+template <int MODEL>
+__global__ void __launch_bounds__(128, MODEL == 0 ? 4 : 6) k_local2(Params P, const int4* __restrict__ tet,
+                                                                     const float* __restrict__ Bm,
+                                                                     const float* __restrict__ hw2,
+                                                                     const double4* __restrict__ x, float* __restrict__ fc) {
+    pdl_enter();
+    const int SI = P.S, half = SI >> 1;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gt >= P.n_t * half) return;
+    const int t = gt / half, inst = 2 * (gt - t * half);   // instances inst, inst + 1
+    const int nt = P.n_t;
+    const int4 tv = __ldg(&tet[t]);
+    v2 D[3][3];
+    {
+        const double4 a0 = x[tv.x * SI + inst], a1 = x[tv.y * SI + inst], a2 = x[tv.z * SI + inst], a3 = x[tv.w * SI + inst];
+        const double4 b0 = x[tv.x * SI + inst + 1], b1 = x[tv.y * SI + inst + 1], b2 = x[tv.z * SI + inst + 1],
+                      b3 = x[tv.w * SI + inst + 1];
+        D[0][0] = v2((float)(a1.x - a0.x), (float)(b1.x - b0.x)); D[1][0] = v2((float)(a1.y - a0.y), (float)(b1.y - b0.y));
+        D[2][0] = v2((float)(a1.z - a0.z), (float)(b1.z - b0.z));
+        D[0][1] = v2((float)(a2.x - a0.x), (float)(b2.x - b0.x)); D[1][1] = v2((float)(a2.y - a0.y), (float)(b2.y - b0.y));
+        D[2][1] = v2((float)(a2.z - a0.z), (float)(b2.z - b0.z));
+        D[0][2] = v2((float)(a3.x - a0.x), (float)(b3.x - b0.x)); D[1][2] = v2((float)(a3.y - a0.y), (float)(b3.y - b0.y));
+        D[2][2] = v2((float)(a3.z - a0.z), (float)(b3.z - b0.z));
+    }
+    float B[9];
+#pragma unroll
+    for (int e = 0; e < 9; ++e) B[e] = __ldg(&Bm[(size_t)e * nt + t]);
+    v2 F[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) F[i][j] = fma2(D[i][0], v2(B[j]), fma2(D[i][1], v2(B[3 + j]), D[i][2] * v2(B[6 + j])));
+    v2 S[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) S[i][j] = fma2(F[0][i], F[0][j], fma2(F[1][i], F[1][j], F[2][i] * F[2][j]));
+    v2 V[3][3];
+    jacobi3_2(S, V);
+    v2 ev[3] = {S[0][0], S[1][1], S[2][2]};
+    swapcol2(V, ev, 0, 1, ev[0].a.x < ev[1].a.x, ev[0].a.y < ev[1].a.y);
+    swapcol2(V, ev, 0, 2, ev[0].a.x < ev[2].a.x, ev[0].a.y < ev[2].a.y);
+    swapcol2(V, ev, 1, 2, ev[1].a.x < ev[2].a.x, ev[1].a.y < ev[2].a.y);
+    {
+        const v2 detV = fma2(V[0][0], fma2(V[1][1], V[2][2], v2(0.f) - V[1][2] * V[2][1]),
+                             fma2(v2(0.f) - V[0][1], fma2(V[1][0], V[2][2], v2(0.f) - V[1][2] * V[2][0]),
+                                  V[0][2] * fma2(V[1][0], V[2][1], v2(0.f) - V[1][1] * V[2][0])));
+        const v2 sgn(detV.a.x < 0.f ? -1.f : 1.f, detV.a.y < 0.f ? -1.f : 1.f);
+        V[0][2] = V[0][2] * sgn; V[1][2] = V[1][2] * sgn; V[2][2] = V[2][2] * sgn;
+    }
+    v2 FV[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) FV[i][j] = fma2(F[i][0], V[0][j], fma2(F[i][1], V[1][j], F[i][2] * V[2][j]));
+    // U by Gram-Schmidt on F V (lane-wise fallbacks for degenerate columns, as the scalar kernel)
+    v2 U[3][3];
+    const v2 q0 = fma2(FV[0][0], FV[0][0], fma2(FV[1][0], FV[1][0], FV[2][0] * FV[2][0]));
+    const v2 r0 = rsqrt2(q0);
+    const v2 n0 = sel2(q0.a.x > 0.f, q0.a.y > 0.f, q0 * r0, v2(0.f));
+    const bool u0x = q0.a.x > 1e-36f, u0y = q0.a.y > 1e-36f;
+    U[0][0] = sel2(u0x, u0y, FV[0][0] * r0, v2(1.f));
+    U[1][0] = sel2(u0x, u0y, FV[1][0] * r0, v2(0.f));
+    U[2][0] = sel2(u0x, u0y, FV[2][0] * r0, v2(0.f));
+    const v2 dt = fma2(U[0][0], FV[0][1], fma2(U[1][0], FV[1][1], U[2][0] * FV[2][1]));
+    v2 w0 = FV[0][1] - dt * U[0][0], w1 = FV[1][1] - dt * U[1][0], w2 = FV[2][1] - dt * U[2][0];
+    const v2 q1 = fma2(w0, w0, fma2(w1, w1, w2 * w2));
+    const v2 r1 = rsqrt2(q1);
+    const v2 n1 = sel2(q1.a.x > 0.f, q1.a.y > 0.f, q1 * r1, v2(0.f));
+    const bool u1x = n1.a.x > 1e-30f * fmaxf(1.f, n0.a.x), u1y = n1.a.y > 1e-30f * fmaxf(1.f, n0.a.y);
+    U[0][1] = w0 * r1; U[1][1] = w1 * r1; U[2][1] = w2 * r1;
+    if (!u1x || !u1y) {   // any unit vector orthogonal to u0 (rare), lane by lane
+#pragma unroll
+        for (int l = 0; l < 2; ++l) {
+            if (l == 0 ? u1x : u1y) continue;
+            const float a0 = l == 0 ? U[0][0].a.x : U[0][0].a.y, a1 = l == 0 ? U[1][0].a.x : U[1][0].a.y,
+                        a2 = l == 0 ? U[2][0].a.x : U[2][0].a.y;
+            const float e0 = fabsf(a0) < 0.577f ? 1.f : 0.f, e1 = e0 == 0.f && fabsf(a1) < 0.577f ? 1.f : 0.f;
+            const float e2 = (e0 == 0.f && e1 == 0.f) ? 1.f : 0.f;
+            const float dp = a0 * e0 + a1 * e1 + a2 * e2;
+            const float z0 = e0 - dp * a0, z1 = e1 - dp * a1, z2 = e2 - dp * a2;
+            const float nz = sqrtf(z0 * z0 + z1 * z1 + z2 * z2);
+            if (l == 0) {
+                U[0][1].a.x = z0 / nz; U[1][1].a.x = z1 / nz; U[2][1].a.x = z2 / nz;
+            } else {
+                U[0][1].a.y = z0 / nz; U[1][1].a.y = z1 / nz; U[2][1].a.y = z2 / nz;
+            }
+        }
+    }
+    U[0][2] = fma2(U[1][0], U[2][1], v2(0.f) - U[2][0] * U[1][1]);
+    U[1][2] = fma2(U[2][0], U[0][1], v2(0.f) - U[0][0] * U[2][1]);
+    U[2][2] = fma2(U[0][0], U[1][1], v2(0.f) - U[1][0] * U[0][1]);
+    v2 sg[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sg[j] = fma2(U[0][j], FV[0][j], fma2(U[1][j], FV[1][j], U[2][j] * FV[2][j]));
+    v2 dlt[3];
+    project_sigma2<MODEL>(sg, P.k, P.mu, P.lam, dlt);
+    const v2 hw(__ldg(&hw2[t]));
+    v2 Q[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            Q[i][j] = hw * fma2(U[i][0] * dlt[0], V[j][0], fma2(U[i][1] * dlt[1], V[j][1], U[i][2] * dlt[2] * V[j][2]));
+    float2* o = reinterpret_cast<float2*>(fc + 12 * (size_t)t * SI + inst);   // [tet][corner][xyz][instance]
+    const int ss = SI >> 1;                                                    // float2 stride of one plane
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        v2 sum(0.f);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const v2 fa = fma2(Q[i][0], v2(B[3 * a]), fma2(Q[i][1], v2(B[3 * a + 1]), Q[i][2] * v2(B[3 * a + 2])));
+            o[(3 * (a + 1) + i) * ss] = fa.a;
+            sum = sum + fa;
+        }
+        o[i * ss] = make_float2(-sum.a.x, -sum.a.y);
+    }
+}
+
 void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
                   const double4* x, float* fc, float* Pdbg, float* du, int admm_first) {
+    if (P.S > 1 && (P.S & 1) == 0 && !du && !Pdbg && P.pair_local) {   // packed-FP32 pairs of instances
+        const unsigned g2 = (unsigned)((P.n_t * (size_t)(P.S / 2) + 127) / 128);
+        if (P.model == 1)
+            launch_pdl(k_local2<1>, dim3(g2), dim3(128), 0, st, P, tet, Bm, hw2, x, fc);
+        else if (P.model == 2)
+            launch_pdl(k_local2<2>, dim3(g2), dim3(128), 0, st, P, tet, Bm, hw2, x, fc);
+        else
+            launch_pdl(k_local2<0>, dim3(g2), dim3(128), 0, st, P, tet, Bm, hw2, x, fc);
+        return;
+    }
     const unsigned g = (unsigned)((P.n_t * (size_t)P.S + 127) / 128);
     if (P.model == 1)
         launch_pdl(k_local<1>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
@@ -2281,13 +2608,13 @@ __device__ __forceinline__ void chain_rho(int S, int inst, int s, double t0, dou
     if (c >= 0) {
         const double4 xa = x[(size_t)cc.v0[c] * S + inst];
         const double xs0 = xa.x + t0, xs1 = xa.y + t1, xs2 = xa.z + t2;
+        // the fp64 rows the h-vector's theta J x^k was formed with: its x^k terms cancel to fp64
+        // rounding here (fp32 rows would leave a bias of ~6e-8 |x^k| in rho)
+        const DContact& ct = cc.dc[c];
 #pragma unroll
-        for (int kk = 0; kk < 3; ++kk) {
-            const float* c3 = cc.c9 + 9 * c + 3 * kk;
-            cs.rho[3 * c + kk] = cs.hvec[3 * c + kk] - cs.theta[3 * c + kk] * ((double)c3[0] * xs0 +
-                                                                               (double)c3[1] * xs1 +
-                                                                               (double)c3[2] * xs2);
-        }
+        for (int kk = 0; kk < 3; ++kk)
+            cs.rho[3 * c + kk] = cs.hvec[3 * c + kk] -
+                                 cs.theta[3 * c + kk] * (ct.c[kk][0] * xs0 + ct.c[kk][1] * xs1 + ct.c[kk][2] * xs2);
     }
 }
 

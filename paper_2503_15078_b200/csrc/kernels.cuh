@@ -56,6 +56,7 @@ struct Params {
     double len_scale;     // max(rest bbox diagonal, max |rest coordinate|): gaps within 1e-12 of it are 0 (A15)
     int ncp;              // 0 Fischer-Burmeister (App. B.2, the paper's choice), 1 minimum map (App. B.1)
     int precond;          // 0 Delassus diagonal, 1 mass inverse
+    int pair_local;       // S > 1, S even: the packed-FP32 paired local step (k_local2)
 };
 
 // Offsets of the packed contact data.  Instances whose contact-vertex sets are equal form
@@ -105,6 +106,7 @@ struct CrActive {
 // compact per-contact arrays for the CR: rows' directions, single-vertex slot / vertex (-1 otherwise)
 struct CrContacts {
     const float* c9;   // [C][3][3] rows n, t1, t2
+    const DContact* dc;   // the fp64 rows (the Schur RHS uses the directions h-vector used)
     const int* s0;     // [C] global slot of a single-vertex weight-1 contact, else -1
     const int* v0;     // [C] its internal vertex, else -1
     const int* c1;     // [NS] the only contact (global id) on a slot if it is single-vertex weight-1, else -1
