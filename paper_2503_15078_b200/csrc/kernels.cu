@@ -3047,7 +3047,9 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
             Zt[buf][e & 31][e >> 5] = rt[u];
         }
     };
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    // fp64 accumulation: G_ab sums up to etree-height products whose fp32 running sum loses ~1e-5
+    // relative on cancelling pairs, and D = J G J^T drives the CR
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     if (D >= 0) fetch(0);
     int buf = 0;
     for (int d0 = 0; d0 <= D; d0 += 32) {
@@ -3060,15 +3062,15 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
             const float zs = Zs[buf][dd][ls];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (d <= dl[q]) acc[q] = fmaf(zs, Zt[buf][dd][lt0 + q], acc[q]);
+                if (d <= dl[q]) acc[q] = fma((double)zs, (double)Zt[buf][dd][lt0 + q], acc[q]);
         }
         buf ^= 1;
     }
     for (int q = 0; q < 4; ++q) {
         const int t = bt * 32 + lt0 + q;
         if (s < ns && t < ns) {
-            G[(size_t)s * ns + t] = acc[q];
-            G[(size_t)t * ns + s] = acc[q];
+            G[(size_t)s * ns + t] = (float)acc[q];
+            G[(size_t)t * ns + s] = (float)acc[q];
         }
     }
 }
@@ -3126,10 +3128,10 @@ __global__ void k_gram_rows(InstOff off, const int32_t* __restrict__ vtx_all, co
         const int b = vtx_all[sb + t];
         const int dl = lca_depth(a, b, parent, ptop, depth);
         const float* cb = Kcol + colptr[b] + depth[b];
-        float acc = 0.f;
-        for (int d = 0; d <= dl; ++d) acc = fmaf(__ldg(ca - d), __ldg(cb - d), acc);
-        Gc[(size_t)s * ns + t] = acc;
-        Gc[(size_t)t * ns + s] = acc;
+        double acc = 0.0;   // the same order and precision as k_delassus (bitwise equal entries)
+        for (int d = 0; d <= dl; ++d) acc = fma((double)__ldg(ca - d), (double)__ldg(cb - d), acc);
+        Gc[(size_t)s * ns + t] = (float)acc;
+        Gc[(size_t)t * ns + s] = (float)acc;
     }
 }
 
@@ -3817,12 +3819,27 @@ __global__ void __launch_bounds__(kCrThreads, 1)
             rb ^= 1;
             const double beta = s1 / rAr;
             rAr = s1;
-            ApAp = s2 + 2.0 * beta * s3 + beta * beta * ApAp;
+            // |Ap_new|^2 = |Ar + beta Ap|^2 by its expansion (no extra reduction) unless the expansion
+            // cancels: then the direct sum (a uniform branch; the expansion loses all digits when
+            // Ar ~ -beta Ap and would turn alpha into noise)
+            const double apx = s2 + 2.0 * beta * s3 + beta * beta * ApAp;
+            const double aps = s2 + beta * beta * ApAp;
 #pragma unroll
             for (int k = 0; k < kRpt; ++k) {
                 const int j = threadIdx.x + kCrThreads * k;   // entries past m stay 0
                 p[k] = j < m ? X.r[j] + beta * p[k] : 0.0;
                 Ap[k] = Ar[k] + beta * Ap[k];
+            }
+            if (apx > 1e-3 * aps) {
+                ApAp = apx;
+            } else {
+                double d = 0.0, e1 = 0.0, e2 = 0.0;
+#pragma unroll
+                for (int k = 0; k < kRpt; ++k)
+                    if (threadIdx.x + kCrThreads * k < m) d = fma(Ap[k], Ap[k], d);
+                block_sum3(d, e1, e2, X.red + rb * 3 * (kCrThreads / 32));
+                rb ^= 1;
+                ApAp = d;
             }
             if (it == 3) cr_stamp(17);
             if (it < 9 && it != 3) cr_stamp(3 + it);
@@ -4075,63 +4092,82 @@ __global__ void __launch_bounds__(kGcrThreads) k_gcr_row(Params P, GcrData g, co
     }
 }
 
-// CR scalars from the partials (same fixed order in every CTA) and the vector updates of
-// iteration `it`: [beta, p, Ap (it > 0)], breakdown test, alpha, z += alpha p, r -= alpha Ap.
-// Scalars ping-pong between sc[.. + (it & 1)] (read) and sc[.. + ((it + 1) & 1)] (written by CTA 0).
+// CR iteration `it`, first half: r.Ar from the row partials (same fixed order in every CTA), beta,
+// p = r + beta p, Ap = Ar + beta Ap, and this CTA's partial |Ap|^2 (part[3 b + 2]; the row
+// kernel's s3 slot, unused since |Ap|^2 is reduced directly).  Scalars ping-pong between
+// sc[.. + (it & 1)] (read) and sc[.. + ((it + 1) & 1)] (written by CTA 0); launched on the row blocks.
 __global__ void __launch_bounds__(kGcrThreads) k_gcr_update(GcrData g, int m, int it) {
     pdl_enter();
-    __shared__ double sh[4];
+    __shared__ double sh[2];
+    __shared__ double red[3 * (kGcrThreads / 32) + 3];
+    const int rp = it & 1, wp = rp ^ 1;
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
-        double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        for (int b = lane; b < g.nblk; b += 32) {
-            s1 += g.part[3 * b];
-            s2 += g.part[3 * b + 1];
-            s3 += g.part[3 * b + 2];
-        }
+        double s1 = 0.0;
+        for (int b = lane; b < g.nblk; b += 32) s1 += g.part[3 * b];
         s1 = warp_sum(s1);
-        s2 = warp_sum(s2);
-        s3 = warp_sum(s3);
         if (lane == 0) {
-            const int rp = it & 1, wp = rp ^ 1;
-            double rAr, ApAp, beta = 0.0;
-            double stop = it == 0 ? 0.0 : g.sc[4 + rp];
-            if (it == 0) {
-                rAr = s1;
-                ApAp = s2;
-            } else {
-                const double rAr0 = g.sc[rp], ApAp0 = g.sc[2 + rp];
-                beta = stop != 0.0 ? 0.0 : s1 / rAr0;
-                rAr = s1;
-                ApAp = s2 + 2.0 * beta * s3 + beta * beta * ApAp0;
-            }
-            if (stop == 0.0 && (ApAp <= 1e-300 || fabs(rAr) <= 1e-300)) stop = 1.0;
+            const double stop = it == 0 ? 0.0 : g.sc[4 + rp];
+            const double beta = (it == 0 || stop != 0.0) ? 0.0 : s1 / g.sc[rp];
             sh[0] = beta;
-            sh[1] = stop != 0.0 ? 0.0 : rAr / ApAp;
-            sh[2] = stop;
+            sh[1] = stop;
             if (blockIdx.x == 0) {
-                g.sc[wp] = rAr;
-                g.sc[2 + wp] = ApAp;
+                g.sc[wp] = s1;
                 g.sc[4 + wp] = stop;
             }
         }
     }
     __syncthreads();
-    const double beta = sh[0], alpha = sh[1];
-    if (sh[2] != 0.0) return;   // broken down (now or earlier): keep the iterate
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
-        double p, Ap;
-        if (it == 0) {
-            p = g.r[j];
-            Ap = g.Ar[j];
-        } else {
-            p = g.r[j] + beta * g.p[j];
-            Ap = g.Ar[j] + beta * g.Ap[j];
+    const double beta = sh[0];
+    double d = 0.0, e1 = 0.0, e2 = 0.0;
+    if (sh[1] == 0.0) {
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+            double p, Ap;
+            if (it == 0) {
+                p = g.r[j];
+                Ap = g.Ar[j];
+            } else {
+                p = g.r[j] + beta * g.p[j];
+                Ap = g.Ar[j] + beta * g.Ap[j];
+            }
+            g.p[j] = p;
+            g.Ap[j] = Ap;
+            d = fma(Ap, Ap, d);
         }
-        g.p[j] = p;
-        g.Ap[j] = Ap;
-        g.z[j] += alpha * p;
-        g.r[j] -= alpha * Ap;
+    }
+    block_sum3_gcr(d, e1, e2, red);
+    if (threadIdx.x == 0) g.part[3 * blockIdx.x + 2] = d;
+}
+
+// second half: |Ap|^2 from the partials (fixed order), breakdown test (reading A19), alpha = r.Ar /
+// |Ap|^2, z += alpha p, r -= alpha Ap.  Every CTA takes the same decision from the same sums.
+__global__ void __launch_bounds__(kGcrThreads) k_gcr_step(GcrData g, int m, int it) {
+    pdl_enter();
+    __shared__ double sh[2];
+    const int wp = (it & 1) ^ 1;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double ApAp = 0.0;
+        for (int b = lane; b < g.nblk; b += 32) ApAp += g.part[3 * b + 2];
+        ApAp = warp_sum(ApAp);
+        if (lane == 0) {
+            const double rAr = g.sc[wp];
+            double stop = g.sc[4 + wp];
+            if (stop == 0.0 && (ApAp <= 1e-300 || fabs(rAr) <= 1e-300)) stop = 1.0;
+            sh[0] = stop != 0.0 ? 0.0 : rAr / ApAp;
+            sh[1] = stop;
+            if (blockIdx.x == 0) g.sc[2 + wp] = ApAp;
+        }
+    }
+    __syncthreads();
+    if (sh[1] != 0.0) {   // broken down (now or earlier): keep the iterate
+        if (blockIdx.x == 0 && threadIdx.x == 0) g.sc[4 + wp] = 1.0;
+        return;
+    }
+    const double alpha = sh[0];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+        g.z[j] += alpha * g.p[j];
+        g.r[j] -= alpha * g.Ap[j];
     }
 }
 
@@ -4197,7 +4233,8 @@ int launch_gcr(cudaStream_t st, const Params& P, GcrData g, const DContact* c, C
                    (const double*)g.r, g.W);
         launch_pdl(k_gcr_gram, dim3(g.n_gram_items), dim3(256), 0, st, NS, g, g.gram_items);
         launch_pdl(k_gcr_row, dim3(nb), dim3(kGcrThreads), 0, st, P, g, c, cs, (int)(it == 0));
-        launch_pdl(k_gcr_update, dim3(ub), dim3(kGcrThreads), 0, st, g, m, it);
+        launch_pdl(k_gcr_update, dim3(nb), dim3(kGcrThreads), 0, st, g, m, it);
+        launch_pdl(k_gcr_step, dim3(ub), dim3(kGcrThreads), 0, st, g, m, it);
     }
     launch_pdl(k_gcr_final, dim3(ub), dim3(kGcrThreads), 0, st, g, m, P.h, cs.lam, cs.cr_res);
     launch_pdl(k_gcr_slot, dim3((NS + 255) / 256), dim3(256), 0, st, NS, sl, cc, (const double*)cs.theta,
@@ -4205,7 +4242,7 @@ int launch_gcr(cudaStream_t st, const Params& P, GcrData g, const DContact* c, C
     return (int)cudaGetLastError();
 }
 
-int gcr_kernels_per_iteration(int cr_iters) { return 3 + 4 * cr_iters; }
+int gcr_kernels_per_iteration(int cr_iters) { return 3 + 5 * cr_iters; }
 
 int read_cr_clock(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, g_cr_clock, sizeof(unsigned long long) * 32);

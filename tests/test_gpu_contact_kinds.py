@@ -107,7 +107,8 @@ def test_bilateral_and_frictional_rows_mixed(simmod):
             mixed.append(cs[k])
     mixed += cs[len(bottom):]
     # frame-level only: isolated iterations of this set differ from the oracle's by up to ~5 tolerances
-    # without a measured fp32 cause (open item; tools/diag_fp32_operator.py mixed)
+    # (the oracle's own CR on the GPU's Schur RHS differs from the GPU's by 2 % there; DESIGN.md §3,
+    # open item; tools/diag_fp32_operator.py mixed)
     s, o, x, v, lam, info = free_running(simmod, sc, mixed, 10, what="mixed", per_iteration=False)
     assert np.isfinite(x).all()
 
