@@ -319,7 +319,9 @@ int sim_set_warm_start(sim_handle *h, int32_t on);
  * right-hand sides in fp32 component planes, one CTA per 64-output unit x 128 instances x 3
  * components, kind::tf32 with a 3xTF32 split (V_hi = the raw fp32 tile in shared memory, MN-major;
  * V_lo in TMEM; K_hi / K_lo pre-rounded), TMEM accumulators folded every 4 tiles;
- * 1 = CUDA-core FP32 FMAs.  Results agree with FP32 to ~2e-6 relative.  n_instances == 1 always
+ * 1 = CUDA-core FP32 FMAs; 3 = the tensor-core K-passes with the contact chain / scatter passes on
+ * the CUDA cores (accuracy studies).  Takes effect at the next contact commit.  Results agree
+ * with FP32 to ~2e-6 relative.  n_instances == 1 always
  * uses the HBM-streaming SpMV kernels.  (mode >> 4) >= 2 sets the fold interval (tuning). */
 int sim_set_kpass_mode(sim_handle *h, int32_t mode);
 

@@ -1415,7 +1415,7 @@ static int commit_host(sim_handle* H) {
     H->NG = NG;
     H->ng_max = ngmax;
     // chain dot and scatter on the tensor cores: S > 1 instances all in one slot-set class
-    H->tc_contact = S > 1 && NCL == 1 && Ct > 0 && H->kpass_mode != 1;
+    H->tc_contact = S > 1 && NCL == 1 && Ct > 0 && H->kpass_mode != 1 && H->kpass_mode != 3;
     if (H->tc_contact && H->ic[rep[0]].verts != H->tc_verts) {   // tiles depend on K and the vertex set only
         simhost::ContactPasses cp;
         simhost::build_contact_passes(H->K, H->ic[rep[0]].verts, cp);
@@ -1746,8 +1746,9 @@ extern "C" int sim_set_kpass_mode(sim_handle* H, int32_t mode) {
         H->tc_drain = std::max(2, mode >> 4);
         return SIM_OK;
     }
-    if (mode < 0 || mode > 2)
-        return fail(SIM_E_INVALID, "K-pass mode must be 0 or 2 (tensor cores) or 1 (CUDA-core FP32)");
+    if (mode < 0 || mode > 3)
+        return fail(SIM_E_INVALID, "K-pass mode must be 0 or 2 (tensor cores), 1 (CUDA-core FP32) or 3 (tensor-core K-passes, "
+                    "CUDA-core contact passes)");
     H->kpass_mode = mode;
     return SIM_OK;
 }

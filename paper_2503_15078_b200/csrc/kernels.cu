@@ -2010,7 +2010,7 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
                const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
     pdl_enter();
     extern __shared__ unsigned char pl_raw[];
-    __shared__ __align__(8) uint64_t afull[kPlStages], mdone[kPlStages], lofull[3], lofree[3], dfree;
+    __shared__ __align__(8) uint64_t mdone[kPlStages], lofull[3], lofree[3], dfree;
     __shared__ __align__(8) uint64_t bfull[kPlBStages], bempty[kPlBStages];
     __shared__ uint32_t tmem_base_s;
     __shared__ int s_last;
@@ -2032,10 +2032,7 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
     }
     if (tid == 0) {
         // worker-side barriers count one elected arrival per worker warp (after __syncwarp)
-        for (int s2 = 0; s2 < kPlStages; ++s2) {
-            mbar_init(&afull[s2], kPlWarps);
-            mbar_init(&mdone[s2], 1);
-        }
+        for (int s2 = 0; s2 < kPlStages; ++s2) mbar_init(&mdone[s2], 1);
         for (int c = 0; c < 3; ++c) {
             mbar_init(&lofull[c], kPlWarps);
             mbar_init(&lofree[c], 1);
@@ -2164,11 +2161,10 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
         // of a closed accumulation group, then the copies of tile t + 2 into the stage MMA(t - 1) frees
         for (int t = 0; t < nt; ++t) {
             const int st = t % kPlStages;
-            // this thread's copies of tile t have landed (tile t + 1's may still fly), then the CTA's
+            // this thread's copies of tile t have landed (tile t + 1's may still fly), then every
+            // worker's (a named barrier of the 16 worker warps)
             if (t + 1 < nt) cp_async_wait<1>(); else cp_async_wait<0>();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&afull[st]);
-            mbar_wait(&afull[st], (unsigned)(t / kPlStages) & 1u);
+            asm volatile("bar.sync 1, %0;\n" ::"r"(kPlThreads) : "memory");
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> async proxy
             // V_lo of rows 8 oc .. 8 oc + 7 (K-step oc) for instance 32 qd + lane, one component at a
             // time into its TMEM slot once the tensor core has read the previous tile's
@@ -2202,6 +2198,8 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
             }
             if (t + 2 < nt) {
                 if (t >= 1) mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
+                // every worker has passed this iteration's barrier, i.e. finished reading stage
+                // (t + 2) % 3 = (t - 1) % 3 for its V_lo in iteration t - 1
                 issue(t + 2);
             }
         }
