@@ -504,13 +504,24 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(dev)          # graph capture needs a non-default stream
     torch.cuda.set_stream(stream)
+    line = rank_flow(args, ws, rank, dev, stream)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
 
+
+def rank_flow(args, ws, rank, dev, stream, measure_fn=None):
+    """The per-rank part of the bench: this rank's share of the cfg5 batch, the max-over-ranks
+    timings and the all-gathered per-rank rows (NCCL on the GPU box; gloo with a stubbed
+    `measure_fn` in tests/test_bench_dist.py), and on rank 0 the JSON line (None elsewhere)."""
+    measure_fn = measure_fn or measure
     # cfg5 (BASELINE configs[4]): 1024 cfg3 instances sharded over the ranks (strong scaling);
     # --instances S fixes the per-GPU count instead (weak scaling)
     total = 1024
     S = args.instances if args.instances else max(1, total // ws)
     scaling = "weak" if args.instances else "strong"
-    r = measure(args, S, rank, ws, dev, stream, full=True)
+    r = measure_fn(args, S, rank, ws, dev, stream, full=True)
 
     def max_over_ranks(v):   # NCCL: per-rank timings only, after the timed regions
         return reduce_max(v, ws, dev)
@@ -519,12 +530,10 @@ def run_ours(args):
     gathered = gather_stats(r["summary"], ws, dev)   # results and stats of every rank (NCCL all_gather)
     e2e_ms = max_over_ranks(r["e2e_ms"])
     # single-scene latency (cfg3, S = 1): the paper-comparable ms per L-G iteration
-    r1 = measure(args, 1, rank, ws, dev, stream, full=False) if S > 1 else r
+    r1 = measure_fn(args, 1, rank, ws, dev, stream, full=False) if S > 1 else r
     single_ms = max_over_ranks(r1["total_ms"])
     if rank != 0:
-        if ws > 1:
-            dist.destroy_process_group()
-        return
+        return None
     scenes_total = ws * S
     ms_per_step = total_ms / args.steps
     value = scenes_total * args.steps * ITERS / (total_ms / 1000.0)
@@ -595,9 +604,7 @@ def run_ours(args):
         "clocks": r["clocks"],
         "nnz_K": nnz, "n_free": nf, "etree_height": int(st0["etree_height"]),
     }
-    print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
+    return line
 
 
 def main():

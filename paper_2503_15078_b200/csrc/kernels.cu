@@ -843,7 +843,7 @@ __device__ __forceinline__ void project_sigma2(const v2 sg[3], float kf, float m
 }
 
 template <int MODEL>
-__global__ void __launch_bounds__(128, MODEL == 0 ? 4 : 6) k_local2(Params P, const int4* __restrict__ tet,
+__global__ void __launch_bounds__(128, MODEL == 0 ? 5 : 6) k_local2(Params P, const int4* __restrict__ tet,
                                                                      const float* __restrict__ Bm,
                                                                      const float* __restrict__ hw2,
                                                                      const double4* __restrict__ x, float* __restrict__ fc) {
@@ -3045,8 +3045,9 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
             Zt[buf][e & 31][e >> 5] = rt[u];
         }
     };
-    // fp64 accumulation: G_ab sums up to etree-height products whose fp32 running sum loses ~1e-5
-    // relative on cancelling pairs, and D = J G J^T drives the CR
+    // fp64 accumulation: G_ab sums up to etree-height products; an fp32 running sum loses ~1e-5
+    // relative on cancelling pairs, and fp32 sums of 32-term chunks folded into fp64 still flip an
+    // A21 classification on the soft-soft pile -- D = J G J^T drives the CR
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     if (D >= 0) fetch(0);
     int buf = 0;
