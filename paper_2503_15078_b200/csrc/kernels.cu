@@ -2997,7 +2997,8 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
     int idx = blockIdx.x, bs = 0;
     while (idx >= tiles - bs) { idx -= tiles - bs; ++bs; }
     const int bt = bs + idx;
-    __shared__ float Zs[2][32][33], Zt[2][32][33];
+    constexpr int NST = 4;   // chunks of 32 depth levels in flight (cp.async straight into shared memory)
+    __shared__ float Zs[NST][32][33], Zt[NST][32][33];
     __shared__ int ds_[32], dt_[32];
     __shared__ int64_t cs_[32], ct_[32];
     __shared__ int smax;
@@ -3026,44 +3027,42 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
     atomicMax(&smax, maxd);
     __syncthreads();
     const int D = smax;
-    // staging: each thread loads 4 (slot, depth) entries of each block per 32-level chunk
-    float rs[4], rt[4];
-    auto fetch = [&](int d0) {
+    // staging: each thread copies 4 (slot, depth) entries of each block per 32-level chunk, NST - 1
+    // chunks ahead (latency-bound otherwise: ~2 CTAs per SM for an 800-slot Gram)
+    const int nch = D >= 0 ? D / 32 + 1 : 0;
+    auto issue = [&](int c) {
+        if (c < nch) {
+            const int d0 = 32 * c, st = c % NST;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = tid + 256 * u;
-            const int sl = e >> 5, dd = e & 31, d = d0 + dd;
-            rs[u] = (ds_[sl] >= d) ? __ldg(&Kcol[cs_[sl] + ds_[sl] - d]) : 0.f;
-            rt[u] = (dt_[sl] >= d) ? __ldg(&Kcol[ct_[sl] + dt_[sl] - d]) : 0.f;
+            for (int u = 0; u < 4; ++u) {
+                const int e = tid + 256 * u;
+                const int sl = e >> 5, dd = e & 31, d = d0 + dd;
+                const bool vs = ds_[sl] >= d, vt = dt_[sl] >= d;
+                cp_async4(&Zs[st][dd][sl], vs ? &Kcol[cs_[sl] + ds_[sl] - d] : Kcol, vs);
+                cp_async4(&Zt[st][dd][sl], vt ? &Kcol[ct_[sl] + dt_[sl] - d] : Kcol, vt);
+            }
         }
-    };
-    auto stash = [&](int buf) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = tid + 256 * u;
-            Zs[buf][e & 31][e >> 5] = rs[u];
-            Zt[buf][e & 31][e >> 5] = rt[u];
-        }
+        cp_async_commit();   // possibly empty: keeps one group per chunk slot
     };
     // fp64 accumulation: G_ab sums up to etree-height products; an fp32 running sum loses ~1e-5
     // relative on cancelling pairs, and fp32 sums of 32-term chunks folded into fp64 still flip an
     // A21 classification on the soft-soft pile -- D = J G J^T drives the CR
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    if (D >= 0) fetch(0);
-    int buf = 0;
-    for (int d0 = 0; d0 <= D; d0 += 32) {
-        stash(buf);
-        __syncthreads();
-        if (d0 + 32 <= D) fetch(d0 + 32);   // next chunk in flight while this one is consumed
+#pragma unroll
+    for (int c = 0; c < NST - 1; ++c) issue(c);
+    for (int c = 0; c < nch; ++c) {
+        cp_async_wait<NST - 2>();   // chunk c landed (this thread's copies)
+        __syncthreads();            // ... everyone's; and chunk c - 1 is consumed everywhere
+        issue(c + NST - 1);         // into the stage chunk c - 1 used
+        const int st = c % NST, d0 = 32 * c;
 #pragma unroll 8
         for (int dd = 0; dd < 32; ++dd) {
             const int d = d0 + dd;
-            const float zs = Zs[buf][dd][ls];
+            const float zs = Zs[st][dd][ls];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (d <= dl[q]) acc[q] = fma((double)zs, (double)Zt[buf][dd][lt0 + q], acc[q]);
+                if (d <= dl[q]) acc[q] = fma((double)zs, (double)Zt[st][dd][lt0 + q], acc[q]);
         }
-        buf ^= 1;
     }
     for (int q = 0; q < 4; ++q) {
         const int t = bt * 32 + lt0 + q;
