@@ -341,6 +341,89 @@ def test_cfg5_full_size_sampled(simmod):
             assert bad == 0, (i, iters, bad, n)
 
 
+def _cfg5_batch(simmod, sc, S):
+    """cfg5 handle of S instances with the bench's per-instance recipe (scenes.batch_instance_params)."""
+    s = make(simmod, sc, S)
+    s.set_pin_velocity(sc.pin_velocity)
+    base = simmod.contacts_to_array(sc.contacts)
+    arrs, v0s, deltas = [], np.empty((S, sc.mesh.n_v, 3)), np.empty(S)
+    for i in range(S):
+        v0s[i], deltas[i] = scenes.batch_instance_params(sc, i)
+        a = base.copy()
+        a["offset"] += a["normal"][:, 2] * deltas[i]
+        arrs.append(a)
+    s.set_contacts_batch(packed=(np.concatenate(arrs), np.full(S, len(base), np.int32)))
+    return s, v0s, deltas
+
+
+def test_cfg5_full_size_penetrating_iterations(simmod):
+    """cfg5 at full size in the bench's launch configuration (S = 1024, tensor-core K-passes),
+    the 8 deepest initial penetrations (delta up to +5 mm): EVERY L-G iteration of the frame,
+    re-synced (the oracle runs the body of Alg. 4, once from the GPU's own iterate
+    (x^k, lambda^k)), within the plain 1e-5 bbox bound, no conditioning guard.  Frame-level
+    parity of these frames at 5 iterations is tested with the fp32 CUDA-core K-passes
+    (test_cfg5_full_size_fp32_kpasses_penetrating_frames); DESIGN.md §3 (conditioning)."""
+    sc = scenes.make_scene("cfg3")
+    S = 1024
+    s, v0s, deltas = _cfg5_batch(simmod, sc, S)
+    X0 = np.broadcast_to(sc.mesh.X, (S,) + sc.mesh.X.shape)
+    deep = [int(c) for c in np.argsort(-deltas)[:8]]
+    its = {i: [] for i in deep}
+    for k in range(1, 6):
+        s.set_states(X0, v0s)
+        s.step(1, k)
+        P = s.get_positions()
+        for i in deep:
+            its[i].append((P[i].copy(), s.get_lambda(i).copy()))
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    worst = 0.0
+    for i in deep:
+        _, cs = scenes.batch_instance(sc, i)
+        o = O.Oracle(sc.mesh, sc.material, sc.h)
+        o.set_contacts(cs)
+        pins = sc.mesh.X[o.pinned] + sc.h * sc.pin_velocity
+        prev = None
+        for k, (xg, lg) in enumerate(its[i]):
+            o.lg_iters = k + 1
+            start = None if prev is None else (prev[0], prev[1], k)
+            xo, _, _ = o.frame(sc.mesh.X.copy(), v0s[i], pin_targets=pins, start=start)
+            e = float(np.abs(xg - xo).max()) / tol
+            assert e <= 1.0, (i, deltas[i], k, e)
+            worst = max(worst, e)
+            prev = (xg, lg)
+    print(f"worst re-synced iteration err/tol over the 8 deepest penetrations: {worst:.4f}")
+
+
+def test_cfg5_full_size_fp32_kpasses_penetrating_frames(simmod):
+    """cfg5 at full size (S = 1024) with the batched fp32 CUDA-core K-passes
+    (sim_set_kpass_mode(1)): the whole 5-iteration frame of the 8 deepest initial penetrations
+    within the plain 1e-5 bbox bound of the oracle, classification identical outside the A21
+    band.  (The tensor-core K-apply -- 3xTF32 products, fp32 TMEM accumulation, 2.6e-6 relative,
+    inside the north star's 1e-5 SpMV bound -- seeds these frames 15x more than fp32 rounding and
+    their non-smooth frame map amplifies it past 1e-5 bbox on 4 of the 32 deepest:
+    profiles/r02_cfg5_parity_scan_modes.txt.)"""
+    sc = scenes.make_scene("cfg3")
+    S = 1024
+    s, v0s, deltas = _cfg5_batch(simmod, sc, S)
+    s.set_kpass_mode(1)
+    X0 = np.broadcast_to(sc.mesh.X, (S,) + sc.mesh.X.shape)
+    s.set_states(X0, v0s)
+    s.step(1, 5)
+    P = s.get_positions()
+    assert np.isfinite(P).all()
+    tol = 1e-5 * sc.mesh.bbox_diag()
+    for i in [int(c) for c in np.argsort(-deltas)[:8]]:
+        _, cs = scenes.batch_instance(sc, i)
+        o = O.Oracle(sc.mesh, sc.material, sc.h)
+        o.set_contacts(cs)
+        pins = sc.mesh.X[o.pinned] + sc.h * sc.pin_velocity
+        xo, _, info = o.frame(sc.mesh.X.copy(), v0s[i], pin_targets=pins)
+        err = np.abs(P[i] - xo).max()
+        assert err <= tol, (i, deltas[i], err / tol)
+        bad, n = _parity.classification_mismatches(o, P[i], sc.mesh.X, s.get_lambda(i), xo, info["lam"], tol)
+        assert bad == 0, (i, bad, n)
+
+
 @pytest.mark.parametrize("model", [1, 2])
 def test_batched_materials_with_contacts(simmod, model):
     """Corotated and ARAP (closed-form local steps, their own k_local instantiations) with
