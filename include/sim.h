@@ -399,6 +399,12 @@ int sim_debug_contact_rho(sim_handle *h, int32_t instance, double *rho);
  * solve: [1] rho built, [2] active set + G_A gathered, [3 + it] after CR
  * iteration it, [20] loop end, [21] epilogue end.  out must hold 32 doubles. */
 int sim_debug_cr_timeline(sim_handle *h, double *out);
+/* Per-tile timeline of the plane K-passes (CTA (0, 0) of the last pass-1 / pass-2 launch, first 64
+ * tiles; out[4][64][8] %globaltimer ns: MMA warp [K tile landed, V_lo(c=0) seen, V_lo(c=2) seen,
+ * committed], workers [copies landed, V_lo written, fold done, next copies issued]; out[p][63][0] =
+ * CTA start, out[p][62][0] = tile count).  Caller-owned buffer of 2048 values; all zero unless the
+ * library was built with -DSIM_PL_TIMELINE (tools/pl_timeline.py).  Returns a cudaError_t code. */
+int sim_debug_pl_timeline(unsigned long long *out);
 /* Failure-injection hook: the next frame (run outside the captured graph) writes a NaN into
  * vertex 0 of `instance` right after the prediction step, so the end-of-frame check must roll
  * that instance back to its frame-start state and sim_synchronize must report

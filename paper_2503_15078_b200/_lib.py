@@ -16,7 +16,7 @@ EXPORTED_SYMBOLS = [
     "sim_synchronize", "sim_set_pin_velocity", "sim_get_state", "sim_set_state", "sim_get_lambda",
     "sim_get_stats", "sim_set_stream", "sim_destroy", "sim_last_error", "sim_debug_get_inverse",
     "sim_debug_apply_inverse", "sim_debug_local", "sim_debug_get_delassus", "sim_set_profiling",
-    "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_set_contacts_batch",
+    "sim_get_kernel_times", "sim_debug_contact_state", "sim_debug_cr_timeline", "sim_debug_pl_timeline", "sim_set_contacts_batch",
     "sim_get_positions", "sim_set_states", "sim_set_cr_mode", "sim_set_ncp", "sim_set_admm", "sim_set_kpass_mode", "sim_debug_poison", "sim_get_positions_async",
     "sim_wait_positions", "sim_detect_contacts", "sim_get_contacts",
     "sim_set_schur_reuse", "sim_set_lambda", "sim_set_pins", "sim_set_allocator", "sim_set_warm_start", "sim_set_persistent", "sim_set_local_mode", "sim_debug_contact_rho",

@@ -2343,3 +2343,8 @@ extern "C" int sim_debug_cr_timeline(sim_handle* H, double* out) {
     for (int i = 0; i < 32; ++i) out[i] = (double)(t[i] - t[0]) * 1e-3;   // us since start
     return SIM_OK;
 }
+
+namespace simdev { int debug_pl_clock(unsigned long long* out); }
+// plane K-pass timeline of CTA (0, 0): [pass][tile][8] %globaltimer stamps (all zero unless built with
+// -DSIM_PL_TIMELINE; tools/pl_timeline.py)
+extern "C" int sim_debug_pl_timeline(unsigned long long* out) { return simdev::debug_pl_clock(out); }

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -1407,6 +1408,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
             : "memory");
     }
 }
+// warp-uniform wait (the whole warp leaves the loop together: the code after it is provably converged,
+// so warp-uniform values stay in uniform registers)
+__device__ __forceinline__ void mbar_wait_w(uint64_t* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned done = 0;
+    while (!__all_sync(0xffffffffu, done)) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
 // global -> shared bulk copy completing `bytes` on `bar`; evict-first in L2 when `stream`
 __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar, bool stream,
                                          unsigned long long pol) {
@@ -1981,6 +1995,29 @@ __device__ __forceinline__ void umma_pl_ss(uint32_t dt, uint64_t da, uint64_t db
         "l"(da), "l"(db), "r"(kIdescPlS), "r"(acc)
         : "memory");
 }
+// warp-converged variants: the whole warp runs the issue loop (its descriptors are warp-uniform, so
+// they live in uniform registers) and elect.sync picks the one lane that issues; the same lane (the
+// lowest) issues every MMA and commit, as tcgen05.commit tracks the issuing thread's operations
+__device__ __forceinline__ void umma_pl_ss_w(uint32_t dt, uint64_t da, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+        "l"(da), "l"(db), "r"(kIdescPlS), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_pl_ts_w(uint32_t dt, uint32_t at, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dt),
+        "r"(at), "l"(db), "r"(kIdescPlT), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+    asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+                 " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void umma_pl_ts(uint32_t dt, uint32_t at, uint64_t db, uint32_t acc) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -2002,6 +2039,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ float tf32_trunc(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
+__device__ unsigned long long g_pl_clock[4][64][8];   // plane K-pass timeline of CTA (0, 0), first 64 tiles (SIM_PL_TIMELINE builds)
+__device__ __forceinline__ void pl_stamp(int pass, int t, int k) {
+#ifdef SIM_PL_TIMELINE   // build with SIM_NVCC_EXTRA=-DSIM_PL_TIMELINE for tools/pl_timeline.py
+    if (blockIdx.x == 0 && blockIdx.y == 0 && t < 64) {
+        unsigned long long v;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+        g_pl_clock[pass][t][k] = v;
+    }
+#endif
+}
+int debug_pl_clock(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_pl_clock, sizeof(g_pl_clock));
+}
 template <int PASS>
 __global__ void __launch_bounds__(kPlThreads + 64, 1)
     k_kpass_pl(int S, int Sp, int n_f, const BUnit* __restrict__ units, const float* __restrict__ T,
@@ -2010,7 +2060,7 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
                const double4* __restrict__ xt, double4* __restrict__ v, double inv_h, int finalize_v, int drain) {
     pdl_enter();
     extern __shared__ unsigned char pl_raw[];
-    __shared__ __align__(8) uint64_t mdone[kPlStages], lofull[3], lofree[3], dfree;
+    __shared__ __align__(8) uint64_t mdone[kPlStages], lofull[4], lofree[4], dfree;
     __shared__ __align__(8) uint64_t bfull[kPlBStages], bempty[kPlBStages];
     __shared__ uint32_t tmem_base_s;
     __shared__ int s_last;
@@ -2033,9 +2083,9 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
     if (tid == 0) {
         // worker-side barriers count one elected arrival per worker warp (after __syncwarp)
         for (int s2 = 0; s2 < kPlStages; ++s2) mbar_init(&mdone[s2], 1);
-        for (int c = 0; c < 3; ++c) {
-            mbar_init(&lofull[c], kPlWarps);
-            mbar_init(&lofree[c], 1);
+        for (int k = 0; k < 4; ++k) {
+            mbar_init(&lofull[k], kPlWarps);
+            mbar_init(&lofree[k], 1);
         }
         for (int s2 = 0; s2 < kPlBStages; ++s2) {
             mbar_init(&bfull[s2], 1);
@@ -2049,6 +2099,9 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_base_s;
     const int nt = U.ntiles;
+#ifdef SIM_PL_TIMELINE
+    if (tid == 0) { pl_stamp(PASS - 1, 63, 0); if (blockIdx.x == 0 && blockIdx.y == 0) g_pl_clock[PASS - 1][62][0] = nt; }
+#endif
     if (kload_warp) {
         // K tiles: one bulk copy each, kPlBStages ahead of the tensor core
         if (lane == 0) {
@@ -2061,29 +2114,35 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
         }
         __syncwarp();
     } else if (mma_warp) {
-        if (lane == 0) {
+        {   // the whole warp runs the loop (uniform descriptors); one elected lane issues
+            const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_base_s, 0);
             for (int t = 0; t < nt; ++t) {
                 const int st = t % kPlStages, sb = t % kPlBStages;
-                mbar_wait(&bfull[sb], (unsigned)(t / kPlBStages) & 1u);
-                if (t > 0 && t % drain == 0) mbar_wait(&dfree, (unsigned)(t / drain - 1) & 1u);
+                mbar_wait_w(&bfull[sb], (unsigned)(t / kPlBStages) & 1u);
+                pl_stamp(PASS - 1, t, 0);
+                if (t > 0 && t % drain == 0) mbar_wait_w(&dfree, (unsigned)(t / drain - 1) & 1u);
                 const uint32_t abase = sm_a + st * kPlA, bbase = sm_a + kPlBOff + sb * kPlB;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     // V_lo of component c written (and this tile's V_hi copies visible to the tensor core)
-                    mbar_wait(&lofull[c], (unsigned)t & 1u);
+                    const int sl = 3 * t + c, ks = sl & 3;   // V_lo slot of (t, c): 4 slots rotate over the 3 components
+                    mbar_wait_w(&lofull[ks], (unsigned)(sl >> 2) & 1u);
+                    if (c == 0) pl_stamp(PASS - 1, t, 1);
+                    if (c == 2) pl_stamp(PASS - 1, t, 2);
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                     const uint32_t dt = tmem + 128u * c;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t da = umma_desc_mn32(abase + 16384u * c + 1024u * kk);
                         const uint64_t db = umma_desc_k(bbase + 256u * kk);   // [K_hi ; K_lo]: N = 128
-                        umma_pl_ss(dt, da, db, (t % drain != 0 || kk > 0) ? 1u : 0u);
-                        umma_pl_ts(dt, tmem + 384u + 32u * c + 8u * kk, db, 1u);      // V_lo K_hi: N = 64
+                        umma_pl_ss_w(dt, da, db, (t % drain != 0 || kk > 0) ? 1u : 0u);
+                        umma_pl_ts_w(dt, tmem + 384u + 32u * ks + 8u * kk, db, 1u);      // V_lo K_hi: N = 64
                     }
-                    umma_commit(&lofree[c]);   // the lo slot of component c may be rewritten
+                    umma_commit_w(&lofree[ks]);   // the lo slot may be rewritten
                 }
-                umma_commit(&mdone[st]);
-                umma_commit(&bempty[sb]);
+                umma_commit_w(&mdone[st]);
+                pl_stamp(PASS - 1, t, 3);
+                umma_commit_w(&bempty[sb]);
             }
         }
         __syncwarp();
@@ -2099,6 +2158,17 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
             const int q = w + 16 * e;
             dsto[e] = 4096u * (lane >> 3) + 128u * q + 32u * (((lane & 7) >> 1) ^ (q & 3)) + 16u * (lane & 1);
         }
+        // pass 2: the cover rows of a tile are read one tile before its copies are issued (the
+        // dependent index load is off the copy issue path)
+        int crow[2] = {0, 0};
+        auto load_cover = [&](int t) {
+            if (PASS == 2)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int q = w + 16 * e;
+                    crow[e] = (t < nt && 32 * t + q < U.nlist) ? __ldg(&cover[U.list0 + 32 * t + q]) : 0;
+                }
+        };
         auto issue = [&](int t) {
             const int st = t % kPlStages;
             const uint32_t abase = sm_a + st * kPlA;
@@ -2112,7 +2182,7 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
                     ok = r < n_f;
                 } else {
                     ok = 32 * t + q < U.nlist;
-                    r = ok ? __ldg(&cover[U.list0 + 32 * t + q]) : 0;
+                    r = crow[e];
                 }
                 ok = ok && ilive4;
                 const float* src = ok ? vin + (size_t)r * Sp + inst4 : vin;
@@ -2155,8 +2225,11 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         };
+        load_cover(0);
         issue(0);
+        load_cover(1);
         if (nt > 1) issue(1);
+        load_cover(2);
         // per tile t: V_lo(t) as soon as its copies landed (MMA(t - 1) runs meanwhile), then the fold
         // of a closed accumulation group, then the copies of tile t + 2 into the stage MMA(t - 1) frees
         for (int t = 0; t < nt; ++t) {
@@ -2165,6 +2238,7 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
             // worker's (a named barrier of the 16 worker warps)
             if (t + 1 < nt) cp_async_wait<1>(); else cp_async_wait<0>();
             asm volatile("bar.sync 1, %0;\n" ::"r"(kPlThreads) : "memory");
+            if (tid == 0) pl_stamp(PASS - 1, t, 4);
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> async proxy
             // V_lo of rows 8 oc .. 8 oc + 7 (K-step oc) for instance 32 qd + lane, one component at a
             // time into its TMEM slot once the tensor core has read the previous tile's
@@ -2179,16 +2253,18 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
                                                                     4 * (lane & 7));
                     lo[r] = __float_as_uint(tf32_rn(a - tf32_trunc(a)));
                 }
-                if (t >= 1) mbar_wait(&lofree[c], (unsigned)(t - 1) & 1u);
+                const int sl = 3 * t + c, ks = sl & 3;
+                if (sl >= 4) mbar_wait(&lofree[ks], (unsigned)((sl >> 2) - 1) & 1u);   // its previous MMA read it
                 asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
-                                 lanebase + 384u + 32u * c + 8u * oc),
+                                 lanebase + 384u + 32u * ks + 8u * oc),
                              "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7])
                              : "memory");
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&lofull[c]);
+                if (lane == 0) mbar_arrive(&lofull[ks]);
             }
+            if (tid == 0) pl_stamp(PASS - 1, t, 5);
             // the group of tiles ending at t - 1 is complete once MMA(t - 1) is: fold it, free D
             if (t > 0 && t % drain == 0) {
                 mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
@@ -2196,12 +2272,15 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&dfree);
             }
+            if (tid == 0) pl_stamp(PASS - 1, t, 6);
             if (t + 2 < nt) {
                 if (t >= 1) mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
                 // every worker has passed this iteration's barrier, i.e. finished reading stage
                 // (t + 2) % 3 = (t - 1) % 3 for its V_lo in iteration t - 1
                 issue(t + 2);
+                load_cover(t + 3);
             }
+            if (tid == 0) pl_stamp(PASS - 1, t, 7);
         }
         if (nt > 0) {
             mbar_wait(&mdone[(nt - 1) % kPlStages], (unsigned)((nt - 1) / kPlStages) & 1u);
@@ -2997,8 +3076,9 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
     int idx = blockIdx.x, bs = 0;
     while (idx >= tiles - bs) { idx -= tiles - bs; ++bs; }
     const int bt = bs + idx;
-    constexpr int NST = 4;   // chunks of 32 depth levels in flight (cp.async straight into shared memory)
+    constexpr int NST = 3;   // chunks of 32 depth levels in flight (cp.async straight into shared memory)
     __shared__ float Zs[NST][32][33], Zt[NST][32][33];
+    __shared__ double Ds[32][33], Dt[32][33];   // the chunk being consumed, converted to fp64 once
     __shared__ int ds_[32], dt_[32];
     __shared__ int64_t cs_[32], ct_[32];
     __shared__ int smax;
@@ -3014,13 +3094,13 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
     }
     if (tid == 0) smax = -1;
     __syncthreads();
-    // thread owns pairs (ls, lt0..lt0+3)
-    const int ls = tid >> 3, lt0 = (tid & 7) * 4;
+    // thread owns pairs (ls, lt0 + 8 q), q = 0..3 (the fp64 reads of Dt hit distinct banks)
+    const int ls = tid >> 3, lt0 = tid & 7;
     const int s = bs * 32 + ls;
     int dl[4];
     int maxd = -1;
     for (int q = 0; q < 4; ++q) {
-        const int t = bt * 32 + lt0 + q;
+        const int t = bt * 32 + lt0 + 8 * q;
         dl[q] = (s < ns && t < ns) ? lca_depth(slot_vtx[s], slot_vtx[t], parent, ptop, depth) : -1;
         maxd = max(maxd, dl[q]);
     }
@@ -3055,17 +3135,27 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
         __syncthreads();            // ... everyone's; and chunk c - 1 is consumed everywhere
         issue(c + NST - 1);         // into the stage chunk c - 1 used
         const int st = c % NST, d0 = 32 * c;
+        // fp32 -> fp64 once per staged element (the products are exact in fp64 either way; converting
+        // in the FMA loop cost 5 conversions per 4 DFMA and bound the kernel)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + 256 * u;
+            const int dd = e >> 5, sl = e & 31;
+            Ds[dd][sl] = (double)Zs[st][dd][sl];
+            Dt[dd][sl] = (double)Zt[st][dd][sl];
+        }
+        __syncthreads();
 #pragma unroll 8
         for (int dd = 0; dd < 32; ++dd) {
             const int d = d0 + dd;
-            const float zs = Zs[st][dd][ls];
+            const double zs = Ds[dd][ls];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (d <= dl[q]) acc[q] = fma((double)zs, (double)Zt[st][dd][lt0 + q], acc[q]);
+                if (d <= dl[q]) acc[q] = fma(zs, Dt[dd][lt0 + 8 * q], acc[q]);
         }
     }
     for (int q = 0; q < 4; ++q) {
-        const int t = bt * 32 + lt0 + q;
+        const int t = bt * 32 + lt0 + 8 * q;
         if (s < ns && t < ns) {
             G[(size_t)s * ns + t] = (float)acc[q];
             G[(size_t)t * ns + s] = (float)acc[q];
@@ -3381,9 +3471,33 @@ __device__ __forceinline__ void block_sum3(double& a, double& b, double& c, doub
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { a += red[3 * q]; b += red[3 * q + 1]; c += red[3 * q + 2]; }
 }
 
+// Per-thread row metadata of the contact-row map C^T (fixed for one CR solve: Theta and the active
+// slots do not change inside it), hoisted out of the CR iterations into registers: ip = the active
+// position of the row's single contact vertex (-2: theta = 0, -1: multi-vertex contact, mapped
+// through its vertex list).
+template <int kRpt>
+struct CrRows {
+    int ip[kRpt];
+};
+
+template <int kRpt>
+__device__ __forceinline__ void cr_rows_init(const CrCtx& X, int m, CrRows<kRpt>& R) {
+#pragma unroll
+    for (int k = 0; k < kRpt; ++k) {
+        const int j = min(threadIdx.x + kCrThreads * k, m - 1);
+        const int c = j / 3;
+        R.ip[k] = -2;
+        if (X.th[j] != 0.f) {
+            const int sl0 = X.s0[c];
+            R.ip[k] = sl0 >= 0 ? X.apos[sl0] : -1;
+        }
+    }
+}
+
 // Ar = S r for this thread's rows (registers); r is read from shared memory
 template <int kRpt>
-__device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int buf, double (&Ar)[kRpt]) {
+__device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int buf, double (&Ar)[kRpt],
+                                         const CrRows<kRpt>& R) {
     const int na = X.na;
     double* qb = X.q + (size_t)buf * 3 * X.na;   // SoA: q0 | q1 | q2
     const unsigned bar = X.mbar + 8u * (unsigned)buf;
@@ -3533,13 +3647,7 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
         d0 = warp_sum(d0);
         d1 = warp_sum(d1);
         d2 = warp_sum(d2);
-        if (solo) {
-            if (lane == 0) {
-                qb[i] = d0;
-                qb[na + i] = d1;
-                qb[2 * na + i] = d2;
-            }
-        } else if (lane < X.csize) {
+        if (lane < X.csize) {
             // asynchronous stores of q_i into CTA `lane` of the cluster, completing 24 tx bytes on its mbarrier
             const unsigned l0 = (unsigned)__cvta_generic_to_shared(qb + i);
             const unsigned l1 = (unsigned)__cvta_generic_to_shared(qb + na + i);
@@ -3580,22 +3688,19 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) {
         const int j = min(threadIdx.x + kCrThreads * k, m - 1);   // rows >= m are padding (never used)
-        const int c = j / 3, kk = j - 3 * c;
         const double th = (double)X.th[j];
         double acc = 0.0;
-        if (th != 0.0) {
-            const float* cc = X.c9 + 9 * c + 3 * kk;
-            const int sl0 = X.s0[c];
-            if (sl0 >= 0) {
-                const int ip = X.apos[sl0];
-                acc = (double)cc[0] * qb[ip] + (double)cc[1] * qb[na + ip] + (double)cc[2] * qb[2 * na + ip];
-            } else {
-                const DContact& ct = I.C[c];
-                for (int p = 0; p < ct.nv; ++p) {
-                    const int ip = X.apos[ct.slot[p] - I.sb];
-                    acc += ct.w[p] * ((double)cc[0] * qb[ip] + (double)cc[1] * qb[na + ip] +
-                                      (double)cc[2] * qb[2 * na + ip]);
-                }
+        const int ip = R.ip[k];
+        const int c = j / 3, kk = j - 3 * c;
+        const float* cc = X.c9 + 9 * c + 3 * kk;
+        if (ip >= 0) {
+            acc = (double)cc[0] * qb[ip] + (double)cc[1] * qb[na + ip] + (double)cc[2] * qb[2 * na + ip];
+        } else if (ip == -1) {
+            const DContact& ct = I.C[c];
+            for (int p = 0; p < ct.nv; ++p) {
+                const int iq = X.apos[ct.slot[p] - I.sb];
+                acc += ct.w[p] * ((double)cc[0] * qb[iq] + (double)cc[1] * qb[na + iq] +
+                                  (double)cc[2] * qb[2 * na + iq]);
             }
         }
         Ar[k] = th * acc + (double)X.cd[j] * X.r[j];
@@ -3757,6 +3862,8 @@ __global__ void __launch_bounds__(kCrThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     cl.sync();   // smem staged everywhere; every CTA's exchange mbarriers initialised
+    CrRows<kRpt> R;
+    cr_rows_init<kRpt>(X, m, R);
     cr_stamp(1);
     if (threadIdx.x == 0 && blockIdx.x == 0) {   // debug: na, G_A placement (1 = shared memory), csize
         g_cr_clock[31] = g_cr_clock[0] + 1000ull * na;
@@ -3771,7 +3878,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     cr_stamp(2);
     if (rr > 0.0 && P.cr_iters > 0) {
         int buf = 0;
-        cr_apply<kRpt>(X, m, I, buf, Ar);
+        cr_apply<kRpt>(X, m, I, buf, Ar, R);
         buf ^= 1;
         double rAr = 0.0, ApAp = 0.0, dummy = 0.0;
 #pragma unroll
@@ -3800,7 +3907,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
             if (it == P.cr_iters - 1) break;
             X.stamp = it == 3 ? 13 : -1;
             if (it == 3) cr_stamp(12);
-            cr_apply<kRpt>(X, m, I, buf, Ar);
+            cr_apply<kRpt>(X, m, I, buf, Ar, R);
             buf ^= 1;
             if (it == 3) cr_stamp(16);
             double s1 = 0.0, s2 = 0.0, s3 = 0.0;
