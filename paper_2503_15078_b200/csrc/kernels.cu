@@ -2412,6 +2412,15 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t dt, uint32_t at, uint64_t 
         : "memory");
 }
 
+// warp-converged issue (see umma_pl_ss_w)
+__device__ __forceinline__ void umma_tf32_ts_w(uint32_t dt, uint32_t at, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(dt),
+        "r"(at), "l"(db), "r"(kIdescTf32), "r"(acc)
+        : "memory");
+}
+
 template <int PASS>
 __global__ void __launch_bounds__(kTcThreads + 32, 1)
     k_kpass_ts(int S, int n_f, const BUnit* __restrict__ units, const float* __restrict__ Ttc,
@@ -2491,11 +2500,12 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     };
     if (mma_warp) {
-        if (lane == 0) {
+        {   // the whole warp runs the loop (uniform descriptors); one elected lane issues
+            const uint32_t tmem = __shfl_sync(0xffffffffu, tmem_base_s, 0);
             for (int t = 0; t < U.ntiles; ++t) {
                 const int st = t & 1;
-                mbar_wait(&afull[st], (t >> 1) & 1);
-                mbar_wait(&bfull[st], (t >> 1) & 1);
+                mbar_wait_w(&afull[st], (t >> 1) & 1);
+                mbar_wait_w(&bfull[st], (t >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 const uint32_t b0 = (unsigned)__cvta_generic_to_shared(bsm[st]);
                 const uint32_t b1 = b0 + 4096u;
@@ -2506,12 +2516,12 @@ __global__ void __launch_bounds__(kTcThreads + 32, 1)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t dbh = umma_desc_k(b0 + 256u * kk), dbl = umma_desc_k(b1 + 256u * kk);
-                        umma_tf32_ts(dt, ah + 8u * kk, dbh, (t % drain != 0 || kk > 0) ? 1u : 0u);
-                        umma_tf32_ts(dt, al + 8u * kk, dbh, 1u);
-                        umma_tf32_ts(dt, ah + 8u * kk, dbl, 1u);
+                        umma_tf32_ts_w(dt, ah + 8u * kk, dbh, (t % drain != 0 || kk > 0) ? 1u : 0u);
+                        umma_tf32_ts_w(dt, al + 8u * kk, dbh, 1u);
+                        umma_tf32_ts_w(dt, ah + 8u * kk, dbl, 1u);
                     }
                 }
-                umma_commit(&mdone[st]);
+                umma_commit_w(&mdone[st]);
             }
         }
         __syncwarp();
