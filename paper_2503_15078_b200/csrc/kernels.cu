@@ -687,28 +687,31 @@ __device__ __forceinline__ void jacobi3_2(v2 S[3][3], v2 V[3][3]) {
             const int q = pq == 0 ? 1 : 2;
             const int r = 3 - p - q;
             const v2 apq = S[p][q];
-            const bool rx = !cx && fabsf(apq.a.x) > 1e-30f, ry = !cy && fabsf(apq.a.y) > 1e-30f;   // rotate this lane
-            const v2 theta = (S[q][q] - S[p][p]) * rcp2(v2(2.f) * apq);
-            const v2 at = abs2(theta);
-            const v2 w = fma2(theta, theta, v2(1.f));
-            v2 t = rcp2(fma2(w, rsqrt2(w), at));
-            if (at.a.x > 1e15f) t.a.x = 0.5f * rcp_ftz(at.a.x);
-            if (at.a.y > 1e15f) t.a.y = 0.5f * rcp_ftz(at.a.y);
-            t = sel2(theta.a.x < 0.f, theta.a.y < 0.f, v2(-t.a.x, -t.a.y), t);
+            // rotate this lane (|a_pq| > 1e-18 keeps 4 a_pq^2 a normal fp32 number)
+            const bool rx = !cx && fabsf(apq.a.x) > 1e-18f, ry = !cy && fabsf(apq.a.y) > 1e-18f;
+            // t = tan(phi), the smaller root of t^2 + 2 theta t - 1 = 0 with theta = d / (2 a_pq),
+            // d = a_qq - a_pp, written without theta: t = sgn(d) 2 a_pq / (|d| + sqrt(d^2 + 4 a_pq^2))
+            // (two MUFU operations per lane instead of three, no overflow branch)
+            const v2 d = S[q][q] - S[p][p];
+            const v2 a2 = apq + apq;
+            const v2 rr = fma2(d, d, a2 * a2);
+            v2 t = a2 * rcp2(fma2(rr, rsqrt2(rr), abs2(d)));
+            t = sel2(d.a.x < 0.f, d.a.y < 0.f, v2(-t.a.x, -t.a.y), t);
             t = sel2(rx, ry, t, v2(0.f));   // null rotation (c = 1, s = 0) for a lane that skips
             const v2 c = rsqrt2(fma2(t, t, v2(1.f)));
             const v2 sn = t * c;
+            const v2 nsn(-sn.a.x, -sn.a.y);
             const v2 ta = t * apq;
             S[p][p] = S[p][p] - ta;
             S[q][q] = S[q][q] + ta;
             S[p][q] = S[q][p] = sel2(rx, ry, v2(0.f), apq);
             const v2 srp = S[r][p], srq = S[r][q];
-            S[r][p] = S[p][r] = fma2(c, srp, v2(0.f) - sn * srq);
+            S[r][p] = S[p][r] = fma2(nsn, srq, c * srp);
             S[r][q] = S[q][r] = fma2(sn, srp, c * srq);
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const v2 vkp = V[k][p], vkq = V[k][q];
-                V[k][p] = fma2(c, vkp, v2(0.f) - sn * vkq);
+                V[k][p] = fma2(nsn, vkq, c * vkp);
                 V[k][q] = fma2(sn, vkp, c * vkq);
             }
         }
