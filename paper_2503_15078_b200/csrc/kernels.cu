@@ -847,7 +847,10 @@ __device__ __forceinline__ void project_sigma2(const v2 sg[3], float kf, float m
 }
 
 template <int MODEL>
-__global__ void __launch_bounds__(128, MODEL == 0 ? 5 : 6) k_local2(Params P, const int4* __restrict__ tet,
+#ifndef SIM_LOCAL2_MINB
+#define SIM_LOCAL2_MINB 5
+#endif
+__global__ void __launch_bounds__(128, MODEL == 0 ? SIM_LOCAL2_MINB : 6) k_local2(Params P, const int4* __restrict__ tet,
                                                                      const float* __restrict__ Bm,
                                                                      const float* __restrict__ hw2,
                                                                      const double4* __restrict__ x, float* __restrict__ fc) {
@@ -1973,8 +1976,14 @@ __device__ __forceinline__ float tf32_rn(float v) {
 constexpr int kPlInst = 128;
 constexpr int kPlWarps = 16;
 constexpr int kPlThreads = 32 * kPlWarps;
-constexpr int kPlStages = 3;
-constexpr int kPlBStages = 5;                     // K tiles run further ahead (they come from HBM)
+#ifndef SIM_PL_STAGES
+#define SIM_PL_STAGES 3
+#endif
+#ifndef SIM_PL_BSTAGES
+#define SIM_PL_BSTAGES 5
+#endif
+constexpr int kPlStages = SIM_PL_STAGES;           // V_hi stages
+constexpr int kPlBStages = SIM_PL_BSTAGES;         // K tiles run further ahead (they come from HBM)
 constexpr uint32_t kPlA = 3u * 16384u;            // V_hi: 3 components x 4 blocks x (32 rows x 128 B)
 constexpr uint32_t kPlB = 16384u;                 // K hi (8 KB) + lo (8 KB), 64 x 32 each
 constexpr uint32_t kPlBOff = kPlStages * kPlA;    // the K-tile stages follow the V_hi stages
@@ -2277,9 +2286,10 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
             }
             if (tid == 0) pl_stamp(PASS - 1, t, 6);
             if (t + 2 < nt) {
-                if (t >= 1) mbar_wait(&mdone[(t - 1) % kPlStages], (unsigned)((t - 1) / kPlStages) & 1u);
-                // every worker has passed this iteration's barrier, i.e. finished reading stage
-                // (t + 2) % 3 = (t - 1) % 3 for its V_lo in iteration t - 1
+                // stage (t + 2) % kPlStages was last read by MMA(t + 2 - kPlStages); every worker has
+                // passed this iteration's barrier, i.e. finished its V_lo reads of that stage
+                const int tp = t + 2 - kPlStages;
+                if (tp >= 0) mbar_wait(&mdone[tp % kPlStages], (unsigned)((tp / kPlStages) & 1));
                 issue(t + 2);
                 load_cover(t + 3);
             }
