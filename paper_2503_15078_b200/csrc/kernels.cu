@@ -2160,15 +2160,19 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
         __syncwarp();
     } else {
         // ---- workers: copies, V_lo, folds ----
-        // this thread's copies: 16-byte chunk j = lane of rows q = w and w + 16 of the 3 planes (the
-        // 3 x 32 rows x 128 instances of a tile = 3072 chunks over 512 threads)
-        const int inst4 = i0 + 4 * lane;
+        // each worker warp copies exactly the V_hi rows it later reads for its V_lo (rows 8 oc .. 8 oc + 7
+        // of the 32-instance block qd, 3 planes): 192 16-byte chunks per warp, 6 per lane; the warps
+        // then need no CTA-wide barrier per tile (each waits for its own copies; the tensor core sees
+        // every warp's through the lofull arrivals)
+        const int qd = w & 3, oc = w >> 2;     // TMEM lane quadrant (= 32-instance block) / row octet
+        const int ch = lane & 7;                // 16-byte chunk (4 instances) of a 128-byte row
+        const int inst4 = i0 + 32 * qd + 4 * ch;
         const bool ilive4 = inst4 < Sp;
         uint32_t dsto[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const int q = w + 16 * e;
-            dsto[e] = 4096u * (lane >> 3) + 128u * q + 32u * (((lane & 7) >> 1) ^ (q & 3)) + 16u * (lane & 1);
+            const int q = 8 * oc + (lane >> 3) + 4 * e;
+            dsto[e] = 4096u * qd + 128u * q + 32u * ((ch >> 1) ^ (q & 3)) + 16u * (ch & 1);
         }
         // pass 2: the cover rows of a tile are read one tile before its copies are issued (the
         // dependent index load is off the copy issue path)
@@ -2177,7 +2181,7 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
             if (PASS == 2)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const int q = w + 16 * e;
+                    const int q = 8 * oc + (lane >> 3) + 4 * e;
                     crow[e] = (t < nt && 32 * t + q < U.nlist) ? __ldg(&cover[U.list0 + 32 * t + q]) : 0;
                 }
         };
@@ -2186,7 +2190,7 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
             const uint32_t abase = sm_a + st * kPlA;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int q = w + 16 * e;
+                const int q = 8 * oc + (lane >> 3) + 4 * e;
                 int r;
                 bool ok;
                 if (PASS == 1) {
@@ -2204,7 +2208,6 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
             }
             cp_async_commit();
         };
-        const int qd = w & 3, oc = w >> 2;     // TMEM lane quadrant (= 32-instance block) / row octet
         const uint32_t lanebase = tmem + ((uint32_t)(32 * qd) << 16);
         float acc[3][16];
 #pragma unroll
@@ -2246,25 +2249,27 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
         // of a closed accumulation group, then the copies of tile t + 2 into the stage MMA(t - 1) frees
         for (int t = 0; t < nt; ++t) {
             const int st = t % kPlStages;
-            // this thread's copies of tile t have landed (tile t + 1's may still fly), then every
-            // worker's (a named barrier of the 16 worker warps)
+            // this thread's copies of tile t have landed (tile t + 1's may still fly), then the warp's
             if (t + 1 < nt) cp_async_wait<1>(); else cp_async_wait<0>();
-            asm volatile("bar.sync 1, %0;\n" ::"r"(kPlThreads) : "memory");
+            __syncwarp();
             if (tid == 0) pl_stamp(PASS - 1, t, 4);
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // cp.async data -> async proxy
             // V_lo of rows 8 oc .. 8 oc + 7 (K-step oc) for instance 32 qd + lane, one component at a
             // time into its TMEM slot once the tensor core has read the previous tile's
             const unsigned char* ab = sm + st * kPlA + 4096 * qd;
+            uint32_t lo3[3][8];   // all three components first: the shared-memory loads leave the hand-off path
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                uint32_t lo[8];
+            for (int c = 0; c < 3; ++c)
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const int q = 8 * oc + r;
                     const float a = *reinterpret_cast<const float*>(ab + 16384 * c + 128 * q + 32 * ((lane >> 3) ^ (q & 3)) +
                                                                     4 * (lane & 7));
-                    lo[r] = __float_as_uint(tf32_rn(a - tf32_trunc(a)));
+                    lo3[c][r] = __float_as_uint(tf32_rn(a - tf32_trunc(a)));
                 }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const uint32_t* lo = lo3[c];
                 const int sl = 3 * t + c, ks = sl & 3;
                 if (sl >= 4) mbar_wait(&lofree[ks], (unsigned)((sl >> 2) - 1) & 1u);   // its previous MMA read it
                 asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(
