@@ -1,4 +1,5 @@
-"""DEBUG: plane K-pass per-tile timeline of CTA (0, 0) at S = 1024 (the largest unit, sorted first)."""
+"""Plane K-pass per-tile timeline of CTA (0, 0) at S = 1024 (the largest unit, sorted first); needs a
+library built with SIM_NVCC_EXTRA=-DSIM_PL_TIMELINE (sim_debug_pl_timeline)."""
 import os, sys, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np

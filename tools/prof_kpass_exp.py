@@ -1,4 +1,4 @@
-"""cfg5 (S = 1024) per-frame kernel times from in-graph events (K-pass experiments: SIM_PL_EXP)."""
+"""cfg5 (S = 1024) per-frame kernel times from in-graph events, frames restarted from the cfg5 initial states (K-pass A/B runs)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
