@@ -3395,14 +3395,24 @@ struct CrLayout {
 // CR shape of one instance: the G_A row stride in shared memory and the column groups of the
 // one-CTA-per-instance matvec
 __host__ __device__ inline int cr_lda(int na, int csize) { return csize == 1 ? (na | 1) : na; }
-__host__ __device__ inline int cr_parts(int na, int csize) {
+__host__ __device__ inline int cr_parts_max(int na, int csize) {
     return csize == 1 ? max(1, min(4, kCrThreads / max(32, (na + 31) & ~31))) : 1;
+}
+// column groups of the one-CTA matvec: as many as keep the threads busy, unless their partial-sum
+// buffer (qp) is what keeps G_A out of shared memory -- G_A resident beats the extra parallelism
+__host__ __device__ inline int cr_parts(int nc, int ns, int na, int csize) {
+    const int P = cr_parts_max(na, csize);
+    if (P == 1) return 1;
+    const size_t ga = (size_t)na * cr_lda(na, csize) * sizeof(float);
+    if (CrLayout(nc, ns, na, false, P).total + ga > kCrMaxSmem && CrLayout(nc, ns, na, false, 1).total + ga <= kCrMaxSmem)
+        return 1;
+    return P;
 }
 // a lone CTA holds the whole instance and its G_A fits next to the minimal layout: it gathers
 // G_A from the class Gram itself (k_active skips the global copy)
 __host__ __device__ bool cr_ga_direct(int nc, int ns, int na, int csize) {
     if (csize != 1) return false;
-    return CrLayout(nc, ns, na, false, cr_parts(na, csize)).total + (size_t)na * cr_lda(na, csize) * sizeof(float) <=
+    return CrLayout(nc, ns, na, false, cr_parts(nc, ns, na, csize)).total + (size_t)na * cr_lda(na, csize) * sizeof(float) <=
            kCrMaxSmem;
 }
 
@@ -3566,35 +3576,61 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
     __syncthreads();
     if (X.stamp >= 0) cr_stamp(X.stamp);
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    if (solo && X.gA_smem) {
-        // one row of G_A per thread (odd row stride: the 32 rows a warp reads sit in 32 banks; W is a
-        // broadcast), the columns split over `parts` groups of threads whose partial sums are added in
-        // part order (deterministic); no warp reductions
+    if (solo) {
+        // one row of G_A per thread, the columns split over `parts` groups of threads whose partial sums
+        // are added in part order (deterministic); no warp reductions.  G_A in shared memory: row i at
+        // stride lda (odd: the 32 rows a warp reads sit in 32 banks; W is a broadcast).  G_A in global
+        // memory (too large for shared memory): G_A is symmetric (G_A[b][i] = G_A[i][b], both written
+        // from one sum), so thread i reads column i -- a warp's 32 rows are 128 contiguous bytes of row
+        // b, coalesced -- and the result is bitwise that of the shared-memory path
         const int nap = (na + 31) & ~31, P = X.parts, cs = (na + P - 1) / P;
+        const bool sm_ga = X.gA_smem;
         for (int t = threadIdx.x; t < nap * P; t += blockDim.x) {
             const int part = t / nap, i = t - part * nap;
             if (i >= na) continue;
-            const float* g = X.gA + (size_t)i * X.lda;
             const int b1 = min(na, (part + 1) * cs);
             int b = part * cs;
             double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-            for (; b + 4 <= b1; b += 4) {
-                float gv[4];
+            if (sm_ga) {
+                const float* g = X.gA + (size_t)i * X.lda;
+                for (; b + 4 <= b1; b += 4) {
+                    float gv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) gv[u] = g[b + u];
+                    for (int u = 0; u < 4; ++u) gv[u] = g[b + u];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const double gd = (double)gv[u];
-                    d0 = fma(gd, X.W[b + u], d0);
-                    d1 = fma(gd, X.W[na + b + u], d1);
-                    d2 = fma(gd, X.W[2 * na + b + u], d2);
+                    for (int u = 0; u < 4; ++u) {
+                        const double gd = (double)gv[u];
+                        d0 = fma(gd, X.W[b + u], d0);
+                        d1 = fma(gd, X.W[na + b + u], d1);
+                        d2 = fma(gd, X.W[2 * na + b + u], d2);
+                    }
                 }
-            }
-            for (; b < b1; ++b) {
-                const double gd = (double)g[b];
-                d0 = fma(gd, X.W[b], d0);
-                d1 = fma(gd, X.W[na + b], d1);
-                d2 = fma(gd, X.W[2 * na + b], d2);
+                for (; b < b1; ++b) {
+                    const double gd = (double)g[b];
+                    d0 = fma(gd, X.W[b], d0);
+                    d1 = fma(gd, X.W[na + b], d1);
+                    d2 = fma(gd, X.W[2 * na + b], d2);
+                }
+            } else {
+                const float* g = X.GAg + i;   // column i
+                for (; b + 8 <= b1; b += 8) {
+                    float gv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) gv[u] = __ldcg(g + (size_t)(b + u) * na);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const double gd = (double)gv[u];
+                        d0 = fma(gd, X.W[b + u], d0);
+                        d1 = fma(gd, X.W[na + b + u], d1);
+                        d2 = fma(gd, X.W[2 * na + b + u], d2);
+                    }
+                }
+                for (; b < b1; ++b) {
+                    const double gd = (double)__ldcg(g + (size_t)b * na);
+                    d0 = fma(gd, X.W[b], d0);
+                    d1 = fma(gd, X.W[na + b], d1);
+                    d2 = fma(gd, X.W[2 * na + b], d2);
+                }
             }
             double* o = P > 1 ? X.qp + (size_t)part * 3 * na : qb;
             o[i] = d0;
@@ -3607,50 +3643,6 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
                 double acc = X.qp[e];
                 for (int q = 1; q < P; ++q) acc += X.qp[(size_t)q * 3 * na + e];
                 qb[e] = acc;
-            }
-        }
-    } else if (solo) {   // G_A in global memory: four rows per warp at a time (8 G_A loads in flight per lane)
-        for (int i = wid; i < na; i += 4 * nw) {
-            double d[4][3];
-            const float* g[4];
-            bool ok[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int ik = i + k * nw;
-                ok[k] = ik < na;
-                g[k] = X.GAg + (size_t)(ok[k] ? ik : 0) * na;
-                d[k][0] = d[k][1] = d[k][2] = 0.0;
-            }
-            for (int b0 = 0; b0 < na; b0 += 64) {
-                float gv[4][2];
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int bb = b0 + 32 * u + lane;
-                        gv[k][u] = (ok[k] && bb < na) ? __ldcg(&g[k][bb]) : 0.f;
-                    }
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int bb = min(b0 + 32 * u + lane, na - 1);
-                    const double w0 = X.W[bb], w1 = X.W[na + bb], w2 = X.W[2 * na + bb];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        d[k][0] = fma((double)gv[k][u], w0, d[k][0]);
-                        d[k][1] = fma((double)gv[k][u], w1, d[k][1]);
-                        d[k][2] = fma((double)gv[k][u], w2, d[k][2]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const double e0 = warp_sum(d[k][0]), e1 = warp_sum(d[k][1]), e2 = warp_sum(d[k][2]);
-                if (lane == 0 && ok[k]) {
-                    const int ik = i + k * nw;
-                    qb[ik] = e0;
-                    qb[na + ik] = e1;
-                    qb[2 * na + ik] = e2;
-                }
             }
         }
     }
@@ -3770,7 +3762,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     const int i0 = min(na, rank * per), i1 = min(na, i0 + per);
     const bool solo = csize == 1;
     const int lda = cr_lda(na, csize);
-    const int parts = cr_parts(na, csize);
+    const int parts = cr_parts(nc, ns, na, csize);
     const size_t needA = (size_t)(i1 - i0) * lda * sizeof(float);
     // prefer G_A rows in shared memory; stage c9 too when both fit
     const bool c9s = CrLayout(nc, ns, na, true, parts).total + needA <= kCrMaxSmem ||
