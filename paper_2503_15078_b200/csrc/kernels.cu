@@ -3404,9 +3404,9 @@ __host__ __device__ inline int cr_parts(int nc, int ns, int na, int csize) {
     const int P = cr_parts_max(na, csize);
     if (P == 1) return 1;
     const size_t ga = (size_t)na * cr_lda(na, csize) * sizeof(float);
-    if (CrLayout(nc, ns, na, false, P).total + ga > kCrMaxSmem && CrLayout(nc, ns, na, false, 1).total + ga <= kCrMaxSmem)
-        return 1;
-    return P;
+    const size_t t1 = CrLayout(nc, ns, na, false, 1).total;   // + the partial sums of P groups:
+    const size_t qp = ((size_t)8 * 3 * na * P + 15) & ~(size_t)15;
+    return (t1 + qp + ga > kCrMaxSmem && t1 + ga <= kCrMaxSmem) ? 1 : P;
 }
 // a lone CTA holds the whole instance and its G_A fits next to the minimal layout: it gathers
 // G_A from the class Gram itself (k_active skips the global copy)
@@ -3533,13 +3533,14 @@ __device__ __forceinline__ void cr_rows_init(const CrCtx& X, int m, CrRows<kRpt>
 }
 
 // Ar = S r for this thread's rows (registers); r is read from shared memory
-template <int kRpt>
+template <int kRpt, int kSolo>
 __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int buf, double (&Ar)[kRpt],
                                          const CrRows<kRpt>& R) {
     const int na = X.na;
     double* qb = X.q + (size_t)buf * 3 * X.na;   // SoA: q0 | q1 | q2
     const unsigned bar = X.mbar + 8u * (unsigned)buf;
-    const bool solo = X.csize == 1;   // one CTA per instance: q stays local, no cluster exchange
+    constexpr bool solo = kSolo != 0;   // (X.csize == 1) one CTA per instance: q stays local, no cluster exchange
+    //   // one CTA per instance: q stays local, no cluster exchange
     if (!solo && threadIdx.x == 0 && na > 0)   // this phase expects 24 bytes per row of G_A from the peers
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(24 * na) : "memory");
     for (int i = threadIdx.x; i < na; i += blockDim.x) {
@@ -3584,15 +3585,14 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
         // from one sum), so thread i reads column i -- a warp's 32 rows are 128 contiguous bytes of row
         // b, coalesced -- and the result is bitwise that of the shared-memory path
         const int nap = (na + 31) & ~31, P = X.parts, cs = (na + P - 1) / P;
-        const bool sm_ga = X.gA_smem;
-        for (int t = threadIdx.x; t < nap * P; t += blockDim.x) {
-            const int part = t / nap, i = t - part * nap;
-            if (i >= na) continue;
-            const int b1 = min(na, (part + 1) * cs);
-            int b = part * cs;
-            double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-            if (sm_ga) {
+        if (X.gA_smem) {
+            for (int t = threadIdx.x; t < nap * P; t += blockDim.x) {
+                const int part = t / nap, i = t - part * nap;
+                if (i >= na) continue;
                 const float* g = X.gA + (size_t)i * X.lda;
+                const int b1 = min(na, (part + 1) * cs);
+                int b = part * cs;
+                double d0 = 0.0, d1 = 0.0, d2 = 0.0;
                 for (; b + 4 <= b1; b += 4) {
                     float gv[4];
 #pragma unroll
@@ -3611,31 +3611,30 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
                     d1 = fma(gd, X.W[na + b], d1);
                     d2 = fma(gd, X.W[2 * na + b], d2);
                 }
-            } else {
+                double* o = P > 1 ? X.qp + (size_t)part * 3 * na : qb;
+                o[i] = d0;
+                o[na + i] = d1;
+                o[2 * na + i] = d2;
+            }
+        } else {
+            for (int t = threadIdx.x; t < nap * P; t += blockDim.x) {
+                const int part = t / nap, i = t - part * nap;
+                if (i >= na) continue;
                 const float* g = X.GAg + i;   // column i
-                for (; b + 8 <= b1; b += 8) {
-                    float gv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) gv[u] = __ldcg(g + (size_t)(b + u) * na);
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const double gd = (double)gv[u];
-                        d0 = fma(gd, X.W[b + u], d0);
-                        d1 = fma(gd, X.W[na + b + u], d1);
-                        d2 = fma(gd, X.W[2 * na + b + u], d2);
-                    }
-                }
-                for (; b < b1; ++b) {
+                const int b1 = min(na, (part + 1) * cs);
+                double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+#pragma unroll 4
+                for (int b = part * cs; b < b1; ++b) {
                     const double gd = (double)__ldcg(g + (size_t)b * na);
                     d0 = fma(gd, X.W[b], d0);
                     d1 = fma(gd, X.W[na + b], d1);
                     d2 = fma(gd, X.W[2 * na + b], d2);
                 }
+                double* o = P > 1 ? X.qp + (size_t)part * 3 * na : qb;
+                o[i] = d0;
+                o[na + i] = d1;
+                o[2 * na + i] = d2;
             }
-            double* o = P > 1 ? X.qp + (size_t)part * 3 * na : qb;
-            o[i] = d0;
-            o[na + i] = d1;
-            o[2 * na + i] = d2;
         }
         if (P > 1) {
             __syncthreads();
@@ -3729,7 +3728,9 @@ __device__ __forceinline__ void cr_apply(CrCtx& X, int m, const CrInst& I, int b
 
 // One cluster of csize CTAs per instance (csize = 16 for a single scene, fewer when many
 // instances fill the GPU).  Launched with a runtime cluster dimension (cudaLaunchKernelEx).
-template <int kRpt>
+// kSolo: compiled separately for one CTA per instance (csize == 1) and for clusters, so that neither
+// path's registers weigh on the other's allocation
+template <int kRpt, int kSolo>
 __global__ void __launch_bounds__(kCrThreads, 1)
     k_cr(Params P, InstOff off, const DContact* __restrict__ C, CrContacts cc, Slots sl, const float* __restrict__ G,
          float* GA, const double4* __restrict__ x, ContactState cs, CrActive act) {
@@ -3760,7 +3761,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     }
     const int per = (na + csize - 1) / csize;
     const int i0 = min(na, rank * per), i1 = min(na, i0 + per);
-    const bool solo = csize == 1;
+    constexpr bool solo = kSolo != 0;   // == (csize == 1), chosen by the launcher
     const int lda = cr_lda(na, csize);
     const int parts = cr_parts(nc, ns, na, csize);
     const size_t needA = (size_t)(i1 - i0) * lda * sizeof(float);
@@ -3898,7 +3899,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     cr_stamp(2);
     if (rr > 0.0 && P.cr_iters > 0) {
         int buf = 0;
-        cr_apply<kRpt>(X, m, I, buf, Ar, R);
+        cr_apply<kRpt, kSolo>(X, m, I, buf, Ar, R);
         buf ^= 1;
         double rAr = 0.0, ApAp = 0.0, dummy = 0.0;
 #pragma unroll
@@ -3927,7 +3928,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
             if (it == P.cr_iters - 1) break;
             X.stamp = it == 3 ? 13 : -1;
             if (it == 3) cr_stamp(12);
-            cr_apply<kRpt>(X, m, I, buf, Ar, R);
+            cr_apply<kRpt, kSolo>(X, m, I, buf, Ar, R);
             buf ^= 1;
             if (it == 3) cr_stamp(16);
             double s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -4387,7 +4388,9 @@ int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, 
     static unsigned long long attr = 0;
     cudaError_t err = cudaSuccess;
     per_device_once(attr, [&] {
-        void* fns[kRptMax] = {(void*)k_cr<1>, (void*)k_cr<2>, (void*)k_cr<3>, (void*)k_cr<4>, (void*)k_cr<5>, (void*)k_cr<6>};
+        void* fns[2 * kRptMax] = {(void*)k_cr<1, 0>, (void*)k_cr<2, 0>, (void*)k_cr<3, 0>, (void*)k_cr<4, 0>,
+                                  (void*)k_cr<5, 0>, (void*)k_cr<6, 0>, (void*)k_cr<1, 1>, (void*)k_cr<2, 1>,
+                                  (void*)k_cr<3, 1>, (void*)k_cr<4, 1>, (void*)k_cr<5, 1>, (void*)k_cr<6, 1>};
         for (void* f : fns) {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             if (e != cudaSuccess) { err = e; return; }
@@ -4413,15 +4416,19 @@ int launch_cr(cudaStream_t st, const Params& P, InstOff off, const DContact* c, 
     cfg.numAttrs = 2;
     const int rpt = (3 * P.nc_max + kCrThreads - 1) / kCrThreads;
     cudaError_t e;
+#define SIM_CR_LAUNCH(R)                                                                                   \
+    (csize == 1 ? cudaLaunchKernelEx(&cfg, k_cr<R, 1>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act) \
+                : cudaLaunchKernelEx(&cfg, k_cr<R, 0>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act))
     switch (rpt) {
         case 0:
-        case 1: e = cudaLaunchKernelEx(&cfg, k_cr<1>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
-        case 2: e = cudaLaunchKernelEx(&cfg, k_cr<2>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
-        case 3: e = cudaLaunchKernelEx(&cfg, k_cr<3>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
-        case 4: e = cudaLaunchKernelEx(&cfg, k_cr<4>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
-        case 5: e = cudaLaunchKernelEx(&cfg, k_cr<5>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
-        default: e = cudaLaunchKernelEx(&cfg, k_cr<6>, P, off, c, cc, sl, G, const_cast<float*>(GA), x, cs, act); break;
+        case 1: e = SIM_CR_LAUNCH(1); break;
+        case 2: e = SIM_CR_LAUNCH(2); break;
+        case 3: e = SIM_CR_LAUNCH(3); break;
+        case 4: e = SIM_CR_LAUNCH(4); break;
+        case 5: e = SIM_CR_LAUNCH(5); break;
+        default: e = SIM_CR_LAUNCH(6); break;
     }
+#undef SIM_CR_LAUNCH
     return (int)e;
 }
 
