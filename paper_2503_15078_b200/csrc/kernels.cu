@@ -3079,6 +3079,38 @@ void launch_scatter(cudaStream_t st, const Params& P, int max_rows, InstOff off,
 // 32x32 tiles of slot pairs, depth staged in chunks of 32 levels.
 // ----------------------------------------------------------------------------
 
+// four LCA walks advanced together (their dependent ptop / parent loads overlap instead of running
+// one after the other); each walk is lca_depth's
+__device__ void lca_depth4(const int (&a_)[4], const int (&b_)[4], const bool (&on)[4], int (&out)[4],
+                           const int32_t* parent, const int32_t* ptop, const int32_t* depth) {
+    int i[4], b[4];
+    bool live[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int lo = min(a_[q], b_[q]), hi = max(a_[q], b_[q]);
+        i[q] = lo;
+        b[q] = hi;
+        live[q] = on[q];
+        out[q] = -1;
+    }
+    while (live[0] || live[1] || live[2] || live[3]) {
+        int top[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) top[q] = live[q] ? __ldg(&ptop[i[q]]) : 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!live[q]) continue;
+            if (top[q] >= b[q]) {
+                out[q] = __ldg(&depth[i[q] > b[q] ? i[q] : b[q]]);
+                live[q] = false;
+            } else {
+                i[q] = __ldg(&parent[top[q]]);
+                if (i[q] < 0) live[q] = false;
+            }
+        }
+    }
+}
+
 __device__ int lca_depth(int a, int b, const int32_t* parent, const int32_t* ptop, const int32_t* depth) {
     // a <= b in postorder: lca = first ancestor run of a whose top >= b, at row max(i, b)
     if (a > b) { int t = a; a = b; b = t; }
@@ -3127,10 +3159,19 @@ __global__ void __launch_bounds__(256) k_delassus(InstOff off, const int32_t* __
     const int s = bs * 32 + ls;
     int dl[4];
     int maxd = -1;
-    for (int q = 0; q < 4; ++q) {
-        const int t = bt * 32 + lt0 + 8 * q;
-        dl[q] = (s < ns && t < ns) ? lca_depth(slot_vtx[s], slot_vtx[t], parent, ptop, depth) : -1;
-        maxd = max(maxd, dl[q]);
+    {
+        int av[4], bv[4];
+        bool on[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = bt * 32 + lt0 + 8 * q;
+            on[q] = s < ns && t < ns;
+            av[q] = on[q] ? slot_vtx[s] : 0;
+            bv[q] = on[q] ? slot_vtx[t] : 0;
+        }
+        lca_depth4(av, bv, on, dl, parent, ptop, depth);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) maxd = max(maxd, dl[q]);
     }
     atomicMax(&smax, maxd);
     __syncthreads();
