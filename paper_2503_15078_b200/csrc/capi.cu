@@ -710,7 +710,11 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     simhost::trim_dropped(H->K);   // kept skyline (drop tolerance, reading A25)
     H->nnz_kept = 0;
     for (float q : H->K.Krow) H->nnz_kept += q != 0.f;
-    simhost::build_worklists(H->K, H->wl, 1024);
+    {   // pass-1 items: <= 32 rows x p1cols columns (SIM_P1_ITEM_COLS overrides, multiple of 32)
+        int p1cols = 512;   // 1024: 9 % slower pass 1 on cfg3 (the largest items set the tail), 256 / 128 slower too
+        if (const char* e = getenv("SIM_P1_ITEM_COLS")) p1cols = std::max(32, atoi(e) / 32 * 32);
+        simhost::build_worklists(H->K, H->wl, p1cols);
+    }
     simhost::build_tiles(H->K, H->wl, H->T1h, H->T2h);
     if (H->S > 1) {
         H->bparts = simhost::build_batched(H->K, H->wl, 64, H->bu1, H->T1ph, H->bu2, H->bblocks1);
