@@ -1357,8 +1357,14 @@ __device__ __forceinline__ double warp_sum(double v) {
 // 32 vector entries) into shared memory with cp.async (4-byte, zero-fill for
 // entries outside the skyline), kStages tiles in flight per warp.
 constexpr int kStages = 3;       // pass-1 tiles in flight per warp
-constexpr int kStages2 = 3;      // pass-2 tiles in flight per warp
-constexpr int kWarps2 = 6;       // pass-2 warps per CTA
+#ifndef SIM_P2_STAGES
+#define SIM_P2_STAGES 3
+#endif
+#ifndef SIM_P2_WARPS
+#define SIM_P2_WARPS 6
+#endif
+constexpr int kStages2 = SIM_P2_STAGES;   // pass-2 tiles in flight per warp
+constexpr int kWarps2 = SIM_P2_WARPS;     // pass-2 warps per CTA
 
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
