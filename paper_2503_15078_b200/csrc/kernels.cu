@@ -3806,6 +3806,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
     } else {
         na = act.na[inst];
     }
+    cr_stamp(22);   // active list built
     const int per = (na + csize - 1) / csize;
     const int i0 = min(na, rank * per), i1 = min(na, i0 + per);
     constexpr bool solo = kSolo != 0;   // == (csize == 1), chosen by the launcher
@@ -3893,6 +3894,7 @@ __global__ void __launch_bounds__(kCrThreads, 1)
         }
         __syncthreads();   // visible to this CTA's matvec (L2 loads)
     }
+    cr_stamp(23);   // G_A copies issued
     double z[kRpt], p[kRpt], Ap[kRpt], Ar[kRpt];
 #pragma unroll
     for (int k = 0; k < kRpt; ++k) {
@@ -3902,8 +3904,11 @@ __global__ void __launch_bounds__(kCrThreads, 1)
             const int c = j / 3;
             const double th = th_g[j];
             double rho = rho_g[j];
+            // v0 and s0 loaded together, then c1: two dependent loads instead of three
             const int v0 = __ldg(&cc.v0[cb + c]);
-            const bool viaSlot = v0 >= 0 && __ldg(&cc.c1[__ldg(&cc.s0[cb + c])]) == cb + c;
+            const int s0i = __ldg(&cc.s0[cb + c]);
+            const int c1v = __ldg(&cc.c1[s0i >= 0 ? s0i : 0]);
+            const bool viaSlot = v0 >= 0 && s0i >= 0 && c1v == cb + c;
             if (!viaSlot) {   // rho of contacts the chain dot did not cover
                 const int kk = j - 3 * c;
                 const DContact& ct = I.C[c];
@@ -3923,7 +3928,9 @@ __global__ void __launch_bounds__(kCrThreads, 1)
             p[k] = rho;
         }
     }
+    cr_stamp(24);   // rho / vectors staged (this thread)
     cp_async_wait<0>();
+    cr_stamp(25);   // this thread's copies landed
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(X.mbar));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(X.mbar + 8u));

@@ -21,3 +21,5 @@ its = [t[3 + i] - (t[2] if i == 0 else t[3 + i - 1]) for i in range(9) if i != 3
 print("CR iterations (us):", np.round(its, 2).tolist())
 print("iteration 3: W %.2f us, matvec + exchange %.2f us, reduction + update %.2f us" % (t[13] - t[12], t[16] - t[13], t[17] - t[16]))
 print("epilogue %.2f us; active slots %d, G_A in smem %d, cluster %d" % (t[21] - t[20], (t[31] - t[0]) / 1000, int((t[30] - t[0]) / 1000) % 10, int((t[30] - t[0]) / 10000)))
+print("staging: active list %.2f, G_A copies issued %.2f, rho/vectors %.2f, copies landed %.2f, cluster sync %.2f us"
+      % (t[22] - t[0], t[23] - t[22], t[24] - t[23], t[25] - t[24], t[1] - t[25]))
