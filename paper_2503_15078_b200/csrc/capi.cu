@@ -718,7 +718,9 @@ extern "C" int sim_build_sparse_inverse(sim_handle* H, double drop_tol) {
     simhost::build_tiles(H->K, H->wl, H->T1h, H->T2h);
     if (H->S > 1) {
         H->bparts = simhost::build_batched(H->K, H->wl, 64, H->bu1, H->T1ph, H->bu2, H->bblocks1);
-        simhost::build_plane_units(H->K, 48, H->pu);
+        int ut = 96;   // tiles per plane unit (SIM_PL_UNIT_TILES overrides; 48 / 64 / 128 / 192: pass 1 7 / 2 / 3 / 8 % slower)
+        if (const char* e = getenv("SIM_PL_UNIT_TILES")) ut = std::max(4, atoi(e));
+        simhost::build_plane_units(H->K, ut, H->pu);
     }
     lap(4);
     H->n_f = nf;
