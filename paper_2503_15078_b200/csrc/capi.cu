@@ -1430,7 +1430,9 @@ static int commit_host(sim_handle* H) {
         auto split = [&](std::vector<simhost::BUnit>& units, bool cover_list, DBuf<double>& part,
                          DBuf<int>& cnt) -> cudaError_t {
             const int nch = (S + 127) / 128, nu = (int)units.size();
-            const int want = nu ? std::max(1, (2 * 148 + nu * nch - 1) / (nu * nch)) : 1;
+            int per_sm = 2;   // target CTAs in flight per SM (SIM_TS_CTAS_PER_SM overrides)
+            if (const char* e = getenv("SIM_TS_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));
+            const int want = nu ? std::max(1, (per_sm * 148 + nu * nch - 1) / (nu * nch)) : 1;
             std::vector<simhost::BUnit> su;
             int nslot = 0;
             for (int b = 0; b < nu; ++b) {
