@@ -2086,8 +2086,26 @@ __global__ void __launch_bounds__(kPlThreads + 64, 1)
     const uint32_t sm_a = (unsigned)__cvta_generic_to_shared(sm);
     const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
     const bool mma_warp = w == kPlWarps, kload_warp = w == kPlWarps + 1;
-    const BUnit U = units[blockIdx.x];
-    const int chunk = blockIdx.y;
+#ifndef SIM_PL_CGROUP
+#define SIM_PL_CGROUP 1
+#endif
+    // pass 1 launch order: groups of SIM_PL_CGROUP instance chunks run unit by unit (the chunks of a
+    // group share each K tile in L2; 1 = all units of chunk 0, then chunk 1, ...)
+    int unit = blockIdx.x, chunk = blockIdx.y;
+    if (PASS == 1 && SIM_PL_CGROUP > 1) {
+        const int G = SIM_PL_CGROUP, nu = gridDim.x, nc = gridDim.y;
+        const int b = blockIdx.y * nu + blockIdx.x, full = (nc / G) * G * nu;
+        if (b < full) {
+            const int r = b % (G * nu);
+            unit = r / G;
+            chunk = (b / (G * nu)) * G + r % G;
+        } else {
+            const int g2 = nc - (nc / G) * G, r = b - full;
+            unit = r / g2;
+            chunk = (nc / G) * G + r % g2;
+        }
+    }
+    const BUnit U = units[unit];
     const int i0 = chunk * kPlInst;
     const size_t PS = (size_t)n_f * Sp;            // plane stride
     const unsigned long long pol = l2_evict_first();
