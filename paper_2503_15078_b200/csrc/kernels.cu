@@ -850,7 +850,10 @@ template <int MODEL>
 #ifndef SIM_LOCAL2_MINB
 #define SIM_LOCAL2_MINB 5
 #endif
-__global__ void __launch_bounds__(128, MODEL == 0 ? SIM_LOCAL2_MINB : 6) k_local2(Params P, const int4* __restrict__ tet,
+#ifndef SIM_LOCAL2_THREADS
+#define SIM_LOCAL2_THREADS 32   // one warp per CTA, 20 CTAs per SM (64 / 128 / 256: 0.7 / 2.1 / 7 % slower)
+#endif
+__global__ void __launch_bounds__(SIM_LOCAL2_THREADS, MODEL == 0 ? SIM_LOCAL2_MINB * 128 / SIM_LOCAL2_THREADS : 6 * 128 / SIM_LOCAL2_THREADS) k_local2(Params P, const int4* __restrict__ tet,
                                                                      const float* __restrict__ Bm,
                                                                      const float* __restrict__ hw2,
                                                                      const double4* __restrict__ x, float* __restrict__ fc) {
@@ -971,13 +974,13 @@ __global__ void __launch_bounds__(128, MODEL == 0 ? SIM_LOCAL2_MINB : 6) k_local
 void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float* Bm, const float* hw2,
                   const double4* x, float* fc, float* Pdbg, float* du, int admm_first) {
     if (P.S > 1 && (P.S & 1) == 0 && !du && !Pdbg && P.pair_local) {   // packed-FP32 pairs of instances
-        const unsigned g2 = (unsigned)((P.n_t * (size_t)(P.S / 2) + 127) / 128);
+        const unsigned g2 = (unsigned)((P.n_t * (size_t)(P.S / 2) + SIM_LOCAL2_THREADS - 1) / SIM_LOCAL2_THREADS);
         if (P.model == 1)
-            launch_pdl(k_local2<1>, dim3(g2), dim3(128), 0, st, P, tet, Bm, hw2, x, fc);
+            launch_pdl(k_local2<1>, dim3(g2), dim3(SIM_LOCAL2_THREADS), 0, st, P, tet, Bm, hw2, x, fc);
         else if (P.model == 2)
-            launch_pdl(k_local2<2>, dim3(g2), dim3(128), 0, st, P, tet, Bm, hw2, x, fc);
+            launch_pdl(k_local2<2>, dim3(g2), dim3(SIM_LOCAL2_THREADS), 0, st, P, tet, Bm, hw2, x, fc);
         else
-            launch_pdl(k_local2<0>, dim3(g2), dim3(128), 0, st, P, tet, Bm, hw2, x, fc);
+            launch_pdl(k_local2<0>, dim3(g2), dim3(SIM_LOCAL2_THREADS), 0, st, P, tet, Bm, hw2, x, fc);
         return;
     }
     const unsigned g = (unsigned)((P.n_t * (size_t)P.S + 127) / 128);
