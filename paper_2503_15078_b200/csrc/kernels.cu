@@ -564,7 +564,10 @@ __device__ __forceinline__ void svd_project(const float F[3][3], float k, float 
 }
 
 template <int MODEL>
-__global__ void __launch_bounds__(128, MODEL == 0 ? 6 : 8) k_local(Params P, const int4* __restrict__ tet, const float* __restrict__ Bm,
+#ifndef SIM_LOCAL_THREADS
+#define SIM_LOCAL_THREADS 128
+#endif
+__global__ void __launch_bounds__(SIM_LOCAL_THREADS, (MODEL == 0 ? 6 : 8) * 128 / SIM_LOCAL_THREADS) k_local(Params P, const int4* __restrict__ tet, const float* __restrict__ Bm,
                                                const float* __restrict__ hw2, const double4* __restrict__ x,
                                                float* __restrict__ fc, float* __restrict__ Pdbg,
                                                float* __restrict__ du, int admm_first) {
@@ -983,13 +986,13 @@ void launch_local(cudaStream_t st, const Params& P, const int4* tet, const float
             launch_pdl(k_local2<0>, dim3(g2), dim3(SIM_LOCAL2_THREADS), 0, st, P, tet, Bm, hw2, x, fc);
         return;
     }
-    const unsigned g = (unsigned)((P.n_t * (size_t)P.S + 127) / 128);
+    const unsigned g = (unsigned)((P.n_t * (size_t)P.S + SIM_LOCAL_THREADS - 1) / SIM_LOCAL_THREADS);
     if (P.model == 1)
-        launch_pdl(k_local<1>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
+        launch_pdl(k_local<1>, dim3(g), dim3(SIM_LOCAL_THREADS), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
     else if (P.model == 2)
-        launch_pdl(k_local<2>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
+        launch_pdl(k_local<2>, dim3(g), dim3(SIM_LOCAL_THREADS), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
     else
-        launch_pdl(k_local<0>, dim3(g), dim3(128), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
+        launch_pdl(k_local<0>, dim3(g), dim3(SIM_LOCAL_THREADS), 0, st, P, tet, Bm, hw2, x, fc, Pdbg, du, admm_first);
 }
 
 // ----------------------------------------------------------------------------
