@@ -400,8 +400,10 @@ def test_cfg5_full_size_fp32_kpasses_penetrating_frames(simmod):
     within the plain 1e-5 bbox bound of the oracle, classification identical outside the A21
     band.  (The tensor-core K-apply -- 3xTF32 products, fp32 TMEM accumulation, 2.6e-6 relative,
     inside the north star's 1e-5 SpMV bound -- seeds these frames 15x more than fp32 rounding and
-    their non-smooth frame map amplifies it past 1e-5 bbox on 4 of the 32 deepest:
-    profiles/r02_cfg5_parity_scan_modes.txt.)"""
+    their non-smooth frame map amplifies it past 1e-5 bbox on some of the deepest; deeper in the
+    distribution a few frames are ill-conditioned even for fp32 (the oracle itself moves by
+    several tolerances under fp32 input rounding): profiles/r02s3_cfg5_parity_scan_wide.txt,
+    DESIGN.md §3.)"""
     sc = scenes.make_scene("cfg3")
     S = 1024
     s, v0s, deltas = _cfg5_batch(simmod, sc, S)
